@@ -1,0 +1,73 @@
+"""One synchronous data-parallel training step over N simulated workers
+(PAPER.md:89-97 steps 3-6), run sequentially in one process.
+
+  step 3: every worker r runs fprop + bprop on its mini-batch m_r
+  step 4: gradients aggregated and averaged (÷N, ÷alpha -- reading Q6)
+  step 5: optimizer update of the global weights (Eqs. 1-2 or Adam)
+  step 6: the updated weights are what every worker uses next step
+          (mixed mode: the fp16 copy of the fp32 master, R1)
+
+The global batch is split contiguously: worker r gets rows
+[r*B/N, (r+1)*B/N).  The learning rate is passed in (``schedule``
+computes it); the oracle does not decide N-dependence itself.
+"""
+from __future__ import annotations
+
+from typing import Dict, Optional
+
+import numpy as np
+
+from . import lstm, optim
+from .binary16 import count_nonfinite, r16
+
+
+def working_weights(master: np.ndarray, mode: str) -> np.ndarray:
+    """R1: the weights used by fprop/bprop (fp16 copy of the master in mixed mode)."""
+    return r16(master) if mode == "mixed" else np.asarray(master, np.float64)
+
+
+def worker_grads(cfg, wflat, x, targets, alpha, mode):
+    """Steps 3 for one worker: returns (L_r scaled, flat gradient, y)."""
+    P = lstm.unpack(cfg, wflat)
+    L, y, cache = lstm.forward(cfg, P, x, targets, alpha, mode)
+    G = lstm.backward(cfg, P, cache, alpha, mode)
+    return L, lstm.pack(cfg, G), y
+
+
+def train_step(cfg, master, state: Dict[str, np.ndarray], x_global, t_global, N: int,
+               alpha: float, lam: float, mode: str, optimizer: str = "sgdm",
+               momentum: float = 0.9, adam_k: int = 1,
+               grads_override: Optional[list] = None):
+    """Returns a dict with loss (unscaled mean over workers), per-worker
+    gradients (carrying alpha), the averaged gradient, new master/state,
+    the fp16 working copy and the non-finite count."""
+    B = x_global.shape[0]
+    assert B % N == 0
+    b = B // N
+    w = working_weights(master, mode)
+    losses, grads = [], []
+    for r in range(N):
+        sl = slice(r * b, (r + 1) * b)
+        L, g, _ = worker_grads(cfg, w, x_global[sl], t_global[sl], alpha, mode)
+        losses.append(L)
+        grads.append(g)
+    if grads_override is not None:
+        grads = grads_override
+    nonfinite = sum(count_nonfinite(g) for g in grads)
+    avg = optim.average(grads, N, alpha)
+    if optimizer == "sgdm":
+        W, H = optim.sgdm(master, state["H"], avg, lam, momentum)
+        new_state = {"H": H}
+    else:
+        W, m1, v = optim.adam(master, state["m1"], state["v"], avg, lam, adam_k)
+        new_state = {"m1": m1, "v": v}
+    return {
+        "loss": float(np.sum(losses) / (N * alpha)),
+        "losses_scaled": losses,
+        "grads": grads,
+        "avg": avg,
+        "master": W,
+        "state": new_state,
+        "w16": r16(W),
+        "nonfinite": nonfinite,
+    }

@@ -1,0 +1,327 @@
+"""Pins for oracle.lstm and oracle.step
+(PAPER.md:89-97): finite differences, torch.nn.LSTM(float64) as an
+independent library special case, hand evaluation, closed-form counts,
+alpha-linearity and the data-parallel averaging identity."""
+import math
+
+import numpy as np
+import pytest
+import torch
+
+import synth
+from oracle import lstm, optim, step
+from oracle.binary16 import r16
+
+TINY = {
+    # per-step linear head (C1 / C4 flavour)
+    "lin": synth.ModelConfig("t-lin", n_layers=2, input_dim=3, hidden=4, seq=5, batch=2),
+    # per-step FC(ReLU) + linear (C2 flavour, Fig. 2)
+    "fc": synth.ModelConfig("t-fc", n_layers=2, input_dim=3, hidden=4, seq=5, batch=2, fc_hidden=3),
+    # embedding + last-step head (C3 flavour)
+    "emb": synth.ModelConfig("t-emb", n_layers=2, input_dim=0, hidden=4, seq=5, batch=3,
+                             head_last_step=True, vocab=7, embed_dim=3),
+}
+
+
+def _inputs(cfg, B, seed):
+    rng = np.random.default_rng(seed)
+    if cfg.vocab:
+        x = rng.integers(0, cfg.vocab, (B, cfg.seq)).astype(np.int32)
+        t = np.where(rng.random(B) < 0.5, 1, -1).astype(np.int8)
+    else:
+        x = rng.standard_normal((B, cfg.seq, cfg.input_dim))
+        t = np.where(rng.random((B, cfg.seq)) < 0.5, 1, -1).astype(np.int8)
+    return x, t
+
+
+def _params(cfg, seed, scale=0.6):
+    rng = np.random.default_rng(seed)
+    return rng.uniform(-scale, scale, lstm.count(cfg))
+
+
+# ---------------------------------------------------------------- counts
+
+def test_param_counts_golden(golden):
+    for name, expected in golden("param_counts.txt"):
+        cfg = synth.CONFIGS[name]
+        assert lstm.count(cfg) == int(expected)
+        assert synth.n_params(cfg) == int(expected)
+
+
+def test_param_counts_table1():
+    # SPEC.md:156-158 / PAPER.md Table 1 (:228-232): first layer 168,000;
+    # 29 stacked layers ~ 9.2e6 (within 1%), 58 layers ~ 18.2e6 (within 2%)
+    c1 = synth.ModelConfig("x", n_layers=1, input_dim=9, hidden=200, seq=1, batch=1)
+    n1 = lstm.count(c1) - 201     # minus the linear head (200 + 1)
+    assert n1 == 168000
+    for L, ref, tol in ((29, 9.2e6, 0.01), (58, 18.2e6, 0.02)):
+        c = synth.ModelConfig("x", n_layers=L, input_dim=9, hidden=200, seq=1, batch=1)
+        assert abs(lstm.count(c) - 201 - ref) / ref < tol
+
+
+# ---------------------------------------------------------------- forward
+
+def test_zero_weights_zero_output():
+    # all-zero weights and biases -> outputs all 0
+    for cfg in TINY.values():
+        x, t = _inputs(cfg, cfg.batch, 0)
+        P = lstm.unpack(cfg, np.zeros(lstm.count(cfg)))
+        L, y, _ = lstm.forward(cfg, P, x, t, 1.0, "fp64")
+        assert np.all(y == 0.0) and L == pytest.approx(1.0)   # hinge at y = 0 is 1
+
+
+def test_single_step_hand_evaluated():
+    # T = 1, h = 1, hand-set weights
+    cfg = synth.ModelConfig("h1", n_layers=1, input_dim=1, hidden=1, seq=1, batch=1)
+    Wi, Wf, Wg, Wo = 0.5, -0.3, 0.8, 0.2
+    bi, bf, bg, bo_ = 0.1, 1.0, -0.2, 0.05
+    wo, bo = 1.5, -0.25
+    flat = np.array([Wi, Wf, Wg, Wo, 0, 0, 0, 0, bi, bf, bg, bo_, wo, bo], dtype=np.float64)
+    x = np.array([[[0.7]]])
+    sig = lambda v: 1.0 / (1.0 + math.exp(-v))
+    i, f, g, o = sig(Wi * 0.7 + bi), sig(Wf * 0.7 + bf), math.tanh(Wg * 0.7 + bg), sig(Wo * 0.7 + bo_)
+    c = f * 0.0 + i * g
+    hh = o * math.tanh(c)
+    y_ref = hh * wo + bo
+    L, y, _ = lstm.forward(cfg, lstm.unpack(cfg, flat), x, np.array([[1]]), 10.0, "fp64")
+    assert y[0, 0] == pytest.approx(y_ref, rel=1e-15)
+    assert L == pytest.approx(10.0 * max(0.0, 1.0 - y_ref), rel=1e-15)
+
+
+def test_hinge_examples():
+    # SPEC.md:174-176 through the real forward: zero weights, y = bo everywhere
+    cfg = synth.ModelConfig("h", n_layers=1, input_dim=2, hidden=2, seq=1, batch=1)
+    x = np.zeros((1, 1, 2))
+    for t, yv, a, expected in ((1, 1.0, 1.0, 0.0), (1, 0.0, 10.0, 10.0), (-1, 0.5, 1.0, 1.5)):
+        flat = np.zeros(lstm.count(cfg))
+        flat[-1] = yv
+        L, y, _ = lstm.forward(cfg, lstm.unpack(cfg, flat), x, np.array([[t]]), a, "fp64")
+        assert L == pytest.approx(expected, abs=1e-15)
+
+
+# ------------------------------------------------------- torch.nn.LSTM special case
+
+def _torch_reference(cfg, flat, x, t, alpha):
+    """Independent library computation: torch.nn.LSTM (gate order i,f,g,o,
+    bias_hh = 0) + head + alpha*mean hinge, autograd for the gradients."""
+    P = {k: torch.tensor(v, dtype=torch.float64) for k, v in lstm.unpack(cfg, flat).items()}
+    h = cfg.hidden
+    in0 = cfg.embed_dim if cfg.vocab else cfg.input_dim
+    net = torch.nn.LSTM(in0, h, num_layers=cfg.n_layers, batch_first=True, dtype=torch.float64)
+    leaf = {}
+    with torch.no_grad():
+        for l in range(cfg.n_layers):
+            getattr(net, f"weight_ih_l{l}").copy_(P[f"W{l}"])
+            getattr(net, f"weight_hh_l{l}").copy_(P[f"U{l}"])
+            getattr(net, f"bias_ih_l{l}").copy_(P[f"b{l}"])
+            getattr(net, f"bias_hh_l{l}").zero_()
+    for k in ("E", "F", "fb", "wo", "bo"):
+        if k in P:
+            leaf[k] = P[k].clone().requires_grad_(True)
+    if cfg.vocab:
+        inp = leaf["E"][torch.tensor(x, dtype=torch.long)]
+    else:
+        inp = torch.tensor(x, dtype=torch.float64)
+    out, _ = net(inp)                                  # [B][T][h]
+    if cfg.fc_hidden:
+        z = torch.relu(out @ leaf["F"].T + leaf["fb"])
+        y = z @ leaf["wo"] + leaf["bo"][0]             # [B][T]
+    elif cfg.head_last_step:
+        y = out[:, -1] @ leaf["wo"] + leaf["bo"][0]    # [B]
+    else:
+        y = out @ leaf["wo"] + leaf["bo"][0]
+    tt = torch.tensor(t, dtype=torch.float64)
+    L = alpha * torch.clamp(1.0 - tt * y, min=0.0).mean()
+    L.backward()
+    grads = {}
+    for l in range(cfg.n_layers):
+        grads[f"W{l}"] = getattr(net, f"weight_ih_l{l}").grad.numpy()
+        grads[f"U{l}"] = getattr(net, f"weight_hh_l{l}").grad.numpy()
+        grads[f"b{l}"] = getattr(net, f"bias_ih_l{l}").grad.numpy()
+    for k, v in leaf.items():
+        grads[k] = v.grad.numpy()
+    yy = y.detach().numpy()
+    return L.item(), (yy if cfg.head_last_step else yy.T), grads
+
+
+@pytest.mark.parametrize("kind", sorted(TINY))
+def test_matches_torch_lstm_float64(kind):
+    cfg = TINY[kind]
+    for seed in range(3):
+        flat = _params(cfg, 10 + seed)
+        x, t = _inputs(cfg, cfg.batch, 20 + seed)
+        P = lstm.unpack(cfg, flat)
+        L, y, cache = lstm.forward(cfg, P, x, t, 10.0, "fp64")
+        G = lstm.backward(cfg, P, cache, 10.0, "fp64")
+        Lt, yt, Gt = _torch_reference(cfg, flat, x, t, 10.0)
+        assert L == pytest.approx(Lt, rel=1e-12)
+        assert np.allclose(y, yt, rtol=1e-12, atol=1e-14)
+        for k, gt in Gt.items():
+            scale = max(np.max(np.abs(gt)), 1e-30)
+            assert np.max(np.abs(G[k] - gt)) <= 1e-12 * scale, k
+
+
+# ---------------------------------------------------------------- finite differences
+
+def _near_kink(cfg, cache):
+    if np.min(np.abs(cache["margin"])) < 1e-3:
+        return True
+    if cfg.fc_hidden and np.min(np.abs(cache["zpre"])) < 1e-3:
+        return True
+    return False
+
+
+@pytest.mark.parametrize("kind", sorted(TINY))
+def test_bptt_matches_central_differences(kind):
+    # fp64 central differences, relative error < 1e-6
+    cfg = TINY[kind]
+    alpha = 10.0
+    seed = 0
+    while True:
+        flat = _params(cfg, 100 + seed)
+        x, t = _inputs(cfg, cfg.batch, 200 + seed)
+        P = lstm.unpack(cfg, flat)
+        L, _, cache = lstm.forward(cfg, P, x, t, alpha, "fp64")
+        if not _near_kink(cfg, cache):
+            break
+        seed += 1
+    G = lstm.pack(cfg, lstm.backward(cfg, P, cache, alpha, "fp64"))
+    eps = 1e-5
+    fd = np.zeros_like(flat)
+    for k in range(flat.size):
+        d = np.zeros_like(flat)
+        d[k] = eps
+        Lp = lstm.forward(cfg, lstm.unpack(cfg, flat + d), x, t, alpha, "fp64")[0]
+        Lm = lstm.forward(cfg, lstm.unpack(cfg, flat - d), x, t, alpha, "fp64")[0]
+        fd[k] = (Lp - Lm) / (2 * eps)
+    # relative error < 1e-6 plus the central-difference noise
+    # floor: loss round-off (~1e-16 * L) / eps and O(eps^2) truncation
+    floor = 1e-9 * max(1.0, abs(L))
+    err = np.abs(G - fd)
+    assert np.all(err <= 1e-6 * np.abs(G) + floor), np.max(err / (np.abs(G) + floor))
+    assert np.count_nonzero(np.abs(G) > 1e3 * floor) > flat.size // 2   # the check bites
+    # the embedding rows of unused tokens get exactly zero gradient
+    if cfg.vocab:
+        E_grad = lstm.unpack(cfg, G)["E"]
+        unused = sorted(set(range(cfg.vocab)) - set(np.unique(x).tolist()))
+        assert np.all(E_grad[unused] == 0.0)
+
+
+def test_zero_margin_batch_gives_zero_gradients():
+    # all hinge terms inactive -> all-zero gradients
+    cfg = TINY["lin"]
+    flat = _params(cfg, 3)
+    P = lstm.unpack(cfg, flat)
+    P["bo"][0] = 50.0            # y >> 1 everywhere; all targets +1
+    x, _ = _inputs(cfg, cfg.batch, 4)
+    t = np.ones((cfg.batch, cfg.seq), np.int8)
+    L, _, cache = lstm.forward(cfg, P, x, t, 10.0, "fp64")
+    G = lstm.backward(cfg, P, cache, 10.0, "fp64")
+    assert L == 0.0 and all(np.all(v == 0.0) for v in G.values())
+
+
+def test_alpha_linearity():
+    # SPEC.md:185, :198; exact for a power-of-two alpha, ~ulp for alpha = 10
+    cfg = TINY["fc"]
+    flat = _params(cfg, 7)
+    x, t = _inputs(cfg, cfg.batch, 8)
+    P = lstm.unpack(cfg, flat)
+    g1 = lstm.pack(cfg, lstm.backward(cfg, P, lstm.forward(cfg, P, x, t, 1.0, "fp64")[2], 1.0, "fp64"))
+    g8 = lstm.pack(cfg, lstm.backward(cfg, P, lstm.forward(cfg, P, x, t, 8.0, "fp64")[2], 8.0, "fp64"))
+    g10 = lstm.pack(cfg, lstm.backward(cfg, P, lstm.forward(cfg, P, x, t, 10.0, "fp64")[2], 10.0, "fp64"))
+    assert np.array_equal(g8 / 8.0, g1)
+    assert np.max(np.abs(g10 / 10.0 - g1)) <= 1e-13 * np.max(np.abs(g1))
+
+
+def test_mixed_mode_rounding_points_are_fp16():
+    cfg = TINY["fc"]
+    flat = r16(_params(cfg, 9))
+    x, t = _inputs(cfg, cfg.batch, 9)
+    x = r16(x)
+    P = lstm.unpack(cfg, flat)
+    L, y, cache = lstm.forward(cfg, P, x, t, 10.0, "mixed")
+    for Lc in cache["layers"]:
+        assert np.array_equal(Lc["H"], r16(Lc["H"]))
+        assert np.array_equal(Lc["gates"], r16(Lc["gates"]))
+        assert np.array_equal(Lc["C"], Lc["C"].astype(np.float32).astype(np.float64))
+    assert np.array_equal(cache["z"], r16(cache["z"]))
+    G = lstm.backward(cfg, P, cache, 10.0, "mixed")
+    assert all(np.array_equal(v, r16(v)) for v in G.values())
+    # fp16 vs fp32 policy after 1 timestep within 2^-10 max|act|
+    Lf, yf, cf = lstm.forward(cfg, P, x, t, 10.0, "fp32")
+    h16, h32 = cache["layers"][0]["H"][0], cf["layers"][0]["H"][0]
+    assert np.max(np.abs(h16 - h32)) <= 2.0 ** -10 * max(np.max(np.abs(h32)), 1e-30)
+
+
+# ---------------------------------------------------------------- data-parallel step
+
+def test_n_workers_equal_single_worker_fp64():
+    # north_star: N-worker averaged training with batch B/N == single-worker
+    # batch B in fp64 (lambda held fixed; the schedule changes lambda with N)
+    for kind in ("lin", "fc"):
+        cfg = TINY[kind].with_(batch=8)
+        master = _params(cfg, 11, 0.4)
+        x, t = _inputs(cfg, 8, 12)
+        ref = step.train_step(cfg, master, {"H": np.zeros_like(master)}, x, t, 1, 10.0, 1e-2, "fp64")
+        for N in (2, 4, 8):
+            out = step.train_step(cfg, master, {"H": np.zeros_like(master)}, x, t, N, 10.0, 1e-2, "fp64")
+            # equal shards: mean of shard means == global mean
+            assert np.max(np.abs(out["avg"] - ref["avg"])) <= 1e-12 * np.max(np.abs(ref["avg"]))
+            assert out["loss"] == pytest.approx(ref["loss"], rel=1e-12)
+
+
+def test_n_workers_equal_single_worker_embedding():
+    cfg = TINY["emb"].with_(batch=6)
+    master = _params(cfg, 13, 0.4)
+    x, t = _inputs(cfg, 6, 14)
+    ref = step.train_step(cfg, master, {"H": np.zeros_like(master)}, x, t, 1, 10.0, 1e-2, "fp64")
+    out = step.train_step(cfg, master, {"H": np.zeros_like(master)}, x, t, 3, 10.0, 1e-2, "fp64")
+    assert np.max(np.abs(out["avg"] - ref["avg"])) <= 1e-12 * np.max(np.abs(ref["avg"]))
+
+
+def test_duplicated_shards_equal_n1():
+    # N copies of the same batch -> identical update to N = 1
+    cfg = TINY["fc"]
+    master = _params(cfg, 15, 0.4)
+    x, t = _inputs(cfg, 2, 16)
+    ref = step.train_step(cfg, master, {"H": np.zeros_like(master)}, x, t, 1, 10.0, 1e-2, "fp64")
+    xd, td = np.concatenate([x] * 4), np.concatenate([t] * 4)
+    out = step.train_step(cfg, master, {"H": np.zeros_like(master)}, xd, td, 4, 10.0, 1e-2, "fp64")
+    assert np.max(np.abs(out["avg"] - ref["avg"])) <= 1e-15 * np.max(np.abs(ref["avg"])) + 0.0
+    assert np.array_equal(out["master"], ref["master"])
+
+
+def test_scale_neutrality():
+    # alpha in {1, 10, 100} -> same post-descale update (1e-10)
+    cfg = TINY["lin"]
+    master = _params(cfg, 17, 0.4)
+    x, t = _inputs(cfg, 4, 18)
+    avgs = [step.train_step(cfg, master, {"H": np.zeros_like(master)}, x, t, 2, a, 1e-2, "fp64")["avg"]
+            for a in (1.0, 10.0, 100.0)]
+    for a in avgs[1:]:
+        assert np.max(np.abs(a - avgs[0])) <= 1e-10 * np.max(np.abs(avgs[0]))
+
+
+def test_loss_scale_reduces_fp16_underflow():
+    # with alpha = 10 strictly fewer gradient
+    # coordinates quantise to zero on the fp16 wire than with alpha = 1
+    cfg = synth.ModelConfig("u", n_layers=1, input_dim=4, hidden=8, seq=6, batch=4)
+    master = r16(_params(cfg, 19, 0.02))        # small weights -> tiny gradients
+    x, t = _inputs(cfg, 4, 20)
+    x = r16(x * 1e-3)
+    zeros = {}
+    for a in (1.0, 10.0):
+        out = step.train_step(cfg, master, {"H": np.zeros_like(master)}, x, t, 1, a, 1e-2, "mixed")
+        zeros[a] = int(np.count_nonzero(out["grads"][0] == 0.0))
+    assert zeros[10.0] < zeros[1.0]
+
+
+def test_mixed_step_invariants_c1():
+    cfg = synth.CONFIGS["C1"]
+    master = synth.init_params(cfg).astype(np.float64)
+    x, t = synth.model_batch(cfg, 8, synth.DATA_SEED)
+    out = step.train_step(cfg, master, {"H": np.zeros_like(master)}, x, t, 2, cfg.alpha, 5e-3, "mixed")
+    assert out["nonfinite"] == 0
+    assert np.array_equal(out["w16"], r16(out["master"]))
+    assert np.array_equal(out["master"], out["master"].astype(np.float32).astype(np.float64))
+    assert 0.0 < out["loss"] < 10.0

@@ -1,0 +1,122 @@
+"""Pins for oracle.schedule and oracle.optim
+(PAPER.md:94-103): closed forms, SPEC worked examples, invariants."""
+import numpy as np
+import pytest
+
+from oracle import optim, schedule
+
+
+def test_lr_golden(golden):
+    for lam0, N, n, gamma, e, expected in golden("lr_schedule.txt"):
+        got = schedule.rate_for_epoch(float(lam0), int(N), float(n), float(gamma), int(e))
+        assert got == pytest.approx(float(expected), rel=1e-15, abs=0), (lam0, N, n, gamma, e)
+
+
+def test_halving_at_n():
+    # PAPER.md:119 "equal to the number of workers at which it is halved"
+    for lam0 in (1e-4, 4e-4, 1e-3):
+        for n in (2, 8, 50, 100):
+            assert schedule.base_rate(lam0, n, n, max_eff=1e9) == pytest.approx(lam0 / 2, rel=1e-15)
+
+
+def test_clip_invariant_and_monotone():
+    # base_rate * N <= 0.1; strictly decreasing in N and epoch
+    for lam0 in (4e-4, 1e-3, 0.02, 0.05, 0.5):
+        prev = None
+        for N in range(1, 1025):
+            r = schedule.base_rate(lam0, N, 100.0)
+            assert r * N <= 0.1 * (1 + 1e-15)
+            if prev is not None:
+                assert r < prev
+            prev = r
+        rates = [schedule.rate_for_epoch(lam0, 8, 100.0, 0.8, e) for e in range(10)]
+        assert all(a > b for a, b in zip(rates, rates[1:]))
+    # gamma = 1 => constant
+    assert len({schedule.rate_for_epoch(4e-4, 4, 100.0, 1.0, e) for e in range(5)}) == 1
+
+
+def test_sgdm_golden(golden):
+    W0 = np.array([0.5])
+    W, H = W0.copy(), np.zeros(1)
+    for k, Hk, dWk in golden("sgdm_example.txt"):
+        W, H = optim.sgdm(W, H, np.ones(1), lam=0.1, m=0.9)
+        assert H[0] == pytest.approx(float(Hk), rel=1e-6)
+        assert (W - W0)[0] == pytest.approx(float(dWk), rel=1e-6)
+
+
+def test_sgdm_special_cases():
+    rng = np.random.default_rng(0)
+    W = rng.standard_normal(100).astype(np.float32).astype(np.float64)
+    H = rng.standard_normal(100).astype(np.float32).astype(np.float64)
+    g = rng.standard_normal(100)
+    # m = 0 -> plain SGD
+    W1, H1 = optim.sgdm(W, H, g, lam=0.01, m=0.0)
+    assert np.array_equal(H1, optim.r32(-0.01 * g))
+    assert np.array_equal(W1, optim.r32(W + H1))
+    # lambda = 0 -> W unchanged apart from the momentum term, H = m H
+    W2, H2 = optim.sgdm(W, np.zeros(100), g, lam=0.0, m=0.9)
+    assert np.array_equal(W2, W) and np.all(H2 == 0)
+
+
+def test_average_divides_by_N_alpha():
+    gs = [np.full(4, 10.0), np.full(4, 30.0)]
+    assert np.allclose(optim.average(gs, 2, 10.0), 2.0)
+    # SPEC.md:193 descale example g = [10, -20], alpha = 10 -> [1, -2]
+    assert np.array_equal(optim.average([np.array([10.0, -20.0])], 1, 10.0), [1.0, -2.0])
+
+
+def test_fused_f32_emulation_vs_fp64():
+    rng = np.random.default_rng(3)
+    n, N, alpha = 10000, 4, 10.0
+    gs = [rng.normal(0, 0.05, n).astype(np.float16) for _ in range(N)]
+    W = rng.uniform(-0.1, 0.1, n).astype(np.float32)
+    H = rng.normal(0, 1e-3, n).astype(np.float32)
+    lam, m = 3.7e-4, 0.9
+    inv, lam32, m32 = optim.scalars_f32(N, alpha, lam, m)
+    Wn, Hn, w16, nf = optim.fused_avg_update_f32(gs, W, H, inv, lam32, m32)
+    avg = optim.average([g.astype(np.float64) for g in gs], N, alpha)
+    Hr = 0.9 * H.astype(np.float64) - lam * avg
+    Wr = W.astype(np.float64) + Hr
+    assert nf == 0
+    assert np.max(np.abs(Hn - Hr)) <= 1e-6 * np.max(np.abs(Hr))
+    assert np.max(np.abs(Wn - Wr)) <= 1e-6 * np.max(np.abs(Wr))
+    assert np.array_equal(w16, Wn.astype(np.float16))
+
+
+def test_fused_f32_hand_example():
+    # two ranks, alpha = 10: g = (20 + 10) / 20 = 1.5; H = 0.9*0 - 0.1*1.5 = -0.15; W = 1 - 0.15
+    gs = [np.array([20.0], np.float16), np.array([10.0], np.float16)]
+    inv, lam, m = optim.scalars_f32(2, 10.0, 0.1, 0.9)
+    Wn, Hn, w16, nf = optim.fused_avg_update_f32(gs, np.array([1.0], np.float32), np.zeros(1, np.float32), inv, lam, m)
+    assert Hn[0] == np.float32(-0.15) or abs(Hn[0] + 0.15) < 1e-7
+    assert abs(Wn[0] - 0.85) < 1e-7
+    # a non-finite contribution is counted
+    gs.append(np.array([np.inf], np.float16))
+    assert optim.fused_avg_update_f32(gs, Wn, Hn, inv, lam, m)[3] == 1
+
+
+def test_adam_first_step_closed_form():
+    # with bias correction, step 1 has mhat = g, vhat = g^2:
+    # W1 = W0 - lambda * g / (|g| + eps)   (Kingma & Ba, reading Q15)
+    rng = np.random.default_rng(5)
+    g = rng.standard_normal(50)
+    W0 = np.zeros(50)
+    W1, m1, v = optim.adam(W0, np.zeros(50), np.zeros(50), g, lam=1e-3, k=1)
+    ref = -1e-3 * g / (np.abs(g) + 1e-8)
+    assert np.allclose(W1, ref, rtol=1e-6, atol=0)
+
+
+def test_adam_f32_emulation_vs_fp64():
+    rng = np.random.default_rng(6)
+    n, N, alpha = 5000, 2, 10.0
+    gs = [rng.normal(0, 0.05, n).astype(np.float16) for _ in range(N)]
+    W = rng.uniform(-0.1, 0.1, n).astype(np.float32)
+    m1 = rng.normal(0, 1e-3, n).astype(np.float32)
+    v = np.abs(rng.normal(0, 1e-4, n)).astype(np.float32)
+    lam, k = 1e-3, 3
+    c = optim.adam_consts_f32(lam, k)
+    Wn, m1n, vn, _, _ = optim.fused_avg_adam_f32(gs, W, m1, v, np.float32(1.0 / (N * alpha)), c)
+    avg = optim.average([g.astype(np.float64) for g in gs], N, alpha)
+    Wr, m1r, vr = optim.adam(W.astype(np.float64), m1.astype(np.float64), v.astype(np.float64), avg, lam, k)
+    assert np.max(np.abs(Wn - Wr)) <= 1e-6 * np.max(np.abs(Wr))
+    assert np.max(np.abs(m1n - m1r)) <= 1e-6 * np.max(np.abs(m1r))
