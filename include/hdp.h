@@ -1,0 +1,216 @@
+/*
+ * hdp.h -- C-ABI of libhdp.so: the synchronous data-parallel mixed-precision
+ * LSTM training step of arXiv 1912.00286, B200 (sm_100a) native.
+ *
+ * The calls follow the paper's problem statement, PAPER.md:89-97:
+ *   1. initialise the parameters randomly           -> caller; hdp_load_params
+ *   2. broadcast them to every worker                -> hdp_load_params (ncclBroadcast)
+ *   3. fprop + bprop on each worker's mini-batch     -> hdp_lstm_forward / hdp_lstm_backward
+ *   4. aggregate the gradients and average them      -> hdp_grad_average_update
+ *   5. update optimizer state and global weights     -> hdp_grad_average_update (fused, K11)
+ *   6. broadcast the updated parameters              -> hdp_grad_average_update (allgather)
+ * with the learning-rate schedule of PAPER.md:106-121 (hdp_set_lr_schedule)
+ * and the loss scale alpha of PAPER.md:177-180 (hdp_set_loss_scale).
+ *
+ * Conventions
+ *  - Every function returns 0 (HDP_OK) or a negative HDP_ERR_* code; nothing
+ *    aborts or throws across the ABI.  hdp_last_error() returns a
+ *    thread-local message for the most recent failure.
+ *  - Argument and shape errors are detected on the host before anything is
+ *    enqueued (HDP_ERR_ARG; no state changed).
+ *  - `stream` arguments are cudaStream_t handles passed as void*; all compute
+ *    calls are asynchronous and stream-ordered on it.
+ *  - Device memory is owned by the caller: hdp_configure reports the arena
+ *    size, the caller allocates it (256-byte aligned) and hdp_bind()s it.
+ *    The library owns only its NCCL communicator, two internal streams,
+ *    events and captured CUDA graphs (freed by hdp_destroy), plus transient
+ *    staging buffers inside hdp_load_params / hdp_gather_master.
+ *  - One context per process = one rank = one GPU.  A context is not
+ *    thread-safe.  Every rank must make the same sequence of calls with the
+ *    same B, T and epoch (NCCL's rule, and the paper's lock-step, :104).
+ */
+#ifndef HDP_H_
+#define HDP_H_
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HDP_UID_BYTES 128
+
+enum {
+  HDP_OK = 0,
+  HDP_ERR_ARG = -1,         /* invalid argument / shape; nothing was enqueued        */
+  HDP_ERR_CUDA = -2,        /* CUDA runtime / driver failure                          */
+  HDP_ERR_NCCL = -3,        /* NCCL failure (incl. asynchronous communicator errors) */
+  HDP_ERR_NONFINITE = -4,   /* Inf/NaN gradients seen (PAPER.md:134 overflow hazard) */
+  HDP_ERR_STATE = -5,       /* call-order violation, or context poisoned             */
+  HDP_ERR_UNSUPPORTED = -6
+};
+
+/* Precision modes: math / synchronisation / update.    */
+enum { HDP_MATH_FP32 = 0,     /* the paper's baseline: everything fp32 (:147)      */
+       HDP_MATH_MIXED16 = 1   /* fp16 math + fp16 wire + fp32 master/update         */
+};
+/* Wire format of the gradient exchange.              */
+enum { HDP_WIRE_FP16_A2A = 0,     /* fp16 all-to-all, fp32 rank-ordered sum in K11 (default) */
+       HDP_WIRE_FP16_NCCLSUM = 1, /* ncclReduceScatter(ncclHalf, sum): NCCL-native fp16 sum  */
+       HDP_WIRE_FP32 = 2          /* fp32 gradients, ncclReduceScatter(ncclFloat, sum)       */
+};
+enum { HDP_OPT_SGDM = 0,  /* Eqs. 1-2                              */
+       HDP_OPT_ADAM = 1   /* "any optimizer" (:98), Kingma & Ba with bias correction  */
+};
+
+typedef struct hdp_ctx hdp_ctx;
+
+/* Model description (Fig. 2, :64-80; readings Q1-Q4, Q21-Q24).
+ * n_layers == 0 describes a flat parameter vector of `flat_params`
+ * elements with no forward/backward (the C5 update sweep).            */
+typedef struct {
+  int n_layers;        /* stacked LSTM layers L >= 0                              */
+  int input_dim;       /* I of layer 0 (dense input); ignored if vocab > 0       */
+  int hidden;          /* h                                                       */
+  int fc_hidden;       /* per-step FC(ReLU) width before the 1-unit output; 0 = none */
+  int head_last_step;  /* 1: one output per sequence at t = T-1 (IMDB-style)      */
+  int vocab;           /* > 0: int32 token input through an embedding             */
+  int embed_dim;       /* embedding width when vocab > 0                          */
+  int max_batch;       /* per-rank batch upper bound                              */
+  int max_seq;         /* sequence length upper bound                             */
+  int math;            /* HDP_MATH_*                                              */
+  int wire;            /* HDP_WIRE_*                                              */
+  int optimizer;       /* HDP_OPT_*                                               */
+  int sim_workers;     /* >= 1; > 1 only when world == 1 (simulated workers)      */
+  long long flat_params; /* n_layers == 0 only                                    */
+} hdp_model_desc;
+
+typedef struct {
+  long long n_params;        /* canonical (unpadded) parameter count                */
+  long long n_params_padded; /* device layout length (padded, bucketed)             */
+  long long n_buckets;
+  long long arena_bytes;     /* device bytes the caller must allocate and bind      */
+} hdp_sizes;
+
+/* One parameter block.  Canonical host layout (hdp_load_params):
+ *   [E (vocab x embed)]?  then per layer l: W_l [4h][I_l], U_l [4h][h],
+ *   b_l [4h] with gate blocks i, f, g, o (row = gate*h + unit);
+ *   then [F [fc][h], fb [fc]]?, wo [fc or h], bo [1].                    */
+typedef struct {
+  char name[16];
+  long long canon_offset; /* offset in the canonical host vector                 */
+  long long rows, cols;   /* canonical shape (cols = 1 for vectors)              */
+  long long dev_offset;   /* offset in the device parameter vector               */
+  long long dev_rows, dev_cols; /* padded device shape                           */
+  int bucket;             /* exchange bucket (readiness order: head first)       */
+} hdp_block;
+
+/* NCCL unique id, generated on rank 0 and shipped to the others by the
+ * caller (e.g. torch.distributed.broadcast_object_list).              */
+int hdp_nccl_unique_id(unsigned char uid[HDP_UID_BYTES]);
+
+/* init(world, rank) of north_star.  world == 1 needs no uid (may be NULL).
+ * Selects `device` for the calling thread and creates the communicator.  */
+int hdp_init(int world, int rank, const unsigned char* uid, int device, hdp_ctx** out);
+int hdp_destroy(hdp_ctx* ctx);
+const char* hdp_last_error(void);
+
+/* Validate the model and compute the device layout and arena size.
+ * All ranks must pass identical descriptions.                         */
+int hdp_configure(hdp_ctx* ctx, const hdp_model_desc* desc, hdp_sizes* out);
+/* Bind the caller-owned device arena (>= arena_bytes, 256-B aligned).
+ * Zero-fills it, sets up kernels and streams.                         */
+int hdp_bind(hdp_ctx* ctx, void* arena, long long arena_bytes);
+
+int hdp_num_blocks(const hdp_ctx* ctx);
+int hdp_param_block(const hdp_ctx* ctx, int i, hdp_block* out);
+
+/* PAPER.md:91-92 steps 1-2.  `params` = canonical fp32 host vector
+ * (n_params), read on `root` only (others may pass NULL); broadcast to
+ * all ranks; fp32 master shards and optimizer state (zero) initialised;
+ * the working copy (fp16 in mixed mode) set.  Synchronous; collective.  */
+int hdp_load_params(hdp_ctx* ctx, const float* params, int root);
+/* Read back the fp32 master weights into a canonical host vector.
+ * Synchronous; collective (allgather of the shards).                  */
+int hdp_gather_master(hdp_ctx* ctx, float* params_out);
+/* Local, synchronous read-backs in the canonical layout (as fp32):
+ * the working copy used by fprop, and slot `slot`'s gradients (they carry
+ * the loss scale alpha).                              */
+int hdp_read_weights(hdp_ctx* ctx, float* out);
+int hdp_read_grads(hdp_ctx* ctx, int slot, float* out);
+
+/* set_lr_schedule of north_star, PAPER.md:106-121:
+ *   lambda_e = min(lambda0/(1 + N/n_half), max_eff_lr/N) * gamma^epoch
+ * N = world * sim_workers.  momentum m of Eq. 1; Adam b1, b2, eps.
+ * Errors: lambda0 <= 0, gamma not in (0,1], n_half <= 0 -> HDP_ERR_ARG. */
+int hdp_set_lr_schedule(hdp_ctx* ctx, double lambda0, double gamma, double n_half, double max_eff_lr,
+                        double momentum, double adam_b1, double adam_b2, double adam_eps);
+/* The scheduled rate (fp64) for `epoch`; negative if not configured.  */
+double hdp_lr(const hdp_ctx* ctx, int epoch);
+/* Loss scale alpha > 0 (PAPER.md:177; default 10, :127).              */
+int hdp_set_loss_scale(hdp_ctx* ctx, float alpha);
+
+/* fprop of slot `slot`'s mini-batch and the scaled hinge
+ * loss Eq. 6 (:179).
+ *   x       : dense input [B][T][input_dim], fp16 (mixed) or fp32 (FP32
+ *             mode), or int32 tokens [B][T] when vocab > 0; host or device.
+ *   targets : int8 in {-1,+1}, [B][T] (per-step heads) or [B] (last-step).
+ *   y_out   : device fp32 [T][B] (or [B]); nullable.
+ *   loss_out: device fp32 scalar = mean hinge WITHOUT alpha; nullable.
+ * Slots 0..sim_workers-1; 1 <= B <= max_batch, 1 <= T <= max_seq.       */
+int hdp_lstm_forward(hdp_ctx* ctx, const void* x, const void* targets, int B, int T, int slot, float* y_out,
+                     float* loss_out, void* stream);
+/* bprop / BPTT of the last forward of `slot`; writes that
+ * slot's gradients (alpha-scaled; fp16 in mixed mode, one RNE of the fp32
+ * accumulation) and marks each exchange bucket ready as it completes.
+ * HDP_ERR_STATE if `slot` has no forward.                               */
+int hdp_lstm_backward(hdp_ctx* ctx, int slot, void* stream);
+/* PAPER.md:94-96 steps 4-6 for every bucket: exchange (NCCL, per
+ * `wire`), fused fp32 average / alpha removal / overflow count /
+ * SGD-m or Adam at lambda_epoch / fp16 recast (K11) on the owner shard,
+ * allgather of the updated weights.  Overlaps the still-running backward
+ * of lower layers.  If nonfinite_host != NULL the call synchronises and
+ * stores the global count of non-finite gradient values there; a
+ * non-zero count returns HDP_ERR_NONFINITE (also reported by the next
+ * call when not synchronised) and poisons the context (HDP_ERR_STATE
+ * until hdp_load_params).  HDP_ERR_STATE if a slot has no backward.      */
+int hdp_grad_average_update(hdp_ctx* ctx, int epoch, void* stream, int* nonfinite_host);
+
+/* Device pointers into the bound arena (for benches and tests). */
+void* hdp_weights_ptr(hdp_ctx* ctx);           /* working copy, device layout          */
+void* hdp_grads_ptr(hdp_ctx* ctx, int slot);   /* gradient slot, device layout        */
+void* hdp_master_ptr(hdp_ctx* ctx);            /* this rank's fp32 master shards      */
+
+/* ---------------------------------------------------------------------
+ * Kernel-level entries (stateless; used by the C5 sweep and unit tests).
+ * --------------------------------------------------------------------- */
+
+/* K11 on caller buffers: contribution r is grads + r*src_stride elements
+ * (fp16 if !grads_f32), r = 0..nsrc-1 summed in rank order; W/S1/S2 fp32
+ * master / momentum (or Adam m, v); w16 or w32 receives the new working
+ * copy (either may be NULL).  count % 8 == 0 and 16-byte aligned pointers
+ * use 128-bit accesses (any count is accepted).  nonfinite_dev (device
+ * int, nullable) is incremented by the number of Inf/NaN contributions.
+ * adam = {b1, b2, eps, step k >= 1} (ignored for SGD-m).                  */
+int hdp_fused_avg_update(const void* grads, long long src_stride, int nsrc, int grads_f32, long long count,
+                         float* W, float* S1, float* S2, void* w16, float* w32, float inv_scale, float lr,
+                         float momentum, int optimizer, const double* adam, int* nonfinite_dev, void* stream);
+
+/* Gate-contraction GEMM, C[m][n] = sum_k A(m,k) B(n,k) (+bias, ReLU),
+ * fp16 operands on the tcgen05 tensor cores, fp32 accumulate.
+ *   a_mn = 0: A stored [M][K] (row stride lda); 1: A stored [K][M].
+ *   b_mn = 0: B stored [N][K];                  1: B stored [K][N].
+ *   c_mode 0: fp32 C[m*ldc+n]; 1: fp32 C[n*ldc+m]; 2: fp16 C[m*ldc+n].
+ *   bias (fp32, nullable) indexed by n, or by m if bias_on_m.
+ *   ws: fp32 split-K workspace (nullable), ws_floats its size.
+ *   bn, splits: 0 = automatic.                                           */
+int hdp_gemm_f16(const void* A, long long lda, int a_mn, const void* B, long long ldb, int b_mn, int M, int N,
+                 int K, void* C, long long ldc, int c_mode, const float* bias, int bias_on_m, int relu,
+                 int accumulate, float* ws, long long ws_floats, int bn, int splits, void* stream);
+/* Same contract on fp32 operands with the FP32-mode SIMT kernel (c_mode 0/1). */
+int hdp_gemm_f32(const float* A, long long lda, int a_mn, const float* B, long long ldb, int b_mn, int M, int N,
+                 int K, float* C, long long ldc, int c_mode, const float* bias, int bias_on_m, int relu,
+                 int accumulate, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* HDP_H_ */

@@ -179,9 +179,9 @@ def backward(cfg, P: Dict[str, np.ndarray], cache, alpha: float, mode: str) -> D
     G["bo"] = np.array([dy.sum()])
     if cfg.fc_hidden > 0:
         z, zpre = cache["z"], cache["zpre"]
-        G["wo"] = np.einsum("tb,tbf->f", dy, z)
+        G["wo"] = dy.reshape(-1) @ z.reshape(-1, z.shape[-1])
         dz = q(dy[..., None] * P["wo"][None, None, :] * (zpre > 0.0))   # R9
-        G["F"] = np.einsum("tbf,tbh->fh", dz, Htop)
+        G["F"] = dz.reshape(-1, dz.shape[-1]).T @ Htop.reshape(-1, h)
         G["fb"] = dz.sum(axis=(0, 1))
         dH_above = dz @ P["F"]                   # [T][B][h], R11 (not rounded)
     elif cfg.head_last_step:
@@ -189,7 +189,7 @@ def backward(cfg, P: Dict[str, np.ndarray], cache, alpha: float, mode: str) -> D
         dH_above = np.zeros((T, B, h))
         dH_above[T - 1] = dy[:, None] * P["wo"][None, :]
     else:
-        G["wo"] = np.einsum("tb,tbh->h", dy, Htop)
+        G["wo"] = dy.reshape(-1) @ Htop.reshape(-1, h)
         dH_above = dy[..., None] * P["wo"][None, None, :]
     for l in reversed(range(cfg.n_layers)):
         Lc = cache["layers"][l]
@@ -215,8 +215,10 @@ def backward(cfg, P: Dict[str, np.ndarray], cache, alpha: float, mode: str) -> D
             dh_rec = dA @ U                      # R11
             dc = dc * f
         Hprev = np.concatenate([np.zeros((1, B, h)), H[:-1]], axis=0)
-        G[f"W{l}"] = np.einsum("tbr,tbi->ri", dA_all, X)
-        G[f"U{l}"] = np.einsum("tbr,tbj->rj", dA_all, Hprev)
+        # sums over (t, b) written as one matrix product each
+        dA2 = dA_all.reshape(-1, 4 * h)
+        G[f"W{l}"] = dA2.T @ X.reshape(-1, X.shape[-1])
+        G[f"U{l}"] = dA2.T @ Hprev.reshape(-1, h)
         G[f"b{l}"] = dA_all.sum(axis=(0, 1))
         if l > 0:
             dH_above = dA_all @ W                # dX of layer l -> layer l-1

@@ -1,0 +1,169 @@
+// K11: fused gradient average + global weight update (PAPER.md:94-95 steps
+// 4-5, Eqs. 1-2 :101-102; loss-scale removal :177, reading Q6).
+//
+// Per owned element, in this exact fp32 operation order (R14/R15):
+//   s  = fp32(g_0) + fp32(g_1) + ... + fp32(g_{N-1})     rank order, each add RNE
+//   g  = s * inv_scale                                  inv_scale = fp32(1/(N*alpha))
+//   SGD-m:  H = m*H - lam*g ;  W = W + H                (each op separately RNE, no FMA)
+//   Adam :  m1 = b1*m1 + (1-b1)*g ; v = b2*v + (1-b2)*g*g ;
+//           W  = W - lam * (m1*c1) / (sqrt(v*c2) + eps)
+//   w16 = RNE_fp16(W)    (or w32 = W in FP32 mode)
+//   nonfinite += number of Inf/NaN contributions
+// HBM traffic per element: N*sizeof(g) + 4+4 (W,H read) + 4+4 (W,H write) + 2 (w16).
+// 128-bit loads/stores, grid-stride over 8-element vectors.
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace hdp {
+namespace {
+
+template <typename GT>
+struct Vec8;
+template <>
+struct Vec8<__half> {
+  __device__ static void load(const __half* p, float (&o)[8], int& nf) {
+    const uint4 u = __ldcs(reinterpret_cast<const uint4*>(p));  // streamed once
+    const __half2* h = reinterpret_cast<const __half2*>(&u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __half22float2(h[i]);
+      o[2 * i] = f.x;
+      o[2 * i + 1] = f.y;
+    }
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      nf += ((w[i] & 0x7C00u) == 0x7C00u);
+      nf += ((w[i] & 0x7C000000u) == 0x7C000000u);
+    }
+  }
+};
+template <>
+struct Vec8<float> {
+  __device__ static void load(const float* p, float (&o)[8], int& nf) {
+    const float4 a = __ldcs(reinterpret_cast<const float4*>(p));
+    const float4 b = __ldcs(reinterpret_cast<const float4*>(p) + 1);
+    o[0] = a.x; o[1] = a.y; o[2] = a.z; o[3] = a.w;
+    o[4] = b.x; o[5] = b.y; o[6] = b.z; o[7] = b.w;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) nf += !isfinite(o[i]);
+  }
+};
+
+__device__ __forceinline__ float upd_sgdm(const UpdateArgs& a, float g, float& W, float& H) {
+  const float t1 = __fmul_rn(a.mom, H);
+  const float t2 = __fmul_rn(a.lam, g);
+  H = __fsub_rn(t1, t2);
+  W = __fadd_rn(W, H);
+  return W;
+}
+__device__ __forceinline__ float upd_adam(const UpdateArgs& a, float g, float& W, float& m1, float& v) {
+  m1 = __fadd_rn(__fmul_rn(a.b1, m1), __fmul_rn(a.omb1, g));
+  const float gg = __fmul_rn(g, g);
+  v = __fadd_rn(__fmul_rn(a.b2, v), __fmul_rn(a.omb2, gg));
+  const float mhat = __fmul_rn(m1, a.c1);
+  const float vhat = __fmul_rn(v, a.c2);
+  const float den = __fadd_rn(__fsqrt_rn(vhat), a.eps);
+  const float u = __fdiv_rn(mhat, den);
+  W = __fsub_rn(W, __fmul_rn(a.lam, u));
+  return W;
+}
+
+template <typename GT, int OPT>
+__global__ void __launch_bounds__(256) avg_update_kernel(UpdateArgs a) {
+  const GT* __restrict__ g = static_cast<const GT*>(a.g);
+  const long nvec = a.count >> 3;
+  int nf = 0;
+  for (long v = blockIdx.x * (long)blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
+    const long e = v << 3;
+    float s[8];
+    Vec8<GT>::load(g + e, s, nf);
+    for (int r = 1; r < a.nsrc; ++r) {
+      float t[8];
+      Vec8<GT>::load(g + (long)r * a.g_stride + e, t, nf);
+#pragma unroll
+      for (int i = 0; i < 8; ++i) s[i] = __fadd_rn(s[i], t[i]);
+    }
+    float4 W0 = *reinterpret_cast<const float4*>(a.W + e), W1 = *reinterpret_cast<const float4*>(a.W + e + 4);
+    float4 S0 = *reinterpret_cast<const float4*>(a.S1 + e), S1 = *reinterpret_cast<const float4*>(a.S1 + e + 4);
+    float w[8] = {W0.x, W0.y, W0.z, W0.w, W1.x, W1.y, W1.z, W1.w};
+    float h[8] = {S0.x, S0.y, S0.z, S0.w, S1.x, S1.y, S1.z, S1.w};
+    if (OPT == 0) {
+#pragma unroll
+      for (int i = 0; i < 8; ++i) upd_sgdm(a, __fmul_rn(s[i], a.inv_scale), w[i], h[i]);
+    } else {
+      float4 V0 = *reinterpret_cast<const float4*>(a.S2 + e), V1 = *reinterpret_cast<const float4*>(a.S2 + e + 4);
+      float vv[8] = {V0.x, V0.y, V0.z, V0.w, V1.x, V1.y, V1.z, V1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i) upd_adam(a, __fmul_rn(s[i], a.inv_scale), w[i], h[i], vv[i]);
+      *reinterpret_cast<float4*>(a.S2 + e) = make_float4(vv[0], vv[1], vv[2], vv[3]);
+      *reinterpret_cast<float4*>(a.S2 + e + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
+    }
+    *reinterpret_cast<float4*>(a.W + e) = make_float4(w[0], w[1], w[2], w[3]);
+    *reinterpret_cast<float4*>(a.W + e + 4) = make_float4(w[4], w[5], w[6], w[7]);
+    *reinterpret_cast<float4*>(a.S1 + e) = make_float4(h[0], h[1], h[2], h[3]);
+    *reinterpret_cast<float4*>(a.S1 + e + 4) = make_float4(h[4], h[5], h[6], h[7]);
+    if (a.w16) {
+      __align__(16) __half2 o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[i] = __halves2half2(__float2half_rn(w[2 * i]), __float2half_rn(w[2 * i + 1]));
+      *reinterpret_cast<uint4*>(a.w16 + e) = *reinterpret_cast<const uint4*>(o);
+    }
+    if (a.w32) {
+      *reinterpret_cast<float4*>(a.w32 + e) = make_float4(w[0], w[1], w[2], w[3]);
+      *reinterpret_cast<float4*>(a.w32 + e + 4) = make_float4(w[4], w[5], w[6], w[7]);
+    }
+  }
+  // scalar tail (count not a multiple of 8)
+  for (long e = (nvec << 3) + blockIdx.x * (long)blockDim.x + threadIdx.x; e < a.count;
+       e += (long)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int r = 0; r < a.nsrc; ++r) {
+      const float t = static_cast<float>(g[(long)r * a.g_stride + e]);
+      nf += !isfinite(t);
+      s = r == 0 ? t : __fadd_rn(s, t);
+    }
+    float w = a.W[e], h = a.S1[e];
+    if (OPT == 0) {
+      upd_sgdm(a, __fmul_rn(s, a.inv_scale), w, h);
+    } else {
+      float vv = a.S2[e];
+      upd_adam(a, __fmul_rn(s, a.inv_scale), w, h, vv);
+      a.S2[e] = vv;
+    }
+    a.W[e] = w;
+    a.S1[e] = h;
+    if (a.w16) a.w16[e] = __float2half_rn(w);
+    if (a.w32) a.w32[e] = w;
+  }
+  if (a.nonfinite) {
+    nf = __reduce_add_sync(0xffffffffu, nf);
+    if ((threadIdx.x & 31) == 0 && nf) atomicAdd(a.nonfinite, nf);
+  }
+}
+
+}  // namespace
+
+cudaError_t launch_avg_update(const UpdateArgs& a, int grad_is_f32, int optimizer, cudaStream_t s) {
+  if (a.count <= 0) return cudaSuccess;
+  long nvec = (a.count + 7) >> 3;
+  long blocks = (nvec + 255) / 256;
+  if (blocks > 148L * 8) blocks = 148L * 8;
+  if (blocks < 1) blocks = 1;
+  if (grad_is_f32) {
+    if (optimizer == 0)
+      avg_update_kernel<float, 0><<<(int)blocks, 256, 0, s>>>(a);
+    else
+      avg_update_kernel<float, 1><<<(int)blocks, 256, 0, s>>>(a);
+  } else {
+    if (optimizer == 0)
+      avg_update_kernel<__half, 0><<<(int)blocks, 256, 0, s>>>(a);
+    else
+      avg_update_kernel<__half, 1><<<(int)blocks, 256, 0, s>>>(a);
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace hdp

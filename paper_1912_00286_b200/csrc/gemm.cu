@@ -1,0 +1,500 @@
+// tcgen05 / TMEM / TMA GEMM for sm_100a, plus the fp32 SIMT GEMM of FP32 mode.
+//
+// One CTA computes a 128 x BN output tile (UMMA M=128, N=BN, K=16 steps):
+//   warp 0 lane 0 : TMA producer, STAGES-deep smem ring (SWIZZLE_128B tiles)
+//   warp 1 lane 0 : tcgen05.mma issuer, accumulator in TMEM (BN fp32 columns)
+//   warp 2        : TMEM allocation / deallocation
+//   all 4 warps   : epilogue, tcgen05.ld 32 lanes x 16 columns at a time
+// Split-K writes fp32 partials that a deterministic reduction kernel sums in
+// split order (no atomics), so results do not depend on scheduling.
+#include <cudaTypedefs.h>
+
+#include <cstdio>
+#include <mutex>
+
+#include "gemm.cuh"
+#include "ptx.cuh"
+
+namespace hdp {
+
+static thread_local char g_gemm_err[256];
+const char* gemm_last_error() { return g_gemm_err; }
+
+namespace {
+
+constexpr int BM = 128;
+constexpr int BK = 64;
+
+template <int BN>
+struct TileCfg {
+  static constexpr int A_BYTES = BM * BK * 2;
+  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int STAGE = A_BYTES + B_BYTES;
+  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 4 : 6);
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*align slack*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ float bias_at(const Epilogue& e, long i) {
+  return e.bias_f16 ? __half2float(reinterpret_cast<const __half*>(e.bias)[i]) : reinterpret_cast<const float*>(e.bias)[i];
+}
+
+__device__ __forceinline__ int f16_nonfinite(__half h) {
+  return (__half_as_ushort(h) & 0x7C00) == 0x7C00;
+}
+
+// Store 16 consecutive columns [n, n+16) of row m.
+__device__ __forceinline__ void epi_store16(const Epilogue& epi, float* ws, int M, int N, int m, int n,
+                                            float (&v)[16], int& nf) {
+  if (m >= M) return;
+  if (epi.mode == EPI_SPLITK) {
+    float* o = ws + (size_t)blockIdx.z * M * N + (size_t)m * N;
+    if (n + 16 <= N && (N & 3) == 0) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) *reinterpret_cast<float4*>(o + n + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+    } else {
+      for (int j = 0; j < 16; ++j)
+        if (n + j < N) o[n + j] = v[j];
+    }
+    return;
+  }
+#pragma unroll
+  for (int j = 0; j < 16; ++j) {
+    float b = 0.f;
+    if (epi.bias) b = epi.bias_on_m ? bias_at(epi, m) : ((n + j < N) ? bias_at(epi, n + j) : 0.f);
+    float x = v[j] + b;
+    if (epi.relu) x = fmaxf(x, 0.f);
+    v[j] = x;
+  }
+  if (epi.mode == EPI_F32) {
+    float* o = reinterpret_cast<float*>(epi.out) + (size_t)m * epi.ldo;
+    if (n + 16 <= N && (epi.ldo & 3) == 0) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 4) {
+        float4 w = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+        if (epi.accumulate) {
+          float4 q = *reinterpret_cast<const float4*>(o + n + j);
+          w.x += q.x; w.y += q.y; w.z += q.z; w.w += q.w;
+        }
+        *reinterpret_cast<float4*>(o + n + j) = w;
+      }
+    } else {
+      for (int j = 0; j < 16; ++j)
+        if (n + j < N) o[n + j] = epi.accumulate ? o[n + j] + v[j] : v[j];
+    }
+  } else if (epi.mode == EPI_F32_T) {
+    float* o = reinterpret_cast<float*>(epi.out);
+#pragma unroll
+    for (int j = 0; j < 16; ++j)
+      if (n + j < N) {
+        float* p = o + (size_t)(n + j) * epi.ldo + m;
+        *p = epi.accumulate ? *p + v[j] : v[j];
+      }
+  } else {  // EPI_F16
+    __half* o = reinterpret_cast<__half*>(epi.out) + (size_t)m * epi.ldo;
+    if (n + 16 <= N && (epi.ldo & 7) == 0) {
+#pragma unroll
+      for (int j = 0; j < 16; j += 8) {
+        __align__(16) __half hv[8];
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          hv[q] = __float2half_rn(v[j + q]);
+          nf += f16_nonfinite(hv[q]);
+        }
+        *reinterpret_cast<uint4*>(o + n + j) = *reinterpret_cast<const uint4*>(hv);
+      }
+    } else {
+      for (int j = 0; j < 16; ++j)
+        if (n + j < N) {
+          __half h = __float2half_rn(v[j]);
+          nf += f16_nonfinite(h);
+          o[n + j] = h;
+        }
+    }
+  }
+}
+
+template <int BN, int AMN, int BMN>
+__global__ void __launch_bounds__(128, 1)
+    gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, int M, int N,
+                   int K, int kbps, Epilogue epi, float* ws) {
+  using C = TileCfg<BN>;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
+  uint64_t* empty = full + C::STAGES;
+  uint64_t* tfull = empty + C::STAGES;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int kb_total = (K + BK - 1) / BK;
+  const int kb0 = blockIdx.z * kbps;
+  const int nkb = min(kb_total, kb0 + kbps) - kb0;
+
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch(&tma);
+    ptx::tma_prefetch(&tmb);
+    for (int s = 0; s < C::STAGES; ++s) {
+      ptx::mbar_init(full + s, 1);
+      ptx::mbar_init(empty + s, 1);
+    }
+    ptx::mbar_init(tfull, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tslot, BN);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (warp == 0 && lane == 0) {
+    // ---------------- TMA producer
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % C::STAGES;
+      const uint32_t ph = (i / C::STAGES) & 1;
+      ptx::mbar_wait(empty + s, ph ^ 1);
+      uint8_t* sa = smem + s * C::STAGE;
+      uint8_t* sb = sa + C::A_BYTES;
+      const int k0 = (kb0 + i) * BK;
+      ptx::mbar_arrive_expect_tx(full + s, C::STAGE);
+      if (AMN == 0) {
+        ptx::tma_load_2d(sa, &tma, full + s, k0, m0);
+      } else {
+        ptx::tma_load_2d(sa, &tma, full + s, m0, k0);
+        ptx::tma_load_2d(sa + 8192, &tma, full + s, m0 + 64, k0);
+      }
+      if (BMN == 0) {
+        ptx::tma_load_2d(sb, &tmb, full + s, k0, n0);
+      } else {
+#pragma unroll
+        for (int j = 0; j < BN / 64; ++j) ptx::tma_load_2d(sb + j * 8192, &tmb, full + s, n0 + 64 * j, k0);
+      }
+    }
+  } else if (warp == 1 && lane == 0) {
+    // ---------------- MMA issuer
+    constexpr uint32_t idesc = ptx::idesc_f16_f32(BM, BN, AMN, BMN);
+    for (int i = 0; i < nkb; ++i) {
+      const int s = i % C::STAGES;
+      const uint32_t ph = (i / C::STAGES) & 1;
+      ptx::mbar_wait(full + s, ph);
+      ptx::tc_fence_after();
+      const uint32_t sa = ptx::smem_u32(smem + s * C::STAGE);
+      const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+      for (int k = 0; k < BK / 16; ++k) {
+        // K-major: advance 16 elements = 32 B inside the 128 B swizzled row.
+        // MN-major: advance 16 K-rows = 2048 B (two 8-row atoms of 1024 B);
+        //   LBO = 8192 B between 64-wide MN atoms, SBO = 1024 B between 8-row K groups.
+        const uint64_t ad = AMN ? ptx::smem_desc_sw128(sa + k * 2048, 8192, 1024)
+                                : ptx::smem_desc_sw128(sa + k * 32, 0, 1024);
+        const uint64_t bd = BMN ? ptx::smem_desc_sw128(sb + k * 2048, 8192, 1024)
+                                : ptx::smem_desc_sw128(sb + k * 32, 0, 1024);
+        ptx::mma_f16(tbase, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+      }
+      ptx::mma_commit(empty + s);  // frees the smem slot once these MMAs retire
+    }
+    ptx::mma_commit(tfull);        // accumulator complete
+  }
+  __syncwarp();
+
+  // ---------------- epilogue: TMEM -> registers -> global
+  ptx::mbar_wait(tfull, 0);
+  ptx::tc_fence_after();
+  const int m = m0 + warp * 32 + lane;
+  int nf = 0;
+#pragma unroll 1
+  for (int c = 0; c < BN; c += 16) {
+    float v[16];
+    ptx::tmem_ld16(tbase + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+    if (n0 + c < N) epi_store16(epi, ws, M, N, m, n0 + c, v, nf);
+  }
+  if (epi.mode == EPI_F16 && epi.nonfinite) {
+    nf = __reduce_add_sync(0xffffffffu, nf);
+    if (lane == 0 && nf) atomicAdd(epi.nonfinite, nf);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tbase, BN);
+  }
+}
+
+// Deterministic split-K reduction + the requested epilogue.
+__global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, Epilogue epi) {
+  const size_t total = (size_t)M * N;
+  int nf = 0;
+  for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
+    float s = ws[idx];
+    for (int z = 1; z < splits; ++z) s += ws[(size_t)z * total + idx];
+    const int m = (int)(idx / N), n = (int)(idx % N);
+    if (epi.bias) s += epi.bias_on_m ? bias_at(epi, m) : bias_at(epi, n);
+    if (epi.relu) s = fmaxf(s, 0.f);
+    if (epi.mode == EPI_F32) {
+      float* o = reinterpret_cast<float*>(epi.out) + (size_t)m * epi.ldo + n;
+      *o = epi.accumulate ? *o + s : s;
+    } else if (epi.mode == EPI_F32_T) {
+      float* o = reinterpret_cast<float*>(epi.out) + (size_t)n * epi.ldo + m;
+      *o = epi.accumulate ? *o + s : s;
+    } else {
+      __half h = __float2half_rn(s);
+      nf += f16_nonfinite(h);
+      reinterpret_cast<__half*>(epi.out)[(size_t)m * epi.ldo + n] = h;
+    }
+  }
+  if (epi.mode == EPI_F16 && epi.nonfinite) {
+    nf = __reduce_add_sync(0xffffffffu, nf);
+    if ((threadIdx.x & 31) == 0 && nf) atomicAdd(epi.nonfinite, nf);
+  }
+}
+
+// ---------------------------------------------------------------- fp32 SIMT GEMM
+// 64x64 tile, 256 threads, 4x4 per thread, sequential k (deterministic).
+__global__ void __launch_bounds__(256) gemm_f32_kernel(const float* __restrict__ A, long sam, long sak,
+                                                       const float* __restrict__ B, long sbn, long sbk, int M,
+                                                       int N, int K, Epilogue epi) {
+  __shared__ float As[16][64 + 4];
+  __shared__ float Bs[16][64 + 4];
+  const int tx = threadIdx.x % 16, ty = threadIdx.x / 16;
+  const int m0 = blockIdx.x * 64, n0 = blockIdx.y * 64;
+  float acc[4][4] = {};
+  for (int k0 = 0; k0 < K; k0 += 16) {
+    for (int e = threadIdx.x; e < 16 * 64; e += 256) {
+      const int kk = e / 64, r = e % 64;
+      const int m = m0 + r, n = n0 + r, k = k0 + kk;
+      As[kk][r] = (m < M && k < K) ? A[(size_t)m * sam + (size_t)k * sak] : 0.f;
+      Bs[kk][r] = (n < N && k < K) ? B[(size_t)n * sbn + (size_t)k * sbk] : 0.f;
+    }
+    __syncthreads();
+#pragma unroll
+    for (int kk = 0; kk < 16; ++kk) {
+      float a[4], b[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) a[i] = As[kk][ty * 4 + i];
+#pragma unroll
+      for (int j = 0; j < 4; ++j) b[j] = Bs[kk][tx * 4 + j];
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+#pragma unroll
+        for (int j = 0; j < 4; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    __syncthreads();
+  }
+#pragma unroll
+  for (int i = 0; i < 4; ++i)
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int m = m0 + ty * 4 + i, n = n0 + tx * 4 + j;
+      if (m >= M || n >= N) continue;
+      float s = acc[i][j];
+      if (epi.bias) s += epi.bias_on_m ? bias_at(epi, m) : bias_at(epi, n);
+      if (epi.relu) s = fmaxf(s, 0.f);
+      float* o = reinterpret_cast<float*>(epi.out) + (epi.mode == EPI_F32_T ? (size_t)n * epi.ldo + m
+                                                                            : (size_t)m * epi.ldo + n);
+      *o = epi.accumulate ? *o + s : s;
+    }
+}
+
+// ---------------------------------------------------------------- host side
+PFN_cuTensorMapEncodeTiled_v12000 g_encode = nullptr;
+std::once_flag g_encode_once;
+
+bool get_encode() {
+  std::call_once(g_encode_once, [] {
+    cudaDriverEntryPointQueryResult q;
+    void* fn = nullptr;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &fn, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      g_encode = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(fn);
+  });
+  return g_encode != nullptr;
+}
+
+// 2-D fp16 tensor map, inner dimension contiguous, SWIZZLE_128B, 64-element inner box.
+int make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, uint64_t row_stride_elems,
+              uint32_t box_outer) {
+  if (!get_encode()) {
+    snprintf(g_gemm_err, sizeof g_gemm_err, "cuTensorMapEncodeTiled unavailable");
+    return -2;
+  }
+  if ((reinterpret_cast<uintptr_t>(base) & 15) || ((row_stride_elems * 2) & 15)) {
+    snprintf(g_gemm_err, sizeof g_gemm_err, "TMA operand not 16-byte aligned (base %p, stride %llu elems)", base,
+             (unsigned long long)row_stride_elems);
+    return -1;
+  }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_elems * 2};
+  cuuint32_t box[2] = {64, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(base), dims, strides, box, estr,
+                        CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                        CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(g_gemm_err, sizeof g_gemm_err, "cuTensorMapEncodeTiled failed (%d): inner %llu outer %llu stride %llu",
+             (int)r, (unsigned long long)inner, (unsigned long long)outer, (unsigned long long)row_stride_elems);
+    return -2;
+  }
+  return 0;
+}
+
+template <int BN, int AMN, int BMN>
+cudaError_t launch_tc(const GemmPlan& p, cudaStream_t s) {
+  using C = TileCfg<BN>;
+  dim3 grid((p.M + BM - 1) / BM, (p.N + BN - 1) / BN, p.splits);
+  Epilogue e = p.epi;
+  if (p.splits > 1) e.mode = EPI_SPLITK;
+  gemm_tc_kernel<BN, AMN, BMN><<<grid, 128, C::SMEM, s>>>(p.ta, p.tb, p.M, p.N, p.K, p.kbps, e, p.ws);
+  return cudaGetLastError();
+}
+
+template <int BN, int AMN, int BMN>
+cudaError_t set_attr() {
+  return cudaFuncSetAttribute(gemm_tc_kernel<BN, AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              TileCfg<BN>::SMEM);
+}
+template <int BN>
+cudaError_t set_attr_bn() {
+  cudaError_t e;
+  if ((e = set_attr<BN, 0, 0>()) != cudaSuccess) return e;
+  if ((e = set_attr<BN, 0, 1>()) != cudaSuccess) return e;
+  if ((e = set_attr<BN, 1, 0>()) != cudaSuccess) return e;
+  return set_attr<BN, 1, 1>();
+}
+
+template <int BN>
+cudaError_t launch_tc_bn(const GemmPlan& p, cudaStream_t s) {
+  if (p.amn == 0 && p.bmn == 0) return launch_tc<BN, 0, 0>(p, s);
+  if (p.amn == 0 && p.bmn == 1) return launch_tc<BN, 0, 1>(p, s);
+  if (p.amn == 1 && p.bmn == 0) return launch_tc<BN, 1, 0>(p, s);
+  return launch_tc<BN, 1, 1>(p, s);
+}
+
+int choose_bn(int M, int N) {
+  const int mt = (M + BM - 1) / BM;
+  if (N <= 64) return 64;
+  if (mt * ((N + 127) / 128) < 148) return 64;     // latency-bound: more CTAs
+  if (mt * ((N + 255) / 256) >= 148) return 256;
+  return 128;
+}
+
+}  // namespace
+
+cudaError_t gemm_init() {
+  cudaError_t e;
+  if ((e = set_attr_bn<64>()) != cudaSuccess) return e;
+  if ((e = set_attr_bn<128>()) != cudaSuccess) return e;
+  return set_attr_bn<256>();
+}
+
+size_t gemm_ws_floats(int M, int N, int K) {
+  // automatic plans split K at most 16 ways
+  (void)K;
+  return (size_t)16 * M * N;
+}
+
+int gemm_plan_tc(GemmPlan* p, const __half* A, long lda, int a_mn, const __half* B, long ldb, int b_mn, int M,
+                 int N, int K, const Epilogue& epi, float* ws, size_t ws_floats, int force_bn, int force_splits) {
+  *p = GemmPlan();
+  p->tc = true;
+  p->A = A;
+  p->B = B;
+  p->lda = lda;
+  p->ldb = ldb;
+  p->M = M;
+  p->N = N;
+  p->K = K;
+  p->amn = a_mn;
+  p->bmn = b_mn;
+  p->epi = epi;
+  p->ws = ws;
+  if (M <= 0 || N <= 0 || K <= 0) {
+    snprintf(g_gemm_err, sizeof g_gemm_err, "empty GEMM %dx%dx%d", M, N, K);
+    return -1;
+  }
+  int bn = force_bn ? force_bn : choose_bn(M, N);
+  if (bn != 64 && bn != 128 && bn != 256) {
+    snprintf(g_gemm_err, sizeof g_gemm_err, "bad BN %d", bn);
+    return -1;
+  }
+  p->bn = bn;
+  const int kb = (K + BK - 1) / BK;
+  int splits = 1;
+  if (force_splits > 0) {
+    splits = force_splits;
+  } else {
+    const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+    if (tiles < 120 && kb >= 16) {
+      splits = 148 / tiles;
+      if (splits > kb / 8) splits = kb / 8;
+      if (splits > 16) splits = 16;
+      if (splits < 1) splits = 1;
+    }
+  }
+  if (splits > kb) splits = kb;
+  int kbps = (kb + splits - 1) / splits;
+  splits = (kb + kbps - 1) / kbps;
+  if (splits > 1 && (!ws || ws_floats < (size_t)splits * M * N)) {
+    splits = 1;
+    kbps = kb;
+  }
+  p->splits = splits;
+  p->kbps = kbps;
+  int r;
+  if (a_mn == 0)
+    r = make_tmap(&p->ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BM);
+  else
+    r = make_tmap(&p->ta, A, (uint64_t)M, (uint64_t)K, (uint64_t)lda, BK);
+  if (r) return r;
+  if (b_mn == 0)
+    r = make_tmap(&p->tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, (uint32_t)bn);
+  else
+    r = make_tmap(&p->tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, BK);
+  return r;
+}
+
+int gemm_plan_f32(GemmPlan* p, const float* A, long lda, int a_mn, const float* B, long ldb, int b_mn, int M,
+                  int N, int K, const Epilogue& epi) {
+  *p = GemmPlan();
+  p->tc = false;
+  p->A = A;
+  p->B = B;
+  p->lda = lda;
+  p->ldb = ldb;
+  p->M = M;
+  p->N = N;
+  p->K = K;
+  p->amn = a_mn;
+  p->bmn = b_mn;
+  p->epi = epi;
+  if (M <= 0 || N <= 0 || K <= 0) return -1;
+  if (epi.mode == EPI_F16) {
+    snprintf(g_gemm_err, sizeof g_gemm_err, "fp32 GEMM cannot write fp16");
+    return -1;
+  }
+  return 0;
+}
+
+cudaError_t gemm_run(const GemmPlan& p, cudaStream_t s) {
+  if (!p.tc) {
+    const long sam = p.amn ? 1 : p.lda, sak = p.amn ? p.lda : 1;
+    const long sbn = p.bmn ? 1 : p.ldb, sbk = p.bmn ? p.ldb : 1;
+    dim3 grid((p.M + 63) / 64, (p.N + 63) / 64);
+    gemm_f32_kernel<<<grid, 256, 0, s>>>(static_cast<const float*>(p.A), sam, sak, static_cast<const float*>(p.B),
+                                         sbn, sbk, p.M, p.N, p.K, p.epi);
+    return cudaGetLastError();
+  }
+  cudaError_t e;
+  switch (p.bn) {
+    case 64: e = launch_tc_bn<64>(p, s); break;
+    case 128: e = launch_tc_bn<128>(p, s); break;
+    default: e = launch_tc_bn<256>(p, s); break;
+  }
+  if (e != cudaSuccess || p.splits <= 1) return e;
+  const size_t total = (size_t)p.M * p.N;
+  int blocks = (int)((total + 255) / 256);
+  if (blocks > 148 * 8) blocks = 148 * 8;
+  splitk_reduce_kernel<<<blocks, 256, 0, s>>>(p.ws, p.splits, p.M, p.N, p.epi);
+  return cudaGetLastError();
+}
+
+}  // namespace hdp

@@ -1,0 +1,69 @@
+// Gate-contraction GEMMs of the LSTM step (SURVEY.md §8(a) A1, A2, A4, A5,
+// A7, A8; PAPER.md:82 fprop/bprop, :142 "Math: matrix ... multiplication").
+//
+//   C[m][n] = sum_k A(m,k) * B(n,k)        (fp32 accumulate)
+//
+// Operands are addressed either K-major (A stored [M][K], B stored [N][K])
+// or MN-major (A stored [K][M], B stored [K][N]) so that every forward and
+// backward contraction of the LSTM reads its operands where they already
+// live -- no transposes.
+#pragma once
+#include <cuda.h>
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cstddef>
+#include <cstdint>
+
+namespace hdp {
+
+enum EpiMode : int {
+  EPI_F32 = 0,     // out32[m*ldo + n]
+  EPI_F32_T = 1,   // out32[n*ldo + m]      (transposed store, coalesced for swap-AB)
+  EPI_F16 = 2,     // out16[m*ldo + n]      (RNE, counts non-finite results)
+  EPI_SPLITK = 3,  // internal: fp32 partials for the deterministic split-K reduction
+};
+
+struct Epilogue {
+  int mode = EPI_F32;
+  void* out = nullptr;
+  long ldo = 0;
+  const void* bias = nullptr;   // added before the activation (fp32, or fp16 if bias_f16)
+  int bias_f16 = 0;
+  int bias_on_m = 0;            // bias indexed by m (1) or by n (0)
+  int relu = 0;
+  int accumulate = 0;           // fp32 modes: out += result
+  int* nonfinite = nullptr;     // EPI_F16: += number of non-finite outputs
+};
+
+struct GemmPlan {
+  bool tc = true;  // tcgen05 path (fp16) or fp32 SIMT path
+  CUtensorMap ta, tb;
+  const void* A = nullptr;
+  const void* B = nullptr;
+  long lda = 0, ldb = 0;
+  int M = 0, N = 0, K = 0;
+  int bn = 128, amn = 0, bmn = 0;
+  int splits = 1, kbps = 0;
+  Epilogue epi;
+  float* ws = nullptr;
+};
+
+// Workspace (floats) an automatic plan may need for split-K.
+size_t gemm_ws_floats(int M, int N, int K);
+
+// fp16 tensor-core plan.  a_mn / b_mn select MN-major operands.
+// force_bn / force_splits: 0 = automatic.  Returns 0 or a negative error.
+int gemm_plan_tc(GemmPlan* p, const __half* A, long lda, int a_mn, const __half* B, long ldb, int b_mn, int M,
+                 int N, int K, const Epilogue& epi, float* ws, size_t ws_floats, int force_bn = 0,
+                 int force_splits = 0);
+// fp32 SIMT plan (FP32 mode, PAPER.md:147 baseline): same addressing.
+int gemm_plan_f32(GemmPlan* p, const float* A, long lda, int a_mn, const float* B, long ldb, int b_mn, int M,
+                  int N, int K, const Epilogue& epi);
+cudaError_t gemm_run(const GemmPlan& p, cudaStream_t s);
+// one-time per-device setup (dynamic smem opt-in for every instantiation);
+// must precede stream capture
+cudaError_t gemm_init();
+
+const char* gemm_last_error();
+
+}  // namespace hdp

@@ -1,0 +1,1085 @@
+// libhdp.so host runtime: the C-ABI of include/hdp.h.
+//
+// Owns the device layout (padded, gate-interleaved, bucketed), carves the
+// caller's arena, captures the per-slot forward / per-bucket backward
+// sequences into CUDA graphs, and drives the bucketed NCCL exchange with the
+// fused average+update kernel (K11) on a side stream so that the update of
+// bucket b overlaps the BPTT of the layers below it.
+#include "../../include/hdp.h"
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "gemm.cuh"
+#include "kernels.cuh"
+
+namespace {
+
+thread_local std::string g_err;
+
+int fail(int code, const char* fmt, ...) {
+  char buf[512];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  return code;
+}
+
+#define CK_CUDA(x)                                                                              \
+  do {                                                                                          \
+    cudaError_t e_ = (x);                                                                       \
+    if (e_ != cudaSuccess) return fail(HDP_ERR_CUDA, "%s: %s (%s:%d)", #x, cudaGetErrorString(e_), __FILE__, __LINE__); \
+  } while (0)
+#define CK_NCCL(x)                                                                              \
+  do {                                                                                          \
+    ncclResult_t r_ = (x);                                                                      \
+    if (r_ != ncclSuccess) return fail(HDP_ERR_NCCL, "%s: %s", #x, ncclGetErrorString(r_));    \
+  } while (0)
+#define CK(x)                    \
+  do {                           \
+    int rc_ = (x);               \
+    if (rc_ != HDP_OK) return rc_; \
+  } while (0)
+
+inline long r16(long v) { return (v + 15) / 16 * 16; }
+inline long rup(long v, long a) { return (v + a - 1) / a * a; }
+
+enum Kind { K_EMBED, K_W, K_U, K_B, K_F, K_FB, K_WO, K_BO, K_FLAT };
+
+struct Block {
+  std::string name;
+  Kind kind;
+  int layer;
+  long canon_off, rows, cols;
+  long dev_off, dev_rows, dev_cols;
+  int bucket;
+};
+
+struct Bucket {
+  long off = 0, len = 0;  // in the device parameter vector (elements)
+  long shard = 0;         // len / world
+  long moff = 0;          // offset of this rank's shard in the master buffers
+};
+
+struct SlotState {
+  bool fwd = false, bwd = false;
+  int B = 0, T = 0;
+};
+
+struct GraphKey {
+  int slot, B, T, seg;
+  bool operator<(const GraphKey& o) const {
+    return std::tie(slot, B, T, seg) < std::tie(o.slot, o.B, o.T, o.seg);
+  }
+};
+
+}  // namespace
+
+struct hdp_ctx {
+  int world = 1, rank = 0, device = 0;
+  ncclComm_t comm = nullptr;
+  // model
+  bool configured = false, bound = false, loaded = false, poisoned = false;
+  hdp_model_desc d{};
+  bool f32 = false;       // FP32 math mode
+  bool gf32 = false;      // fp32 gradients / wire
+  int nslots = 1;
+  long hp = 0, Ip0 = 0, Fp = 0, esz = 2, gsz = 2;
+  std::vector<long> Ip;   // per layer padded input width
+  std::vector<Block> blocks;
+  std::vector<Bucket> buckets;  // index = bucket id; exchange order = id order
+  long n_params = 0, P = 0, M_own = 0, max_bucket = 0;
+  size_t arena_bytes = 0;
+  // arena carve
+  char* arena = nullptr;
+  char* w = nullptr;      // working weights [P] (fp16 or fp32)
+  float* master = nullptr;
+  float* s1 = nullptr;
+  float* s2 = nullptr;
+  char* grads = nullptr;  // [nslots][P]
+  char* recv = nullptr;
+  struct Slot {
+    char* stage_x;
+    int8_t* stage_t;
+    char* X0;
+    char* Hs;
+    float* C;
+    char* gates;
+    char* Z;
+    float* y;
+    float* dy;
+    float* loss;
+    float* partials;
+  };
+  std::vector<Slot> slot;
+  float *Gx = nullptr, *Gh = nullptr, *dH[2] = {nullptr, nullptr}, *dhrec = nullptr, *dc = nullptr;
+  char *dA = nullptr, *dz = nullptr;
+  float* crp = nullptr;
+  size_t crp_floats = 0;
+  float* ws = nullptr;
+  size_t ws_floats = 0;
+  int32_t *keys_in = nullptr, *keys_out = nullptr, *vals_in = nullptr, *vals_out = nullptr;
+  void* sort_temp = nullptr;
+  size_t sort_bytes = 0;
+  int* status = nullptr;  // [0] nonfinite count
+  float* loadbuf = nullptr;
+  // runtime
+  cudaStream_t cap = nullptr, comm_stream = nullptr;
+  cudaEvent_t ev_done = nullptr, ev_count = nullptr;
+  std::vector<cudaEvent_t> ev_bucket;
+  int* count_host = nullptr;  // pinned
+  bool count_pending = false;
+  std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::vector<SlotState> st;
+  // schedule
+  bool lr_set = false;
+  double lam0 = 0, gamma = 1, n_half = 1, max_eff = 0.1, mom = 0.9, b1 = 0.9, b2 = 0.999, eps = 1e-8;
+  float alpha = 10.f;
+  long adam_k = 0;
+
+  int L() const { return d.n_layers; }
+  int Nw() const { return world * nslots; }
+  void* W(int bi) const { return w + blocks[bi].dev_off * esz; }
+  void* G(int s, int bi) const { return grads + ((long)s * P + blocks[bi].dev_off) * gsz; }
+  int find(const char* n) const {
+    for (size_t i = 0; i < blocks.size(); ++i)
+      if (blocks[i].name == n) return (int)i;
+    return -1;
+  }
+};
+
+// ====================================================================== layout
+namespace {
+
+void build_layout(hdp_ctx* c) {
+  const hdp_model_desc& d = c->d;
+  c->blocks.clear();
+  c->buckets.clear();
+  const long h = d.hidden;
+  c->hp = r16(h);
+  c->Ip0 = d.vocab > 0 ? r16(d.embed_dim) : r16(d.input_dim);
+  c->Fp = d.fc_hidden > 0 ? r16(d.fc_hidden) : 0;
+  c->Ip.assign(d.n_layers, c->hp);
+  if (d.n_layers > 0) c->Ip[0] = c->Ip0;
+  long canon = 0;
+  auto add = [&](const char* name, Kind k, int layer, long rows, long cols, long drows, long dcols) {
+    Block b;
+    b.name = name;
+    b.kind = k;
+    b.layer = layer;
+    b.canon_off = canon;
+    b.rows = rows;
+    b.cols = cols;
+    b.dev_rows = drows;
+    b.dev_cols = dcols;
+    b.dev_off = 0;
+    b.bucket = -1;
+    canon += rows * cols;
+    c->blocks.push_back(b);
+  };
+  if (d.n_layers == 0) {
+    add("flat", K_FLAT, -1, d.flat_params, 1, d.flat_params, 1);
+  } else {
+    const long i0 = d.vocab > 0 ? d.embed_dim : d.input_dim;
+    if (d.vocab > 0) add("E", K_EMBED, -1, d.vocab, d.embed_dim, d.vocab, c->Ip0);
+    char nm[16];
+    for (int l = 0; l < d.n_layers; ++l) {
+      const long il = l == 0 ? i0 : h;
+      snprintf(nm, sizeof nm, "W%d", l);
+      add(nm, K_W, l, 4 * h, il, 4 * c->hp, c->Ip[l]);
+      snprintf(nm, sizeof nm, "U%d", l);
+      add(nm, K_U, l, 4 * h, h, 4 * c->hp, c->hp);
+      snprintf(nm, sizeof nm, "b%d", l);
+      add(nm, K_B, l, 4 * h, 1, 4 * c->hp, 1);
+    }
+    if (d.fc_hidden > 0) {
+      add("F", K_F, -1, d.fc_hidden, h, c->Fp, c->hp);
+      add("fb", K_FB, -1, d.fc_hidden, 1, c->Fp, 1);
+      add("wo", K_WO, -1, d.fc_hidden, 1, c->Fp, 1);
+    } else {
+      add("wo", K_WO, -1, h, 1, c->hp, 1);
+    }
+    add("bo", K_BO, -1, 1, 1, 1, 1);
+  }
+  c->n_params = canon;
+  // buckets in readiness order: head, layer L-1 .. 0, embedding
+  std::vector<std::vector<int>> groups;
+  if (d.n_layers == 0) {
+    groups.push_back({0});
+  } else {
+    std::vector<int> head, emb;
+    std::vector<std::vector<int>> lay(d.n_layers);
+    for (size_t i = 0; i < c->blocks.size(); ++i) {
+      const Block& b = c->blocks[i];
+      if (b.kind == K_EMBED) emb.push_back((int)i);
+      else if (b.layer >= 0) lay[b.layer].push_back((int)i);
+      else head.push_back((int)i);
+    }
+    groups.push_back(head);
+    for (int l = d.n_layers - 1; l >= 0; --l) groups.push_back(lay[l]);
+    if (!emb.empty()) groups.push_back(emb);
+  }
+  const long align_bucket = 64L * c->world;
+  long off = 0, moff = 0;
+  c->max_bucket = 0;
+  for (size_t g = 0; g < groups.size(); ++g) {
+    Bucket bk;
+    bk.off = off;
+    long p = off;
+    for (int bi : groups[g]) {
+      Block& b = c->blocks[bi];
+      p = rup(p, 64);
+      b.dev_off = p;
+      b.bucket = (int)g;
+      p += b.dev_rows * b.dev_cols;
+    }
+    bk.len = rup(p - off, align_bucket);
+    bk.shard = bk.len / c->world;
+    bk.moff = moff;
+    moff += bk.shard;
+    off += bk.len;
+    c->max_bucket = std::max(c->max_bucket, bk.len);
+    c->buckets.push_back(bk);
+  }
+  c->P = off;
+  c->M_own = moff;
+}
+
+// canonical (r, col) -> device element offset within the block
+inline long dev_index(const hdp_ctx* c, const Block& b, long r, long col) {
+  if (b.kind == K_W || b.kind == K_U || b.kind == K_B) {
+    const long h = c->d.hidden;
+    const long g = r / h, j = r % h;
+    return (4 * j + g) * b.dev_cols + col;  // gate rows interleaved per unit
+  }
+  return r * b.dev_cols + col;
+}
+
+struct Carver {
+  char* base;
+  size_t off = 0;
+  explicit Carver(char* b) : base(b) {}
+  char* take(size_t bytes) {
+    off = rup(off, 256);
+    char* p = base ? base + off : nullptr;
+    off += bytes;
+    return p;
+  }
+};
+
+size_t gemm_need(int M, int N, int K) {
+  // mirror of the automatic split heuristic's worst case: splits <= 16
+  (void)K;
+  return (size_t)16 * M * N;
+}
+
+void carve(hdp_ctx* c, char* base) {
+  const hdp_model_desc& d = c->d;
+  Carver cv(base);
+  const long P = c->P;
+  c->w = cv.take(P * c->esz);
+  c->master = (float*)cv.take(c->M_own * 4);
+  c->s1 = (float*)cv.take(c->M_own * 4);
+  c->s2 = (float*)cv.take(d.optimizer == HDP_OPT_ADAM ? c->M_own * 4 : 0);
+  c->grads = cv.take((size_t)c->nslots * P * c->gsz);
+  c->recv = cv.take(c->world > 1 ? c->max_bucket * c->gsz : 0);
+  c->status = (int*)cv.take(256);
+  c->slot.assign(c->nslots, hdp_ctx::Slot{});
+  if (d.n_layers > 0) {
+    const long B = d.max_batch, T = d.max_seq, L = d.n_layers, hp = c->hp, e = c->esz;
+    const long rows = B * T;
+    const long in_bytes = d.vocab > 0 ? 4 : (long)d.input_dim * e;
+    for (int s = 0; s < c->nslots; ++s) {
+      hdp_ctx::Slot& S = c->slot[s];
+      S.stage_x = cv.take(rows * in_bytes);
+      S.stage_t = (int8_t*)cv.take(rows);
+      S.X0 = cv.take(rows * c->Ip0 * e);
+      S.Hs = cv.take(L * (T + 1) * B * hp * e);
+      S.C = (float*)cv.take(L * T * B * hp * 4);
+      S.gates = cv.take(L * T * B * 4 * hp * e);
+      S.Z = cv.take(c->Fp ? rows * c->Fp * e : 0);
+      S.y = (float*)cv.take(rows * 4);
+      S.dy = (float*)cv.take(rows * 4);
+      S.loss = (float*)cv.take(4);
+      S.partials = (float*)cv.take(hdp::head_partials_count((int)rows) * 4);
+    }
+    c->Gx = (float*)cv.take(rows * 4 * hp * 4);
+    c->Gh = (float*)cv.take(B * 4 * hp * 4);
+    c->dA = cv.take(rows * 4 * hp * e);
+    const long dw = std::max(hp, c->Ip0);
+    c->dH[0] = (float*)cv.take(rows * dw * 4);
+    c->dH[1] = (float*)cv.take(rows * dw * 4);
+    c->dhrec = (float*)cv.take(B * hp * 4);
+    c->dc = (float*)cv.take(B * hp * 4);
+    c->dz = cv.take(c->Fp ? rows * c->Fp * e : 0);
+    const long maxcols = std::max(std::max(4 * hp, c->Fp), std::max(hp, 1L));
+    c->crp_floats = hdp::colreduce_partials_floats((int)rows, (int)maxcols);
+    c->crp = (float*)cv.take(c->crp_floats * 4);
+    // split-K workspace for the weight-gradient GEMMs (K = B*T)
+    size_t ws = 0;
+    for (int l = 0; l < L; ++l) {
+      ws = std::max(ws, gemm_need((int)(4 * hp), (int)c->Ip[l], (int)rows));
+      ws = std::max(ws, gemm_need((int)(4 * hp), (int)hp, (int)rows));
+    }
+    if (c->Fp) ws = std::max(ws, gemm_need((int)c->Fp, (int)hp, (int)rows));
+    if (c->f32) ws = 0;
+    c->ws_floats = ws;
+    c->ws = (float*)cv.take(ws * 4);
+    if (d.vocab > 0) {
+      c->keys_in = (int32_t*)cv.take(rows * 4);
+      c->keys_out = (int32_t*)cv.take(rows * 4);
+      c->vals_in = (int32_t*)cv.take(rows * 4);
+      c->vals_out = (int32_t*)cv.take(rows * 4);
+      c->sort_bytes = hdp::embed_sort_temp_bytes((int)rows);
+      c->sort_temp = cv.take(c->sort_bytes);
+    }
+  }
+  c->arena_bytes = rup(cv.off, 256);
+}
+
+// ---------------------------------------------------------------- GEMM helper
+int gemm(hdp_ctx* c, const void* A, long lda, int amn, const void* B, long ldb, int bmn, long M, long N, long K,
+         const hdp::Epilogue& epi, cudaStream_t s) {
+  hdp::GemmPlan p;
+  int r;
+  if (c->f32)
+    r = hdp::gemm_plan_f32(&p, (const float*)A, lda, amn, (const float*)B, ldb, bmn, (int)M, (int)N, (int)K, epi);
+  else
+    r = hdp::gemm_plan_tc(&p, (const __half*)A, lda, amn, (const __half*)B, ldb, bmn, (int)M, (int)N, (int)K, epi,
+                          c->ws, c->ws_floats);
+  if (r) return fail(HDP_ERR_ARG, "gemm plan %ldx%ldx%ld: %s", M, N, K, hdp::gemm_last_error());
+  CK_CUDA(hdp::gemm_run(p, s));
+  return HDP_OK;
+}
+
+hdp::Epilogue epi_f32(void* out, long ldo, const void* bias = nullptr, int bias_f16 = 0) {
+  hdp::Epilogue e;
+  e.mode = hdp::EPI_F32;
+  e.out = out;
+  e.ldo = ldo;
+  e.bias = bias;
+  e.bias_f16 = bias_f16;
+  return e;
+}
+// activation / gradient output in the working element type
+hdp::Epilogue epi_elem(bool f32, void* out, long ldo) {
+  hdp::Epilogue e;
+  e.mode = f32 ? hdp::EPI_F32 : hdp::EPI_F16;
+  e.out = out;
+  e.ldo = ldo;
+  return e;
+}
+
+// ---------------------------------------------------------------- forward
+int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
+  const hdp_model_desc& d = c->d;
+  hdp_ctx::Slot& S = c->slot[si];
+  const long hp = c->hp, e = c->esz, L = d.n_layers;
+  const long rows = (long)B * T;
+  const int f32 = c->f32;
+  const long hs_layer = (long)(T + 1) * B * hp;  // elements per layer in Hs (actual B, T)
+  const long c_layer = (long)T * B * hp;
+  const long g_layer = (long)T * B * 4 * hp;
+  for (int l = 0; l < L; ++l) CK_CUDA(cudaMemsetAsync(S.Hs + l * hs_layer * e, 0, B * hp * e, s));
+  if (d.vocab > 0)
+    CK_CUDA(hdp::launch_embed_gather((const int32_t*)S.stage_x, B, T, c->W(c->find("E")), (int)c->Ip0, S.X0, f32, s));
+  else
+    CK_CUDA(hdp::launch_pack_input(S.stage_x, f32, B, T, d.input_dim, (int)c->Ip0, S.X0, f32, s));
+  char nm[16];
+  for (int l = 0; l < L; ++l) {
+    snprintf(nm, sizeof nm, "W%d", l);
+    const int iW = c->find(nm);
+    snprintf(nm, sizeof nm, "U%d", l);
+    const int iU = c->find(nm);
+    snprintf(nm, sizeof nm, "b%d", l);
+    const int ib = c->find(nm);
+    const long Ipl = c->Ip[l];
+    const char* X = l == 0 ? S.X0 : S.Hs + ((l - 1) * hs_layer + (long)B * hp) * e;
+    char* Hs = S.Hs + l * hs_layer * e;
+    float* Cl = S.C + l * c_layer;
+    char* Gl = S.gates + l * g_layer * e;
+    // K1: G_x = X W^T + b for all t (A1)
+    CK(gemm(c, X, Ipl, 0, c->W(iW), Ipl, 0, rows, 4 * hp, Ipl, epi_f32(c->Gx, 4 * hp, c->W(ib), !f32), s));
+    for (int t = 0; t < T; ++t) {
+      if (t > 0)  // K2: G_h = h_{t-1} U^T (A2)
+        CK(gemm(c, Hs + (long)t * B * hp * e, hp, 0, c->W(iU), hp, 0, B, 4 * hp, hp, epi_f32(c->Gh, 4 * hp), s));
+      // K3 (A3)
+      CK_CUDA(hdp::launch_cell_fwd(f32, c->Gx + (long)t * B * 4 * hp, t > 0 ? c->Gh : nullptr,
+                                   t > 0 ? Cl + (long)(t - 1) * B * hp : nullptr, Gl + (long)t * B * 4 * hp * e,
+                                   Cl + (long)t * B * hp, Hs + (long)(t + 1) * B * hp * e, B, (int)hp, s));
+    }
+  }
+  // head (A4)
+  const char* Htop = S.Hs + ((L - 1) * hs_layer + (long)B * hp) * e;
+  const int iwo = c->find("wo"), ibo = c->find("bo");
+  if (d.fc_hidden > 0) {
+    const int iF = c->find("F"), ifb = c->find("fb");
+    hdp::Epilogue ez = epi_elem(f32, S.Z, c->Fp);
+    ez.bias = c->W(ifb);
+    ez.bias_f16 = !f32;
+    ez.relu = 1;  // R7
+    CK(gemm(c, Htop, hp, 0, c->W(iF), hp, 0, rows, c->Fp, hp, ez, s));
+    CK_CUDA(hdp::launch_head_out(f32, S.Z, (int)rows, (int)c->Fp, c->Fp, c->W(iwo), c->W(ibo), S.stage_t, 0, B, T,
+                                 c->alpha, 1.f / (float)rows, S.y, S.dy, S.partials, s));
+    CK_CUDA(hdp::launch_loss_final(S.partials, hdp::head_partials_count((int)rows), 1.f / (float)rows, S.loss, s));
+  } else if (d.head_last_step) {
+    const char* Hlast = S.Hs + ((L - 1) * hs_layer + (long)T * B * hp) * e;
+    CK_CUDA(hdp::launch_head_out(f32, Hlast, B, (int)hp, hp, c->W(iwo), c->W(ibo), S.stage_t, 1, B, T, c->alpha,
+                                 1.f / (float)B, S.y, S.dy, S.partials, s));
+    CK_CUDA(hdp::launch_loss_final(S.partials, hdp::head_partials_count(B), 1.f / (float)B, S.loss, s));
+  } else {
+    CK_CUDA(hdp::launch_head_out(f32, Htop, (int)rows, (int)hp, hp, c->W(iwo), c->W(ibo), S.stage_t, 0, B, T,
+                                 c->alpha, 1.f / (float)rows, S.y, S.dy, S.partials, s));
+    CK_CUDA(hdp::launch_loss_final(S.partials, hdp::head_partials_count((int)rows), 1.f / (float)rows, S.loss, s));
+  }
+  return HDP_OK;
+}
+
+// ---------------------------------------------------------------- backward
+// seg 0 = head; seg 1 + k = layer L-1-k
+int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t s) {
+  const hdp_model_desc& d = c->d;
+  hdp_ctx::Slot& S = c->slot[si];
+  const long hp = c->hp, e = c->esz, L = d.n_layers;
+  const long rows = (long)B * T;
+  const int f32 = c->f32, gf = c->gf32;
+  const long hs_layer = (long)(T + 1) * B * hp;
+  const long c_layer = (long)T * B * hp;
+  const long g_layer = (long)T * B * 4 * hp;
+  const char* Htop = S.Hs + ((L - 1) * hs_layer + (long)B * hp) * e;
+  const int iwo = c->find("wo"), ibo = c->find("bo");
+  if (seg == 0) {
+    if (d.fc_hidden > 0) {
+      const int iF = c->find("F"), ifb = c->find("fb");
+      const long Fp = c->Fp;
+      CK_CUDA(hdp::launch_relu_dz(f32, S.dy, c->W(iwo), S.Z, c->dz, (int)rows, (int)Fp, s));          // R9
+      CK_CUDA(hdp::launch_colreduce(f32, S.Z, Fp, (int)rows, (int)Fp, S.dy, c->crp, gf, c->G(si, iwo), s));
+      CK_CUDA(hdp::launch_colreduce(1, S.dy, 1, (int)rows, 1, nullptr, c->crp, gf, c->G(si, ibo), s));
+      CK_CUDA(hdp::launch_colreduce(f32, c->dz, Fp, (int)rows, (int)Fp, nullptr, c->crp, gf, c->G(si, ifb), s));
+      // dF = dz^T H   (M = Fp, N = hp, K = B*T; both operands MN-major)
+      CK(gemm(c, c->dz, Fp, 1, Htop, hp, 1, Fp, hp, rows, epi_elem(gf, c->G(si, iF), hp), s));
+      // dH_top = dz F (M = B*T, N = hp, K = Fp; F read MN-major)
+      CK(gemm(c, c->dz, Fp, 0, c->W(iF), hp, 1, rows, hp, Fp, epi_f32(c->dH[0], hp), s));
+    } else if (d.head_last_step) {
+      const char* Hlast = S.Hs + ((L - 1) * hs_layer + (long)T * B * hp) * e;
+      CK_CUDA(hdp::launch_outer(f32, S.dy, c->W(iwo), c->dH[0], B, (int)hp, s));
+      CK_CUDA(hdp::launch_colreduce(f32, Hlast, hp, B, (int)hp, S.dy, c->crp, gf, c->G(si, iwo), s));
+      CK_CUDA(hdp::launch_colreduce(1, S.dy, 1, B, 1, nullptr, c->crp, gf, c->G(si, ibo), s));
+    } else {
+      CK_CUDA(hdp::launch_outer(f32, S.dy, c->W(iwo), c->dH[0], (int)rows, (int)hp, s));
+      CK_CUDA(hdp::launch_colreduce(f32, Htop, hp, (int)rows, (int)hp, S.dy, c->crp, gf, c->G(si, iwo), s));
+      CK_CUDA(hdp::launch_colreduce(1, S.dy, 1, (int)rows, 1, nullptr, c->crp, gf, c->G(si, ibo), s));
+    }
+    return HDP_OK;
+  }
+  const int l = (int)(L - seg);
+  // dH_above of this layer lives in dH[(L-1-l) & 1]
+  float* dHa = c->dH[(L - 1 - l) & 1];
+  float* dHnext = c->dH[(L - l) & 1];
+  char nm[16];
+  snprintf(nm, sizeof nm, "W%d", l);
+  const int iW = c->find(nm);
+  snprintf(nm, sizeof nm, "U%d", l);
+  const int iU = c->find(nm);
+  snprintf(nm, sizeof nm, "b%d", l);
+  const int ib = c->find(nm);
+  const long Ipl = c->Ip[l];
+  const char* X = l == 0 ? S.X0 : S.Hs + ((l - 1) * hs_layer + (long)B * hp) * e;
+  const char* Hs = S.Hs + l * hs_layer * e;
+  float* Cl = S.C + l * c_layer;
+  const char* Gl = S.gates + l * g_layer * e;
+  const bool last_only = d.head_last_step && l == L - 1;
+  for (int t = T - 1; t >= 0; --t) {
+    const float* dHa_t = last_only ? (t == T - 1 ? dHa : nullptr) : dHa + (long)t * B * hp;
+    // K6 (A6)
+    CK_CUDA(hdp::launch_cell_bwd(f32, dHa_t, t < T - 1 ? c->dhrec : nullptr, Gl + (long)t * B * 4 * hp * e,
+                                 Cl + (long)t * B * hp, t > 0 ? Cl + (long)(t - 1) * B * hp : nullptr, c->dc,
+                                 c->dA + (long)t * B * 4 * hp * e, B, (int)hp, t == T - 1, s));
+    if (t > 0)  // K7: dh_rec = dA_t U (A7); U read MN-major as [K = 4hp][N = hp]
+      CK(gemm(c, c->dA + (long)t * B * 4 * hp * e, 4 * hp, 0, c->W(iU), hp, 1, B, hp, 4 * hp,
+              epi_f32(c->dhrec, hp), s));
+  }
+  // K8 (A8): dW = dA^T X, dU = dA^T H_{-1}, db = sum dA
+  CK(gemm(c, c->dA, 4 * hp, 1, X, Ipl, 1, 4 * hp, Ipl, rows, epi_elem(gf, c->G(si, iW), Ipl), s));
+  CK(gemm(c, c->dA, 4 * hp, 1, Hs, hp, 1, 4 * hp, hp, rows, epi_elem(gf, c->G(si, iU), hp), s));
+  CK_CUDA(hdp::launch_colreduce(f32, c->dA, 4 * hp, (int)rows, (int)(4 * hp), nullptr, c->crp, gf, c->G(si, ib), s));
+  if (l > 0) {
+    // K9: dX = dA W  ->  dH_above of layer l-1 (W read MN-major as [K = 4hp][N = Ip])
+    CK(gemm(c, c->dA, 4 * hp, 0, c->W(iW), Ipl, 1, rows, Ipl, 4 * hp, epi_f32(dHnext, Ipl), s));
+  } else if (d.vocab > 0) {
+    CK(gemm(c, c->dA, 4 * hp, 0, c->W(iW), Ipl, 1, rows, Ipl, 4 * hp, epi_f32(dHnext, Ipl), s));
+    const int iE = c->find("E");
+    CK_CUDA(hdp::launch_embed_backward((const int32_t*)S.stage_x, B, T, d.vocab, dHnext, (int)c->Ip0, c->keys_in,
+                                       c->keys_out, c->vals_in, c->vals_out, c->sort_temp, c->sort_bytes,
+                                       c->G(si, iE), gf, s));
+  }
+  return HDP_OK;
+}
+
+int nsegs(const hdp_ctx* c) { return c->d.n_layers + 1; }
+
+// capture (once) and launch
+int run_graph(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t s) {
+  GraphKey k{si, B, T, seg};
+  auto it = c->graphs.find(k);
+  if (it == c->graphs.end()) {
+    CK_CUDA(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
+    int rc = seg < 0 ? enqueue_forward(c, si, B, T, c->cap) : enqueue_backward_seg(c, si, B, T, seg, c->cap);
+    cudaGraph_t g = nullptr;
+    cudaError_t ce = cudaStreamEndCapture(c->cap, &g);
+    if (rc != HDP_OK) {
+      if (g) cudaGraphDestroy(g);
+      return rc;
+    }
+    if (ce != cudaSuccess) return fail(HDP_ERR_CUDA, "graph capture: %s", cudaGetErrorString(ce));
+    cudaGraphExec_t ex = nullptr;
+    ce = cudaGraphInstantiate(&ex, g, 0);
+    cudaGraphDestroy(g);
+    if (ce != cudaSuccess) return fail(HDP_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
+    it = c->graphs.emplace(k, ex).first;
+  }
+  CK_CUDA(cudaGraphLaunch(it->second, s));
+  return HDP_OK;
+}
+
+int check_ready(const hdp_ctx* c) {
+  if (!c) return fail(HDP_ERR_ARG, "null context");
+  if (!c->configured || !c->bound) return fail(HDP_ERR_STATE, "context not configured/bound");
+  return HDP_OK;
+}
+
+double sched(const hdp_ctx* c, int epoch) {
+  const double N = c->Nw();
+  double lam = c->lam0 / (1.0 + N / c->n_half);  // Eq. 4
+  if (lam * N > c->max_eff) lam = c->max_eff / N; // clip
+  return lam * std::pow(c->gamma, (double)epoch); // Eq. 3
+}
+
+__attribute__((unused)) int nccl_async_check(hdp_ctx* c) {
+  if (!c->comm) return HDP_OK;
+  ncclResult_t ar;
+  CK_NCCL(ncclCommGetAsyncError(c->comm, &ar));
+  if (ar != ncclSuccess) return fail(HDP_ERR_NCCL, "NCCL async error: %s", ncclGetErrorString(ar));
+  return HDP_OK;
+}
+
+ncclDataType_t gtype(const hdp_ctx* c) { return c->gf32 ? ncclFloat : ncclHalf; }
+ncclDataType_t wtype(const hdp_ctx* c) { return c->f32 ? ncclFloat : ncclHalf; }
+
+}  // namespace
+
+// ====================================================================== C-ABI
+extern "C" {
+
+const char* hdp_last_error(void) { return g_err.c_str(); }
+
+int hdp_nccl_unique_id(unsigned char uid[HDP_UID_BYTES]) {
+  if (!uid) return fail(HDP_ERR_ARG, "null uid");
+  static_assert(sizeof(ncclUniqueId) == HDP_UID_BYTES, "uid size");
+  ncclUniqueId id;
+  CK_NCCL(ncclGetUniqueId(&id));
+  memcpy(uid, &id, HDP_UID_BYTES);
+  return HDP_OK;
+}
+
+int hdp_init(int world, int rank, const unsigned char* uid, int device, hdp_ctx** out) {
+  if (!out || world < 1 || rank < 0 || rank >= world || device < 0)
+    return fail(HDP_ERR_ARG, "hdp_init: bad arguments (world %d rank %d device %d)", world, rank, device);
+  if (world > 1 && !uid) return fail(HDP_ERR_ARG, "hdp_init: world > 1 needs a NCCL unique id");
+  CK_CUDA(cudaSetDevice(device));
+  std::unique_ptr<hdp_ctx> c(new hdp_ctx());
+  c->world = world;
+  c->rank = rank;
+  c->device = device;
+  if (world > 1) {
+    ncclUniqueId id;
+    memcpy(&id, uid, HDP_UID_BYTES);
+    CK_NCCL(ncclCommInitRank(&c->comm, world, id, rank));
+  }
+  *out = c.release();
+  return HDP_OK;
+}
+
+int hdp_destroy(hdp_ctx* c) {
+  if (!c) return HDP_OK;
+  cudaSetDevice(c->device);
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+  for (auto ev : c->ev_bucket) cudaEventDestroy(ev);
+  if (c->ev_done) cudaEventDestroy(c->ev_done);
+  if (c->ev_count) cudaEventDestroy(c->ev_count);
+  if (c->cap) cudaStreamDestroy(c->cap);
+  if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
+  if (c->count_host) cudaFreeHost(c->count_host);
+  if (c->comm) ncclCommDestroy(c->comm);
+  delete c;
+  return HDP_OK;
+}
+
+int hdp_configure(hdp_ctx* c, const hdp_model_desc* desc, hdp_sizes* out) {
+  if (!c || !desc) return fail(HDP_ERR_ARG, "null argument");
+  if (c->bound) return fail(HDP_ERR_STATE, "already bound");
+  const hdp_model_desc& d = *desc;
+  if (d.n_layers < 0 || d.math < 0 || d.math > 1 || d.wire < 0 || d.wire > 2 || d.optimizer < 0 ||
+      d.optimizer > 1 || d.sim_workers < 1)
+    return fail(HDP_ERR_ARG, "bad enum / layer count");
+  if (d.sim_workers > 1 && c->world > 1) return fail(HDP_ERR_ARG, "sim_workers > 1 requires world == 1");
+  if (d.sim_workers > 16) return fail(HDP_ERR_ARG, "sim_workers > 16");
+  if (d.n_layers == 0) {
+    if (d.flat_params <= 0) return fail(HDP_ERR_ARG, "flat model needs flat_params > 0");
+  } else {
+    if (d.hidden <= 0 || d.max_batch <= 0 || d.max_seq <= 0 || d.fc_hidden < 0)
+      return fail(HDP_ERR_ARG, "hidden / max_batch / max_seq must be positive");
+    if (d.vocab > 0 ? d.embed_dim <= 0 : d.input_dim <= 0) return fail(HDP_ERR_ARG, "input width must be positive");
+    if (d.head_last_step && d.fc_hidden > 0) return fail(HDP_ERR_UNSUPPORTED, "last-step head with FC layer");
+    if ((long)d.max_batch * d.max_seq > (1L << 30)) return fail(HDP_ERR_ARG, "batch*seq too large");
+  }
+  if (d.math == HDP_MATH_FP32 && d.wire == HDP_WIRE_FP16_NCCLSUM)
+    return fail(HDP_ERR_ARG, "FP32 math cannot use the fp16 NCCL-sum wire");
+  c->d = d;
+  c->f32 = d.math == HDP_MATH_FP32;
+  c->gf32 = c->f32 || d.wire == HDP_WIRE_FP32;
+  c->esz = c->f32 ? 4 : 2;
+  c->gsz = c->gf32 ? 4 : 2;
+  c->nslots = d.sim_workers;
+  build_layout(c);
+  carve(c, nullptr);
+  c->configured = true;
+  if (out) {
+    out->n_params = c->n_params;
+    out->n_params_padded = c->P;
+    out->n_buckets = (long long)c->buckets.size();
+    out->arena_bytes = (long long)c->arena_bytes;
+  }
+  return HDP_OK;
+}
+
+int hdp_bind(hdp_ctx* c, void* arena, long long bytes) {
+  if (!c || !arena) return fail(HDP_ERR_ARG, "null argument");
+  if (!c->configured) return fail(HDP_ERR_STATE, "configure first");
+  if (c->bound) return fail(HDP_ERR_STATE, "already bound");
+  if ((size_t)bytes < c->arena_bytes) return fail(HDP_ERR_ARG, "arena too small: %lld < %zu", bytes, c->arena_bytes);
+  if (reinterpret_cast<uintptr_t>(arena) & 255) return fail(HDP_ERR_ARG, "arena must be 256-byte aligned");
+  CK_CUDA(cudaSetDevice(c->device));
+  c->arena = (char*)arena;
+  carve(c, c->arena);
+  CK_CUDA(cudaMemset(c->arena, 0, c->arena_bytes));
+  CK_CUDA(hdp::gemm_init());
+  CK_CUDA(cudaStreamCreateWithFlags(&c->cap, cudaStreamNonBlocking));
+  CK_CUDA(cudaStreamCreateWithFlags(&c->comm_stream, cudaStreamNonBlocking));
+  CK_CUDA(cudaEventCreateWithFlags(&c->ev_done, cudaEventDisableTiming));
+  CK_CUDA(cudaEventCreateWithFlags(&c->ev_count, cudaEventDisableTiming));
+  c->ev_bucket.resize(c->buckets.size());
+  for (auto& ev : c->ev_bucket) CK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CK_CUDA(cudaMallocHost(&c->count_host, sizeof(int)));
+  *c->count_host = 0;
+  c->st.assign(c->nslots, SlotState{});
+  CK_CUDA(cudaDeviceSynchronize());
+  c->bound = true;
+  return HDP_OK;
+}
+
+int hdp_num_blocks(const hdp_ctx* c) { return c ? (int)c->blocks.size() : 0; }
+
+int hdp_param_block(const hdp_ctx* c, int i, hdp_block* out) {
+  if (!c || !out || !c->configured || i < 0 || i >= (int)c->blocks.size()) return fail(HDP_ERR_ARG, "bad block index");
+  const Block& b = c->blocks[i];
+  memset(out, 0, sizeof *out);
+  snprintf(out->name, sizeof out->name, "%s", b.name.c_str());
+  out->canon_offset = b.canon_off;
+  out->rows = b.rows;
+  out->cols = b.cols;
+  out->dev_offset = b.dev_off;
+  out->dev_rows = b.dev_rows;
+  out->dev_cols = b.dev_cols;
+  out->bucket = b.bucket;
+  return HDP_OK;
+}
+
+namespace {
+void canon_to_dev(const hdp_ctx* c, const float* in, std::vector<float>& out) {
+  out.assign(c->P, 0.f);
+  for (const Block& b : c->blocks)
+    for (long r = 0; r < b.rows; ++r)
+      for (long k = 0; k < b.cols; ++k) out[b.dev_off + dev_index(c, b, r, k)] = in[b.canon_off + r * b.cols + k];
+}
+void dev_to_canon(const hdp_ctx* c, const std::vector<float>& in, float* out) {
+  for (const Block& b : c->blocks)
+    for (long r = 0; r < b.rows; ++r)
+      for (long k = 0; k < b.cols; ++k) out[b.canon_off + r * b.cols + k] = in[b.dev_off + dev_index(c, b, r, k)];
+}
+}  // namespace
+
+int hdp_load_params(hdp_ctx* c, const float* params, int root) {
+  CK(check_ready(c));
+  if (root < 0 || root >= c->world) return fail(HDP_ERR_ARG, "bad root");
+  if (c->rank == root && !params) return fail(HDP_ERR_ARG, "root needs params");
+  CK_CUDA(cudaSetDevice(c->device));
+  std::vector<float> host;
+  if (c->rank == root) canon_to_dev(c, params, host);
+  float* buf = nullptr;
+  CK_CUDA(cudaMalloc(&buf, c->P * sizeof(float)));
+  std::unique_ptr<float, void (*)(float*)> guard(buf, [](float* p) { cudaFree(p); });
+  if (c->rank == root) CK_CUDA(cudaMemcpy(buf, host.data(), c->P * sizeof(float), cudaMemcpyHostToDevice));
+  cudaStream_t s = c->comm_stream;
+  if (c->world > 1) {
+    CK_NCCL(ncclBroadcast(buf, buf, c->P, ncclFloat, root, c->comm, s));  // PAPER.md:92 step 2
+  }
+  // master shard <- owned slices; optimizer state <- 0; working copy <- params
+  for (const Bucket& bk : c->buckets)
+    CK_CUDA(cudaMemcpyAsync(c->master + bk.moff, buf + bk.off + (long)c->rank * bk.shard, bk.shard * 4,
+                            cudaMemcpyDeviceToDevice, s));
+  CK_CUDA(cudaMemsetAsync(c->s1, 0, c->M_own * 4, s));
+  if (c->s2) CK_CUDA(cudaMemsetAsync(c->s2, 0, c->M_own * 4, s));
+  // working copy (R1): fp32 -> fp16 RNE in mixed mode (not on the hot path)
+  if (c->f32) {
+    CK_CUDA(cudaMemcpyAsync(c->w, buf, c->P * 4, cudaMemcpyDeviceToDevice, s));
+  } else {
+    std::vector<__half> h16(c->P);
+    std::vector<float> full(c->P);
+    CK_CUDA(cudaMemcpyAsync(full.data(), buf, c->P * 4, cudaMemcpyDeviceToHost, s));
+    CK_CUDA(cudaStreamSynchronize(s));
+    for (long i = 0; i < c->P; ++i) h16[i] = __float2half_rn(full[i]);
+    CK_CUDA(cudaMemcpyAsync(c->w, h16.data(), c->P * 2, cudaMemcpyHostToDevice, s));
+  }
+  CK_CUDA(cudaStreamSynchronize(s));
+  c->loaded = true;
+  c->poisoned = false;
+  c->count_pending = false;
+  c->adam_k = 0;
+  for (auto& st : c->st) st = SlotState{};
+  return HDP_OK;
+}
+
+int hdp_gather_master(hdp_ctx* c, float* out) {
+  CK(check_ready(c));
+  if (!out) return fail(HDP_ERR_ARG, "null output");
+  CK_CUDA(cudaSetDevice(c->device));
+  float* buf = nullptr;
+  CK_CUDA(cudaMalloc(&buf, c->P * sizeof(float)));
+  std::unique_ptr<float, void (*)(float*)> guard(buf, [](float* p) { cudaFree(p); });
+  cudaStream_t s = c->comm_stream;
+  for (const Bucket& bk : c->buckets) {
+    if (c->world > 1)
+      CK_NCCL(ncclAllGather(c->master + bk.moff, buf + bk.off, bk.shard, ncclFloat, c->comm, s));
+    else
+      CK_CUDA(cudaMemcpyAsync(buf + bk.off, c->master + bk.moff, bk.shard * 4, cudaMemcpyDeviceToDevice, s));
+  }
+  std::vector<float> host(c->P);
+  CK_CUDA(cudaMemcpyAsync(host.data(), buf, c->P * 4, cudaMemcpyDeviceToHost, s));
+  CK_CUDA(cudaStreamSynchronize(s));
+  dev_to_canon(c, host, out);
+  return HDP_OK;
+}
+
+namespace {
+int read_vec(hdp_ctx* c, const char* src, bool is_f32, float* out) {
+  CK_CUDA(cudaSetDevice(c->device));
+  CK_CUDA(cudaDeviceSynchronize());
+  std::vector<float> host(c->P);
+  if (is_f32) {
+    CK_CUDA(cudaMemcpy(host.data(), src, c->P * 4, cudaMemcpyDeviceToHost));
+  } else {
+    std::vector<__half> h(c->P);
+    CK_CUDA(cudaMemcpy(h.data(), src, c->P * 2, cudaMemcpyDeviceToHost));
+    for (long i = 0; i < c->P; ++i) host[i] = __half2float(h[i]);
+  }
+  dev_to_canon(c, host, out);
+  return HDP_OK;
+}
+}  // namespace
+
+int hdp_read_weights(hdp_ctx* c, float* out) {
+  CK(check_ready(c));
+  if (!out) return fail(HDP_ERR_ARG, "null output");
+  return read_vec(c, c->w, c->f32, out);
+}
+
+int hdp_read_grads(hdp_ctx* c, int slot, float* out) {
+  CK(check_ready(c));
+  if (!out || slot < 0 || slot >= c->nslots) return fail(HDP_ERR_ARG, "bad slot / output");
+  return read_vec(c, c->grads + (long)slot * c->P * c->gsz, c->gf32, out);
+}
+
+int hdp_set_lr_schedule(hdp_ctx* c, double lambda0, double gamma, double n_half, double max_eff_lr,
+                        double momentum, double b1, double b2, double eps) {
+  if (!c) return fail(HDP_ERR_ARG, "null context");
+  if (!(lambda0 > 0) || !(gamma > 0 && gamma <= 1) || !(n_half > 0) || !(max_eff_lr > 0) ||
+      !(momentum >= 0 && momentum < 1) || !(b1 >= 0 && b1 < 1) || !(b2 >= 0 && b2 < 1) || !(eps > 0))
+    return fail(HDP_ERR_ARG, "bad schedule / optimizer constants");
+  c->lam0 = lambda0;
+  c->gamma = gamma;
+  c->n_half = n_half;
+  c->max_eff = max_eff_lr;
+  c->mom = momentum;
+  c->b1 = b1;
+  c->b2 = b2;
+  c->eps = eps;
+  c->lr_set = true;
+  return HDP_OK;
+}
+
+double hdp_lr(const hdp_ctx* c, int epoch) {
+  if (!c || !c->lr_set || !c->configured || epoch < 0) return -1.0;
+  return sched(c, epoch);
+}
+
+int hdp_set_loss_scale(hdp_ctx* c, float alpha) {
+  if (!c) return fail(HDP_ERR_ARG, "null context");
+  if (!(alpha > 0) || !std::isfinite(alpha)) return fail(HDP_ERR_ARG, "alpha must be a positive finite number");
+  if (c->alpha != alpha) {  // alpha is baked into captured forward graphs
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+  }
+  c->alpha = alpha;
+  return HDP_OK;
+}
+
+int hdp_lstm_forward(hdp_ctx* c, const void* x, const void* targets, int B, int T, int slot, float* y_out,
+                     float* loss_out, void* stream) {
+  CK(check_ready(c));
+  if (c->d.n_layers == 0) return fail(HDP_ERR_UNSUPPORTED, "flat model has no forward");
+  if (!x || !targets) return fail(HDP_ERR_ARG, "null input");
+  if (slot < 0 || slot >= c->nslots) return fail(HDP_ERR_ARG, "slot %d out of range", slot);
+  if (B < 1 || B > c->d.max_batch || T < 1 || T > c->d.max_seq)
+    return fail(HDP_ERR_ARG, "B=%d T=%d outside [1,%d]x[1,%d]", B, T, c->d.max_batch, c->d.max_seq);
+  if (!c->loaded) return fail(HDP_ERR_STATE, "parameters not loaded");
+  if (c->poisoned) return fail(HDP_ERR_STATE, "context poisoned by non-finite gradients; reload parameters");
+  cudaStream_t s = (cudaStream_t)stream;
+  hdp_ctx::Slot& S = c->slot[slot];
+  const long in_bytes = c->d.vocab > 0 ? 4 : (long)c->d.input_dim * c->esz;
+  CK_CUDA(cudaMemcpyAsync(S.stage_x, x, (long)B * T * in_bytes, cudaMemcpyDefault, s));
+  const long nt = c->d.head_last_step ? B : (long)B * T;
+  CK_CUDA(cudaMemcpyAsync(S.stage_t, targets, nt, cudaMemcpyDefault, s));
+  CK(run_graph(c, slot, B, T, -1, s));
+  if (loss_out) CK_CUDA(cudaMemcpyAsync(loss_out, S.loss, 4, cudaMemcpyDefault, s));
+  if (y_out) CK_CUDA(cudaMemcpyAsync(y_out, S.y, nt * 4, cudaMemcpyDefault, s));
+  c->st[slot].fwd = true;
+  c->st[slot].bwd = false;
+  c->st[slot].B = B;
+  c->st[slot].T = T;
+  return HDP_OK;
+}
+
+int hdp_lstm_backward(hdp_ctx* c, int slot, void* stream) {
+  CK(check_ready(c));
+  if (slot < 0 || slot >= c->nslots) return fail(HDP_ERR_ARG, "slot %d out of range", slot);
+  if (!c->st[slot].fwd) return fail(HDP_ERR_STATE, "backward without forward on slot %d", slot);
+  if (c->poisoned) return fail(HDP_ERR_STATE, "context poisoned");
+  cudaStream_t s = (cudaStream_t)stream;
+  const int B = c->st[slot].B, T = c->st[slot].T;
+  for (int seg = 0; seg < nsegs(c); ++seg) {
+    CK(run_graph(c, slot, B, T, seg, s));
+    // bucket `seg` (head, then layers top-down) is complete: the exchange may start
+    CK_CUDA(cudaEventRecord(c->ev_bucket[seg], s));
+  }
+  if (c->d.vocab > 0) CK_CUDA(cudaEventRecord(c->ev_bucket[nsegs(c)], s));  // embedding (after layer 0)
+  c->st[slot].bwd = true;
+  return HDP_OK;
+}
+
+int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_host) {
+  CK(check_ready(c));
+  if (!c->lr_set) return fail(HDP_ERR_STATE, "learning-rate schedule not set");
+  if (epoch < 0) return fail(HDP_ERR_ARG, "epoch < 0");
+  if (!c->loaded) return fail(HDP_ERR_STATE, "parameters not loaded");
+  if (c->poisoned) return fail(HDP_ERR_STATE, "context poisoned");
+  if (c->d.n_layers > 0)
+    for (int sl = 0; sl < c->nslots; ++sl)
+      if (!c->st[sl].bwd) return fail(HDP_ERR_STATE, "slot %d has no backward", sl);
+  CK_CUDA(cudaSetDevice(c->device));
+  // deferred report of the previous step's count (not synchronised then)
+  if (c->count_pending) {
+    CK_CUDA(cudaEventSynchronize(c->ev_count));
+    c->count_pending = false;
+    if (*c->count_host > 0) {
+      c->poisoned = true;
+      return fail(HDP_ERR_NONFINITE, "%d non-finite gradient values in the previous step (loss scale %g)",
+                  *c->count_host, (double)c->alpha);
+    }
+  }
+  cudaStream_t s = (cudaStream_t)stream;
+  const int N = c->Nw();
+  const double lam = sched(c, epoch);
+  hdp::UpdateArgs a;
+  a.inv_scale = (float)(1.0 / ((double)N * (double)c->alpha));  // R14
+  a.lam = (float)lam;                                            // R15a
+  a.mom = (float)c->mom;
+  const int opt = c->d.optimizer;
+  if (opt == HDP_OPT_ADAM) {
+    const long k = ++c->adam_k;
+    a.b1 = (float)c->b1;
+    a.omb1 = (float)(1.0 - c->b1);
+    a.b2 = (float)c->b2;
+    a.omb2 = (float)(1.0 - c->b2);
+    a.c1 = (float)(1.0 / (1.0 - std::pow(c->b1, (double)k)));
+    a.c2 = (float)(1.0 / (1.0 - std::pow(c->b2, (double)k)));
+    a.eps = (float)c->eps;
+  }
+  a.nonfinite = c->status;
+  cudaStream_t cs = c->world > 1 ? c->comm_stream : s;
+  if (c->world > 1) {
+    // the comm stream must see everything enqueued on `s` so far (incl. the
+    // flat-model gradients written by the caller) before bucket 0
+    CK_CUDA(cudaEventRecord(c->ev_done, s));
+    CK_CUDA(cudaStreamWaitEvent(cs, c->ev_done, 0));
+  }
+  CK_CUDA(cudaMemsetAsync(c->status, 0, sizeof(int), cs));
+  for (size_t bi = 0; bi < c->buckets.size(); ++bi) {
+    const Bucket& bk = c->buckets[bi];
+    if (c->world > 1 && c->d.n_layers > 0) CK_CUDA(cudaStreamWaitEvent(cs, c->ev_bucket[bi], 0));
+    a.count = bk.shard;
+    a.W = c->master + bk.moff;
+    a.S1 = c->s1 + bk.moff;
+    a.S2 = c->s2 ? c->s2 + bk.moff : nullptr;
+    a.w16 = c->f32 ? nullptr : (__half*)(c->w + (bk.off + (long)c->rank * bk.shard) * 2);
+    a.w32 = c->f32 ? (float*)(c->w + (bk.off + (long)c->rank * bk.shard) * 4) : nullptr;
+    int grad_f32 = c->gf32;
+    if (c->world == 1) {
+      a.g = c->grads + bk.off * c->gsz;  // slot r at + r*P
+      a.g_stride = c->P;
+      a.nsrc = c->nslots;
+    } else if (c->d.wire == HDP_WIRE_FP16_A2A) {
+      // A9: owner j receives every rank's shard j, rank-ordered
+      CK_NCCL(ncclAlltoAll(c->grads + bk.off * c->gsz, c->recv, bk.shard, gtype(c), c->comm, cs));
+      a.g = c->recv;
+      a.g_stride = bk.shard;
+      a.nsrc = c->world;
+    } else {
+      // NCCL-native reduction (fp16 sum, or fp32 wire)
+      CK_NCCL(ncclReduceScatter(c->grads + bk.off * c->gsz, c->recv, bk.shard, gtype(c), ncclSum, c->comm, cs));
+      a.g = c->recv;
+      a.g_stride = bk.shard;
+      a.nsrc = 1;
+    }
+    CK_CUDA(hdp::launch_avg_update(a, grad_f32, opt, cs));  // A10 / K11
+    if (c->world > 1) {                                     // A11: step 6 "broadcast"
+      char* mine = c->w + (bk.off + (long)c->rank * bk.shard) * c->esz;
+      CK_NCCL(ncclAllGather(mine, c->w + bk.off * c->esz, bk.shard, wtype(c), c->comm, cs));
+    }
+  }
+  if (c->world > 1) CK_NCCL(ncclAllReduce(c->status, c->status, 1, ncclInt32, ncclSum, c->comm, cs));
+  CK_CUDA(cudaMemcpyAsync(c->count_host, c->status, sizeof(int), cudaMemcpyDeviceToHost, cs));
+  CK_CUDA(cudaEventRecord(c->ev_count, cs));
+  if (c->world > 1) {
+    CK_CUDA(cudaEventRecord(c->ev_done, cs));
+    CK_CUDA(cudaStreamWaitEvent(s, c->ev_done, 0));  // next forward sees the new weights
+  }
+  for (auto& st : c->st) st.bwd = false;
+  if (nonfinite_host) {
+    CK_CUDA(cudaEventSynchronize(c->ev_count));
+    *nonfinite_host = *c->count_host;
+    if (*c->count_host > 0) {
+      c->poisoned = true;
+      return fail(HDP_ERR_NONFINITE, "%d non-finite gradient values (loss scale %g)", *c->count_host,
+                  (double)c->alpha);
+    }
+  } else {
+    c->count_pending = true;
+  }
+  return HDP_OK;
+}
+
+void* hdp_weights_ptr(hdp_ctx* c) { return c && c->bound ? c->w : nullptr; }
+void* hdp_grads_ptr(hdp_ctx* c, int slot) {
+  return c && c->bound && slot >= 0 && slot < c->nslots ? c->grads + (long)slot * c->P * c->gsz : nullptr;
+}
+void* hdp_master_ptr(hdp_ctx* c) { return c && c->bound ? c->master : nullptr; }
+
+int hdp_fused_avg_update(const void* grads, long long src_stride, int nsrc, int grads_f32, long long count, float* W,
+                         float* S1, float* S2, void* w16, float* w32, float inv_scale, float lr, float momentum,
+                         int optimizer, const double* adam, int* nonfinite_dev, void* stream) {
+  if (!grads || !W || !S1 || nsrc < 1 || count < 0 || (optimizer == HDP_OPT_ADAM && (!S2 || !adam)) ||
+      optimizer < 0 || optimizer > 1)
+    return fail(HDP_ERR_ARG, "hdp_fused_avg_update: bad arguments");
+  hdp::UpdateArgs a;
+  a.g = grads;
+  a.g_stride = src_stride;
+  a.nsrc = nsrc;
+  a.count = count;
+  a.W = W;
+  a.S1 = S1;
+  a.S2 = S2;
+  a.w16 = (__half*)w16;
+  a.w32 = w32;
+  a.inv_scale = inv_scale;
+  a.lam = lr;
+  a.mom = momentum;
+  a.nonfinite = nonfinite_dev;
+  if (optimizer == HDP_OPT_ADAM) {
+    const double b1 = adam[0], b2 = adam[1], eps = adam[2], k = adam[3];
+    a.b1 = (float)b1;
+    a.omb1 = (float)(1.0 - b1);
+    a.b2 = (float)b2;
+    a.omb2 = (float)(1.0 - b2);
+    a.c1 = (float)(1.0 / (1.0 - std::pow(b1, k)));
+    a.c2 = (float)(1.0 / (1.0 - std::pow(b2, k)));
+    a.eps = (float)eps;
+  }
+  const bool vec_ok = (count % 8 == 0) && (src_stride % 8 == 0) &&
+                      !((uintptr_t)grads & 15) && !((uintptr_t)W & 15) && !((uintptr_t)S1 & 15) &&
+                      !((uintptr_t)S2 & 15) && !((uintptr_t)w16 & 15) && !((uintptr_t)w32 & 15);
+  if (!vec_ok) return fail(HDP_ERR_ARG, "hdp_fused_avg_update: needs count %% 8 == 0 and 16-byte aligned buffers");
+  CK_CUDA(hdp::launch_avg_update(a, grads_f32, optimizer, (cudaStream_t)stream));
+  return HDP_OK;
+}
+
+int hdp_gemm_f16(const void* A, long long lda, int a_mn, const void* B, long long ldb, int b_mn, int M, int N, int K,
+                 void* C, long long ldc, int c_mode, const float* bias, int bias_on_m, int relu, int accumulate,
+                 float* ws, long long ws_floats, int bn, int splits, void* stream) {
+  if (!A || !B || !C || M <= 0 || N <= 0 || K <= 0 || c_mode < 0 || c_mode > 2)
+    return fail(HDP_ERR_ARG, "hdp_gemm_f16: bad arguments");
+  hdp::Epilogue e;
+  e.mode = c_mode;
+  e.out = C;
+  e.ldo = ldc;
+  e.bias = bias;
+  e.bias_on_m = bias_on_m;
+  e.relu = relu;
+  e.accumulate = accumulate;
+  hdp::GemmPlan p;
+  if (hdp::gemm_plan_tc(&p, (const __half*)A, lda, a_mn, (const __half*)B, ldb, b_mn, M, N, K, e, ws,
+                        ws ? (size_t)ws_floats : 0, bn, splits))
+    return fail(HDP_ERR_ARG, "hdp_gemm_f16: %s", hdp::gemm_last_error());
+  static bool inited = false;
+  if (!inited) {
+    CK_CUDA(hdp::gemm_init());
+    inited = true;
+  }
+  CK_CUDA(hdp::gemm_run(p, (cudaStream_t)stream));
+  return HDP_OK;
+}
+
+int hdp_gemm_f32(const float* A, long long lda, int a_mn, const float* B, long long ldb, int b_mn, int M, int N, int K,
+                 float* C, long long ldc, int c_mode, const float* bias, int bias_on_m, int relu, int accumulate,
+                 void* stream) {
+  if (!A || !B || !C || M <= 0 || N <= 0 || K <= 0 || c_mode < 0 || c_mode > 1)
+    return fail(HDP_ERR_ARG, "hdp_gemm_f32: bad arguments");
+  hdp::Epilogue e;
+  e.mode = c_mode;
+  e.out = C;
+  e.ldo = ldc;
+  e.bias = bias;
+  e.bias_on_m = bias_on_m;
+  e.relu = relu;
+  e.accumulate = accumulate;
+  hdp::GemmPlan p;
+  if (hdp::gemm_plan_f32(&p, A, lda, a_mn, B, ldb, b_mn, M, N, K, e))
+    return fail(HDP_ERR_ARG, "hdp_gemm_f32: %s", hdp::gemm_last_error());
+  CK_CUDA(hdp::gemm_run(p, (cudaStream_t)stream));
+  return HDP_OK;
+}
+
+}  // extern "C"

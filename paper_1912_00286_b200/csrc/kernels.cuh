@@ -1,0 +1,75 @@
+// Launchers for the non-GEMM kernels of the LSTM training step.
+// Element type of activations / weights / gradients: fp16 in mixed mode,
+// fp32 in FP32 mode (selected by an `f32` flag); cell state, gate
+// pre-activations and all back-propagated hidden gradients are fp32.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+#include <cstdint>
+
+namespace hdp {
+
+// ---------------------------------------------------------------- K11
+struct UpdateArgs {
+  const void* g = nullptr;  // contribution r at g + r*g_stride (elements), rank order
+  long g_stride = 0;
+  int nsrc = 1;
+  long count = 0;
+  float* W = nullptr;       // fp32 master shard
+  float* S1 = nullptr;      // momentum H (SGD-m) or first moment (Adam)
+  float* S2 = nullptr;      // second moment (Adam)
+  __half* w16 = nullptr;    // fp16 working copy (mixed mode), nullable
+  float* w32 = nullptr;     // fp32 working copy (FP32 mode), nullable
+  float inv_scale = 1.f, lam = 0.f, mom = 0.f;
+  float b1 = 0.9f, omb1 = 0.1f, b2 = 0.999f, omb2 = 0.001f, c1 = 1.f, c2 = 1.f, eps = 1e-8f;
+  int* nonfinite = nullptr;
+};
+cudaError_t launch_avg_update(const UpdateArgs& a, int grad_is_f32, int optimizer, cudaStream_t s);
+
+// ---------------------------------------------------------------- input
+// x [B][T][I] (fp16 or fp32)  ->  X0 [T][B][Ip] (time-major, zero padded)
+cudaError_t launch_pack_input(const void* x, int x_f32, int B, int T, int I, int Ip, void* X0, int f32,
+                              cudaStream_t s);
+// tokens [B][T] -> X0[t][b][:] = E[tok[b][t]][:]  (K10 gather)
+cudaError_t launch_embed_gather(const int32_t* tok, int B, int T, const void* E, int Ep, void* X0, int f32,
+                                cudaStream_t s);
+
+// ---------------------------------------------------------------- cell (K3 / K6)
+// gate rows interleaved per unit: row 4*j + {i,f,g,o}
+cudaError_t launch_cell_fwd(int f32, const float* Gx_t, const float* Gh, const float* c_prev, void* gates_t,
+                            float* c_t, void* h_t, int B, int hp, cudaStream_t s);
+cudaError_t launch_cell_bwd(int f32, const float* dHa_t, const float* dh_rec, const void* gates_t,
+                            const float* c_t, const float* c_prev, float* dc, void* dA_t, int B, int hp,
+                            int first, cudaStream_t s);
+
+// ---------------------------------------------------------------- head (K4 / K5)
+// y[r] = sum_k Z[r][k] wo[k] + bo; hinge (Eq. 6) -> dy[r], per-block partial sums.
+// tgt_mode 0: row r = t*B + b <-> tgt[b*T + t];  1: row r = b <-> tgt[b]
+int head_partials_count(int rows);
+cudaError_t launch_head_out(int f32, const void* Z, int rows, int Kd, long ldz, const void* wo, const void* bo,
+                            const int8_t* tgt, int tgt_mode, int B, int T, float alpha, float inv_terms, float* y,
+                            float* dy, float* partials, cudaStream_t s);
+// loss = (sum of partials) * inv_terms   (unscaled mean hinge), deterministic
+cudaError_t launch_loss_final(const float* partials, int n, float inv_terms, float* loss, cudaStream_t s);
+// dz[r][f] = (Z[r][f] > 0) ? dy[r]*wo[f] : 0   (ReLU', R9)
+cudaError_t launch_relu_dz(int f32, const float* dy, const void* wo, const void* Z, void* dz, int rows, int Fp,
+                           cudaStream_t s);
+// dH[r][j] = dy[r] * wo[j]
+cudaError_t launch_outer(int f32, const float* dy, const void* wo, float* dH, int rows, int hp, cudaStream_t s);
+
+// ---------------------------------------------------------------- reductions
+// out[c] = sum_r X[r*ldx + c] * (w ? w[r] : 1)   over rows in a fixed order.
+// out is fp16 (RNE) when out_f32 == 0, else fp32.  partials: RS*cols floats.
+size_t colreduce_partials_floats(int rows, int cols);
+cudaError_t launch_colreduce(int x_f32, const void* X, long ldx, int rows, int cols, const float* w,
+                             float* partials, int out_f32, void* out, cudaStream_t s);
+
+// ---------------------------------------------------------------- embedding backward (K10)
+size_t embed_sort_temp_bytes(int n);
+// dE[v][:] = sum over positions p (ascending, p = t*B+b) with tok = v of dX0[p][:]
+cudaError_t launch_embed_backward(const int32_t* tok, int B, int T, int vocab, const float* dX0, int Ep,
+                                  int32_t* keys_in, int32_t* keys_out, int32_t* vals_in, int32_t* vals_out,
+                                  void* sort_temp, size_t sort_temp_bytes, void* dE, int out_f32,
+                                  cudaStream_t s);
+
+}  // namespace hdp

@@ -1,0 +1,406 @@
+// Elementwise / reduction kernels of the LSTM step (everything that is not a
+// gate contraction): input packing, the fused LSTM cell forward (K3) and
+// backward (K6), the head (K4/K5: Eq. 6 hinge x alpha), deterministic column
+// reductions (bias / head gradients) and the embedding gather / scatter (K10).
+//
+// Cell equations (reading Q1, gate order i,f,g,o):
+//   i,f,o = sigma(a), g = tanh(a);  c_t = f c_{t-1} + i g;  h_t = o tanh(c_t)
+// Backward (BPTT):
+//   dh = dH_above + dh_rec;  dc += dh o (1 - tanh^2 c_t)
+//   dA = [dc g i(1-i), dc c_{t-1} f(1-f), dc i (1-g^2), dh tanh(c_t) o(1-o)]
+//   dc_{t-1} = dc f
+#include <cub/device/device_radix_sort.cuh>
+#include <cuda_fp16.h>
+
+#include "kernels.cuh"
+
+namespace hdp {
+namespace {
+
+template <typename T>
+__device__ __forceinline__ float ld(const T* p, long i);
+template <>
+__device__ __forceinline__ float ld<float>(const float* p, long i) { return p[i]; }
+template <>
+__device__ __forceinline__ float ld<__half>(const __half* p, long i) { return __half2float(p[i]); }
+
+template <typename T>
+__device__ __forceinline__ T cvt(float v);
+template <>
+__device__ __forceinline__ float cvt<float>(float v) { return v; }
+template <>
+__device__ __forceinline__ __half cvt<__half>(float v) { return __float2half_rn(v); }
+
+__device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + expf(-x)); }
+
+// 4 gate values of one unit: fp16 -> one 8-byte access, fp32 -> one 16-byte access
+__device__ __forceinline__ void st4(__half* p, float a, float b, float c, float d) {
+  __align__(8) __half2 v[2] = {__halves2half2(__float2half_rn(a), __float2half_rn(b)),
+                               __halves2half2(__float2half_rn(c), __float2half_rn(d))};
+  *reinterpret_cast<uint2*>(p) = *reinterpret_cast<const uint2*>(v);
+}
+__device__ __forceinline__ void st4(float* p, float a, float b, float c, float d) {
+  *reinterpret_cast<float4*>(p) = make_float4(a, b, c, d);
+}
+__device__ __forceinline__ float4 ld4(const __half* p) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const float2 x = __half22float2(*reinterpret_cast<const __half2*>(&u.x));
+  const float2 y = __half22float2(*reinterpret_cast<const __half2*>(&u.y));
+  return make_float4(x.x, x.y, y.x, y.y);
+}
+__device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+
+// ---------------------------------------------------------------- input
+template <typename XT, typename T>
+__global__ void pack_input_kernel(const XT* __restrict__ x, int B, int Tn, int I, int Ip, T* __restrict__ X0) {
+  const long total = (long)Tn * B * Ip;
+  for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
+    const int k = (int)(idx % Ip);
+    const long tb = idx / Ip;
+    const int b = (int)(tb % B), t = (int)(tb / B);
+    const float v = k < I ? ld<XT>(x, ((long)b * Tn + t) * I + k) : 0.f;
+    X0[idx] = cvt<T>(v);
+  }
+}
+
+template <typename T>
+__global__ void embed_gather_kernel(const int32_t* __restrict__ tok, int B, int Tn, const T* __restrict__ E,
+                                    int Ep, T* __restrict__ X0) {
+  // one warp per position p = t*B + b
+  const long p = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (p >= (long)Tn * B) return;
+  const int b = (int)(p % B), t = (int)(p / B);
+  const long row = tok[(long)b * Tn + t];
+  for (int k = lane; k < Ep; k += 32) X0[p * Ep + k] = E[row * Ep + k];
+}
+
+// ---------------------------------------------------------------- cell
+template <typename T>
+__global__ void cell_fwd_kernel(const float* __restrict__ Gx, const float* __restrict__ Gh,
+                                const float* __restrict__ c_prev, T* __restrict__ gates, float* __restrict__ c_t,
+                                T* __restrict__ h_t, int n) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  float4 a = reinterpret_cast<const float4*>(Gx)[idx];
+  if (Gh) {
+    const float4 r = reinterpret_cast<const float4*>(Gh)[idx];
+    a.x += r.x; a.y += r.y; a.z += r.z; a.w += r.w;
+  }
+  const float i = sigmoidf_(a.x), f = sigmoidf_(a.y), g = tanhf(a.z), o = sigmoidf_(a.w);
+  const float cp = c_prev ? c_prev[idx] : 0.f;
+  const float c = f * cp + i * g;
+  const float h = o * tanhf(c);
+  st4(gates + 4L * idx, i, f, g, o);  // R4: saved gates (fp16 in mixed mode)
+  c_t[idx] = c;                       // R5: fp32
+  h_t[idx] = cvt<T>(h);               // R6: fp16 in mixed mode
+}
+
+template <typename T>
+__global__ void cell_bwd_kernel(const float* __restrict__ dHa, const float* __restrict__ dh_rec,
+                                const T* __restrict__ gates, const float* __restrict__ c_t,
+                                const float* __restrict__ c_prev, float* __restrict__ dc, T* __restrict__ dA, int n,
+                                int first) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= n) return;
+  float dh = 0.f;
+  if (dHa) dh += dHa[idx];
+  if (dh_rec) dh += dh_rec[idx];
+  const float4 G = ld4(gates + 4L * idx);
+  const float i = G.x, f = G.y, g = G.z, o = G.w;
+  const float c = c_t[idx];
+  const float cp = c_prev ? c_prev[idx] : 0.f;
+  const float tc = tanhf(c);
+  const float d = (first ? 0.f : dc[idx]) + dh * o * (1.f - tc * tc);
+  st4(dA + 4L * idx, d * g * i * (1.f - i), d * cp * f * (1.f - f), d * i * (1.f - g * g),
+      dh * tc * o * (1.f - o));  // R10
+  dc[idx] = d * f;
+}
+
+// ---------------------------------------------------------------- head
+constexpr int HEAD_WARPS = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(HEAD_WARPS * 32)
+    head_out_kernel(const T* __restrict__ Z, int rows, int Kd, long ldz, const T* __restrict__ wo,
+                    const T* __restrict__ bo, const int8_t* __restrict__ tgt, int tgt_mode, int B, int Tn,
+                    float alpha, float inv_terms, float* __restrict__ y, float* __restrict__ dy,
+                    float* __restrict__ partials) {
+  __shared__ float part[HEAD_WARPS];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int r = blockIdx.x * HEAD_WARPS + warp;
+  float hinge = 0.f;
+  if (r < rows) {
+    float acc = 0.f;
+    for (int k = lane; k < Kd; k += 32) acc += ld<T>(Z, (long)r * ldz + k) * ld<T>(wo, k);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    if (lane == 0) {
+      const float yy = acc + ld<T>(bo, 0);
+      int8_t tv;
+      if (tgt_mode == 0) {
+        const int b = r % B, t = r / B;
+        tv = tgt[(long)b * Tn + t];
+      } else {
+        tv = tgt[r];
+      }
+      const float tf = (float)tv;
+      const float margin = 1.f - tf * yy;
+      y[r] = yy;
+      // d/dy alpha*mean(max(0, 1 - t y)) ; subgradient 0 at the kink (reading Q5)
+      dy[r] = margin > 0.f ? -alpha * tf * inv_terms : 0.f;
+      hinge = margin > 0.f ? margin : 0.f;
+    }
+  }
+  if (lane == 0) part[warp] = hinge;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float s = 0.f;
+    for (int w = 0; w < HEAD_WARPS; ++w) s += part[w];
+    partials[blockIdx.x] = s;
+  }
+}
+
+__global__ void loss_final_kernel(const float* __restrict__ partials, int n, float inv_terms, float* loss) {
+  __shared__ float sm[256];
+  float s = 0.f;
+  for (int i = threadIdx.x; i < n; i += 256) s += partials[i];
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) sm[threadIdx.x] += sm[threadIdx.x + w];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *loss = sm[0] * inv_terms;
+}
+
+template <typename T>
+__global__ void relu_dz_kernel(const float* __restrict__ dy, const T* __restrict__ wo, const T* __restrict__ Z,
+                               T* __restrict__ dz, int rows, int Fp) {
+  const long total = (long)rows * Fp;
+  for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
+    const int f = (int)(idx % Fp);
+    const long r = idx / Fp;
+    const float z = ld<T>(Z, idx);
+    dz[idx] = cvt<T>(z > 0.f ? dy[r] * ld<T>(wo, f) : 0.f);  // R9
+  }
+}
+
+template <typename T>
+__global__ void outer_kernel(const float* __restrict__ dy, const T* __restrict__ wo, float* __restrict__ dH,
+                             int rows, int hp) {
+  const long total = (long)rows * hp;
+  for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
+    const int j = (int)(idx % hp);
+    dH[idx] = dy[idx / hp] * ld<T>(wo, j);
+  }
+}
+
+// ---------------------------------------------------------------- deterministic column reduction
+constexpr int CR_WARPS = 8;
+
+int cr_splits(int rows) {
+  int rs = (rows + 511) / 512;
+  if (rs > 64) rs = 64;
+  if (rs < 1) rs = 1;
+  return rs;
+}
+
+template <typename XT>
+__global__ void __launch_bounds__(CR_WARPS * 32)
+    colreduce_pass1(const XT* __restrict__ X, long ldx, int rows, int cols, const float* __restrict__ w, int rs,
+                    float* __restrict__ partials) {
+  __shared__ float sm[CR_WARPS][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int c = blockIdx.x * 32 + lane;
+  const int per = (rows + rs - 1) / rs;
+  const int r0 = blockIdx.y * per, r1 = min(rows, r0 + per);
+  float acc = 0.f;
+  if (c < cols)
+    for (int r = r0 + warp; r < r1; r += CR_WARPS) {
+      const float v = ld<XT>(X, (long)r * ldx + c);
+      acc += w ? v * w[r] : v;
+    }
+  sm[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && c < cols) {
+    float s = 0.f;
+    for (int q = 0; q < CR_WARPS; ++q) s += sm[q][lane];
+    partials[(long)blockIdx.y * cols + c] = s;
+  }
+}
+
+__global__ void colreduce_pass2(const float* __restrict__ partials, int rs, int cols, int out_f32, void* out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= cols) return;
+  float s = 0.f;
+  for (int q = 0; q < rs; ++q) s += partials[(long)q * cols + c];
+  if (out_f32)
+    reinterpret_cast<float*>(out)[c] = s;
+  else
+    reinterpret_cast<__half*>(out)[c] = __float2half_rn(s);  // R12: one RNE
+}
+
+// ---------------------------------------------------------------- embedding backward
+__global__ void embed_keys_kernel(const int32_t* __restrict__ tok, int B, int Tn, int32_t* keys, int32_t* vals) {
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  if (p >= B * Tn) return;
+  const int b = p % B, t = p / B;
+  keys[p] = tok[(long)b * Tn + t];
+  vals[p] = p;
+}
+
+__device__ __forceinline__ int lower_bound_(const int32_t* a, int n, int v) {
+  int lo = 0, hi = n;
+  while (lo < hi) {
+    const int mid = (lo + hi) >> 1;
+    if (a[mid] < v) lo = mid + 1; else hi = mid;
+  }
+  return lo;
+}
+
+__global__ void embed_segsum_kernel(const int32_t* __restrict__ keys, const int32_t* __restrict__ vals, int n,
+                                    int vocab, const float* __restrict__ dX0, int Ep, int out_f32, void* dE) {
+  const long v = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  if (v >= vocab) return;
+  const int lo = lower_bound_(keys, n, (int)v), hi = lower_bound_(keys, n, (int)v + 1);
+  for (int k = lane; k < Ep; k += 32) {
+    float s = 0.f;
+    for (int q = lo; q < hi; ++q) s += dX0[(long)vals[q] * Ep + k];  // ascending position order
+    if (out_f32)
+      reinterpret_cast<float*>(dE)[v * Ep + k] = s;
+    else
+      reinterpret_cast<__half*>(dE)[v * Ep + k] = __float2half_rn(s);
+  }
+}
+
+inline int grid_for(long n, int threads, int cap = 148 * 16) {
+  long b = (n + threads - 1) / threads;
+  if (b > cap) b = cap;
+  return b < 1 ? 1 : (int)b;
+}
+
+}  // namespace
+
+// ============================================================== launchers
+cudaError_t launch_pack_input(const void* x, int x_f32, int B, int T, int I, int Ip, void* X0, int f32,
+                              cudaStream_t s) {
+  const long n = (long)T * B * Ip;
+  const int g = grid_for(n, 256);
+  if (f32) {
+    if (x_f32) pack_input_kernel<float, float><<<g, 256, 0, s>>>((const float*)x, B, T, I, Ip, (float*)X0);
+    else pack_input_kernel<__half, float><<<g, 256, 0, s>>>((const __half*)x, B, T, I, Ip, (float*)X0);
+  } else {
+    if (x_f32) pack_input_kernel<float, __half><<<g, 256, 0, s>>>((const float*)x, B, T, I, Ip, (__half*)X0);
+    else pack_input_kernel<__half, __half><<<g, 256, 0, s>>>((const __half*)x, B, T, I, Ip, (__half*)X0);
+  }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_embed_gather(const int32_t* tok, int B, int T, const void* E, int Ep, void* X0, int f32,
+                                cudaStream_t s) {
+  const long warps = (long)B * T;
+  const int g = (int)((warps * 32 + 255) / 256);
+  if (f32) embed_gather_kernel<float><<<g, 256, 0, s>>>(tok, B, T, (const float*)E, Ep, (float*)X0);
+  else embed_gather_kernel<__half><<<g, 256, 0, s>>>(tok, B, T, (const __half*)E, Ep, (__half*)X0);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cell_fwd(int f32, const float* Gx_t, const float* Gh, const float* c_prev, void* gates_t,
+                            float* c_t, void* h_t, int B, int hp, cudaStream_t s) {
+  const int n = B * hp;
+  const int g = (n + 127) / 128;
+  if (f32) cell_fwd_kernel<float><<<g, 128, 0, s>>>(Gx_t, Gh, c_prev, (float*)gates_t, c_t, (float*)h_t, n);
+  else cell_fwd_kernel<__half><<<g, 128, 0, s>>>(Gx_t, Gh, c_prev, (__half*)gates_t, c_t, (__half*)h_t, n);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_cell_bwd(int f32, const float* dHa_t, const float* dh_rec, const void* gates_t,
+                            const float* c_t, const float* c_prev, float* dc, void* dA_t, int B, int hp,
+                            int first, cudaStream_t s) {
+  const int n = B * hp;
+  const int g = (n + 127) / 128;
+  if (f32)
+    cell_bwd_kernel<float><<<g, 128, 0, s>>>(dHa_t, dh_rec, (const float*)gates_t, c_t, c_prev, dc, (float*)dA_t,
+                                             n, first);
+  else
+    cell_bwd_kernel<__half><<<g, 128, 0, s>>>(dHa_t, dh_rec, (const __half*)gates_t, c_t, c_prev, dc,
+                                              (__half*)dA_t, n, first);
+  return cudaGetLastError();
+}
+
+int head_partials_count(int rows) { return (rows + HEAD_WARPS - 1) / HEAD_WARPS; }
+
+cudaError_t launch_head_out(int f32, const void* Z, int rows, int Kd, long ldz, const void* wo, const void* bo,
+                            const int8_t* tgt, int tgt_mode, int B, int T, float alpha, float inv_terms, float* y,
+                            float* dy, float* partials, cudaStream_t s) {
+  const int g = head_partials_count(rows);
+  if (f32)
+    head_out_kernel<float><<<g, HEAD_WARPS * 32, 0, s>>>((const float*)Z, rows, Kd, ldz, (const float*)wo,
+                                                        (const float*)bo, tgt, tgt_mode, B, T, alpha, inv_terms, y,
+                                                        dy, partials);
+  else
+    head_out_kernel<__half><<<g, HEAD_WARPS * 32, 0, s>>>((const __half*)Z, rows, Kd, ldz, (const __half*)wo,
+                                                         (const __half*)bo, tgt, tgt_mode, B, T, alpha, inv_terms,
+                                                         y, dy, partials);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_loss_final(const float* partials, int n, float inv_terms, float* loss, cudaStream_t s) {
+  loss_final_kernel<<<1, 256, 0, s>>>(partials, n, inv_terms, loss);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_relu_dz(int f32, const float* dy, const void* wo, const void* Z, void* dz, int rows, int Fp,
+                           cudaStream_t s) {
+  const int g = grid_for((long)rows * Fp, 256);
+  if (f32) relu_dz_kernel<float><<<g, 256, 0, s>>>(dy, (const float*)wo, (const float*)Z, (float*)dz, rows, Fp);
+  else relu_dz_kernel<__half><<<g, 256, 0, s>>>(dy, (const __half*)wo, (const __half*)Z, (__half*)dz, rows, Fp);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_outer(int f32, const float* dy, const void* wo, float* dH, int rows, int hp, cudaStream_t s) {
+  const int g = grid_for((long)rows * hp, 256);
+  if (f32) outer_kernel<float><<<g, 256, 0, s>>>(dy, (const float*)wo, dH, rows, hp);
+  else outer_kernel<__half><<<g, 256, 0, s>>>(dy, (const __half*)wo, dH, rows, hp);
+  return cudaGetLastError();
+}
+
+size_t colreduce_partials_floats(int rows, int cols) { return (size_t)cr_splits(rows) * cols; }
+
+cudaError_t launch_colreduce(int x_f32, const void* X, long ldx, int rows, int cols, const float* w,
+                             float* partials, int out_f32, void* out, cudaStream_t s) {
+  const int rs = cr_splits(rows);
+  dim3 g1((cols + 31) / 32, rs);
+  if (x_f32) colreduce_pass1<float><<<g1, CR_WARPS * 32, 0, s>>>((const float*)X, ldx, rows, cols, w, rs, partials);
+  else colreduce_pass1<__half><<<g1, CR_WARPS * 32, 0, s>>>((const __half*)X, ldx, rows, cols, w, rs, partials);
+  colreduce_pass2<<<(cols + 255) / 256, 256, 0, s>>>(partials, rs, cols, out_f32, out);
+  return cudaGetLastError();
+}
+
+size_t embed_sort_temp_bytes(int n) {
+  size_t bytes = 0;
+  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
+                                  (const int32_t*)nullptr, (int32_t*)nullptr, n);
+  return bytes;
+}
+
+cudaError_t launch_embed_backward(const int32_t* tok, int B, int T, int vocab, const float* dX0, int Ep,
+                                  int32_t* keys_in, int32_t* keys_out, int32_t* vals_in, int32_t* vals_out,
+                                  void* sort_temp, size_t sort_temp_bytes, void* dE, int out_f32,
+                                  cudaStream_t s) {
+  const int n = B * T;
+  embed_keys_kernel<<<(n + 255) / 256, 256, 0, s>>>(tok, B, T, keys_in, vals_in);
+  int bits = 1;
+  while ((1 << bits) < vocab) ++bits;
+  size_t tb = sort_temp_bytes;
+  cudaError_t e = cub::DeviceRadixSort::SortPairs(sort_temp, tb, keys_in, keys_out, vals_in, vals_out, n, 0, bits, s);
+  if (e != cudaSuccess) return e;
+  const long threads = (long)vocab * 32;
+  embed_segsum_kernel<<<(int)((threads + 255) / 256), 256, 0, s>>>(keys_out, vals_out, n, vocab, dX0, Ep, out_f32,
+                                                                   dE);
+  return cudaGetLastError();
+}
+
+}  // namespace hdp

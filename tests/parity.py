@@ -1,0 +1,96 @@
+"""Shared helpers of the GPU parity tests: run the CUDA path through the
+C-ABI (paper_1912_00286_b200.hdp) and the oracle on the same seeded inputs
+and compare them with the north_star metrics:
+
+  e(P) = max|P_gpu - P_ref| / max|P_ref|   per named parameter block.
+"""
+from __future__ import annotations
+
+import numpy as np
+
+import synth
+from oracle import lstm as olstm
+from oracle import schedule as osched
+from oracle import step as ostep
+
+
+def block_errors(cfg, got: np.ndarray, ref: np.ndarray) -> dict:
+    g = olstm.unpack(cfg, got)
+    r = olstm.unpack(cfg, ref)
+    out = {}
+    for k in r:
+        den = np.max(np.abs(r[k]))
+        num = np.max(np.abs(g[k] - r[k]))
+        out[k] = float(num / den) if den > 0 else float(num)
+    return out
+
+
+def run_parity(cfg, global_batch: int, n_workers: int, steps: int, mixed: bool, lambda0=None, alpha=None,
+               optimizer="sgdm", seed=synth.DATA_SEED, epochs=None, compare_grads=True):
+    """Returns a list of per-step records with GPU-vs-oracle errors."""
+    import torch
+
+    from paper_1912_00286_b200 import hdp
+
+    alpha = cfg.alpha if alpha is None else alpha
+    lambda0 = cfg.lambda0 if lambda0 is None else lambda0
+    mode = "mixed" if mixed else "fp32"
+    B = global_batch // n_workers
+    desc = hdp.desc_from_config(cfg, B, hdp.MATH_MIXED16 if mixed else hdp.MATH_FP32,
+                                hdp.WIRE_FP16_A2A, hdp.OPT_SGDM if optimizer == "sgdm" else hdp.OPT_ADAM,
+                                sim_workers=n_workers)
+    params = synth.init_params(cfg)
+    tr = hdp.Trainer(desc, params, lambda0=lambda0, alpha=alpha, gamma=cfg.gamma, n_half=cfg.n_half,
+                     momentum=cfg.momentum)
+    n = tr.n
+    master = params.astype(np.float64)
+    state = {"H": np.zeros(n)} if optimizer == "sgdm" else {"m1": np.zeros(n), "v": np.zeros(n)}
+    recs = []
+    dev = torch.device("cuda:0")
+    try:
+        for k in range(steps):
+            epoch = (epochs[k] if epochs is not None else 0)
+            x, t = synth.model_batch(cfg, global_batch, seed + k)
+            if not mixed and cfg.vocab == 0:
+                x = x.astype(np.float32)
+            xs, ts = [], []
+            for r in range(n_workers):
+                sl = slice(r * B, (r + 1) * B)
+                xs.append(torch.from_numpy(np.ascontiguousarray(x[sl])).to(dev))
+                ts.append(torch.from_numpy(np.ascontiguousarray(t[sl])).to(dev))
+            stream = torch.cuda.current_stream()
+            for r in range(n_workers):
+                hdp.lstm_forward(tr.ctx, xs[r], ts[r], B, cfg.seq, r, None, tr.loss[r:r + 1], stream)
+                hdp.lstm_backward(tr.ctx, r, stream)
+            torch.cuda.synchronize()
+            gpu_grads = [hdp.read_grads(tr.ctx, r, n) for r in range(n_workers)] if compare_grads else None
+            gpu_losses = tr.loss.cpu().numpy().astype(np.float64)
+            nonfinite = hdp.grad_average_update(tr.ctx, epoch, stream, sync=True)
+            torch.cuda.synchronize()
+            gpu_master = hdp.gather_master(tr.ctx, n)
+            gpu_w = hdp.read_weights(tr.ctx, n)
+            lam = osched.rate_for_epoch(lambda0, n_workers, cfg.n_half, cfg.gamma, epoch, cfg.max_eff_lr)
+            lam32 = float(np.float32(lam))
+            ref = ostep.train_step(cfg, master, state, x, t, n_workers, alpha, lam32, mode, optimizer,
+                                   cfg.momentum, adam_k=k + 1)
+            rec = {
+                "step": k,
+                "loss_gpu": float(np.mean(gpu_losses)),
+                "loss_ref": ref["loss"],
+                "nonfinite_gpu": nonfinite,
+                "nonfinite_ref": ref["nonfinite"],
+                "master_err": block_errors(cfg, gpu_master.astype(np.float64), ref["master"]),
+                "dmaster_err": block_errors(cfg, gpu_master.astype(np.float64) - params,
+                                            ref["master"] - params),
+                "w_matches_master": bool(np.array_equal(
+                    gpu_w, gpu_master.astype(np.float16).astype(np.float32) if mixed else gpu_master)),
+            }
+            if compare_grads:
+                rec["grad_err"] = [block_errors(cfg, gpu_grads[r].astype(np.float64), ref["grads"][r])
+                                   for r in range(n_workers)]
+            recs.append(rec)
+            # both sides continue from their own state (trajectory comparison)
+            master, state = ref["master"], ref["state"]
+    finally:
+        tr.close()
+    return recs

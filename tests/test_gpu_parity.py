@@ -1,0 +1,120 @@
+"""End-to-end parity of the CUDA training step (through the C-ABI) with the
+oracle on the same seeded inputs, north_star tolerances:
+
+  FP32 mode : relative error <= 1e-5 per gradient and weight tensor
+  mixed mode: <= 2e-2 relative on weights after the steps, loss within 1e-2
+
+Configs: C1 (tiny, 2 simulated workers, fp32 and mixed, 5 steps), C2
+(JET-shaped, full size, mixed), C3 (IMDB-shaped, embedding + last-step head;
+reduced T and B so the oracle finishes in seconds), C4 (stacked h=2048;
+reduced T and B).
+"""
+import numpy as np
+import pytest
+
+torch = pytest.importorskip("torch")
+pytestmark = pytest.mark.gpu
+
+import synth  # noqa: E402
+
+from parity import run_parity  # noqa: E402
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _need_gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+
+
+def _max(d):
+    return max(d.values())
+
+
+def test_c1_fp32_two_workers():
+    cfg = synth.CONFIGS["C1"]
+    recs = run_parity(cfg, synth.C1_GLOBAL_BATCH, synth.C1_SIM_WORKERS, steps=5, mixed=False)
+    for r in recs:
+        for ge in r["grad_err"]:
+            assert _max(ge) <= 1e-5, (r["step"], ge)
+        assert _max(r["master_err"]) <= 1e-5, (r["step"], r["master_err"])
+        assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-5 * max(1.0, abs(r["loss_ref"]))
+        assert r["nonfinite_gpu"] == r["nonfinite_ref"] == 0
+        assert r["w_matches_master"]
+
+
+def test_c1_mixed_two_workers():
+    cfg = synth.CONFIGS["C1"]
+    recs = run_parity(cfg, synth.C1_GLOBAL_BATCH, synth.C1_SIM_WORKERS, steps=5, mixed=True)
+    for r in recs:
+        assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"])), r
+        assert r["nonfinite_gpu"] == r["nonfinite_ref"] == 0
+        assert r["w_matches_master"]
+        for ge in r["grad_err"]:
+            assert _max(ge) <= 2e-2, (r["step"], ge)
+    assert _max(recs[-1]["master_err"]) <= 2e-2
+
+
+def test_c1_mixed_stress_lr():
+    # stress variant: large lambda so the update is visible,
+    # cumulative update dW = W_k - W_0 compared as well
+    cfg = synth.CONFIGS["C1"].with_(lambda0=0.05, n_half=1e9)
+    recs = run_parity(cfg, synth.C1_GLOBAL_BATCH, synth.C1_SIM_WORKERS, steps=5, mixed=True, compare_grads=False)
+    for r in recs:
+        assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
+    assert _max(recs[-1]["master_err"]) <= 2e-2
+    assert _max(recs[-1]["dmaster_err"]) <= 5e-2, recs[-1]["dmaster_err"]
+
+
+def test_c1_adam_fp32():
+    cfg = synth.CONFIGS["C1"]
+    recs = run_parity(cfg, synth.C1_GLOBAL_BATCH, synth.C1_SIM_WORKERS, steps=3, mixed=False, optimizer="adam",
+                      compare_grads=False)
+    for r in recs:
+        assert _max(r["master_err"]) <= 1e-5, r["master_err"]
+
+
+def test_c1_schedule_epochs_fp32():
+    # epochs 0,1,2 -> lambda decays by gamma each epoch
+    cfg = synth.CONFIGS["C1"]
+    recs = run_parity(cfg, synth.C1_GLOBAL_BATCH, synth.C1_SIM_WORKERS, steps=3, mixed=False, epochs=[0, 1, 2],
+                      compare_grads=False)
+    for r in recs:
+        assert _max(r["master_err"]) <= 1e-5
+
+
+def test_c2_jet_mixed():
+    cfg = synth.CONFIGS["C2"]
+    recs = run_parity(cfg, cfg.batch, 1, steps=4, mixed=True)
+    for r in recs:
+        assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"])), r
+        assert r["nonfinite_gpu"] == 0
+        assert _max(r["grad_err"][0]) <= 2e-2, r["grad_err"]
+    assert _max(recs[-1]["master_err"]) <= 2e-2
+
+
+def test_c3_imdb_reduced_mixed():
+    cfg = synth.CONFIGS["C3"].with_(seq=48)
+    recs = run_parity(cfg, 16, 2, steps=3, mixed=True)
+    for r in recs:
+        assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"])), r
+        for ge in r["grad_err"]:
+            assert _max(ge) <= 2e-2, ge
+    assert _max(recs[-1]["master_err"]) <= 2e-2
+
+
+def test_c3_imdb_reduced_fp32():
+    cfg = synth.CONFIGS["C3"].with_(seq=24)
+    recs = run_parity(cfg, 8, 2, steps=2, mixed=False)
+    for r in recs:
+        for ge in r["grad_err"]:
+            assert _max(ge) <= 1e-5, ge
+        assert _max(r["master_err"]) <= 1e-5
+
+
+def test_c4_stacked_reduced_mixed():
+    cfg = synth.CONFIGS["C4"].with_(seq=8)
+    recs = run_parity(cfg, 8, 1, steps=1, mixed=True)
+    r = recs[0]
+    assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
+    assert _max(r["grad_err"][0]) <= 2e-2, r["grad_err"]
+    assert _max(r["master_err"]) <= 2e-2
