@@ -1,0 +1,368 @@
+"""Benchmark of the data-parallel mixed-precision LSTM training step
+(arXiv 1912.00286) on B200 -- the driver contract.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--config C2|C3|C4|C5] [--impl hdp|reference]
+    torchrun --nproc-per-node N bench.py --gpus N ...            (N > 1)
+
+A step = forward + BPTT + bucketed exchange + fused average/update of one
+per-rank mini-batch (all §8(a) rows), through libhdp's C-ABI.  Prints ONE
+JSON line on rank 0.  Default workload: C2 (JET-shaped, BASELINE.json
+configs[1]): 2-layer LSTM h=200, FC 200 + ReLU, T=128, 128 sequences per
+rank, fp16 math with loss scaling, fp32 master weights.
+
+Timing: W warm-up steps; then K steps, each bracketed by CUDA events on the
+launching stream with an L2 flush (256 MiB memset, outside the events)
+between steps; barrier + synchronize on both sides; max over ranks.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import tempfile
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "LSTM training samples/s at 1/2/4/8 B200; avg+update GB/s vs HBM peak"
+
+# kernel classes of include/hdp.h (HDP_K_*)
+KCLASS = ["input", "gemm_x(K1)", "gemm_h(K2)", "cell_fwd(K3)", "head_fwd(K4)", "head_bwd(K5)", "cell_bwd(K6)",
+          "gemm_dh(K7)", "gemm_dw(K8)", "gemm_dx(K9)", "embed_bwd(K10)", "update(K11)", "comm(A9/A11)"]
+
+
+def peaks():
+    p = {"hbm_gbs": 6456.2, "bf16_tflops": 1660.9, "bf16_tflops_sustained": 1415.3, "src": "fallback"}
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            m = json.load(f)
+        p.update({k: m[k] for k in ("hbm_gbs", "bf16_tflops", "bf16_tflops_sustained") if k in m})
+        p["src"] = "measured"
+    except Exception:
+        p["src"] = "fallback (B200_PROFILING.md)"
+    return p
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    def __init__(self, index):
+        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
+        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
+                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        self.p.wait()
+        self.f.seek(0)
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in self.f.read().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        os.unlink(self.f.name)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def algorithmic_work(cfg, B, world):
+    """Per-launch algorithmic work of each kernel class:
+    flops for contractions (unpadded shapes), HBM bytes for the elementwise /
+    update kernels.  Returns {class: (kind, per_launch_amount)}."""
+    h, T, L = cfg.hidden, cfg.seq, cfg.n_layers
+    I0 = cfg.embed_dim if cfg.vocab else cfg.input_dim
+    ins = [I0] + [h] * (L - 1)
+    w = {}
+    w["gemm_h(K2)"] = ("flop", 2.0 * B * 4 * h * h)
+    w["gemm_dh(K7)"] = ("flop", 2.0 * B * 4 * h * h)
+    w["gemm_x(K1)"] = ("flop", sum(2.0 * B * T * 4 * h * i for i in ins) / L)
+    w["gemm_dw(K8)"] = ("flop", sum(2.0 * 4 * h * (i + h) * B * T for i in ins) / (3 * L))  # dW, dU, db launches
+    w["gemm_dx(K9)"] = ("flop", 2.0 * B * T * 4 * h * h)
+    w["cell_fwd(K3)"] = ("byte", 50.0 * B * h)   # Gx 16 + Gh 16 + c_prev 4 + gates 8 + c 4 + h 2
+    w["cell_bwd(K6)"] = ("byte", 40.0 * B * h)   # dHa 4 + dh_rec 4 + gates 8 + c 4 + c_prev 4 + dc 8 + dA 8
+    return w
+
+
+def run_hdp(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import synth
+    from paper_1912_00286_b200 import hdp
+
+    dev = torch.device(f"cuda:{local_rank}")
+    torch.cuda.set_device(dev)
+    cfg = synth.CONFIGS[args.config]
+    B = args.batch or cfg.batch
+    uid = None
+    if world > 1:
+        import torch.distributed as dist
+        obj = [hdp.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    desc = hdp.desc_from_config(cfg, B, hdp.MATH_MIXED16, hdp.WIRE_FP16_A2A, hdp.OPT_SGDM, 1)
+    params = synth.init_params(cfg) if rank == 0 else None
+    tr = hdp.Trainer(desc, params, lambda0=cfg.lambda0, alpha=cfg.alpha, gamma=cfg.gamma, n_half=cfg.n_half,
+                     momentum=cfg.momentum, world=world, rank=rank, uid=uid, device=local_rank)
+    x, t = synth.model_batch(cfg, B, synth.DATA_SEED + 1000 * rank)
+    xd = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
+    td = torch.from_numpy(np.ascontiguousarray(t)).to(dev)
+    xh = torch.from_numpy(np.ascontiguousarray(x)).pin_memory()
+    th = torch.from_numpy(np.ascontiguousarray(t)).pin_memory()
+    loss_h = torch.zeros(1, dtype=torch.float32).pin_memory()
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)   # > 126 MB L2
+
+    def step(xx, tt, epoch=0):
+        hdp.lstm_forward(tr.ctx, xx, tt, B, cfg.seq, 0, None, tr.loss[0:1], stream)
+        hdp.lstm_backward(tr.ctx, 0, stream)
+        hdp.grad_average_update(tr.ctx, epoch, stream)
+
+    def barrier():
+        torch.cuda.synchronize(dev)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    def max_over_ranks(v):
+        if world == 1:
+            return v
+        import torch.distributed as dist
+        tv = torch.tensor([v], dtype=torch.float64, device=dev)
+        dist.all_reduce(tv, op=dist.ReduceOp.MAX)
+        return tv.item()
+
+    for _ in range(args.warmup):
+        step(xd, td)
+    barrier()
+
+    # ---------------- timed region (device-resident inputs)
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    clk = Clocks(local_rank)
+    k0 = hdp.lib().hdp_kernel_launches(tr.ctx)
+    barrier()
+    for k in range(args.steps):
+        flush.zero_()
+        evs[k][0].record(stream)
+        step(xd, td)
+        evs[k][1].record(stream)
+    barrier()
+    clocks = clk.stop()
+    launches = hdp.lib().hdp_kernel_launches(tr.ctx) - k0
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    ms = max_over_ranks(statistics.mean(step_ms))
+    loss_dev = tr.loss.item()
+
+    # ---------------- e2e: host (pinned) buffers through the C-ABI, loss read back every step
+    e_evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+    barrier()
+    for k in range(args.steps):
+        flush.zero_()
+        e_evs[k][0].record(stream)
+        step(xh, th)
+        loss_h.copy_(tr.loss[0:1], non_blocking=True)
+        e_evs[k][1].record(stream)
+    barrier()
+    e2e_ms = max_over_ranks(statistics.mean([a.elapsed_time(b) for a, b in e_evs]))
+
+    # ---------------- live per-kernel-class profile (eager, CUDA events around each launch)
+    nk = len(KCLASS)
+    ms_by = (__import__("ctypes").c_double * nk)()
+    n_by = (__import__("ctypes").c_longlong * nk)()
+    hdp.lib().hdp_profile(tr.ctx, 1)
+    hdp.lib().hdp_profile_read(tr.ctx, ms_by, n_by, 1)
+    prof_steps = 2
+    for _ in range(prof_steps):
+        step(xd, td)
+    hdp.lib().hdp_profile_read(tr.ctx, ms_by, n_by, 1)
+    hdp.lib().hdp_profile(tr.ctx, 0)
+    barrier()
+    prof = {KCLASS[i]: {"ms_per_step": ms_by[i] / prof_steps, "launches_per_step": n_by[i] / prof_steps}
+            for i in range(nk) if n_by[i]}
+    tr.close()
+
+    if rank != 0:
+        return None
+    pk = peaks()
+    work = algorithmic_work(cfg, B, world)
+    cand = {k: v for k, v in prof.items() if k in work}
+    dom = max(cand, key=lambda k: cand[k]["ms_per_step"])
+    kind, per_launch = work[dom]
+    avg_launch_ms = cand[dom]["ms_per_step"] / cand[dom]["launches_per_step"]
+    if kind == "flop":
+        achieved = per_launch / (avg_launch_ms * 1e-3) / 1e12
+        peak = pk["bf16_tflops_sustained"]
+        roof = {"bound": "tensor", "achieved": achieved, "peak": peak, "unit": "TFLOP/s", "frac": achieved / peak,
+                "traffic": None}
+    else:
+        achieved = per_launch / (avg_launch_ms * 1e-3) / 1e9
+        peak = pk["hbm_gbs"]
+        roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                "traffic": None}
+    roof.update({"kernel": dom, "peak_src": pk["src"] + (" sustained" if kind == "flop" else ""),
+                 "avg_launch_us": avg_launch_ms * 1e3, "per_launch": per_launch,
+                 "per_launch_unit": "flop" if kind == "flop" else "byte",
+                 "share_of_step": cand[dom]["ms_per_step"] / sum(v["ms_per_step"] for v in prof.values())})
+    samples = B * world
+    x_bytes = int(xh.numel() * xh.element_size())
+    t_bytes = int(th.numel() * th.element_size())
+    out = {
+        "metric": METRIC,
+        "value": samples / (ms * 1e-3),
+        "unit": "samples/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f16",
+        "data": "synthetic (seeded JET-shaped / IMDB-shaped / dense generators, random init)",
+        "config": {"workload": cfg.name, "per_rank_batch": B, "global_batch": samples, "seq_len": cfg.seq,
+                   "hidden": cfg.hidden, "layers": cfg.n_layers, "fc_hidden": cfg.fc_hidden,
+                   "parallelism": f"dp{world}", "math": "fp16 (fp32 accumulate, fp32 master)",
+                   "wire": "fp16 all-to-all", "optimizer": "sgd-momentum", "loss_scale": cfg.alpha,
+                   "l2": "flushed between timed steps (256 MiB memset, outside the events)"},
+        "e2e": {"value": samples / (e2e_ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": x_bytes + t_bytes,
+                "d2h_bytes_per_step": 4},
+        "gpu_launches": int(launches),
+        "roofline": roof,
+        "clocks": clocks,
+        "loss_last": loss_dev,
+        "profile_ms_per_step": {k: round(v["ms_per_step"], 4) for k, v in prof.items()},
+    }
+    return out
+
+
+def cpu_baseline(args, seconds=15.0, max_steps=4):
+    """The oracle as it stands, on the host cores, on a bounded sample."""
+    import numpy as np
+
+    import synth
+    from oracle import step as ostep
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = os.cpu_count()
+    cfg = synth.CONFIGS[args.config]
+    B = args.batch or cfg.batch
+    if args.config == "C4":
+        B = min(B, 4)
+    master = synth.init_params(cfg).astype(np.float64)
+    x, t = synth.model_batch(cfg, B, synth.DATA_SEED)
+    n, t0 = 0, time.perf_counter()
+    state = {"H": np.zeros_like(master)}
+    while n < max_steps:
+        out = ostep.train_step(cfg, master, state, x, t, 1, cfg.alpha, float(np.float32(cfg.lambda0 / 1.01)),
+                               "mixed")
+        master, state = out["master"], out["state"]
+        n += 1
+        if time.perf_counter() - t0 > seconds:
+            break
+    dt = time.perf_counter() - t0
+    return {"value": n * B / dt, "unit": "samples/s", "cores": threads, "kind": "oracle",
+            "sample": f"{n} oracle.step.train_step of {cfg.name} ({B} sequences x T={cfg.seq}, mixed mode, N=1) "
+                      f"in {dt:.1f} s"}
+
+
+def run_reference(args):
+    """--impl reference: the oracle (NumPy fp64 with fp16 rounding points) on the host."""
+    import numpy as np
+
+    import synth
+    from oracle import step as ostep
+    cfg = synth.CONFIGS[args.config]
+    Bs = {"C1": 8, "C2": 8, "C3": 4, "C4": 1}.get(args.config, 8)   # bounded sample per step
+    cfgs = cfg if args.config != "C4" else cfg.with_(seq=16)
+    master = synth.init_params(cfgs).astype(np.float64)
+    x, t = synth.model_batch(cfgs, Bs, synth.DATA_SEED)
+    state = {"H": np.zeros_like(master)}
+
+    def one():
+        nonlocal master, state
+        out = ostep.train_step(cfgs, master, state, x, t, 1, cfg.alpha, 4e-4, "mixed")
+        master, state = out["master"], out["state"]
+
+    for _ in range(args.warmup):
+        one()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        one()
+    dt = time.perf_counter() - t0
+    try:
+        from threadpoolctl import threadpool_info
+        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:
+        threads = os.cpu_count()
+    v = Bs * args.steps / dt
+    sample = f"{Bs} sequences of {cfgs.name} (T={cfgs.seq}) per step, oracle.step.train_step, mixed mode"
+    return {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt / args.steps * 1e3,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic", "config": {"workload": cfg.name, "per_rank_batch": Bs, "seq_len": cfgs.seq,
+                                              "parallelism": "host"},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--batch", type=int, default=0, help="per-rank batch (default: the config's)")
+    ap.add_argument("--impl", default="hdp", choices=["hdp", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank == 0:
+            print(json.dumps(run_reference(args)), flush=True)
+        return
+
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    out = run_hdp(args, rank, world, local_rank)
+    if rank == 0:
+        if world == 1 and not args.no_cpu_baseline:
+            out["cpu_baseline"] = cpu_baseline(args)
+        print(json.dumps(out), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -174,6 +174,31 @@ int hdp_lstm_backward(hdp_ctx* ctx, int slot, void* stream);
  * until hdp_load_params).  HDP_ERR_STATE if a slot has no backward.      */
 int hdp_grad_average_update(hdp_ctx* ctx, int epoch, void* stream, int* nonfinite_host);
 
+/* Live profiler.  Kernel classes: */
+enum { HDP_K_INPUT = 0,     /* input packing / embedding gather (A1 prologue, K10) */
+       HDP_K_GEMM_X = 1,    /* K1  input projection X W^T + b (A1)                 */
+       HDP_K_GEMM_H = 2,    /* K2  recurrent gate GEMM h U^T per step (A2)         */
+       HDP_K_CELL_FWD = 3,  /* K3  fused cell forward (A3)                         */
+       HDP_K_HEAD_FWD = 4,  /* K4  head + scaled hinge loss (A4)                   */
+       HDP_K_HEAD_BWD = 5,  /* K5  head backward (A5)                              */
+       HDP_K_CELL_BWD = 6,  /* K6  fused cell backward (A6)                        */
+       HDP_K_GEMM_DH = 7,   /* K7  recurrent backward GEMM dA U per step (A7)      */
+       HDP_K_GEMM_DW = 8,   /* K8  weight / bias gradients (A8)                    */
+       HDP_K_GEMM_DX = 9,   /* K9  input gradient dA W (A8)                        */
+       HDP_K_EMBED_BWD = 10,/* K10 embedding scatter-add (A8)                      */
+       HDP_K_UPDATE = 11,   /* K11 fused average + update (A10)                    */
+       HDP_K_COMM = 12,     /* NCCL exchange / allgather (A9, A11)                 */
+       HDP_K_NTAGS = 13 };
+/* enable != 0: subsequent forward / backward run eagerly (no CUDA graphs)
+ * with a CUDA event pair around every launch on its stream.              */
+int hdp_profile(hdp_ctx* ctx, int enable);
+/* Synchronises; accumulated milliseconds and event-pair counts per class
+ * (arrays of HDP_K_NTAGS, nullable); reset != 0 clears the totals.        */
+int hdp_profile_read(hdp_ctx* ctx, double* ms, long long* launches, int reset);
+/* Number of this library's kernels enqueued so far (graph launches count
+ * their captured kernels; NCCL's and cub's kernels are not counted).     */
+long long hdp_kernel_launches(const hdp_ctx* ctx);
+
 /* Device pointers into the bound arena (for benches and tests). */
 void* hdp_weights_ptr(hdp_ctx* ctx);           /* working copy, device layout          */
 void* hdp_grads_ptr(hdp_ctx* ctx, int slot);   /* gradient slot, device layout        */

@@ -143,6 +143,20 @@ struct hdp_ctx {
   int* count_host = nullptr;  // pinned
   bool count_pending = false;
   std::map<GraphKey, cudaGraphExec_t> graphs;
+  std::map<GraphKey, long long> graph_kernels;  // kernels per captured graph
+  long long kernels = 0;                        // library kernels enqueued so far
+  // live profiler: CUDA events around every launch (eager mode, no graphs)
+  bool prof = false;
+  struct ProfRec {
+    int tag;
+    cudaEvent_t a, b;
+    int nk;
+  };
+  std::vector<ProfRec> precs;
+  std::vector<cudaEvent_t> evpool;
+  size_t evused = 0;
+  double prof_ms[HDP_K_NTAGS] = {};
+  long long prof_n[HDP_K_NTAGS] = {};
   std::vector<SlotState> st;
   // schedule
   bool lr_set = false;
@@ -350,9 +364,41 @@ void carve(hdp_ctx* c, char* base) {
   c->arena_bytes = rup(cv.off, 256);
 }
 
+// ---------------------------------------------------------------- profiler
+cudaEvent_t prof_event(hdp_ctx* c) {
+  if (c->evused == c->evpool.size()) {
+    cudaEvent_t e;
+    cudaEventCreate(&e);
+    c->evpool.push_back(e);
+  }
+  return c->evpool[c->evused++];
+}
+// Counts the kernels a launch site enqueues and, when profiling, brackets
+// them with CUDA events on the launching stream.
+struct KScope {
+  hdp_ctx* c;
+  int tag, nk;
+  cudaStream_t s;
+  cudaEvent_t a = nullptr;
+  KScope(hdp_ctx* c_, int tag_, int nk_, cudaStream_t s_) : c(c_), tag(tag_), nk(nk_), s(s_) {
+    if (c->prof) {
+      a = prof_event(c);
+      cudaEventRecord(a, s);
+    }
+  }
+  ~KScope() {
+    c->kernels += nk;
+    if (c->prof) {
+      cudaEvent_t b = prof_event(c);
+      cudaEventRecord(b, s);
+      c->precs.push_back({tag, a, b, nk});
+    }
+  }
+};
+
 // ---------------------------------------------------------------- GEMM helper
-int gemm(hdp_ctx* c, const void* A, long lda, int amn, const void* B, long ldb, int bmn, long M, long N, long K,
-         const hdp::Epilogue& epi, cudaStream_t s) {
+int gemm(hdp_ctx* c, int tag, const void* A, long lda, int amn, const void* B, long ldb, int bmn, long M, long N,
+         long K, const hdp::Epilogue& epi, cudaStream_t s) {
   hdp::GemmPlan p;
   int r;
   if (c->f32)
@@ -361,6 +407,7 @@ int gemm(hdp_ctx* c, const void* A, long lda, int amn, const void* B, long ldb, 
     r = hdp::gemm_plan_tc(&p, (const __half*)A, lda, amn, (const __half*)B, ldb, bmn, (int)M, (int)N, (int)K, epi,
                           c->ws, c->ws_floats);
   if (r) return fail(HDP_ERR_ARG, "gemm plan %ldx%ldx%ld: %s", M, N, K, hdp::gemm_last_error());
+  KScope ks(c, tag, p.tc && p.splits > 1 ? 2 : 1, s);
   CK_CUDA(hdp::gemm_run(p, s));
   return HDP_OK;
 }
@@ -395,9 +442,15 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
   const long g_layer = (long)T * B * 4 * hp;
   for (int l = 0; l < L; ++l) CK_CUDA(cudaMemsetAsync(S.Hs + l * hs_layer * e, 0, B * hp * e, s));
   if (d.vocab > 0)
-    CK_CUDA(hdp::launch_embed_gather((const int32_t*)S.stage_x, B, T, c->W(c->find("E")), (int)c->Ip0, S.X0, f32, s));
+    {
+      KScope ks_(c, HDP_K_INPUT, 1, s);
+      CK_CUDA(hdp::launch_embed_gather((const int32_t*)S.stage_x, B, T, c->W(c->find("E")), (int)c->Ip0, S.X0, f32, s));
+    }
   else
-    CK_CUDA(hdp::launch_pack_input(S.stage_x, f32, B, T, d.input_dim, (int)c->Ip0, S.X0, f32, s));
+    {
+      KScope ks_(c, HDP_K_INPUT, 1, s);
+      CK_CUDA(hdp::launch_pack_input(S.stage_x, f32, B, T, d.input_dim, (int)c->Ip0, S.X0, f32, s));
+    }
   char nm[16];
   for (int l = 0; l < L; ++l) {
     snprintf(nm, sizeof nm, "W%d", l);
@@ -412,14 +465,17 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
     float* Cl = S.C + l * c_layer;
     char* Gl = S.gates + l * g_layer * e;
     // K1: G_x = X W^T + b for all t (A1)
-    CK(gemm(c, X, Ipl, 0, c->W(iW), Ipl, 0, rows, 4 * hp, Ipl, epi_f32(c->Gx, 4 * hp, c->W(ib), !f32), s));
+    CK(gemm(c, HDP_K_GEMM_X, X, Ipl, 0, c->W(iW), Ipl, 0, rows, 4 * hp, Ipl, epi_f32(c->Gx, 4 * hp, c->W(ib), !f32), s));
     for (int t = 0; t < T; ++t) {
       if (t > 0)  // K2: G_h = h_{t-1} U^T (A2)
-        CK(gemm(c, Hs + (long)t * B * hp * e, hp, 0, c->W(iU), hp, 0, B, 4 * hp, hp, epi_f32(c->Gh, 4 * hp), s));
+        CK(gemm(c, HDP_K_GEMM_H, Hs + (long)t * B * hp * e, hp, 0, c->W(iU), hp, 0, B, 4 * hp, hp, epi_f32(c->Gh, 4 * hp), s));
       // K3 (A3)
-      CK_CUDA(hdp::launch_cell_fwd(f32, c->Gx + (long)t * B * 4 * hp, t > 0 ? c->Gh : nullptr,
-                                   t > 0 ? Cl + (long)(t - 1) * B * hp : nullptr, Gl + (long)t * B * 4 * hp * e,
-                                   Cl + (long)t * B * hp, Hs + (long)(t + 1) * B * hp * e, B, (int)hp, s));
+      {
+        KScope ks_(c, HDP_K_CELL_FWD, 1, s);
+        CK_CUDA(hdp::launch_cell_fwd(f32, c->Gx + (long)t * B * 4 * hp, t > 0 ? c->Gh : nullptr,
+                                     t > 0 ? Cl + (long)(t - 1) * B * hp : nullptr, Gl + (long)t * B * 4 * hp * e,
+                                     Cl + (long)t * B * hp, Hs + (long)(t + 1) * B * hp * e, B, (int)hp, s));
+      }
     }
   }
   // head (A4)
@@ -431,19 +487,37 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
     ez.bias = c->W(ifb);
     ez.bias_f16 = !f32;
     ez.relu = 1;  // R7
-    CK(gemm(c, Htop, hp, 0, c->W(iF), hp, 0, rows, c->Fp, hp, ez, s));
-    CK_CUDA(hdp::launch_head_out(f32, S.Z, (int)rows, (int)c->Fp, c->Fp, c->W(iwo), c->W(ibo), S.stage_t, 0, B, T,
-                                 c->alpha, 1.f / (float)rows, S.y, S.dy, S.partials, s));
-    CK_CUDA(hdp::launch_loss_final(S.partials, hdp::head_partials_count((int)rows), 1.f / (float)rows, S.loss, s));
+    CK(gemm(c, HDP_K_HEAD_FWD, Htop, hp, 0, c->W(iF), hp, 0, rows, c->Fp, hp, ez, s));
+    {
+      KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
+      CK_CUDA(hdp::launch_head_out(f32, S.Z, (int)rows, (int)c->Fp, c->Fp, c->W(iwo), c->W(ibo), S.stage_t, 0, B, T,
+                                   c->alpha, 1.f / (float)rows, S.y, S.dy, S.partials, s));
+    }
+    {
+      KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
+      CK_CUDA(hdp::launch_loss_final(S.partials, hdp::head_partials_count((int)rows), 1.f / (float)rows, S.loss, s));
+    }
   } else if (d.head_last_step) {
     const char* Hlast = S.Hs + ((L - 1) * hs_layer + (long)T * B * hp) * e;
-    CK_CUDA(hdp::launch_head_out(f32, Hlast, B, (int)hp, hp, c->W(iwo), c->W(ibo), S.stage_t, 1, B, T, c->alpha,
-                                 1.f / (float)B, S.y, S.dy, S.partials, s));
-    CK_CUDA(hdp::launch_loss_final(S.partials, hdp::head_partials_count(B), 1.f / (float)B, S.loss, s));
+    {
+      KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
+      CK_CUDA(hdp::launch_head_out(f32, Hlast, B, (int)hp, hp, c->W(iwo), c->W(ibo), S.stage_t, 1, B, T, c->alpha,
+                                   1.f / (float)B, S.y, S.dy, S.partials, s));
+    }
+    {
+      KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
+      CK_CUDA(hdp::launch_loss_final(S.partials, hdp::head_partials_count(B), 1.f / (float)B, S.loss, s));
+    }
   } else {
-    CK_CUDA(hdp::launch_head_out(f32, Htop, (int)rows, (int)hp, hp, c->W(iwo), c->W(ibo), S.stage_t, 0, B, T,
-                                 c->alpha, 1.f / (float)rows, S.y, S.dy, S.partials, s));
-    CK_CUDA(hdp::launch_loss_final(S.partials, hdp::head_partials_count((int)rows), 1.f / (float)rows, S.loss, s));
+    {
+      KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
+      CK_CUDA(hdp::launch_head_out(f32, Htop, (int)rows, (int)hp, hp, c->W(iwo), c->W(ibo), S.stage_t, 0, B, T,
+                                   c->alpha, 1.f / (float)rows, S.y, S.dy, S.partials, s));
+    }
+    {
+      KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
+      CK_CUDA(hdp::launch_loss_final(S.partials, hdp::head_partials_count((int)rows), 1.f / (float)rows, S.loss, s));
+    }
   }
   return HDP_OK;
 }
@@ -465,23 +539,53 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
     if (d.fc_hidden > 0) {
       const int iF = c->find("F"), ifb = c->find("fb");
       const long Fp = c->Fp;
-      CK_CUDA(hdp::launch_relu_dz(f32, S.dy, c->W(iwo), S.Z, c->dz, (int)rows, (int)Fp, s));          // R9
-      CK_CUDA(hdp::launch_colreduce(f32, S.Z, Fp, (int)rows, (int)Fp, S.dy, c->crp, gf, c->G(si, iwo), s));
-      CK_CUDA(hdp::launch_colreduce(1, S.dy, 1, (int)rows, 1, nullptr, c->crp, gf, c->G(si, ibo), s));
-      CK_CUDA(hdp::launch_colreduce(f32, c->dz, Fp, (int)rows, (int)Fp, nullptr, c->crp, gf, c->G(si, ifb), s));
+      {
+        KScope ks_(c, HDP_K_HEAD_BWD, 1, s);
+        CK_CUDA(hdp::launch_relu_dz(f32, S.dy, c->W(iwo), S.Z, c->dz, (int)rows, (int)Fp, s));          // R9
+      }
+      {
+        KScope ks_(c, HDP_K_HEAD_BWD, 2, s);
+        CK_CUDA(hdp::launch_colreduce(f32, S.Z, Fp, (int)rows, (int)Fp, S.dy, c->crp, gf, c->G(si, iwo), s));
+      }
+      {
+        KScope ks_(c, HDP_K_HEAD_BWD, 2, s);
+        CK_CUDA(hdp::launch_colreduce(1, S.dy, 1, (int)rows, 1, nullptr, c->crp, gf, c->G(si, ibo), s));
+      }
+      {
+        KScope ks_(c, HDP_K_HEAD_BWD, 2, s);
+        CK_CUDA(hdp::launch_colreduce(f32, c->dz, Fp, (int)rows, (int)Fp, nullptr, c->crp, gf, c->G(si, ifb), s));
+      }
       // dF = dz^T H   (M = Fp, N = hp, K = B*T; both operands MN-major)
-      CK(gemm(c, c->dz, Fp, 1, Htop, hp, 1, Fp, hp, rows, epi_elem(gf, c->G(si, iF), hp), s));
+      CK(gemm(c, HDP_K_HEAD_BWD, c->dz, Fp, 1, Htop, hp, 1, Fp, hp, rows, epi_elem(gf, c->G(si, iF), hp), s));
       // dH_top = dz F (M = B*T, N = hp, K = Fp; F read MN-major)
-      CK(gemm(c, c->dz, Fp, 0, c->W(iF), hp, 1, rows, hp, Fp, epi_f32(c->dH[0], hp), s));
+      CK(gemm(c, HDP_K_HEAD_BWD, c->dz, Fp, 0, c->W(iF), hp, 1, rows, hp, Fp, epi_f32(c->dH[0], hp), s));
     } else if (d.head_last_step) {
       const char* Hlast = S.Hs + ((L - 1) * hs_layer + (long)T * B * hp) * e;
-      CK_CUDA(hdp::launch_outer(f32, S.dy, c->W(iwo), c->dH[0], B, (int)hp, s));
-      CK_CUDA(hdp::launch_colreduce(f32, Hlast, hp, B, (int)hp, S.dy, c->crp, gf, c->G(si, iwo), s));
-      CK_CUDA(hdp::launch_colreduce(1, S.dy, 1, B, 1, nullptr, c->crp, gf, c->G(si, ibo), s));
+      {
+        KScope ks_(c, HDP_K_HEAD_BWD, 1, s);
+        CK_CUDA(hdp::launch_outer(f32, S.dy, c->W(iwo), c->dH[0], B, (int)hp, s));
+      }
+      {
+        KScope ks_(c, HDP_K_HEAD_BWD, 2, s);
+        CK_CUDA(hdp::launch_colreduce(f32, Hlast, hp, B, (int)hp, S.dy, c->crp, gf, c->G(si, iwo), s));
+      }
+      {
+        KScope ks_(c, HDP_K_HEAD_BWD, 2, s);
+        CK_CUDA(hdp::launch_colreduce(1, S.dy, 1, B, 1, nullptr, c->crp, gf, c->G(si, ibo), s));
+      }
     } else {
-      CK_CUDA(hdp::launch_outer(f32, S.dy, c->W(iwo), c->dH[0], (int)rows, (int)hp, s));
-      CK_CUDA(hdp::launch_colreduce(f32, Htop, hp, (int)rows, (int)hp, S.dy, c->crp, gf, c->G(si, iwo), s));
-      CK_CUDA(hdp::launch_colreduce(1, S.dy, 1, (int)rows, 1, nullptr, c->crp, gf, c->G(si, ibo), s));
+      {
+        KScope ks_(c, HDP_K_HEAD_BWD, 1, s);
+        CK_CUDA(hdp::launch_outer(f32, S.dy, c->W(iwo), c->dH[0], (int)rows, (int)hp, s));
+      }
+      {
+        KScope ks_(c, HDP_K_HEAD_BWD, 2, s);
+        CK_CUDA(hdp::launch_colreduce(f32, Htop, hp, (int)rows, (int)hp, S.dy, c->crp, gf, c->G(si, iwo), s));
+      }
+      {
+        KScope ks_(c, HDP_K_HEAD_BWD, 2, s);
+        CK_CUDA(hdp::launch_colreduce(1, S.dy, 1, (int)rows, 1, nullptr, c->crp, gf, c->G(si, ibo), s));
+      }
     }
     return HDP_OK;
   }
@@ -505,41 +609,54 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
   for (int t = T - 1; t >= 0; --t) {
     const float* dHa_t = last_only ? (t == T - 1 ? dHa : nullptr) : dHa + (long)t * B * hp;
     // K6 (A6)
-    CK_CUDA(hdp::launch_cell_bwd(f32, dHa_t, t < T - 1 ? c->dhrec : nullptr, Gl + (long)t * B * 4 * hp * e,
-                                 Cl + (long)t * B * hp, t > 0 ? Cl + (long)(t - 1) * B * hp : nullptr, c->dc,
-                                 c->dA + (long)t * B * 4 * hp * e, B, (int)hp, t == T - 1, s));
+    {
+      KScope ks_(c, HDP_K_CELL_BWD, 1, s);
+      CK_CUDA(hdp::launch_cell_bwd(f32, dHa_t, t < T - 1 ? c->dhrec : nullptr, Gl + (long)t * B * 4 * hp * e,
+                                   Cl + (long)t * B * hp, t > 0 ? Cl + (long)(t - 1) * B * hp : nullptr, c->dc,
+                                   c->dA + (long)t * B * 4 * hp * e, B, (int)hp, t == T - 1, s));
+    }
     if (t > 0)  // K7: dh_rec = dA_t U (A7); U read MN-major as [K = 4hp][N = hp]
-      CK(gemm(c, c->dA + (long)t * B * 4 * hp * e, 4 * hp, 0, c->W(iU), hp, 1, B, hp, 4 * hp,
+      CK(gemm(c, HDP_K_GEMM_DH, c->dA + (long)t * B * 4 * hp * e, 4 * hp, 0, c->W(iU), hp, 1, B, hp, 4 * hp,
               epi_f32(c->dhrec, hp), s));
   }
   // K8 (A8): dW = dA^T X, dU = dA^T H_{-1}, db = sum dA
-  CK(gemm(c, c->dA, 4 * hp, 1, X, Ipl, 1, 4 * hp, Ipl, rows, epi_elem(gf, c->G(si, iW), Ipl), s));
-  CK(gemm(c, c->dA, 4 * hp, 1, Hs, hp, 1, 4 * hp, hp, rows, epi_elem(gf, c->G(si, iU), hp), s));
-  CK_CUDA(hdp::launch_colreduce(f32, c->dA, 4 * hp, (int)rows, (int)(4 * hp), nullptr, c->crp, gf, c->G(si, ib), s));
+  CK(gemm(c, HDP_K_GEMM_DW, c->dA, 4 * hp, 1, X, Ipl, 1, 4 * hp, Ipl, rows, epi_elem(gf, c->G(si, iW), Ipl), s));
+  CK(gemm(c, HDP_K_GEMM_DW, c->dA, 4 * hp, 1, Hs, hp, 1, 4 * hp, hp, rows, epi_elem(gf, c->G(si, iU), hp), s));
+  {
+    KScope ks_(c, HDP_K_GEMM_DW, 2, s);
+    CK_CUDA(hdp::launch_colreduce(f32, c->dA, 4 * hp, (int)rows, (int)(4 * hp), nullptr, c->crp, gf, c->G(si, ib), s));
+  }
   if (l > 0) {
     // K9: dX = dA W  ->  dH_above of layer l-1 (W read MN-major as [K = 4hp][N = Ip])
-    CK(gemm(c, c->dA, 4 * hp, 0, c->W(iW), Ipl, 1, rows, Ipl, 4 * hp, epi_f32(dHnext, Ipl), s));
+    CK(gemm(c, HDP_K_GEMM_DX, c->dA, 4 * hp, 0, c->W(iW), Ipl, 1, rows, Ipl, 4 * hp, epi_f32(dHnext, Ipl), s));
   } else if (d.vocab > 0) {
-    CK(gemm(c, c->dA, 4 * hp, 0, c->W(iW), Ipl, 1, rows, Ipl, 4 * hp, epi_f32(dHnext, Ipl), s));
+    CK(gemm(c, HDP_K_GEMM_DX, c->dA, 4 * hp, 0, c->W(iW), Ipl, 1, rows, Ipl, 4 * hp, epi_f32(dHnext, Ipl), s));
     const int iE = c->find("E");
-    CK_CUDA(hdp::launch_embed_backward((const int32_t*)S.stage_x, B, T, d.vocab, dHnext, (int)c->Ip0, c->keys_in,
-                                       c->keys_out, c->vals_in, c->vals_out, c->sort_temp, c->sort_bytes,
-                                       c->G(si, iE), gf, s));
+    {
+      KScope ks_(c, HDP_K_EMBED_BWD, 2, s);
+      CK_CUDA(hdp::launch_embed_backward((const int32_t*)S.stage_x, B, T, d.vocab, dHnext, (int)c->Ip0, c->keys_in,
+                                         c->keys_out, c->vals_in, c->vals_out, c->sort_temp, c->sort_bytes,
+                                         c->G(si, iE), gf, s));
+    }
   }
   return HDP_OK;
 }
 
 int nsegs(const hdp_ctx* c) { return c->d.n_layers + 1; }
 
-// capture (once) and launch
+// capture (once) and launch; eager (no graph) while profiling
 int run_graph(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t s) {
+  if (c->prof) return seg < 0 ? enqueue_forward(c, si, B, T, s) : enqueue_backward_seg(c, si, B, T, seg, s);
   GraphKey k{si, B, T, seg};
   auto it = c->graphs.find(k);
   if (it == c->graphs.end()) {
+    const long long before = c->kernels;
     CK_CUDA(cudaStreamBeginCapture(c->cap, cudaStreamCaptureModeThreadLocal));
     int rc = seg < 0 ? enqueue_forward(c, si, B, T, c->cap) : enqueue_backward_seg(c, si, B, T, seg, c->cap);
     cudaGraph_t g = nullptr;
     cudaError_t ce = cudaStreamEndCapture(c->cap, &g);
+    const long long nk = c->kernels - before;
+    c->kernels = before;
     if (rc != HDP_OK) {
       if (g) cudaGraphDestroy(g);
       return rc;
@@ -550,8 +667,10 @@ int run_graph(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t s) {
     cudaGraphDestroy(g);
     if (ce != cudaSuccess) return fail(HDP_ERR_CUDA, "graph instantiate: %s", cudaGetErrorString(ce));
     it = c->graphs.emplace(k, ex).first;
+    c->graph_kernels[k] = nk;
   }
   CK_CUDA(cudaGraphLaunch(it->second, s));
+  c->kernels += c->graph_kernels[k];
   return HDP_OK;
 }
 
@@ -618,6 +737,7 @@ int hdp_destroy(hdp_ctx* c) {
   cudaSetDevice(c->device);
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   for (auto ev : c->ev_bucket) cudaEventDestroy(ev);
+  for (auto ev : c->evpool) cudaEventDestroy(ev);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->ev_count) cudaEventDestroy(c->ev_count);
   if (c->cap) cudaStreamDestroy(c->cap);
@@ -953,20 +1073,26 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
       a.nsrc = c->nslots;
     } else if (c->d.wire == HDP_WIRE_FP16_A2A) {
       // A9: owner j receives every rank's shard j, rank-ordered
+      KScope ks_(c, HDP_K_COMM, 0, cs);
       CK_NCCL(ncclAlltoAll(c->grads + bk.off * c->gsz, c->recv, bk.shard, gtype(c), c->comm, cs));
       a.g = c->recv;
       a.g_stride = bk.shard;
       a.nsrc = c->world;
     } else {
       // NCCL-native reduction (fp16 sum, or fp32 wire)
+      KScope ks_(c, HDP_K_COMM, 0, cs);
       CK_NCCL(ncclReduceScatter(c->grads + bk.off * c->gsz, c->recv, bk.shard, gtype(c), ncclSum, c->comm, cs));
       a.g = c->recv;
       a.g_stride = bk.shard;
       a.nsrc = 1;
     }
-    CK_CUDA(hdp::launch_avg_update(a, grad_f32, opt, cs));  // A10 / K11
+    {
+      KScope ks_(c, HDP_K_UPDATE, 1, cs);
+      CK_CUDA(hdp::launch_avg_update(a, grad_f32, opt, cs));  // A10 / K11
+    }
     if (c->world > 1) {                                     // A11: step 6 "broadcast"
       char* mine = c->w + (bk.off + (long)c->rank * bk.shard) * c->esz;
+      KScope ks_(c, HDP_K_COMM, 0, cs);
       CK_NCCL(ncclAllGather(mine, c->w + bk.off * c->esz, bk.shard, wtype(c), c->comm, cs));
     }
   }
@@ -991,6 +1117,36 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
   }
   return HDP_OK;
 }
+
+int hdp_profile(hdp_ctx* c, int enable) {
+  CK(check_ready(c));
+  c->prof = enable != 0;
+  return HDP_OK;
+}
+
+int hdp_profile_read(hdp_ctx* c, double* ms, long long* launches, int reset) {
+  CK(check_ready(c));
+  CK_CUDA(cudaDeviceSynchronize());
+  for (const auto& r : c->precs) {
+    float t = 0.f;
+    CK_CUDA(cudaEventElapsedTime(&t, r.a, r.b));
+    c->prof_ms[r.tag] += t;
+    c->prof_n[r.tag] += 1;
+  }
+  c->precs.clear();
+  c->evused = 0;
+  for (int i = 0; i < HDP_K_NTAGS; ++i) {
+    if (ms) ms[i] = c->prof_ms[i];
+    if (launches) launches[i] = c->prof_n[i];
+    if (reset) {
+      c->prof_ms[i] = 0;
+      c->prof_n[i] = 0;
+    }
+  }
+  return HDP_OK;
+}
+
+long long hdp_kernel_launches(const hdp_ctx* c) { return c ? c->kernels : -1; }
 
 void* hdp_weights_ptr(hdp_ctx* c) { return c && c->bound ? c->w : nullptr; }
 void* hdp_grads_ptr(hdp_ctx* c, int slot) {

@@ -206,39 +206,41 @@ int cr_splits(int rows) {
   return rs;
 }
 
+// fp64 accumulation: these sums (bias / head gradients) cancel strongly over
+// B*T terms; double accumulation keeps the reduction itself exact to fp32
 template <typename XT>
 __global__ void __launch_bounds__(CR_WARPS * 32)
     colreduce_pass1(const XT* __restrict__ X, long ldx, int rows, int cols, const float* __restrict__ w, int rs,
-                    float* __restrict__ partials) {
-  __shared__ float sm[CR_WARPS][33];
+                    double* __restrict__ partials) {
+  __shared__ double sm[CR_WARPS][33];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int c = blockIdx.x * 32 + lane;
   const int per = (rows + rs - 1) / rs;
   const int r0 = blockIdx.y * per, r1 = min(rows, r0 + per);
-  float acc = 0.f;
+  double acc = 0.0;
   if (c < cols)
     for (int r = r0 + warp; r < r1; r += CR_WARPS) {
       const float v = ld<XT>(X, (long)r * ldx + c);
-      acc += w ? v * w[r] : v;
+      acc += w ? (double)v * (double)w[r] : (double)v;
     }
   sm[warp][lane] = acc;
   __syncthreads();
   if (warp == 0 && c < cols) {
-    float s = 0.f;
+    double s = 0.0;
     for (int q = 0; q < CR_WARPS; ++q) s += sm[q][lane];
     partials[(long)blockIdx.y * cols + c] = s;
   }
 }
 
-__global__ void colreduce_pass2(const float* __restrict__ partials, int rs, int cols, int out_f32, void* out) {
+__global__ void colreduce_pass2(const double* __restrict__ partials, int rs, int cols, int out_f32, void* out) {
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
   if (c >= cols) return;
-  float s = 0.f;
+  double s = 0.0;
   for (int q = 0; q < rs; ++q) s += partials[(long)q * cols + c];
   if (out_f32)
-    reinterpret_cast<float*>(out)[c] = s;
+    reinterpret_cast<float*>(out)[c] = (float)s;
   else
-    reinterpret_cast<__half*>(out)[c] = __float2half_rn(s);  // R12: one RNE
+    reinterpret_cast<__half*>(out)[c] = __float2half_rn((float)s);  // R12: fp32 value, one RNE
 }
 
 // ---------------------------------------------------------------- embedding backward
@@ -367,15 +369,16 @@ cudaError_t launch_outer(int f32, const float* dy, const void* wo, float* dH, in
   return cudaGetLastError();
 }
 
-size_t colreduce_partials_floats(int rows, int cols) { return (size_t)cr_splits(rows) * cols; }
+size_t colreduce_partials_floats(int rows, int cols) { return (size_t)cr_splits(rows) * cols * 2; }
 
 cudaError_t launch_colreduce(int x_f32, const void* X, long ldx, int rows, int cols, const float* w,
                              float* partials, int out_f32, void* out, cudaStream_t s) {
   const int rs = cr_splits(rows);
   dim3 g1((cols + 31) / 32, rs);
-  if (x_f32) colreduce_pass1<float><<<g1, CR_WARPS * 32, 0, s>>>((const float*)X, ldx, rows, cols, w, rs, partials);
-  else colreduce_pass1<__half><<<g1, CR_WARPS * 32, 0, s>>>((const __half*)X, ldx, rows, cols, w, rs, partials);
-  colreduce_pass2<<<(cols + 255) / 256, 256, 0, s>>>(partials, rs, cols, out_f32, out);
+  double* part = reinterpret_cast<double*>(partials);
+  if (x_f32) colreduce_pass1<float><<<g1, CR_WARPS * 32, 0, s>>>((const float*)X, ldx, rows, cols, w, rs, part);
+  else colreduce_pass1<__half><<<g1, CR_WARPS * 32, 0, s>>>((const __half*)X, ldx, rows, cols, w, rs, part);
+  colreduce_pass2<<<(cols + 255) / 256, 256, 0, s>>>(part, rs, cols, out_f32, out);
   return cudaGetLastError();
 }
 

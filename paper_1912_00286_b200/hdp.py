@@ -28,8 +28,10 @@ EXPORTED = [
     "hdp_num_blocks", "hdp_param_block", "hdp_load_params", "hdp_gather_master", "hdp_read_weights",
     "hdp_read_grads", "hdp_set_lr_schedule", "hdp_lr", "hdp_set_loss_scale", "hdp_lstm_forward",
     "hdp_lstm_backward", "hdp_grad_average_update", "hdp_weights_ptr", "hdp_grads_ptr", "hdp_master_ptr",
-    "hdp_fused_avg_update", "hdp_gemm_f16", "hdp_gemm_f32",
+    "hdp_fused_avg_update", "hdp_gemm_f16", "hdp_gemm_f32", "hdp_profile", "hdp_profile_read",
+    "hdp_kernel_launches",
 ]
+NTAGS = 13
 
 
 class HDPError(RuntimeError):
@@ -87,6 +89,9 @@ def _load():
         "hdp_fused_avg_update": ([vp, ll, i, i, ll, vp, vp, vp, vp, vp, f, f, f, i, vp, vp, vp], i),
         "hdp_gemm_f16": ([vp, ll, i, vp, ll, i, i, i, i, vp, ll, i, vp, i, i, i, vp, ll, i, i, vp], i),
         "hdp_gemm_f32": ([vp, ll, i, vp, ll, i, i, i, i, vp, ll, i, vp, i, i, i, vp], i),
+        "hdp_profile": ([vp, i], i),
+        "hdp_profile_read": ([vp, vp, vp, i], i),
+        "hdp_kernel_launches": ([vp], ll),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
