@@ -256,6 +256,116 @@ def run_hdp(args, rank, world, local_rank):
     return out
 
 
+class _CAI:
+    def __init__(self, ptr, n, typestr):
+        self.__cuda_array_interface__ = {"shape": (n,), "typestr": typestr, "data": (ptr, False), "version": 3}
+
+
+def device_view(ptr, n, typestr, dev):
+    """torch view of library-owned device memory (no copy)."""
+    import torch
+    return torch.as_tensor(_CAI(ptr, n, typestr), device=dev)
+
+
+def run_c5(args, rank, world, local_rank):
+    """C5: fused fp16 gradient average + weight update sweep (BASELINE.json
+    configs[4]) through hdp_grad_average_update on a flat parameter vector:
+    per size, exchange (all-to-all) + K11 + allgather, timed per step with
+    CUDA events; K11 alone from the live profiler."""
+    import ctypes
+
+    import numpy as np
+    import torch
+
+    import synth
+    from paper_1912_00286_b200 import hdp
+
+    dev = torch.device(f"cuda:{local_rank}")
+    torch.cuda.set_device(dev)
+    uid = None
+    if world > 1:
+        import torch.distributed as dist
+        obj = [hdp.nccl_unique_id() if rank == 0 else None]
+        dist.broadcast_object_list(obj, src=0)
+        uid = obj[0]
+    sizes_mib = [int(v) for v in args.sizes.split(",")]
+    wire = {"fp16": hdp.WIRE_FP16_A2A, "fp16sum": hdp.WIRE_FP16_NCCLSUM, "fp32": hdp.WIRE_FP32}[args.wire]
+    gsz = 4 if wire == hdp.WIRE_FP32 else 2
+    nsim = 1 if world > 1 else max(1, args.sim)
+    stream = torch.cuda.current_stream(dev)
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
+    rows = []
+    clk = Clocks(local_rank)
+    for mib in sizes_mib:
+        S = (mib << 20) // 2          # fp16 gradient elements
+        desc = hdp.ModelDesc(n_layers=0, max_batch=1, max_seq=1, math=hdp.MATH_MIXED16, wire=wire,
+                             optimizer=hdp.OPT_SGDM, sim_workers=nsim, flat_params=S)
+        ctx = hdp.init(world, rank, uid, local_rank)
+        sz = hdp.configure(ctx, desc)
+        arena = torch.empty(sz.arena_bytes + 256, dtype=torch.uint8, device=dev)
+        base = arena.data_ptr() + ((-arena.data_ptr()) % 256)
+        hdp.bind(ctx, base, sz.arena_bytes)
+        rng = np.random.default_rng(1912 + rank)
+        hdp.load_params(ctx, rng.uniform(-0.1, 0.1, S).astype(np.float32) if rank == 0 else None, 0)
+        hdp.set_lr_schedule(ctx, 4e-4)
+        hdp.set_loss_scale(ctx, 10.0)
+        P = sz.n_params_padded
+        for sl in range(nsim):
+            dst = device_view(hdp.grads_ptr(ctx, sl), P, "<f2" if gsz == 2 else "<f4", dev)
+            dst.copy_((torch.randn(P, device=dev) * 0.05).to(dst.dtype))
+        for _ in range(args.warmup):
+            hdp.grad_average_update(ctx, 0, stream)
+        evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)) for _ in range(args.steps)]
+        torch.cuda.synchronize(dev)
+        for k in range(args.steps):
+            flush.zero_()
+            evs[k][0].record(stream)
+            hdp.grad_average_update(ctx, 0, stream)
+            evs[k][1].record(stream)
+        torch.cuda.synchronize(dev)
+        ms = statistics.mean(a.elapsed_time(b) for a, b in evs)
+        ms_by = (ctypes.c_double * len(KCLASS))()
+        n_by = (ctypes.c_longlong * len(KCLASS))()
+        hdp.lib().hdp_profile(ctx, 1)
+        hdp.lib().hdp_profile_read(ctx, ms_by, n_by, 1)
+        for _ in range(3):
+            flush.zero_()
+            hdp.grad_average_update(ctx, 0, stream)
+        hdp.lib().hdp_profile_read(ctx, ms_by, n_by, 1)
+        hdp.lib().hdp_profile(ctx, 0)
+        k11_ms = ms_by[11] / max(1, n_by[11]) * (n_by[11] / 3.0)     # per step
+        k11_launch_ms = ms_by[11] / max(1, n_by[11])
+        comm_ms = ms_by[12] / 3.0
+        own = P // world
+        nsrc = world if (world > 1 and wire != hdp.WIRE_FP16_NCCLSUM and wire != hdp.WIRE_FP32) else (1 if world > 1 else nsim)
+        k11_bytes = own * (nsrc * gsz + 18)
+        wire_bytes = 2 * (world - 1) / world * P * gsz if world > 1 else 0
+        rows.append({"mib": mib, "elements": P, "step_ms": ms, "k11_ms": k11_ms, "comm_ms": comm_ms,
+                     "k11_gbs": k11_bytes / (k11_ms * 1e-3) / 1e9,
+                     "k11_launch_us": k11_launch_ms * 1e3, "k11_bytes": k11_bytes,
+                     "busbw_gbs": (wire_bytes / (comm_ms * 1e-3) / 1e9) if world > 1 and comm_ms > 0 else None})
+        hdp.destroy(ctx)
+        del arena
+        torch.cuda.synchronize(dev)
+    clocks = clk.stop()
+    if rank != 0:
+        return None
+    pk = peaks()
+    big = rows[-1]
+    return {"metric": METRIC, "value": big["k11_gbs"], "unit": "GB/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": big["step_ms"], "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f32 (fp16 wire)" if gsz == 2 else "f32",
+            "data": "synthetic gradients N(0, 0.05^2)",
+            "config": {"workload": "C5-avg-update", "sizes_mib": sizes_mib, "wire": args.wire,
+                       "contributions": nsim if world == 1 else world, "parallelism": f"dp{world}",
+                       "l2": "flushed between timed steps"},
+            "roofline": {"bound": "hbm", "achieved": big["k11_gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                         "frac": big["k11_gbs"] / pk["hbm_gbs"], "traffic": None, "kernel": "update(K11)",
+                         "peak_src": pk["src"], "avg_launch_us": big["k11_launch_us"], "per_launch": big["k11_bytes"],
+                         "per_launch_unit": "byte"},
+            "sweep": rows, "clocks": clocks, "gpu_launches": None}
+
+
 def cpu_baseline(args, seconds=15.0, max_steps=4):
     """The oracle as it stands, on the host cores, on a bounded sample."""
     import numpy as np
@@ -333,7 +443,10 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4"])
+    ap.add_argument("--config", default="C2", choices=["C1", "C2", "C3", "C4", "C5"])
+    ap.add_argument("--sizes", default="1,4,16,64,256,1024", help="C5 sweep sizes in MiB of fp16 gradient")
+    ap.add_argument("--wire", default="fp16", choices=["fp16", "fp16sum", "fp32"], help="C5 wire format")
+    ap.add_argument("--sim", type=int, default=1, help="C5 at N=1: simulated contributions")
     ap.add_argument("--batch", type=int, default=0, help="per-rank batch (default: the config's)")
     ap.add_argument("--impl", default="hdp", choices=["hdp", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -353,9 +466,9 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
-    out = run_hdp(args, rank, world, local_rank)
+    out = run_c5(args, rank, world, local_rank) if args.config == "C5" else run_hdp(args, rank, world, local_rank)
     if rank == 0:
-        if world == 1 and not args.no_cpu_baseline:
+        if world == 1 and not args.no_cpu_baseline and args.config != "C5":
             out["cpu_baseline"] = cpu_baseline(args)
         print(json.dumps(out), flush=True)
     if world > 1:

@@ -108,7 +108,10 @@ typedef struct {
 int hdp_nccl_unique_id(unsigned char uid[HDP_UID_BYTES]);
 
 /* init(world, rank) of north_star.  world == 1 needs no uid (may be NULL).
- * Selects `device` for the calling thread and creates the communicator.  */
+ * Selects `device` for the calling thread and creates the communicator.
+ * device == -1 creates a host-only context (no CUDA, no NCCL) that can
+ * configure and answer layout / schedule queries (hdp_param_block, hdp_lr)
+ * but not bind or compute -- used by CPU tests of the host logic.        */
 int hdp_init(int world, int rank, const unsigned char* uid, int device, hdp_ctx** out);
 int hdp_destroy(hdp_ctx* ctx);
 const char* hdp_last_error(void);

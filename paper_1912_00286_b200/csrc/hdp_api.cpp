@@ -90,6 +90,7 @@ struct GraphKey {
 
 struct hdp_ctx {
   int world = 1, rank = 0, device = 0;
+  bool host_only = false;
   ncclComm_t comm = nullptr;
   // model
   bool configured = false, bound = false, loaded = false, poisoned = false;
@@ -715,14 +716,19 @@ int hdp_nccl_unique_id(unsigned char uid[HDP_UID_BYTES]) {
 }
 
 int hdp_init(int world, int rank, const unsigned char* uid, int device, hdp_ctx** out) {
-  if (!out || world < 1 || rank < 0 || rank >= world || device < 0)
+  if (!out || world < 1 || rank < 0 || rank >= world || device < -1)
     return fail(HDP_ERR_ARG, "hdp_init: bad arguments (world %d rank %d device %d)", world, rank, device);
-  if (world > 1 && !uid) return fail(HDP_ERR_ARG, "hdp_init: world > 1 needs a NCCL unique id");
-  CK_CUDA(cudaSetDevice(device));
   std::unique_ptr<hdp_ctx> c(new hdp_ctx());
   c->world = world;
   c->rank = rank;
   c->device = device;
+  if (device == -1) {  // host-only context: layout / schedule queries, no CUDA, no NCCL
+    c->host_only = true;
+    *out = c.release();
+    return HDP_OK;
+  }
+  if (world > 1 && !uid) return fail(HDP_ERR_ARG, "hdp_init: world > 1 needs a NCCL unique id");
+  CK_CUDA(cudaSetDevice(device));
   if (world > 1) {
     ncclUniqueId id;
     memcpy(&id, uid, HDP_UID_BYTES);
@@ -734,6 +740,10 @@ int hdp_init(int world, int rank, const unsigned char* uid, int device, hdp_ctx*
 
 int hdp_destroy(hdp_ctx* c) {
   if (!c) return HDP_OK;
+  if (c->host_only) {
+    delete c;
+    return HDP_OK;
+  }
   cudaSetDevice(c->device);
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   for (auto ev : c->ev_bucket) cudaEventDestroy(ev);
@@ -790,6 +800,7 @@ int hdp_bind(hdp_ctx* c, void* arena, long long bytes) {
   if (!c || !arena) return fail(HDP_ERR_ARG, "null argument");
   if (!c->configured) return fail(HDP_ERR_STATE, "configure first");
   if (c->bound) return fail(HDP_ERR_STATE, "already bound");
+  if (c->host_only) return fail(HDP_ERR_STATE, "host-only context (device -1) cannot bind device memory");
   if ((size_t)bytes < c->arena_bytes) return fail(HDP_ERR_ARG, "arena too small: %lld < %zu", bytes, c->arena_bytes);
   if (reinterpret_cast<uintptr_t>(arena) & 255) return fail(HDP_ERR_ARG, "arena must be 256-byte aligned");
   CK_CUDA(cudaSetDevice(c->device));
