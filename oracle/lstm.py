@@ -160,11 +160,16 @@ def forward(cfg, P: Dict[str, np.ndarray], x, targets, alpha: float, mode: str):
 # backward (BPTT)
 # ----------------------------------------------------------------------------
 
-def backward(cfg, P: Dict[str, np.ndarray], cache, alpha: float, mode: str) -> Dict[str, np.ndarray]:
+def backward(cfg, P: Dict[str, np.ndarray], cache, alpha: float, mode: str,
+             abs_terms: Dict[str, np.ndarray] = None) -> Dict[str, np.ndarray]:
     """Gradients of L = alpha * mean hinge w.r.t. every parameter block.
 
     In mixed mode each returned gradient is rounded once to fp16 (R12); the
-    caller counts non-finite values.
+    caller counts non-finite values.  If ``abs_terms`` is a dict, it receives
+    for the bias-type blocks (b_l, fb, bo) the sum of the absolute values of
+    the B*T terms each element sums -- the scale of any finite-precision
+    evaluation's rounding error for those sums (diagnostic only; the
+    gradients are unchanged).
     """
     q = _q16(mode)
     h = cfg.hidden
@@ -177,12 +182,16 @@ def backward(cfg, P: Dict[str, np.ndarray], cache, alpha: float, mode: str) -> D
     dy = np.where(margin > 0.0, -alpha * tt / n_terms, 0.0)
     G: Dict[str, np.ndarray] = {}
     G["bo"] = np.array([dy.sum()])
+    if abs_terms is not None:
+        abs_terms["bo"] = np.array([np.abs(dy).sum()])
     if cfg.fc_hidden > 0:
         z, zpre = cache["z"], cache["zpre"]
         G["wo"] = dy.reshape(-1) @ z.reshape(-1, z.shape[-1])
         dz = q(dy[..., None] * P["wo"][None, None, :] * (zpre > 0.0))   # R9
         G["F"] = dz.reshape(-1, dz.shape[-1]).T @ Htop.reshape(-1, h)
         G["fb"] = dz.sum(axis=(0, 1))
+        if abs_terms is not None:
+            abs_terms["fb"] = np.abs(dz).sum(axis=(0, 1))
         dH_above = dz @ P["F"]                   # [T][B][h], R11 (not rounded)
     elif cfg.head_last_step:
         G["wo"] = dy @ Htop[T - 1]
@@ -220,6 +229,8 @@ def backward(cfg, P: Dict[str, np.ndarray], cache, alpha: float, mode: str) -> D
         G[f"W{l}"] = dA2.T @ X.reshape(-1, X.shape[-1])
         G[f"U{l}"] = dA2.T @ Hprev.reshape(-1, h)
         G[f"b{l}"] = dA_all.sum(axis=(0, 1))
+        if abs_terms is not None:
+            abs_terms[f"b{l}"] = np.abs(dA_all).sum(axis=(0, 1))
         if l > 0:
             dH_above = dA_all @ W                # dX of layer l -> layer l-1
         elif cfg.vocab > 0:

@@ -26,11 +26,11 @@ def working_weights(master: np.ndarray, mode: str) -> np.ndarray:
     return r16(master) if mode == "mixed" else np.asarray(master, np.float64)
 
 
-def worker_grads(cfg, wflat, x, targets, alpha, mode):
+def worker_grads(cfg, wflat, x, targets, alpha, mode, abs_terms=None):
     """Steps 3 for one worker: returns (L_r scaled, flat gradient, y)."""
     P = lstm.unpack(cfg, wflat)
     L, y, cache = lstm.forward(cfg, P, x, targets, alpha, mode)
-    G = lstm.backward(cfg, P, cache, alpha, mode)
+    G = lstm.backward(cfg, P, cache, alpha, mode, abs_terms)
     return L, lstm.pack(cfg, G), y
 
 
@@ -45,12 +45,14 @@ def train_step(cfg, master, state: Dict[str, np.ndarray], x_global, t_global, N:
     assert B % N == 0
     b = B // N
     w = working_weights(master, mode)
-    losses, grads = [], []
+    losses, grads, abs_terms = [], [], []
     for r in range(N):
         sl = slice(r * b, (r + 1) * b)
-        L, g, _ = worker_grads(cfg, w, x_global[sl], t_global[sl], alpha, mode)
+        at = {}
+        L, g, _ = worker_grads(cfg, w, x_global[sl], t_global[sl], alpha, mode, at)
         losses.append(L)
         grads.append(g)
+        abs_terms.append(at)
     if grads_override is not None:
         grads = grads_override
     nonfinite = sum(count_nonfinite(g) for g in grads)
@@ -65,6 +67,7 @@ def train_step(cfg, master, state: Dict[str, np.ndarray], x_global, t_global, N:
         "loss": float(np.sum(losses) / (N * alpha)),
         "losses_scaled": losses,
         "grads": grads,
+        "abs_terms": abs_terms,
         "avg": avg,
         "master": W,
         "state": new_state,
