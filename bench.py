@@ -32,7 +32,8 @@ METRIC = "LSTM training samples/s at 1/2/4/8 B200; avg+update GB/s vs HBM peak"
 
 # kernel classes of include/hdp.h (HDP_K_*)
 KCLASS = ["input", "gemm_x(K1)", "gemm_h(K2)", "cell_fwd(K3)", "head_fwd(K4)", "head_bwd(K5)", "cell_bwd(K6)",
-          "gemm_dh(K7)", "gemm_dw(K8)", "gemm_dx(K9)", "embed_bwd(K10)", "update(K11)", "comm(A9/A11)"]
+          "gemm_dh(K7)", "gemm_dw(K8)", "gemm_dx(K9)", "embed_bwd(K10)", "update(K11)", "comm(A9/A11)",
+          "recur_fwd(K2+K3)", "recur_bwd(K6+K7)"]
 
 
 def peaks():
@@ -99,6 +100,8 @@ def algorithmic_work(cfg, B, world):
     w["gemm_x(K1)"] = ("flop", sum(2.0 * B * T * 4 * h * i for i in ins) / L)
     w["gemm_dw(K8)"] = ("flop", sum(2.0 * 4 * h * (i + h) * B * T for i in ins) / (3 * L))  # dW, dU, db launches
     w["gemm_dx(K9)"] = ("flop", 2.0 * B * T * 4 * h * h)
+    w["recur_fwd(K2+K3)"] = ("flop", 2.0 * B * 4 * h * h * (T - 1))   # one launch = all T steps of a layer
+    w["recur_bwd(K6+K7)"] = ("flop", 2.0 * B * 4 * h * h * (T - 1))
     w["cell_fwd(K3)"] = ("byte", 50.0 * B * h)   # Gx 16 + Gh 16 + c_prev 4 + gates 8 + c 4 + h 2
     w["cell_bwd(K6)"] = ("byte", 40.0 * B * h)   # dHa 4 + dh_rec 4 + gates 8 + c 4 + c_prev 4 + dc 8 + dA 8
     return w

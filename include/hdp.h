@@ -191,7 +191,9 @@ enum { HDP_K_INPUT = 0,     /* input packing / embedding gather (A1 prologue, K1
        HDP_K_EMBED_BWD = 10,/* K10 embedding scatter-add (A8)                      */
        HDP_K_UPDATE = 11,   /* K11 fused average + update (A10)                    */
        HDP_K_COMM = 12,     /* NCCL exchange / allgather (A9, A11)                 */
-       HDP_K_NTAGS = 13 };
+       HDP_K_RECUR_FWD = 13,/* persistent fused K2+K3 over all t (A2+A3)           */
+       HDP_K_RECUR_BWD = 14,/* persistent fused K6+K7 over all t (A6+A7)           */
+       HDP_K_NTAGS = 15 };
 /* enable != 0: subsequent forward / backward run eagerly (no CUDA graphs)
  * with a CUDA event pair around every launch on its stream.              */
 int hdp_profile(hdp_ctx* ctx, int enable);

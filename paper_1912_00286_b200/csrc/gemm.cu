@@ -337,6 +337,29 @@ int make_tmap(CUtensorMap* m, const void* base, uint64_t inner, uint64_t outer, 
   return 0;
 }
 
+}  // namespace
+
+int encode_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
+                   uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw) {
+  if (!get_encode()) {
+    snprintf(g_gemm_err, sizeof g_gemm_err, "cuTensorMapEncodeTiled unavailable");
+    return -2;
+  }
+  cuuint64_t dims[2] = {inner, outer};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_inner, box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = g_encode(m, dt, 2, const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                        sw, CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    snprintf(g_gemm_err, sizeof g_gemm_err, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    return -2;
+  }
+  return 0;
+}
+
+namespace {
+
 template <int BN, int AMN, int BMN>
 cudaError_t launch_tc(const GemmPlan& p, cudaStream_t s) {
   using C = TileCfg<BN>;

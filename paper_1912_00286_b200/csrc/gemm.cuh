@@ -66,4 +66,8 @@ cudaError_t gemm_init();
 
 const char* gemm_last_error();
 
+// Generic 2-D tensor map (inner dimension contiguous); 0 on success.
+int encode_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uint64_t inner, uint64_t outer,
+                   uint64_t row_stride_bytes, uint32_t box_inner, uint32_t box_outer, CUtensorMapSwizzle sw);
+
 }  // namespace hdp

@@ -14,6 +14,7 @@
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <memory>
@@ -23,6 +24,7 @@
 
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "recur.cuh"
 
 namespace {
 
@@ -96,6 +98,7 @@ struct hdp_ctx {
   bool configured = false, bound = false, loaded = false, poisoned = false;
   hdp_model_desc d{};
   bool f32 = false;       // FP32 math mode
+  bool persistent = true; // persistent fused recurrence kernels where they fit (env HDP_PERSISTENT=0 disables)
   bool gf32 = false;      // fp32 gradients / wire
   int nslots = 1;
   long hp = 0, Ip0 = 0, Fp = 0, esz = 2, gsz = 2;
@@ -467,6 +470,22 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
     char* Gl = S.gates + l * g_layer * e;
     // K1: G_x = X W^T + b for all t (A1)
     CK(gemm(c, HDP_K_GEMM_X, X, Ipl, 0, c->W(iW), Ipl, 0, rows, 4 * hp, Ipl, epi_f32(c->Gx, 4 * hp, c->W(ib), !f32), s));
+    if (!f32 && c->persistent && hdp::recur_fwd_supported(B, (int)hp)) {
+      // A2 + A3 for all t in one persistent kernel (U resident in SMEM)
+      hdp::RecurFwdArgs ra;
+      ra.U = (const __half*)c->W(iU);
+      ra.Gx = c->Gx;
+      ra.Hs = (__half*)Hs;
+      ra.C = Cl;
+      ra.gates = (__half*)Gl;
+      ra.counter = (unsigned*)((char*)c->status + 64);
+      ra.T = T;
+      ra.B = B;
+      ra.hp = (int)hp;
+      KScope ks_(c, HDP_K_RECUR_FWD, 1, s);
+      CK_CUDA(hdp::launch_recur_fwd(ra, s));
+      continue;
+    }
     for (int t = 0; t < T; ++t) {
       if (t > 0)  // K2: G_h = h_{t-1} U^T (A2)
         CK(gemm(c, HDP_K_GEMM_H, Hs + (long)t * B * hp * e, hp, 0, c->W(iU), hp, 0, B, 4 * hp, hp, epi_f32(c->Gh, 4 * hp), s));
@@ -779,6 +798,10 @@ int hdp_configure(hdp_ctx* c, const hdp_model_desc* desc, hdp_sizes* out) {
   if (d.math == HDP_MATH_FP32 && d.wire == HDP_WIRE_FP16_NCCLSUM)
     return fail(HDP_ERR_ARG, "FP32 math cannot use the fp16 NCCL-sum wire");
   c->d = d;
+  {
+    const char* ev = getenv("HDP_PERSISTENT");
+    c->persistent = !(ev && ev[0] == '0');
+  }
   c->f32 = d.math == HDP_MATH_FP32;
   c->gf32 = c->f32 || d.wire == HDP_WIRE_FP32;
   c->esz = c->f32 ? 4 : 2;

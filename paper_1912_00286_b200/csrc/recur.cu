@@ -1,0 +1,268 @@
+// Persistent fused LSTM recurrence for small h:
+// one cooperative kernel runs all T steps of one layer's forward pass.
+//
+//   a_t = G_x[t] + h_{t-1} U^T ;  i,f,o = sigma(a), g = tanh(a)
+//   c_t = f c_{t-1} + i g ;  h_t = o tanh(c_t)          (reading Q1)
+//
+// CTA k owns 128 interleaved gate rows = 32 units [32k, 32k+32).  Its U slice
+// (128 x h_p fp16, K-major SWIZZLE_128B) is loaded ONCE by TMA and stays in
+// shared memory for all T steps.  Per step:
+//   1. TMA prefetch of this CTA's G_x[t] slice (B x 128 fp32) -- independent of
+//      the recurrence, issued before the grid barrier;
+//   2. grid barrier: wait until every CTA published h_{t-1} (monotonic counter,
+//      release/acquire at gpu scope);
+//   3. TMA load of h_{t-1} (B x h_p fp16) and tcgen05.mma (M=128 gate rows,
+//      N=B, K=h_p) into TMEM;
+//   4. epilogue: tcgen05.ld -> a = acc + G_x; each lane activates its own gate,
+//      a 4x4 shuffle transpose inside each quad gives every lane all four
+//      gates of its unit for 1/4 of the columns; c stays in registers across
+//      steps; h_t (fp16), c_t (fp32) and the rounded gates are stored;
+//   5. publish: fence + release-add on the step counter.
+// Layout conventions are those of hdp_api.cpp (gate row 4j+g).
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+#include "gemm.cuh"
+#include "ptx.cuh"
+#include "recur.cuh"
+
+namespace hdp {
+namespace {
+
+constexpr int RT_THREADS = 128;
+
+__device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + expf(-x)); }
+
+__device__ __forceinline__ void release_add(unsigned* p, unsigned v) {
+  asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ unsigned acquire_ld(const unsigned* p) {
+  unsigned v;
+  asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+
+// select v[q*4 + sel] for runtime sel in [0,4)
+__device__ __forceinline__ float pick4(const float (&v)[16], int q, int sel) {
+  const float a = v[q * 4 + 0], b = v[q * 4 + 1], c = v[q * 4 + 2], d = v[q * 4 + 3];
+  return sel == 0 ? a : sel == 1 ? b : sel == 2 ? c : d;
+}
+
+// smem: [U: nkb x 16 KB][H: nkb x B*128 B][Gx: B x 128 fp32][barriers]
+template <int BN>
+__global__ void __launch_bounds__(RT_THREADS, 1)
+    recur_fwd_kernel(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmH,
+                     const __grid_constant__ CUtensorMap tmG, int T, int B, int hp, __half* __restrict__ Hs,
+                     float* __restrict__ Cst, __half* __restrict__ gates, unsigned* __restrict__ counter) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int nkb = (hp + 63) / 64;
+  const int nk16 = (hp + 15) / 16;
+  uint8_t* sU = smem;
+  uint8_t* sH = sU + nkb * 16384;
+  float* sG = reinterpret_cast<float*>(sH + (size_t)nkb * BN * 128);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sG) + (size_t)BN * 128 * 4);
+  uint64_t* barU = bars;
+  uint64_t* barH = bars + 1;
+  uint64_t* barG = bars + 2;
+  uint64_t* barM = bars + 3;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int row0 = blockIdx.x * 128;          // first gate row of this CTA
+  const int r = warp * 32 + lane;              // tile row = TMEM lane
+  const int grow = row0 + r;                   // gate row
+  const int gate = r & 3;
+  const int unit = grow >> 2;
+  const bool unit_ok = unit < hp;
+  const int fourhp = 4 * hp;
+
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch(&tmU);
+    ptx::tma_prefetch(&tmH);
+    ptx::tma_prefetch(&tmG);
+    for (int i = 0; i < 4; ++i) ptx::mbar_init(bars + i, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tslot, BN);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_arrive_expect_tx(barU, nkb * 16384);
+    for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sU + kb * 16384, &tmU, barU, kb * 64, row0);
+    ptx::mbar_wait(barU, 0);
+  }
+
+  // per-lane cell state for its (unit, column) pairs: columns c0 + 4q + gate
+  float creg[BN / 4];
+#pragma unroll
+  for (int i = 0; i < BN / 4; ++i) creg[i] = 0.f;
+
+  const uint32_t idesc = ptx::idesc_f16_f32(128, B, 0, 0);  // N = B (multiple of 16, <= BN)
+  const int nchunk = B / 16;
+
+  for (int t = 0; t < T; ++t) {
+    const uint32_t ph = t & 1;
+    // (1) G_x[t] slice -> smem (independent of the recurrence)
+    if (threadIdx.x == 0) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic smem reads vs TMA writes
+      ptx::mbar_arrive_expect_tx(barG, B * 128 * 4);
+      ptx::tma_load_2d(sG, &tmG, barG, row0, t * B);
+    }
+    if (t > 0) {
+      // (2) grid barrier: all CTAs published h_{t-1}
+      if (threadIdx.x == 0) {
+        const unsigned target = (unsigned)(G * t);
+        if (acquire_ld(counter) < target) {
+          const uint64_t t0 = ptx::globaltimer_ns();
+          while (acquire_ld(counter) < target) {
+            if (ptx::globaltimer_ns() - t0 > 10000000000ull) __trap();
+          }
+        }
+        fence_proxy_async();
+        // (3) h_{t-1} = Hs slot t -> smem, then MMA
+        ptx::mbar_arrive_expect_tx(barH, nkb * B * 128);
+        for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sH + kb * B * 128, &tmH, barH, kb * 64, t * B);
+        ptx::mbar_wait(barH, (t - 1) & 1);
+        ptx::tc_fence_after();
+        const uint32_t aU = ptx::smem_u32(sU), aH = ptx::smem_u32(sH);
+        for (int k = 0; k < nk16; ++k) {
+          const int kb = k >> 2, kk = k & 3;
+          const uint64_t ad = ptx::smem_desc_sw128(aU + kb * 16384 + kk * 32, 0, 1024);
+          const uint64_t bd = ptx::smem_desc_sw128(aH + kb * B * 128 + kk * 32, 0, 1024);
+          ptx::mma_f16(tbase, ad, bd, idesc, k > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(barM);
+      }
+      __syncwarp();
+      ptx::mbar_wait(barM, (t - 1) & 1);
+      ptx::tc_fence_after();
+    }
+    ptx::mbar_wait(barG, ph);
+
+    // (4) epilogue
+    __half* hout = Hs + (size_t)(t + 1) * B * hp;
+    float* cout = Cst + (size_t)t * B * hp;
+    __half* gout = gates + (size_t)t * B * fourhp;
+#pragma unroll
+    for (int ch = 0; ch < BN / 16; ++ch) {
+      if (ch >= nchunk) break;
+      const int c0 = ch * 16;
+      float v[16];
+      if (t > 0) {
+        ptx::tmem_ld16(tbase + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) {
+        const float a = v[k] + sG[(c0 + k) * 128 + r];
+        v[k] = gate == 2 ? tanhf(a) : sigm(a);
+      }
+      // 4x4 transpose inside each quad: lane (gate g) gathers gates 0..3 of
+      // its unit for columns c0 + 4q + g, q = 0..3
+      // round rr delivers gate (gate + rr) & 3; recv[q*4 + rr]
+      float recv[16];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+#pragma unroll
+        for (int rr = 0; rr < 4; ++rr) {
+          const float send = pick4(v, q, (gate - rr) & 3);
+          recv[q * 4 + rr] = __shfl_sync(0xffffffffu, send, (lane & ~3) | ((gate + rr) & 3));
+        }
+      }
+      if (unit_ok) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int b = c0 + 4 * q + gate;
+          const float i = pick4(recv, q, (0 - gate) & 3), f = pick4(recv, q, (1 - gate) & 3);
+          const float g = pick4(recv, q, (2 - gate) & 3), o = pick4(recv, q, (3 - gate) & 3);
+          const float c = f * creg[ch * 4 + q] + i * g;
+          creg[ch * 4 + q] = c;
+          const float h = o * tanhf(c);
+          cout[(size_t)b * hp + unit] = c;                   // R5
+          hout[(size_t)b * hp + unit] = __float2half_rn(h);  // R6
+          __align__(8) __half2 gg[2] = {__halves2half2(__float2half_rn(i), __float2half_rn(f)),
+                                        __halves2half2(__float2half_rn(g), __float2half_rn(o))};
+          *reinterpret_cast<uint2*>(gout + (size_t)b * fourhp + 4 * unit) =
+              *reinterpret_cast<const uint2*>(gg);           // R4
+        }
+      }
+    }
+    // (5) publish h_t
+    ptx::tc_fence_before();
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      release_add(counter, 1u);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tbase, BN);
+  }
+}
+
+template <int BN>
+size_t fwd_smem(int hp) {
+  const int nkb = (hp + 63) / 64;
+  return 1024 + (size_t)nkb * 16384 + (size_t)nkb * BN * 128 + (size_t)BN * 128 * 4 + 128;
+}
+
+template <int BN>
+cudaError_t launch_fwd_bn(const RecurFwdArgs& a, cudaStream_t s) {
+  CUtensorMap mU, mH, mG;
+  if (encode_tmap_2d(&mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U, a.hp, 4 * a.hp, a.hp * 2, 64, 128,
+               CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  if (encode_tmap_2d(&mH, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.Hs, a.hp, (uint64_t)(a.T + 1) * a.B, a.hp * 2, 64, a.B,
+               CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  if (encode_tmap_2d(&mG, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.Gx, 4 * a.hp, (uint64_t)a.T * a.B, 4 * a.hp * 4, 128, a.B,
+               CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
+  const size_t smem = fwd_smem<BN>(a.hp);
+  cudaError_t e = cudaFuncSetAttribute(recur_fwd_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((4 * a.hp + 127) / 128));
+  cfg.blockDim = dim3(RT_THREADS);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, recur_fwd_kernel<BN>, mU, mH, mG, a.T, a.B, a.hp, a.Hs, a.C, a.gates,
+                            a.counter);
+}
+
+}  // namespace
+
+bool recur_fwd_supported(int B, int hp) {
+  if (B < 16 || B > 256 || (B & 15) || (hp & 15)) return false;
+  const int bn = B <= 64 ? 64 : (B <= 128 ? 128 : 256);
+  const size_t smem = bn == 64 ? fwd_smem<64>(hp) : bn == 128 ? fwd_smem<128>(hp) : fwd_smem<256>(hp);
+  const int ctas = (4 * hp + 127) / 128;
+  return smem <= 227 * 1024 && ctas <= 148;
+}
+
+cudaError_t launch_recur_fwd(const RecurFwdArgs& a, cudaStream_t s) {
+  cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  if (a.B <= 64) return launch_fwd_bn<64>(a, s);
+  if (a.B <= 128) return launch_fwd_bn<128>(a, s);
+  return launch_fwd_bn<256>(a, s);
+}
+
+}  // namespace hdp

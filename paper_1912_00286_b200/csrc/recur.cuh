@@ -1,0 +1,21 @@
+// Persistent fused LSTM recurrence kernels.
+#pragma once
+#include <cuda_fp16.h>
+#include <cuda_runtime.h>
+
+namespace hdp {
+
+struct RecurFwdArgs {
+  const __half* U = nullptr;  // [4hp][hp] gate rows interleaved (4j+g)
+  const float* Gx = nullptr;  // [T][B][4hp] = X W^T + b
+  __half* Hs = nullptr;       // [T+1][B][hp]; slot 0 = h_{-1} = 0 (read), slots 1..T written
+  float* C = nullptr;         // [T][B][hp]
+  __half* gates = nullptr;    // [T][B][4hp] activated gates, fp16 (R4)
+  unsigned* counter = nullptr;  // grid-barrier counter (zeroed by the launcher)
+  int T = 0, B = 0, hp = 0;
+};
+
+bool recur_fwd_supported(int B, int hp);
+cudaError_t launch_recur_fwd(const RecurFwdArgs& a, cudaStream_t s);
+
+}  // namespace hdp

@@ -31,7 +31,7 @@ EXPORTED = [
     "hdp_fused_avg_update", "hdp_gemm_f16", "hdp_gemm_f32", "hdp_profile", "hdp_profile_read",
     "hdp_kernel_launches",
 ]
-NTAGS = 13
+NTAGS = 15
 
 
 class HDPError(RuntimeError):

@@ -118,3 +118,42 @@ def test_c4_stacked_reduced_mixed():
     assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
     assert _max(r["grad_err"][0]) <= 2e-2, r["grad_err"]
     assert _max(r["master_err"]) <= 2e-2
+
+
+# ---------------------------------------------------------------- persistent recurrence path
+# B >= 16 and small h select the persistent fused recurrence kernel (one
+# cooperative launch per layer); these cases cover 1 CTA (h = 32), 8 CTAs
+# (h = 256) and a ragged batch.
+
+def test_c1_persistent_b16_mixed():
+    cfg = synth.CONFIGS["C1"]
+    recs = run_parity(cfg, 32, 2, steps=3, mixed=True)
+    for r in recs:
+        assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
+        for ge in r["grad_err"]:
+            assert _max(ge) <= 2e-2, ge
+    assert _max(recs[-1]["master_err"]) <= 2e-2
+
+
+def test_c3_persistent_b48_mixed():
+    cfg = synth.CONFIGS["C3"].with_(seq=40)
+    recs = run_parity(cfg, 48, 1, steps=2, mixed=True)
+    for r in recs:
+        assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
+        assert _max(r["grad_err"][0]) <= 2e-2, r["grad_err"]
+    assert _max(recs[-1]["master_err"]) <= 2e-2
+
+
+def test_persistent_matches_per_step_path(monkeypatch):
+    """The persistent kernel and the per-step GEMM + cell path compute the
+    same thing (fp32 accumulation order is the only difference)."""
+    import numpy as np
+    cfg = synth.CONFIGS["C2"].with_(seq=32)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("HDP_PERSISTENT", flag)
+        recs = run_parity(cfg, 64, 1, steps=1, mixed=True)
+        out[flag] = recs[0]
+    for k in out["1"]["grad_err"][0]:
+        assert out["1"]["grad_err"][0][k] <= 2e-2 and out["0"]["grad_err"][0][k] <= 2e-2
+    assert abs(out["1"]["loss_gpu"] - out["0"]["loss_gpu"]) <= 1e-4
