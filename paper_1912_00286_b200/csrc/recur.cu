@@ -29,7 +29,8 @@
 namespace hdp {
 namespace {
 
-constexpr int RT_THREADS = 128;
+constexpr int RT_WARPS = 16;  // 4 lane quarters x 4 column groups
+constexpr int RT_THREADS = RT_WARPS * 32;
 
 __device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + expf(-x)); }
 
@@ -70,9 +71,11 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int quarter = warp & 3;                // TMEM lane quarter this warp may access
+  const int cg = warp >> 2;                    // column group: chunks ch = 4*ci + cg
   const int G = gridDim.x;
   const int row0 = blockIdx.x * 128;          // first gate row of this CTA
-  const int r = warp * 32 + lane;              // tile row = TMEM lane
+  const int r = quarter * 32 + lane;           // tile row = TMEM lane
   const int grow = row0 + r;                   // gate row
   const int gate = r & 3;
   const int unit = grow >> 2;
@@ -99,9 +102,10 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
   }
 
   // per-lane cell state for its (unit, column) pairs: columns c0 + 4q + gate
-  float creg[BN / 4];
+  constexpr int NCI = BN / 64;  // chunks per column group
+  float creg[NCI * 4];
 #pragma unroll
-  for (int i = 0; i < BN / 4; ++i) creg[i] = 0.f;
+  for (int i = 0; i < NCI * 4; ++i) creg[i] = 0.f;
 
   const uint32_t idesc = ptx::idesc_f16_f32(128, B, 0, 0);  // N = B (multiple of 16, <= BN)
   const int nchunk = B / 16;
@@ -150,12 +154,13 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
     float* cout = Cst + (size_t)t * B * hp;
     __half* gout = gates + (size_t)t * B * fourhp;
 #pragma unroll
-    for (int ch = 0; ch < BN / 16; ++ch) {
+    for (int ci = 0; ci < NCI; ++ci) {
+      const int ch = ci * 4 + cg;
       if (ch >= nchunk) break;
       const int c0 = ch * 16;
       float v[16];
       if (t > 0) {
-        ptx::tmem_ld16(tbase + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
+        ptx::tmem_ld16(tbase + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
       } else {
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = 0.f;
@@ -183,8 +188,8 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
           const int b = c0 + 4 * q + gate;
           const float i = pick4(recv, q, (0 - gate) & 3), f = pick4(recv, q, (1 - gate) & 3);
           const float g = pick4(recv, q, (2 - gate) & 3), o = pick4(recv, q, (3 - gate) & 3);
-          const float c = f * creg[ch * 4 + q] + i * g;
-          creg[ch * 4 + q] = c;
+          const float c = f * creg[ci * 4 + q] + i * g;
+          creg[ci * 4 + q] = c;
           const float h = o * tanhf(c);
           cout[(size_t)b * hp + unit] = c;                   // R5
           hout[(size_t)b * hp + unit] = __float2half_rn(h);  // R6
