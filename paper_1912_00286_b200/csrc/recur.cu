@@ -32,7 +32,11 @@ namespace {
 constexpr int RT_WARPS = 16;  // 4 lane quarters x 4 column groups
 constexpr int RT_THREADS = RT_WARPS * 32;
 
-__device__ __forceinline__ float sigm(float x) { return 1.f / (1.f + expf(-x)); }
+// sigma(x) with the SFU exponential; relative error ~1e-6, far below the
+// fp16 rounding (R4, R6) applied to everything this kernel stores.
+__device__ __forceinline__ float sigm_fast(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
+// branch-free gate activation: tanh(a) = 2 sigma(2a) - 1 for the g gate
+__device__ __forceinline__ float act_gate(float a, float s) { return fmaf(s, sigm_fast(s * a), 1.f - s); }
 
 __device__ __forceinline__ void release_add(unsigned* p, unsigned v) {
   asm volatile("red.release.gpu.global.add.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
@@ -44,17 +48,12 @@ __device__ __forceinline__ unsigned acquire_ld(const unsigned* p) {
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
-// select v[q*4 + sel] for runtime sel in [0,4)
-__device__ __forceinline__ float pick4(const float (&v)[16], int q, int sel) {
-  const float a = v[q * 4 + 0], b = v[q * 4 + 1], c = v[q * 4 + 2], d = v[q * 4 + 3];
-  return sel == 0 ? a : sel == 1 ? b : sel == 2 ? c : d;
-}
-
-// smem: [U: nkb x 16 KB][H: nkb x B*128 B][Gx: B x 128 fp32][barriers]
+// smem: [U: nkb x 16 KB][H: nkb x BN*128 B][act: 16 warps x 16 x 40 fp32][barriers]
+constexpr int ACT_LD = 40;  // 32 rows + 8 pad: conflict-free float4 reads (see epilogue)
 template <int BN>
 __global__ void __launch_bounds__(RT_THREADS, 1)
     recur_fwd_kernel(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmH,
-                     const __grid_constant__ CUtensorMap tmG, int T, int B, int hp, __half* __restrict__ Hs,
+                     const float* __restrict__ Gx, int T, int B, int hp, __half* __restrict__ Hs,
                      float* __restrict__ Cst, __half* __restrict__ gates, unsigned* __restrict__ counter) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -62,8 +61,8 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
   const int nk16 = (hp + 15) / 16;
   uint8_t* sU = smem;
   uint8_t* sH = sU + nkb * 16384;
-  float* sG = reinterpret_cast<float*>(sH + (size_t)nkb * BN * 128);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sG) + (size_t)BN * 128 * 4);
+  float* sAct = reinterpret_cast<float*>(sH + (size_t)nkb * BN * 128);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sAct + RT_WARPS * 16 * ACT_LD);
   uint64_t* barU = bars;
   uint64_t* barH = bars + 1;
   uint64_t* barG = bars + 2;
@@ -85,7 +84,6 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
   if (threadIdx.x == 0) {
     ptx::tma_prefetch(&tmU);
     ptx::tma_prefetch(&tmH);
-    ptx::tma_prefetch(&tmG);
     for (int i = 0; i < 4; ++i) ptx::mbar_init(bars + i, 1);
     ptx::fence_mbar_init();
   }
@@ -110,13 +108,18 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
   const uint32_t idesc = ptx::idesc_f16_f32(128, B, 0, 0);  // N = B (multiple of 16, <= BN)
   const int nchunk = B / 16;
 
+  float* myAct = sAct + warp * 16 * ACT_LD;
+  const float gsc = gate == 2 ? 2.f : 1.f;
   for (int t = 0; t < T; ++t) {
-    const uint32_t ph = t & 1;
-    // (1) G_x[t] slice -> smem (independent of the recurrence)
-    if (threadIdx.x == 0) {
-      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // prior generic smem reads vs TMA writes
-      ptx::mbar_arrive_expect_tx(barG, B * 128 * 4);
-      ptx::tma_load_2d(sG, &tmG, barG, row0, t * B);
+    // (1) G_x[t] for this warp's chunks -> registers (independent of the recurrence;
+    //     issued before the grid barrier so its latency overlaps the wait)
+    float gx[NCI][16];
+#pragma unroll
+    for (int ci = 0; ci < NCI; ++ci) {
+      const int ch = ci * 4 + cg;
+#pragma unroll
+      for (int k = 0; k < 16; ++k)
+        gx[ci][k] = (ch < nchunk && grow < fourhp) ? __ldg(Gx + ((size_t)t * B + ch * 16 + k) * fourhp + grow) : 0.f;
     }
     if (t > 0) {
       // (2) grid barrier: all CTAs published h_{t-1}
@@ -147,7 +150,6 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
       ptx::mbar_wait(barM, (t - 1) & 1);
       ptx::tc_fence_after();
     }
-    ptx::mbar_wait(barG, ph);
 
     // (4) epilogue
     __half* hout = Hs + (size_t)(t + 1) * B * hp;
@@ -165,32 +167,23 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = 0.f;
       }
+      // activate own gate, stage [col][row] in this warp's smem tile (rows = its 32 gate rows)
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const float a = v[k] + sG[(c0 + k) * 128 + r];
-        v[k] = gate == 2 ? tanhf(a) : sigm(a);
-      }
-      // 4x4 transpose inside each quad: lane (gate g) gathers gates 0..3 of
-      // its unit for columns c0 + 4q + g, q = 0..3
-      // round rr delivers gate (gate + rr) & 3; recv[q*4 + rr]
-      float recv[16];
-#pragma unroll
-      for (int q = 0; q < 4; ++q) {
-#pragma unroll
-        for (int rr = 0; rr < 4; ++rr) {
-          const float send = pick4(v, q, (gate - rr) & 3);
-          recv[q * 4 + rr] = __shfl_sync(0xffffffffu, send, (lane & ~3) | ((gate + rr) & 3));
-        }
-      }
+      for (int k = 0; k < 16; ++k) myAct[k * ACT_LD + lane] = act_gate(v[k] + gx[ci][k], gsc);
+      __syncwarp();
       if (unit_ok) {
+        // lane = (unit u = lane>>2, column class g = lane&3): columns c0 + 4q + g
+        // float4 at [col][4u]: slots (col*10 + u) mod 8 distinct in each 8-lane phase
+        const int u = lane >> 2;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-          const int b = c0 + 4 * q + gate;
-          const float i = pick4(recv, q, (0 - gate) & 3), f = pick4(recv, q, (1 - gate) & 3);
-          const float g = pick4(recv, q, (2 - gate) & 3), o = pick4(recv, q, (3 - gate) & 3);
+          const int col = 4 * q + gate;
+          const float4 a4 = *reinterpret_cast<const float4*>(myAct + col * ACT_LD + 4 * u);
+          const int b = c0 + col;
+          const float i = a4.x, f = a4.y, g = a4.z, o = a4.w;
           const float c = f * creg[ci * 4 + q] + i * g;
           creg[ci * 4 + q] = c;
-          const float h = o * tanhf(c);
+          const float h = o * act_gate(c, 2.f);   // o * tanh(c)
           cout[(size_t)b * hp + unit] = c;                   // R5
           hout[(size_t)b * hp + unit] = __float2half_rn(h);  // R6
           __align__(8) __half2 gg[2] = {__halves2half2(__float2half_rn(i), __float2half_rn(f)),
@@ -199,6 +192,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
               *reinterpret_cast<const uint2*>(gg);           // R4
         }
       }
+      __syncwarp();
     }
     // (5) publish h_t
     ptx::tc_fence_before();
@@ -220,20 +214,17 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
 template <int BN>
 size_t fwd_smem(int hp) {
   const int nkb = (hp + 63) / 64;
-  return 1024 + (size_t)nkb * 16384 + (size_t)nkb * BN * 128 + (size_t)BN * 128 * 4 + 128;
+  return 1024 + (size_t)nkb * 16384 + (size_t)nkb * BN * 128 + (size_t)RT_WARPS * 16 * ACT_LD * 4 + 128;
 }
 
 template <int BN>
 cudaError_t launch_fwd_bn(const RecurFwdArgs& a, cudaStream_t s) {
-  CUtensorMap mU, mH, mG;
+  CUtensorMap mU, mH;
   if (encode_tmap_2d(&mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U, a.hp, 4 * a.hp, a.hp * 2, 64, 128,
                CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   if (encode_tmap_2d(&mH, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.Hs, a.hp, (uint64_t)(a.T + 1) * a.B, a.hp * 2, 64, a.B,
                CU_TENSOR_MAP_SWIZZLE_128B))
-    return cudaErrorInvalidValue;
-  if (encode_tmap_2d(&mG, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.Gx, 4 * a.hp, (uint64_t)a.T * a.B, 4 * a.hp * 4, 128, a.B,
-               CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
   const size_t smem = fwd_smem<BN>(a.hp);
   cudaError_t e = cudaFuncSetAttribute(recur_fwd_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
@@ -248,7 +239,7 @@ cudaError_t launch_fwd_bn(const RecurFwdArgs& a, cudaStream_t s) {
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, recur_fwd_kernel<BN>, mU, mH, mG, a.T, a.B, a.hp, a.Hs, a.C, a.gates,
+  return cudaLaunchKernelEx(&cfg, recur_fwd_kernel<BN>, mU, mH, a.Gx, a.T, a.B, a.hp, a.Hs, a.C, a.gates,
                             a.counter);
 }
 
