@@ -314,7 +314,7 @@ void carve(hdp_ctx* c, char* base) {
   c->s2 = (float*)cv.take(d.optimizer == HDP_OPT_ADAM ? c->M_own * 4 : 0);
   c->grads = cv.take((size_t)c->nslots * P * c->gsz);
   c->recv = cv.take(c->world > 1 ? c->max_bucket * c->gsz : 0);
-  c->status = (int*)cv.take(256);
+  c->status = (int*)cv.take(4096);  // [0] non-finite count; +1024 B: recurrence barrier counters
   c->slot.assign(c->nslots, hdp_ctx::Slot{});
   if (d.n_layers > 0) {
     const long B = d.max_batch, T = d.max_seq, L = d.n_layers, hp = c->hp, e = c->esz;
@@ -478,7 +478,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
       ra.Hs = (__half*)Hs;
       ra.C = Cl;
       ra.gates = (__half*)Gl;
-      ra.counter = (unsigned*)((char*)c->status + 64);
+      ra.counter = (unsigned*)((char*)c->status + 1024);
       ra.T = T;
       ra.B = B;
       ra.hp = (int)hp;

@@ -22,6 +22,8 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "gemm.cuh"
 #include "ptx.cuh"
 #include "recur.cuh"
@@ -29,8 +31,6 @@
 namespace hdp {
 namespace {
 
-constexpr int RT_WARPS = 16;  // 4 lane quarters x 4 column groups
-constexpr int RT_THREADS = RT_WARPS * 32;
 
 // sigma(x) with the SFU exponential; relative error ~1e-6, far below the
 // fp16 rounding (R4, R6) applied to everything this kernel stores.
@@ -48,46 +48,55 @@ __device__ __forceinline__ unsigned acquire_ld(const unsigned* p) {
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
 
-// smem: [U: nkb x 16 KB][H: nkb x BN*128 B][act: 16 warps x 16 x 40 fp32][barriers]
+// smem: [U: nkb x 16 KB][H: nkb x Bc*128 B][act: nwarps x 16 x ACT_LD fp32][barriers]
 constexpr int ACT_LD = 40;  // 32 rows + 8 pad: conflict-free float4 reads (see epilogue)
-template <int BN>
-__global__ void __launch_bounds__(RT_THREADS, 1)
+
+// Grid (G row tiles) x (NBG batch groups).  Batch rows are independent
+// recurrences, so each batch group synchronises only its own G CTAs on its
+// own counter.  Block = 4 lane quarters x cgN column groups of warps; each
+// warp handles NCI chunks of 16 batch columns.
+template <int NCI>
+__global__ void __launch_bounds__(512, 1)
     recur_fwd_kernel(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmH,
-                     const float* __restrict__ Gx, int T, int B, int hp, __half* __restrict__ Hs,
-                     float* __restrict__ Cst, __half* __restrict__ gates, unsigned* __restrict__ counter) {
+                     const float* __restrict__ Gx, int T, int B, int Bc, int hp, __half* __restrict__ Hs,
+                     float* __restrict__ Cst, __half* __restrict__ gates, unsigned* __restrict__ counters) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int nkb = (hp + 63) / 64;
   const int nk16 = (hp + 15) / 16;
+  const int nwarps = blockDim.x >> 5;
+  const int cgN = nwarps >> 2;
   uint8_t* sU = smem;
   uint8_t* sH = sU + nkb * 16384;
-  float* sAct = reinterpret_cast<float*>(sH + (size_t)nkb * BN * 128);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sAct + RT_WARPS * 16 * ACT_LD);
+  float* sAct = reinterpret_cast<float*>(sH + (size_t)nkb * Bc * 128);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sAct + nwarps * 16 * ACT_LD);
   uint64_t* barU = bars;
   uint64_t* barH = bars + 1;
-  uint64_t* barG = bars + 2;
-  uint64_t* barM = bars + 3;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
+  uint64_t* barM = bars + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int quarter = warp & 3;                // TMEM lane quarter this warp may access
-  const int cg = warp >> 2;                    // column group: chunks ch = 4*ci + cg
+  const int cg = warp >> 2;                    // column group: chunks ch = ci*cgN + cg
   const int G = gridDim.x;
   const int row0 = blockIdx.x * 128;          // first gate row of this CTA
+  const int col0 = blockIdx.y * Bc;           // first batch column of this CTA
+  unsigned* counter = counters + blockIdx.y * 32;
   const int r = quarter * 32 + lane;           // tile row = TMEM lane
   const int grow = row0 + r;                   // gate row
   const int gate = r & 3;
   const int unit = grow >> 2;
   const bool unit_ok = unit < hp;
   const int fourhp = 4 * hp;
+  const uint32_t tcols = Bc <= 32 ? 32 : Bc <= 64 ? 64 : Bc <= 128 ? 128 : 256;
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch(&tmU);
     ptx::tma_prefetch(&tmH);
-    for (int i = 0; i < 4; ++i) ptx::mbar_init(bars + i, 1);
+    for (int i = 0; i < 3; ++i) ptx::mbar_init(bars + i, 1);
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tslot, BN);
+  if (warp == 2) ptx::tmem_alloc(tslot, tcols);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -100,29 +109,29 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
   }
 
   // per-lane cell state for its (unit, column) pairs: columns c0 + 4q + gate
-  constexpr int NCI = BN / 64;  // chunks per column group
   float creg[NCI * 4];
 #pragma unroll
   for (int i = 0; i < NCI * 4; ++i) creg[i] = 0.f;
 
-  const uint32_t idesc = ptx::idesc_f16_f32(128, B, 0, 0);  // N = B (multiple of 16, <= BN)
-  const int nchunk = B / 16;
-
+  const uint32_t idesc = ptx::idesc_f16_f32(128, Bc, 0, 0);
+  const int nchunk = Bc / 16;
   float* myAct = sAct + warp * 16 * ACT_LD;
   const float gsc = gate == 2 ? 2.f : 1.f;
+
   for (int t = 0; t < T; ++t) {
-    // (1) G_x[t] for this warp's chunks -> registers (independent of the recurrence;
-    //     issued before the grid barrier so its latency overlaps the wait)
+    // (1) G_x[t] for this warp's chunks -> registers (independent of the
+    //     recurrence; issued before the grid barrier so its latency overlaps it)
     float gx[NCI][16];
 #pragma unroll
     for (int ci = 0; ci < NCI; ++ci) {
-      const int ch = ci * 4 + cg;
+      const int ch = ci * cgN + cg;
+      const bool ok = ch < nchunk && grow < fourhp;
+      const float* gp = Gx + ((size_t)t * B + col0 + ch * 16) * fourhp + grow;
 #pragma unroll
-      for (int k = 0; k < 16; ++k)
-        gx[ci][k] = (ch < nchunk && grow < fourhp) ? __ldg(Gx + ((size_t)t * B + ch * 16 + k) * fourhp + grow) : 0.f;
+      for (int k = 0; k < 16; ++k) gx[ci][k] = ok ? __ldg(gp + (size_t)k * fourhp) : 0.f;
     }
     if (t > 0) {
-      // (2) grid barrier: all CTAs published h_{t-1}
+      // (2) grid barrier of this batch group: all its CTAs published h_{t-1}
       if (threadIdx.x == 0) {
         const unsigned target = (unsigned)(G * t);
         if (acquire_ld(counter) < target) {
@@ -132,16 +141,17 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
           }
         }
         fence_proxy_async();
-        // (3) h_{t-1} = Hs slot t -> smem, then MMA
-        ptx::mbar_arrive_expect_tx(barH, nkb * B * 128);
-        for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sH + kb * B * 128, &tmH, barH, kb * 64, t * B);
+        // (3) h_{t-1} (Hs slot t, this group's rows) -> smem, then MMA
+        ptx::mbar_arrive_expect_tx(barH, nkb * Bc * 128);
+        for (int kb = 0; kb < nkb; ++kb)
+          ptx::tma_load_2d(sH + kb * Bc * 128, &tmH, barH, kb * 64, t * B + col0);
         ptx::mbar_wait(barH, (t - 1) & 1);
         ptx::tc_fence_after();
         const uint32_t aU = ptx::smem_u32(sU), aH = ptx::smem_u32(sH);
         for (int k = 0; k < nk16; ++k) {
           const int kb = k >> 2, kk = k & 3;
           const uint64_t ad = ptx::smem_desc_sw128(aU + kb * 16384 + kk * 32, 0, 1024);
-          const uint64_t bd = ptx::smem_desc_sw128(aH + kb * B * 128 + kk * 32, 0, 1024);
+          const uint64_t bd = ptx::smem_desc_sw128(aH + kb * Bc * 128 + kk * 32, 0, 1024);
           ptx::mma_f16(tbase, ad, bd, idesc, k > 0 ? 1u : 0u);
         }
         ptx::mma_commit(barM);
@@ -157,7 +167,7 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
     __half* gout = gates + (size_t)t * B * fourhp;
 #pragma unroll
     for (int ci = 0; ci < NCI; ++ci) {
-      const int ch = ci * 4 + cg;
+      const int ch = ci * cgN + cg;
       if (ch >= nchunk) break;
       const int c0 = ch * 16;
       float v[16];
@@ -167,29 +177,28 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = 0.f;
       }
-      // activate own gate, stage [col][row] in this warp's smem tile (rows = its 32 gate rows)
+      // activate own gate, stage [col][row] in this warp's smem tile (its 32 gate rows)
 #pragma unroll
       for (int k = 0; k < 16; ++k) myAct[k * ACT_LD + lane] = act_gate(v[k] + gx[ci][k], gsc);
       __syncwarp();
       if (unit_ok) {
-        // lane = (unit u = lane>>2, column class g = lane&3): columns c0 + 4q + g
-        // float4 at [col][4u]: slots (col*10 + u) mod 8 distinct in each 8-lane phase
+        // lane = (unit u = lane>>2, column class g = lane&3): columns c0 + 4q + g.
+        // float4 at [col][4u]: 16-B slot (10*col + u) mod 8 is distinct in every 8-lane phase
         const int u = lane >> 2;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int col = 4 * q + gate;
           const float4 a4 = *reinterpret_cast<const float4*>(myAct + col * ACT_LD + 4 * u);
-          const int b = c0 + col;
+          const size_t b = (size_t)col0 + c0 + col;
           const float i = a4.x, f = a4.y, g = a4.z, o = a4.w;
           const float c = f * creg[ci * 4 + q] + i * g;
           creg[ci * 4 + q] = c;
           const float h = o * act_gate(c, 2.f);   // o * tanh(c)
-          cout[(size_t)b * hp + unit] = c;                   // R5
-          hout[(size_t)b * hp + unit] = __float2half_rn(h);  // R6
+          cout[b * hp + unit] = c;                   // R5
+          hout[b * hp + unit] = __float2half_rn(h);  // R6
           __align__(8) __half2 gg[2] = {__halves2half2(__float2half_rn(i), __float2half_rn(f)),
                                         __halves2half2(__float2half_rn(g), __float2half_rn(o))};
-          *reinterpret_cast<uint2*>(gout + (size_t)b * fourhp + 4 * unit) =
-              *reinterpret_cast<const uint2*>(gg);           // R4
+          *reinterpret_cast<uint2*>(gout + b * fourhp + 4 * unit) = *reinterpret_cast<const uint2*>(gg);  // R4
         }
       }
       __syncwarp();
@@ -207,31 +216,60 @@ __global__ void __launch_bounds__(RT_THREADS, 1)
   __syncthreads();
   if (warp == 2) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tbase, BN);
+    ptx::tmem_dealloc(tbase, tcols);
   }
 }
 
-template <int BN>
-size_t fwd_smem(int hp) {
+size_t fwd_smem(int hp, int Bc, int nwarps) {
   const int nkb = (hp + 63) / 64;
-  return 1024 + (size_t)nkb * 16384 + (size_t)nkb * BN * 128 + (size_t)RT_WARPS * 16 * ACT_LD * 4 + 128;
+  return 1024 + (size_t)nkb * 16384 + (size_t)nkb * Bc * 128 + (size_t)nwarps * 16 * ACT_LD * 4 + 128;
 }
 
-template <int BN>
-cudaError_t launch_fwd_bn(const RecurFwdArgs& a, cudaStream_t s) {
+struct FwdPlan {
+  int nbg = 1, Bc = 0, cgN = 1, nci = 1, G = 1;
+};
+
+bool plan_fwd(int B, int hp, FwdPlan* p) {
+  if (B < 16 || (B & 15) || (hp & 15)) return false;
+  p->G = (4 * hp + 127) / 128;
+  int force = 0;
+  if (const char* e = getenv("HDP_RECUR_NBG")) force = atoi(e);
+  int best = 0;
+  for (int nbg = 16; nbg >= 1; nbg >>= 1) {
+    if (force && nbg != force) continue;
+    if (B % nbg) continue;
+    const int Bc = B / nbg;
+    if ((Bc & 15) || Bc < 16 || Bc > 256) continue;
+    if (p->G * nbg > 148) continue;
+    best = nbg;  // largest batch-group count that fits: most SMs, shortest per-step critical path
+    break;
+  }
+  if (!best) return false;
+  p->nbg = best;
+  p->Bc = B / best;
+  const int nchunk = p->Bc / 16;
+  p->cgN = nchunk < 4 ? nchunk : 4;
+  p->nci = (nchunk + p->cgN - 1) / p->cgN;
+  if (p->nci > 4) return false;
+  return fwd_smem(hp, p->Bc, 4 * p->cgN) <= 227 * 1024;
+}
+
+template <int NCI>
+cudaError_t launch_fwd_t(const RecurFwdArgs& a, const FwdPlan& p, cudaStream_t s) {
   CUtensorMap mU, mH;
   if (encode_tmap_2d(&mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U, a.hp, 4 * a.hp, a.hp * 2, 64, 128,
-               CU_TENSOR_MAP_SWIZZLE_128B))
+                     CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
-  if (encode_tmap_2d(&mH, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.Hs, a.hp, (uint64_t)(a.T + 1) * a.B, a.hp * 2, 64, a.B,
-               CU_TENSOR_MAP_SWIZZLE_128B))
+  if (encode_tmap_2d(&mH, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.Hs, a.hp, (uint64_t)(a.T + 1) * a.B, a.hp * 2, 64,
+                     p.Bc, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
-  const size_t smem = fwd_smem<BN>(a.hp);
-  cudaError_t e = cudaFuncSetAttribute(recur_fwd_kernel<BN>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  const int nwarps = 4 * p.cgN;
+  const size_t smem = fwd_smem(a.hp, p.Bc, nwarps);
+  cudaError_t e = cudaFuncSetAttribute(recur_fwd_kernel<NCI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((4 * a.hp + 127) / 128));
-  cfg.blockDim = dim3(RT_THREADS);
+  cfg.gridDim = dim3((unsigned)p.G, (unsigned)p.nbg);
+  cfg.blockDim = dim3((unsigned)(32 * nwarps));
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
   cudaLaunchAttribute at[1];
@@ -239,26 +277,25 @@ cudaError_t launch_fwd_bn(const RecurFwdArgs& a, cudaStream_t s) {
   at[0].val.cooperative = 1;
   cfg.attrs = at;
   cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, recur_fwd_kernel<BN>, mU, mH, a.Gx, a.T, a.B, a.hp, a.Hs, a.C, a.gates,
+  return cudaLaunchKernelEx(&cfg, recur_fwd_kernel<NCI>, mU, mH, a.Gx, a.T, a.B, p.Bc, a.hp, a.Hs, a.C, a.gates,
                             a.counter);
 }
 
 }  // namespace
 
 bool recur_fwd_supported(int B, int hp) {
-  if (B < 16 || B > 256 || (B & 15) || (hp & 15)) return false;
-  const int bn = B <= 64 ? 64 : (B <= 128 ? 128 : 256);
-  const size_t smem = bn == 64 ? fwd_smem<64>(hp) : bn == 128 ? fwd_smem<128>(hp) : fwd_smem<256>(hp);
-  const int ctas = (4 * hp + 127) / 128;
-  return smem <= 227 * 1024 && ctas <= 148;
+  FwdPlan p;
+  return plan_fwd(B, hp, &p);
 }
 
 cudaError_t launch_recur_fwd(const RecurFwdArgs& a, cudaStream_t s) {
-  cudaError_t e = cudaMemsetAsync(a.counter, 0, sizeof(unsigned), s);
+  FwdPlan p;
+  if (!plan_fwd(a.B, a.hp, &p)) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaMemsetAsync(a.counter, 0, (size_t)p.nbg * 32 * sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
-  if (a.B <= 64) return launch_fwd_bn<64>(a, s);
-  if (a.B <= 128) return launch_fwd_bn<128>(a, s);
-  return launch_fwd_bn<256>(a, s);
+  if (p.nci == 1) return launch_fwd_t<1>(a, p, s);
+  if (p.nci == 2) return launch_fwd_t<2>(a, p, s);
+  return launch_fwd_t<4>(a, p, s);
 }
 
 }  // namespace hdp

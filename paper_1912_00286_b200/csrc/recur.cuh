@@ -11,7 +11,7 @@ struct RecurFwdArgs {
   __half* Hs = nullptr;       // [T+1][B][hp]; slot 0 = h_{-1} = 0 (read), slots 1..T written
   float* C = nullptr;         // [T][B][hp]
   __half* gates = nullptr;    // [T][B][4hp] activated gates, fp16 (R4)
-  unsigned* counter = nullptr;  // grid-barrier counter (zeroed by the launcher)
+  unsigned* counter = nullptr;  // grid-barrier counters, 16 x 32 uints (zeroed by the launcher)
   int T = 0, B = 0, hp = 0;
 };
 
