@@ -1,3 +1,3 @@
-timeout -s KILL 900 python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider -x -k "persistent or c2" > gpurun_out/persist_tests.log 2>&1; echo exit=$? >> gpurun_out/persist_tests.log
-for nbg in 8 4 2 1; do HDP_RECUR_NBG=$nbg timeout -s KILL 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench_nbg$nbg.json 2>> gpurun_out/bench6.err; done
+timeout -s KILL 900 python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider -x -k "persistent or c2 or c3" > gpurun_out/persist_tests.log 2>&1; echo exit=$? >> gpurun_out/persist_tests.log
+timeout -s KILL 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/bench9.json 2>> gpurun_out/bench9.err
 tail -3 gpurun_out/persist_tests.log

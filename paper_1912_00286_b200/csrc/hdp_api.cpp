@@ -626,6 +626,22 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
   float* Cl = S.C + l * c_layer;
   const char* Gl = S.gates + l * g_layer * e;
   const bool last_only = d.head_last_step && l == L - 1;
+  if (!f32 && c->persistent && hdp::recur_bwd_supported(B, (int)hp)) {
+    // A6 + A7 for all t in one persistent kernel (U^T slice resident in SMEM)
+    hdp::RecurBwdArgs ra;
+    ra.U = (const __half*)c->W(iU);
+    ra.dHa = dHa;
+    ra.dHa_last_only = last_only ? 1 : 0;
+    ra.gates = (const __half*)Gl;
+    ra.C = Cl;
+    ra.dA = (__half*)c->dA;
+    ra.counter = (unsigned*)((char*)c->status + 1024);
+    ra.T = T;
+    ra.B = B;
+    ra.hp = (int)hp;
+    KScope ks_(c, HDP_K_RECUR_BWD, 1, s);
+    CK_CUDA(hdp::launch_recur_bwd(ra, s));
+  } else
   for (int t = T - 1; t >= 0; --t) {
     const float* dHa_t = last_only ? (t == T - 1 ? dHa : nullptr) : dHa + (long)t * B * hp;
     // K6 (A6)

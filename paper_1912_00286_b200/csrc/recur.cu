@@ -281,6 +281,236 @@ cudaError_t launch_fwd_t(const RecurFwdArgs& a, const FwdPlan& p, cudaStream_t s
                             a.counter);
 }
 
+
+// ============================================================== backward
+// BPTT over all t of one layer (A6 + A7):
+//   dh_t = dH_above[t] + dA_{t+1} U ;  dc = dc + dh o (1 - tanh^2 c_t)
+//   dA_t = [dc g i(1-i), dc c_{t-1} f(1-f), dc i (1-g^2), dh tanh(c_t) o(1-o)] ; dc <- dc f
+// CTA (x = 64-unit tile, y = batch group of Bc columns).  Swap-AB tcgen05:
+//   D[unit][b] = sum_r U[r][unit] dA_{t+1}[b][r]     M = 64 units, N = Bc, K = 4hp
+// A = U^T slice read MN-major straight from U (resident in SMEM for all t),
+// B = dA_{t+1} rows of the group (K-major), streamed by TMA each step.
+// M = 64 accumulator layout (1-SM): row 16q + i lives in TMEM lane 32q + i.
+// Epilogue: lane i < 16 takes columns [0, 8) of each 16-column chunk of unit
+// row 16*warp + i, lane i + 16 the columns [8, 16) (shuffled over).
+template <int NC>  // 16-column chunks per CTA (Bc = 16 * NC)
+__global__ void __launch_bounds__(128, 1)
+    recur_bwd_kernel(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmA,
+                     const float* __restrict__ dHa, int dHa_last_only, const __half* __restrict__ gates,
+                     const float* __restrict__ Cst, __half* __restrict__ dA, int T, int B, int hp,
+                     unsigned* __restrict__ counters) {
+  constexpr int Bc = 16 * NC;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int fourhp = 4 * hp;
+  const int nkb = fourhp / 64;           // K blocks (4hp is a multiple of 64)
+  uint8_t* sU = smem;                    // nkb x 8 KB  (64 units x 64 K-rows, MN-major SW128)
+  uint8_t* sA = sU + nkb * 8192;         // nkb x Bc*128 B (K-major SW128)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (size_t)nkb * Bc * 128);
+  uint64_t* barU = bars;
+  uint64_t* barA = bars + 1;
+  uint64_t* barM = bars + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int j0 = blockIdx.x * 64;
+  const int col0 = blockIdx.y * Bc;
+  unsigned* counter = counters + blockIdx.y * 32;
+  const int jl = lane & 15;
+  const int half = lane >> 4;            // 0: columns [0,8) of a chunk, 1: [8,16)
+  const int unit = j0 + warp * 16 + jl;
+  const bool unit_ok = unit < hp;
+  constexpr uint32_t tcols = Bc <= 32 ? 32 : Bc <= 64 ? 64 : 128;
+
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch(&tmU);
+    ptx::tma_prefetch(&tmA);
+    for (int i = 0; i < 3; ++i) ptx::mbar_init(bars + i, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tslot, tcols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = *tslot;
+
+  if (threadIdx.x == 0) {
+    ptx::mbar_arrive_expect_tx(barU, nkb * 8192);
+    for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sU + kb * 8192, &tmU, barU, j0, kb * 64);
+    ptx::mbar_wait(barU, 0);
+  }
+
+  float dcr[NC * 8];  // dc state of (unit, column) pairs this lane owns
+#pragma unroll
+  for (int i = 0; i < NC * 8; ++i) dcr[i] = 0.f;
+  const uint32_t idesc = ptx::idesc_f16_f32(64, Bc, 1, 0);
+
+  for (int t = T - 1; t >= 0; --t) {
+    // (1) inputs independent of the recurrence -> registers, before the barrier
+    float dh0[NC * 8], cc[NC * 8], cp[NC * 8];
+    uint2 gq[NC * 8];
+#pragma unroll
+    for (int ch = 0; ch < NC; ++ch)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int idx = ch * 8 + k;
+        const size_t b = (size_t)col0 + ch * 16 + half * 8 + k;
+        float d = 0.f, c1 = 0.f, c0 = 0.f;
+        uint2 gg = make_uint2(0u, 0u);
+        if (unit_ok) {
+          if (dHa_last_only) {
+            if (t == T - 1) d = __ldg(dHa + b * hp + unit);
+          } else {
+            d = __ldg(dHa + ((size_t)t * B + b) * hp + unit);
+          }
+          c1 = __ldg(Cst + ((size_t)t * B + b) * hp + unit);
+          if (t > 0) c0 = __ldg(Cst + ((size_t)(t - 1) * B + b) * hp + unit);
+          gg = __ldg(reinterpret_cast<const uint2*>(gates + ((size_t)t * B + b) * fourhp + 4 * unit));
+        }
+        dh0[idx] = d;
+        cc[idx] = c1;
+        cp[idx] = c0;
+        gq[idx] = gg;
+      }
+    if (t < T - 1) {
+      // (2) barrier: every CTA of this batch group published dA_{t+1}
+      if (threadIdx.x == 0) {
+        const unsigned target = (unsigned)(G * (T - 1 - t));
+        if (acquire_ld(counter) < target) {
+          const uint64_t t0 = ptx::globaltimer_ns();
+          while (acquire_ld(counter) < target) {
+            if (ptx::globaltimer_ns() - t0 > 10000000000ull) __trap();
+          }
+        }
+        fence_proxy_async();
+        // (3) dA_{t+1} rows of the group -> smem; MMA D[unit][b] = sum_r U[r][unit] dA[b][r]
+        const uint32_t ph = (T - 2 - t) & 1;
+        ptx::mbar_arrive_expect_tx(barA, nkb * Bc * 128);
+        for (int kb = 0; kb < nkb; ++kb)
+          ptx::tma_load_2d(sA + kb * Bc * 128, &tmA, barA, kb * 64, (t + 1) * B + col0);
+        ptx::mbar_wait(barA, ph);
+        ptx::tc_fence_after();
+        const uint32_t aU = ptx::smem_u32(sU), aA = ptx::smem_u32(sA);
+        for (int k = 0; k < nkb * 4; ++k) {
+          const int kb = k >> 2, kk = k & 3;
+          const uint64_t ad = ptx::smem_desc_sw128(aU + kb * 8192 + kk * 2048, 8192, 1024);
+          const uint64_t bd = ptx::smem_desc_sw128(aA + kb * Bc * 128 + kk * 32, 0, 1024);
+          ptx::mma_f16(tbase, ad, bd, idesc, k > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(barM);
+      }
+      __syncwarp();
+      ptx::mbar_wait(barM, (T - 2 - t) & 1);
+      ptx::tc_fence_after();
+    }
+    // (4) epilogue: dh_rec from TMEM, cell backward, dA_t stores
+    __half* dAout = dA + (size_t)t * B * fourhp;
+#pragma unroll
+    for (int ch = 0; ch < NC; ++ch) {
+      float v[16];
+      if (t < T - 1) {
+        ptx::tmem_ld16(tbase + (static_cast<uint32_t>(warp * 32) << 16) + ch * 16, v);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = 0.f;
+      }
+      // lane i+16 takes columns 8..15 of lane i's row
+      float rec[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float hi = __shfl_sync(0xffffffffu, v[8 + k], jl);
+        rec[k] = half ? hi : v[k];
+      }
+      if (unit_ok) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int idx = ch * 8 + k;
+          const size_t b = (size_t)col0 + ch * 16 + half * 8 + k;
+          const float dh = dh0[idx] + rec[k];
+          const float2 if2 = __half22float2(*reinterpret_cast<const __half2*>(&gq[idx].x));
+          const float2 go2 = __half22float2(*reinterpret_cast<const __half2*>(&gq[idx].y));
+          const float i = if2.x, f = if2.y, g = go2.x, o = go2.y;
+          const float tc = tanhf(cc[idx]);
+          const float d = dcr[idx] + dh * o * (1.f - tc * tc);
+          __align__(8) __half2 q2[2] = {
+              __halves2half2(__float2half_rn(d * g * i * (1.f - i)), __float2half_rn(d * cp[idx] * f * (1.f - f))),
+              __halves2half2(__float2half_rn(d * i * (1.f - g * g)), __float2half_rn(dh * tc * o * (1.f - o)))};
+          *reinterpret_cast<uint2*>(dAout + b * fourhp + 4 * unit) = *reinterpret_cast<const uint2*>(q2);  // R10
+          dcr[idx] = d * f;
+        }
+      }
+    }
+    // (5) publish dA_t
+    ptx::tc_fence_before();
+    fence_proxy_async();
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      __threadfence();
+      release_add(counter, 1u);
+    }
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tbase, tcols);
+  }
+}
+
+size_t bwd_smem(int hp, int Bc) {
+  const int nkb = 4 * hp / 64;
+  return 1024 + (size_t)nkb * 8192 + (size_t)nkb * Bc * 128 + 128;
+}
+
+bool plan_bwd(int B, int hp, int* Bc_out, int* nbg_out) {
+  if (B < 16 || (B & 15) || (hp & 15)) return false;
+  const int G = (hp + 63) / 64;
+  int force = 0;
+  if (const char* e = getenv("HDP_RECUR_NBG")) force = atoi(e);
+  for (int nbg = 16; nbg >= 1; nbg >>= 1) {
+    if (force && nbg != force) continue;
+    if (B % nbg) continue;
+    const int Bc = B / nbg;
+    if ((Bc & 15) || Bc < 16 || Bc > 64) continue;
+    if (G * nbg > 148) continue;
+    if (bwd_smem(hp, Bc) > 227 * 1024) continue;
+    *Bc_out = Bc;
+    *nbg_out = nbg;
+    return true;
+  }
+  return false;
+}
+
+template <int NC>
+cudaError_t launch_bwd_t(const RecurBwdArgs& a, int nbg, cudaStream_t s) {
+  constexpr int Bc = 16 * NC;
+  CUtensorMap mU, mA;
+  // A operand: U^T slice, MN-major = U rows (K = 4hp) with units contiguous
+  if (encode_tmap_2d(&mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U, a.hp, 4 * a.hp, a.hp * 2, 64, 64,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  // B operand: dA rows [T*B][4hp], K-major
+  if (encode_tmap_2d(&mA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.dA, 4 * a.hp, (uint64_t)a.T * a.B, 4 * a.hp * 2, 64, Bc,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  const size_t smem = bwd_smem(a.hp, Bc);
+  cudaError_t e = cudaFuncSetAttribute(recur_bwd_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3((unsigned)((a.hp + 63) / 64), (unsigned)nbg);
+  cfg.blockDim = dim3(128);
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeCooperative;
+  at[0].val.cooperative = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelEx(&cfg, recur_bwd_kernel<NC>, mU, mA, a.dHa, a.dHa_last_only, a.gates, a.C, a.dA, a.T,
+                            a.B, a.hp, a.counter);
+}
+
 }  // namespace
 
 bool recur_fwd_supported(int B, int hp) {
@@ -296,6 +526,28 @@ cudaError_t launch_recur_fwd(const RecurFwdArgs& a, cudaStream_t s) {
   if (p.nci == 1) return launch_fwd_t<1>(a, p, s);
   if (p.nci == 2) return launch_fwd_t<2>(a, p, s);
   return launch_fwd_t<4>(a, p, s);
+}
+
+}  // namespace hdp
+
+namespace hdp {
+
+bool recur_bwd_supported(int B, int hp) {
+  int Bc, nbg;
+  return plan_bwd(B, hp, &Bc, &nbg);
+}
+
+cudaError_t launch_recur_bwd(const RecurBwdArgs& a, cudaStream_t s) {
+  int Bc = 0, nbg = 0;
+  if (!plan_bwd(a.B, a.hp, &Bc, &nbg)) return cudaErrorInvalidConfiguration;
+  cudaError_t e = cudaMemsetAsync(a.counter, 0, (size_t)nbg * 32 * sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  switch (Bc / 16) {
+    case 1: return launch_bwd_t<1>(a, nbg, s);
+    case 2: return launch_bwd_t<2>(a, nbg, s);
+    case 3: return launch_bwd_t<3>(a, nbg, s);
+    default: return launch_bwd_t<4>(a, nbg, s);
+  }
 }
 
 }  // namespace hdp
