@@ -511,6 +511,371 @@ cudaError_t launch_bwd_t(const RecurBwdArgs& a, int nbg, cudaStream_t s) {
                             a.B, a.hp, a.counter);
 }
 
+
+// ============================================================== cluster variants
+// One thread-block cluster per batch group (cluster = all row / unit tiles of
+// the layer, <= 8 CTAs).  The per-step exchange never leaves the chip: each
+// CTA pushes its slice of h_t (forward) or dA_t (backward) into every peer's
+// shared-memory operand buffer with st.shared::cluster (double-buffered by
+// step parity), then one barrier.cluster.arrive/wait replaces the L2 counter
+// barrier and the TMA reload.  Global copies (needed by later kernels) are
+// still written, off the critical path.
+
+template <int NCI>
+__global__ void __launch_bounds__(512, 1)
+    recur_fwd_cl_kernel(const __grid_constant__ CUtensorMap tmU, const float* __restrict__ Gx, int T, int B, int Bc,
+                        int hp, __half* __restrict__ Hs, float* __restrict__ Cst, __half* __restrict__ gates) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int nkb = (hp + 63) / 64;
+  const int nk16 = (hp + 15) / 16;
+  const int nwarps = blockDim.x >> 5;
+  const int cgN = nwarps >> 2;
+  const int hbuf = nkb * Bc * 128;            // one h operand buffer
+  uint8_t* sU = smem;
+  uint8_t* sH = sU + nkb * 16384;             // [2][hbuf]
+  __half* sX = reinterpret_cast<__half*>(sH + 2 * hbuf);  // [Bc][32] staging of my h_t slice
+  float* sAct = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(sX) + ((Bc * 64 + 127) & ~127));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sAct + nwarps * 16 * ACT_LD);
+  uint64_t* barU = bars;
+  uint64_t* barM = bars + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int quarter = warp & 3, cg = warp >> 2;
+  const int G = gridDim.x;                    // == cluster size
+  const int rank = blockIdx.x;
+  const int row0 = rank * 128;
+  const int col0 = blockIdx.y * Bc;
+  const int r = quarter * 32 + lane;
+  const int grow = row0 + r;
+  const int gate = r & 3;
+  const int unit = grow >> 2;
+  const bool unit_ok = unit < hp;
+  const int fourhp = 4 * hp;
+  const uint32_t tcols = Bc <= 32 ? 32 : Bc <= 64 ? 64 : Bc <= 128 ? 128 : 256;
+
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch(&tmU);
+    for (int i = 0; i < 2; ++i) ptx::mbar_init(bars + i, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tslot, tcols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  if (threadIdx.x == 0) {
+    ptx::mbar_arrive_expect_tx(barU, nkb * 16384);
+    for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sU + kb * 16384, &tmU, barU, kb * 64, row0);
+    ptx::mbar_wait(barU, 0);
+  }
+  ptx::cluster_arrive();  // every CTA of the cluster is resident before any remote write
+  ptx::cluster_wait();
+
+  float creg[NCI * 4];
+#pragma unroll
+  for (int i = 0; i < NCI * 4; ++i) creg[i] = 0.f;
+  const uint32_t idesc = ptx::idesc_f16_f32(128, Bc, 0, 0);
+  const int nchunk = Bc / 16;
+  float* myAct = sAct + warp * 16 * ACT_LD;
+  const float gsc = gate == 2 ? 2.f : 1.f;
+  const int nvalid = max(0, min(32, hp - 32 * rank));  // units of my slice inside h_p
+  const int nq = nvalid / 8;
+  const int kbx = (32 * rank) / 64, cbase = ((32 * rank) % 64) / 8;
+  const uint32_t sH_addr = ptx::smem_u32(sH);
+
+  for (int t = 0; t < T; ++t) {
+    float gx[NCI][16];
+#pragma unroll
+    for (int ci = 0; ci < NCI; ++ci) {
+      const int ch = ci * cgN + cg;
+      const bool ok = ch < nchunk && grow < fourhp;
+      const float* gp = Gx + ((size_t)t * B + col0 + ch * 16) * fourhp + grow;
+#pragma unroll
+      for (int k = 0; k < 16; ++k) gx[ci][k] = ok ? __ldg(gp + (size_t)k * fourhp) : 0.f;
+    }
+    if (t > 0) {
+      ptx::cluster_wait();  // all peers pushed h_{t-1} into sH[(t-1)&1]
+      ptx::tc_fence_after();
+      if (threadIdx.x == 0) {
+        ptx::fence_async_smem();
+        const uint32_t aU = ptx::smem_u32(sU), aH = sH_addr + ((t - 1) & 1) * hbuf;
+        for (int k = 0; k < nk16; ++k) {
+          const int kb = k >> 2, kk = k & 3;
+          const uint64_t ad = ptx::smem_desc_sw128(aU + kb * 16384 + kk * 32, 0, 1024);
+          const uint64_t bd = ptx::smem_desc_sw128(aH + kb * Bc * 128 + kk * 32, 0, 1024);
+          ptx::mma_f16(tbase, ad, bd, idesc, k > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(barM);
+      }
+      __syncwarp();
+      ptx::mbar_wait(barM, (t - 1) & 1);
+      ptx::tc_fence_after();
+    }
+    __half* hout = Hs + (size_t)(t + 1) * B * hp;
+    float* cout = Cst + (size_t)t * B * hp;
+    __half* gout = gates + (size_t)t * B * fourhp;
+#pragma unroll
+    for (int ci = 0; ci < NCI; ++ci) {
+      const int ch = ci * cgN + cg;
+      if (ch >= nchunk) break;
+      const int c0 = ch * 16;
+      float v[16];
+      if (t > 0) {
+        ptx::tmem_ld16(tbase + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = 0.f;
+      }
+#pragma unroll
+      for (int k = 0; k < 16; ++k) myAct[k * ACT_LD + lane] = act_gate(v[k] + gx[ci][k], gsc);
+      __syncwarp();
+      if (unit_ok) {
+        const int u = lane >> 2;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int col = 4 * q + gate;
+          const float4 a4 = *reinterpret_cast<const float4*>(myAct + col * ACT_LD + 4 * u);
+          const int bl = c0 + col;
+          const size_t b = (size_t)col0 + bl;
+          const float i = a4.x, f = a4.y, g = a4.z, o = a4.w;
+          const float c = f * creg[ci * 4 + q] + i * g;
+          creg[ci * 4 + q] = c;
+          const __half hh = __float2half_rn(o * act_gate(c, 2.f));
+          cout[b * hp + unit] = c;                   // R5
+          hout[b * hp + unit] = hh;                  // R6
+          sX[bl * 32 + quarter * 8 + u] = hh;
+          __align__(8) __half2 gg[2] = {__halves2half2(__float2half_rn(i), __float2half_rn(f)),
+                                        __halves2half2(__float2half_rn(g), __float2half_rn(o))};
+          *reinterpret_cast<uint2*>(gout + b * fourhp + 4 * unit) = *reinterpret_cast<const uint2*>(gg);  // R4
+        }
+      }
+      __syncwarp();
+    }
+    __syncthreads();
+    // push my h_t slice (units [32 rank, 32 rank + nvalid)) into every peer's sH[t & 1]
+    {
+      const uint32_t dstbuf = sH_addr + (t & 1) * hbuf + kbx * Bc * 128;
+      const int n = Bc * nq * G;
+      for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+        const int dst = idx % G, rest = idx / G, q = rest % nq, bl = rest / nq;
+        const uint4 val = *reinterpret_cast<const uint4*>(sX + bl * 32 + 8 * q);
+        const uint32_t off = dstbuf + bl * 128 + (((cbase + q) ^ (bl & 7)) << 4);
+        ptx::st_cluster_v4(ptx::mapa(off, dst), val);
+      }
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_arrive();
+  }
+  ptx::cluster_wait();  // no CTA leaves while peers may still write into its shared memory
+  ptx::tc_fence_after();
+  __syncthreads();
+  if (warp == 2) ptx::tmem_dealloc(tbase, tcols);
+}
+
+size_t fwd_cl_smem(int hp, int Bc, int nwarps) {
+  const int nkb = (hp + 63) / 64;
+  return 1024 + (size_t)nkb * 16384 + 2 * (size_t)nkb * Bc * 128 + ((Bc * 64 + 127) & ~127) +
+         (size_t)nwarps * 16 * ACT_LD * 4 + 128;
+}
+
+template <int NC>
+__global__ void __launch_bounds__(128, 1)
+    recur_bwd_cl_kernel(const __grid_constant__ CUtensorMap tmU, const float* __restrict__ dHa, int dHa_last_only,
+                        const __half* __restrict__ gates, const float* __restrict__ Cst, __half* __restrict__ dA,
+                        int T, int B, int hp) {
+  constexpr int Bc = 16 * NC;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int fourhp = 4 * hp;
+  const int nkb = fourhp / 64;
+  const int abuf = nkb * Bc * 128;
+  uint8_t* sU = smem;                          // nkb x 8 KB (U^T slice, MN-major)
+  uint8_t* sA = sU + nkb * 8192;               // [2][abuf]
+  __half* sX = reinterpret_cast<__half*>(sA + 2 * abuf);   // [Bc][256] staging of my dA_t slice
+  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sX) + Bc * 512);
+  uint64_t* barU = bars;
+  uint64_t* barM = bars + 1;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int rank = blockIdx.x;
+  const int j0 = rank * 64;
+  const int col0 = blockIdx.y * Bc;
+  const int jl = lane & 15;
+  const int half = lane >> 4;
+  const int ul = warp * 16 + jl;               // unit within my 64-unit slice
+  const int unit = j0 + ul;
+  const bool unit_ok = unit < hp;
+  constexpr uint32_t tcols = Bc <= 32 ? 32 : Bc <= 64 ? 64 : 128;
+
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch(&tmU);
+    for (int i = 0; i < 2; ++i) ptx::mbar_init(bars + i, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tslot, tcols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  if (threadIdx.x == 0) {
+    ptx::mbar_arrive_expect_tx(barU, nkb * 8192);
+    for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sU + kb * 8192, &tmU, barU, j0, kb * 64);
+    ptx::mbar_wait(barU, 0);
+  }
+  ptx::cluster_arrive();
+  ptx::cluster_wait();
+
+  float dcr[NC * 8];
+#pragma unroll
+  for (int i = 0; i < NC * 8; ++i) dcr[i] = 0.f;
+  const uint32_t idesc = ptx::idesc_f16_f32(64, Bc, 1, 0);
+  const int nvalid = max(0, min(64, hp - j0));  // units of my slice
+  const int nq = nvalid / 2;                    // 16-B chunks (8 gate rows) per batch row
+  const uint32_t sA_addr = ptx::smem_u32(sA);
+
+  for (int t = T - 1; t >= 0; --t) {
+    float dh0[NC * 8], cc[NC * 8], cp[NC * 8];
+    uint2 gq[NC * 8];
+#pragma unroll
+    for (int ch = 0; ch < NC; ++ch)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int idx = ch * 8 + k;
+        const size_t b = (size_t)col0 + ch * 16 + half * 8 + k;
+        float d = 0.f, c1 = 0.f, c0 = 0.f;
+        uint2 gg = make_uint2(0u, 0u);
+        if (unit_ok) {
+          if (dHa_last_only) {
+            if (t == T - 1) d = __ldg(dHa + b * hp + unit);
+          } else {
+            d = __ldg(dHa + ((size_t)t * B + b) * hp + unit);
+          }
+          c1 = __ldg(Cst + ((size_t)t * B + b) * hp + unit);
+          if (t > 0) c0 = __ldg(Cst + ((size_t)(t - 1) * B + b) * hp + unit);
+          gg = __ldg(reinterpret_cast<const uint2*>(gates + ((size_t)t * B + b) * fourhp + 4 * unit));
+        }
+        dh0[idx] = d;
+        cc[idx] = c1;
+        cp[idx] = c0;
+        gq[idx] = gg;
+      }
+    if (t < T - 1) {
+      ptx::cluster_wait();  // all peers pushed dA_{t+1} into sA[(t+1)&1]
+      ptx::tc_fence_after();
+      if (threadIdx.x == 0) {
+        ptx::fence_async_smem();
+        const uint32_t aU = ptx::smem_u32(sU), aA = sA_addr + ((t + 1) & 1) * abuf;
+        for (int k = 0; k < nkb * 4; ++k) {
+          const int kb = k >> 2, kk = k & 3;
+          const uint64_t ad = ptx::smem_desc_sw128(aU + kb * 8192 + kk * 2048, 8192, 1024);
+          const uint64_t bd = ptx::smem_desc_sw128(aA + kb * Bc * 128 + kk * 32, 0, 1024);
+          ptx::mma_f16(tbase, ad, bd, idesc, k > 0 ? 1u : 0u);
+        }
+        ptx::mma_commit(barM);
+      }
+      __syncwarp();
+      ptx::mbar_wait(barM, (T - 2 - t) & 1);
+      ptx::tc_fence_after();
+    }
+    __half* dAout = dA + (size_t)t * B * fourhp;
+#pragma unroll
+    for (int ch = 0; ch < NC; ++ch) {
+      float v[16];
+      if (t < T - 1) {
+        ptx::tmem_ld16(tbase + (static_cast<uint32_t>(warp * 32) << 16) + ch * 16, v);
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = 0.f;
+      }
+      float rec[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float hi = __shfl_sync(0xffffffffu, v[8 + k], jl);
+        rec[k] = half ? hi : v[k];
+      }
+      if (unit_ok) {
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int idx = ch * 8 + k;
+          const int bl = ch * 16 + half * 8 + k;
+          const size_t b = (size_t)col0 + bl;
+          const float dh = dh0[idx] + rec[k];
+          const float2 if2 = __half22float2(*reinterpret_cast<const __half2*>(&gq[idx].x));
+          const float2 go2 = __half22float2(*reinterpret_cast<const __half2*>(&gq[idx].y));
+          const float i = if2.x, f = if2.y, g = go2.x, o = go2.y;
+          const float tc = tanhf(cc[idx]);
+          const float d = dcr[idx] + dh * o * (1.f - tc * tc);
+          __align__(8) __half2 q2[2] = {
+              __halves2half2(__float2half_rn(d * g * i * (1.f - i)), __float2half_rn(d * cp[idx] * f * (1.f - f))),
+              __halves2half2(__float2half_rn(d * i * (1.f - g * g)), __float2half_rn(dh * tc * o * (1.f - o)))};
+          const uint2 pk = *reinterpret_cast<const uint2*>(q2);
+          *reinterpret_cast<uint2*>(dAout + b * fourhp + 4 * unit) = pk;      // R10 (for K8 / K9)
+          *reinterpret_cast<uint2*>(sX + bl * 256 + 4 * ul) = pk;            // staging for the peers
+          dcr[idx] = d * f;
+        }
+      }
+    }
+    __syncthreads();
+    // push my dA_t slice (gate rows [256 rank, 256 rank + 4 nvalid)) into every peer's sA[t & 1]
+    {
+      const uint32_t dstbuf = sA_addr + (t & 1) * abuf;
+      const int n = Bc * nq * G;
+      for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
+        const int dst = idx % G, rest = idx / G, q = rest % nq, bl = rest / nq;
+        const uint4 val = *reinterpret_cast<const uint4*>(sX + bl * 256 + 8 * q);
+        const int kb = 4 * rank + (q >> 3), c = q & 7;
+        const uint32_t off = dstbuf + kb * Bc * 128 + bl * 128 + ((c ^ (bl & 7)) << 4);
+        ptx::st_cluster_v4(ptx::mapa(off, dst), val);
+      }
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_arrive();
+  }
+  ptx::cluster_wait();
+  ptx::tc_fence_after();
+  __syncthreads();
+  if (warp == 2) ptx::tmem_dealloc(tbase, tcols);
+}
+
+size_t bwd_cl_smem(int hp, int Bc) {
+  const int nkb = 4 * hp / 64;
+  return 1024 + (size_t)nkb * 8192 + 2 * (size_t)nkb * Bc * 128 + (size_t)Bc * 512 + 128;
+}
+
+cudaError_t launch_cluster(const void* fn, dim3 grid, dim3 block, size_t smem, int cluster_x, cudaStream_t s,
+                           void** args) {
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = cluster_x;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  return cudaLaunchKernelExC(&cfg, fn, args);
+}
+
+bool use_cluster() {
+  const char* e = getenv("HDP_RECUR_CLUSTER");
+  return !(e && e[0] == '0');
+}
+
+int pow2ceil(int v) {
+  int p = 1;
+  while (p < v) p <<= 1;
+  return p;
+}
+
 }  // namespace
 
 bool recur_fwd_supported(int B, int hp) {
@@ -521,6 +886,22 @@ bool recur_fwd_supported(int B, int hp) {
 cudaError_t launch_recur_fwd(const RecurFwdArgs& a, cudaStream_t s) {
   FwdPlan p;
   if (!plan_fwd(a.B, a.hp, &p)) return cudaErrorInvalidConfiguration;
+  const int Gc = pow2ceil(p.G);
+  if (use_cluster() && Gc <= 8 && fwd_cl_smem(a.hp, p.Bc, 4 * p.cgN) <= 227 * 1024) {
+    CUtensorMap mU;
+    if (encode_tmap_2d(&mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U, a.hp, 4 * a.hp, a.hp * 2, 64, 128,
+                       CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+    const float* gx = a.Gx;
+    int T = a.T, B = a.B, Bc = p.Bc, hp = a.hp;
+    __half* hs = a.Hs;
+    float* cst = a.C;
+    __half* gt = a.gates;
+    void* args[] = {&mU, &gx, &T, &B, &Bc, &hp, &hs, &cst, &gt};
+    const void* fn = p.nci == 1 ? (const void*)recur_fwd_cl_kernel<1>
+                   : p.nci == 2 ? (const void*)recur_fwd_cl_kernel<2> : (const void*)recur_fwd_cl_kernel<4>;
+    return launch_cluster(fn, dim3(Gc, p.nbg), dim3(128 * p.cgN), fwd_cl_smem(a.hp, p.Bc, 4 * p.cgN), Gc, s, args);
+  }
   cudaError_t e = cudaMemsetAsync(a.counter, 0, (size_t)p.nbg * 32 * sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
   if (p.nci == 1) return launch_fwd_t<1>(a, p, s);
@@ -540,6 +921,23 @@ bool recur_bwd_supported(int B, int hp) {
 cudaError_t launch_recur_bwd(const RecurBwdArgs& a, cudaStream_t s) {
   int Bc = 0, nbg = 0;
   if (!plan_bwd(a.B, a.hp, &Bc, &nbg)) return cudaErrorInvalidConfiguration;
+  const int Gc = pow2ceil((a.hp + 63) / 64);
+  if (use_cluster() && Gc <= 8 && bwd_cl_smem(a.hp, Bc) <= 227 * 1024) {
+    CUtensorMap mU;
+    if (encode_tmap_2d(&mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U, a.hp, 4 * a.hp, a.hp * 2, 64, 64,
+                       CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+    const float* dha = a.dHa;
+    int last = a.dHa_last_only, T = a.T, B = a.B, hp = a.hp;
+    const __half* gt = a.gates;
+    const float* cst = a.C;
+    __half* da = a.dA;
+    void* args[] = {&mU, &dha, &last, &gt, &cst, &da, &T, &B, &hp};
+    const void* fn = Bc == 16 ? (const void*)recur_bwd_cl_kernel<1>
+                   : Bc == 32 ? (const void*)recur_bwd_cl_kernel<2>
+                   : Bc == 48 ? (const void*)recur_bwd_cl_kernel<3> : (const void*)recur_bwd_cl_kernel<4>;
+    return launch_cluster(fn, dim3(Gc, nbg), dim3(128), bwd_cl_smem(a.hp, Bc), Gc, s, args);
+  }
   cudaError_t e = cudaMemsetAsync(a.counter, 0, (size_t)nbg * 32 * sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
   switch (Bc / 16) {
