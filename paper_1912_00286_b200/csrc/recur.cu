@@ -35,6 +35,16 @@ namespace {
 // sigma(x) with the SFU exponential; relative error ~1e-6, far below the
 // fp16 rounding (R4, R6) applied to everything this kernel stores.
 __device__ __forceinline__ float sigm_fast(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
+// tanh(c) and 1 - tanh(c)^2 from s = sigma(2c): tanh = s - (1 - s), sech^2 = 4 s (1 - s)
+// (no cancellation in sech^2; |c| clamped to 15 where both are exact in fp32)
+__device__ __forceinline__ void tanh_sech2(float c, float& th, float& sech2) {
+  const float cc = fminf(fmaxf(c, -15.f), 15.f);
+  const float e = __expf(-2.f * cc);
+  const float sg = __fdividef(1.f, 1.f + e);
+  const float om = e * sg;  // 1 - sigma(2c)
+  th = sg - om;
+  sech2 = 4.f * sg * om;
+}
 // branch-free gate activation: tanh(a) = 2 sigma(2a) - 1 for the g gate
 __device__ __forceinline__ float act_gate(float a, float s) { return fmaf(s, sigm_fast(s * a), 1.f - s); }
 
@@ -601,10 +611,11 @@ __global__ void __launch_bounds__(512, 1)
       if (threadIdx.x == 0) {
         ptx::fence_async_smem();
         const uint32_t aU = ptx::smem_u32(sU), aH = sH_addr + ((t - 1) & 1) * hbuf;
+        const uint64_t ad0 = ptx::smem_desc_sw128(aU, 0, 1024), bd0 = ptx::smem_desc_sw128(aH, 0, 1024);
         for (int k = 0; k < nk16; ++k) {
-          const int kb = k >> 2, kk = k & 3;
-          const uint64_t ad = ptx::smem_desc_sw128(aU + kb * 16384 + kk * 32, 0, 1024);
-          const uint64_t bd = ptx::smem_desc_sw128(aH + kb * Bc * 128 + kk * 32, 0, 1024);
+          const int kb = k >> 2, kk = k & 3;  // start-address field is in 16-B units
+          const uint64_t ad = ad0 + (uint64_t)((kb * 16384 + kk * 32) >> 4);
+          const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kk * 32) >> 4);
           ptx::mma_f16(tbase, ad, bd, idesc, k > 0 ? 1u : 0u);
         }
         ptx::mma_commit(barM);
@@ -656,14 +667,15 @@ __global__ void __launch_bounds__(512, 1)
     __syncthreads();
     // push my h_t slice (units [32 rank, 32 rank + nvalid)) into every peer's sH[t & 1]
     {
+      // thread = (chunk q = tid & 3, row bl = tid >> 2): 8 units per 16-B chunk
       const uint32_t dstbuf = sH_addr + (t & 1) * hbuf + kbx * Bc * 128;
-      const int n = Bc * nq * G;
-      for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
-        const int dst = idx % G, rest = idx / G, q = rest % nq, bl = rest / nq;
-        const uint4 val = *reinterpret_cast<const uint4*>(sX + bl * 32 + 8 * q);
-        const uint32_t off = dstbuf + bl * 128 + (((cbase + q) ^ (bl & 7)) << 4);
-        ptx::st_cluster_v4(ptx::mapa(off, dst), val);
-      }
+      const int q = threadIdx.x & 3;
+      if (q < nq)
+        for (int bl = threadIdx.x >> 2; bl < Bc; bl += blockDim.x >> 2) {
+          const uint4 val = *reinterpret_cast<const uint4*>(sX + bl * 32 + 8 * q);
+          const uint32_t off = dstbuf + bl * 128 + (((cbase + q) ^ (bl & 7)) << 4);
+          for (int dst = 0; dst < G; ++dst) ptx::st_cluster_v4(ptx::mapa(off, dst), val);
+        }
     }
     ptx::tc_fence_before();
     ptx::cluster_arrive();
@@ -769,10 +781,11 @@ __global__ void __launch_bounds__(128, 1)
       if (threadIdx.x == 0) {
         ptx::fence_async_smem();
         const uint32_t aU = ptx::smem_u32(sU), aA = sA_addr + ((t + 1) & 1) * abuf;
+        const uint64_t ad0 = ptx::smem_desc_sw128(aU, 8192, 1024), bd0 = ptx::smem_desc_sw128(aA, 0, 1024);
         for (int k = 0; k < nkb * 4; ++k) {
-          const int kb = k >> 2, kk = k & 3;
-          const uint64_t ad = ptx::smem_desc_sw128(aU + kb * 8192 + kk * 2048, 8192, 1024);
-          const uint64_t bd = ptx::smem_desc_sw128(aA + kb * Bc * 128 + kk * 32, 0, 1024);
+          const int kb = k >> 2, kk = k & 3;  // start-address field is in 16-B units
+          const uint64_t ad = ad0 + (uint64_t)((kb * 8192 + kk * 2048) >> 4);
+          const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kk * 32) >> 4);
           ptx::mma_f16(tbase, ad, bd, idesc, k > 0 ? 1u : 0u);
         }
         ptx::mma_commit(barM);
@@ -807,8 +820,9 @@ __global__ void __launch_bounds__(128, 1)
           const float2 if2 = __half22float2(*reinterpret_cast<const __half2*>(&gq[idx].x));
           const float2 go2 = __half22float2(*reinterpret_cast<const __half2*>(&gq[idx].y));
           const float i = if2.x, f = if2.y, g = go2.x, o = go2.y;
-          const float tc = tanhf(cc[idx]);
-          const float d = dcr[idx] + dh * o * (1.f - tc * tc);
+          float tc, sech2;
+          tanh_sech2(cc[idx], tc, sech2);
+          const float d = dcr[idx] + dh * o * sech2;
           __align__(8) __half2 q2[2] = {
               __halves2half2(__float2half_rn(d * g * i * (1.f - i)), __float2half_rn(d * cp[idx] * f * (1.f - f))),
               __halves2half2(__float2half_rn(d * i * (1.f - g * g)), __float2half_rn(dh * tc * o * (1.f - o)))};
@@ -822,14 +836,16 @@ __global__ void __launch_bounds__(128, 1)
     __syncthreads();
     // push my dA_t slice (gate rows [256 rank, 256 rank + 4 nvalid)) into every peer's sA[t & 1]
     {
+      // thread = (chunk q = lane, rows bl = warp, warp + 4, ...): 16-B chunk q covers gate rows 8q..8q+7
       const uint32_t dstbuf = sA_addr + (t & 1) * abuf;
-      const int n = Bc * nq * G;
-      for (int idx = threadIdx.x; idx < n; idx += blockDim.x) {
-        const int dst = idx % G, rest = idx / G, q = rest % nq, bl = rest / nq;
-        const uint4 val = *reinterpret_cast<const uint4*>(sX + bl * 256 + 8 * q);
+      const int q = lane;
+      if (q < nq) {
         const int kb = 4 * rank + (q >> 3), c = q & 7;
-        const uint32_t off = dstbuf + kb * Bc * 128 + bl * 128 + ((c ^ (bl & 7)) << 4);
-        ptx::st_cluster_v4(ptx::mapa(off, dst), val);
+        for (int bl = warp; bl < Bc; bl += 4) {
+          const uint4 val = *reinterpret_cast<const uint4*>(sX + bl * 256 + 8 * q);
+          const uint32_t off = dstbuf + kb * Bc * 128 + bl * 128 + ((c ^ (bl & 7)) << 4);
+          for (int dst = 0; dst < G; ++dst) ptx::st_cluster_v4(ptx::mapa(off, dst), val);
+        }
       }
     }
     ptx::tc_fence_before();
