@@ -58,7 +58,7 @@ class Clocks:
              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
         try:
             self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+                                       "-lms", "20"], stdout=self.f, stderr=subprocess.DEVNULL)
         except Exception:
             self.p = None
 
@@ -285,12 +285,15 @@ def run_c5(args, rank, world, local_rank):
 
     dev = torch.device(f"cuda:{local_rank}")
     torch.cuda.set_device(dev)
-    uid = None
-    if world > 1:
+
+    def fresh_uid():  # a NCCL unique id is single-use: one per communicator
+        if world == 1:
+            return None
         import torch.distributed as dist
         obj = [hdp.nccl_unique_id() if rank == 0 else None]
         dist.broadcast_object_list(obj, src=0)
-        uid = obj[0]
+        return obj[0]
+
     sizes_mib = [int(v) for v in args.sizes.split(",")]
     wire = {"fp16": hdp.WIRE_FP16_A2A, "fp16sum": hdp.WIRE_FP16_NCCLSUM, "fp32": hdp.WIRE_FP32}[args.wire]
     gsz = 4 if wire == hdp.WIRE_FP32 else 2
@@ -303,7 +306,7 @@ def run_c5(args, rank, world, local_rank):
         S = (mib << 20) // 2          # fp16 gradient elements
         desc = hdp.ModelDesc(n_layers=0, max_batch=1, max_seq=1, math=hdp.MATH_MIXED16, wire=wire,
                              optimizer=hdp.OPT_SGDM, sim_workers=nsim, flat_params=S)
-        ctx = hdp.init(world, rank, uid, local_rank)
+        ctx = hdp.init(world, rank, fresh_uid(), local_rank)
         sz = hdp.configure(ctx, desc)
         arena = torch.empty(sz.arena_bytes + 256, dtype=torch.uint8, device=dev)
         base = arena.data_ptr() + ((-arena.data_ptr()) % 256)
