@@ -1,5 +1,4 @@
-nvidia-smi topo -m > gpurun_out/topo.txt 2>&1
-timeout -s KILL 900 python -m pytest tests/test_gpu_multi.py -q -p no:cacheprovider > gpurun_out/multi_tests.log 2>&1; echo exit=$? >> gpurun_out/multi_tests.log
-timeout -s KILL 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 20 --warmup 5 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err; echo exit=$? >> gpurun_out/bench_n2.err
-timeout -s KILL 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 2 --config C5 --steps 10 --warmup 3 > gpurun_out/c5_n2.json 2> gpurun_out/c5_n2.err; echo exit=$? >> gpurun_out/c5_n2.err
-tail -5 gpurun_out/multi_tests.log
+timeout -s KILL 600 python tools/gemm_bench.py > gpurun_out/gemm_bench.log 2>&1; echo exit=$? >> gpurun_out/gemm_bench.log
+timeout -s KILL 900 python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider -x -k "c3" > gpurun_out/c3_tests.log 2>&1; echo exit=$? >> gpurun_out/c3_tests.log
+timeout -s KILL 600 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_c3.json 2> gpurun_out/bench_c3.err
+tail -3 gpurun_out/c3_tests.log

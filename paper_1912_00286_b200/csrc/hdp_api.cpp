@@ -137,6 +137,7 @@ struct hdp_ctx {
   size_t ws_floats = 0;
   int32_t *keys_in = nullptr, *keys_out = nullptr, *vals_in = nullptr, *vals_out = nullptr;
   void* sort_temp = nullptr;
+  float* emb_part = nullptr;
   size_t sort_bytes = 0;
   int* status = nullptr;  // [0] nonfinite count
   float* loadbuf = nullptr;
@@ -363,6 +364,7 @@ void carve(hdp_ctx* c, char* base) {
       c->vals_out = (int32_t*)cv.take(rows * 4);
       c->sort_bytes = hdp::embed_sort_temp_bytes((int)rows);
       c->sort_temp = cv.take(c->sort_bytes);
+      c->emb_part = (float*)cv.take(hdp::embed_part_floats((int)rows, (int)c->Ip0) * 4);
     }
   }
   c->arena_bytes = rup(cv.off, 256);

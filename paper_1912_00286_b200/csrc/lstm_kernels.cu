@@ -261,19 +261,69 @@ __device__ __forceinline__ int lower_bound_(const int32_t* a, int n, int v) {
   return lo;
 }
 
-__global__ void embed_segsum_kernel(const int32_t* __restrict__ keys, const int32_t* __restrict__ vals, int n,
-                                    int vocab, const float* __restrict__ dX0, int Ep, int out_f32, void* dE) {
+// Deterministic two-level segmented sum over the token-sorted positions:
+// (1) one warp per fixed chunk of EMB_CHUNK sorted positions sums each run of
+//     equal tokens inside its chunk (ascending position order) and stores the
+//     partial at the run's first index;
+// (2) one warp per vocabulary row adds its partials (at its first index and
+//     at every chunk start inside its range) in index order.
+// No atomics; load-balanced for Zipf-frequent tokens.
+constexpr int EMB_CHUNK = 32;
+
+__global__ void embed_chunk_kernel(const int32_t* __restrict__ keys, const int32_t* __restrict__ vals, int n,
+                                   const float* __restrict__ dX0, int Ep, float* __restrict__ part) {
+  const long w = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  const int lane = threadIdx.x & 31;
+  const long i0 = w * EMB_CHUNK;
+  if (i0 >= n) return;
+  const long i1 = min((long)n, i0 + EMB_CHUNK);
+  for (int k0 = 0; k0 < Ep; k0 += 128) {
+    float acc[4] = {0.f, 0.f, 0.f, 0.f};
+    long start = i0;
+    int cur = keys[i0];
+    for (long i = i0; i < i1; ++i) {
+      const int key = keys[i];
+      if (key != cur) {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int k = k0 + lane + 32 * q;
+          if (k < Ep) part[start * Ep + k] = acc[q];
+          acc[q] = 0.f;
+        }
+        start = i;
+        cur = key;
+      }
+      const float* row = dX0 + (long)vals[i] * Ep;
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int k = k0 + lane + 32 * q;
+        if (k < Ep) acc[q] += row[k];
+      }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      const int k = k0 + lane + 32 * q;
+      if (k < Ep) part[start * Ep + k] = acc[q];
+    }
+  }
+}
+
+__global__ void embed_segsum_kernel(const int32_t* __restrict__ keys, int n, int vocab,
+                                    const float* __restrict__ part, int Ep, int out_f32, void* dE) {
   const long v = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (v >= vocab) return;
   const int lo = lower_bound_(keys, n, (int)v), hi = lower_bound_(keys, n, (int)v + 1);
   for (int k = lane; k < Ep; k += 32) {
     float s = 0.f;
-    for (int q = lo; q < hi; ++q) s += dX0[(long)vals[q] * Ep + k];  // ascending position order
+    if (lo < hi) {
+      s = part[(long)lo * Ep + k];
+      for (long c = ((long)lo / EMB_CHUNK + 1) * EMB_CHUNK; c < hi; c += EMB_CHUNK) s += part[c * Ep + k];
+    }
     if (out_f32)
       reinterpret_cast<float*>(dE)[v * Ep + k] = s;
     else
-      reinterpret_cast<__half*>(dE)[v * Ep + k] = __float2half_rn(s);
+      reinterpret_cast<__half*>(dE)[v * Ep + k] = __float2half_rn(s);  // R12
   }
 }
 
@@ -389,9 +439,11 @@ size_t embed_sort_temp_bytes(int n) {
   return bytes;
 }
 
+size_t embed_part_floats(int n, int Ep) { return (size_t)n * Ep; }
+
 cudaError_t launch_embed_backward(const int32_t* tok, int B, int T, int vocab, const float* dX0, int Ep,
                                   int32_t* keys_in, int32_t* keys_out, int32_t* vals_in, int32_t* vals_out,
-                                  void* sort_temp, size_t sort_temp_bytes, void* dE, int out_f32,
+                                  void* sort_temp, size_t sort_temp_bytes, float* part, void* dE, int out_f32,
                                   cudaStream_t s) {
   const int n = B * T;
   embed_keys_kernel<<<(n + 255) / 256, 256, 0, s>>>(tok, B, T, keys_in, vals_in);
@@ -400,9 +452,10 @@ cudaError_t launch_embed_backward(const int32_t* tok, int B, int T, int vocab, c
   size_t tb = sort_temp_bytes;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(sort_temp, tb, keys_in, keys_out, vals_in, vals_out, n, 0, bits, s);
   if (e != cudaSuccess) return e;
+  const long cw = ((long)n + EMB_CHUNK - 1) / EMB_CHUNK * 32;
+  embed_chunk_kernel<<<(int)((cw + 255) / 256), 256, 0, s>>>(keys_out, vals_out, n, dX0, Ep, part);
   const long threads = (long)vocab * 32;
-  embed_segsum_kernel<<<(int)((threads + 255) / 256), 256, 0, s>>>(keys_out, vals_out, n, vocab, dX0, Ep, out_f32,
-                                                                   dE);
+  embed_segsum_kernel<<<(int)((threads + 255) / 256), 256, 0, s>>>(keys_out, n, vocab, part, Ep, out_f32, dE);
   return cudaGetLastError();
 }
 
