@@ -674,7 +674,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
       KScope ks_(c, HDP_K_EMBED_BWD, 2, s);
       CK_CUDA(hdp::launch_embed_backward((const int32_t*)S.stage_x, B, T, d.vocab, dHnext, (int)c->Ip0, c->keys_in,
                                          c->keys_out, c->vals_in, c->vals_out, c->sort_temp, c->sort_bytes,
-                                         c->G(si, iE), gf, s));
+                                         c->emb_part, c->G(si, iE), gf, s));
     }
   }
   return HDP_OK;
