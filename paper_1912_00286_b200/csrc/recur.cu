@@ -563,7 +563,11 @@ __global__ void __launch_bounds__(512, 1)
   const int unit = grow >> 2;
   const bool unit_ok = unit < hp;
   const int fourhp = 4 * hp;
-  const uint32_t tcols = Bc <= 32 ? 32 : Bc <= 64 ? 64 : Bc <= 128 ? 128 : 256;
+  // independent accumulators: K-steps round-robin over nacc TMEM tiles so
+  // consecutive tcgen05.mma do not serialise on one accumulator
+  const int nacc = Bc <= 64 ? 4 : Bc <= 128 ? 2 : 1;
+  const int ac = nacc * Bc;
+  const uint32_t tcols = ac <= 32 ? 32 : ac <= 64 ? 64 : ac <= 128 ? 128 : ac <= 256 ? 256 : 512;
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch(&tmU);
@@ -616,7 +620,8 @@ __global__ void __launch_bounds__(512, 1)
           const int kb = k >> 2, kk = k & 3;  // start-address field is in 16-B units
           const uint64_t ad = ad0 + (uint64_t)((kb * 16384 + kk * 32) >> 4);
           const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kk * 32) >> 4);
-          ptx::mma_f16(tbase, ad, bd, idesc, k > 0 ? 1u : 0u);
+          const int a = k % nacc;
+          ptx::mma_f16(tbase + a * Bc, ad, bd, idesc, k >= nacc ? 1u : 0u);
         }
         ptx::mma_commit(barM);
       }
@@ -634,7 +639,14 @@ __global__ void __launch_bounds__(512, 1)
       const int c0 = ch * 16;
       float v[16];
       if (t > 0) {
-        ptx::tmem_ld16(tbase + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
+        const uint32_t ta = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + c0;
+        ptx::tmem_ld16(ta, v);
+        for (int a = 1; a < nacc && a < nk16; ++a) {
+          float w[16];
+          ptx::tmem_ld16(ta + a * Bc, w);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] += w[k];
+        }
       } else {
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = 0.f;
@@ -721,7 +733,9 @@ __global__ void __launch_bounds__(128, 1)
   const int ul = warp * 16 + jl;               // unit within my 64-unit slice
   const int unit = j0 + ul;
   const bool unit_ok = unit < hp;
-  constexpr uint32_t tcols = Bc <= 32 ? 32 : Bc <= 64 ? 64 : 128;
+  constexpr int NACC = Bc <= 32 ? 8 : 4;  // independent accumulators (see forward)
+  constexpr int AC = NACC * Bc;
+  constexpr uint32_t tcols = AC <= 32 ? 32 : AC <= 64 ? 64 : AC <= 128 ? 128 : 256;
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch(&tmU);
@@ -786,7 +800,7 @@ __global__ void __launch_bounds__(128, 1)
           const int kb = k >> 2, kk = k & 3;  // start-address field is in 16-B units
           const uint64_t ad = ad0 + (uint64_t)((kb * 8192 + kk * 2048) >> 4);
           const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kk * 32) >> 4);
-          ptx::mma_f16(tbase, ad, bd, idesc, k > 0 ? 1u : 0u);
+          ptx::mma_f16(tbase + (k % NACC) * Bc, ad, bd, idesc, k >= NACC ? 1u : 0u);
         }
         ptx::mma_commit(barM);
       }
@@ -799,7 +813,16 @@ __global__ void __launch_bounds__(128, 1)
     for (int ch = 0; ch < NC; ++ch) {
       float v[16];
       if (t < T - 1) {
-        ptx::tmem_ld16(tbase + (static_cast<uint32_t>(warp * 32) << 16) + ch * 16, v);
+        const uint32_t ta = tbase + (static_cast<uint32_t>(warp * 32) << 16) + ch * 16;
+        ptx::tmem_ld16(ta, v);
+#pragma unroll
+        for (int a = 1; a < NACC; ++a) {
+          if (a >= nkb * 4) break;  // accumulator never written (tiny K)
+          float w[16];
+          ptx::tmem_ld16(ta + a * Bc, w);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] += w[k];
+        }
       } else {
 #pragma unroll
         for (int k = 0; k < 16; ++k) v[k] = 0.f;
