@@ -612,9 +612,7 @@ __global__ void __launch_bounds__(512, 1)
     if (t > 0) {
       ptx::cluster_wait();  // all peers pushed h_{t-1} into sH[(t-1)&1]
       ptx::tc_fence_after();
-      if (warp == 0) {
-        // converged warp: descriptor math stays in the uniform datapath,
-        // one elected lane issues each tcgen05.mma
+      if (threadIdx.x == 0) {
         ptx::fence_async_smem();
         const uint32_t aU = ptx::smem_u32(sU), aH = sH_addr + ((t - 1) & 1) * hbuf;
         const uint64_t ad0 = ptx::smem_desc_sw128(aU, 0, 1024), bd0 = ptx::smem_desc_sw128(aH, 0, 1024);
@@ -623,12 +621,11 @@ __global__ void __launch_bounds__(512, 1)
           const uint64_t ad = ad0 + (uint64_t)((kb * 16384 + kk * 32) >> 4);
           const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kk * 32) >> 4);
           const int a = k % nacc;
-          if (ptx::elect_one()) ptx::mma_f16(tbase + a * Bc, ad, bd, idesc, k >= nacc ? 1u : 0u);
-          __syncwarp();
+          ptx::mma_f16(tbase + a * Bc, ad, bd, idesc, k >= nacc ? 1u : 0u);
         }
-        if (ptx::elect_one()) ptx::mma_commit(barM);
-        __syncwarp();
+        ptx::mma_commit(barM);
       }
+      __syncwarp();
       ptx::mbar_wait(barM, (t - 1) & 1);
       ptx::tc_fence_after();
     }
@@ -795,7 +792,7 @@ __global__ void __launch_bounds__(128, 1)
     if (t < T - 1) {
       ptx::cluster_wait();  // all peers pushed dA_{t+1} into sA[(t+1)&1]
       ptx::tc_fence_after();
-      if (warp == 0) {
+      if (threadIdx.x == 0) {
         ptx::fence_async_smem();
         const uint32_t aU = ptx::smem_u32(sU), aA = sA_addr + ((t + 1) & 1) * abuf;
         const uint64_t ad0 = ptx::smem_desc_sw128(aU, 8192, 1024), bd0 = ptx::smem_desc_sw128(aA, 0, 1024);
@@ -803,12 +800,11 @@ __global__ void __launch_bounds__(128, 1)
           const int kb = k >> 2, kk = k & 3;  // start-address field is in 16-B units
           const uint64_t ad = ad0 + (uint64_t)((kb * 8192 + kk * 2048) >> 4);
           const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kk * 32) >> 4);
-          if (ptx::elect_one()) ptx::mma_f16(tbase + (k % NACC) * Bc, ad, bd, idesc, k >= NACC ? 1u : 0u);
-          __syncwarp();
+          ptx::mma_f16(tbase + (k % NACC) * Bc, ad, bd, idesc, k >= NACC ? 1u : 0u);
         }
-        if (ptx::elect_one()) ptx::mma_commit(barM);
-        __syncwarp();
+        ptx::mma_commit(barM);
       }
+      __syncwarp();
       ptx::mbar_wait(barM, (T - 2 - t) & 1);
       ptx::tc_fence_after();
     }
