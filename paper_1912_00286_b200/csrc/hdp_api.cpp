@@ -641,8 +641,34 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
     ra.T = T;
     ra.B = B;
     ra.hp = (int)hp;
-    KScope ks_(c, HDP_K_RECUR_BWD, 1, s);
-    CK_CUDA(hdp::launch_recur_bwd(ra, s));
+    static unsigned long long* trace_buf = nullptr;  // debug: HDP_RECUR_TRACE=1 in profile (eager) mode
+    const bool want_trace = c->prof && getenv("HDP_RECUR_TRACE") && getenv("HDP_RECUR_TRACE")[0] == '1';
+    if (want_trace) {
+      if (!trace_buf) CK_CUDA(cudaMalloc(&trace_buf, 8192 * 5 * sizeof(unsigned long long)));
+      ra.trace = trace_buf;
+    }
+    {
+      KScope ks_(c, HDP_K_RECUR_BWD, 1, s);
+      CK_CUDA(hdp::launch_recur_bwd(ra, s));
+    }
+    if (want_trace && T <= 8192) {
+      std::vector<unsigned long long> h((size_t)T * 5);
+      CK_CUDA(cudaStreamSynchronize(s));
+      CK_CUDA(cudaMemcpy(h.data(), trace_buf, h.size() * 8, cudaMemcpyDeviceToHost));
+      double ph[4] = {0, 0, 0, 0}, step = 0;
+      int n = 0;
+      for (int t = T - 2; t >= 1; --t) {  // steps with an MMA; t+1 -> t gap is the step time
+        const unsigned long long* r = &h[(size_t)t * 5];
+        ph[0] += (double)(r[1] - r[0]);   // prefetch issue + cluster wait
+        ph[1] += (double)(r[2] - r[1]);   // MMA issue + completion
+        ph[2] += (double)(r[3] - r[2]);   // epilogue + syncthreads
+        ph[3] += (double)(r[4] - r[3]);   // DSMEM push + arrive
+        step += (double)(h[(size_t)(t - 1) * 5] - r[0]);
+        ++n;
+      }
+      fprintf(stderr, "[hdp trace] recur_bwd layer %d: per step ns: wait %.0f mma %.0f epilogue %.0f push %.0f | step %.0f\n",
+              l, ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, step / n);
+    }
   } else
   for (int t = T - 1; t >= 0; --t) {
     const float* dHa_t = last_only ? (t == T - 1 ? dHa : nullptr) : dHa + (long)t * B * hp;

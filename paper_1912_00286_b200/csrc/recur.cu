@@ -708,8 +708,10 @@ template <int NC>
 __global__ void __launch_bounds__(128, 1)
     recur_bwd_cl_kernel(const __grid_constant__ CUtensorMap tmU, const float* __restrict__ dHa, int dHa_last_only,
                         const __half* __restrict__ gates, const float* __restrict__ Cst, __half* __restrict__ dA,
-                        int T, int B, int hp) {
+                        int T, int B, int hp, unsigned long long* __restrict__ trace) {
   constexpr int Bc = 16 * NC;
+  // optional phase trace (CTA (0,0), thread 0): [t][5] globaltimer stamps
+  const bool tr = trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int fourhp = 4 * hp;
@@ -764,6 +766,7 @@ __global__ void __launch_bounds__(128, 1)
   const uint32_t sA_addr = ptx::smem_u32(sA);
 
   for (int t = T - 1; t >= 0; --t) {
+    if (tr) trace[t * 5 + 0] = ptx::globaltimer_ns();
     float dh0[NC * 8], cc[NC * 8], cp[NC * 8];
     uint2 gq[NC * 8];
 #pragma unroll
@@ -792,6 +795,7 @@ __global__ void __launch_bounds__(128, 1)
     if (t < T - 1) {
       ptx::cluster_wait();  // all peers pushed dA_{t+1} into sA[(t+1)&1]
       ptx::tc_fence_after();
+      if (tr) trace[t * 5 + 1] = ptx::globaltimer_ns();
       if (threadIdx.x == 0) {
         ptx::fence_async_smem();
         const uint32_t aU = ptx::smem_u32(sU), aA = sA_addr + ((t + 1) & 1) * abuf;
@@ -808,6 +812,7 @@ __global__ void __launch_bounds__(128, 1)
       ptx::mbar_wait(barM, (T - 2 - t) & 1);
       ptx::tc_fence_after();
     }
+    if (tr) trace[t * 5 + 2] = ptx::globaltimer_ns();
     __half* dAout = dA + (size_t)t * B * fourhp;
 #pragma unroll
     for (int ch = 0; ch < NC; ++ch) {
@@ -857,6 +862,7 @@ __global__ void __launch_bounds__(128, 1)
       }
     }
     __syncthreads();
+    if (tr) trace[t * 5 + 3] = ptx::globaltimer_ns();
     // push my dA_t slice (gate rows [256 rank, 256 rank + 4 nvalid)) into every peer's sA[t & 1]
     {
       // thread = (chunk q = lane, rows bl = warp, warp + 4, ...): 16-B chunk q covers gate rows 8q..8q+7
@@ -873,6 +879,7 @@ __global__ void __launch_bounds__(128, 1)
     }
     ptx::tc_fence_before();
     ptx::cluster_arrive();
+    if (tr) trace[t * 5 + 4] = ptx::globaltimer_ns();
   }
   ptx::cluster_wait();
   ptx::tc_fence_after();
@@ -971,7 +978,8 @@ cudaError_t launch_recur_bwd(const RecurBwdArgs& a, cudaStream_t s) {
     const __half* gt = a.gates;
     const float* cst = a.C;
     __half* da = a.dA;
-    void* args[] = {&mU, &dha, &last, &gt, &cst, &da, &T, &B, &hp};
+    unsigned long long* trace = a.trace;
+    void* args[] = {&mU, &dha, &last, &gt, &cst, &da, &T, &B, &hp, &trace};
     const void* fn = Bc == 16 ? (const void*)recur_bwd_cl_kernel<1>
                    : Bc == 32 ? (const void*)recur_bwd_cl_kernel<2>
                    : Bc == 48 ? (const void*)recur_bwd_cl_kernel<3> : (const void*)recur_bwd_cl_kernel<4>;

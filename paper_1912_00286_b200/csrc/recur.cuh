@@ -27,6 +27,7 @@ struct RecurBwdArgs {
   __half* dA = nullptr;           // [T][B][4hp] output (fp16, R10)
   unsigned* counter = nullptr;    // 16 x 32 uints
   int T = 0, B = 0, hp = 0;
+  unsigned long long* trace = nullptr;  // debug: per-step phase timestamps (T x 5), nullable
 };
 bool recur_bwd_supported(int B, int hp);
 cudaError_t launch_recur_bwd(const RecurBwdArgs& a, cudaStream_t s);
