@@ -125,6 +125,14 @@ __device__ __forceinline__ void st_cluster_v4(uint32_t addr, uint4 v) {
                "r"(v.w)
                : "memory");
 }
+// bulk async copy of `bytes` from my shared memory into a cluster peer's shared
+// memory; completes (complete_tx) on the peer's mbarrier.  dst / mbar are
+// shared::cluster addresses (mapa), src a shared::cta address.
+__device__ __forceinline__ void bulk_copy_to_peer(uint32_t dst, uint32_t src, uint32_t bytes, uint32_t mbar) {
+  asm volatile("cp.async.bulk.shared::cluster.shared::cta.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+               "r"(src), "r"(bytes), "r"(mbar)
+               : "memory");
+}
 __device__ __forceinline__ void cluster_arrive() { asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory"); }
 __device__ __forceinline__ void cluster_wait() { asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory"); }
 __device__ __forceinline__ void fence_async_smem() { asm volatile("fence.proxy.async.shared::cta;" ::: "memory"); }

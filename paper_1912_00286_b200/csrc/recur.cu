@@ -717,13 +717,15 @@ __global__ void __launch_bounds__(128, 1)
   const int fourhp = 4 * hp;
   const int nkb = fourhp / 64;
   const int abuf = nkb * Bc * 128;
+  constexpr int SX = 4 * Bc * 128;             // my 4 K-blocks (256 gate rows) in destination layout
   uint8_t* sU = smem;                          // nkb x 8 KB (U^T slice, MN-major)
-  uint8_t* sA = sU + nkb * 8192;               // [2][abuf]
-  __half* sX = reinterpret_cast<__half*>(sA + 2 * abuf);   // [Bc][256] staging of my dA_t slice
-  uint64_t* bars = reinterpret_cast<uint64_t*>(reinterpret_cast<uint8_t*>(sX) + Bc * 512);
+  uint8_t* sA = sU + nkb * 8192;               // [2][abuf] B operand (dA_{t+1}), filled by peers
+  uint8_t* sX = sA + 2 * abuf;                 // [2][SX] staging of my dA_t slice, swizzled like sA
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sX + 2 * SX);
   uint64_t* barU = bars;
   uint64_t* barM = bars + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+  uint64_t* fullA = bars + 2;                  // [2]: peers' bulk copies into sA[p]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
@@ -735,13 +737,20 @@ __global__ void __launch_bounds__(128, 1)
   const int ul = warp * 16 + jl;               // unit within my 64-unit slice
   const int unit = j0 + ul;
   const bool unit_ok = unit < hp;
-  constexpr int NACC = Bc <= 32 ? 8 : 4;  // independent accumulators (see forward)
+  constexpr int NACC = Bc <= 32 ? 8 : 4;
   constexpr int AC = NACC * Bc;
   constexpr uint32_t tcols = AC <= 32 ? 32 : AC <= 64 ? 64 : AC <= 128 ? 128 : 256;
+  // bytes every consumer receives per step: all producers' valid K-blocks
+  int total_bytes = 0;
+  for (int r = 0; r < G; ++r) total_bytes += max(0, min(64, hp - 64 * r)) / 16 * Bc * 128;
+  const int my_kblocks = max(0, min(64, hp - j0)) / 16;
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch(&tmU);
-    for (int i = 0; i < 2; ++i) ptx::mbar_init(bars + i, 1);
+    ptx::mbar_init(barU, 1);
+    ptx::mbar_init(barM, 4);  // one commit per issuing warp
+    ptx::mbar_init(fullA, 1);
+    ptx::mbar_init(fullA + 1, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc(tslot, tcols);
@@ -750,20 +759,22 @@ __global__ void __launch_bounds__(128, 1)
   ptx::tc_fence_after();
   const uint32_t tbase = *tslot;
   if (threadIdx.x == 0) {
+    // arm both operand slots for their first use before any peer can deliver
+    ptx::mbar_arrive_expect_tx(fullA, total_bytes);
+    ptx::mbar_arrive_expect_tx(fullA + 1, total_bytes);
     ptx::mbar_arrive_expect_tx(barU, nkb * 8192);
     for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sU + kb * 8192, &tmU, barU, j0, kb * 64);
     ptx::mbar_wait(barU, 0);
   }
-  ptx::cluster_arrive();
+  ptx::cluster_arrive();  // all CTAs resident, barriers initialised and armed
   ptx::cluster_wait();
 
   float dcr[NC * 8];
 #pragma unroll
   for (int i = 0; i < NC * 8; ++i) dcr[i] = 0.f;
   const uint32_t idesc = ptx::idesc_f16_f32(64, Bc, 1, 0);
-  const int nvalid = max(0, min(64, hp - j0));  // units of my slice
-  const int nq = nvalid / 2;                    // 16-B chunks (8 gate rows) per batch row
-  const uint32_t sA_addr = ptx::smem_u32(sA);
+  const uint32_t sA_addr = ptx::smem_u32(sA), sX_addr = ptx::smem_u32(sX);
+  uint32_t fphase[2] = {0u, 0u};
 
   for (int t = T - 1; t >= 0; --t) {
     if (tr) trace[t * 5 + 0] = ptx::globaltimer_ns();
@@ -793,14 +804,15 @@ __global__ void __launch_bounds__(128, 1)
         gq[idx] = gg;
       }
     if (t < T - 1) {
-      ptx::cluster_wait();  // all peers pushed dA_{t+1} into sA[(t+1)&1]
-      ptx::tc_fence_after();
-      if (tr) trace[t * 5 + 1] = ptx::globaltimer_ns();
-      if (threadIdx.x == 0) {
-        ptx::fence_async_smem();
-        const uint32_t aU = ptx::smem_u32(sU), aA = sA_addr + ((t + 1) & 1) * abuf;
+      const int p = (t + 1) & 1;
+      if (lane == 0) {
+        ptx::mbar_wait(fullA + p, fphase[p]);  // every peer's dA_{t+1} slice landed in sA[p]
+        ptx::tc_fence_after();
+        if (tr) trace[t * 5 + 1] = ptx::globaltimer_ns();
+        // lane 0 of each warp issues K-steps k = warp, warp + 4, ... (barM counts 4 commits)
+        const uint32_t aU = ptx::smem_u32(sU), aA = sA_addr + p * abuf;
         const uint64_t ad0 = ptx::smem_desc_sw128(aU, 8192, 1024), bd0 = ptx::smem_desc_sw128(aA, 0, 1024);
-        for (int k = 0; k < nkb * 4; ++k) {
+        for (int k = warp; k < nkb * 4; k += 4) {
           const int kb = k >> 2, kk = k & 3;  // start-address field is in 16-B units
           const uint64_t ad = ad0 + (uint64_t)((kb * 8192 + kk * 2048) >> 4);
           const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kk * 32) >> 4);
@@ -811,9 +823,14 @@ __global__ void __launch_bounds__(128, 1)
       __syncwarp();
       ptx::mbar_wait(barM, (T - 2 - t) & 1);
       ptx::tc_fence_after();
+      fphase[p] ^= 1u;
+      // re-arm slot p for its next use (peers can deliver into it only after
+      // they consumed my dA_t, i.e. after this point -- see the WAR note below)
+      if (threadIdx.x == 0 && t >= 2) ptx::mbar_arrive_expect_tx(fullA + p, total_bytes);
     }
     if (tr) trace[t * 5 + 2] = ptx::globaltimer_ns();
     __half* dAout = dA + (size_t)t * B * fourhp;
+    uint8_t* stg = sX + (t & 1) * SX;
 #pragma unroll
     for (int ch = 0; ch < NC; ++ch) {
       float v[16];
@@ -839,6 +856,9 @@ __global__ void __launch_bounds__(128, 1)
         rec[k] = half ? hi : v[k];
       }
       if (unit_ok) {
+        // staging position of my unit's 4 gate rows (local gate row 4*ul) in row bl:
+        // K-block j = ul/16, 16-B chunk c = (4ul % 64)/8, byte (4ul % 8)*2
+        const int j = ul >> 4, c = (ul & 15) >> 1, byo = (ul & 1) * 8;
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int idx = ch * 8 + k;
@@ -855,41 +875,37 @@ __global__ void __launch_bounds__(128, 1)
               __halves2half2(__float2half_rn(d * g * i * (1.f - i)), __float2half_rn(d * cp[idx] * f * (1.f - f))),
               __halves2half2(__float2half_rn(d * i * (1.f - g * g)), __float2half_rn(dh * tc * o * (1.f - o)))};
           const uint2 pk = *reinterpret_cast<const uint2*>(q2);
-          *reinterpret_cast<uint2*>(dAout + b * fourhp + 4 * unit) = pk;      // R10 (for K8 / K9)
-          *reinterpret_cast<uint2*>(sX + bl * 256 + 4 * ul) = pk;            // staging for the peers
+          *reinterpret_cast<uint2*>(dAout + b * fourhp + 4 * unit) = pk;  // R10 (for K8 / K9)
+          *reinterpret_cast<uint2*>(stg + j * Bc * 128 + bl * 128 + ((c ^ (bl & 7)) << 4) + byo) = pk;
           dcr[idx] = d * f;
         }
       }
     }
+    ptx::tc_fence_before();
+    ptx::fence_async_smem();  // staging writes (generic) -> bulk copy reads (async proxy)
     __syncthreads();
     if (tr) trace[t * 5 + 3] = ptx::globaltimer_ns();
-    // push my dA_t slice (gate rows [256 rank, 256 rank + 4 nvalid)) into every peer's sA[t & 1]
-    {
-      // thread = (chunk q = lane, rows bl = warp, warp + 4, ...): 16-B chunk q covers gate rows 8q..8q+7
-      const uint32_t dstbuf = sA_addr + (t & 1) * abuf;
-      const int q = lane;
-      if (q < nq) {
-        const int kb = 4 * rank + (q >> 3), c = q & 7;
-        for (int bl = warp; bl < Bc; bl += 4) {
-          const uint4 val = *reinterpret_cast<const uint4*>(sX + bl * 256 + 8 * q);
-          const uint32_t off = dstbuf + kb * Bc * 128 + bl * 128 + ((c ^ (bl & 7)) << 4);
-          for (int dst = 0; dst < G; ++dst) ptx::st_cluster_v4(ptx::mapa(off, dst), val);
-        }
-      }
+    // push dA_t (consumed by step t-1) into every peer's sA[t & 1]: one bulk copy per peer.
+    // WAR: a peer writes sA[p] of step s only after consuming my dA_{s+1}, which I produce
+    // after my MMA that read sA[p] for step s+2 -- the double buffers need no extra barrier.
+    if (t > 0 && threadIdx.x < G && my_kblocks > 0) {
+      const int dst = threadIdx.x;
+      const uint32_t dsta = ptx::mapa(sA_addr + (t & 1) * abuf + 4 * rank * Bc * 128, dst);
+      const uint32_t mb = ptx::mapa(ptx::smem_u32(fullA + (t & 1)), dst);
+      ptx::bulk_copy_to_peer(dsta, sX_addr + (t & 1) * SX, my_kblocks * Bc * 128, mb);
     }
-    ptx::tc_fence_before();
-    ptx::cluster_arrive();
     if (tr) trace[t * 5 + 4] = ptx::globaltimer_ns();
   }
+  // nobody leaves while a peer may still read my staging / write my sA
+  ptx::cluster_arrive();
   ptx::cluster_wait();
   ptx::tc_fence_after();
-  __syncthreads();
   if (warp == 2) ptx::tmem_dealloc(tbase, tcols);
 }
 
 size_t bwd_cl_smem(int hp, int Bc) {
   const int nkb = 4 * hp / 64;
-  return 1024 + (size_t)nkb * 8192 + 2 * (size_t)nkb * Bc * 128 + (size_t)Bc * 512 + 128;
+  return 1024 + (size_t)nkb * 8192 + 2 * (size_t)nkb * Bc * 128 + 2 * (size_t)4 * Bc * 128 + 128;
 }
 
 cudaError_t launch_cluster(const void* fn, dim3 grid, dim3 block, size_t smem, int cluster_x, cudaStream_t s,
