@@ -541,15 +541,16 @@ __global__ void __launch_bounds__(512, 1)
   const int nk16 = (hp + 15) / 16;
   const int nwarps = blockDim.x >> 5;
   const int cgN = nwarps >> 2;
-  const int hbuf = nkb * Bc * 128;            // one h operand buffer
+  const int hbuf = nkb * Bc * 128;            // one h operand buffer (K-major SW128)
   uint8_t* sU = smem;
-  uint8_t* sH = sU + nkb * 16384;             // [2][hbuf]
-  __half* sX = reinterpret_cast<__half*>(sH + 2 * hbuf);  // [Bc][32] staging of my h_t slice
-  float* sAct = reinterpret_cast<float*>(reinterpret_cast<uint8_t*>(sX) + ((Bc * 64 + 127) & ~127));
+  uint8_t* sH = sU + nkb * 16384;             // [2][hbuf], filled by the peers' bulk copies
+  uint8_t* sX = sH + 2 * hbuf;                // [2][Bc][64 B] staging of my h_t slice (destination order)
+  float* sAct = reinterpret_cast<float*>(sX + 2 * Bc * 64);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sAct + nwarps * 16 * ACT_LD);
   uint64_t* barU = bars;
   uint64_t* barM = bars + 1;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2);
+  uint64_t* fullH = bars + 2;                 // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int quarter = warp & 3, cg = warp >> 2;
@@ -563,15 +564,22 @@ __global__ void __launch_bounds__(512, 1)
   const int unit = grow >> 2;
   const bool unit_ok = unit < hp;
   const int fourhp = 4 * hp;
-  // independent accumulators: K-steps round-robin over nacc TMEM tiles so
-  // consecutive tcgen05.mma do not serialise on one accumulator
+  // independent accumulators, one per issuing warp (K-steps round-robin)
   const int nacc = Bc <= 64 ? 4 : Bc <= 128 ? 2 : 1;
+  const int nis = min(nacc, nk16);            // issuing warps
   const int ac = nacc * Bc;
   const uint32_t tcols = ac <= 32 ? 32 : ac <= 64 ? 64 : ac <= 128 ? 128 : ac <= 256 ? 256 : 512;
+  const int nvalid = max(0, min(32, hp - 32 * rank));  // units of my slice inside h_p
+  const int nq = nvalid / 8;                  // 16-B chunks per row (2 or 4)
+  const int kbx = (32 * rank) / 64, cbase = ((32 * rank) % 64) / 8;
+  const int total_bytes = Bc * hp * 2;        // every consumer receives all of h_{t-1}
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch(&tmU);
-    for (int i = 0; i < 2; ++i) ptx::mbar_init(bars + i, 1);
+    ptx::mbar_init(barU, 1);
+    ptx::mbar_init(barM, nis);
+    ptx::mbar_init(fullH, 1);
+    ptx::mbar_init(fullH + 1, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc(tslot, tcols);
@@ -580,11 +588,13 @@ __global__ void __launch_bounds__(512, 1)
   ptx::tc_fence_after();
   const uint32_t tbase = *tslot;
   if (threadIdx.x == 0) {
+    ptx::mbar_arrive_expect_tx(fullH, total_bytes);
+    ptx::mbar_arrive_expect_tx(fullH + 1, total_bytes);
     ptx::mbar_arrive_expect_tx(barU, nkb * 16384);
     for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sU + kb * 16384, &tmU, barU, kb * 64, row0);
     ptx::mbar_wait(barU, 0);
   }
-  ptx::cluster_arrive();  // every CTA of the cluster is resident before any remote write
+  ptx::cluster_arrive();  // all CTAs resident, barriers initialised and armed
   ptx::cluster_wait();
 
   float creg[NCI * 4];
@@ -594,10 +604,8 @@ __global__ void __launch_bounds__(512, 1)
   const int nchunk = Bc / 16;
   float* myAct = sAct + warp * 16 * ACT_LD;
   const float gsc = gate == 2 ? 2.f : 1.f;
-  const int nvalid = max(0, min(32, hp - 32 * rank));  // units of my slice inside h_p
-  const int nq = nvalid / 8;
-  const int kbx = (32 * rank) / 64, cbase = ((32 * rank) % 64) / 8;
-  const uint32_t sH_addr = ptx::smem_u32(sH);
+  const uint32_t sH_addr = ptx::smem_u32(sH), sX_addr = ptx::smem_u32(sX);
+  uint32_t fphase[2] = {0u, 0u};
 
   for (int t = 0; t < T; ++t) {
     float gx[NCI][16];
@@ -610,28 +618,30 @@ __global__ void __launch_bounds__(512, 1)
       for (int k = 0; k < 16; ++k) gx[ci][k] = ok ? __ldg(gp + (size_t)k * fourhp) : 0.f;
     }
     if (t > 0) {
-      ptx::cluster_wait();  // all peers pushed h_{t-1} into sH[(t-1)&1]
-      ptx::tc_fence_after();
-      if (threadIdx.x == 0) {
-        ptx::fence_async_smem();
-        const uint32_t aU = ptx::smem_u32(sU), aH = sH_addr + ((t - 1) & 1) * hbuf;
+      const int p = (t - 1) & 1;
+      if (lane == 0 && warp < nis) {
+        ptx::mbar_wait(fullH + p, fphase[p]);  // every peer's h_{t-1} slice landed in sH[p]
+        ptx::tc_fence_after();
+        const uint32_t aU = ptx::smem_u32(sU), aH = sH_addr + p * hbuf;
         const uint64_t ad0 = ptx::smem_desc_sw128(aU, 0, 1024), bd0 = ptx::smem_desc_sw128(aH, 0, 1024);
-        for (int k = 0; k < nk16; ++k) {
+        for (int k = warp; k < nk16; k += nis) {
           const int kb = k >> 2, kk = k & 3;  // start-address field is in 16-B units
           const uint64_t ad = ad0 + (uint64_t)((kb * 16384 + kk * 32) >> 4);
           const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kk * 32) >> 4);
-          const int a = k % nacc;
-          ptx::mma_f16(tbase + a * Bc, ad, bd, idesc, k >= nacc ? 1u : 0u);
+          ptx::mma_f16(tbase + warp * Bc, ad, bd, idesc, k >= nis ? 1u : 0u);
         }
         ptx::mma_commit(barM);
       }
       __syncwarp();
       ptx::mbar_wait(barM, (t - 1) & 1);
       ptx::tc_fence_after();
+      fphase[p] ^= 1u;
+      if (threadIdx.x == 0 && t + 2 <= T - 1) ptx::mbar_arrive_expect_tx(fullH + p, total_bytes);
     }
     __half* hout = Hs + (size_t)(t + 1) * B * hp;
     float* cout = Cst + (size_t)t * B * hp;
     __half* gout = gates + (size_t)t * B * fourhp;
+    uint8_t* stg = sX + (t & 1) * Bc * 64;
 #pragma unroll
     for (int ci = 0; ci < NCI; ++ci) {
       const int ch = ci * cgN + cg;
@@ -641,7 +651,7 @@ __global__ void __launch_bounds__(512, 1)
       if (t > 0) {
         const uint32_t ta = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + c0;
         ptx::tmem_ld16(ta, v);
-        for (int a = 1; a < nacc && a < nk16; ++a) {
+        for (int a = 1; a < nis; ++a) {
           float w[16];
           ptx::tmem_ld16(ta + a * Bc, w);
 #pragma unroll
@@ -656,6 +666,8 @@ __global__ void __launch_bounds__(512, 1)
       __syncwarp();
       if (unit_ok) {
         const int u = lane >> 2;
+        const int ul = quarter * 8 + u;       // unit within my 32-unit slice
+        const int c = cbase + (ul >> 3);      // 16-B chunk of the destination row
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int col = 4 * q + gate;
@@ -663,12 +675,14 @@ __global__ void __launch_bounds__(512, 1)
           const int bl = c0 + col;
           const size_t b = (size_t)col0 + bl;
           const float i = a4.x, f = a4.y, g = a4.z, o = a4.w;
-          const float c = f * creg[ci * 4 + q] + i * g;
-          creg[ci * 4 + q] = c;
-          const __half hh = __float2half_rn(o * act_gate(c, 2.f));
-          cout[b * hp + unit] = c;                   // R5
-          hout[b * hp + unit] = hh;                  // R6
-          sX[bl * 32 + quarter * 8 + u] = hh;
+          const float cv = f * creg[ci * 4 + q] + i * g;
+          creg[ci * 4 + q] = cv;
+          const __half hh = __float2half_rn(o * act_gate(cv, 2.f));
+          cout[b * hp + unit] = cv;                   // R5
+          hout[b * hp + unit] = hh;                   // R6
+          // staging in destination order: chunk c sits at slot (c ^ (bl & 7)) within my nq-chunk group
+          const int slot = (c ^ (bl & 7)) & (nq - 1);
+          *reinterpret_cast<__half*>(stg + bl * 64 + slot * 16 + (ul & 7) * 2) = hh;
           __align__(8) __half2 gg[2] = {__halves2half2(__float2half_rn(i), __float2half_rn(f)),
                                         __halves2half2(__float2half_rn(g), __float2half_rn(o))};
           *reinterpret_cast<uint2*>(gout + b * fourhp + 4 * unit) = *reinterpret_cast<const uint2*>(gg);  // R4
@@ -676,31 +690,29 @@ __global__ void __launch_bounds__(512, 1)
       }
       __syncwarp();
     }
-    __syncthreads();
-    // push my h_t slice (units [32 rank, 32 rank + nvalid)) into every peer's sH[t & 1]
-    {
-      // thread = (chunk q = tid & 3, row bl = tid >> 2): 8 units per 16-B chunk
-      const uint32_t dstbuf = sH_addr + (t & 1) * hbuf + kbx * Bc * 128;
-      const int q = threadIdx.x & 3;
-      if (q < nq)
-        for (int bl = threadIdx.x >> 2; bl < Bc; bl += blockDim.x >> 2) {
-          const uint4 val = *reinterpret_cast<const uint4*>(sX + bl * 32 + 8 * q);
-          const uint32_t off = dstbuf + bl * 128 + (((cbase + q) ^ (bl & 7)) << 4);
-          for (int dst = 0; dst < G; ++dst) ptx::st_cluster_v4(ptx::mapa(off, dst), val);
-        }
-    }
     ptx::tc_fence_before();
-    ptx::cluster_arrive();
+    ptx::fence_async_smem();  // staging writes (generic) -> bulk copy reads (async proxy)
+    __syncthreads();
+    // push h_t (consumed at step t+1) into every peer's sH[t & 1]: one copy per (row, peer)
+    if (t < T - 1 && nq > 0) {
+      for (int idx = threadIdx.x; idx < Bc * G; idx += blockDim.x) {
+        const int bl = idx / G, dst = idx - bl * G;
+        const int gstart = (cbase ^ (bl & 7)) & ~(nq - 1);
+        const uint32_t dsta = ptx::mapa(sH_addr + (t & 1) * hbuf + kbx * Bc * 128 + bl * 128 + gstart * 16, dst);
+        const uint32_t mb = ptx::mapa(ptx::smem_u32(fullH + (t & 1)), dst);
+        ptx::bulk_copy_to_peer(dsta, sX_addr + (t & 1) * Bc * 64 + bl * 64, nq * 16, mb);
+      }
+    }
   }
-  ptx::cluster_wait();  // no CTA leaves while peers may still write into its shared memory
+  ptx::cluster_arrive();  // nobody leaves while a peer may still read my staging / write my sH
+  ptx::cluster_wait();
   ptx::tc_fence_after();
-  __syncthreads();
   if (warp == 2) ptx::tmem_dealloc(tbase, tcols);
 }
 
 size_t fwd_cl_smem(int hp, int Bc, int nwarps) {
   const int nkb = (hp + 63) / 64;
-  return 1024 + (size_t)nkb * 16384 + 2 * (size_t)nkb * Bc * 128 + ((Bc * 64 + 127) & ~127) +
+  return 1024 + (size_t)nkb * 16384 + 2 * (size_t)nkb * Bc * 128 + 2 * (size_t)Bc * 64 +
          (size_t)nwarps * 16 * ACT_LD * 4 + 128;
 }
 
