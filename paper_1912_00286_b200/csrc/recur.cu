@@ -531,21 +531,25 @@ cudaError_t launch_bwd_t(const RecurBwdArgs& a, int nbg, cudaStream_t s) {
 // barrier and the TMA reload.  Global copies (needed by later kernels) are
 // still written, off the critical path.
 
+// CTA = 64 units = 256 interleaved gate rows (two M=128 MMAs per K-step) =
+// one full 64-wide K-block of h, so its h_t slice is one contiguous region of
+// every peer's operand buffer.  Warps: 4 lane quarters x 2 row halves x cgN
+// column groups.
 template <int NCI>
 __global__ void __launch_bounds__(512, 1)
     recur_fwd_cl_kernel(const __grid_constant__ CUtensorMap tmU, const float* __restrict__ Gx, int T, int B, int Bc,
                         int hp, __half* __restrict__ Hs, float* __restrict__ Cst, __half* __restrict__ gates) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int nkb = (hp + 63) / 64;
+  const int nkb = (hp + 63) / 64;             // == cluster size
   const int nk16 = (hp + 15) / 16;
   const int nwarps = blockDim.x >> 5;
-  const int cgN = nwarps >> 2;
+  const int cgN = nwarps >> 3;
   const int hbuf = nkb * Bc * 128;            // one h operand buffer (K-major SW128)
-  uint8_t* sU = smem;
-  uint8_t* sH = sU + nkb * 16384;             // [2][hbuf], filled by the peers' bulk copies
-  uint8_t* sX = sH + 2 * hbuf;                // [2][Bc][64 B] staging of my h_t slice (destination order)
-  float* sAct = reinterpret_cast<float*>(sX + 2 * Bc * 64);
+  uint8_t* sU = smem;                         // [2 halves][nkb][16 KB]
+  uint8_t* sH = sU + 2 * nkb * 16384;         // [2][hbuf], filled by the peers' bulk copies
+  uint8_t* sX = sH + 2 * hbuf;                // [2][Bc][128 B] my h_t K-block (destination layout)
+  float* sAct = reinterpret_cast<float*>(sX + 2 * Bc * 128);
   uint64_t* bars = reinterpret_cast<uint64_t*>(sAct + nwarps * 16 * ACT_LD);
   uint64_t* barU = bars;
   uint64_t* barM = bars + 1;
@@ -553,26 +557,22 @@ __global__ void __launch_bounds__(512, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int quarter = warp & 3, cg = warp >> 2;
+  const int quarter = warp & 3, hf = (warp >> 2) & 1, cg = warp >> 3;
   const int G = gridDim.x;                    // == cluster size
   const int rank = blockIdx.x;
-  const int row0 = rank * 128;
+  const int row0 = rank * 256;
   const int col0 = blockIdx.y * Bc;
-  const int r = quarter * 32 + lane;
+  const int r = hf * 128 + quarter * 32 + lane;  // tile row in [0, 256)
   const int grow = row0 + r;
   const int gate = r & 3;
   const int unit = grow >> 2;
   const bool unit_ok = unit < hp;
   const int fourhp = 4 * hp;
-  // independent accumulators, one per issuing warp (K-steps round-robin)
-  const int nacc = Bc <= 64 ? 4 : Bc <= 128 ? 2 : 1;
+  const int nacc = Bc <= 32 ? 4 : Bc <= 64 ? 2 : 1;
   const int nis = min(nacc, nk16);            // issuing warps
-  const int ac = nacc * Bc;
+  const int ac = 2 * nacc * Bc;               // [half][acc][Bc] fp32 columns
   const uint32_t tcols = ac <= 32 ? 32 : ac <= 64 ? 64 : ac <= 128 ? 128 : ac <= 256 ? 256 : 512;
-  const int nvalid = max(0, min(32, hp - 32 * rank));  // units of my slice inside h_p
-  const int nq = nvalid / 8;                  // 16-B chunks per row (2 or 4)
-  const int kbx = (32 * rank) / 64, cbase = ((32 * rank) % 64) / 8;
-  const int total_bytes = Bc * hp * 2;        // every consumer receives all of h_{t-1}
+  const int total_bytes = nkb * Bc * 128;     // every consumer receives all of h_{t-1}
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch(&tmU);
@@ -590,8 +590,10 @@ __global__ void __launch_bounds__(512, 1)
   if (threadIdx.x == 0) {
     ptx::mbar_arrive_expect_tx(fullH, total_bytes);
     ptx::mbar_arrive_expect_tx(fullH + 1, total_bytes);
-    ptx::mbar_arrive_expect_tx(barU, nkb * 16384);
-    for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sU + kb * 16384, &tmU, barU, kb * 64, row0);
+    ptx::mbar_arrive_expect_tx(barU, 2 * nkb * 16384);
+    for (int h2 = 0; h2 < 2; ++h2)
+      for (int kb = 0; kb < nkb; ++kb)
+        ptx::tma_load_2d(sU + (h2 * nkb + kb) * 16384, &tmU, barU, kb * 64, row0 + h2 * 128);
     ptx::mbar_wait(barU, 0);
   }
   ptx::cluster_arrive();  // all CTAs resident, barriers initialised and armed
@@ -620,15 +622,18 @@ __global__ void __launch_bounds__(512, 1)
     if (t > 0) {
       const int p = (t - 1) & 1;
       if (lane == 0 && warp < nis) {
-        ptx::mbar_wait(fullH + p, fphase[p]);  // every peer's h_{t-1} slice landed in sH[p]
+        ptx::mbar_wait(fullH + p, fphase[p]);  // every peer's h_{t-1} K-block landed in sH[p]
         ptx::tc_fence_after();
         const uint32_t aU = ptx::smem_u32(sU), aH = sH_addr + p * hbuf;
         const uint64_t ad0 = ptx::smem_desc_sw128(aU, 0, 1024), bd0 = ptx::smem_desc_sw128(aH, 0, 1024);
         for (int k = warp; k < nk16; k += nis) {
           const int kb = k >> 2, kk = k & 3;  // start-address field is in 16-B units
-          const uint64_t ad = ad0 + (uint64_t)((kb * 16384 + kk * 32) >> 4);
           const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kk * 32) >> 4);
-          ptx::mma_f16(tbase + warp * Bc, ad, bd, idesc, k >= nis ? 1u : 0u);
+#pragma unroll
+          for (int h2 = 0; h2 < 2; ++h2) {
+            const uint64_t ad = ad0 + (uint64_t)(((h2 * nkb + kb) * 16384 + kk * 32) >> 4);
+            ptx::mma_f16(tbase + (h2 * nacc + warp) * Bc, ad, bd, idesc, k >= nis ? 1u : 0u);
+          }
         }
         ptx::mma_commit(barM);
       }
@@ -641,7 +646,7 @@ __global__ void __launch_bounds__(512, 1)
     __half* hout = Hs + (size_t)(t + 1) * B * hp;
     float* cout = Cst + (size_t)t * B * hp;
     __half* gout = gates + (size_t)t * B * fourhp;
-    uint8_t* stg = sX + (t & 1) * Bc * 64;
+    uint8_t* stg = sX + (t & 1) * Bc * 128;
 #pragma unroll
     for (int ci = 0; ci < NCI; ++ci) {
       const int ch = ci * cgN + cg;
@@ -649,7 +654,7 @@ __global__ void __launch_bounds__(512, 1)
       const int c0 = ch * 16;
       float v[16];
       if (t > 0) {
-        const uint32_t ta = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + c0;
+        const uint32_t ta = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + hf * nacc * Bc + c0;
         ptx::tmem_ld16(ta, v);
         for (int a = 1; a < nis; ++a) {
           float w[16];
@@ -666,8 +671,8 @@ __global__ void __launch_bounds__(512, 1)
       __syncwarp();
       if (unit_ok) {
         const int u = lane >> 2;
-        const int ul = quarter * 8 + u;       // unit within my 32-unit slice
-        const int c = cbase + (ul >> 3);      // 16-B chunk of the destination row
+        const int ul = (r >> 2);              // unit within my 64-unit slice
+        const int c = ul >> 3;                // 16-B chunk of the K-block row
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int col = 4 * q + gate;
@@ -680,9 +685,7 @@ __global__ void __launch_bounds__(512, 1)
           const __half hh = __float2half_rn(o * act_gate(cv, 2.f));
           cout[b * hp + unit] = cv;                   // R5
           hout[b * hp + unit] = hh;                   // R6
-          // staging in destination order: chunk c sits at slot (c ^ (bl & 7)) within my nq-chunk group
-          const int slot = (c ^ (bl & 7)) & (nq - 1);
-          *reinterpret_cast<__half*>(stg + bl * 64 + slot * 16 + (ul & 7) * 2) = hh;
+          *reinterpret_cast<__half*>(stg + bl * 128 + ((c ^ (bl & 7)) << 4) + (ul & 7) * 2) = hh;
           __align__(8) __half2 gg[2] = {__halves2half2(__float2half_rn(i), __float2half_rn(f)),
                                         __halves2half2(__float2half_rn(g), __float2half_rn(o))};
           *reinterpret_cast<uint2*>(gout + b * fourhp + 4 * unit) = *reinterpret_cast<const uint2*>(gg);  // R4
@@ -693,15 +696,12 @@ __global__ void __launch_bounds__(512, 1)
     ptx::tc_fence_before();
     ptx::fence_async_smem();  // staging writes (generic) -> bulk copy reads (async proxy)
     __syncthreads();
-    // push h_t (consumed at step t+1) into every peer's sH[t & 1]: one copy per (row, peer)
-    if (t < T - 1 && nq > 0) {
-      for (int idx = threadIdx.x; idx < Bc * G; idx += blockDim.x) {
-        const int bl = idx / G, dst = idx - bl * G;
-        const int gstart = (cbase ^ (bl & 7)) & ~(nq - 1);
-        const uint32_t dsta = ptx::mapa(sH_addr + (t & 1) * hbuf + kbx * Bc * 128 + bl * 128 + gstart * 16, dst);
-        const uint32_t mb = ptx::mapa(ptx::smem_u32(fullH + (t & 1)), dst);
-        ptx::bulk_copy_to_peer(dsta, sX_addr + (t & 1) * Bc * 64 + bl * 64, nq * 16, mb);
-      }
+    // push h_t (consumed at step t+1): my K-block rows into every peer's sH[t & 1], one copy per peer
+    if (t < T - 1 && threadIdx.x < G) {
+      const int dst = threadIdx.x;
+      const uint32_t dsta = ptx::mapa(sH_addr + (t & 1) * hbuf + rank * Bc * 128, dst);
+      const uint32_t mb = ptx::mapa(ptx::smem_u32(fullH + (t & 1)), dst);
+      ptx::bulk_copy_to_peer(dsta, sX_addr + (t & 1) * Bc * 128, Bc * 128, mb);
     }
   }
   ptx::cluster_arrive();  // nobody leaves while a peer may still read my staging / write my sH
@@ -712,7 +712,7 @@ __global__ void __launch_bounds__(512, 1)
 
 size_t fwd_cl_smem(int hp, int Bc, int nwarps) {
   const int nkb = (hp + 63) / 64;
-  return 1024 + (size_t)nkb * 16384 + 2 * (size_t)nkb * Bc * 128 + 2 * (size_t)Bc * 64 +
+  return 1024 + 2 * (size_t)nkb * 16384 + 2 * (size_t)nkb * Bc * 128 + 2 * (size_t)Bc * 128 +
          (size_t)nwarps * 16 * ACT_LD * 4 + 128;
 }
 
@@ -960,8 +960,9 @@ bool recur_fwd_supported(int B, int hp) {
 cudaError_t launch_recur_fwd(const RecurFwdArgs& a, cudaStream_t s) {
   FwdPlan p;
   if (!plan_fwd(a.B, a.hp, &p)) return cudaErrorInvalidConfiguration;
-  const int Gc = pow2ceil(p.G);
-  if (use_cluster() && Gc <= 8 && fwd_cl_smem(a.hp, p.Bc, 4 * p.cgN) <= 227 * 1024) {
+  const int Gc = (a.hp + 63) / 64;  // CTAs of 64 units = cluster size
+  const int nw = 8 * p.cgN;
+  if (use_cluster() && Gc <= 8 && nw <= 16 && fwd_cl_smem(a.hp, p.Bc, nw) <= 227 * 1024) {
     CUtensorMap mU;
     if (encode_tmap_2d(&mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U, a.hp, 4 * a.hp, a.hp * 2, 64, 128,
                        CU_TENSOR_MAP_SWIZZLE_128B))
@@ -974,7 +975,7 @@ cudaError_t launch_recur_fwd(const RecurFwdArgs& a, cudaStream_t s) {
     void* args[] = {&mU, &gx, &T, &B, &Bc, &hp, &hs, &cst, &gt};
     const void* fn = p.nci == 1 ? (const void*)recur_fwd_cl_kernel<1>
                    : p.nci == 2 ? (const void*)recur_fwd_cl_kernel<2> : (const void*)recur_fwd_cl_kernel<4>;
-    return launch_cluster(fn, dim3(Gc, p.nbg), dim3(128 * p.cgN), fwd_cl_smem(a.hp, p.Bc, 4 * p.cgN), Gc, s, args);
+    return launch_cluster(fn, dim3(Gc, p.nbg), dim3(32 * nw), fwd_cl_smem(a.hp, p.Bc, nw), Gc, s, args);
   }
   cudaError_t e = cudaMemsetAsync(a.counter, 0, (size_t)p.nbg * 32 * sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
