@@ -484,8 +484,34 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
       ra.T = T;
       ra.B = B;
       ra.hp = (int)hp;
-      KScope ks_(c, HDP_K_RECUR_FWD, 1, s);
-      CK_CUDA(hdp::launch_recur_fwd(ra, s));
+      static unsigned long long* ftrace = nullptr;  // debug: HDP_RECUR_TRACE=1 in profile (eager) mode
+      const bool want_trace = c->prof && getenv("HDP_RECUR_TRACE") && getenv("HDP_RECUR_TRACE")[0] == '1';
+      if (want_trace) {
+        if (!ftrace) CK_CUDA(cudaMalloc(&ftrace, 8192 * 5 * sizeof(unsigned long long)));
+        ra.trace = ftrace;
+      }
+      {
+        KScope ks_(c, HDP_K_RECUR_FWD, 1, s);
+        CK_CUDA(hdp::launch_recur_fwd(ra, s));
+      }
+      if (want_trace && T <= 8192) {
+        std::vector<unsigned long long> h((size_t)T * 5);
+        CK_CUDA(cudaStreamSynchronize(s));
+        CK_CUDA(cudaMemcpy(h.data(), ftrace, h.size() * 8, cudaMemcpyDeviceToHost));
+        double ph[4] = {0, 0, 0, 0}, step = 0;
+        int n = 0;
+        for (int t = 1; t < T - 1; ++t) {
+          const unsigned long long* r = &h[(size_t)t * 5];
+          ph[0] += (double)(r[1] - r[0]);
+          ph[1] += (double)(r[2] - r[1]);
+          ph[2] += (double)(r[3] - r[2]);
+          ph[3] += (double)(r[4] - r[3]);
+          step += (double)(h[(size_t)(t + 1) * 5] - r[0]);
+          ++n;
+        }
+        fprintf(stderr, "[hdp trace] recur_fwd layer %d: per step ns: wait %.0f mma %.0f epilogue %.0f push %.0f | step %.0f\n",
+                l, ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, step / n);
+      }
       continue;
     }
     for (int t = 0; t < T; ++t) {

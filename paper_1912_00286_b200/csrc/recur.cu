@@ -538,7 +538,9 @@ cudaError_t launch_bwd_t(const RecurBwdArgs& a, int nbg, cudaStream_t s) {
 template <int NCI>
 __global__ void __launch_bounds__(512, 1)
     recur_fwd_cl_kernel(const __grid_constant__ CUtensorMap tmU, const float* __restrict__ Gx, int T, int B, int Bc,
-                        int hp, __half* __restrict__ Hs, float* __restrict__ Cst, __half* __restrict__ gates) {
+                        int hp, __half* __restrict__ Hs, float* __restrict__ Cst, __half* __restrict__ gates,
+                        unsigned long long* __restrict__ trace) {
+  const bool tr = trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int nkb = (hp + 63) / 64;             // == cluster size
@@ -610,6 +612,7 @@ __global__ void __launch_bounds__(512, 1)
   uint32_t fphase[2] = {0u, 0u};
 
   for (int t = 0; t < T; ++t) {
+    if (tr) trace[t * 5 + 0] = ptx::globaltimer_ns();
     float gx[NCI][16];
 #pragma unroll
     for (int ci = 0; ci < NCI; ++ci) {
@@ -624,6 +627,7 @@ __global__ void __launch_bounds__(512, 1)
       if (lane == 0 && warp < nis) {
         ptx::mbar_wait(fullH + p, fphase[p]);  // every peer's h_{t-1} K-block landed in sH[p]
         ptx::tc_fence_after();
+        if (tr) trace[t * 5 + 1] = ptx::globaltimer_ns();
         const uint32_t aU = ptx::smem_u32(sU), aH = sH_addr + p * hbuf;
         const uint64_t ad0 = ptx::smem_desc_sw128(aU, 0, 1024), bd0 = ptx::smem_desc_sw128(aH, 0, 1024);
         for (int k = warp; k < nk16; k += nis) {
@@ -643,6 +647,7 @@ __global__ void __launch_bounds__(512, 1)
       fphase[p] ^= 1u;
       if (threadIdx.x == 0 && t + 2 <= T - 1) ptx::mbar_arrive_expect_tx(fullH + p, total_bytes);
     }
+    if (tr) trace[t * 5 + 2] = ptx::globaltimer_ns();
     __half* hout = Hs + (size_t)(t + 1) * B * hp;
     float* cout = Cst + (size_t)t * B * hp;
     __half* gout = gates + (size_t)t * B * fourhp;
@@ -696,6 +701,7 @@ __global__ void __launch_bounds__(512, 1)
     ptx::tc_fence_before();
     ptx::fence_async_smem();  // staging writes (generic) -> bulk copy reads (async proxy)
     __syncthreads();
+    if (tr) trace[t * 5 + 3] = ptx::globaltimer_ns();
     // push h_t (consumed at step t+1): my K-block rows into every peer's sH[t & 1], one copy per peer
     if (t < T - 1 && threadIdx.x < G) {
       const int dst = threadIdx.x;
@@ -703,6 +709,7 @@ __global__ void __launch_bounds__(512, 1)
       const uint32_t mb = ptx::mapa(ptx::smem_u32(fullH + (t & 1)), dst);
       ptx::bulk_copy_to_peer(dsta, sX_addr + (t & 1) * Bc * 128, Bc * 128, mb);
     }
+    if (tr) trace[t * 5 + 4] = ptx::globaltimer_ns();
   }
   ptx::cluster_arrive();  // nobody leaves while a peer may still read my staging / write my sH
   ptx::cluster_wait();
@@ -972,7 +979,8 @@ cudaError_t launch_recur_fwd(const RecurFwdArgs& a, cudaStream_t s) {
     __half* hs = a.Hs;
     float* cst = a.C;
     __half* gt = a.gates;
-    void* args[] = {&mU, &gx, &T, &B, &Bc, &hp, &hs, &cst, &gt};
+    unsigned long long* trace = a.trace;
+    void* args[] = {&mU, &gx, &T, &B, &Bc, &hp, &hs, &cst, &gt, &trace};
     const void* fn = p.nci == 1 ? (const void*)recur_fwd_cl_kernel<1>
                    : p.nci == 2 ? (const void*)recur_fwd_cl_kernel<2> : (const void*)recur_fwd_cl_kernel<4>;
     return launch_cluster(fn, dim3(Gc, p.nbg), dim3(32 * nw), fwd_cl_smem(a.hp, p.Bc, nw), Gc, s, args);

@@ -13,6 +13,7 @@ struct RecurFwdArgs {
   __half* gates = nullptr;    // [T][B][4hp] activated gates, fp16 (R4)
   unsigned* counter = nullptr;  // grid-barrier counters, 16 x 32 uints (zeroed by the launcher)
   int T = 0, B = 0, hp = 0;
+  unsigned long long* trace = nullptr;  // debug: per-step phase timestamps (T x 5), nullable
 };
 
 bool recur_fwd_supported(int B, int hp);
