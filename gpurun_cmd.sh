@@ -1,4 +1,4 @@
-timeout -s KILL 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/gpu_tests.log 2>&1; echo exit=$? >> gpurun_out/gpu_tests.log
-timeout -s KILL 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29511 bench.py --gpus 2 --steps 20 --warmup 5 > gpurun_out/bench_n2.json 2> gpurun_out/bench_n2.err
-timeout -s KILL 900 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29512 bench.py --gpus 2 --config C5 --steps 10 --warmup 3 > gpurun_out/c5_n2.json 2> gpurun_out/c5_n2.err
-tail -3 gpurun_out/gpu_tests.log
+timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py -q -p no:cacheprovider -x > gpurun_out/persist_tests.log 2>&1; echo exit=$? >> gpurun_out/persist_tests.log
+timeout -s KILL 300 python bench.py --steps 30 --warmup 5 --no-cpu-baseline > gpurun_out/bench28.json 2>> gpurun_out/bench28.err
+timeout -s KILL 300 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench28_c3.json 2>> gpurun_out/bench28.err
+tail -2 gpurun_out/persist_tests.log

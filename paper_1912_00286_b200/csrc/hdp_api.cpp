@@ -472,6 +472,27 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
     char* Gl = S.gates + l * g_layer * e;
     // K1: G_x = X W^T + b for all t (A1)
     CK(gemm(c, HDP_K_GEMM_X, X, Ipl, 0, c->W(iW), Ipl, 0, rows, 4 * hp, Ipl, epi_f32(c->Gx, 4 * hp, c->W(ib), !f32), s));
+    if (l == 0 && L == 2 && !f32 && c->persistent && hdp::recur2_fwd_supported(B, (int)hp)) {
+      // both layers' recurrences as one wavefront; layer 1's input projection runs inside
+      hdp::Recur2FwdArgs ra;
+      ra.U0 = (const __half*)c->W(iU);
+      ra.W1 = (const __half*)c->W(c->find("W1"));
+      ra.U1 = (const __half*)c->W(c->find("U1"));
+      ra.b1 = (const __half*)c->W(c->find("b1"));
+      ra.Gx0 = c->Gx;
+      ra.Hs0 = (__half*)Hs;
+      ra.C0 = Cl;
+      ra.gates0 = (__half*)Gl;
+      ra.Hs1 = (__half*)(S.Hs + hs_layer * e);
+      ra.C1 = S.C + c_layer;
+      ra.gates1 = (__half*)(S.gates + g_layer * e);
+      ra.T = T;
+      ra.B = B;
+      ra.hp = (int)hp;
+      KScope ks_(c, HDP_K_RECUR_FWD, 1, s);
+      CK_CUDA(hdp::launch_recur2_fwd(ra, s));
+      break;
+    }
     if (!f32 && c->persistent && hdp::recur_fwd_supported(B, (int)hp)) {
       // A2 + A3 for all t in one persistent kernel (U resident in SMEM)
       hdp::RecurFwdArgs ra;

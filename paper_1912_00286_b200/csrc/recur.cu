@@ -957,6 +957,281 @@ int pow2ceil(int v) {
   return p;
 }
 
+
+// ============================================================== 2-layer wavefront (forward)
+// One cluster of 3G CTAs per batch group of 16 columns (G = ceil(hp/64)):
+//   role 0 (R0_k): layer-0 recurrence, units [64k, 64k+64)
+//   role 1 (P_k) : layer-1 input projection a1x_t = W1 h0_t + b1, gate rows [256k, 256k+256)
+//   role 2 (R1_k): layer-1 recurrence, units [64k, 64k+64), a1x from P_k
+// Layer 1 runs one step behind layer 0, so the two layers' T-step chains
+// overlap (critical path ~T+2 steps instead of 2T).  Hand-offs:
+//   R0_k --h0_t (its K-block)--> all R0 peers (sH) and all P (sIn)   [bulk copy + fullH / fullIn]
+//   P_k  --a1x_t (256 x 16 fp32)--> R1_k (sGx)                        [bulk copy + fullGx]
+//   R1_k --h1_t (its K-block)--> all R1 peers (sH)                     [bulk copy + fullH]
+// Back-pressure (double buffers): P acks R0's emptyIn after its MMA read sIn;
+// R1 acks P's emptyOut after its epilogue read sGx (remote mbarrier arrives).
+constexpr int W2_BC = 16;
+
+__global__ void __launch_bounds__(256, 1)
+    recur2_fwd_kernel(const __grid_constant__ CUtensorMap tmU0, const __grid_constant__ CUtensorMap tmW1,
+                      const __grid_constant__ CUtensorMap tmU1, const float* __restrict__ Gx0,
+                      const __half* __restrict__ b1, int T, int B, int hp, __half* __restrict__ Hs0,
+                      float* __restrict__ C0, __half* __restrict__ gates0, __half* __restrict__ Hs1,
+                      float* __restrict__ C1, __half* __restrict__ gates1) {
+  constexpr int Bc = W2_BC;
+  constexpr int NACC = 4;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int nkb = (hp + 63) / 64;
+  const int nk16 = (hp + 15) / 16;
+  const int G = nkb;
+  const int hbuf = nkb * Bc * 128;
+  uint8_t* sA = smem;                          // [2 halves][nkb][16 KB] resident A slice (U0 / W1 / U1)
+  uint8_t* sB = sA + 2 * nkb * 16384;          // [2][hbuf] B operand (h of the previous / same step)
+  uint8_t* sX = sB + 2 * hbuf;                 // [2][Bc][128 B] staging of my h_t K-block
+  float* sAct = reinterpret_cast<float*>(sX + 2 * Bc * 128);   // [8 warps][16][ACT_LD]
+  float* sG = sAct + 8 * 16 * ACT_LD;          // [2][Bc][256] fp32: P out staging / R1 a1x input
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sG + 2 * Bc * 256);
+  uint64_t* barU = bars;
+  uint64_t* barM = bars + 1;
+  uint64_t* fullB = bars + 2;                  // [2] B operand delivered
+  uint64_t* fullG = bars + 4;                  // [2] R1: a1x delivered
+  uint64_t* emptyA = bars + 6;                 // [2] R0: P consumed my slice (count G) / P: R1 consumed (count 1)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int quarter = warp & 3, hf = warp >> 2;
+  const int rank = blockIdx.x;
+  const int role = rank / G, k = rank % G;
+  const int col0 = blockIdx.y * Bc;
+  const int r = hf * 128 + quarter * 32 + lane;
+  const int grow = k * 256 + r;
+  const int gate = r & 3;
+  const int unit = grow >> 2;
+  const bool unit_ok = unit < hp;
+  const int fourhp = 4 * hp;
+  const int nis = min(NACC, nk16);
+  const int total_bytes = nkb * Bc * 128;
+  const CUtensorMap* tmA = role == 0 ? &tmU0 : role == 1 ? &tmW1 : &tmU1;
+
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch(tmA);
+    ptx::mbar_init(barU, 1);
+    ptx::mbar_init(barM, nis);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(fullB + i, 1);
+      ptx::mbar_init(fullG + i, 1);
+      ptx::mbar_init(emptyA + i, role == 0 ? G : 1);
+    }
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tslot, 128);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  if (threadIdx.x == 0) {
+    // arm first uses; load the resident A slice
+    ptx::mbar_arrive_expect_tx(fullB, total_bytes);
+    ptx::mbar_arrive_expect_tx(fullB + 1, total_bytes);
+    if (role == 2) {
+      ptx::mbar_arrive_expect_tx(fullG, Bc * 256 * 4);
+      ptx::mbar_arrive_expect_tx(fullG + 1, Bc * 256 * 4);
+    }
+    ptx::mbar_arrive_expect_tx(barU, 2 * nkb * 16384);
+    for (int h2 = 0; h2 < 2; ++h2)
+      for (int kb = 0; kb < nkb; ++kb)
+        ptx::tma_load_2d(sA + (h2 * nkb + kb) * 16384, tmA, barU, kb * 64, k * 256 + h2 * 128);
+    ptx::mbar_wait(barU, 0);
+  }
+  ptx::cluster_arrive();
+  ptx::cluster_wait();
+
+  const uint32_t idesc = ptx::idesc_f16_f32(128, Bc, 0, 0);
+  float* myAct = sAct + warp * 16 * ACT_LD;
+  const float gsc = gate == 2 ? 2.f : 1.f;
+  const uint32_t sB_addr = ptx::smem_u32(sB), sX_addr = ptx::smem_u32(sX), sG_addr = ptx::smem_u32(sG);
+  uint32_t fph[2] = {0u, 0u}, gph[2] = {0u, 0u}, eph[2] = {0u, 0u};
+  uint32_t mph = 0;
+  float creg[4] = {0.f, 0.f, 0.f, 0.f};
+
+  // MMA over the resident A slice (two M=128 halves) and B operand slot p
+  auto issue_mma = [&](int p) {
+    const uint32_t aA = ptx::smem_u32(sA), aB = sB_addr + p * hbuf;
+    const uint64_t ad0 = ptx::smem_desc_sw128(aA, 0, 1024), bd0 = ptx::smem_desc_sw128(aB, 0, 1024);
+    for (int kk = warp; kk < nk16; kk += nis) {
+      const int kb = kk >> 2, kq = kk & 3;
+      const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kq * 32) >> 4);
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const uint64_t ad = ad0 + (uint64_t)(((h2 * nkb + kb) * 16384 + kq * 32) >> 4);
+        ptx::mma_f16(tbase + (h2 * NACC + warp) * Bc, ad, bd, idesc, kk >= nis ? 1u : 0u);
+      }
+    }
+    ptx::mma_commit(barM);
+  };
+  auto load_acc = [&](float (&v)[16]) {
+    const uint32_t ta = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + hf * NACC * Bc;
+    ptx::tmem_ld16(ta, v);
+    for (int a = 1; a < nis; ++a) {
+      float w[16];
+      ptx::tmem_ld16(ta + a * Bc, w);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] += w[q];
+    }
+  };
+
+  if (role == 1) {
+    // ---------------------------------------------------------------- projection P_k
+    float bias = unit_ok ? __half2float(b1[grow]) : 0.f;
+    for (int t = 0; t < T; ++t) {
+      const int p = t & 1;
+      if (lane == 0 && warp < nis) {
+        ptx::mbar_wait(fullB + p, fph[p]);  // h0_t from every R0
+        ptx::tc_fence_after();
+        issue_mma(p);
+      }
+      __syncwarp();
+      ptx::mbar_wait(barM, mph);
+      mph ^= 1u;
+      ptx::tc_fence_after();
+      fph[p] ^= 1u;
+      if (threadIdx.x == 0) {
+        if (t + 2 <= T - 1) ptx::mbar_arrive_expect_tx(fullB + p, total_bytes);
+        // sIn[p] consumed: ack every R0 (they may overwrite it / their staging)
+        for (int j = 0; j < G; ++j) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(emptyA + p), j));
+      }
+      // out staging slot p free? (R1 read it at step t-2)
+      if (t >= 2) {
+        ptx::mbar_wait_cluster(emptyA + p, eph[p]);
+        eph[p] ^= 1u;
+      }
+      float v[16];
+      load_acc(v);
+      float* out = sG + p * Bc * 256;
+#pragma unroll
+      for (int q = 0; q < 16; ++q) out[q * 256 + r] = v[q] + bias;
+      ptx::tc_fence_before();
+      ptx::fence_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        const int dst = 2 * G + k;  // R1_k
+        ptx::bulk_copy_to_peer(ptx::mapa(sG_addr + p * Bc * 256 * 4, dst), sG_addr + p * Bc * 256 * 4, Bc * 256 * 4,
+                               ptx::mapa(ptx::smem_u32(fullG + p), dst));
+      }
+    }
+  } else {
+    // ---------------------------------------------------------------- recurrence R0_k / R1_k
+    const bool L1 = role == 2;
+    __half* Hs = L1 ? Hs1 : Hs0;
+    float* Cst = L1 ? C1 : C0;
+    __half* gts = L1 ? gates1 : gates0;
+    const int peer0 = role * G;  // first CTA of my layer
+    for (int t = 0; t < T; ++t) {
+      const int p = t & 1;
+      float gx[16];
+      if (!L1) {
+        const float* gp = Gx0 + ((size_t)t * B + col0) * fourhp + grow;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) gx[q] = unit_ok ? __ldg(gp + (size_t)q * fourhp) : 0.f;
+      }
+      if (t > 0) {
+        const int pp = (t - 1) & 1;
+        if (lane == 0 && warp < nis) {
+          ptx::mbar_wait(fullB + pp, fph[pp]);  // h_{t-1} of my layer from every peer
+          ptx::tc_fence_after();
+          issue_mma(pp);
+        }
+        __syncwarp();
+        ptx::mbar_wait(barM, mph);
+        mph ^= 1u;
+        ptx::tc_fence_after();
+        fph[pp] ^= 1u;
+        if (threadIdx.x == 0 && t + 2 <= T - 1) ptx::mbar_arrive_expect_tx(fullB + pp, total_bytes);
+      }
+      if (L1) {
+        ptx::mbar_wait(fullG + p, gph[p]);  // a1x_t from P_k
+        gph[p] ^= 1u;
+        const float* gsrc = sG + p * Bc * 256;
+#pragma unroll
+        for (int q = 0; q < 16; ++q) gx[q] = gsrc[q * 256 + r];
+      } else if (t >= 2) {
+        // my staging slot p and P's sIn slot p are free once every P consumed step t-2
+        ptx::mbar_wait_cluster(emptyA + p, eph[p]);
+        eph[p] ^= 1u;
+      }
+      float v[16];
+      if (t > 0) {
+        load_acc(v);
+      } else {
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] = 0.f;
+      }
+#pragma unroll
+      for (int q = 0; q < 16; ++q) myAct[q * ACT_LD + lane] = act_gate(v[q] + gx[q], gsc);
+      __syncwarp();
+      __half* hout = Hs + (size_t)(t + 1) * B * hp;
+      float* cout = Cst + (size_t)t * B * hp;
+      __half* gout = gts + (size_t)t * B * fourhp;
+      uint8_t* stg = sX + p * Bc * 128;
+      if (unit_ok) {
+        const int u = lane >> 2;
+        const int ul = r >> 2;
+        const int c = ul >> 3;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const int col = 4 * q + gate;
+          const float4 a4 = *reinterpret_cast<const float4*>(myAct + col * ACT_LD + 4 * u);
+          const int bl = col;
+          const size_t b = (size_t)col0 + bl;
+          const float i = a4.x, f = a4.y, g = a4.z, o = a4.w;
+          const float cv = f * creg[q] + i * g;
+          creg[q] = cv;
+          const __half hh = __float2half_rn(o * act_gate(cv, 2.f));
+          cout[b * hp + unit] = cv;                   // R5
+          hout[b * hp + unit] = hh;                   // R6
+          *reinterpret_cast<__half*>(stg + bl * 128 + ((c ^ (bl & 7)) << 4) + (ul & 7) * 2) = hh;
+          __align__(8) __half2 gg[2] = {__halves2half2(__float2half_rn(i), __float2half_rn(f)),
+                                        __halves2half2(__float2half_rn(g), __float2half_rn(o))};
+          *reinterpret_cast<uint2*>(gout + b * fourhp + 4 * unit) = *reinterpret_cast<const uint2*>(gg);  // R4
+        }
+      }
+      __syncwarp();
+      ptx::tc_fence_before();
+      ptx::fence_async_smem();
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        if (L1) {
+          // a1x slot p read: ack P_k, re-arm for step t+2
+          ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(emptyA + p), G + k));
+          if (t + 2 <= T - 1) ptx::mbar_arrive_expect_tx(fullG + p, Bc * 256 * 4);
+        }
+      }
+      // push h_t: my K-block to my layer's peers (consumed at t+1), and h0_t to every P (consumed at t)
+      if (threadIdx.x < G) {
+        const int dst = peer0 + threadIdx.x;
+        if (t < T - 1)
+          ptx::bulk_copy_to_peer(ptx::mapa(sB_addr + p * hbuf + k * Bc * 128, dst), sX_addr + p * Bc * 128,
+                                 Bc * 128, ptx::mapa(ptx::smem_u32(fullB + p), dst));
+      } else if (!L1 && threadIdx.x >= 32 && threadIdx.x < 32 + G) {
+        const int dst = G + (threadIdx.x - 32);
+        ptx::bulk_copy_to_peer(ptx::mapa(sB_addr + p * hbuf + k * Bc * 128, dst), sX_addr + p * Bc * 128, Bc * 128,
+                               ptx::mapa(ptx::smem_u32(fullB + p), dst));
+      }
+    }
+  }
+  ptx::cluster_arrive();
+  ptx::cluster_wait();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc(tbase, 128);
+}
+
+size_t recur2_fwd_smem(int hp) {
+  const int nkb = (hp + 63) / 64;
+  return 1024 + 2 * (size_t)nkb * 16384 + 2 * (size_t)nkb * W2_BC * 128 + 2 * (size_t)W2_BC * 128 +
+         (size_t)8 * 16 * ACT_LD * 4 + 2 * (size_t)W2_BC * 256 * 4 + 128;
+}
+
 }  // namespace
 
 bool recur_fwd_supported(int B, int hp) {
@@ -1030,6 +1305,48 @@ cudaError_t launch_recur_bwd(const RecurBwdArgs& a, cudaStream_t s) {
     case 3: return launch_bwd_t<3>(a, nbg, s);
     default: return launch_bwd_t<4>(a, nbg, s);
   }
+}
+
+}  // namespace hdp
+
+namespace hdp {
+
+bool recur2_fwd_supported(int B, int hp) {
+  const char* e = getenv("HDP_WAVEFRONT");
+  if (e && e[0] == '0') return false;
+  if (B % W2_BC || (hp & 15) || hp > 256) return false;
+  if (3 * ((hp + 63) / 64) > 16) return false;
+  if ((size_t)((hp + 63) / 64) * 3 * (B / W2_BC) > 148) return false;
+  return recur2_fwd_smem(hp) <= 227 * 1024;
+}
+
+cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
+  if (!recur2_fwd_supported(a.B, a.hp)) return cudaErrorInvalidConfiguration;
+  CUtensorMap mU0, mW1, mU1;
+  const uint64_t hp = a.hp;
+  if (encode_tmap_2d(&mU0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U0, hp, 4 * hp, hp * 2, 64, 128,
+                     CU_TENSOR_MAP_SWIZZLE_128B) ||
+      encode_tmap_2d(&mW1, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.W1, hp, 4 * hp, hp * 2, 64, 128,
+                     CU_TENSOR_MAP_SWIZZLE_128B) ||
+      encode_tmap_2d(&mU1, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U1, hp, 4 * hp, hp * 2, 64, 128,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  const int G = (a.hp + 63) / 64;
+  const size_t smem = recur2_fwd_smem(a.hp);
+  const void* fn = (const void*)recur2_fwd_kernel;
+  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (e != cudaSuccess) return e;
+  if (3 * G > 8) {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+    if (e != cudaSuccess) return e;
+  }
+  const float* gx = a.Gx0;
+  const __half* b1 = a.b1;
+  int T = a.T, B = a.B, hpi = a.hp;
+  __half *hs0 = a.Hs0, *g0 = a.gates0, *hs1 = a.Hs1, *g1 = a.gates1;
+  float *c0 = a.C0, *c1 = a.C1;
+  void* args[] = {&mU0, &mW1, &mU1, &gx, &b1, &T, &B, &hpi, &hs0, &c0, &g0, &hs1, &c1, &g1};
+  return launch_cluster(fn, dim3(3 * G, a.B / W2_BC), dim3(256), smem, 3 * G, s, args);
 }
 
 }  // namespace hdp

@@ -31,6 +31,19 @@ struct RecurBwdArgs {
   unsigned long long* trace = nullptr;  // debug: per-step phase timestamps (T x 5), nullable
 };
 bool recur_bwd_supported(int B, int hp);
+
+// Two stacked layers' forward recurrences as one wavefront (layer 1 one step
+// behind layer 0); layer 1's input projection W1 h0_t + b1 is computed inside.
+struct Recur2FwdArgs {
+  const __half *U0 = nullptr, *W1 = nullptr, *U1 = nullptr, *b1 = nullptr;  // [4hp][hp], b1 [4hp]
+  const float* Gx0 = nullptr;                 // [T][B][4hp] = X W0^T + b0
+  __half *Hs0 = nullptr, *Hs1 = nullptr;      // [T+1][B][hp], slot 0 = 0
+  float *C0 = nullptr, *C1 = nullptr;         // [T][B][hp]
+  __half *gates0 = nullptr, *gates1 = nullptr;
+  int T = 0, B = 0, hp = 0;
+};
+bool recur2_fwd_supported(int B, int hp);
+cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s);
 cudaError_t launch_recur_bwd(const RecurBwdArgs& a, cudaStream_t s);
 
 }  // namespace hdp
