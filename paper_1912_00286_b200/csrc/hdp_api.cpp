@@ -489,8 +489,37 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
       ra.T = T;
       ra.B = B;
       ra.hp = (int)hp;
-      KScope ks_(c, HDP_K_RECUR_FWD, 1, s);
-      CK_CUDA(hdp::launch_recur2_fwd(ra, s));
+      static unsigned long long* w2trace = nullptr;  // debug: HDP_RECUR_TRACE=1 in profile (eager) mode
+      const bool want_trace = c->prof && getenv("HDP_RECUR_TRACE") && getenv("HDP_RECUR_TRACE")[0] == '1';
+      if (want_trace) {
+        if (!w2trace) CK_CUDA(cudaMalloc(&w2trace, 3 * 8192 * 5 * sizeof(unsigned long long)));
+        ra.trace = w2trace;
+      }
+      {
+        KScope ks_(c, HDP_K_RECUR_FWD, 1, s);
+        CK_CUDA(hdp::launch_recur2_fwd(ra, s));
+      }
+      if (want_trace && T <= 8192) {
+        std::vector<unsigned long long> h((size_t)3 * T * 5);
+        CK_CUDA(cudaStreamSynchronize(s));
+        CK_CUDA(cudaMemcpy(h.data(), w2trace, h.size() * 8, cudaMemcpyDeviceToHost));
+        const unsigned long long t00 = h[0];
+        const char* names[3] = {"R0", "P", "R1"};
+        for (int role = 0; role < 3; ++role) {
+          double ph[4] = {0, 0, 0, 0}, step = 0;
+          int n = 0;
+          for (int t = 2; t < T - 1; ++t) {
+            const unsigned long long* r = &h[((size_t)role * T + t) * 5];
+            for (int q = 0; q < 4; ++q) ph[q] += (double)(r[q + 1] - r[q]);
+            step += (double)(h[((size_t)role * T + t + 1) * 5] - r[0]);
+            ++n;
+          }
+          const unsigned long long* st = &h[((size_t)role * T + 1) * 5];
+          fprintf(stderr, "[hdp trace] wavefront %s: per step ns: %.0f %.0f %.0f %.0f | step %.0f | t=1 starts at +%.0f ns, t=T-1 ends at +%.0f\n",
+                  names[role], ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, step / n, (double)(st[0] - t00),
+                  (double)(h[((size_t)role * T + T - 1) * 5 + 4] - t00));
+        }
+      }
       break;
     }
     if (!f32 && c->persistent && hdp::recur_fwd_supported(B, (int)hp)) {

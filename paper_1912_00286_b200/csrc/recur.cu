@@ -977,7 +977,7 @@ __global__ void __launch_bounds__(256, 1)
                       const __grid_constant__ CUtensorMap tmU1, const float* __restrict__ Gx0,
                       const __half* __restrict__ b1, int T, int B, int hp, __half* __restrict__ Hs0,
                       float* __restrict__ C0, __half* __restrict__ gates0, __half* __restrict__ Hs1,
-                      float* __restrict__ C1, __half* __restrict__ gates1) {
+                      float* __restrict__ C1, __half* __restrict__ gates1, unsigned long long* __restrict__ trace) {
   constexpr int Bc = W2_BC;
   constexpr int NACC = 4;
   extern __shared__ uint8_t smem_raw[];
@@ -1013,6 +1013,11 @@ __global__ void __launch_bounds__(256, 1)
   const int nis = min(NACC, nk16);
   const int total_bytes = nkb * Bc * 128;
   const CUtensorMap* tmA = role == 0 ? &tmU0 : role == 1 ? &tmW1 : &tmU1;
+  // debug trace: CTA k == 0 of each role, batch group 0, thread 0: [role][t][5]
+  const bool tr = trace != nullptr && k == 0 && blockIdx.y == 0 && threadIdx.x == 0;
+  unsigned long long* trr = trace ? trace + (size_t)role * T * 5 : nullptr;
+#define TR(t, i) \
+  if (tr) trr[(t) * 5 + (i)] = ptx::globaltimer_ns()
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch(tmA);
@@ -1086,8 +1091,10 @@ __global__ void __launch_bounds__(256, 1)
     float bias = unit_ok ? __half2float(b1[grow]) : 0.f;
     for (int t = 0; t < T; ++t) {
       const int p = t & 1;
+      TR(t, 0);
       if (lane == 0 && warp < nis) {
         ptx::mbar_wait(fullB + p, fph[p]);  // h0_t from every R0
+        TR(t, 1);
         ptx::tc_fence_after();
         issue_mma(p);
       }
@@ -1101,11 +1108,13 @@ __global__ void __launch_bounds__(256, 1)
         // sIn[p] consumed: ack every R0 (they may overwrite it / their staging)
         for (int j = 0; j < G; ++j) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(emptyA + p), j));
       }
+      TR(t, 2);
       // out staging slot p free? (R1 read it at step t-2)
       if (t >= 2) {
         ptx::mbar_wait_cluster(emptyA + p, eph[p]);
         eph[p] ^= 1u;
       }
+      TR(t, 3);
       float v[16];
       load_acc(v);
       float* out = sG + p * Bc * 256;
@@ -1119,6 +1128,7 @@ __global__ void __launch_bounds__(256, 1)
         ptx::bulk_copy_to_peer(ptx::mapa(sG_addr + p * Bc * 256 * 4, dst), sG_addr + p * Bc * 256 * 4, Bc * 256 * 4,
                                ptx::mapa(ptx::smem_u32(fullG + p), dst));
       }
+      TR(t, 4);
     }
   } else {
     // ---------------------------------------------------------------- recurrence R0_k / R1_k
@@ -1129,6 +1139,7 @@ __global__ void __launch_bounds__(256, 1)
     const int peer0 = role * G;  // first CTA of my layer
     for (int t = 0; t < T; ++t) {
       const int p = t & 1;
+      TR(t, 0);
       float gx[16];
       if (!L1) {
         const float* gp = Gx0 + ((size_t)t * B + col0) * fourhp + grow;
@@ -1139,6 +1150,7 @@ __global__ void __launch_bounds__(256, 1)
         const int pp = (t - 1) & 1;
         if (lane == 0 && warp < nis) {
           ptx::mbar_wait(fullB + pp, fph[pp]);  // h_{t-1} of my layer from every peer
+          TR(t, 1);
           ptx::tc_fence_after();
           issue_mma(pp);
         }
@@ -1149,6 +1161,7 @@ __global__ void __launch_bounds__(256, 1)
         fph[pp] ^= 1u;
         if (threadIdx.x == 0 && t + 2 <= T - 1) ptx::mbar_arrive_expect_tx(fullB + pp, total_bytes);
       }
+      TR(t, 2);
       if (L1) {
         ptx::mbar_wait(fullG + p, gph[p]);  // a1x_t from P_k
         gph[p] ^= 1u;
@@ -1160,6 +1173,7 @@ __global__ void __launch_bounds__(256, 1)
         ptx::mbar_wait_cluster(emptyA + p, eph[p]);
         eph[p] ^= 1u;
       }
+      TR(t, 3);
       float v[16];
       if (t > 0) {
         load_acc(v);
@@ -1218,8 +1232,10 @@ __global__ void __launch_bounds__(256, 1)
         ptx::bulk_copy_to_peer(ptx::mapa(sB_addr + p * hbuf + k * Bc * 128, dst), sX_addr + p * Bc * 128, Bc * 128,
                                ptx::mapa(ptx::smem_u32(fullB + p), dst));
       }
+      TR(t, 4);
     }
   }
+#undef TR
   ptx::cluster_arrive();
   ptx::cluster_wait();
   ptx::tc_fence_after();
@@ -1345,7 +1361,8 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
   int T = a.T, B = a.B, hpi = a.hp;
   __half *hs0 = a.Hs0, *g0 = a.gates0, *hs1 = a.Hs1, *g1 = a.gates1;
   float *c0 = a.C0, *c1 = a.C1;
-  void* args[] = {&mU0, &mW1, &mU1, &gx, &b1, &T, &B, &hpi, &hs0, &c0, &g0, &hs1, &c1, &g1};
+  unsigned long long* trace = a.trace;
+  void* args[] = {&mU0, &mW1, &mU1, &gx, &b1, &T, &B, &hpi, &hs0, &c0, &g0, &hs1, &c1, &g1, &trace};
   return launch_cluster(fn, dim3(3 * G, a.B / W2_BC), dim3(256), smem, 3 * G, s, args);
 }
 

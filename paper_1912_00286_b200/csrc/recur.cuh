@@ -41,6 +41,7 @@ struct Recur2FwdArgs {
   float *C0 = nullptr, *C1 = nullptr;         // [T][B][hp]
   __half *gates0 = nullptr, *gates1 = nullptr;
   int T = 0, B = 0, hp = 0;
+  unsigned long long* trace = nullptr;  // debug: [3 roles][T][5] timestamps, nullable
 };
 bool recur2_fwd_supported(int B, int hp);
 cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s);
