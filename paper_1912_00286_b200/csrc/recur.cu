@@ -22,6 +22,7 @@
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
+#include <cstdio>
 #include <cstdlib>
 
 #include "gemm.cuh"
@@ -970,15 +971,15 @@ int pow2ceil(int v) {
 //   R1_k --h1_t (its K-block)--> all R1 peers (sH)                     [bulk copy + fullH]
 // Back-pressure (double buffers): P acks R0's emptyIn after its MMA read sIn;
 // R1 acks P's emptyOut after its epilogue read sGx (remote mbarrier arrives).
-constexpr int W2_BC = 16;
-
+template <int BC>
 __global__ void __launch_bounds__(256, 1)
     recur2_fwd_kernel(const __grid_constant__ CUtensorMap tmU0, const __grid_constant__ CUtensorMap tmW1,
                       const __grid_constant__ CUtensorMap tmU1, const float* __restrict__ Gx0,
                       const __half* __restrict__ b1, int T, int B, int hp, __half* __restrict__ Hs0,
                       float* __restrict__ C0, __half* __restrict__ gates0, __half* __restrict__ Hs1,
                       float* __restrict__ C1, __half* __restrict__ gates1, unsigned long long* __restrict__ trace) {
-  constexpr int Bc = W2_BC;
+  constexpr int Bc = BC;
+  constexpr int NC = BC / 16;  // 16-column chunks per CTA
   constexpr int NACC = 4;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -990,13 +991,13 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sB = sA + 2 * nkb * 16384;          // [2][hbuf] B operand (h of the previous / same step)
   uint8_t* sX = sB + 2 * hbuf;                 // [2][Bc][128 B] staging of my h_t K-block
   float* sAct = reinterpret_cast<float*>(sX + 2 * Bc * 128);   // [8 warps][16][ACT_LD]
-  float* sG = sAct + 8 * 16 * ACT_LD;          // [2][Bc][256] fp32: P out staging / R1 a1x input
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sG + 2 * Bc * 256);
+  float* sG = sAct + 8 * 16 * ACT_LD;          // [Bc][256] fp32: P out staging / R1 a1x input (single buffer)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sG + Bc * 256);
   uint64_t* barU = bars;
   uint64_t* barM = bars + 1;
   uint64_t* fullB = bars + 2;                  // [2] B operand delivered
-  uint64_t* fullG = bars + 4;                  // [2] R1: a1x delivered
-  uint64_t* emptyA = bars + 6;                 // [2] R0: P consumed my slice (count G) / P: R1 consumed (count 1)
+  uint64_t* fullG = bars + 4;                  // R1: a1x delivered (single slot)
+  uint64_t* emptyA = bars + 6;                 // [2] R0: P consumed my slice (count G); P: [0] R1 consumed a1x (count 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -1030,7 +1031,8 @@ __global__ void __launch_bounds__(256, 1)
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tslot, 128);
+  constexpr uint32_t TCOLS = 2 * NACC * Bc <= 128 ? 128 : 256;
+  if (warp == 2) ptx::tmem_alloc(tslot, TCOLS);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
@@ -1039,10 +1041,7 @@ __global__ void __launch_bounds__(256, 1)
     // arm first uses; load the resident A slice
     ptx::mbar_arrive_expect_tx(fullB, total_bytes);
     ptx::mbar_arrive_expect_tx(fullB + 1, total_bytes);
-    if (role == 2) {
-      ptx::mbar_arrive_expect_tx(fullG, Bc * 256 * 4);
-      ptx::mbar_arrive_expect_tx(fullG + 1, Bc * 256 * 4);
-    }
+    if (role == 2) ptx::mbar_arrive_expect_tx(fullG, Bc * 256 * 4);
     ptx::mbar_arrive_expect_tx(barU, 2 * nkb * 16384);
     for (int h2 = 0; h2 < 2; ++h2)
       for (int kb = 0; kb < nkb; ++kb)
@@ -1056,9 +1055,11 @@ __global__ void __launch_bounds__(256, 1)
   float* myAct = sAct + warp * 16 * ACT_LD;
   const float gsc = gate == 2 ? 2.f : 1.f;
   const uint32_t sB_addr = ptx::smem_u32(sB), sX_addr = ptx::smem_u32(sX), sG_addr = ptx::smem_u32(sG);
-  uint32_t fph[2] = {0u, 0u}, gph[2] = {0u, 0u}, eph[2] = {0u, 0u};
-  uint32_t mph = 0;
-  float creg[4] = {0.f, 0.f, 0.f, 0.f};
+  uint32_t fph[2] = {0u, 0u}, eph[2] = {0u, 0u};
+  uint32_t gph = 0, oph = 0, mph = 0;
+  float creg[NC * 4];
+#pragma unroll
+  for (int i = 0; i < NC * 4; ++i) creg[i] = 0.f;
 
   // MMA over the resident A slice (two M=128 halves) and B operand slot p
   auto issue_mma = [&](int p) {
@@ -1075,8 +1076,8 @@ __global__ void __launch_bounds__(256, 1)
     }
     ptx::mma_commit(barM);
   };
-  auto load_acc = [&](float (&v)[16]) {
-    const uint32_t ta = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + hf * NACC * Bc;
+  auto load_acc = [&](float (&v)[16], int c0) {
+    const uint32_t ta = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + hf * NACC * Bc + c0;
     ptx::tmem_ld16(ta, v);
     for (int a = 1; a < nis; ++a) {
       float w[16];
@@ -1109,24 +1110,25 @@ __global__ void __launch_bounds__(256, 1)
         for (int j = 0; j < G; ++j) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(emptyA + p), j));
       }
       TR(t, 2);
-      // out staging slot p free? (R1 read it at step t-2)
-      if (t >= 2) {
-        ptx::mbar_wait_cluster(emptyA + p, eph[p]);
-        eph[p] ^= 1u;
+      // out staging free? (R1 consumed a1x_{t-1}, so its copy from my staging completed too)
+      if (t >= 1) {
+        ptx::mbar_wait_cluster(emptyA, oph);
+        oph ^= 1u;
       }
       TR(t, 3);
-      float v[16];
-      load_acc(v);
-      float* out = sG + p * Bc * 256;
 #pragma unroll
-      for (int q = 0; q < 16; ++q) out[q * 256 + r] = v[q] + bias;
+      for (int ch = 0; ch < NC; ++ch) {
+        float v[16];
+        load_acc(v, ch * 16);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) sG[(ch * 16 + q) * 256 + r] = v[q] + bias;
+      }
       ptx::tc_fence_before();
       ptx::fence_async_smem();
       __syncthreads();
       if (threadIdx.x == 0) {
         const int dst = 2 * G + k;  // R1_k
-        ptx::bulk_copy_to_peer(ptx::mapa(sG_addr + p * Bc * 256 * 4, dst), sG_addr + p * Bc * 256 * 4, Bc * 256 * 4,
-                               ptx::mapa(ptx::smem_u32(fullG + p), dst));
+        ptx::bulk_copy_to_peer(ptx::mapa(sG_addr, dst), sG_addr, Bc * 256 * 4, ptx::mapa(ptx::smem_u32(fullG), dst));
       }
       TR(t, 4);
     }
@@ -1140,11 +1142,13 @@ __global__ void __launch_bounds__(256, 1)
     for (int t = 0; t < T; ++t) {
       const int p = t & 1;
       TR(t, 0);
-      float gx[16];
+      float gx[NC][16];
       if (!L1) {
         const float* gp = Gx0 + ((size_t)t * B + col0) * fourhp + grow;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) gx[q] = unit_ok ? __ldg(gp + (size_t)q * fourhp) : 0.f;
+        for (int ch = 0; ch < NC; ++ch)
+#pragma unroll
+          for (int q = 0; q < 16; ++q) gx[ch][q] = unit_ok ? __ldg(gp + (size_t)(ch * 16 + q) * fourhp) : 0.f;
       }
       if (t > 0) {
         const int pp = (t - 1) & 1;
@@ -1163,62 +1167,66 @@ __global__ void __launch_bounds__(256, 1)
       }
       TR(t, 2);
       if (L1) {
-        ptx::mbar_wait(fullG + p, gph[p]);  // a1x_t from P_k
-        gph[p] ^= 1u;
-        const float* gsrc = sG + p * Bc * 256;
+        ptx::mbar_wait(fullG, gph);  // a1x_t from P_k
+        gph ^= 1u;
 #pragma unroll
-        for (int q = 0; q < 16; ++q) gx[q] = gsrc[q * 256 + r];
+        for (int ch = 0; ch < NC; ++ch)
+#pragma unroll
+          for (int q = 0; q < 16; ++q) gx[ch][q] = sG[(ch * 16 + q) * 256 + r];
       } else if (t >= 2) {
         // my staging slot p and P's sIn slot p are free once every P consumed step t-2
         ptx::mbar_wait_cluster(emptyA + p, eph[p]);
         eph[p] ^= 1u;
       }
       TR(t, 3);
-      float v[16];
-      if (t > 0) {
-        load_acc(v);
-      } else {
-#pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] = 0.f;
-      }
-#pragma unroll
-      for (int q = 0; q < 16; ++q) myAct[q * ACT_LD + lane] = act_gate(v[q] + gx[q], gsc);
-      __syncwarp();
       __half* hout = Hs + (size_t)(t + 1) * B * hp;
       float* cout = Cst + (size_t)t * B * hp;
       __half* gout = gts + (size_t)t * B * fourhp;
       uint8_t* stg = sX + p * Bc * 128;
-      if (unit_ok) {
-        const int u = lane >> 2;
-        const int ul = r >> 2;
-        const int c = ul >> 3;
 #pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int col = 4 * q + gate;
-          const float4 a4 = *reinterpret_cast<const float4*>(myAct + col * ACT_LD + 4 * u);
-          const int bl = col;
-          const size_t b = (size_t)col0 + bl;
-          const float i = a4.x, f = a4.y, g = a4.z, o = a4.w;
-          const float cv = f * creg[q] + i * g;
-          creg[q] = cv;
-          const __half hh = __float2half_rn(o * act_gate(cv, 2.f));
-          cout[b * hp + unit] = cv;                   // R5
-          hout[b * hp + unit] = hh;                   // R6
-          *reinterpret_cast<__half*>(stg + bl * 128 + ((c ^ (bl & 7)) << 4) + (ul & 7) * 2) = hh;
-          __align__(8) __half2 gg[2] = {__halves2half2(__float2half_rn(i), __float2half_rn(f)),
-                                        __halves2half2(__float2half_rn(g), __float2half_rn(o))};
-          *reinterpret_cast<uint2*>(gout + b * fourhp + 4 * unit) = *reinterpret_cast<const uint2*>(gg);  // R4
+      for (int ch = 0; ch < NC; ++ch) {
+        float v[16];
+        if (t > 0) {
+          load_acc(v, ch * 16);
+        } else {
+#pragma unroll
+          for (int q = 0; q < 16; ++q) v[q] = 0.f;
         }
+#pragma unroll
+        for (int q = 0; q < 16; ++q) myAct[q * ACT_LD + lane] = act_gate(v[q] + gx[ch][q], gsc);
+        __syncwarp();
+        if (unit_ok) {
+          const int u = lane >> 2;
+          const int ul = r >> 2;
+          const int c = ul >> 3;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int col = 4 * q + gate;
+            const float4 a4 = *reinterpret_cast<const float4*>(myAct + col * ACT_LD + 4 * u);
+            const int bl = ch * 16 + col;
+            const size_t b = (size_t)col0 + bl;
+            const float i = a4.x, f = a4.y, g = a4.z, o = a4.w;
+            const float cv = f * creg[ch * 4 + q] + i * g;
+            creg[ch * 4 + q] = cv;
+            const __half hh = __float2half_rn(o * act_gate(cv, 2.f));
+            cout[b * hp + unit] = cv;                   // R5
+            hout[b * hp + unit] = hh;                   // R6
+            *reinterpret_cast<__half*>(stg + bl * 128 + ((c ^ (bl & 7)) << 4) + (ul & 7) * 2) = hh;
+            __align__(8) __half2 gg[2] = {__halves2half2(__float2half_rn(i), __float2half_rn(f)),
+                                          __halves2half2(__float2half_rn(g), __float2half_rn(o))};
+            *reinterpret_cast<uint2*>(gout + b * fourhp + 4 * unit) = *reinterpret_cast<const uint2*>(gg);  // R4
+          }
+        }
+        __syncwarp();
       }
-      __syncwarp();
       ptx::tc_fence_before();
       ptx::fence_async_smem();
       __syncthreads();
       if (threadIdx.x == 0) {
         if (L1) {
-          // a1x slot p read: ack P_k, re-arm for step t+2
-          ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(emptyA + p), G + k));
-          if (t + 2 <= T - 1) ptx::mbar_arrive_expect_tx(fullG + p, Bc * 256 * 4);
+          // a1x read: re-arm for step t+1, then ack P_k (its next copy may land only after the re-arm)
+          if (t + 1 <= T - 1) ptx::mbar_arrive_expect_tx(fullG, Bc * 256 * 4);
+          ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(emptyA), G + k));
         }
       }
       // push h_t: my K-block to my layer's peers (consumed at t+1), and h0_t to every P (consumed at t)
@@ -1239,13 +1247,13 @@ __global__ void __launch_bounds__(256, 1)
   ptx::cluster_arrive();
   ptx::cluster_wait();
   ptx::tc_fence_after();
-  if (warp == 2) ptx::tmem_dealloc(tbase, 128);
+  if (warp == 2) ptx::tmem_dealloc(tbase, TCOLS);
 }
 
-size_t recur2_fwd_smem(int hp) {
+size_t recur2_fwd_smem(int hp, int Bc) {
   const int nkb = (hp + 63) / 64;
-  return 1024 + 2 * (size_t)nkb * 16384 + 2 * (size_t)nkb * W2_BC * 128 + 2 * (size_t)W2_BC * 128 +
-         (size_t)8 * 16 * ACT_LD * 4 + 2 * (size_t)W2_BC * 256 * 4 + 128;
+  return 1024 + 2 * (size_t)nkb * 16384 + 2 * (size_t)nkb * Bc * 128 + 2 * (size_t)Bc * 128 +
+         (size_t)8 * 16 * ACT_LD * 4 + (size_t)Bc * 256 * 4 + 128;
 }
 
 }  // namespace
@@ -1330,10 +1338,11 @@ namespace hdp {
 bool recur2_fwd_supported(int B, int hp) {
   const char* e = getenv("HDP_WAVEFRONT");
   if (e && e[0] == '0') return false;
-  if (B % W2_BC || (hp & 15) || hp > 256) return false;
-  if (3 * ((hp + 63) / 64) > 16) return false;
-  if ((size_t)((hp + 63) / 64) * 3 * (B / W2_BC) > 148) return false;
-  return recur2_fwd_smem(hp) <= 227 * 1024;
+  if (B % 32 || (hp & 15) || hp > 256) return false;
+  const int G = (hp + 63) / 64;
+  if (3 * G > 16) return false;
+  if ((size_t)G * 3 * (B / 32) > 148) return false;
+  return recur2_fwd_smem(hp, 32) <= 227 * 1024;
 }
 
 cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
@@ -1348,13 +1357,35 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
                      CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
   const int G = (a.hp + 63) / 64;
-  const size_t smem = recur2_fwd_smem(a.hp);
-  const void* fn = (const void*)recur2_fwd_kernel;
-  cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  if (3 * G > 8) {
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+  // batch group width: 16 if all B/16 clusters can be co-resident, else 32
+  int Bc = 16;
+  if (const char* e = getenv("HDP_WAVEFRONT_BC")) Bc = atoi(e) == 32 ? 32 : 16;
+  const void* fn16 = (const void*)recur2_fwd_kernel<16>;
+  const void* fn32 = (const void*)recur2_fwd_kernel<32>;
+  for (const void* f : {fn16, fn32}) {
+    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         (int)recur2_fwd_smem(a.hp, f == fn16 ? 16 : 32));
     if (e != cudaSuccess) return e;
+    if (3 * G > 8) {
+      e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
+      if (e != cudaSuccess) return e;
+    }
+  }
+  if (!getenv("HDP_WAVEFRONT_BC")) {
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(3 * G, a.B / 16);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = recur2_fwd_smem(a.hp, 16);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = 3 * G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, fn16, &cfg) != cudaSuccess) nclusters = 0;
+    Bc = (nclusters >= a.B / 16) ? 16 : 32;
   }
   const float* gx = a.Gx0;
   const __half* b1 = a.b1;
@@ -1363,7 +1394,8 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
   float *c0 = a.C0, *c1 = a.C1;
   unsigned long long* trace = a.trace;
   void* args[] = {&mU0, &mW1, &mU1, &gx, &b1, &T, &B, &hpi, &hs0, &c0, &g0, &hs1, &c1, &g1, &trace};
-  return launch_cluster(fn, dim3(3 * G, a.B / W2_BC), dim3(256), smem, 3 * G, s, args);
+  return launch_cluster(Bc == 16 ? fn16 : fn32, dim3(3 * G, a.B / Bc), dim3(256), recur2_fwd_smem(a.hp, Bc), 3 * G, s,
+                        args);
 }
 
 }  // namespace hdp
