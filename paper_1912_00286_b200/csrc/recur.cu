@@ -972,14 +972,14 @@ int pow2ceil(int v) {
 // Back-pressure (double buffers): P acks R0's emptyIn after its MMA read sIn;
 // R1 acks P's emptyOut after its epilogue read sGx (remote mbarrier arrives).
 template <int BC>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(BC * 16, 1)
     recur2_fwd_kernel(const __grid_constant__ CUtensorMap tmU0, const __grid_constant__ CUtensorMap tmW1,
                       const __grid_constant__ CUtensorMap tmU1, const float* __restrict__ Gx0,
                       const __half* __restrict__ b1, int T, int B, int hp, __half* __restrict__ Hs0,
                       float* __restrict__ C0, __half* __restrict__ gates0, __half* __restrict__ Hs1,
                       float* __restrict__ C1, __half* __restrict__ gates1, unsigned long long* __restrict__ trace) {
   constexpr int Bc = BC;
-  constexpr int NC = BC / 16;  // 16-column chunks per CTA
+  constexpr int NC = 1;        // each warp handles one 16-column chunk: chunk = cg
   constexpr int NACC = 4;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -991,7 +991,7 @@ __global__ void __launch_bounds__(256, 1)
   uint8_t* sB = sA + 2 * nkb * 16384;          // [2][hbuf] B operand (h of the previous / same step)
   uint8_t* sX = sB + 2 * hbuf;                 // [2][Bc][128 B] staging of my h_t K-block
   float* sAct = reinterpret_cast<float*>(sX + 2 * Bc * 128);   // [8 warps][16][ACT_LD]
-  float* sG = sAct + 8 * 16 * ACT_LD;          // [Bc][256] fp32: P out staging / R1 a1x input (single buffer)
+  float* sG = sAct + (BC / 2) * 16 * ACT_LD;          // [Bc][256] fp32: P out staging / R1 a1x input (single buffer)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sG + Bc * 256);
   uint64_t* barU = bars;
   uint64_t* barM = bars + 1;
@@ -1001,10 +1001,10 @@ __global__ void __launch_bounds__(256, 1)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int quarter = warp & 3, hf = warp >> 2;
+  const int quarter = warp & 3, hf = (warp >> 2) & 1, cg = warp >> 3;  // BC/16 column groups
   const int rank = blockIdx.x;
   const int role = rank / G, k = rank % G;
-  const int col0 = blockIdx.y * Bc;
+  const int col0 = blockIdx.y * Bc + cg * 16;  // this warp's 16 batch columns
   const int r = hf * 128 + quarter * 32 + lane;
   const int grow = k * 256 + r;
   const int gate = r & 3;
@@ -1078,13 +1078,17 @@ __global__ void __launch_bounds__(256, 1)
   };
   auto load_acc = [&](float (&v)[16], int c0) {
     const uint32_t ta = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + hf * NACC * Bc + c0;
-    ptx::tmem_ld16(ta, v);
-    for (int a = 1; a < nis; ++a) {
-      float w[16];
-      ptx::tmem_ld16(ta + a * Bc, w);
+    float w[NACC - 1][16];
+    ptx::tmem_ld16_nowait(ta, v);
 #pragma unroll
-      for (int q = 0; q < 16; ++q) v[q] += w[q];
-    }
+    for (int a = 1; a < NACC; ++a)
+      if (a < nis) ptx::tmem_ld16_nowait(ta + a * Bc, w[a - 1]);
+    ptx::tmem_wait_ld();
+#pragma unroll
+    for (int a = 1; a < NACC; ++a)
+      if (a < nis)
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] += w[a - 1][q];
   };
 
   if (role == 1) {
@@ -1116,12 +1120,11 @@ __global__ void __launch_bounds__(256, 1)
         oph ^= 1u;
       }
       TR(t, 3);
-#pragma unroll
-      for (int ch = 0; ch < NC; ++ch) {
+      {
         float v[16];
-        load_acc(v, ch * 16);
+        load_acc(v, cg * 16);
 #pragma unroll
-        for (int q = 0; q < 16; ++q) sG[(ch * 16 + q) * 256 + r] = v[q] + bias;
+        for (int q = 0; q < 16; ++q) sG[(cg * 16 + q) * 256 + r] = v[q] + bias;
       }
       ptx::tc_fence_before();
       ptx::fence_async_smem();
@@ -1172,7 +1175,7 @@ __global__ void __launch_bounds__(256, 1)
 #pragma unroll
         for (int ch = 0; ch < NC; ++ch)
 #pragma unroll
-          for (int q = 0; q < 16; ++q) gx[ch][q] = sG[(ch * 16 + q) * 256 + r];
+          for (int q = 0; q < 16; ++q) gx[ch][q] = sG[(cg * 16 + q) * 256 + r];
       } else if (t >= 2) {
         // my staging slot p and P's sIn slot p are free once every P consumed step t-2
         ptx::mbar_wait_cluster(emptyA + p, eph[p]);
@@ -1187,7 +1190,7 @@ __global__ void __launch_bounds__(256, 1)
       for (int ch = 0; ch < NC; ++ch) {
         float v[16];
         if (t > 0) {
-          load_acc(v, ch * 16);
+          load_acc(v, cg * 16);
         } else {
 #pragma unroll
           for (int q = 0; q < 16; ++q) v[q] = 0.f;
@@ -1203,8 +1206,8 @@ __global__ void __launch_bounds__(256, 1)
           for (int q = 0; q < 4; ++q) {
             const int col = 4 * q + gate;
             const float4 a4 = *reinterpret_cast<const float4*>(myAct + col * ACT_LD + 4 * u);
-            const int bl = ch * 16 + col;
-            const size_t b = (size_t)col0 + bl;
+            const int bl = cg * 16 + col;                 // row within the CTA's Bc batch rows
+            const size_t b = (size_t)blockIdx.y * Bc + bl;
             const float i = a4.x, f = a4.y, g = a4.z, o = a4.w;
             const float cv = f * creg[ch * 4 + q] + i * g;
             creg[ch * 4 + q] = cv;
@@ -1253,7 +1256,7 @@ __global__ void __launch_bounds__(256, 1)
 size_t recur2_fwd_smem(int hp, int Bc) {
   const int nkb = (hp + 63) / 64;
   return 1024 + 2 * (size_t)nkb * 16384 + 2 * (size_t)nkb * Bc * 128 + 2 * (size_t)Bc * 128 +
-         (size_t)8 * 16 * ACT_LD * 4 + (size_t)Bc * 256 * 4 + 128;
+         (size_t)(Bc / 2) * 16 * ACT_LD * 4 + (size_t)Bc * 256 * 4 + 128;
 }
 
 }  // namespace
@@ -1374,7 +1377,7 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
   if (!getenv("HDP_WAVEFRONT_BC")) {
     cudaLaunchConfig_t cfg = {};
     cfg.gridDim = dim3(3 * G, a.B / 16);
-    cfg.blockDim = dim3(256);
+    cfg.blockDim = dim3(256);  // BC = 16 -> 8 warps
     cfg.dynamicSmemBytes = recur2_fwd_smem(a.hp, 16);
     cudaLaunchAttribute at[1];
     at[0].id = cudaLaunchAttributeClusterDimension;
@@ -1394,8 +1397,8 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
   float *c0 = a.C0, *c1 = a.C1;
   unsigned long long* trace = a.trace;
   void* args[] = {&mU0, &mW1, &mU1, &gx, &b1, &T, &B, &hpi, &hs0, &c0, &g0, &hs1, &c1, &g1, &trace};
-  return launch_cluster(Bc == 16 ? fn16 : fn32, dim3(3 * G, a.B / Bc), dim3(256), recur2_fwd_smem(a.hp, Bc), 3 * G, s,
-                        args);
+  return launch_cluster(Bc == 16 ? fn16 : fn32, dim3(3 * G, a.B / Bc), dim3(16 * Bc), recur2_fwd_smem(a.hp, Bc), 3 * G,
+                        s, args);
 }
 
 }  // namespace hdp
