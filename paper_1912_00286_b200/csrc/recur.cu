@@ -990,8 +990,8 @@ __global__ void __launch_bounds__(BC * 16, 1)
   uint8_t* sA = smem;                          // [2 halves][nkb][16 KB] resident A slice (U0 / W1 / U1)
   uint8_t* sB = sA + 2 * nkb * 16384;          // [2][hbuf] B operand (h of the previous / same step)
   uint8_t* sX = sB + 2 * hbuf;                 // [2][Bc][128 B] staging of my h_t K-block
-  float* sAct = reinterpret_cast<float*>(sX + 2 * Bc * 128);   // [8 warps][16][ACT_LD]
-  float* sG = sAct + (BC / 2) * 16 * ACT_LD;          // [Bc][256] fp32: P out staging / R1 a1x input (single buffer)
+  float* sAct = reinterpret_cast<float*>(sX + 2 * Bc * 128);   // [warps][8 columns][ACT_LD]
+  float* sG = sAct + (BC / 2) * 8 * ACT_LD;          // [Bc][256] fp32: P out staging / R1 a1x input (single buffer)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sG + Bc * 256);
   uint64_t* barU = bars;
   uint64_t* barM = bars + 1;
@@ -1052,7 +1052,7 @@ __global__ void __launch_bounds__(BC * 16, 1)
   ptx::cluster_wait();
 
   const uint32_t idesc = ptx::idesc_f16_f32(128, Bc, 0, 0);
-  float* myAct = sAct + warp * 16 * ACT_LD;
+  float* myAct = sAct + warp * 8 * ACT_LD;  // 8 columns staged at a time
   const float gsc = gate == 2 ? 2.f : 1.f;
   const uint32_t sB_addr = ptx::smem_u32(sB), sX_addr = ptx::smem_u32(sX), sG_addr = ptx::smem_u32(sG);
   uint32_t fph[2] = {0u, 0u}, eph[2] = {0u, 0u};
@@ -1196,16 +1196,19 @@ __global__ void __launch_bounds__(BC * 16, 1)
           for (int q = 0; q < 16; ++q) v[q] = 0.f;
         }
 #pragma unroll
-        for (int q = 0; q < 16; ++q) myAct[q * ACT_LD + lane] = act_gate(v[q] + gx[ch][q], gsc);
+        for (int hh8 = 0; hh8 < 2; ++hh8) {
+        // stage columns [8*hh8, 8*hh8 + 8) of the chunk, then each lane takes q = 2*hh8, 2*hh8 + 1
+#pragma unroll
+        for (int q = 0; q < 8; ++q) myAct[q * ACT_LD + lane] = act_gate(v[hh8 * 8 + q] + gx[ch][hh8 * 8 + q], gsc);
         __syncwarp();
         if (unit_ok) {
           const int u = lane >> 2;
           const int ul = r >> 2;
           const int c = ul >> 3;
 #pragma unroll
-          for (int q = 0; q < 4; ++q) {
+          for (int q = 2 * hh8; q < 2 * hh8 + 2; ++q) {
             const int col = 4 * q + gate;
-            const float4 a4 = *reinterpret_cast<const float4*>(myAct + col * ACT_LD + 4 * u);
+            const float4 a4 = *reinterpret_cast<const float4*>(myAct + (col - 8 * hh8) * ACT_LD + 4 * u);
             const int bl = cg * 16 + col;                 // row within the CTA's Bc batch rows
             const size_t b = (size_t)blockIdx.y * Bc + bl;
             const float i = a4.x, f = a4.y, g = a4.z, o = a4.w;
@@ -1221,6 +1224,7 @@ __global__ void __launch_bounds__(BC * 16, 1)
           }
         }
         __syncwarp();
+        }
       }
       ptx::tc_fence_before();
       ptx::fence_async_smem();
@@ -1256,7 +1260,7 @@ __global__ void __launch_bounds__(BC * 16, 1)
 size_t recur2_fwd_smem(int hp, int Bc) {
   const int nkb = (hp + 63) / 64;
   return 1024 + 2 * (size_t)nkb * 16384 + 2 * (size_t)nkb * Bc * 128 + 2 * (size_t)Bc * 128 +
-         (size_t)(Bc / 2) * 16 * ACT_LD * 4 + (size_t)Bc * 256 * 4 + 128;
+         (size_t)(Bc / 2) * 8 * ACT_LD * 4 + (size_t)Bc * 256 * 4 + 128;
 }
 
 }  // namespace
