@@ -131,6 +131,7 @@ struct hdp_ctx {
   std::vector<Slot> slot;
   float *Gx = nullptr, *Gh = nullptr, *dH[2] = {nullptr, nullptr}, *dhrec = nullptr, *dc = nullptr;
   char *dA = nullptr, *dz = nullptr;
+  char* dA2 = nullptr;  // layer-0 dA of the 2-layer backward wavefront (layer 1 keeps dA)
   float* crp = nullptr;
   size_t crp_floats = 0;
   float* ws = nullptr;
@@ -315,7 +316,8 @@ void carve(hdp_ctx* c, char* base) {
   c->s2 = (float*)cv.take(d.optimizer == HDP_OPT_ADAM ? c->M_own * 4 : 0);
   c->grads = cv.take((size_t)c->nslots * P * c->gsz);
   c->recv = cv.take(c->world > 1 ? c->max_bucket * c->gsz : 0);
-  c->status = (int*)cv.take(4096);  // [0] non-finite count; +1024 B: recurrence barrier counters
+  c->status = (int*)cv.take(32768);  // [0] non-finite count; +1024 B: recurrence barrier counters;
+                                       // +4096 B: backward-wavefront hand-off counters
   c->slot.assign(c->nslots, hdp_ctx::Slot{});
   if (d.n_layers > 0) {
     const long B = d.max_batch, T = d.max_seq, L = d.n_layers, hp = c->hp, e = c->esz;
@@ -338,6 +340,7 @@ void carve(hdp_ctx* c, char* base) {
     c->Gx = (float*)cv.take(rows * 4 * hp * 4);
     c->Gh = (float*)cv.take(B * 4 * hp * 4);
     c->dA = cv.take(rows * 4 * hp * e);
+    c->dA2 = cv.take(L == 2 && !c->f32 ? rows * 4 * hp * e : 0);
     const long dw = std::max(hp, c->Ip0);
     c->dH[0] = (float*)cv.take(rows * dw * 4);
     c->dH[1] = (float*)cv.take(rows * dw * 4);
@@ -704,7 +707,33 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
   float* Cl = S.C + l * c_layer;
   const char* Gl = S.gates + l * g_layer * e;
   const bool last_only = d.head_last_step && l == L - 1;
-  if (!f32 && c->persistent && hdp::recur_bwd_supported(B, (int)hp)) {
+  // 2 layers, mixed mode: both layers' BPTT and the dX1 projection in one wavefront
+  // launch (segment for layer 1); layer 0's segment then only has its K8 / K9 work
+  const bool wave = L == 2 && !f32 && c->persistent && hdp::recur2_bwd_supported(B, (int)hp);
+  char* dAl = wave && l == 0 ? c->dA2 : c->dA;
+  if (wave && l == 1) {
+    hdp::Recur2BwdArgs wa;
+    wa.U0 = (const __half*)c->W(c->find("U0"));
+    wa.U1 = (const __half*)c->W(iU);
+    wa.W1 = (const __half*)c->W(iW);
+    wa.dHtop = dHa;
+    wa.dHtop_last_only = last_only ? 1 : 0;
+    wa.gates0 = (const __half*)S.gates;
+    wa.gates1 = (const __half*)Gl;
+    wa.C0 = S.C;
+    wa.C1 = Cl;
+    wa.dA0 = (__half*)c->dA2;
+    wa.dA1 = (__half*)c->dA;
+    wa.dX1 = dHnext;
+    wa.flags = (unsigned*)((char*)c->status + 4096);
+    wa.T = T;
+    wa.B = B;
+    wa.hp = (int)hp;
+    KScope ks_(c, HDP_K_RECUR_BWD, 1, s);
+    CK_CUDA(hdp::launch_recur2_bwd(wa, s));
+  } else if (wave) {
+    // layer 0: already done by the wavefront launch of the layer-1 segment
+  } else if (!f32 && c->persistent && hdp::recur_bwd_supported(B, (int)hp)) {
     // A6 + A7 for all t in one persistent kernel (U^T slice resident in SMEM)
     hdp::RecurBwdArgs ra;
     ra.U = (const __half*)c->W(iU);
@@ -760,17 +789,17 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
               epi_f32(c->dhrec, hp), s));
   }
   // K8 (A8): dW = dA^T X, dU = dA^T H_{-1}, db = sum dA
-  CK(gemm(c, HDP_K_GEMM_DW, c->dA, 4 * hp, 1, X, Ipl, 1, 4 * hp, Ipl, rows, epi_elem(gf, c->G(si, iW), Ipl), s));
-  CK(gemm(c, HDP_K_GEMM_DW, c->dA, 4 * hp, 1, Hs, hp, 1, 4 * hp, hp, rows, epi_elem(gf, c->G(si, iU), hp), s));
+  CK(gemm(c, HDP_K_GEMM_DW, dAl, 4 * hp, 1, X, Ipl, 1, 4 * hp, Ipl, rows, epi_elem(gf, c->G(si, iW), Ipl), s));
+  CK(gemm(c, HDP_K_GEMM_DW, dAl, 4 * hp, 1, Hs, hp, 1, 4 * hp, hp, rows, epi_elem(gf, c->G(si, iU), hp), s));
   {
     KScope ks_(c, HDP_K_GEMM_DW, 2, s);
-    CK_CUDA(hdp::launch_colreduce(f32, c->dA, 4 * hp, (int)rows, (int)(4 * hp), nullptr, c->crp, gf, c->G(si, ib), s));
+    CK_CUDA(hdp::launch_colreduce(f32, dAl, 4 * hp, (int)rows, (int)(4 * hp), nullptr, c->crp, gf, c->G(si, ib), s));
   }
-  if (l > 0) {
+  if (l > 0 && !wave) {  // (the wavefront computed dX1 itself)
     // K9: dX = dA W  ->  dH_above of layer l-1 (W read MN-major as [K = 4hp][N = Ip])
-    CK(gemm(c, HDP_K_GEMM_DX, c->dA, 4 * hp, 0, c->W(iW), Ipl, 1, rows, Ipl, 4 * hp, epi_f32(dHnext, Ipl), s));
+    CK(gemm(c, HDP_K_GEMM_DX, dAl, 4 * hp, 0, c->W(iW), Ipl, 1, rows, Ipl, 4 * hp, epi_f32(dHnext, Ipl), s));
   } else if (d.vocab > 0) {
-    CK(gemm(c, HDP_K_GEMM_DX, c->dA, 4 * hp, 0, c->W(iW), Ipl, 1, rows, Ipl, 4 * hp, epi_f32(dHnext, Ipl), s));
+    CK(gemm(c, HDP_K_GEMM_DX, dAl, 4 * hp, 0, c->W(iW), Ipl, 1, rows, Ipl, 4 * hp, epi_f32(dHnext, Ipl), s));
     const int iE = c->find("E");
     {
       KScope ks_(c, HDP_K_EMBED_BWD, 2, s);

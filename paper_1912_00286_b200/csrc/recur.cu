@@ -24,6 +24,7 @@
 
 #include <cstdio>
 #include <cstdlib>
+#include <cstring>
 
 #include "gemm.cuh"
 #include "ptx.cuh"
@@ -923,6 +924,375 @@ __global__ void __launch_bounds__(128, 1)
   if (warp == 2) ptx::tmem_dealloc(tbase, tcols);
 }
 
+
+// ============================================================== 2-layer wavefront (backward)
+struct BwdRoleParams {
+  const float* dHa;
+  int last_only;
+  const __half* gates;
+  const float* C;
+  __half* dA;
+};
+struct __align__(64) Bwd2Params {
+  CUtensorMap tmU[2];  // MN-major U^T slices: [0] U1 (role 0), [1] U0 (role 2)
+  CUtensorMap tmW1;    // MN-major W1^T slice (role 1)
+  CUtensorMap tmA1;    // dA1 rows [T*B][4hp], K-major (role 1)
+  BwdRoleParams q[2];  // [0] layer 1, [1] layer 0
+  float* dX1;          // [T][B][hp] = dA1 W1  (dH_above of layer 0)
+  unsigned* q1done;    // [nbg][32]: layer-1 steps published (x G CTAs)
+  unsigned* xdone;     // [nbg][8][32]: projection steps published per unit slice
+  int T, B, hp, nbg;
+};
+
+// Projection role: dX1_t[b][unit] = sum_r dA1_t[b][r] W1[r][unit] for my 64 units
+// (swap-AB tcgen05, A = W1^T slice MN-major resident, B = dA1_t rows via TMA).
+template <int NC>
+__device__ __forceinline__ void bwd_proj_role(const Bwd2Params& P, int grp) {
+  constexpr int Bc = 16 * NC;
+  constexpr int NACC = Bc <= 32 ? 8 : 4;
+  constexpr int AC = NACC * Bc;
+  constexpr uint32_t tcols = AC <= 32 ? 32 : AC <= 64 ? 64 : AC <= 128 ? 128 : 256;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int T = P.T, B = P.B, hp = P.hp;
+  const int fourhp = 4 * hp;
+  const int nkb = fourhp / 64;
+  uint8_t* sW = smem;                 // nkb x 8 KB
+  uint8_t* sA = sW + nkb * 8192;      // nkb x Bc*128 (single buffer)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + nkb * Bc * 128);
+  uint64_t* barU = bars;
+  uint64_t* barM = bars + 1;
+  uint64_t* barA = bars + 2;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = blockIdx.x, G = gridDim.x;
+  const int j0 = rank * 64, col0 = grp * Bc;
+  const int jl = lane & 15, half = lane >> 4;
+  const int unit = j0 + warp * 16 + jl;
+  const bool unit_ok = unit < hp;
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch(&P.tmW1);
+    ptx::tma_prefetch(&P.tmA1);
+    ptx::mbar_init(barU, 1);
+    ptx::mbar_init(barM, 4);
+    ptx::mbar_init(barA, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tslot, tcols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  if (threadIdx.x == 0) {
+    ptx::mbar_arrive_expect_tx(barU, nkb * 8192);
+    for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sW + kb * 8192, &P.tmW1, barU, j0, kb * 64);
+    ptx::mbar_wait(barU, 0);
+  }
+  __syncthreads();
+  const uint32_t idesc = ptx::idesc_f16_f32(64, Bc, 1, 0);
+  uint32_t ph = 0;
+  for (int t = T - 1; t >= 0; --t) {
+    if (threadIdx.x == 0) {
+      // dA1_t published by every layer-1 CTA of my batch group
+      const unsigned* f = P.q1done + grp * 32;
+      const unsigned target = (unsigned)(G * (T - t));
+      if (acquire_ld(f) < target) {
+        const uint64_t t0 = ptx::globaltimer_ns();
+        while (acquire_ld(f) < target) {
+          if (ptx::globaltimer_ns() - t0 > 10000000000ull) __trap();
+        }
+      }
+      fence_proxy_async();
+      ptx::mbar_arrive_expect_tx(barA, nkb * Bc * 128);
+      for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sA + kb * Bc * 128, &P.tmA1, barA, kb * 64, t * B + col0);
+    }
+    if (lane == 0) {
+      ptx::mbar_wait(barA, ph);
+      ptx::tc_fence_after();
+      const uint32_t aW = ptx::smem_u32(sW), aA = ptx::smem_u32(sA);
+      const uint64_t ad0 = ptx::smem_desc_sw128(aW, 8192, 1024), bd0 = ptx::smem_desc_sw128(aA, 0, 1024);
+      for (int k = warp; k < nkb * 4; k += 4) {
+        const int kb = k >> 2, kq = k & 3;
+        const uint64_t ad = ad0 + (uint64_t)((kb * 8192 + kq * 2048) >> 4);
+        const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kq * 32) >> 4);
+        ptx::mma_f16(tbase + (k % NACC) * Bc, ad, bd, idesc, k >= NACC ? 1u : 0u);
+      }
+      ptx::mma_commit(barM);
+    }
+    __syncwarp();
+    ptx::mbar_wait(barM, ph);
+    ph ^= 1u;
+    ptx::tc_fence_after();
+    float* out = P.dX1 + (size_t)t * B * hp;
+#pragma unroll
+    for (int ch = 0; ch < NC; ++ch) {
+      float v[16];
+      const uint32_t ta = tbase + (static_cast<uint32_t>(warp * 32) << 16) + ch * 16;
+      ptx::tmem_ld16(ta, v);
+#pragma unroll
+      for (int a = 1; a < NACC; ++a) {
+        if (a >= nkb * 4) break;
+        float w[16];
+        ptx::tmem_ld16(ta + a * Bc, w);
+#pragma unroll
+        for (int q = 0; q < 16; ++q) v[q] += w[q];
+      }
+      if (unit_ok) {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) {
+          const float hi = __shfl_sync(0xffffffffu, v[8 + q], jl);
+          const float val = half ? hi : v[q];
+          out[((size_t)col0 + ch * 16 + half * 8 + q) * hp + unit] = val;  // R11 (fp32)
+        }
+      } else {
+#pragma unroll
+        for (int q = 0; q < 8; ++q) (void)__shfl_sync(0xffffffffu, v[8 + q], jl);
+      }
+    }
+    ptx::tc_fence_before();
+    __syncthreads();  // MMA reads of sA done (barM) and all dX1 stores issued
+    if (threadIdx.x == 0) {
+      __threadfence();
+      release_add(P.xdone + (grp * 8 + rank) * 32, 1u);
+    }
+  }
+  ptx::tc_fence_after();
+  __syncthreads();
+  if (warp == 2) ptx::tmem_dealloc(tbase, tcols);
+}
+
+template <int NC>
+__global__ void __launch_bounds__(128, 1)
+    recur2_bwd_kernel(const __grid_constant__ Bwd2Params P) {
+  const int T = P.T, B = P.B, hp = P.hp;
+  const int role = blockIdx.y / P.nbg, grp = blockIdx.y % P.nbg;
+  if (role == 1) {
+    bwd_proj_role<NC>(P, grp);
+    return;
+  }
+  const int qi = role == 0 ? 0 : 1;  // 0: layer 1 (Q1), 1: layer 0 (Q0)
+  const CUtensorMap& tmU = P.tmU[qi];
+  const float* __restrict__ dHa = P.q[qi].dHa;
+  const int dHa_last_only = P.q[qi].last_only;
+  const __half* __restrict__ gates = P.q[qi].gates;
+  const float* __restrict__ Cst = P.q[qi].C;
+  __half* __restrict__ dA = P.q[qi].dA;
+  unsigned long long* __restrict__ trace = nullptr;
+  constexpr int Bc = 16 * NC;
+  // optional phase trace (CTA (0,0), thread 0): [t][5] globaltimer stamps
+  const bool tr = trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int fourhp = 4 * hp;
+  const int nkb = fourhp / 64;
+  const int abuf = nkb * Bc * 128;
+  constexpr int SX = 4 * Bc * 128;             // my 4 K-blocks (256 gate rows) in destination layout
+  uint8_t* sU = smem;                          // nkb x 8 KB (U^T slice, MN-major)
+  uint8_t* sA = sU + nkb * 8192;               // [2][abuf] B operand (dA_{t+1}), filled by peers
+  uint8_t* sX = sA + 2 * abuf;                 // [2][SX] staging of my dA_t slice, swizzled like sA
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sX + 2 * SX);
+  uint64_t* barU = bars;
+  uint64_t* barM = bars + 1;
+  uint64_t* fullA = bars + 2;                  // [2]: peers' bulk copies into sA[p]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int G = gridDim.x;
+  const int rank = blockIdx.x;
+  const int j0 = rank * 64;
+  const int col0 = grp * Bc;
+  const int jl = lane & 15;
+  const int half = lane >> 4;
+  const int ul = warp * 16 + jl;               // unit within my 64-unit slice
+  const int unit = j0 + ul;
+  const bool unit_ok = unit < hp;
+  constexpr int NACC = Bc <= 32 ? 8 : 4;
+  constexpr int AC = NACC * Bc;
+  constexpr uint32_t tcols = AC <= 32 ? 32 : AC <= 64 ? 64 : AC <= 128 ? 128 : 256;
+  // bytes every consumer receives per step: all producers' valid K-blocks
+  int total_bytes = 0;
+  for (int r = 0; r < G; ++r) total_bytes += max(0, min(64, hp - 64 * r)) / 16 * Bc * 128;
+  const int my_kblocks = max(0, min(64, hp - j0)) / 16;
+
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch(&tmU);
+    ptx::mbar_init(barU, 1);
+    ptx::mbar_init(barM, 4);  // one commit per issuing warp
+    ptx::mbar_init(fullA, 1);
+    ptx::mbar_init(fullA + 1, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tslot, tcols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  if (threadIdx.x == 0) {
+    // arm both operand slots for their first use before any peer can deliver
+    ptx::mbar_arrive_expect_tx(fullA, total_bytes);
+    ptx::mbar_arrive_expect_tx(fullA + 1, total_bytes);
+    ptx::mbar_arrive_expect_tx(barU, nkb * 8192);
+    for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sU + kb * 8192, &tmU, barU, j0, kb * 64);
+    ptx::mbar_wait(barU, 0);
+  }
+  ptx::cluster_arrive();  // all CTAs resident, barriers initialised and armed
+  ptx::cluster_wait();
+
+  float dcr[NC * 8];
+#pragma unroll
+  for (int i = 0; i < NC * 8; ++i) dcr[i] = 0.f;
+  const uint32_t idesc = ptx::idesc_f16_f32(64, Bc, 1, 0);
+  const uint32_t sA_addr = ptx::smem_u32(sA), sX_addr = ptx::smem_u32(sX);
+  uint32_t fphase[2] = {0u, 0u};
+
+  for (int t = T - 1; t >= 0; --t) {
+    if (tr) trace[t * 5 + 0] = ptx::globaltimer_ns();
+    if (qi == 1) {
+      // dH_above[t] of layer 0 = dX1_t, produced in this kernel by the projection CTA of my units
+      if (threadIdx.x == 0) {
+        const unsigned* f = P.xdone + (grp * 8 + rank) * 32;
+        const unsigned target = (unsigned)(T - t);
+        if (acquire_ld(f) < target) {
+          const uint64_t t0 = ptx::globaltimer_ns();
+          while (acquire_ld(f) < target) {
+            if (ptx::globaltimer_ns() - t0 > 10000000000ull) __trap();
+          }
+        }
+      }
+      __syncthreads();
+    }
+    float dh0[NC * 8], cc[NC * 8], cp[NC * 8];
+    uint2 gq[NC * 8];
+#pragma unroll
+    for (int ch = 0; ch < NC; ++ch)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int idx = ch * 8 + k;
+        const size_t b = (size_t)col0 + ch * 16 + half * 8 + k;
+        float d = 0.f, c1 = 0.f, c0 = 0.f;
+        uint2 gg = make_uint2(0u, 0u);
+        if (unit_ok) {
+          if (dHa_last_only) {
+            if (t == T - 1) d = __ldg(dHa + b * hp + unit);
+          } else if (qi == 1) {
+            d = __ldcg(dHa + ((size_t)t * B + b) * hp + unit);  // written in-kernel: L2-coherent load
+          } else {
+            d = __ldg(dHa + ((size_t)t * B + b) * hp + unit);
+          }
+          c1 = __ldg(Cst + ((size_t)t * B + b) * hp + unit);
+          if (t > 0) c0 = __ldg(Cst + ((size_t)(t - 1) * B + b) * hp + unit);
+          gg = __ldg(reinterpret_cast<const uint2*>(gates + ((size_t)t * B + b) * fourhp + 4 * unit));
+        }
+        dh0[idx] = d;
+        cc[idx] = c1;
+        cp[idx] = c0;
+        gq[idx] = gg;
+      }
+    if (t < T - 1) {
+      const int p = (t + 1) & 1;
+      if (lane == 0) {
+        ptx::mbar_wait(fullA + p, fphase[p]);  // every peer's dA_{t+1} slice landed in sA[p]
+        ptx::tc_fence_after();
+        if (tr) trace[t * 5 + 1] = ptx::globaltimer_ns();
+        // lane 0 of each warp issues K-steps k = warp, warp + 4, ... (barM counts 4 commits)
+        const uint32_t aU = ptx::smem_u32(sU), aA = sA_addr + p * abuf;
+        const uint64_t ad0 = ptx::smem_desc_sw128(aU, 8192, 1024), bd0 = ptx::smem_desc_sw128(aA, 0, 1024);
+        for (int k = warp; k < nkb * 4; k += 4) {
+          const int kb = k >> 2, kk = k & 3;  // start-address field is in 16-B units
+          const uint64_t ad = ad0 + (uint64_t)((kb * 8192 + kk * 2048) >> 4);
+          const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kk * 32) >> 4);
+          ptx::mma_f16(tbase + (k % NACC) * Bc, ad, bd, idesc, k >= NACC ? 1u : 0u);
+        }
+        ptx::mma_commit(barM);
+      }
+      __syncwarp();
+      ptx::mbar_wait(barM, (T - 2 - t) & 1);
+      ptx::tc_fence_after();
+      fphase[p] ^= 1u;
+      // re-arm slot p for its next use (peers can deliver into it only after
+      // they consumed my dA_t, i.e. after this point -- see the WAR note below)
+      if (threadIdx.x == 0 && t >= 2) ptx::mbar_arrive_expect_tx(fullA + p, total_bytes);
+    }
+    if (tr) trace[t * 5 + 2] = ptx::globaltimer_ns();
+    __half* dAout = dA + (size_t)t * B * fourhp;
+    uint8_t* stg = sX + (t & 1) * SX;
+#pragma unroll
+    for (int ch = 0; ch < NC; ++ch) {
+      float v[16];
+      if (t < T - 1) {
+        const uint32_t ta = tbase + (static_cast<uint32_t>(warp * 32) << 16) + ch * 16;
+        ptx::tmem_ld16(ta, v);
+#pragma unroll
+        for (int a = 1; a < NACC; ++a) {
+          if (a >= nkb * 4) break;  // accumulator never written (tiny K)
+          float w[16];
+          ptx::tmem_ld16(ta + a * Bc, w);
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] += w[k];
+        }
+      } else {
+#pragma unroll
+        for (int k = 0; k < 16; ++k) v[k] = 0.f;
+      }
+      float rec[8];
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const float hi = __shfl_sync(0xffffffffu, v[8 + k], jl);
+        rec[k] = half ? hi : v[k];
+      }
+      if (unit_ok) {
+        // staging position of my unit's 4 gate rows (local gate row 4*ul) in row bl:
+        // K-block j = ul/16, 16-B chunk c = (4ul % 64)/8, byte (4ul % 8)*2
+        const int j = ul >> 4, c = (ul & 15) >> 1, byo = (ul & 1) * 8;
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int idx = ch * 8 + k;
+          const int bl = ch * 16 + half * 8 + k;
+          const size_t b = (size_t)col0 + bl;
+          const float dh = dh0[idx] + rec[k];
+          const float2 if2 = __half22float2(*reinterpret_cast<const __half2*>(&gq[idx].x));
+          const float2 go2 = __half22float2(*reinterpret_cast<const __half2*>(&gq[idx].y));
+          const float i = if2.x, f = if2.y, g = go2.x, o = go2.y;
+          float tc, sech2;
+          tanh_sech2(cc[idx], tc, sech2);
+          const float d = dcr[idx] + dh * o * sech2;
+          __align__(8) __half2 q2[2] = {
+              __halves2half2(__float2half_rn(d * g * i * (1.f - i)), __float2half_rn(d * cp[idx] * f * (1.f - f))),
+              __halves2half2(__float2half_rn(d * i * (1.f - g * g)), __float2half_rn(dh * tc * o * (1.f - o)))};
+          const uint2 pk = *reinterpret_cast<const uint2*>(q2);
+          *reinterpret_cast<uint2*>(dAout + b * fourhp + 4 * unit) = pk;  // R10 (for K8 / K9)
+          *reinterpret_cast<uint2*>(stg + j * Bc * 128 + bl * 128 + ((c ^ (bl & 7)) << 4) + byo) = pk;
+          dcr[idx] = d * f;
+        }
+      }
+    }
+    ptx::tc_fence_before();
+    ptx::fence_async_smem();  // staging writes (generic) -> bulk copy reads (async proxy)
+    if (qi == 0) fence_proxy_async();  // global dA_t stores -> the projection role's TMA reads
+    __syncthreads();
+    if (qi == 0 && threadIdx.x == 0) {
+      __threadfence();
+      release_add(P.q1done + grp * 32, 1u);
+    }
+    if (tr) trace[t * 5 + 3] = ptx::globaltimer_ns();
+    // push dA_t (consumed by step t-1) into every peer's sA[t & 1]: one bulk copy per peer.
+    // WAR: a peer writes sA[p] of step s only after consuming my dA_{s+1}, which I produce
+    // after my MMA that read sA[p] for step s+2 -- the double buffers need no extra barrier.
+    if (t > 0 && threadIdx.x < G && my_kblocks > 0) {
+      const int dst = threadIdx.x;
+      const uint32_t dsta = ptx::mapa(sA_addr + (t & 1) * abuf + 4 * rank * Bc * 128, dst);
+      const uint32_t mb = ptx::mapa(ptx::smem_u32(fullA + (t & 1)), dst);
+      ptx::bulk_copy_to_peer(dsta, sX_addr + (t & 1) * SX, my_kblocks * Bc * 128, mb);
+    }
+    if (tr) trace[t * 5 + 4] = ptx::globaltimer_ns();
+  }
+  // nobody leaves while a peer may still read my staging / write my sA
+  ptx::cluster_arrive();
+  ptx::cluster_wait();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc(tbase, tcols);
+}
+
 size_t bwd_cl_smem(int hp, int Bc) {
   const int nkb = 4 * hp / 64;
   return 1024 + (size_t)nkb * 8192 + 2 * (size_t)nkb * Bc * 128 + 2 * (size_t)4 * Bc * 128 + 128;
@@ -1403,6 +1773,73 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
   void* args[] = {&mU0, &mW1, &mU1, &gx, &b1, &T, &B, &hpi, &hs0, &c0, &g0, &hs1, &c1, &g1, &trace};
   return launch_cluster(Bc == 16 ? fn16 : fn32, dim3(3 * G, a.B / Bc), dim3(16 * Bc), recur2_fwd_smem(a.hp, Bc), 3 * G,
                         s, args);
+}
+
+}  // namespace hdp
+
+namespace hdp {
+
+bool recur2_bwd_supported(int B, int hp) {
+  const char* e = getenv("HDP_WAVEFRONT");
+  if (e && e[0] == '0') return false;
+  int Bc = 0, nbg = 0;
+  if (!plan_bwd(B, hp, &Bc, &nbg)) return false;
+  const int G = (hp + 63) / 64;
+  if (G > 8 || 3 * G * nbg > 148 || nbg > 16) return false;
+  return bwd_cl_smem(hp, Bc) <= 227 * 1024;
+}
+
+cudaError_t launch_recur2_bwd(const Recur2BwdArgs& a, cudaStream_t s) {
+  int Bc = 0, nbg = 0;
+  if (!recur2_bwd_supported(a.B, a.hp) || !plan_bwd(a.B, a.hp, &Bc, &nbg)) return cudaErrorInvalidConfiguration;
+  const int G = (a.hp + 63) / 64;
+  const uint64_t hp = a.hp;
+  Bwd2Params P;
+  memset(&P, 0, sizeof P);
+  if (encode_tmap_2d(&P.tmU[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U1, hp, 4 * hp, hp * 2, 64, 64,
+                     CU_TENSOR_MAP_SWIZZLE_128B) ||
+      encode_tmap_2d(&P.tmU[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U0, hp, 4 * hp, hp * 2, 64, 64,
+                     CU_TENSOR_MAP_SWIZZLE_128B) ||
+      encode_tmap_2d(&P.tmW1, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.W1, hp, 4 * hp, hp * 2, 64, 64,
+                     CU_TENSOR_MAP_SWIZZLE_128B) ||
+      encode_tmap_2d(&P.tmA1, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.dA1, 4 * hp, (uint64_t)a.T * a.B, 4 * hp * 2, 64,
+                     Bc, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  P.q[0] = {a.dHtop, a.dHtop_last_only, a.gates1, a.C1, a.dA1};
+  P.q[1] = {a.dX1, 0, a.gates0, a.C0, a.dA0};
+  P.dX1 = a.dX1;
+  P.q1done = a.flags;
+  P.xdone = a.flags + 16 * 32;
+  P.T = a.T;
+  P.B = a.B;
+  P.hp = a.hp;
+  P.nbg = nbg;
+  cudaError_t e = cudaMemsetAsync(a.flags, 0, (16 * 32 + 16 * 8 * 32) * sizeof(unsigned), s);
+  if (e != cudaSuccess) return e;
+  const void* fn = Bc == 16 ? (const void*)recur2_bwd_kernel<1>
+                 : Bc == 32 ? (const void*)recur2_bwd_kernel<2>
+                 : Bc == 48 ? (const void*)recur2_bwd_kernel<3> : (const void*)recur2_bwd_kernel<4>;
+  // all CTAs wait on each other through global counters: they must be co-resident
+  {
+    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_cl_smem(a.hp, Bc));
+    if (e != cudaSuccess) return e;
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3(G, 3 * nbg);
+    cfg.blockDim = dim3(128);
+    cfg.dynamicSmemBytes = bwd_cl_smem(a.hp, Bc);
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeClusterDimension;
+    at[0].val.clusterDim.x = G;
+    at[0].val.clusterDim.y = 1;
+    at[0].val.clusterDim.z = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    int nclusters = 0;
+    if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess || nclusters < 3 * nbg)
+      return cudaErrorCooperativeLaunchTooLarge;
+  }
+  void* args[] = {&P};
+  return launch_cluster(fn, dim3(G, 3 * nbg), dim3(128), bwd_cl_smem(a.hp, Bc), G, s, args);
 }
 
 }  // namespace hdp

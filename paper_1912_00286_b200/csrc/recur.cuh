@@ -44,6 +44,23 @@ struct Recur2FwdArgs {
   unsigned long long* trace = nullptr;  // debug: [3 roles][T][5] timestamps, nullable
 };
 bool recur2_fwd_supported(int B, int hp);
+
+// Two stacked layers' BPTT as one wavefront: layer-1 recurrence, the input
+// gradient projection dX1 = dA1 W1, and the layer-0 recurrence (fed by dX1)
+// run concurrently as three 4-CTA-cluster roles per batch group.
+struct Recur2BwdArgs {
+  const __half *U0 = nullptr, *U1 = nullptr, *W1 = nullptr;
+  const float* dHtop = nullptr;  // dH above layer 1 ([T][B][hp], or [B][hp] at T-1 if last-only)
+  int dHtop_last_only = 0;
+  const __half *gates0 = nullptr, *gates1 = nullptr;
+  const float *C0 = nullptr, *C1 = nullptr;
+  __half *dA0 = nullptr, *dA1 = nullptr;  // separate [T][B][4hp] outputs
+  float* dX1 = nullptr;                   // [T][B][hp] scratch
+  unsigned* flags = nullptr;              // >= 16*32 + 16*8*32 uints
+  int T = 0, B = 0, hp = 0;
+};
+bool recur2_bwd_supported(int B, int hp);
+cudaError_t launch_recur2_bwd(const Recur2BwdArgs& a, cudaStream_t s);
 cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s);
 cudaError_t launch_recur_bwd(const RecurBwdArgs& a, cudaStream_t s);
 

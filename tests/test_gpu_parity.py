@@ -157,3 +157,20 @@ def test_persistent_matches_per_step_path(monkeypatch):
     for k in out["1"]["grad_err"][0]:
         assert out["1"]["grad_err"][0][k] <= 2e-2 and out["0"]["grad_err"][0][k] <= 2e-2
     assert abs(out["1"]["loss_gpu"] - out["0"]["loss_gpu"]) <= 1e-4
+
+
+@pytest.mark.parametrize("batch", [128, 32])
+def test_c2_wavefront_matches_layerwise(monkeypatch, batch):
+    """The 2-layer wavefront kernels (forward: R0/P/R1 roles; backward: Q1/X/Q0
+    roles) against the oracle and against the layer-by-layer persistent path."""
+    cfg = synth.CONFIGS["C2"].with_(seq=24)
+    out = {}
+    for flag in ("1", "0"):
+        monkeypatch.setenv("HDP_WAVEFRONT", flag)
+        recs = run_parity(cfg, batch, 1, steps=2, mixed=True)
+        out[flag] = recs
+        for r in recs:
+            assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
+            assert _max(r["grad_err"][0]) <= 2e-2, (flag, r["grad_err"])
+        assert _max(recs[-1]["master_err"]) <= 2e-2
+    assert abs(out["1"][0]["loss_gpu"] - out["0"][0]["loss_gpu"]) <= 1e-4
