@@ -1,2 +1,3 @@
-timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/t35.log 2>&1; echo pytest_exit=$? >> gpurun_out/t35.log
-timeout -s KILL 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/b35.log 2>&1; echo bench_exit=$? >> gpurun_out/b35.log
+timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py -x -q > gpurun_out/t39.log 2>&1; echo pytest_exit=$? >> gpurun_out/t39.log
+timeout -s KILL 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/b39.log 2>&1; echo bench_exit=$? >> gpurun_out/b39.log
+HDP_RECUR_TRACE=1 timeout -s KILL 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/tr39.log 2>&1

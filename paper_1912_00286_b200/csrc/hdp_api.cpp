@@ -131,7 +131,8 @@ struct hdp_ctx {
   std::vector<Slot> slot;
   float *Gx = nullptr, *Gh = nullptr, *dH[2] = {nullptr, nullptr}, *dhrec = nullptr, *dc = nullptr;
   char *dA = nullptr, *dz = nullptr;
-  char* dA2 = nullptr;  // layer-0 dA of the 2-layer backward wavefront (layer 1 keeps dA)
+  char* dA2 = nullptr;
+  float* Gx1 = nullptr;  // layer-1 G_x of the split forward wavefront  // layer-0 dA of the 2-layer backward wavefront (layer 1 keeps dA)
   float* crp = nullptr;
   size_t crp_floats = 0;
   float* ws = nullptr;
@@ -341,6 +342,7 @@ void carve(hdp_ctx* c, char* base) {
     c->Gh = (float*)cv.take(B * 4 * hp * 4);
     c->dA = cv.take(rows * 4 * hp * e);
     c->dA2 = cv.take(L == 2 && !c->f32 ? rows * 4 * hp * e : 0);
+    c->Gx1 = (float*)cv.take(L == 2 && !c->f32 ? rows * 4 * hp * 4 : 0);
     const long dw = std::max(hp, c->Ip0);
     c->dH[0] = (float*)cv.take(rows * dw * 4);
     c->dH[1] = (float*)cv.take(rows * dw * 4);
@@ -483,6 +485,8 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
       ra.U1 = (const __half*)c->W(c->find("U1"));
       ra.b1 = (const __half*)c->W(c->find("b1"));
       ra.Gx0 = c->Gx;
+      ra.a1x = c->Gx1;
+      ra.flags = (unsigned*)((char*)c->status + 4096);
       ra.Hs0 = (__half*)Hs;
       ra.C0 = Cl;
       ra.gates0 = (__half*)Gl;

@@ -25,6 +25,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <map>
 
 #include "gemm.cuh"
 #include "ptx.cuh"
@@ -1052,7 +1053,6 @@ __device__ __forceinline__ void bwd_proj_role(const Bwd2Params& P, int grp) {
     ptx::tc_fence_before();
     __syncthreads();  // MMA reads of sA done (barM) and all dX1 stores issued
     if (threadIdx.x == 0) {
-      __threadfence();
       release_add(P.xdone + (grp * 8 + rank) * 32, 1u);
     }
   }
@@ -1270,8 +1270,7 @@ __global__ void __launch_bounds__(128, 1)
     ptx::fence_async_smem();  // staging writes (generic) -> bulk copy reads (async proxy)
     if (qi == 0) fence_proxy_async();  // global dA_t stores -> the projection role's TMA reads
     __syncthreads();
-    if (qi == 0 && threadIdx.x == 0) {
-      __threadfence();
+    if (qi == 0 && threadIdx.x == 64) {  // not a pusher: the release waits for the stores to drain
       release_add(P.q1done + grp * 32, 1u);
     }
     if (tr) trace[t * 5 + 3] = ptx::globaltimer_ns();
@@ -1627,6 +1626,316 @@ __global__ void __launch_bounds__(BC * 16, 1)
   if (warp == 2) ptx::tmem_dealloc(tbase, TCOLS);
 }
 
+
+// ============================================================== 2-layer wavefront (forward, split clusters)
+// Three G-CTA clusters per batch group (G = ceil(hp/64)), one per role:
+//   role 0 (R0_k): layer-0 recurrence, units [64k, 64k+64)        (cluster-local h exchange)
+//   role 1 (P_k) : a1x_t = W1 h0_t + b1 for gate rows [256k, 256k+256)
+//   role 2 (R1_k): layer-1 recurrence, units [64k, 64k+64), gate inputs a1x from P_k
+// Cross-role hand-offs go through global memory (every step has its own slot, so
+// no back-pressure is needed) with release/acquire counters:
+//   R0 -> P : h0_t (the Hs0 stores R0 makes anyway), r0done[g] += 1 per CTA
+//   P  -> R1: a1x_t fp32 rows, pdone[g][k] += 1
+// Layer 1 trails layer 0 by a couple of steps; both recurrences run at the
+// single-layer step rate with 8 warps per CTA at Bc = 16.
+struct __align__(64) Fwd2Params {
+  CUtensorMap tmA[3];  // resident A slices (K-major, box 64 x 128): U0, W1, U1
+  CUtensorMap tmH0;    // Hs0 rows [(T+1)B][hp], box (64, Bc): P's B operand
+  const float* Gx0;    // [T][B][4hp]
+  float* a1x;          // [T][B][4hp]
+  const __half* b1;
+  __half* Hs[2];
+  float* C[2];
+  __half* gates[2];
+  unsigned* r0done;    // [16][32]
+  unsigned* pdone;     // [16][8][32]
+  unsigned long long* trace;
+  int T, B, Bc, hp, nbg;
+};
+
+__device__ __forceinline__ void spin_until(const unsigned* f, unsigned target) {
+  if (acquire_ld(f) >= target) return;
+  const uint64_t t0 = ptx::globaltimer_ns();
+  while (acquire_ld(f) < target) {
+    if (ptx::globaltimer_ns() - t0 > 10000000000ull) __trap();
+  }
+}
+
+template <int NCI>
+__global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__ Fwd2Params P) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int T = P.T, B = P.B, Bc = P.Bc, hp = P.hp;
+  const int role = blockIdx.y / P.nbg, grp = blockIdx.y % P.nbg;
+  const int nkb = (hp + 63) / 64;             // == cluster size
+  const int nk16 = (hp + 15) / 16;
+  const int nwarps = blockDim.x >> 5;
+  const int cgN = nwarps >> 3;
+  const int hbuf = nkb * Bc * 128;
+  uint8_t* sU = smem;                         // [2 halves][nkb][16 KB]
+  uint8_t* sH = sU + 2 * nkb * 16384;         // [2][hbuf]
+  uint8_t* sX = sH + 2 * hbuf;                // [2][Bc][128 B]
+  float* sAct = reinterpret_cast<float*>(sX + 2 * Bc * 128);
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sAct + nwarps * 16 * ACT_LD);
+  uint64_t* barU = bars;
+  uint64_t* barM = bars + 1;
+  uint64_t* fullH = bars + 2;                 // [2]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int quarter = warp & 3, hf = (warp >> 2) & 1, cg = warp >> 3;
+  const int G = gridDim.x;
+  const int rank = blockIdx.x;
+  const int row0 = rank * 256;
+  const int col0 = grp * Bc;
+  const int r = hf * 128 + quarter * 32 + lane;
+  const int grow = row0 + r;
+  const int gate = r & 3;
+  const int unit = grow >> 2;
+  const bool unit_ok = unit < hp;
+  const int fourhp = 4 * hp;
+  const int nacc = Bc <= 32 ? 4 : Bc <= 64 ? 2 : 1;
+  const int nis = min(nacc, nk16);
+  const int ac = 2 * nacc * Bc;
+  const uint32_t tcols = ac <= 32 ? 32 : ac <= 64 ? 64 : ac <= 128 ? 128 : ac <= 256 ? 256 : 512;
+  const int total_bytes = nkb * Bc * 128;
+  const bool tr = P.trace != nullptr && rank == 0 && grp == 0 && threadIdx.x == 0;
+  unsigned long long* trr = P.trace ? P.trace + (size_t)role * T * 5 : nullptr;
+#define TR(t, i) \
+  if (tr) trr[(t) * 5 + (i)] = ptx::globaltimer_ns()
+
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch(&P.tmA[role]);
+    ptx::mbar_init(barU, 1);
+    ptx::mbar_init(barM, nis);
+    ptx::mbar_init(fullH, 1);
+    ptx::mbar_init(fullH + 1, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tslot, tcols);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  if (threadIdx.x == 0) {
+    if (role != 1) {
+      ptx::mbar_arrive_expect_tx(fullH, total_bytes);
+      ptx::mbar_arrive_expect_tx(fullH + 1, total_bytes);
+    }
+    ptx::mbar_arrive_expect_tx(barU, 2 * nkb * 16384);
+    for (int h2 = 0; h2 < 2; ++h2)
+      for (int kb = 0; kb < nkb; ++kb)
+        ptx::tma_load_2d(sU + (h2 * nkb + kb) * 16384, &P.tmA[role], barU, kb * 64, row0 + h2 * 128);
+    ptx::mbar_wait(barU, 0);
+  }
+  ptx::cluster_arrive();
+  ptx::cluster_wait();
+
+  const uint32_t idesc = ptx::idesc_f16_f32(128, Bc, 0, 0);
+  const int nchunk = Bc / 16;
+  const uint32_t sH_addr = ptx::smem_u32(sH), sX_addr = ptx::smem_u32(sX);
+  uint32_t fphase[2] = {0u, 0u};
+  auto issue_mma = [&](int p) {
+    const uint32_t aU = ptx::smem_u32(sU), aH = sH_addr + p * hbuf;
+    const uint64_t ad0 = ptx::smem_desc_sw128(aU, 0, 1024), bd0 = ptx::smem_desc_sw128(aH, 0, 1024);
+    for (int k = warp; k < nk16; k += nis) {
+      const int kb = k >> 2, kk = k & 3;
+      const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kk * 32) >> 4);
+#pragma unroll
+      for (int h2 = 0; h2 < 2; ++h2) {
+        const uint64_t ad = ad0 + (uint64_t)(((h2 * nkb + kb) * 16384 + kk * 32) >> 4);
+        ptx::mma_f16(tbase + (h2 * nacc + warp) * Bc, ad, bd, idesc, k >= nis ? 1u : 0u);
+      }
+    }
+    ptx::mma_commit(barM);
+  };
+  auto load_acc = [&](float (&v)[16], int c0) {
+    const uint32_t ta = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + hf * nacc * Bc + c0;
+    ptx::tmem_ld16(ta, v);
+    for (int a = 1; a < nis; ++a) {
+      float w[16];
+      ptx::tmem_ld16(ta + a * Bc, w);
+#pragma unroll
+      for (int k = 0; k < 16; ++k) v[k] += w[k];
+    }
+  };
+
+  if (role == 1) {
+    // ------------------------------------------------------------ projection P_k
+    const float bias = unit_ok ? __half2float(P.b1[grow]) : 0.f;
+    const unsigned* r0f = P.r0done + grp * 32;
+    auto load_h0 = [&](int t) {  // thread 0: h0_t of every R0_k (all stored) -> sH[t & 1]
+      fence_proxy_async();
+      ptx::mbar_arrive_expect_tx(fullH + (t & 1), total_bytes);
+      for (int kb = 0; kb < nkb; ++kb)
+        ptx::tma_load_2d(sH + (t & 1) * hbuf + kb * Bc * 128, &P.tmH0, fullH + (t & 1), kb * 64,
+                         (t + 1) * B + col0);
+    };
+    bool pending = false;
+    if (threadIdx.x == 0) {
+      spin_until(r0f, (unsigned)G);
+      load_h0(0);
+    }
+    for (int t = 0; t < T; ++t) {
+      const int p = t & 1;
+      TR(t, 0);
+      if (lane == 0 && warp < nis) {
+        ptx::mbar_wait(fullH + p, fphase[p]);
+        ptx::tc_fence_after();
+        TR(t, 1);
+        issue_mma(p);
+      }
+      // prefetch h0_{t+1} now if R0 already published it (sH[p^1] was read by MMA t-1, complete)
+      if (threadIdx.x == 0 && t + 1 < T) {
+        if (acquire_ld(r0f) >= (unsigned)(G * (t + 2))) load_h0(t + 1);
+        else pending = true;
+      }
+      __syncwarp();
+      ptx::mbar_wait(barM, t & 1);
+      ptx::tc_fence_after();
+      fphase[p] ^= 1u;
+      TR(t, 2);
+#pragma unroll
+      for (int ci = 0; ci < NCI; ++ci) {
+        const int ch = ci * cgN + cg;
+        if (ch >= nchunk) break;
+        float v[16];
+        load_acc(v, ch * 16);
+        if (grow < fourhp) {
+          float* out = P.a1x + ((size_t)t * B + col0 + ch * 16) * fourhp + grow;
+#pragma unroll
+          for (int k = 0; k < 16; ++k) out[(size_t)k * fourhp] = v[k] + bias;  // layer-1 G_x (R3)
+        }
+      }
+      ptx::tc_fence_before();
+      __syncthreads();
+      TR(t, 3);
+      if (threadIdx.x == 0) {
+        release_add(P.pdone + (grp * 8 + rank) * 32, 1u);
+        if (pending) {
+          spin_until(r0f, (unsigned)(G * (t + 2)));
+          load_h0(t + 1);
+          pending = false;
+        }
+      }
+      TR(t, 4);
+    }
+  } else {
+    // ------------------------------------------------------------ recurrence R0_k / R1_k
+    const int li = role == 0 ? 0 : 1;
+    __half* Hs = P.Hs[li];
+    float* Cst = P.C[li];
+    __half* gts = P.gates[li];
+    const float* Gx = li == 0 ? P.Gx0 : P.a1x;
+    const unsigned* pf = P.pdone + (grp * 8 + rank) * 32;
+    float creg[NCI * 4];
+#pragma unroll
+    for (int i = 0; i < NCI * 4; ++i) creg[i] = 0.f;
+    float* myAct = sAct + warp * 16 * ACT_LD;
+    const float gsc = gate == 2 ? 2.f : 1.f;
+    for (int t = 0; t < T; ++t) {
+      TR(t, 0);
+      float gx[NCI][16];
+      if (li == 1) {
+        if (lane == 0) spin_until(pf, (unsigned)(t + 1));  // a1x_t of my gate rows stored by P_k
+        __syncwarp();
+      }
+#pragma unroll
+      for (int ci = 0; ci < NCI; ++ci) {
+        const int ch = ci * cgN + cg;
+        const bool ok = ch < nchunk && grow < fourhp;
+        const float* gp = Gx + ((size_t)t * B + col0 + ch * 16) * fourhp + grow;
+        if (li == 0) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) gx[ci][k] = ok ? __ldg(gp + (size_t)k * fourhp) : 0.f;
+        } else {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) gx[ci][k] = ok ? __ldcg(gp + (size_t)k * fourhp) : 0.f;
+        }
+      }
+      if (t > 0) {
+        const int p = (t - 1) & 1;
+        if (lane == 0 && warp < nis) {
+          ptx::mbar_wait(fullH + p, fphase[p]);
+          ptx::tc_fence_after();
+          TR(t, 1);
+          issue_mma(p);
+        }
+        __syncwarp();
+        ptx::mbar_wait(barM, (t - 1) & 1);
+        ptx::tc_fence_after();
+        fphase[p] ^= 1u;
+        if (threadIdx.x == 0 && t + 2 <= T - 1) ptx::mbar_arrive_expect_tx(fullH + p, total_bytes);
+      }
+      TR(t, 2);
+      __half* hout = Hs + (size_t)(t + 1) * B * hp;
+      float* cout = Cst + (size_t)t * B * hp;
+      __half* gout = gts + (size_t)t * B * fourhp;
+      uint8_t* stg = sX + (t & 1) * Bc * 128;
+#pragma unroll
+      for (int ci = 0; ci < NCI; ++ci) {
+        const int ch = ci * cgN + cg;
+        if (ch >= nchunk) break;
+        const int c0 = ch * 16;
+        float v[16];
+        if (t > 0) {
+          load_acc(v, c0);
+        } else {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) v[k] = 0.f;
+        }
+#pragma unroll
+        for (int k = 0; k < 16; ++k) myAct[k * ACT_LD + lane] = act_gate(v[k] + gx[ci][k], gsc);
+        __syncwarp();
+        if (unit_ok) {
+          const int u = lane >> 2;
+          const int ul = (r >> 2);
+          const int c = ul >> 3;
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int col = 4 * q + gate;
+            const float4 a4 = *reinterpret_cast<const float4*>(myAct + col * ACT_LD + 4 * u);
+            const int bl = c0 + col;
+            const size_t b = (size_t)col0 + bl;
+            const float i = a4.x, f = a4.y, g = a4.z, o = a4.w;
+            const float cv = f * creg[ci * 4 + q] + i * g;
+            creg[ci * 4 + q] = cv;
+            const __half hh = __float2half_rn(o * act_gate(cv, 2.f));
+            cout[b * hp + unit] = cv;                   // R5
+            hout[b * hp + unit] = hh;                   // R6
+            *reinterpret_cast<__half*>(stg + bl * 128 + ((c ^ (bl & 7)) << 4) + (ul & 7) * 2) = hh;
+            __align__(8) __half2 gg[2] = {__halves2half2(__float2half_rn(i), __float2half_rn(f)),
+                                          __halves2half2(__float2half_rn(g), __float2half_rn(o))};
+            *reinterpret_cast<uint2*>(gout + b * fourhp + 4 * unit) = *reinterpret_cast<const uint2*>(gg);  // R4
+          }
+        }
+        __syncwarp();
+      }
+      ptx::tc_fence_before();
+      ptx::fence_async_smem();
+      if (li == 0) fence_proxy_async();  // Hs0 stores -> P's TMA reads
+      __syncthreads();
+      TR(t, 3);
+      if (li == 0 && threadIdx.x == blockDim.x - 32) {  // neither a pusher nor an MMA issuer:
+                                                        // the release waits for the stores to drain
+        release_add(P.r0done + grp * 32, 1u);
+      }
+      if (t < T - 1 && threadIdx.x < G) {
+        const int dst = threadIdx.x;
+        const uint32_t dsta = ptx::mapa(sH_addr + (t & 1) * hbuf + rank * Bc * 128, dst);
+        const uint32_t mb = ptx::mapa(ptx::smem_u32(fullH + (t & 1)), dst);
+        ptx::bulk_copy_to_peer(dsta, sX_addr + (t & 1) * Bc * 128, Bc * 128, mb);
+      }
+      TR(t, 4);
+    }
+  }
+#undef TR
+  ptx::cluster_arrive();
+  ptx::cluster_wait();
+  ptx::tc_fence_after();
+  if (warp == 2) ptx::tmem_dealloc(tbase, tcols);
+}
+
 size_t recur2_fwd_smem(int hp, int Bc) {
   const int nkb = (hp + 63) / 64;
   return 1024 + 2 * (size_t)nkb * 16384 + 2 * (size_t)nkb * Bc * 128 + 2 * (size_t)Bc * 128 +
@@ -1712,9 +2021,74 @@ cudaError_t launch_recur_bwd(const RecurBwdArgs& a, cudaStream_t s) {
 
 namespace hdp {
 
+// split-cluster forward wavefront plan: largest batch-group count whose 3 x G x nbg
+// CTAs fit on the GPU as co-resident clusters (cached per shape)
+struct W2Plan {
+  int Bc = 0, nbg = 0, cgN = 0, nci = 0;
+};
+const void* recur2f_fn(int nci) {
+  return nci == 1 ? (const void*)recur2f_kernel<1> : nci == 2 ? (const void*)recur2f_kernel<2> : nullptr;
+}
+bool plan_w2f(int B, int hp, W2Plan* out) {
+  static std::map<std::pair<int, int>, W2Plan> cache;
+  auto key = std::make_pair(B, hp);
+  auto it = cache.find(key);
+  if (it != cache.end()) {
+    *out = it->second;
+    return out->nbg > 0;
+  }
+  W2Plan best;
+  const int G = (hp + 63) / 64;
+  if (B >= 16 && !(B & 15) && !(hp & 15) && G <= 8) {
+    for (int nbg = 16; nbg >= 1 && !best.nbg; nbg >>= 1) {
+      if (B % nbg) continue;
+      const int Bc = B / nbg;
+      if ((Bc & 15) || Bc > 32 || 3 * G * nbg > 148) continue;
+      W2Plan p;
+      p.Bc = Bc;
+      p.nbg = nbg;
+      p.cgN = Bc / 16;
+      p.nci = 1;
+      const size_t smem = fwd_cl_smem(hp, Bc, 8 * p.cgN);
+      if (smem > 227 * 1024) continue;
+      const void* fn = recur2f_fn(p.nci);
+      if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) break;
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3(G, 3 * nbg);
+      cfg.blockDim = dim3(256 * p.cgN);
+      cfg.dynamicSmemBytes = smem;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeClusterDimension;
+      at[0].val.clusterDim.x = G;
+      at[0].val.clusterDim.y = 1;
+      at[0].val.clusterDim.z = 1;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      int ncl = 0;
+      if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess) {
+        (void)cudaGetLastError();
+        continue;
+      }
+      if (ncl >= 3 * nbg) best = p;
+    }
+  }
+  cache[key] = best;
+  *out = best;
+  return best.nbg > 0;
+}
+
+bool w2f_split_enabled() {
+  const char* e = getenv("HDP_WAVEFRONT_FWD");
+  return !(e && e[0] == '1');  // HDP_WAVEFRONT_FWD=1: the single-cluster variant
+}
+
 bool recur2_fwd_supported(int B, int hp) {
   const char* e = getenv("HDP_WAVEFRONT");
   if (e && e[0] == '0') return false;
+  if (w2f_split_enabled()) {
+    W2Plan p;
+    return plan_w2f(B, hp, &p);
+  }
   if (B % 32 || (hp & 15) || hp > 256) return false;
   const int G = (hp + 63) / 64;
   if (3 * G > 16) return false;
@@ -1724,6 +2098,45 @@ bool recur2_fwd_supported(int B, int hp) {
 
 cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
   if (!recur2_fwd_supported(a.B, a.hp)) return cudaErrorInvalidConfiguration;
+  if (w2f_split_enabled()) {
+    W2Plan pl;
+    plan_w2f(a.B, a.hp, &pl);
+    const int G = (a.hp + 63) / 64;
+    const uint64_t hp = a.hp;
+    Fwd2Params P;
+    memset(&P, 0, sizeof P);
+    const __half* As[3] = {a.U0, a.W1, a.U1};
+    for (int i = 0; i < 3; ++i)
+      if (encode_tmap_2d(&P.tmA[i], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, As[i], hp, 4 * hp, hp * 2, 64, 128,
+                         CU_TENSOR_MAP_SWIZZLE_128B))
+        return cudaErrorInvalidValue;
+    if (encode_tmap_2d(&P.tmH0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.Hs0, hp, (uint64_t)(a.T + 1) * a.B, hp * 2, 64,
+                       pl.Bc, CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+    P.Gx0 = a.Gx0;
+    P.a1x = a.a1x;
+    P.b1 = a.b1;
+    P.Hs[0] = a.Hs0;
+    P.Hs[1] = a.Hs1;
+    P.C[0] = a.C0;
+    P.C[1] = a.C1;
+    P.gates[0] = a.gates0;
+    P.gates[1] = a.gates1;
+    P.r0done = a.flags;
+    P.pdone = a.flags + 16 * 32;
+    P.trace = a.trace;
+    P.T = a.T;
+    P.B = a.B;
+    P.Bc = pl.Bc;
+    P.hp = a.hp;
+    P.nbg = pl.nbg;
+    if (!a.a1x || !a.flags) return cudaErrorInvalidValue;
+    cudaError_t e = cudaMemsetAsync(a.flags, 0, (16 * 32 + 16 * 8 * 32) * sizeof(unsigned), s);
+    if (e != cudaSuccess) return e;
+    void* args[] = {&P};
+    return launch_cluster(recur2f_fn(pl.nci), dim3(G, 3 * pl.nbg), dim3(256 * pl.cgN),
+                          fwd_cl_smem(a.hp, pl.Bc, 8 * pl.cgN), G, s, args);
+  }
   CUtensorMap mU0, mW1, mU1;
   const uint64_t hp = a.hp;
   if (encode_tmap_2d(&mU0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U0, hp, 4 * hp, hp * 2, 64, 128,
@@ -1779,19 +2192,66 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
 
 namespace hdp {
 
+const void* recur2b_fn(int Bc) {
+  return Bc == 16 ? (const void*)recur2_bwd_kernel<1>
+       : Bc == 32 ? (const void*)recur2_bwd_kernel<2>
+       : Bc == 48 ? (const void*)recur2_bwd_kernel<3> : (const void*)recur2_bwd_kernel<4>;
+}
+
+// backward wavefront plan: largest batch-group count whose 3 x G x nbg CTAs are
+// co-resident as G-CTA clusters (every role waits on the others); cached per shape
+bool plan_w2b(int B, int hp, int* Bc_out, int* nbg_out) {
+  static std::map<std::pair<int, int>, std::pair<int, int>> cache;
+  auto key = std::make_pair(B, hp);
+  auto it = cache.find(key);
+  if (it == cache.end()) {
+    std::pair<int, int> best(0, 0);
+    const int G = (hp + 63) / 64;
+    if (B >= 16 && !(B & 15) && !(hp & 15) && G <= 8) {
+      for (int nbg = 16; nbg >= 1 && !best.second; nbg >>= 1) {
+        if (B % nbg) continue;
+        const int Bc = B / nbg;
+        if ((Bc & 15) || Bc > 64 || 3 * G * nbg > 148) continue;
+        const size_t smem = bwd_cl_smem(hp, Bc);
+        if (smem > 227 * 1024) continue;
+        const void* fn = recur2b_fn(Bc);
+        if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) break;
+        cudaLaunchConfig_t cfg = {};
+        cfg.gridDim = dim3(G, 3 * nbg);
+        cfg.blockDim = dim3(128);
+        cfg.dynamicSmemBytes = smem;
+        cudaLaunchAttribute at[1];
+        at[0].id = cudaLaunchAttributeClusterDimension;
+        at[0].val.clusterDim.x = G;
+        at[0].val.clusterDim.y = 1;
+        at[0].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 1;
+        int ncl = 0;
+        if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess) {
+          (void)cudaGetLastError();
+          continue;
+        }
+        if (ncl >= 3 * nbg) best = std::make_pair(Bc, nbg);
+      }
+    }
+    it = cache.emplace(key, best).first;
+  }
+  *Bc_out = it->second.first;
+  *nbg_out = it->second.second;
+  return it->second.second > 0;
+}
+
 bool recur2_bwd_supported(int B, int hp) {
   const char* e = getenv("HDP_WAVEFRONT");
   if (e && e[0] == '0') return false;
   int Bc = 0, nbg = 0;
-  if (!plan_bwd(B, hp, &Bc, &nbg)) return false;
-  const int G = (hp + 63) / 64;
-  if (G > 8 || 3 * G * nbg > 148 || nbg > 16) return false;
-  return bwd_cl_smem(hp, Bc) <= 227 * 1024;
+  return plan_w2b(B, hp, &Bc, &nbg);
 }
 
 cudaError_t launch_recur2_bwd(const Recur2BwdArgs& a, cudaStream_t s) {
   int Bc = 0, nbg = 0;
-  if (!recur2_bwd_supported(a.B, a.hp) || !plan_bwd(a.B, a.hp, &Bc, &nbg)) return cudaErrorInvalidConfiguration;
+  if (!recur2_bwd_supported(a.B, a.hp) || !plan_w2b(a.B, a.hp, &Bc, &nbg)) return cudaErrorInvalidConfiguration;
   const int G = (a.hp + 63) / 64;
   const uint64_t hp = a.hp;
   Bwd2Params P;
@@ -1816,30 +2276,8 @@ cudaError_t launch_recur2_bwd(const Recur2BwdArgs& a, cudaStream_t s) {
   P.nbg = nbg;
   cudaError_t e = cudaMemsetAsync(a.flags, 0, (16 * 32 + 16 * 8 * 32) * sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
-  const void* fn = Bc == 16 ? (const void*)recur2_bwd_kernel<1>
-                 : Bc == 32 ? (const void*)recur2_bwd_kernel<2>
-                 : Bc == 48 ? (const void*)recur2_bwd_kernel<3> : (const void*)recur2_bwd_kernel<4>;
-  // all CTAs wait on each other through global counters: they must be co-resident
-  {
-    e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bwd_cl_smem(a.hp, Bc));
-    if (e != cudaSuccess) return e;
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(G, 3 * nbg);
-    cfg.blockDim = dim3(128);
-    cfg.dynamicSmemBytes = bwd_cl_smem(a.hp, Bc);
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = G;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, fn, &cfg) != cudaSuccess || nclusters < 3 * nbg)
-      return cudaErrorCooperativeLaunchTooLarge;
-  }
   void* args[] = {&P};
-  return launch_cluster(fn, dim3(G, 3 * nbg), dim3(128), bwd_cl_smem(a.hp, Bc), G, s, args);
+  return launch_cluster(recur2b_fn(Bc), dim3(G, 3 * nbg), dim3(128), bwd_cl_smem(a.hp, Bc), G, s, args);
 }
 
 }  // namespace hdp

@@ -42,6 +42,8 @@ struct Recur2FwdArgs {
   __half *gates0 = nullptr, *gates1 = nullptr;
   int T = 0, B = 0, hp = 0;
   unsigned long long* trace = nullptr;  // debug: [3 roles][T][5] timestamps, nullable
+  float* a1x = nullptr;                 // [T][B][4hp] layer-1 G_x scratch (split-cluster variant)
+  unsigned* flags = nullptr;            // >= 16*32 + 16*8*32 uints (split-cluster variant)
 };
 bool recur2_fwd_supported(int B, int hp);
 
