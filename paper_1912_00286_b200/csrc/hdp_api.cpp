@@ -475,9 +475,12 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
     char* Hs = S.Hs + l * hs_layer * e;
     float* Cl = S.C + l * c_layer;
     char* Gl = S.gates + l * g_layer * e;
-    // K1: G_x = X W^T + b for all t (A1)
-    CK(gemm(c, HDP_K_GEMM_X, X, Ipl, 0, c->W(iW), Ipl, 0, rows, 4 * hp, Ipl, epi_f32(c->Gx, 4 * hp, c->W(ib), !f32), s));
-    if (l == 0 && L == 2 && !f32 && c->persistent && hdp::recur2_fwd_supported(B, (int)hp)) {
+    const bool wave = l == 0 && L == 2 && !f32 && c->persistent && hdp::recur2_fwd_supported(B, (int)hp);
+    const bool fusex = wave && hdp::recur2_fwd_fuses_x(B, (int)hp, (int)Ipl);
+    // K1: G_x = X W^T + b for all t (A1); inside the wavefront's layer-0 role when fused
+    if (!fusex)
+      CK(gemm(c, HDP_K_GEMM_X, X, Ipl, 0, c->W(iW), Ipl, 0, rows, 4 * hp, Ipl, epi_f32(c->Gx, 4 * hp, c->W(ib), !f32), s));
+    if (wave) {
       // both layers' recurrences as one wavefront; layer 1's input projection runs inside
       hdp::Recur2FwdArgs ra;
       ra.U0 = (const __half*)c->W(iU);
@@ -485,6 +488,12 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
       ra.U1 = (const __half*)c->W(c->find("U1"));
       ra.b1 = (const __half*)c->W(c->find("b1"));
       ra.Gx0 = c->Gx;
+      if (fusex) {
+        ra.X0 = (const __half*)X;
+        ra.W0 = (const __half*)c->W(iW);
+        ra.b0 = (const __half*)c->W(ib);
+        ra.Ip0 = (int)Ipl;
+      }
       ra.a1x = c->Gx1;
       ra.flags = (unsigned*)((char*)c->status + 4096);
       ra.Hs0 = (__half*)Hs;
@@ -499,7 +508,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
       static unsigned long long* w2trace = nullptr;  // debug: HDP_RECUR_TRACE=1 in profile (eager) mode
       const bool want_trace = c->prof && getenv("HDP_RECUR_TRACE") && getenv("HDP_RECUR_TRACE")[0] == '1';
       if (want_trace) {
-        if (!w2trace) CK_CUDA(cudaMalloc(&w2trace, 3 * 8192 * 5 * sizeof(unsigned long long)));
+        if (!w2trace) CK_CUDA(cudaMalloc(&w2trace, 4 * 8192 * 5 * sizeof(unsigned long long)));
         ra.trace = w2trace;
       }
       {
@@ -507,7 +516,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
         CK_CUDA(hdp::launch_recur2_fwd(ra, s));
       }
       if (want_trace && T <= 8192) {
-        std::vector<unsigned long long> h((size_t)3 * T * 5);
+        std::vector<unsigned long long> h((size_t)4 * T * 5);
         CK_CUDA(cudaStreamSynchronize(s));
         CK_CUDA(cudaMemcpy(h.data(), w2trace, h.size() * 8, cudaMemcpyDeviceToHost));
         const unsigned long long t00 = h[0];
@@ -525,6 +534,20 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
           fprintf(stderr, "[hdp trace] wavefront %s: per step ns: %.0f %.0f %.0f %.0f | step %.0f | t=1 starts at +%.0f ns, t=T-1 ends at +%.0f\n",
                   names[role], ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, step / n, (double)(st[0] - t00),
                   (double)(h[((size_t)role * T + T - 1) * 5 + 4] - t00));
+        }
+        {
+          double sp = 0, li = 0, mw = 0;
+          int n = 0;
+          for (int t = 2; t < T - 1; ++t) {
+            const unsigned long long* r = &h[((size_t)3 * T + t) * 5];
+            sp += (double)(r[1] - r[0]);
+            li += (double)(r[2] - r[1]);
+            mw += (double)(r[3] - r[2]);
+            ++n;
+          }
+          fprintf(stderr, "[hdp trace] wavefront R1 (thread 0): after MMA issue -> a1x fetch %.0f ns -> barM %.0f ns\n",
+                  li / n, mw / n);
+          (void)sp;
         }
       }
       break;

@@ -1641,16 +1641,21 @@ __global__ void __launch_bounds__(BC * 16, 1)
 struct __align__(64) Fwd2Params {
   CUtensorMap tmA[3];  // resident A slices (K-major, box 64 x 128): U0, W1, U1
   CUtensorMap tmH0;    // Hs0 rows [(T+1)B][hp], box (64, Bc): P's B operand
+  CUtensorMap tmW0;    // W0 [4hp][Ip0], box 64 x 128 (fused layer-0 input projection)
+  CUtensorMap tmX0;    // X0 rows [T B][Ip0], box (64, Bc)
+  CUtensorMap tmG1;    // a1x rows [T B][4hp] fp32, box (256, Bc): R1's gate inputs (r1_tma)
   const float* Gx0;    // [T][B][4hp]
   float* a1x;          // [T][B][4hp]
   const __half* b1;
+  const __half* b0;    // fused input projection: G_x0 = X0 W0^T + b0 inside R0 (fuse_x)
   __half* Hs[2];
   float* C[2];
   __half* gates[2];
   unsigned* r0done;    // [16][32]
   unsigned* pdone;     // [16][8][32]
   unsigned long long* trace;
-  int T, B, Bc, hp, nbg;
+  int T, B, Bc, hp, nbg, fuse_x, r1_tma;
+  int region;          // the 32 KB + 2 x Bc x 128 B region (fused projection / R1 staging) exists
 };
 
 __device__ __forceinline__ void spin_until(const unsigned* f, unsigned target) {
@@ -1675,13 +1680,17 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
   uint8_t* sU = smem;                         // [2 halves][nkb][16 KB]
   uint8_t* sH = sU + 2 * nkb * 16384;         // [2][hbuf]
   uint8_t* sX = sH + 2 * hbuf;                // [2][Bc][128 B]
-  float* sAct = reinterpret_cast<float*>(sX + 2 * Bc * 128);
+  uint8_t* sW0 = sX + 2 * Bc * 128;           // R0, fuse_x: [2 halves][16 KB] W0 slice (Ip0 <= 64)
+                                              // R1, r1_tma: [2][Bc][256] fp32 a1x staging
+  uint8_t* sXin = sW0 + (P.region ? 32768 : 0);  // R0, fuse_x: [2][Bc][128 B] x_t operand
+  float* sAct = reinterpret_cast<float*>(sXin + (P.region ? 2 * Bc * 128 : 0));
   uint64_t* bars = reinterpret_cast<uint64_t*>(sAct + nwarps * 16 * ACT_LD);
   uint64_t* barU = bars;
   uint64_t* barM = bars + 1;
   uint64_t* fullH = bars + 2;                 // [2]
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
-
+  uint64_t* barX = bars + 4;                  // [2] x_t landed (fuse_x)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 6);
+  const bool fx = role == 0 && P.fuse_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int quarter = warp & 3, hf = (warp >> 2) & 1, cg = warp >> 3;
   const int G = gridDim.x;
@@ -1710,6 +1719,8 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
     ptx::mbar_init(barM, nis);
     ptx::mbar_init(fullH, 1);
     ptx::mbar_init(fullH + 1, 1);
+    ptx::mbar_init(barX, 1);
+    ptx::mbar_init(barX + 1, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc(tslot, tcols);
@@ -1722,10 +1733,15 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
       ptx::mbar_arrive_expect_tx(fullH, total_bytes);
       ptx::mbar_arrive_expect_tx(fullH + 1, total_bytes);
     }
-    ptx::mbar_arrive_expect_tx(barU, 2 * nkb * 16384);
+    ptx::mbar_arrive_expect_tx(barU, 2 * nkb * 16384 + (fx ? 32768 : 0));
     for (int h2 = 0; h2 < 2; ++h2)
       for (int kb = 0; kb < nkb; ++kb)
         ptx::tma_load_2d(sU + (h2 * nkb + kb) * 16384, &P.tmA[role], barU, kb * 64, row0 + h2 * 128);
+    if (fx) {
+      for (int h2 = 0; h2 < 2; ++h2) ptx::tma_load_2d(sW0 + h2 * 16384, &P.tmW0, barU, 0, row0 + h2 * 128);
+      ptx::mbar_arrive_expect_tx(barX, Bc * 128);
+      ptx::tma_load_2d(sXin, &P.tmX0, barX, 0, col0);
+    }
     ptx::mbar_wait(barU, 0);
   }
   ptx::cluster_arrive();
@@ -1735,7 +1751,7 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
   const int nchunk = Bc / 16;
   const uint32_t sH_addr = ptx::smem_u32(sH), sX_addr = ptx::smem_u32(sX);
   uint32_t fphase[2] = {0u, 0u};
-  auto issue_mma = [&](int p) {
+  auto issue_mma = [&](int p) {  // fx: accumulator 0 already holds x_t W0^T
     const uint32_t aU = ptx::smem_u32(sU), aH = sH_addr + p * hbuf;
     const uint64_t ad0 = ptx::smem_desc_sw128(aU, 0, 1024), bd0 = ptx::smem_desc_sw128(aH, 0, 1024);
     for (int k = warp; k < nk16; k += nis) {
@@ -1744,15 +1760,15 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
 #pragma unroll
       for (int h2 = 0; h2 < 2; ++h2) {
         const uint64_t ad = ad0 + (uint64_t)(((h2 * nkb + kb) * 16384 + kk * 32) >> 4);
-        ptx::mma_f16(tbase + (h2 * nacc + warp) * Bc, ad, bd, idesc, k >= nis ? 1u : 0u);
+        ptx::mma_f16(tbase + (h2 * nacc + warp) * Bc, ad, bd, idesc, (k >= nis || (fx && warp == 0)) ? 1u : 0u);
       }
     }
     ptx::mma_commit(barM);
   };
-  auto load_acc = [&](float (&v)[16], int c0) {
+  auto load_acc = [&](float (&v)[16], int c0, int nacc_used) {
     const uint32_t ta = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + hf * nacc * Bc + c0;
     ptx::tmem_ld16(ta, v);
-    for (int a = 1; a < nis; ++a) {
+    for (int a = 1; a < nacc_used; ++a) {
       float w[16];
       ptx::tmem_ld16(ta + a * Bc, w);
 #pragma unroll
@@ -1800,7 +1816,7 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
         const int ch = ci * cgN + cg;
         if (ch >= nchunk) break;
         float v[16];
-        load_acc(v, ch * 16);
+        load_acc(v, ch * 16, nis);
         if (grow < fourhp) {
           float* out = P.a1x + ((size_t)t * B + col0 + ch * 16) * fourhp + grow;
 #pragma unroll
@@ -1808,6 +1824,7 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
         }
       }
       ptx::tc_fence_before();
+      fence_proxy_async();  // a1x stores -> R1's TMA reads
       __syncthreads();
       TR(t, 3);
       if (threadIdx.x == 0) {
@@ -1828,14 +1845,30 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
     __half* gts = P.gates[li];
     const float* Gx = li == 0 ? P.Gx0 : P.a1x;
     const unsigned* pf = P.pdone + (grp * 8 + rank) * 32;
+    // r1_tma: a1x_t (my 256 gate rows x Bc) staged by TMA into the (otherwise unused)
+    // fused-projection region, double-buffered, barX[t & 1] -- one thread acquires
+    const bool gt = li == 1 && P.r1_tma;
+    const float* sG1 = reinterpret_cast<const float*>(sW0);
+    auto fetch_a1x = [&](int t) {  // thread 0
+      spin_until(pf, (unsigned)(t + 1));
+      fence_proxy_async();
+      ptx::mbar_arrive_expect_tx(barX + (t & 1), Bc * 256 * 4);
+      ptx::tma_load_2d(sW0 + (t & 1) * Bc * 1024, &P.tmG1, barX + (t & 1), row0, t * B + col0);
+    };
+    if (gt && threadIdx.x == 0) fetch_a1x(0);
     float creg[NCI * 4];
 #pragma unroll
     for (int i = 0; i < NCI * 4; ++i) creg[i] = 0.f;
     float* myAct = sAct + warp * 16 * ACT_LD;
     const float gsc = gate == 2 ? 2.f : 1.f;
-    for (int t = 0; t < T; ++t) {
-      TR(t, 0);
-      float gx[NCI][16];
+    const float bias0 = fx && unit_ok ? __half2float(P.b0[grow]) : 0.f;
+    uint32_t mph = 0;
+    // gate inputs of step t (layer 0: G_x0 rows from K1, or the bias when the projection
+    // is fused; layer 1: a1x rows from P_k once published), loaded one step ahead so
+    // the flag acquire and the L2 latency overlap the previous step's MMA
+    float gx[NCI][16], gxn[NCI][16];
+    auto load_gx = [&](int t, float (&dst)[NCI][16]) {
+      if (gt) return;
       if (li == 1) {
         if (lane == 0) spin_until(pf, (unsigned)(t + 1));  // a1x_t of my gate rows stored by P_k
         __syncwarp();
@@ -1845,14 +1878,42 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
         const int ch = ci * cgN + cg;
         const bool ok = ch < nchunk && grow < fourhp;
         const float* gp = Gx + ((size_t)t * B + col0 + ch * 16) * fourhp + grow;
-        if (li == 0) {
+        if (fx) {
 #pragma unroll
-          for (int k = 0; k < 16; ++k) gx[ci][k] = ok ? __ldg(gp + (size_t)k * fourhp) : 0.f;
+          for (int k = 0; k < 16; ++k) dst[ci][k] = bias0;
+        } else if (li == 0) {
+#pragma unroll
+          for (int k = 0; k < 16; ++k) dst[ci][k] = ok ? __ldg(gp + (size_t)k * fourhp) : 0.f;
         } else {
 #pragma unroll
-          for (int k = 0; k < 16; ++k) gx[ci][k] = ok ? __ldcg(gp + (size_t)k * fourhp) : 0.f;
+          for (int k = 0; k < 16; ++k) dst[ci][k] = ok ? __ldcg(gp + (size_t)k * fourhp) : 0.f;
         }
       }
+    };
+    // layer 0 with G_x0 from K1: loads one step ahead (NCI = 1; the 512-thread variant's
+    // register budget keeps them in-step)
+    const bool PIPE = NCI == 1 && li == 0 && !fx;
+    if (PIPE) load_gx(0, gx);
+    for (int t = 0; t < T; ++t) {
+      TR(t, 0);
+      if (!PIPE) load_gx(t, gx);
+      if (fx && warp == 0 && lane == 0) {
+        // x_t W0^T into accumulator 0 (both halves) -- off the recurrence's critical path
+        ptx::mbar_wait(barX + (t & 1), (t >> 1) & 1);
+        ptx::tc_fence_after();
+        const uint64_t bd = ptx::smem_desc_sw128(ptx::smem_u32(sXin + (t & 1) * Bc * 128), 0, 1024);
+#pragma unroll
+        for (int h2 = 0; h2 < 2; ++h2)
+          ptx::mma_f16(tbase + (h2 * nacc) * Bc, ptx::smem_desc_sw128(ptx::smem_u32(sW0 + h2 * 16384), 0, 1024), bd,
+                       idesc, 0u);
+        // x_{t+1}: its slot was last read by the x MMA of step t-1 (complete)
+        if (t + 1 < T) {
+          ptx::mbar_arrive_expect_tx(barX + ((t + 1) & 1), Bc * 128);
+          ptx::tma_load_2d(sXin + ((t + 1) & 1) * Bc * 128, &P.tmX0, barX + ((t + 1) & 1), 0, (t + 1) * B + col0);
+        }
+        if (t == 0) ptx::mma_commit(barM);
+      }
+      if (fx && t == 0 && lane == 0 && warp > 0 && warp < nis) ptx::mbar_arrive(barM);
       if (t > 0) {
         const int p = (t - 1) & 1;
         if (lane == 0 && warp < nis) {
@@ -1860,14 +1921,37 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
           ptx::tc_fence_after();
           TR(t, 1);
           issue_mma(p);
+          if (tr && li == 1) P.trace[(size_t)3 * T * 5 + t * 5 + 0] = ptx::globaltimer_ns();
+          if (gt && threadIdx.x == 0 && t + 1 < T) fetch_a1x(t + 1);
+          if (tr && li == 1) P.trace[(size_t)3 * T * 5 + t * 5 + 1] = ptx::globaltimer_ns();
         }
+        if (PIPE && t + 1 < T) load_gx(t + 1, gxn);
         __syncwarp();
-        ptx::mbar_wait(barM, (t - 1) & 1);
+        ptx::mbar_wait(barM, mph);
+        if (tr && li == 1) P.trace[(size_t)3 * T * 5 + t * 5 + 2] = ptx::globaltimer_ns();
+        mph ^= 1u;
         ptx::tc_fence_after();
         fphase[p] ^= 1u;
         if (threadIdx.x == 0 && t + 2 <= T - 1) ptx::mbar_arrive_expect_tx(fullH + p, total_bytes);
+      } else {
+        if (PIPE && t + 1 < T) load_gx(t + 1, gxn);
+        if (gt && threadIdx.x == 0 && t + 1 < T) fetch_a1x(t + 1);
+        if (fx) {
+          __syncwarp();
+          ptx::mbar_wait(barM, mph);
+          mph ^= 1u;
+          ptx::tc_fence_after();
+        }
       }
       TR(t, 2);
+      if (gt) {
+        ptx::mbar_wait(barX + (t & 1), (t >> 1) & 1);
+        const float* g = sG1 + (t & 1) * Bc * 256;
+#pragma unroll
+        for (int ci = 0; ci < NCI; ++ci)
+#pragma unroll
+          for (int k = 0; k < 16; ++k) gx[ci][k] = g[((ci * cgN + cg) * 16 + k) * 256 + r];
+      }
       __half* hout = Hs + (size_t)(t + 1) * B * hp;
       float* cout = Cst + (size_t)t * B * hp;
       __half* gout = gts + (size_t)t * B * fourhp;
@@ -1878,8 +1962,8 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
         if (ch >= nchunk) break;
         const int c0 = ch * 16;
         float v[16];
-        if (t > 0) {
-          load_acc(v, c0);
+        if (t > 0 || fx) {
+          load_acc(v, c0, t > 0 ? nis : 1);
         } else {
 #pragma unroll
           for (int k = 0; k < 16; ++k) v[k] = 0.f;
@@ -1916,6 +2000,12 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
       if (li == 0) fence_proxy_async();  // Hs0 stores -> P's TMA reads
       __syncthreads();
       TR(t, 3);
+      if (PIPE) {
+#pragma unroll
+        for (int ci = 0; ci < NCI; ++ci)
+#pragma unroll
+          for (int k = 0; k < 16; ++k) gx[ci][k] = gxn[ci][k];
+      }
       if (li == 0 && threadIdx.x == blockDim.x - 32) {  // neither a pusher nor an MMA issuer:
                                                         // the release waits for the stores to drain
         release_add(P.r0done + grp * 32, 1u);
@@ -2023,8 +2113,11 @@ namespace hdp {
 
 // split-cluster forward wavefront plan: largest batch-group count whose 3 x G x nbg
 // CTAs fit on the GPU as co-resident clusters (cached per shape)
+// extra shared memory of the fused layer-0 input projection (W0 slice + x_t double buffer)
+size_t w2f_fuse_bytes(int Bc) { return 32768 + 2 * (size_t)Bc * 128; }
+
 struct W2Plan {
-  int Bc = 0, nbg = 0, cgN = 0, nci = 0;
+  int Bc = 0, nbg = 0, cgN = 0, nci = 0, fuse = 0;
 };
 const void* recur2f_fn(int nci) {
   return nci == 1 ? (const void*)recur2f_kernel<1> : nci == 2 ? (const void*)recur2f_kernel<2> : nullptr;
@@ -2049,8 +2142,13 @@ bool plan_w2f(int B, int hp, W2Plan* out) {
       p.nbg = nbg;
       p.cgN = Bc / 16;
       p.nci = 1;
-      const size_t smem = fwd_cl_smem(hp, Bc, 8 * p.cgN);
+      size_t smem = fwd_cl_smem(hp, Bc, 8 * p.cgN);
       if (smem > 227 * 1024) continue;
+      const char* fe = getenv("HDP_WAVEFRONT_FUSEX");
+      if (!(fe && fe[0] == '0') && smem + w2f_fuse_bytes(Bc) <= 227 * 1024) {
+        smem += w2f_fuse_bytes(Bc);
+        p.fuse = 1;
+      }
       const void* fn = recur2f_fn(p.nci);
       if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) break;
       cudaLaunchConfig_t cfg = {};
@@ -2080,6 +2178,12 @@ bool plan_w2f(int B, int hp, W2Plan* out) {
 bool w2f_split_enabled() {
   const char* e = getenv("HDP_WAVEFRONT_FWD");
   return !(e && e[0] == '1');  // HDP_WAVEFRONT_FWD=1: the single-cluster variant
+}
+
+bool recur2_fwd_fuses_x(int B, int hp, int Ip0) {
+  W2Plan p;
+  return recur2_fwd_supported(B, hp) && w2f_split_enabled() && plan_w2f(B, hp, &p) && p.fuse && Ip0 <= 64 &&
+         !(getenv("HDP_WAVEFRONT_FUSEX") && getenv("HDP_WAVEFRONT_FUSEX")[0] == '0');
 }
 
 bool recur2_fwd_supported(int B, int hp) {
@@ -2130,12 +2234,29 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
     P.Bc = pl.Bc;
     P.hp = a.hp;
     P.nbg = pl.nbg;
+    P.fuse_x = a.X0 != nullptr;
+    if (P.fuse_x) {
+      if (!recur2_fwd_fuses_x(a.B, a.hp, a.Ip0) || !a.W0 || !a.b0) return cudaErrorInvalidValue;
+      if (encode_tmap_2d(&P.tmW0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.W0, a.Ip0, 4 * hp, (uint64_t)a.Ip0 * 2, 64, 128,
+                         CU_TENSOR_MAP_SWIZZLE_128B) ||
+          encode_tmap_2d(&P.tmX0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.X0, a.Ip0, (uint64_t)a.T * a.B,
+                         (uint64_t)a.Ip0 * 2, 64, pl.Bc, CU_TENSOR_MAP_SWIZZLE_128B))
+        return cudaErrorInvalidValue;
+      P.b0 = a.b0;
+    } else if (!a.Gx0) {
+      return cudaErrorInvalidValue;
+    }
     if (!a.a1x || !a.flags) return cudaErrorInvalidValue;
+    P.region = pl.fuse;
+    P.r1_tma = pl.fuse && (size_t)2 * pl.Bc * 1024 <= w2f_fuse_bytes(pl.Bc);
+    if (P.r1_tma && encode_tmap_2d(&P.tmG1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.a1x, 4 * hp, (uint64_t)a.T * a.B,
+                                   4 * hp * 4, 256, pl.Bc, CU_TENSOR_MAP_SWIZZLE_NONE))
+      return cudaErrorInvalidValue;
     cudaError_t e = cudaMemsetAsync(a.flags, 0, (16 * 32 + 16 * 8 * 32) * sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
     void* args[] = {&P};
     return launch_cluster(recur2f_fn(pl.nci), dim3(G, 3 * pl.nbg), dim3(256 * pl.cgN),
-                          fwd_cl_smem(a.hp, pl.Bc, 8 * pl.cgN), G, s, args);
+                          fwd_cl_smem(a.hp, pl.Bc, 8 * pl.cgN) + (pl.fuse ? w2f_fuse_bytes(pl.Bc) : 0), G, s, args);
   }
   CUtensorMap mU0, mW1, mU1;
   const uint64_t hp = a.hp;

@@ -43,9 +43,14 @@ struct Recur2FwdArgs {
   int T = 0, B = 0, hp = 0;
   unsigned long long* trace = nullptr;  // debug: [3 roles][T][5] timestamps, nullable
   float* a1x = nullptr;                 // [T][B][4hp] layer-1 G_x scratch (split-cluster variant)
+  // fused layer-0 input projection (split variant, Ip0 <= 64): set X0 to have R0
+  // compute X0 W0^T + b0 itself (Gx0 unused); leave X0 null to read Gx0
+  const __half *X0 = nullptr, *W0 = nullptr, *b0 = nullptr;  // X0 [T][B][Ip0], W0 [4hp][Ip0]
+  int Ip0 = 0;
   unsigned* flags = nullptr;            // >= 16*32 + 16*8*32 uints (split-cluster variant)
 };
 bool recur2_fwd_supported(int B, int hp);
+bool recur2_fwd_fuses_x(int B, int hp, int Ip0);
 
 // Two stacked layers' BPTT as one wavefront: layer-1 recurrence, the input
 // gradient projection dX1 = dA1 W1, and the layer-0 recurrence (fed by dX1)
