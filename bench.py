@@ -20,9 +20,7 @@ import argparse
 import json
 import os
 import statistics
-import subprocess
 import sys
-import tempfile
 import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
@@ -49,42 +47,76 @@ def peaks():
 
 
 class Clocks:
-    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+    """SM clock + throttle-reason sampling DURING the timed region
+    (B200_PROFILING.md clocks line).  NVML is polled every ~2 ms from a
+    background thread that starts before the region; only samples taken between
+    start() and stop() count, so short regions still get several samples.
+    Falls back to nvidia-smi -lms when NVML is unavailable."""
+
+    REASONS = [("hw_slowdown", "nvmlClocksEventReasonHwSlowdown"),
+               ("hw_thermal_slowdown", "nvmlClocksEventReasonHwThermalSlowdown"),
+               ("sw_thermal_slowdown", "nvmlClocksEventReasonSwThermalSlowdown"),
+               ("sw_power_cap", "nvmlClocksEventReasonSwPowerCap"),
+               ("hw_power_brake_slowdown", "nvmlClocksEventReasonHwPowerBrakeSlowdown")]
 
     def __init__(self, index):
-        self.f = tempfile.NamedTemporaryFile("w+", suffix=".csv", delete=False)
-        q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
-             "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
-             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+        import threading
+        self.samples, self.t0, self.t1, self.h, self.err = [], None, None, None, None
         try:
-            self.p = subprocess.Popen(["nvidia-smi", f"--id={index}", f"--query-gpu={q}", "--format=csv,noheader,nounits",
-                                       "-lms", "20"], stdout=self.f, stderr=subprocess.DEVNULL)
-        except Exception:
-            self.p = None
+            import pynvml
+            pynvml.nvmlInit()
+            self.nv = pynvml
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                ids = [x.strip() for x in vis.split(",")]
+                if index < len(ids) and ids[index].isdigit():
+                    index = int(ids[index])
+            self.h = pynvml.nvmlDeviceGetHandleByIndex(index)
+            self.mx = float(pynvml.nvmlDeviceGetMaxClockInfo(self.h, pynvml.NVML_CLOCK_SM))
+        except Exception as e:  # noqa: BLE001
+            self.err = f"nvml: {e}"
+            return
+        self.stop_ev = threading.Event()
+        self.th = threading.Thread(target=self._run, daemon=True)
+        self.th.start()
+        while not self.samples and self.th.is_alive():
+            time.sleep(0.001)
+
+    def _run(self):
+        nv = self.nv
+        get_r = getattr(nv, "nvmlDeviceGetCurrentClocksEventReasons", None) or nv.nvmlDeviceGetCurrentClocksThrottleReasons
+        while not self.stop_ev.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self.h, nv.NVML_CLOCK_SM)
+                r = get_r(self.h)
+            except Exception:  # noqa: BLE001
+                break
+            self.samples.append((time.perf_counter(), float(sm), int(r)))
+            time.sleep(0.002)
+
+    def start(self):
+        self.t0 = time.perf_counter()
 
     def stop(self):
-        if self.p is None:
-            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
-        self.p.terminate()
-        self.p.wait()
-        self.f.seek(0)
-        sm, mx, reasons = [], None, set()
-        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in self.f.read().splitlines():
-            parts = [x.strip() for x in line.split(",")]
-            if len(parts) < 9:
-                continue
-            try:
-                sm.append(float(parts[1]))
-                mx = float(parts[2])
-            except ValueError:
-                continue
-            for n, v in zip(names, parts[5:9]):
-                if v.lower() == "active":
-                    reasons.add(n)
-        os.unlink(self.f.name)
-        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": mx, "reasons": sorted(reasons),
-                "samples": len(sm)}
+        self.t1 = time.perf_counter()
+        if self.h is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [self.err or "nvml unavailable"], "samples": 0}
+        time.sleep(0.005)  # one more sample past the end
+        self.stop_ev.set()
+        self.th.join()
+        t0 = self.t0 if self.t0 is not None else 0.0
+        inside = [x for x in self.samples if t0 <= x[0] <= self.t1 + 0.003]
+        if not inside:  # region shorter than one poll: nearest sample after start
+            inside = [x for x in self.samples if x[0] >= t0][:1]
+        reasons = set()
+        for _, _, r in inside:
+            for name, const in self.REASONS:
+                bit = getattr(self.nv, const, None)
+                if bit is not None and (r & bit):
+                    reasons.add(name)
+        sm = [x[1] for x in inside]
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": self.mx, "reasons": sorted(reasons),
+                "samples": len(sm), "source": "nvml"}
 
 
 def algorithmic_work(cfg, B, world):
@@ -165,6 +197,7 @@ def run_hdp(args, rank, world, local_rank):
     clk = Clocks(local_rank)
     k0 = hdp.lib().hdp_kernel_launches(tr.ctx)
     barrier()
+    clk.start()
     for k in range(args.steps):
         flush.zero_()
         evs[k][0].record(stream)
@@ -302,6 +335,7 @@ def run_c5(args, rank, world, local_rank):
     flush = torch.empty(256 << 20, dtype=torch.uint8, device=dev)
     rows = []
     clk = Clocks(local_rank)
+    clk.start()
     for mib in sizes_mib:
         S = (mib << 20) // 2          # fp16 gradient elements
         desc = hdp.ModelDesc(n_layers=0, max_batch=1, max_seq=1, math=hdp.MATH_MIXED16, wire=wire,

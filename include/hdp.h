@@ -208,6 +208,12 @@ long long hdp_kernel_launches(const hdp_ctx* ctx);
 void* hdp_weights_ptr(hdp_ctx* ctx);           /* working copy, device layout          */
 void* hdp_grads_ptr(hdp_ctx* ctx, int slot);   /* gradient slot, device layout        */
 void* hdp_master_ptr(hdp_ctx* ctx);            /* this rank's fp32 master shards      */
+/* Internal activation buffers of slot `slot` (diagnostics): name is one of
+ * "Hs" (fp16 [L][T+1][B][hp]), "C" (fp32 [L][T][B][hp]), "gates"
+ * (fp16 [L][T][B][4hp]), "X0" (fp16 [T][B][Ip0]), "dA" (fp16 [T][B][4hp]; the
+ * top layer's in the 2-layer wavefront), "dA2" (layer 0's in the wavefront),
+ * "dH0"/"dH1" (fp32).  Returns NULL for an unknown name or unbound context.  */
+void* hdp_debug_buffer(hdp_ctx* ctx, int slot, const char* name);
 
 /* ---------------------------------------------------------------------
  * Kernel-level entries (stateless; used by the C5 sweep and unit tests).

@@ -737,6 +737,8 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
   // 2 layers, mixed mode: both layers' BPTT and the dX1 projection in one wavefront
   // launch (segment for layer 1); layer 0's segment then only has its K8 / K9 work
   const bool wave = L == 2 && !f32 && c->persistent && hdp::recur2_bwd_supported(B, (int)hp);
+  // ... and, on the SMs the recurrences leave idle, the A8 weight gradients of both layers
+  const bool wgrad = wave && !gf && d.vocab == 0 && hdp::recur2_bwd_wgrad(B, (int)hp, (int)c->Ip0);
   char* dAl = wave && l == 0 ? c->dA2 : c->dA;
   if (wave && l == 1) {
     hdp::Recur2BwdArgs wa;
@@ -756,6 +758,16 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
     wa.T = T;
     wa.B = B;
     wa.hp = (int)hp;
+    if (wgrad) {
+      wa.Hs0 = (const __half*)S.Hs;
+      wa.Hs1 = (const __half*)Hs;
+      wa.X0 = (const __half*)S.X0;
+      wa.Ip0 = (int)c->Ip0;
+      const char* nms[4] = {"U1", "W1", "U0", "W0"};
+      for (int i = 0; i < 4; ++i) wa.gW[i] = (__half*)c->G(si, c->find(nms[i]));
+      wa.gb[0] = (__half*)c->G(si, c->find("b1"));
+      wa.gb[1] = (__half*)c->G(si, c->find("b0"));
+    }
     KScope ks_(c, HDP_K_RECUR_BWD, 1, s);
     CK_CUDA(hdp::launch_recur2_bwd(wa, s));
   } else if (wave) {
@@ -815,6 +827,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
       CK(gemm(c, HDP_K_GEMM_DH, c->dA + (long)t * B * 4 * hp * e, 4 * hp, 0, c->W(iU), hp, 1, B, hp, 4 * hp,
               epi_f32(c->dhrec, hp), s));
   }
+  if (wgrad) return HDP_OK;  // A8 done inside the wavefront launch; no K9 (dX1 there too, no embedding)
   // K8 (A8): dW = dA^T X, dU = dA^T H_{-1}, db = sum dA
   CK(gemm(c, HDP_K_GEMM_DW, dAl, 4 * hp, 1, X, Ipl, 1, 4 * hp, Ipl, rows, epi_elem(gf, c->G(si, iW), Ipl), s));
   CK(gemm(c, HDP_K_GEMM_DW, dAl, 4 * hp, 1, Hs, hp, 1, 4 * hp, hp, rows, epi_elem(gf, c->G(si, iU), hp), s));
@@ -1363,6 +1376,21 @@ void* hdp_grads_ptr(hdp_ctx* c, int slot) {
   return c && c->bound && slot >= 0 && slot < c->nslots ? c->grads + (long)slot * c->P * c->gsz : nullptr;
 }
 void* hdp_master_ptr(hdp_ctx* c) { return c && c->bound ? c->master : nullptr; }
+
+void* hdp_debug_buffer(hdp_ctx* c, int slot, const char* name) {
+  if (!c || !c->bound || !name || slot < 0 || slot >= c->nslots || c->d.n_layers <= 0) return nullptr;
+  hdp_ctx::Slot& S = c->slot[slot];
+  const std::string n(name);
+  if (n == "Hs") return S.Hs;
+  if (n == "C") return S.C;
+  if (n == "gates") return S.gates;
+  if (n == "X0") return S.X0;
+  if (n == "dA") return c->dA;
+  if (n == "dA2") return c->dA2;
+  if (n == "dH0") return c->dH[0];
+  if (n == "dH1") return c->dH[1];
+  return nullptr;
+}
 
 int hdp_fused_avg_update(const void* grads, long long src_stride, int nsrc, int grads_f32, long long count, float* W,
                          float* S1, float* S2, void* w16, float* w32, float inv_scale, float lr, float momentum,

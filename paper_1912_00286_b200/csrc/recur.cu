@@ -26,6 +26,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <tuple>
+#include <algorithm>
 
 #include "gemm.cuh"
 #include "ptx.cuh"
@@ -60,6 +62,14 @@ __device__ __forceinline__ unsigned acquire_ld(const unsigned* p) {
   return v;
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// spin (one thread) until a release/acquire counter reaches target; trap after 10 s
+__device__ __forceinline__ void spin_until(const unsigned* f, unsigned target) {
+  if (acquire_ld(f) >= target) return;
+  const uint64_t t0 = ptx::globaltimer_ns();
+  while (acquire_ld(f) < target) {
+    if (ptx::globaltimer_ns() - t0 > 10000000000ull) __trap();
+  }
+}
 
 // smem: [U: nkb x 16 KB][H: nkb x Bc*128 B][act: nwarps x 16 x ACT_LD fp32][barriers]
 constexpr int ACT_LD = 40;  // 32 rows + 8 pad: conflict-free float4 reads (see epilogue)
@@ -943,7 +953,138 @@ struct __align__(64) Bwd2Params {
   unsigned* q1done;    // [nbg][32]: layer-1 steps published (x G CTAs)
   unsigned* xdone;     // [nbg][8][32]: projection steps published per unit slice
   int T, B, hp, nbg;
+  // ---- weight-gradient role (K8 on otherwise idle SMs; wtiles == 0: off)
+  CUtensorMap tmdA[2];  // dA1 / dA0 rows [T*B][4hp], MN-major A operand boxes (64 rows, 64 batch)
+  CUtensorMap tmHs[2];  // Hs1 / Hs0 rows [(T+1)*B][hp], MN-major B operand boxes (64, 64)
+  CUtensorMap tmX0;     // X0 rows [T*B][Ip0] (Ip0 <= 64)
+  __half* gW[4];        // dU1, dW1, dU0, dW0 (fp16 grads, row-major [4hp][N])
+  __half* gb[2];        // db1, db0
+  unsigned* q0done;     // [nbg][32]: layer-0 steps published (x G CTAs)
+  int Ip0, wtiles;
 };
+
+// Weight-gradient role: one CTA per (matrix, 128-gate-row tile) accumulates over all
+// (t, b) in TMEM as the recurrence roles publish dA_t (A8 of the paper's step):
+//   mat 0: dU1 = sum dA1_t^T h1_{t-1}   mat 1: dW1 = sum dA1_t^T h0_t
+//   mat 2: dU0 = sum dA0_t^T h0_{t-1}   mat 3: dW0 = sum dA0_t^T x_t
+// plus db1 / db0 (= sum dA_t, an MMA against a block of ones) on the dU tiles.
+// Items = (t, 64-wide batch chunk) in descending t; 2-stage TMA pipeline:
+// thread 0 acquires the dA_t flags and loads, thread 32 issues the MMAs.
+constexpr int WG_STAGE = 2 * 8192 + 4 * 8192;  // A: 2 m-atoms x 64 b; B: up to 4 n-atoms x 64 b
+size_t wgrad_smem() { return 1024 + 2 * (size_t)WG_STAGE + 2048 + 256; }
+
+__device__ __forceinline__ void bwd_wgrad_role(const Bwd2Params& P, int tile) {
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int T = P.T, B = P.B, hp = P.hp, fourhp = 4 * hp;
+  const int ntile = (fourhp + 127) / 128;
+  if (tile >= 4 * ntile) return;  // padding CTA of the last cluster
+  const int mat = tile / ntile, m0 = (tile % ntile) * 128;
+  const int layer = mat < 2 ? 1 : 0;           // whose dA
+  const int ai = mat < 2 ? 0 : 1;              // tmdA / tmHs index: [0] layer 1, [1] layer 0
+  const int N = mat == 3 ? 16 * ((P.Ip0 + 15) / 16) : hp;
+  const int natom = (N + 63) / 64;
+  const bool withb = mat == 0 || mat == 2;
+  uint8_t* sones = smem + 2 * WG_STAGE;        // [16 rows][128 B] fp16 ones, K-major B operand (N = 16)
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sones + 2048);
+  uint64_t* full = bars;                       // [2]
+  uint64_t* empty = bars + 2;                  // [2]
+  uint64_t* done = bars + 4;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 5);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const unsigned* flags = layer == 1 ? P.q1done : P.q0done;
+  const int G = gridDim.x;
+  const int nbc = (B + 63) / 64;               // 64-wide batch chunks per step
+  const int nitems = T * nbc;
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch(&P.tmdA[ai]);
+    for (int i = 0; i < 2; ++i) {
+      ptx::mbar_init(full + i, 1);
+      ptx::mbar_init(empty + i, 1);
+    }
+    ptx::mbar_init(done, 1);
+    ptx::fence_mbar_init();
+  }
+  for (int i = threadIdx.x; i < 2048 / 4; i += blockDim.x) reinterpret_cast<uint32_t*>(sones)[i] = 0x3C003C00u;
+  ptx::fence_async_smem();
+  if (warp == 2) ptx::tmem_alloc(tslot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = *tslot;               // [0, N): weight grad; [256, 272): bias grad
+  if (threadIdx.x == 0) {
+    // ---- producer
+    const CUtensorMap* tb = mat == 3 ? &P.tmX0 : &P.tmHs[mat == 0 ? 0 : 1];
+    for (int it = 0; it < nitems; ++it) {
+      const int t = T - 1 - it / nbc, bc = it % nbc;
+      const int s = it & 1;
+      if (bc == 0) {
+        const unsigned target = (unsigned)(G * (T - t));
+        for (int g = 0; g < P.nbg; ++g) spin_until(flags + g * 32, target);
+        fence_proxy_async();
+      }
+      ptx::mbar_wait(empty + s, ((it >> 1) & 1) ^ 1);
+      uint8_t* sa = smem + s * WG_STAGE;
+      uint8_t* sb = sa + 2 * 8192;
+      ptx::mbar_arrive_expect_tx(full + s, 2 * 8192 + natom * 8192);
+      const int brow = t * B + bc * 64;        // dA_t / x_t rows
+      ptx::tma_load_2d(sa, &P.tmdA[ai], full + s, m0, brow);
+      ptx::tma_load_2d(sa + 8192, &P.tmdA[ai], full + s, m0 + 64, brow);
+      // B rows: h_{t-1} = Hs slot t (dU), h0_t = Hs0 slot t+1 (dW1), x_t (dW0)
+      const int hrow = mat == 1 ? (t + 1) * B + bc * 64 : mat == 3 ? brow : t * B + bc * 64;
+      for (int a = 0; a < natom; ++a) ptx::tma_load_2d(sb + a * 8192, tb, full + s, a * 64, hrow);
+    }
+  } else if (threadIdx.x == 32) {
+    // ---- MMA issuer
+    const uint32_t idesc = ptx::idesc_f16_f32(128, natom * 64, 1, 1);  // whole 64-wide MN atoms
+    const uint32_t idb = ptx::idesc_f16_f32(128, 16, 1, 0);
+    for (int it = 0; it < nitems; ++it) {
+      const int s = it & 1;
+      ptx::mbar_wait(full + s, (it >> 1) & 1);
+      ptx::tc_fence_after();
+      const uint32_t sa = ptx::smem_u32(smem + s * WG_STAGE), sb = sa + 2 * 8192;
+      const int bc = it % nbc;
+      const int kvalid = min(64, B - bc * 64);
+#pragma unroll 1
+      for (int k = 0; k < kvalid / 16; ++k) {
+        const uint64_t ad = ptx::smem_desc_sw128(sa + k * 2048, 8192, 1024);
+        const uint64_t bd = ptx::smem_desc_sw128(sb + k * 2048, 8192, 1024);
+        const uint32_t acc = (it > 0 || k > 0) ? 1u : 0u;
+        ptx::mma_f16(tbase, ad, bd, idesc, acc);
+        if (withb) ptx::mma_f16(tbase + 256, ad, ptx::smem_desc_sw128(ptx::smem_u32(sones) + k * 32, 0, 1024), idb, acc);
+      }
+      ptx::mma_commit(empty + s);
+    }
+    ptx::mma_commit(done);
+  }
+  __syncwarp();
+  ptx::mbar_wait(done, 0);
+  ptx::tc_fence_after();
+  // ---- epilogue: TMEM lane = tile row; fp32 sums rounded once to fp16 (R13)
+  const int row = m0 + warp * 32 + lane;
+  __half* gout = P.gW[mat];
+  for (int c = 0; c < N; c += 16) {
+    float v[16];
+    ptx::tmem_ld16(tbase + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
+    if (row < fourhp) {
+      const int ld = mat == 3 ? P.Ip0 : hp;
+#pragma unroll
+      for (int q = 0; q < 16; ++q)
+        if (c + q < ld) gout[(size_t)row * ld + c + q] = __float2half_rn(v[q]);
+    }
+  }
+  if (withb) {
+    float v[16];
+    ptx::tmem_ld16(tbase + (static_cast<uint32_t>(warp * 32) << 16) + 256, v);
+    if (row < fourhp) P.gb[mat == 0 ? 0 : 1][row] = __float2half_rn(v[0]);
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  if (warp == 2) {
+    ptx::tc_fence_after();
+    ptx::tmem_dealloc(tbase, 512);
+  }
+}
 
 // Projection role: dX1_t[b][unit] = sum_r dA1_t[b][r] W1[r][unit] for my 64 units
 // (swap-AB tcgen05, A = W1^T slice MN-major resident, B = dA1_t rows via TMA).
@@ -1065,6 +1206,10 @@ template <int NC>
 __global__ void __launch_bounds__(128, 1)
     recur2_bwd_kernel(const __grid_constant__ Bwd2Params P) {
   const int T = P.T, B = P.B, hp = P.hp;
+  if ((int)blockIdx.y >= 3 * P.nbg) {
+    bwd_wgrad_role(P, (blockIdx.y - 3 * P.nbg) * gridDim.x + blockIdx.x);
+    return;
+  }
   const int role = blockIdx.y / P.nbg, grp = blockIdx.y % P.nbg;
   if (role == 1) {
     bwd_proj_role<NC>(P, grp);
@@ -1268,10 +1413,10 @@ __global__ void __launch_bounds__(128, 1)
     }
     ptx::tc_fence_before();
     ptx::fence_async_smem();  // staging writes (generic) -> bulk copy reads (async proxy)
-    if (qi == 0) fence_proxy_async();  // global dA_t stores -> the projection role's TMA reads
+    if (qi == 0 || P.wtiles) fence_proxy_async();  // global dA_t stores -> TMA reads (projection / wgrad roles)
     __syncthreads();
-    if (qi == 0 && threadIdx.x == 64) {  // not a pusher: the release waits for the stores to drain
-      release_add(P.q1done + grp * 32, 1u);
+    if (threadIdx.x == 64 && (qi == 0 || P.wtiles)) {  // not a pusher: the release waits for the stores to drain
+      release_add((qi == 0 ? P.q1done : P.q0done) + grp * 32, 1u);
     }
     if (tr) trace[t * 5 + 3] = ptx::globaltimer_ns();
     // push dA_t (consumed by step t-1) into every peer's sA[t & 1]: one bulk copy per peer.
@@ -1658,13 +1803,6 @@ struct __align__(64) Fwd2Params {
   int region;          // the 32 KB + 2 x Bc x 128 B region (fused projection / R1 staging) exists
 };
 
-__device__ __forceinline__ void spin_until(const unsigned* f, unsigned target) {
-  if (acquire_ld(f) >= target) return;
-  const uint64_t t0 = ptx::globaltimer_ns();
-  while (acquire_ld(f) < target) {
-    if (ptx::globaltimer_ns() - t0 > 10000000000ull) __trap();
-  }
-}
 
 template <int NCI>
 __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__ Fwd2Params P) {
@@ -2321,58 +2459,91 @@ const void* recur2b_fn(int Bc) {
 
 // backward wavefront plan: largest batch-group count whose 3 x G x nbg CTAs are
 // co-resident as G-CTA clusters (every role waits on the others); cached per shape
-bool plan_w2b(int B, int hp, int* Bc_out, int* nbg_out) {
-  static std::map<std::pair<int, int>, std::pair<int, int>> cache;
-  auto key = std::make_pair(B, hp);
+// plan: largest batch-group count whose 3 x G x nbg role CTAs (plus, when wanted,
+// the weight-gradient clusters) are co-resident as G-CTA clusters; cached per shape
+struct W2BPlan {
+  int Bc = 0, nbg = 0, wrows = 0;  // wrows: extra cluster rows of weight-gradient CTAs (0: off)
+};
+int wgrad_rows(int hp) {
+  const int G = (hp + 63) / 64;
+  const int tiles = 4 * ((4 * hp + 127) / 128);
+  return (tiles + G - 1) / G;
+}
+bool plan_w2b(int B, int hp, bool want_wgrad, W2BPlan* out) {
+  static std::map<std::tuple<int, int, bool>, W2BPlan> cache;
+  auto key = std::make_tuple(B, hp, want_wgrad);
   auto it = cache.find(key);
   if (it == cache.end()) {
-    std::pair<int, int> best(0, 0);
+    W2BPlan best;
     const int G = (hp + 63) / 64;
     if (B >= 16 && !(B & 15) && !(hp & 15) && G <= 8) {
-      for (int nbg = 16; nbg >= 1 && !best.second; nbg >>= 1) {
+      for (int nbg = 16; nbg >= 1 && !best.nbg; nbg >>= 1) {
         if (B % nbg) continue;
         const int Bc = B / nbg;
-        if ((Bc & 15) || Bc > 64 || 3 * G * nbg > 148) continue;
-        const size_t smem = bwd_cl_smem(hp, Bc);
+        if ((Bc & 15) || Bc > 64) continue;
+        const size_t smem = std::max(bwd_cl_smem(hp, Bc), wgrad_smem());
         if (smem > 227 * 1024) continue;
         const void* fn = recur2b_fn(Bc);
         if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) break;
-        cudaLaunchConfig_t cfg = {};
-        cfg.gridDim = dim3(G, 3 * nbg);
-        cfg.blockDim = dim3(128);
-        cfg.dynamicSmemBytes = smem;
-        cudaLaunchAttribute at[1];
-        at[0].id = cudaLaunchAttributeClusterDimension;
-        at[0].val.clusterDim.x = G;
-        at[0].val.clusterDim.y = 1;
-        at[0].val.clusterDim.z = 1;
-        cfg.attrs = at;
-        cfg.numAttrs = 1;
-        int ncl = 0;
-        if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess) {
-          (void)cudaGetLastError();
-          continue;
+        for (int w = want_wgrad ? 1 : 0; w >= 0 && !best.nbg; --w) {
+          const int wrows = w ? wgrad_rows(hp) : 0;
+          const int rows = 3 * nbg + wrows;
+          if (G * rows > 148) continue;
+          cudaLaunchConfig_t cfg = {};
+          cfg.gridDim = dim3(G, rows);
+          cfg.blockDim = dim3(128);
+          cfg.dynamicSmemBytes = smem;
+          cudaLaunchAttribute at[1];
+          at[0].id = cudaLaunchAttributeClusterDimension;
+          at[0].val.clusterDim.x = G;
+          at[0].val.clusterDim.y = 1;
+          at[0].val.clusterDim.z = 1;
+          cfg.attrs = at;
+          cfg.numAttrs = 1;
+          int ncl = 0;
+          if (cudaOccupancyMaxActiveClusters(&ncl, fn, &cfg) != cudaSuccess) {
+            (void)cudaGetLastError();
+            continue;
+          }
+          if (ncl >= rows) {
+            best.Bc = Bc;
+            best.nbg = nbg;
+            best.wrows = wrows;
+          }
         }
-        if (ncl >= 3 * nbg) best = std::make_pair(Bc, nbg);
       }
     }
     it = cache.emplace(key, best).first;
   }
-  *Bc_out = it->second.first;
-  *nbg_out = it->second.second;
-  return it->second.second > 0;
+  *out = it->second;
+  return it->second.nbg > 0;
+}
+
+bool wgrad_wanted(int Ip0) {
+  const char* e = getenv("HDP_WAVEFRONT_WGRAD");
+  return !(e && e[0] == '0') && Ip0 > 0 && Ip0 <= 64;
 }
 
 bool recur2_bwd_supported(int B, int hp) {
   const char* e = getenv("HDP_WAVEFRONT");
   if (e && e[0] == '0') return false;
-  int Bc = 0, nbg = 0;
-  return plan_w2b(B, hp, &Bc, &nbg);
+  W2BPlan p;
+  return plan_w2b(B, hp, false, &p);
+}
+
+bool recur2_bwd_wgrad(int B, int hp, int Ip0) {
+  if (!recur2_bwd_supported(B, hp) || !wgrad_wanted(Ip0)) return false;
+  W2BPlan p;
+  return plan_w2b(B, hp, true, &p) && p.wrows > 0;
 }
 
 cudaError_t launch_recur2_bwd(const Recur2BwdArgs& a, cudaStream_t s) {
-  int Bc = 0, nbg = 0;
-  if (!recur2_bwd_supported(a.B, a.hp) || !plan_w2b(a.B, a.hp, &Bc, &nbg)) return cudaErrorInvalidConfiguration;
+  if (!recur2_bwd_supported(a.B, a.hp)) return cudaErrorInvalidConfiguration;
+  const bool wg = a.gW[0] != nullptr;
+  if (wg && !recur2_bwd_wgrad(a.B, a.hp, a.Ip0)) return cudaErrorInvalidConfiguration;
+  W2BPlan pl;
+  if (!plan_w2b(a.B, a.hp, wg, &pl)) return cudaErrorInvalidConfiguration;
+  const int Bc = pl.Bc, nbg = pl.nbg;
   const int G = (a.hp + 63) / 64;
   const uint64_t hp = a.hp;
   Bwd2Params P;
@@ -2391,14 +2562,36 @@ cudaError_t launch_recur2_bwd(const Recur2BwdArgs& a, cudaStream_t s) {
   P.dX1 = a.dX1;
   P.q1done = a.flags;
   P.xdone = a.flags + 16 * 32;
+  P.q0done = a.flags + 16 * 32 + 16 * 8 * 32;
   P.T = a.T;
   P.B = a.B;
   P.hp = a.hp;
   P.nbg = nbg;
-  cudaError_t e = cudaMemsetAsync(a.flags, 0, (16 * 32 + 16 * 8 * 32) * sizeof(unsigned), s);
+  if (wg) {
+    const uint64_t TB = (uint64_t)a.T * a.B, TB1 = (uint64_t)(a.T + 1) * a.B;
+    if (encode_tmap_2d(&P.tmdA[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.dA1, 4 * hp, TB, 4 * hp * 2, 64, 64,
+                       CU_TENSOR_MAP_SWIZZLE_128B) ||
+        encode_tmap_2d(&P.tmdA[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.dA0, 4 * hp, TB, 4 * hp * 2, 64, 64,
+                       CU_TENSOR_MAP_SWIZZLE_128B) ||
+        encode_tmap_2d(&P.tmHs[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.Hs1, hp, TB1, hp * 2, 64, 64,
+                       CU_TENSOR_MAP_SWIZZLE_128B) ||
+        encode_tmap_2d(&P.tmHs[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.Hs0, hp, TB1, hp * 2, 64, 64,
+                       CU_TENSOR_MAP_SWIZZLE_128B) ||
+        encode_tmap_2d(&P.tmX0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.X0, a.Ip0, TB, (uint64_t)a.Ip0 * 2, 64, 64,
+                       CU_TENSOR_MAP_SWIZZLE_128B))
+      return cudaErrorInvalidValue;
+    for (int i = 0; i < 4; ++i) P.gW[i] = a.gW[i];
+    P.gb[0] = a.gb[0];
+    P.gb[1] = a.gb[1];
+    P.Ip0 = a.Ip0;
+    P.wtiles = 4 * ((4 * a.hp + 127) / 128);
+  }
+  cudaError_t e = cudaMemsetAsync(a.flags, 0, (2 * 16 * 32 + 16 * 8 * 32) * sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
   void* args[] = {&P};
-  return launch_cluster(recur2b_fn(Bc), dim3(G, 3 * nbg), dim3(128), bwd_cl_smem(a.hp, Bc), G, s, args);
+  const int rows = 3 * nbg + (wg ? pl.wrows : 0);
+  return launch_cluster(recur2b_fn(Bc), dim3(G, rows), dim3(128), std::max(bwd_cl_smem(a.hp, Bc), wgrad_smem()), G,
+                        s, args);
 }
 
 }  // namespace hdp

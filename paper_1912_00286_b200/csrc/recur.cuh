@@ -63,10 +63,17 @@ struct Recur2BwdArgs {
   const float *C0 = nullptr, *C1 = nullptr;
   __half *dA0 = nullptr, *dA1 = nullptr;  // separate [T][B][4hp] outputs
   float* dX1 = nullptr;                   // [T][B][hp] scratch
-  unsigned* flags = nullptr;              // >= 16*32 + 16*8*32 uints
+  unsigned* flags = nullptr;              // >= 2*16*32 + 16*8*32 uints
   int T = 0, B = 0, hp = 0;
+  // weight-gradient role (A8 on idle SMs, overlapping the recurrences); gW[0] == nullptr: off
+  const __half *Hs0 = nullptr, *Hs1 = nullptr;  // [T+1][B][hp] forward hidden states
+  const __half* X0 = nullptr;                   // [T][B][Ip0] layer-0 input
+  int Ip0 = 0;
+  __half* gW[4] = {nullptr, nullptr, nullptr, nullptr};  // dU1, dW1, dU0, dW0
+  __half* gb[2] = {nullptr, nullptr};                    // db1, db0
 };
 bool recur2_bwd_supported(int B, int hp);
+bool recur2_bwd_wgrad(int B, int hp, int Ip0);  // the launch can also produce the A8 weight gradients
 cudaError_t launch_recur2_bwd(const Recur2BwdArgs& a, cudaStream_t s);
 cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s);
 cudaError_t launch_recur_bwd(const RecurBwdArgs& a, cudaStream_t s);

@@ -29,7 +29,7 @@ EXPORTED = [
     "hdp_read_grads", "hdp_set_lr_schedule", "hdp_lr", "hdp_set_loss_scale", "hdp_lstm_forward",
     "hdp_lstm_backward", "hdp_grad_average_update", "hdp_weights_ptr", "hdp_grads_ptr", "hdp_master_ptr",
     "hdp_fused_avg_update", "hdp_gemm_f16", "hdp_gemm_f32", "hdp_profile", "hdp_profile_read",
-    "hdp_kernel_launches",
+    "hdp_kernel_launches", "hdp_debug_buffer",
 ]
 NTAGS = 15
 
@@ -86,6 +86,7 @@ def _load():
         "hdp_weights_ptr": ([vp], vp),
         "hdp_grads_ptr": ([vp, i], vp),
         "hdp_master_ptr": ([vp], vp),
+        "hdp_debug_buffer": ([vp, i, C.c_char_p], vp),
         "hdp_fused_avg_update": ([vp, ll, i, i, ll, vp, vp, vp, vp, vp, f, f, f, i, vp, vp, vp], i),
         "hdp_gemm_f16": ([vp, ll, i, vp, ll, i, i, i, i, vp, ll, i, vp, i, i, i, vp, ll, i, i, vp], i),
         "hdp_gemm_f32": ([vp, ll, i, vp, ll, i, i, i, i, vp, ll, i, vp, i, i, i, vp], i),
@@ -239,6 +240,10 @@ def weights_ptr(ctx) -> int:
 
 def grads_ptr(ctx, slot=0) -> int:
     return _lib.hdp_grads_ptr(ctx, slot)
+
+
+def debug_buffer(ctx, slot: int, name: str) -> int:
+    return _lib.hdp_debug_buffer(ctx, slot, name.encode())
 
 
 def master_ptr(ctx) -> int:

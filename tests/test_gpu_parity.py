@@ -162,10 +162,12 @@ def test_persistent_matches_per_step_path(monkeypatch):
 @pytest.mark.parametrize("batch,fusex", [(128, "1"), (32, "1"), (64, "0")])
 def test_c2_wavefront_matches_layerwise(monkeypatch, batch, fusex):
     """The 2-layer wavefront kernels (forward: R0/P/R1 roles, layer-0 input
-    projection fused into R0 or read from the K1 GEMM; backward: Q1/X/Q0 roles)
+    projection fused into R0 or read from the K1 GEMM; backward: Q1/X/Q0 roles,
+    weight gradients in the wavefront's W role or by the K8 GEMMs)
     against the oracle and against the layer-by-layer persistent path."""
     cfg = synth.CONFIGS["C2"].with_(seq=24)
     monkeypatch.setenv("HDP_WAVEFRONT_FUSEX", fusex)
+    monkeypatch.setenv("HDP_WAVEFRONT_WGRAD", fusex)  # "0": K8 GEMMs after the wavefront
     out = {}
     for flag in ("1", "0"):
         monkeypatch.setenv("HDP_WAVEFRONT", flag)
