@@ -535,20 +535,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
                   names[role], ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, step / n, (double)(st[0] - t00),
                   (double)(h[((size_t)role * T + T - 1) * 5 + 4] - t00));
         }
-        {
-          double sp = 0, li = 0, mw = 0;
-          int n = 0;
-          for (int t = 2; t < T - 1; ++t) {
-            const unsigned long long* r = &h[((size_t)3 * T + t) * 5];
-            sp += (double)(r[1] - r[0]);
-            li += (double)(r[2] - r[1]);
-            mw += (double)(r[3] - r[2]);
-            ++n;
-          }
-          fprintf(stderr, "[hdp trace] wavefront R1 (thread 0): after MMA issue -> a1x fetch %.0f ns -> barM %.0f ns\n",
-                  li / n, mw / n);
-          (void)sp;
-        }
+
       }
       break;
     }

@@ -62,6 +62,13 @@ __device__ __forceinline__ unsigned acquire_ld(const unsigned* p) {
   return v;
 }
 __device__ __forceinline__ void fence_proxy_async() { asm volatile("fence.proxy.async.global;" ::: "memory"); }
+// named CTA barrier 1..15 (barrier 0 is __syncthreads): arrive without waiting / wait
+__device__ __forceinline__ void named_bar_arrive(int id, int nthreads) {
+  asm volatile("barrier.arrive %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
+__device__ __forceinline__ void named_bar_sync(int id, int nthreads) {
+  asm volatile("barrier.sync %0, %1;" ::"r"(id), "r"(nthreads) : "memory");
+}
 // spin (one thread) until a release/acquire counter reaches target; trap after 10 s
 __device__ __forceinline__ void spin_until(const unsigned* f, unsigned target) {
   if (acquire_ld(f) >= target) return;
@@ -1987,13 +1994,13 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
     // fused-projection region, double-buffered, barX[t & 1] -- one thread acquires
     const bool gt = li == 1 && P.r1_tma;
     const float* sG1 = reinterpret_cast<const float*>(sW0);
-    auto fetch_a1x = [&](int t) {  // thread 0
+    auto fetch_a1x = [&](int t) {  // one thread
       spin_until(pf, (unsigned)(t + 1));
       fence_proxy_async();
       ptx::mbar_arrive_expect_tx(barX + (t & 1), Bc * 256 * 4);
       ptx::tma_load_2d(sW0 + (t & 1) * Bc * 1024, &P.tmG1, barX + (t & 1), row0, t * B + col0);
     };
-    if (gt && threadIdx.x == 0) fetch_a1x(0);
+    if (gt && threadIdx.x == 128) fetch_a1x(0);
     float creg[NCI * 4];
 #pragma unroll
     for (int i = 0; i < NCI * 4; ++i) creg[i] = 0.f;
@@ -2030,11 +2037,22 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
     };
     // layer 0 with G_x0 from K1: loads one step ahead (NCI = 1; the 512-thread variant's
     // register budget keeps them in-step)
-    const bool PIPE = NCI == 1 && li == 0 && !fx;
+    const bool PIPE = false;  // (measured slower: the loads sit between MMA issue and the barM wait)
     if (PIPE) load_gx(0, gx);
+    // operand prefetch for step t+1 (x_{t+1} for the fused projection, a1x_{t+1} for layer 1)
+    // by a thread that issues no MMAs: TMA issued by an MMA issuer measurably delays its commit
+    const int pf_thr = 128;
     for (int t = 0; t < T; ++t) {
       TR(t, 0);
       if (!PIPE) load_gx(t, gx);
+      if (threadIdx.x == pf_thr && t + 1 < T) {
+        // slots (t+1)&1 were last read by step t-1 (x MMA complete at its barM; sG1 in its epilogue)
+        if (fx) {
+          ptx::mbar_arrive_expect_tx(barX + ((t + 1) & 1), Bc * 128);
+          ptx::tma_load_2d(sXin + ((t + 1) & 1) * Bc * 128, &P.tmX0, barX + ((t + 1) & 1), 0, (t + 1) * B + col0);
+        }
+        if (gt) fetch_a1x(t + 1);
+      }
       if (fx && warp == 0 && lane == 0) {
         // x_t W0^T into accumulator 0 (both halves) -- off the recurrence's critical path
         ptx::mbar_wait(barX + (t & 1), (t >> 1) & 1);
@@ -2044,11 +2062,6 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
         for (int h2 = 0; h2 < 2; ++h2)
           ptx::mma_f16(tbase + (h2 * nacc) * Bc, ptx::smem_desc_sw128(ptx::smem_u32(sW0 + h2 * 16384), 0, 1024), bd,
                        idesc, 0u);
-        // x_{t+1}: its slot was last read by the x MMA of step t-1 (complete)
-        if (t + 1 < T) {
-          ptx::mbar_arrive_expect_tx(barX + ((t + 1) & 1), Bc * 128);
-          ptx::tma_load_2d(sXin + ((t + 1) & 1) * Bc * 128, &P.tmX0, barX + ((t + 1) & 1), 0, (t + 1) * B + col0);
-        }
         if (t == 0) ptx::mma_commit(barM);
       }
       if (fx && t == 0 && lane == 0 && warp > 0 && warp < nis) ptx::mbar_arrive(barM);
@@ -2059,21 +2072,16 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
           ptx::tc_fence_after();
           TR(t, 1);
           issue_mma(p);
-          if (tr && li == 1) P.trace[(size_t)3 * T * 5 + t * 5 + 0] = ptx::globaltimer_ns();
-          if (gt && threadIdx.x == 0 && t + 1 < T) fetch_a1x(t + 1);
-          if (tr && li == 1) P.trace[(size_t)3 * T * 5 + t * 5 + 1] = ptx::globaltimer_ns();
         }
         if (PIPE && t + 1 < T) load_gx(t + 1, gxn);
         __syncwarp();
         ptx::mbar_wait(barM, mph);
-        if (tr && li == 1) P.trace[(size_t)3 * T * 5 + t * 5 + 2] = ptx::globaltimer_ns();
         mph ^= 1u;
         ptx::tc_fence_after();
         fphase[p] ^= 1u;
         if (threadIdx.x == 0 && t + 2 <= T - 1) ptx::mbar_arrive_expect_tx(fullH + p, total_bytes);
       } else {
         if (PIPE && t + 1 < T) load_gx(t + 1, gxn);
-        if (gt && threadIdx.x == 0 && t + 1 < T) fetch_a1x(t + 1);
         if (fx) {
           __syncwarp();
           ptx::mbar_wait(barM, mph);
@@ -2135,7 +2143,6 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
       }
       ptx::tc_fence_before();
       ptx::fence_async_smem();
-      if (li == 0) fence_proxy_async();  // Hs0 stores -> P's TMA reads
       __syncthreads();
       TR(t, 3);
       if (PIPE) {
@@ -2144,15 +2151,22 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
 #pragma unroll
           for (int k = 0; k < 16; ++k) gx[ci][k] = gxn[ci][k];
       }
-      if (li == 0 && threadIdx.x == blockDim.x - 32) {  // neither a pusher nor an MMA issuer:
-                                                        // the release waits for the stores to drain
-        release_add(P.r0done + grp * 32, 1u);
-      }
       if (t < T - 1 && threadIdx.x < G) {
         const int dst = threadIdx.x;
         const uint32_t dsta = ptx::mapa(sH_addr + (t & 1) * hbuf + rank * Bc * 128, dst);
         const uint32_t mb = ptx::mapa(ptx::smem_u32(fullH + (t & 1)), dst);
         ptx::bulk_copy_to_peer(dsta, sX_addr + (t & 1) * Bc * 128, Bc * 128, mb);
+      }
+      if (li == 0) {
+        // publish h0_t to the projection role after the push (off the recurrence's critical
+        // path): every thread's Hs0 stores -> async proxy, then one release
+        fence_proxy_async();
+        if (warp == nwarps - 1) {
+          named_bar_sync(1, blockDim.x);
+          if (lane == 0) release_add(P.r0done + grp * 32, 1u);
+        } else {
+          named_bar_arrive(1, blockDim.x);
+        }
       }
       TR(t, 4);
     }
