@@ -725,7 +725,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
   // launch (segment for layer 1); layer 0's segment then only has its K8 / K9 work
   const bool wave = L == 2 && !f32 && c->persistent && hdp::recur2_bwd_supported(B, (int)hp);
   // ... and, on the SMs the recurrences leave idle, the A8 weight gradients of both layers
-  const bool wgrad = wave && !gf && d.vocab == 0 && hdp::recur2_bwd_wgrad(B, (int)hp, (int)c->Ip0);
+  const bool wgrad = wave && !gf && hdp::recur2_bwd_wgrad(B, (int)hp, (int)c->Ip0);
   char* dAl = wave && l == 0 ? c->dA2 : c->dA;
   if (wave && l == 1) {
     hdp::Recur2BwdArgs wa;
@@ -814,11 +814,10 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
       CK(gemm(c, HDP_K_GEMM_DH, c->dA + (long)t * B * 4 * hp * e, 4 * hp, 0, c->W(iU), hp, 1, B, hp, 4 * hp,
               epi_f32(c->dhrec, hp), s));
   }
-  if (wgrad) return HDP_OK;  // A8 done inside the wavefront launch; no K9 (dX1 there too, no embedding)
-  // K8 (A8): dW = dA^T X, dU = dA^T H_{-1}, db = sum dA
-  CK(gemm(c, HDP_K_GEMM_DW, dAl, 4 * hp, 1, X, Ipl, 1, 4 * hp, Ipl, rows, epi_elem(gf, c->G(si, iW), Ipl), s));
-  CK(gemm(c, HDP_K_GEMM_DW, dAl, 4 * hp, 1, Hs, hp, 1, 4 * hp, hp, rows, epi_elem(gf, c->G(si, iU), hp), s));
-  {
+  if (!wgrad) {  // (else A8 was done inside the wavefront launch)
+    // K8 (A8): dW = dA^T X, dU = dA^T H_{-1}, db = sum dA
+    CK(gemm(c, HDP_K_GEMM_DW, dAl, 4 * hp, 1, X, Ipl, 1, 4 * hp, Ipl, rows, epi_elem(gf, c->G(si, iW), Ipl), s));
+    CK(gemm(c, HDP_K_GEMM_DW, dAl, 4 * hp, 1, Hs, hp, 1, 4 * hp, hp, rows, epi_elem(gf, c->G(si, iU), hp), s));
     KScope ks_(c, HDP_K_GEMM_DW, 2, s);
     CK_CUDA(hdp::launch_colreduce(f32, dAl, 4 * hp, (int)rows, (int)(4 * hp), nullptr, c->crp, gf, c->G(si, ib), s));
   }

@@ -963,7 +963,7 @@ struct __align__(64) Bwd2Params {
   // ---- weight-gradient role (K8 on otherwise idle SMs; wtiles == 0: off)
   CUtensorMap tmdA[2];  // dA1 / dA0 rows [T*B][4hp], MN-major A operand boxes (64 rows, 64 batch)
   CUtensorMap tmHs[2];  // Hs1 / Hs0 rows [(T+1)*B][hp], MN-major B operand boxes (64, 64)
-  CUtensorMap tmX0;     // X0 rows [T*B][Ip0] (Ip0 <= 64)
+  CUtensorMap tmX0;     // X0 rows [T*B][Ip0] (Ip0 <= 256)
   __half* gW[4];        // dU1, dW1, dU0, dW0 (fp16 grads, row-major [4hp][N])
   __half* gb[2];        // db1, db0
   unsigned* q0done;     // [nbg][32]: layer-0 steps published (x G CTAs)
@@ -2535,7 +2535,7 @@ bool plan_w2b(int B, int hp, bool want_wgrad, W2BPlan* out) {
 
 bool wgrad_wanted(int Ip0) {
   const char* e = getenv("HDP_WAVEFRONT_WGRAD");
-  return !(e && e[0] == '0') && Ip0 > 0 && Ip0 <= 64;
+  return !(e && e[0] == '0') && Ip0 > 0 && Ip0 <= 256 && !(Ip0 & 15);
 }
 
 bool recur2_bwd_supported(int B, int hp) {

@@ -102,6 +102,17 @@ def test_c3_imdb_reduced_mixed():
     assert _max(recs[-1]["master_err"]) <= 2e-2
 
 
+def test_c3_wavefront_b128_mixed():
+    """C3 at its full per-rank batch (both wavefront launches with the
+    embedding input: K1 + embedding backward outside, A8 in the W role)."""
+    cfg = synth.CONFIGS["C3"].with_(seq=24)
+    recs = run_parity(cfg, 128, 1, steps=2, mixed=True)
+    for r in recs:
+        assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
+        assert _max(r["grad_err"][0]) <= 2e-2, r["grad_err"]
+    assert _max(recs[-1]["master_err"]) <= 2e-2
+
+
 def test_c3_imdb_reduced_fp32():
     cfg = synth.CONFIGS["C3"].with_(seq=24)
     recs = run_parity(cfg, 8, 2, steps=2, mixed=False)
