@@ -9,6 +9,7 @@
 // split order (no atomics), so results do not depend on scheduling.
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdio>
 #include <mutex>
 
@@ -30,8 +31,11 @@ struct TileCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 4 : (BN == 128 ? 4 : 6);
-  static constexpr int SMEM = STAGES * STAGE + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int STAGES = BN == 256 ? 3 : (BN == 128 ? 4 : 6);
+  static constexpr int EPI_LD = 36;  // staging row stride (floats): conflict-free float4 rows
+  static constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quadrant, each half of the columns
+  static constexpr int EPI_BYTES = EPI_WARPS * 32 * EPI_LD * 4;
+  static constexpr int SMEM = STAGES * STAGE + 1024 /*align slack*/ + 256 /*barriers*/ + EPI_BYTES;
 };
 
 __device__ __forceinline__ float bias_at(const Epilogue& e, long i) {
@@ -113,23 +117,39 @@ __device__ __forceinline__ void epi_store16(const Epilogue& epi, float* ws, int 
   }
 }
 
+// Persistent, warp-specialised: each CTA walks tiles blockIdx.x, +gridDim.x, ...
+//   warp 0 (one lane): TMA producer over a continuous k-block stream (STAGES ring)
+//   warp 1           : TMEM allocation; one lane issues tcgen05.mma into one of two
+//                      TMEM accumulators (2 x BN columns) per tile
+//   warps 2..9       : epilogue of tile i (TMEM -> registers -> smem -> coalesced
+//                      global stores) while the MMAs of tile i+1 run; warp w drains
+//                      TMEM lane quadrant w % 4, column half (w - 2) / 4
 template <int BN, int AMN, int BMN>
-__global__ void __launch_bounds__(128, 1)
+__global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, int M, int N,
-                   int K, int kbps, Epilogue epi, float* ws) {
+                   int K, int kbps, int splits, Epilogue epi, float* ws) {
   using C = TileCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
   uint64_t* empty = full + C::STAGES;
-  uint64_t* tfull = empty + C::STAGES;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* accf = empty + C::STAGES;  // [2] accumulator b complete
+  uint64_t* acce = accf + 2;           // [2] accumulator b drained (8 epilogue warps)
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(acce + 2);
+  float* epi_stage = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE + 256);  // [8 warps][32][EPI_LD]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.x * BM, n0 = blockIdx.y * BN;
+  const int mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN;
+  const int ntiles = mt * nt * splits;
   const int kb_total = (K + BK - 1) / BK;
-  const int kb0 = blockIdx.z * kbps;
-  const int nkb = min(kb_total, kb0 + kbps) - kb0;
+  auto decode = [&](int tile, int& m0, int& n0, int& z, int& kb0, int& nkb) {
+    z = tile / (mt * nt);
+    const int r = tile % (mt * nt);
+    m0 = (r % mt) * BM;  // consecutive CTAs share the B tile (n): better L2 reuse of the smaller operand
+    n0 = (r / mt) * BN;
+    kb0 = z * kbps;
+    nkb = min(kb_total, kb0 + kbps) - kb0;
+  };
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch(&tma);
@@ -138,85 +158,187 @@ __global__ void __launch_bounds__(128, 1)
       ptx::mbar_init(full + s, 1);
       ptx::mbar_init(empty + s, 1);
     }
-    ptx::mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(accf + b, 1);
+      ptx::mbar_init(acce + b, C::EPI_WARPS);
+    }
     ptx::fence_mbar_init();
   }
-  if (warp == 2) ptx::tmem_alloc(tslot, BN);
+  if (warp == 1) ptx::tmem_alloc(tslot, 2 * BN);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = *tslot;
 
-  if (warp == 0 && lane == 0) {
-    // ---------------- TMA producer
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % C::STAGES;
-      const uint32_t ph = (i / C::STAGES) & 1;
-      ptx::mbar_wait(empty + s, ph ^ 1);
-      uint8_t* sa = smem + s * C::STAGE;
-      uint8_t* sb = sa + C::A_BYTES;
-      const int k0 = (kb0 + i) * BK;
-      ptx::mbar_arrive_expect_tx(full + s, C::STAGE);
-      if (AMN == 0) {
-        ptx::tma_load_2d(sa, &tma, full + s, k0, m0);
-      } else {
-        ptx::tma_load_2d(sa, &tma, full + s, m0, k0);
-        ptx::tma_load_2d(sa + 8192, &tma, full + s, m0 + 64, k0);
-      }
-      if (BMN == 0) {
-        ptx::tma_load_2d(sb, &tmb, full + s, k0, n0);
-      } else {
+  if (warp == 0) {
+    if (lane == 0) {
+      // ---------------- TMA producer
+      int it = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        int m0, n0, z, kb0, nkb;
+        decode(tile, m0, n0, z, kb0, nkb);
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const int s = it % C::STAGES;
+          const uint32_t ph = (it / C::STAGES) & 1;
+          ptx::mbar_wait(empty + s, ph ^ 1);
+          uint8_t* sa = smem + s * C::STAGE;
+          uint8_t* sb = sa + C::A_BYTES;
+          const int k0 = (kb0 + i) * BK;
+          ptx::mbar_arrive_expect_tx(full + s, C::STAGE);
+          if (AMN == 0) {
+            ptx::tma_load_2d(sa, &tma, full + s, k0, m0);
+          } else {
+            ptx::tma_load_2d(sa, &tma, full + s, m0, k0);
+            ptx::tma_load_2d(sa + 8192, &tma, full + s, m0 + 64, k0);
+          }
+          if (BMN == 0) {
+            ptx::tma_load_2d(sb, &tmb, full + s, k0, n0);
+          } else {
 #pragma unroll
-        for (int j = 0; j < BN / 64; ++j) ptx::tma_load_2d(sb + j * 8192, &tmb, full + s, n0 + 64 * j, k0);
+            for (int j = 0; j < BN / 64; ++j) ptx::tma_load_2d(sb + j * 8192, &tmb, full + s, n0 + 64 * j, k0);
+          }
+        }
       }
     }
-  } else if (warp == 1 && lane == 0) {
-    // ---------------- MMA issuer
-    constexpr uint32_t idesc = ptx::idesc_f16_f32(BM, BN, AMN, BMN);
-    for (int i = 0; i < nkb; ++i) {
-      const int s = i % C::STAGES;
-      const uint32_t ph = (i / C::STAGES) & 1;
-      ptx::mbar_wait(full + s, ph);
+  } else if (warp == 1) {
+    if (lane == 0) {
+      // ---------------- MMA issuer
+      constexpr uint32_t idesc = ptx::idesc_f16_f32(BM, BN, AMN, BMN);
+      int it = 0, lt = 0;
+      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+        int m0, n0, z, kb0, nkb;
+        decode(tile, m0, n0, z, kb0, nkb);
+        const int b = lt & 1;
+        ptx::mbar_wait(acce + b, ((lt >> 1) & 1) ^ 1);  // accumulator b drained by the epilogue
+        ptx::tc_fence_after();
+        const uint32_t tacc = tbase + b * BN;
+        for (int i = 0; i < nkb; ++i, ++it) {
+          const int s = it % C::STAGES;
+          const uint32_t ph = (it / C::STAGES) & 1;
+          ptx::mbar_wait(full + s, ph);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(smem + s * C::STAGE);
+          const uint32_t sb = sa + C::A_BYTES;
+#pragma unroll
+          for (int k = 0; k < BK / 16; ++k) {
+            // K-major: advance 16 elements = 32 B inside the 128 B swizzled row.
+            // MN-major: advance 16 K-rows = 2048 B (two 8-row atoms of 1024 B);
+            //   LBO = 8192 B between 64-wide MN atoms, SBO = 1024 B between 8-row K groups.
+            const uint64_t ad = AMN ? ptx::smem_desc_sw128(sa + k * 2048, 8192, 1024)
+                                    : ptx::smem_desc_sw128(sa + k * 32, 0, 1024);
+            const uint64_t bd = BMN ? ptx::smem_desc_sw128(sb + k * 2048, 8192, 1024)
+                                    : ptx::smem_desc_sw128(sb + k * 32, 0, 1024);
+            ptx::mma_f16(tacc, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+          }
+          ptx::mma_commit(empty + s);  // frees the smem slot once these MMAs retire
+        }
+        ptx::mma_commit(accf + b);     // accumulator b complete
+      }
+    }
+  } else {
+    // ---------------- epilogue warps 2..9: TMEM lane quadrant q = warp % 4, column half ch
+    const int q = warp & 3;
+    const int ch = (warp - 2) >> 2;
+    const int c_lo = ch * (BN / 2), c_hi = c_lo + BN / 2;
+    float* st = epi_stage + (warp - 2) * 32 * C::EPI_LD;
+    const bool f16 = epi.mode == EPI_F16;
+    const bool fast = !epi.accumulate && (epi.mode == EPI_F32 || epi.mode == EPI_SPLITK || f16);
+    __half* o16 = reinterpret_cast<__half*>(epi.out);
+    const bool post = epi.mode != EPI_SPLITK;  // bias / relu belong to the reduction for split-K
+    int nf = 0, lt = 0;
+    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+      int m0, n0, z, kb0, nkb;
+      decode(tile, m0, n0, z, kb0, nkb);
+      const int b = lt & 1;
+      ptx::mbar_wait(accf + b, (lt >> 1) & 1);
       ptx::tc_fence_after();
-      const uint32_t sa = ptx::smem_u32(smem + s * C::STAGE);
-      const uint32_t sb = sa + C::A_BYTES;
-#pragma unroll
-      for (int k = 0; k < BK / 16; ++k) {
-        // K-major: advance 16 elements = 32 B inside the 128 B swizzled row.
-        // MN-major: advance 16 K-rows = 2048 B (two 8-row atoms of 1024 B);
-        //   LBO = 8192 B between 64-wide MN atoms, SBO = 1024 B between 8-row K groups.
-        const uint64_t ad = AMN ? ptx::smem_desc_sw128(sa + k * 2048, 8192, 1024)
-                                : ptx::smem_desc_sw128(sa + k * 32, 0, 1024);
-        const uint64_t bd = BMN ? ptx::smem_desc_sw128(sb + k * 2048, 8192, 1024)
-                                : ptx::smem_desc_sw128(sb + k * 32, 0, 1024);
-        ptx::mma_f16(tbase, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
-      }
-      ptx::mma_commit(empty + s);  // frees the smem slot once these MMAs retire
-    }
-    ptx::mma_commit(tfull);        // accumulator complete
-  }
-  __syncwarp();
-
-  // ---------------- epilogue: TMEM -> registers -> global
-  ptx::mbar_wait(tfull, 0);
-  ptx::tc_fence_after();
-  const int m = m0 + warp * 32 + lane;
-  int nf = 0;
+      const uint32_t tq = tbase + b * BN + (static_cast<uint32_t>(q * 32) << 16);
+      const int m = m0 + q * 32 + lane;
+      if (fast) {
+        // 32 x 32 chunk through shared memory; every store instruction then writes
+        // 4 whole rows (lane -> row i*4 + lane/8, 4 consecutive columns)
+        float* o32 = epi.mode == EPI_SPLITK ? ws + (size_t)z * M * N : reinterpret_cast<float*>(epi.out);
+        const long ldo = epi.mode == EPI_SPLITK ? N : epi.ldo;
+        const bool vec = f16 ? ((ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(o16) & 7) == 0)
+                             : ((ldo & 3) == 0 && (reinterpret_cast<uintptr_t>(o32) & 15) == 0);
+        const float bm = (post && epi.bias && epi.bias_on_m && m < M) ? bias_at(epi, m) : 0.f;
 #pragma unroll 1
-  for (int c = 0; c < BN; c += 16) {
-    float v[16];
-    ptx::tmem_ld16(tbase + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
-    if (n0 + c < N) epi_store16(epi, ws, M, N, m, n0 + c, v, nf);
-  }
-  if (epi.mode == EPI_F16 && epi.nonfinite) {
-    nf = __reduce_add_sync(0xffffffffu, nf);
-    if (lane == 0 && nf) atomicAdd(epi.nonfinite, nf);
+        for (int c = c_lo; c < c_hi; c += 32) {
+          if (n0 + c >= N) break;
+          float v[32];
+          ptx::tmem_ld16_nowait(tq + c, *reinterpret_cast<float(*)[16]>(v));
+          ptx::tmem_ld16_nowait(tq + c + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+          // column bias: one coalesced load per lane, broadcast by shuffles
+          const float bl = (post && epi.bias && !epi.bias_on_m && n0 + c + lane < N) ? bias_at(epi, n0 + c + lane) : 0.f;
+          ptx::tmem_wait_ld();
+          if (post) {
+#pragma unroll
+            for (int j = 0; j < 32; ++j) {
+              float x = v[j] + (epi.bias_on_m ? bm : __shfl_sync(0xffffffffu, bl, j));
+              if (epi.relu) x = fmaxf(x, 0.f);
+              v[j] = x;
+            }
+          }
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(st + lane * C::EPI_LD + j) = make_float4(v[j], v[j + 1], v[j + 2], v[j + 3]);
+          __syncwarp();
+#pragma unroll
+          for (int i = 0; i < 8; ++i) {
+            const int r = i * 4 + (lane >> 3), cc = (lane & 7) * 4;
+            const int mr = m0 + q * 32 + r, n = n0 + c + cc;
+            if (mr < M && n < N) {
+              const float4 qq = *reinterpret_cast<const float4*>(st + r * C::EPI_LD + cc);
+              const float qv[4] = {qq.x, qq.y, qq.z, qq.w};
+              if (f16) {
+                __align__(8) __half h[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                  h[u] = __float2half_rn(qv[u]);
+                  if (n + u < N) nf += f16_nonfinite(h[u]);
+                }
+                __half* dst = o16 + (size_t)mr * ldo + n;
+                if (vec && n + 4 <= N) {
+                  *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(h);
+                } else {
+                  for (int u = 0; u < 4; ++u)
+                    if (n + u < N) dst[u] = h[u];
+                }
+              } else {
+                float* dst = o32 + (size_t)mr * ldo + n;
+                if (vec && n + 4 <= N) {
+                  *reinterpret_cast<float4*>(dst) = qq;
+                } else {
+                  for (int u = 0; u < 4; ++u)
+                    if (n + u < N) dst[u] = qv[u];
+                }
+              }
+            }
+          }
+          __syncwarp();
+        }
+      } else {
+#pragma unroll 1
+        for (int c = c_lo; c < c_hi; c += 16) {
+          float v[16];
+          ptx::tmem_ld16(tq + c, v);
+          if (n0 + c < N) epi_store16(epi, ws, M, N, m, n0 + c, v, nf);
+        }
+      }
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(acce + b);
+    }
+    if (epi.mode == EPI_F16 && epi.nonfinite) {
+      nf = __reduce_add_sync(0xffffffffu, nf);
+      if (lane == 0 && nf) atomicAdd(epi.nonfinite, nf);
+    }
   }
   ptx::tc_fence_before();
   __syncthreads();
-  if (warp == 2) {
+  if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tbase, BN);
+    ptx::tmem_dealloc(tbase, 2 * BN);
   }
 }
 
@@ -360,13 +482,25 @@ int encode_tmap_2d(CUtensorMap* m, CUtensorMapDataType dt, const void* base, uin
 
 namespace {
 
+int num_sms() {
+  static int n = 0;
+  if (!n) {
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess ||
+        n <= 0)
+      n = 148;
+  }
+  return n;
+}
+
 template <int BN, int AMN, int BMN>
 cudaError_t launch_tc(const GemmPlan& p, cudaStream_t s) {
   using C = TileCfg<BN>;
-  dim3 grid((p.M + BM - 1) / BM, (p.N + BN - 1) / BN, p.splits);
+  const int ntiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN) * p.splits;
   Epilogue e = p.epi;
   if (p.splits > 1) e.mode = EPI_SPLITK;
-  gemm_tc_kernel<BN, AMN, BMN><<<grid, 128, C::SMEM, s>>>(p.ta, p.tb, p.M, p.N, p.K, p.kbps, e, p.ws);
+  gemm_tc_kernel<BN, AMN, BMN><<<std::min(ntiles, num_sms()), 320, C::SMEM, s>>>(p.ta, p.tb, p.M, p.N, p.K, p.kbps,
+                                                                                  p.splits, e, p.ws);
   return cudaGetLastError();
 }
 

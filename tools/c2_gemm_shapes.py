@@ -20,6 +20,8 @@ SHAPES = {  # name: (M, N, K, a_mn, b_mn)
     "head dH = dz Fw": (R, H, F, 0, 1),
     "K8 dW0 = dA0^T X0": (H4, I, R, 1, 1),
     "K8 dU0 = dA0^T H0": (H4, H, R, 1, 1),
+    "C3 K1 Gx0 = E X0": (32768, 1024, 128, 0, 0),
+    "C3 K9 dX0 = dA0 W0": (32768, 128, 1024, 0, 1),
 }
 
 
@@ -28,19 +30,29 @@ def run(M, N, K, amn, bmn, bn, splits, iters=50):
     As, lda = tstore(A, amn); Bs, ldb = tstore(B, bmn)
     C = torch.empty(M, N, device="cuda")
     ws = torch.empty(16 * M * N, device="cuda")
-    f = lambda: hdp.gemm_f16(As, lda, amn, Bs, ldb, bmn, M, N, K, C, N, 0, ws=ws, ws_floats=ws.numel(), bn=bn, splits=splits)
-    for _ in range(3): f()
+    f = lambda st: hdp.gemm_f16(As, lda, amn, Bs, ldb, bmn, M, N, K, C, N, 0, ws=ws, ws_floats=ws.numel(), bn=bn,
+                                splits=splits, stream=st)
+    s0 = torch.cuda.current_stream()
+    for _ in range(3): f(s0)
+    torch.cuda.synchronize()
+    # device time only: the launches are replayed from a CUDA graph (host overhead excluded)
+    g = torch.cuda.CUDAGraph()
+    cs = torch.cuda.Stream()
+    with torch.cuda.stream(cs):
+        with torch.cuda.graph(g, stream=cs):
+            for _ in range(iters): f(cs)
+    g.replay(); torch.cuda.synchronize()
     e0, e1 = torch.cuda.Event(True), torch.cuda.Event(True)
     e0.record()
-    for _ in range(iters): f()
+    g.replay()
     e1.record(); torch.cuda.synchronize()
     return e0.elapsed_time(e1) / iters * 1e3
 
 
 for name, (M, N, K, a, b) in SHAPES.items():
     ideal_us = (2 * (M * K + N * K) + 4 * M * N) / 7.0e12 * 1e6
-    for bn in (0, 64, 128, 256):
-        for splits in ((0, 1, 4, 16) if K >= 4096 else (0,)):
+    for bn in (0, 128, 256):
+        for splits in ((0,) if K < 4096 else (0, 16)):
             try:
                 us = run(M, N, K, a, b, bn, splits)
                 print(json.dumps({"shape": name, "M": M, "N": N, "K": K, "bn": bn, "splits": splits, "us": round(us, 2),
