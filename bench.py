@@ -119,21 +119,50 @@ class Clocks:
                 "samples": len(sm), "source": "nvml"}
 
 
-def algorithmic_work(cfg, B, world):
-    """Per-launch algorithmic work of each kernel class (DESIGN.md §Roofline):
+def committed_traffic(workload, kclass):
+    """dram__bytes_read.sum + dram__bytes_write.sum per launch of this kernel
+    class, from one committed `ncu --set full` capture (profiles/traffic.json),
+    or None."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "traffic.json")) as f:
+            return json.load(f)[workload][kclass]["traffic_bytes_per_launch"]
+    except Exception:  # noqa: BLE001
+        return None
+
+
+def algorithmic_work(cfg, B, world, prof=None):
+    """Per-launch algorithmic work of each kernel class (DESIGN.md §9):
     flops for contractions (unpadded shapes), HBM bytes for the elementwise /
-    update kernels.  Returns {class: (kind, per_launch_amount)}."""
+    update kernels.  Returns {class: (kind, per_launch_amount)}.
+
+    With the 2-layer wavefront (one recur_fwd and one recur_bwd launch per step,
+    read from the live profile's launch counts) a launch covers both layers'
+    recurrences plus the work fused into it: the layer-1 input projection, the
+    layer-0 one when no K1 launch remains, the dX1 projection and, when no K8
+    launch remains, the A8 weight gradients of both layers."""
     h, T, L = cfg.hidden, cfg.seq, cfg.n_layers
     I0 = cfg.embed_dim if cfg.vocab else cfg.input_dim
     ins = [I0] + [h] * (L - 1)
     w = {}
+    rec = 2.0 * B * 4 * h * h * (T - 1)          # one layer's U h_{t-1} (or U^T dA) over t = 1..T-1
     w["gemm_h(K2)"] = ("flop", 2.0 * B * 4 * h * h)
     w["gemm_dh(K7)"] = ("flop", 2.0 * B * 4 * h * h)
     w["gemm_x(K1)"] = ("flop", sum(2.0 * B * T * 4 * h * i for i in ins) / L)
     w["gemm_dw(K8)"] = ("flop", sum(2.0 * 4 * h * (i + h) * B * T for i in ins) / (3 * L))  # dW, dU, db launches
     w["gemm_dx(K9)"] = ("flop", 2.0 * B * T * 4 * h * h)
-    w["recur_fwd(K2+K3)"] = ("flop", 2.0 * B * 4 * h * h * (T - 1))   # one launch = all T steps of a layer
-    w["recur_bwd(K6+K7)"] = ("flop", 2.0 * B * 4 * h * h * (T - 1))
+    w["recur_fwd(K2+K3)"] = ("flop", rec)   # one launch = all T steps of a layer
+    w["recur_bwd(K6+K7)"] = ("flop", rec)
+    prof = prof or {}
+    if L == 2 and prof.get("recur_fwd(K2+K3)", {}).get("launches_per_step") == 1:
+        f = 2 * rec + 2.0 * B * T * 4 * h * h                       # R0 + R1 + P (layer-1 projection)
+        if "gemm_x(K1)" not in prof:
+            f += 2.0 * B * T * 4 * h * I0                             # fused layer-0 projection
+        w["recur_fwd(K2+K3)"] = ("flop", f)
+    if L == 2 and prof.get("recur_bwd(K6+K7)", {}).get("launches_per_step") == 1:
+        f = 2 * rec + 2.0 * B * T * 4 * h * h                       # Q1 + Q0 + X (dX1 = dA1 W1)
+        if "gemm_dw(K8)" not in prof:
+            f += sum(2.0 * 4 * h * (i + h) * B * T for i in ins)      # W role: dU, dW of both layers
+        w["recur_bwd(K6+K7)"] = ("flop", f)
     w["cell_fwd(K3)"] = ("byte", 50.0 * B * h)   # Gx 16 + Gh 16 + c_prev 4 + gates 8 + c 4 + h 2
     w["cell_bwd(K6)"] = ("byte", 40.0 * B * h)   # dHa 4 + dh_rec 4 + gates 8 + c 4 + c_prev 4 + dc 8 + dA 8
     return w
@@ -241,7 +270,7 @@ def run_hdp(args, rank, world, local_rank):
     if rank != 0:
         return None
     pk = peaks()
-    work = algorithmic_work(cfg, B, world)
+    work = algorithmic_work(cfg, B, world, prof)
     cand = {k: v for k, v in prof.items() if k in work}
     dom = max(cand, key=lambda k: cand[k]["ms_per_step"])
     kind, per_launch = work[dom]
@@ -256,6 +285,7 @@ def run_hdp(args, rank, world, local_rank):
         peak = pk["hbm_gbs"]
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": None}
+    roof["traffic"] = committed_traffic(cfg.name, dom)
     roof.update({"kernel": dom, "peak_src": pk["src"] + (" sustained" if kind == "flop" else ""),
                  "avg_launch_us": avg_launch_ms * 1e3, "per_launch": per_launch,
                  "per_launch_unit": "flop" if kind == "flop" else "byte",
