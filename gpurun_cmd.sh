@@ -1,4 +1,3 @@
-timeout -s KILL 300 python bench.py --steps 20 --warmup 5 > gpurun_out/b63.log 2>&1; echo bench_exit=$? >> gpurun_out/b63.log
-timeout -s KILL 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches63.csv python bench.py --steps 2 --warmup 3 --no-cpu-baseline > gpurun_out/ncu63a.log 2>&1; echo ncu_exit=$? >> gpurun_out/ncu63a.log
-timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:recur2_bwd -s 2 -c 1 -o gpurun_out/full63_bwd python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu63b.log 2>&1; echo ncu_exit=$? >> gpurun_out/ncu63b.log
-timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:recur2f -s 2 -c 1 -o gpurun_out/full63_fwd python bench.py --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/ncu63c.log 2>&1; echo ncu_exit=$? >> gpurun_out/ncu63c.log
+timeout -s KILL 600 python -m pytest tests/test_gpu_parity.py -x -q -k "wavefront or c2 or c3" > gpurun_out/t69.log 2>&1; echo pytest_exit=$? >> gpurun_out/t69.log
+HDP_RECUR_TRACE=1 timeout -s KILL 300 python bench.py --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/tr69.log 2>&1
+timeout -s KILL 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/b69.log 2>&1

@@ -755,8 +755,36 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
       wa.gb[0] = (__half*)c->G(si, c->find("b1"));
       wa.gb[1] = (__half*)c->G(si, c->find("b0"));
     }
-    KScope ks_(c, HDP_K_RECUR_BWD, 1, s);
-    CK_CUDA(hdp::launch_recur2_bwd(wa, s));
+    static unsigned long long* b2trace = nullptr;  // debug: HDP_RECUR_TRACE=1 in profile (eager) mode
+    const bool want_trace = c->prof && getenv("HDP_RECUR_TRACE") && getenv("HDP_RECUR_TRACE")[0] == '1' && T <= 8192;
+    if (want_trace) {
+      if (!b2trace) CK_CUDA(cudaMalloc(&b2trace, 3 * 8192 * 5 * sizeof(unsigned long long)));
+      wa.trace = b2trace;
+    }
+    {
+      KScope ks_(c, HDP_K_RECUR_BWD, 1, s);
+      CK_CUDA(hdp::launch_recur2_bwd(wa, s));
+    }
+    if (want_trace) {
+      std::vector<unsigned long long> h((size_t)3 * T * 5);
+      CK_CUDA(cudaStreamSynchronize(s));
+      CK_CUDA(cudaMemcpy(h.data(), b2trace, h.size() * 8, cudaMemcpyDeviceToHost));
+      const char* names[3] = {"Q1", "Q0", "X"};
+      const unsigned long long t00 = h[(size_t)(T - 1) * 5];
+      for (int role = 0; role < 3; ++role) {
+        double ph[4] = {0, 0, 0, 0}, step = 0;
+        int n = 0;
+        for (int t = T - 2; t >= 1; --t) {
+          const unsigned long long* r = &h[((size_t)role * T + t) * 5];
+          for (int q = 0; q < 4; ++q) ph[q] += (double)(r[q + 1] - r[q]);
+          step += (double)(h[((size_t)role * T + t - 1) * 5] - r[0]);
+          ++n;
+        }
+        fprintf(stderr, "[hdp trace] bwd wavefront %s: per step ns: %.0f %.0f %.0f %.0f | step %.0f | t=T-2 starts at +%.0f ns, t=0 ends at +%.0f\n",
+                names[role], ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, step / n,
+                (double)(h[((size_t)role * T + T - 2) * 5] - t00), (double)(h[((size_t)role * T) * 5 + 4] - t00));
+      }
+    }
   } else if (wave) {
     // layer 0: already done by the wavefront launch of the layer-1 segment
   } else if (!f32 && c->persistent && hdp::recur_bwd_supported(B, (int)hp)) {

@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(512, 1)
         ptx::mma_commit(barM);
       }
       __syncwarp();
-      ptx::mbar_wait(barM, (t - 1) & 1);
+      ptx::mbar_wait_relaxed(barM, (t - 1) & 1);
       ptx::tc_fence_after();
     }
 
@@ -431,7 +431,7 @@ __global__ void __launch_bounds__(128, 1)
         ptx::mma_commit(barM);
       }
       __syncwarp();
-      ptx::mbar_wait(barM, (T - 2 - t) & 1);
+      ptx::mbar_wait_relaxed(barM, (T - 2 - t) & 1);
       ptx::tc_fence_after();
     }
     // (4) epilogue: dh_rec from TMEM, cell backward, dA_t stores
@@ -662,7 +662,7 @@ __global__ void __launch_bounds__(512, 1)
         ptx::mma_commit(barM);
       }
       __syncwarp();
-      ptx::mbar_wait(barM, (t - 1) & 1);
+      ptx::mbar_wait_relaxed(barM, (t - 1) & 1);
       ptx::tc_fence_after();
       fphase[p] ^= 1u;
       if (threadIdx.x == 0 && t + 2 <= T - 1) ptx::mbar_arrive_expect_tx(fullH + p, total_bytes);
@@ -860,7 +860,7 @@ __global__ void __launch_bounds__(128, 1)
         ptx::mma_commit(barM);
       }
       __syncwarp();
-      ptx::mbar_wait(barM, (T - 2 - t) & 1);
+      ptx::mbar_wait_relaxed(barM, (T - 2 - t) & 1);
       ptx::tc_fence_after();
       fphase[p] ^= 1u;
       // re-arm slot p for its next use (peers can deliver into it only after
@@ -968,6 +968,7 @@ struct __align__(64) Bwd2Params {
   __half* gb[2];        // db1, db0
   unsigned* q0done;     // [nbg][32]: layer-0 steps published (x G CTAs)
   int Ip0, wtiles;
+  unsigned long long* trace;  // debug: [Q1, Q0, X][T][5] stamps of CTA 0 / group 0, nullable
 };
 
 // Weight-gradient role: one CTA per (matrix, 128-gate-row tile) accumulates over all
@@ -1140,7 +1141,9 @@ __device__ __forceinline__ void bwd_proj_role(const Bwd2Params& P, int grp) {
   __syncthreads();
   const uint32_t idesc = ptx::idesc_f16_f32(64, Bc, 1, 0);
   uint32_t ph = 0;
+  unsigned long long* xtr = (P.trace && rank == 0 && grp == 0 && threadIdx.x == 0) ? P.trace + (size_t)2 * T * 5 : nullptr;
   for (int t = T - 1; t >= 0; --t) {
+    if (xtr) xtr[t * 5 + 0] = ptx::globaltimer_ns();
     if (threadIdx.x == 0) {
       // dA1_t published by every layer-1 CTA of my batch group
       const unsigned* f = P.q1done + grp * 32;
@@ -1169,9 +1172,11 @@ __device__ __forceinline__ void bwd_proj_role(const Bwd2Params& P, int grp) {
       ptx::mma_commit(barM);
     }
     __syncwarp();
-    ptx::mbar_wait(barM, ph);
+    if (xtr) xtr[t * 5 + 1] = ptx::globaltimer_ns();
+    ptx::mbar_wait_relaxed(barM, ph);
     ph ^= 1u;
     ptx::tc_fence_after();
+    if (xtr) xtr[t * 5 + 2] = ptx::globaltimer_ns();
     float* out = P.dX1 + (size_t)t * B * hp;
 #pragma unroll
     for (int ch = 0; ch < NC; ++ch) {
@@ -1200,9 +1205,11 @@ __device__ __forceinline__ void bwd_proj_role(const Bwd2Params& P, int grp) {
     }
     ptx::tc_fence_before();
     __syncthreads();  // MMA reads of sA done (barM) and all dX1 stores issued
+    if (xtr) xtr[t * 5 + 3] = ptx::globaltimer_ns();
     if (threadIdx.x == 0) {
       release_add(P.xdone + (grp * 8 + rank) * 32, 1u);
     }
+    if (xtr) xtr[t * 5 + 4] = ptx::globaltimer_ns();
   }
   ptx::tc_fence_after();
   __syncthreads();
@@ -1229,10 +1236,10 @@ __global__ void __launch_bounds__(128, 1)
   const __half* __restrict__ gates = P.q[qi].gates;
   const float* __restrict__ Cst = P.q[qi].C;
   __half* __restrict__ dA = P.q[qi].dA;
-  unsigned long long* __restrict__ trace = nullptr;
+  unsigned long long* __restrict__ trace = P.trace ? P.trace + (size_t)qi * T * 5 : nullptr;
   constexpr int Bc = 16 * NC;
-  // optional phase trace (CTA (0,0), thread 0): [t][5] globaltimer stamps
-  const bool tr = trace != nullptr && blockIdx.x == 0 && blockIdx.y == 0 && threadIdx.x == 0;
+  // optional phase trace (CTA 0 of batch group 0, thread 0): [t][5] globaltimer stamps
+  const bool tr = trace != nullptr && blockIdx.x == 0 && grp == 0 && threadIdx.x == 0;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int fourhp = 4 * hp;
@@ -1358,7 +1365,7 @@ __global__ void __launch_bounds__(128, 1)
         ptx::mma_commit(barM);
       }
       __syncwarp();
-      ptx::mbar_wait(barM, (T - 2 - t) & 1);
+      ptx::mbar_wait_relaxed(barM, (T - 2 - t) & 1);
       ptx::tc_fence_after();
       fphase[p] ^= 1u;
       // re-arm slot p for its next use (peers can deliver into it only after
@@ -1420,11 +1427,11 @@ __global__ void __launch_bounds__(128, 1)
     }
     ptx::tc_fence_before();
     ptx::fence_async_smem();  // staging writes (generic) -> bulk copy reads (async proxy)
-    if (qi == 0 || P.wtiles) fence_proxy_async();  // global dA_t stores -> TMA reads (projection / wgrad roles)
     __syncthreads();
-    if (threadIdx.x == 64 && (qi == 0 || P.wtiles)) {  // not a pusher: the release waits for the stores to drain
-      release_add((qi == 0 ? P.q1done : P.q0done) + grp * 32, 1u);
-    }
+    // publish dA_t to the projection / weight-gradient roles: one release (cumulative over
+    // the CTA's stores via the barrier); the consumers order their TMA reads after their
+    // acquire with a consumer-side fence.proxy.async
+    if (threadIdx.x == 64 && (qi == 0 || P.wtiles)) release_add((qi == 0 ? P.q1done : P.q0done) + grp * 32, 1u);
     if (tr) trace[t * 5 + 3] = ptx::globaltimer_ns();
     // push dA_t (consumed by step t-1) into every peer's sA[t & 1]: one bulk copy per peer.
     // WAR: a peer writes sA[p] of step s only after consuming my dA_{s+1}, which I produce
@@ -1625,7 +1632,7 @@ __global__ void __launch_bounds__(BC * 16, 1)
         issue_mma(p);
       }
       __syncwarp();
-      ptx::mbar_wait(barM, mph);
+      ptx::mbar_wait_relaxed(barM, mph);
       mph ^= 1u;
       ptx::tc_fence_after();
       fph[p] ^= 1u;
@@ -1683,7 +1690,7 @@ __global__ void __launch_bounds__(BC * 16, 1)
           issue_mma(pp);
         }
         __syncwarp();
-        ptx::mbar_wait(barM, mph);
+        ptx::mbar_wait_relaxed(barM, mph);
         mph ^= 1u;
         ptx::tc_fence_after();
         fph[pp] ^= 1u;
@@ -1811,7 +1818,29 @@ struct __align__(64) Fwd2Params {
 };
 
 
-template <int NCI>
+// Forward roles' per-step MMAs for issuing warp W of 4, K-steps known at compile time:
+// warp-uniform, fully unrolled, one elected lane issues (k = W, W+4, ... < NKS; both
+// M=128 halves of the 256-row A slice; accumulator (half, W)).
+template <int NKS, int W>
+__device__ __forceinline__ void fwd_issue_unrolled(uint32_t tbase, uint32_t aU, uint32_t aH, int nkb, int Bc,
+                                                   int nacc, uint32_t idesc, bool acc0, uint64_t* barM) {
+  const uint64_t ad0 = ptx::smem_desc_sw128(aU, 0, 1024), bd0 = ptx::smem_desc_sw128(aH, 0, 1024);
+#pragma unroll
+  for (int k = W; k < NKS; k += 4) {
+    const int kb = k >> 2, kk = k & 3;
+    const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kk * 32) >> 4);
+#pragma unroll
+    for (int h2 = 0; h2 < 2; ++h2) {
+      const uint64_t ad = ad0 + (uint64_t)(((h2 * nkb + kb) * 16384 + kk * 32) >> 4);
+      if (ptx::elect_one_sync())
+        ptx::mma_f16(tbase + (h2 * nacc + W) * Bc, ad, bd, idesc, (k >= 4 || (W == 0 && acc0)) ? 1u : 0u);
+    }
+  }
+  if (ptx::elect_one_sync()) ptx::mma_commit(barM);
+  __syncwarp();
+}
+
+template <int NCI, int NKS>
 __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__ Fwd2Params P) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -1910,6 +1939,27 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
     }
     ptx::mma_commit(barM);
   };
+  int t_cur = 0;  // (phase trace only)
+  // wait for the step's B operand in slot p, then this warp's share of the MMAs
+  auto issue_step = [&](int p, bool acc0) {
+    if (NKS == nk16 && nis == 4) {
+      ptx::mbar_wait(fullH + p, fphase[p]);
+      ptx::tc_fence_after();
+      if (lane == 0) TR(t_cur, 1);
+      const uint32_t aU = ptx::smem_u32(sU), aH = sH_addr + p * hbuf;
+      switch (warp) {
+        case 0: fwd_issue_unrolled<NKS, 0>(tbase, aU, aH, nkb, Bc, nacc, idesc, acc0, barM); break;
+        case 1: fwd_issue_unrolled<NKS, 1>(tbase, aU, aH, nkb, Bc, nacc, idesc, acc0, barM); break;
+        case 2: fwd_issue_unrolled<NKS, 2>(tbase, aU, aH, nkb, Bc, nacc, idesc, acc0, barM); break;
+        default: fwd_issue_unrolled<NKS, 3>(tbase, aU, aH, nkb, Bc, nacc, idesc, acc0, barM); break;
+      }
+    } else if (lane == 0) {
+      ptx::mbar_wait(fullH + p, fphase[p]);
+      ptx::tc_fence_after();
+      TR(t_cur, 1);
+      issue_mma(p);
+    }
+  };
   auto load_acc = [&](float (&v)[16], int c0, int nacc_used) {
     const uint32_t ta = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + hf * nacc * Bc + c0;
     ptx::tmem_ld16(ta, v);
@@ -1939,20 +1989,16 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
     }
     for (int t = 0; t < T; ++t) {
       const int p = t & 1;
+      t_cur = t;
       TR(t, 0);
-      if (lane == 0 && warp < nis) {
-        ptx::mbar_wait(fullH + p, fphase[p]);
-        ptx::tc_fence_after();
-        TR(t, 1);
-        issue_mma(p);
-      }
+      if (warp < nis) issue_step(p, false);
       // prefetch h0_{t+1} now if R0 already published it (sH[p^1] was read by MMA t-1, complete)
       if (threadIdx.x == 0 && t + 1 < T) {
         if (acquire_ld(r0f) >= (unsigned)(G * (t + 2))) load_h0(t + 1);
         else pending = true;
       }
       __syncwarp();
-      ptx::mbar_wait(barM, t & 1);
+      ptx::mbar_wait_relaxed(barM, t & 1);
       ptx::tc_fence_after();
       fphase[p] ^= 1u;
       TR(t, 2);
@@ -2043,6 +2089,7 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
     // by a thread that issues no MMAs: TMA issued by an MMA issuer measurably delays its commit
     const int pf_thr = 128;
     for (int t = 0; t < T; ++t) {
+      t_cur = t;
       TR(t, 0);
       if (!PIPE) load_gx(t, gx);
       if (threadIdx.x == pf_thr && t + 1 < T) {
@@ -2067,15 +2114,10 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
       if (fx && t == 0 && lane == 0 && warp > 0 && warp < nis) ptx::mbar_arrive(barM);
       if (t > 0) {
         const int p = (t - 1) & 1;
-        if (lane == 0 && warp < nis) {
-          ptx::mbar_wait(fullH + p, fphase[p]);
-          ptx::tc_fence_after();
-          TR(t, 1);
-          issue_mma(p);
-        }
+        if (warp < nis) issue_step(p, fx);
         if (PIPE && t + 1 < T) load_gx(t + 1, gxn);
         __syncwarp();
-        ptx::mbar_wait(barM, mph);
+        ptx::mbar_wait_relaxed(barM, mph);
         mph ^= 1u;
         ptx::tc_fence_after();
         fphase[p] ^= 1u;
@@ -2084,7 +2126,7 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
         if (PIPE && t + 1 < T) load_gx(t + 1, gxn);
         if (fx) {
           __syncwarp();
-          ptx::mbar_wait(barM, mph);
+          ptx::mbar_wait_relaxed(barM, mph);
           mph ^= 1u;
           ptx::tc_fence_after();
         }
@@ -2271,8 +2313,15 @@ size_t w2f_fuse_bytes(int Bc) { return 32768 + 2 * (size_t)Bc * 128; }
 struct W2Plan {
   int Bc = 0, nbg = 0, cgN = 0, nci = 0, fuse = 0;
 };
-const void* recur2f_fn(int nci) {
-  return nci == 1 ? (const void*)recur2f_kernel<1> : nci == 2 ? (const void*)recur2f_kernel<2> : nullptr;
+// K-step counts with an unrolled MMA-issue instantiation (h_p = 208, 256); others generic
+template <int NCI>
+const void* recur2f_fn_nks(int nk16) {
+  return nk16 == 13 ? (const void*)recur2f_kernel<NCI, 13>
+       : nk16 == 16 ? (const void*)recur2f_kernel<NCI, 16> : (const void*)recur2f_kernel<NCI, 0>;
+}
+const void* recur2f_fn(int nci, int hp) {
+  const int nk16 = (hp + 15) / 16;
+  return nci == 1 ? recur2f_fn_nks<1>(nk16) : nci == 2 ? recur2f_fn_nks<2>(nk16) : nullptr;
 }
 bool plan_w2f(int B, int hp, W2Plan* out) {
   static std::map<std::pair<int, int>, W2Plan> cache;
@@ -2301,7 +2350,7 @@ bool plan_w2f(int B, int hp, W2Plan* out) {
         smem += w2f_fuse_bytes(Bc);
         p.fuse = 1;
       }
-      const void* fn = recur2f_fn(p.nci);
+      const void* fn = recur2f_fn(p.nci, hp);
       if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) break;
       cudaLaunchConfig_t cfg = {};
       cfg.gridDim = dim3(G, 3 * nbg);
@@ -2407,7 +2456,7 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(a.flags, 0, (16 * 32 + 16 * 8 * 32) * sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
     void* args[] = {&P};
-    return launch_cluster(recur2f_fn(pl.nci), dim3(G, 3 * pl.nbg), dim3(256 * pl.cgN),
+    return launch_cluster(recur2f_fn(pl.nci, a.hp), dim3(G, 3 * pl.nbg), dim3(256 * pl.cgN),
                           fwd_cl_smem(a.hp, pl.Bc, 8 * pl.cgN) + (pl.fuse ? w2f_fuse_bytes(pl.Bc) : 0), G, s, args);
   }
   CUtensorMap mU0, mW1, mU1;
@@ -2600,6 +2649,7 @@ cudaError_t launch_recur2_bwd(const Recur2BwdArgs& a, cudaStream_t s) {
     P.Ip0 = a.Ip0;
     P.wtiles = 4 * ((4 * a.hp + 127) / 128);
   }
+  P.trace = a.trace;
   cudaError_t e = cudaMemsetAsync(a.flags, 0, (2 * 16 * 32 + 16 * 8 * 32) * sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
   void* args[] = {&P};

@@ -71,6 +71,7 @@ struct Recur2BwdArgs {
   int Ip0 = 0;
   __half* gW[4] = {nullptr, nullptr, nullptr, nullptr};  // dU1, dW1, dU0, dW0
   __half* gb[2] = {nullptr, nullptr};                    // db1, db0
+  unsigned long long* trace = nullptr;  // debug: [Q1, Q0, X][T][5] timestamps, nullable
 };
 bool recur2_bwd_supported(int B, int hp);
 bool recur2_bwd_wgrad(int B, int hp, int Ip0);  // the launch can also produce the A8 weight gradients
