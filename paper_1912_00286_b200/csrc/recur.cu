@@ -1815,25 +1815,49 @@ struct __align__(64) Fwd2Params {
   unsigned long long* trace;
   int T, B, Bc, hp, nbg, fuse_x, r1_tma;
   int region;          // the 32 KB + 2 x Bc x 128 B region (fused projection / R1 staging) exists
+  const __half* Ag[3]; // row-major U0, W1, U1 [4hp][hp] (A operands copied into TMEM, NKS != 0)
+  const __half* W0g;   // W0 [4hp][Ip0] (fused projection, TMEM copy)
+  int Ip0;
 };
+
+// Copy rows [row0 + half*128 + 32*quadrant + lane] of a row-major fp16 matrix (ncols K
+// elements, ld elements) into TMEM columns [col, col + ceil(K/32)*16) of this warp's lane
+// quadrant: two K-elements per 32-bit column, zero padded (tcgen05.mma A-operand layout).
+__device__ __forceinline__ void tmem_load_rows(uint32_t taddr_quadrant_col, const __half* __restrict__ src, int row,
+                                               int nrows, int K, int ld) {
+  const bool ok = row < nrows;
+  for (int c0 = 0; c0 < (K + 31) / 32 * 16; c0 += 16) {
+    uint32_t v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int kk = 2 * (c0 + j);
+      const uint32_t lo = (ok && kk < K) ? __half_as_ushort(src[(size_t)row * ld + kk]) : 0u;
+      const uint32_t hi = (ok && kk + 1 < K) ? __half_as_ushort(src[(size_t)row * ld + kk + 1]) : 0u;
+      v[j] = lo | (hi << 16);
+    }
+    ptx::tmem_st16(taddr_quadrant_col + c0, v);
+  }
+  ptx::tmem_wait_st();
+}
 
 
 // Forward roles' per-step MMAs for issuing warp W of 4, K-steps known at compile time:
 // warp-uniform, fully unrolled, one elected lane issues (k = W, W+4, ... < NKS; both
 // M=128 halves of the 256-row A slice; accumulator (half, W)).
-template <int NKS, int W>
-__device__ __forceinline__ void fwd_issue_unrolled(uint32_t tbase, uint32_t aU, uint32_t aH, int nkb, int Bc,
+// A in TMEM (tA: half h2's rows at columns tA + h2*KCP, 8 columns per K-step of 16).
+template <int NKS, int W, int NIS>
+__device__ __forceinline__ void fwd_issue_unrolled(uint32_t tbase, uint32_t tA, int KCP, uint32_t aH, int Bc,
                                                    int nacc, uint32_t idesc, bool acc0, uint64_t* barM) {
-  const uint64_t ad0 = ptx::smem_desc_sw128(aU, 0, 1024), bd0 = ptx::smem_desc_sw128(aH, 0, 1024);
+  const uint64_t bd0 = ptx::smem_desc_sw128(aH, 0, 1024);
 #pragma unroll
-  for (int k = W; k < NKS; k += 4) {
+  for (int k = W; k < NKS; k += NIS) {
     const int kb = k >> 2, kk = k & 3;
     const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kk * 32) >> 4);
 #pragma unroll
     for (int h2 = 0; h2 < 2; ++h2) {
-      const uint64_t ad = ad0 + (uint64_t)(((h2 * nkb + kb) * 16384 + kk * 32) >> 4);
       if (ptx::elect_one_sync())
-        ptx::mma_f16(tbase + (h2 * nacc + W) * Bc, ad, bd, idesc, (k >= 4 || (W == 0 && acc0)) ? 1u : 0u);
+        ptx::mma_f16_ts(tbase + (h2 * nacc + W) * Bc, tA + h2 * KCP + k * 8, bd, idesc,
+                        (k >= NIS || (W == 0 && acc0)) ? 1u : 0u);
     }
   }
   if (ptx::elect_one_sync()) ptx::mma_commit(barM);
@@ -1877,10 +1901,15 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
   const int unit = grow >> 2;
   const bool unit_ok = unit < hp;
   const int fourhp = 4 * hp;
-  const int nacc = Bc <= 32 ? 4 : Bc <= 64 ? 2 : 1;
+  // with the A slice in TMEM (NKS != 0) two issuing warps reach the MMA floor; two
+  // accumulators per half also halve the epilogue's TMEM reads
+  const int nacc = NKS != 0 ? 2 : (Bc <= 32 ? 4 : Bc <= 64 ? 2 : 1);
   const int nis = min(nacc, nk16);
   const int ac = 2 * nacc * Bc;
-  const uint32_t tcols = ac <= 32 ? 32 : ac <= 64 ? 64 : ac <= 128 ? 128 : ac <= 256 ? 256 : 512;
+  // NKS != 0: the role's A slice lives in TMEM (columns [TA, TA + 2*KCP)), fused W0 at TW0
+  constexpr bool TSA = NKS != 0;
+  const int KCP = (hp + 31) / 32 * 16;
+  const uint32_t tcols = TSA ? 512u : (ac <= 32 ? 32u : ac <= 64 ? 64u : ac <= 128 ? 128u : ac <= 256 ? 256u : 512u);
   const int total_bytes = nkb * Bc * 128;
   const bool tr = P.trace != nullptr && rank == 0 && grp == 0 && threadIdx.x == 0;
   unsigned long long* trr = P.trace ? P.trace + (size_t)role * T * 5 : nullptr;
@@ -1902,21 +1931,34 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = *tslot;
+  const uint32_t tA = tbase + 256, tW0 = tbase + 256 + 2 * KCP;
+  if (TSA && cg == 0) {
+    // A slice rows into TMEM: warp (quarter, hf) owns gate rows hf*128 + 32*quarter + lane
+    const uint32_t tq = (static_cast<uint32_t>(quarter * 32) << 16);
+    tmem_load_rows(tA + tq + hf * KCP, P.Ag[role], grow, fourhp, hp, hp);
+    if (fx) tmem_load_rows(tW0 + tq + hf * 16, P.W0g, grow, fourhp, P.Ip0, P.Ip0);  // 16 columns per half
+  }
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
   if (threadIdx.x == 0) {
     if (role != 1) {
       ptx::mbar_arrive_expect_tx(fullH, total_bytes);
       ptx::mbar_arrive_expect_tx(fullH + 1, total_bytes);
     }
-    ptx::mbar_arrive_expect_tx(barU, 2 * nkb * 16384 + (fx ? 32768 : 0));
-    for (int h2 = 0; h2 < 2; ++h2)
-      for (int kb = 0; kb < nkb; ++kb)
-        ptx::tma_load_2d(sU + (h2 * nkb + kb) * 16384, &P.tmA[role], barU, kb * 64, row0 + h2 * 128);
+    if (!TSA) {
+      ptx::mbar_arrive_expect_tx(barU, 2 * nkb * 16384 + (fx ? 32768 : 0));
+      for (int h2 = 0; h2 < 2; ++h2)
+        for (int kb = 0; kb < nkb; ++kb)
+          ptx::tma_load_2d(sU + (h2 * nkb + kb) * 16384, &P.tmA[role], barU, kb * 64, row0 + h2 * 128);
+      if (fx)
+        for (int h2 = 0; h2 < 2; ++h2) ptx::tma_load_2d(sW0 + h2 * 16384, &P.tmW0, barU, 0, row0 + h2 * 128);
+    }
     if (fx) {
-      for (int h2 = 0; h2 < 2; ++h2) ptx::tma_load_2d(sW0 + h2 * 16384, &P.tmW0, barU, 0, row0 + h2 * 128);
       ptx::mbar_arrive_expect_tx(barX, Bc * 128);
       ptx::tma_load_2d(sXin, &P.tmX0, barX, 0, col0);
     }
-    ptx::mbar_wait(barU, 0);
+    if (!TSA) ptx::mbar_wait(barU, 0);
   }
   ptx::cluster_arrive();
   ptx::cluster_wait();
@@ -1942,17 +1984,15 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
   int t_cur = 0;  // (phase trace only)
   // wait for the step's B operand in slot p, then this warp's share of the MMAs
   auto issue_step = [&](int p, bool acc0) {
-    if (NKS == nk16 && nis == 4) {
+    if (NKS == nk16 && nis == 2) {
       ptx::mbar_wait(fullH + p, fphase[p]);
       ptx::tc_fence_after();
       if (lane == 0) TR(t_cur, 1);
-      const uint32_t aU = ptx::smem_u32(sU), aH = sH_addr + p * hbuf;
-      switch (warp) {
-        case 0: fwd_issue_unrolled<NKS, 0>(tbase, aU, aH, nkb, Bc, nacc, idesc, acc0, barM); break;
-        case 1: fwd_issue_unrolled<NKS, 1>(tbase, aU, aH, nkb, Bc, nacc, idesc, acc0, barM); break;
-        case 2: fwd_issue_unrolled<NKS, 2>(tbase, aU, aH, nkb, Bc, nacc, idesc, acc0, barM); break;
-        default: fwd_issue_unrolled<NKS, 3>(tbase, aU, aH, nkb, Bc, nacc, idesc, acc0, barM); break;
-      }
+      const uint32_t aH = sH_addr + p * hbuf;
+      if (warp == 0)
+        fwd_issue_unrolled<NKS, 0, 2>(tbase, tA, KCP, aH, Bc, nacc, idesc, acc0, barM);
+      else
+        fwd_issue_unrolled<NKS, 1, 2>(tbase, tA, KCP, aH, Bc, nacc, idesc, acc0, barM);
     } else if (lane == 0) {
       ptx::mbar_wait(fullH + p, fphase[p]);
       ptx::tc_fence_after();
@@ -2106,9 +2146,13 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
         ptx::tc_fence_after();
         const uint64_t bd = ptx::smem_desc_sw128(ptx::smem_u32(sXin + (t & 1) * Bc * 128), 0, 1024);
 #pragma unroll
-        for (int h2 = 0; h2 < 2; ++h2)
-          ptx::mma_f16(tbase + (h2 * nacc) * Bc, ptx::smem_desc_sw128(ptx::smem_u32(sW0 + h2 * 16384), 0, 1024), bd,
-                       idesc, 0u);
+        for (int h2 = 0; h2 < 2; ++h2) {
+          if (TSA)
+            ptx::mma_f16_ts(tbase + (h2 * nacc) * Bc, tW0 + h2 * 16, bd, idesc, 0u);
+          else
+            ptx::mma_f16(tbase + (h2 * nacc) * Bc, ptx::smem_desc_sw128(ptx::smem_u32(sW0 + h2 * 16384), 0, 1024), bd,
+                         idesc, 0u);
+        }
         if (t == 0) ptx::mma_commit(barM);
       }
       if (fx && t == 0 && lane == 0 && warp > 0 && warp < nis) ptx::mbar_arrive(barM);
@@ -2320,7 +2364,8 @@ const void* recur2f_fn_nks(int nk16) {
        : nk16 == 16 ? (const void*)recur2f_kernel<NCI, 16> : (const void*)recur2f_kernel<NCI, 0>;
 }
 const void* recur2f_fn(int nci, int hp) {
-  const int nk16 = (hp + 15) / 16;
+  const char* e = getenv("HDP_WAVEFRONT_TS");
+  const int nk16 = (e && e[0] == '0') ? -1 : (hp + 15) / 16;  // -1: the generic (SMEM-A) instantiation
   return nci == 1 ? recur2f_fn_nks<1>(nk16) : nci == 2 ? recur2f_fn_nks<2>(nk16) : nullptr;
 }
 bool plan_w2f(int B, int hp, W2Plan* out) {
@@ -2383,7 +2428,9 @@ bool w2f_split_enabled() {
 
 bool recur2_fwd_fuses_x(int B, int hp, int Ip0) {
   W2Plan p;
-  return recur2_fwd_supported(B, hp) && w2f_split_enabled() && plan_w2f(B, hp, &p) && p.fuse && Ip0 <= 64 &&
+  // (with the A slices in TMEM, columns [256, 256 + 2*KCP) + 2 x 16 for W0 must fit in 512)
+  return recur2_fwd_supported(B, hp) && w2f_split_enabled() && plan_w2f(B, hp, &p) && p.fuse && Ip0 <= 16 &&
+         256 + 2 * ((hp + 31) / 32 * 16) + 32 <= 512 &&
          !(getenv("HDP_WAVEFRONT_FUSEX") && getenv("HDP_WAVEFRONT_FUSEX")[0] == '0');
 }
 
@@ -2449,6 +2496,11 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
     }
     if (!a.a1x || !a.flags) return cudaErrorInvalidValue;
     P.region = pl.fuse;
+    P.Ag[0] = a.U0;
+    P.Ag[1] = a.W1;
+    P.Ag[2] = a.U1;
+    P.W0g = a.W0;
+    P.Ip0 = a.Ip0;
     P.r1_tma = pl.fuse && (size_t)2 * pl.Bc * 1024 <= w2f_fuse_bytes(pl.Bc);
     if (P.r1_tma && encode_tmap_2d(&P.tmG1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.a1x, 4 * hp, (uint64_t)a.T * a.B,
                                    4 * hp * 4, 256, pl.Bc, CU_TENSOR_MAP_SWIZZLE_NONE))

@@ -24,7 +24,7 @@ __device__ __forceinline__ void mma_ts(uint32_t d, uint32_t a_tmem, uint64_t bde
                :: "r"(d), "r"(a_tmem), "l"(bdesc), "r"(idesc), "r"(acc) : "memory");
 }
 
-constexpr int M = 128, N = 16, K = 208, NK = K / 16, KB = (K + 63) / 64;
+constexpr int M = 128, N = 16, K = 208, NK = K / 16, KB = (K + 63) / 64;  // (M=64 modes use rows 0..63)
 
 // A: row-major [M][K] fp16; B: row-major [N][K] fp16
 __global__ void __launch_bounds__(128, 1) k(const __half* A, const __half* B, float* D, int mode, int reps,
@@ -51,20 +51,23 @@ __global__ void __launch_bounds__(128, 1) k(const __half* A, const __half* B, fl
     *reinterpret_cast<__half*>(sB + kb * 2048 + r * 128 + ((c ^ (r & 7)) << 4) + e * 2) = v;
   }
   ptx::fence_async_smem();
-  if (threadIdx.x == 0) { ptx::mbar_init(bar, mode >= 2 ? 4 : 1); ptx::fence_mbar_init(); }
+  if (threadIdx.x == 0) { ptx::mbar_init(bar, (mode == 2 || mode == 3) ? 4 : 1); ptx::fence_mbar_init(); }
   if (warp == 0) ptx::tmem_alloc(tslot, 256);
   ptx::tc_fence_before(); __syncthreads(); ptx::tc_fence_after();
   const uint32_t tbase = *tslot;                 // cols [0,16): D ; [128, 128+K/2): A
   const uint32_t tA = tbase + 128;
   // A rows into TMEM: thread = row (lane quadrant = warp), 2 fp16 per column
+  // mode 6: M=64 with row 16q+i placed in lane 32q+i (the M=64 accumulator layout)
   {
-    const int r = warp * 32 + lane;
+    int r = warp * 32 + lane;
+    if (mode == 6) r = (lane < 16) ? warp * 16 + lane : 1000;  // lanes 16..31 of each quadrant unused
     for (int c0 = 0; c0 < (K / 2 + 15) / 16 * 16; c0 += 16) {
       uint32_t v[16];
       for (int j = 0; j < 16; ++j) {
         const int kk = 2 * (c0 + j);
-        const __half lo = kk < K ? A[r * K + kk] : __float2half(0.f);
-        const __half hi = kk + 1 < K ? A[r * K + kk + 1] : __float2half(0.f);
+        const bool okr = r < M;
+        const __half lo = (okr && kk < K) ? A[r * K + kk] : __float2half(0.f);
+        const __half hi = (okr && kk + 1 < K) ? A[r * K + kk + 1] : __float2half(0.f);
         v[j] = (uint32_t)__half_as_ushort(lo) | ((uint32_t)__half_as_ushort(hi) << 16);
       }
       tmem_st16(tA + (static_cast<uint32_t>(warp * 32) << 16) + c0, v);
@@ -72,13 +75,13 @@ __global__ void __launch_bounds__(128, 1) k(const __half* A, const __half* B, fl
     tmem_st_wait();
   }
   ptx::tc_fence_before(); __syncthreads(); ptx::tc_fence_after();
-  const uint32_t idesc = ptx::idesc_f16_f32(M, N, 0, 0);
+  const uint32_t idesc = ptx::idesc_f16_f32(mode >= 4 ? 64 : M, N, 0, 0);
   unsigned long long tsum = 0;
   for (int rep = 0; rep < reps; ++rep) {
     __syncthreads();
     const unsigned long long t0 = ptx::globaltimer_ns();
-    const int nis = mode >= 2 ? 4 : 1;      // issuing warps (each its own accumulator set)
-    const int halves = mode >= 2 ? 2 : 1;   // 2 x M=128 (the forward's 256 gate rows: A reused)
+    const int nis = (mode == 2 || mode == 3) ? 4 : 1;      // issuing warps (each its own accumulator set)
+    const int halves = (mode == 2 || mode == 3) ? 2 : 1;   // 2 x M=128 (the forward's 256 gate rows: A reused)
     if (lane == 0 && warp < nis) {
       for (int s = warp; s < NK; s += nis) {
         const int kb = s / 4, kq = s % 4;
@@ -86,7 +89,7 @@ __global__ void __launch_bounds__(128, 1) k(const __half* A, const __half* B, fl
         for (int h2 = 0; h2 < halves; ++h2) {
           const uint32_t dacc = tbase + (h2 * 4 + (nis > 1 ? warp : 0)) * 16;
           const uint32_t acc = s >= nis;
-          if ((mode & 1) == 0) {
+          if (mode == 0 || mode == 2 || mode == 4) {
             const uint64_t ad = ptx::smem_desc_sw128(ptx::smem_u32(sA) + kb * 16384 + kq * 32, 0, 1024);
             ptx::mma_f16(dacc, ad, bd, idesc, acc);
           } else {
@@ -103,7 +106,11 @@ __global__ void __launch_bounds__(128, 1) k(const __half* A, const __half* B, fl
   }
   float v[16];
   ptx::tmem_ld16(tbase + (static_cast<uint32_t>(warp * 32) << 16), v);
-  for (int j = 0; j < 16; ++j) D[(warp * 32 + lane) * N + j] = v[j];
+  if (mode >= 4) {
+    if (lane < 16) for (int j = 0; j < 16; ++j) D[(warp * 16 + lane) * N + j] = v[j];
+  } else {
+    for (int j = 0; j < 16; ++j) D[(warp * 32 + lane) * N + j] = v[j];
+  }
   if (threadIdx.x == 0) *tout = tsum / reps;
   ptx::tc_fence_before(); __syncthreads();
   if (warp == 0) { ptx::tc_fence_after(); ptx::tmem_dealloc(tbase, 256); }
@@ -121,17 +128,19 @@ int main() {
   cudaMemcpy(dA, hA.data(), M * K * 2, cudaMemcpyHostToDevice); cudaMemcpy(dB, hB.data(), N * K * 2, cudaMemcpyHostToDevice);
   const int smem = KB * 16384 + KB * 2048 + 2048;
   cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, smem);
-  for (int mode = 0; mode < 4; ++mode) {
+  for (int mode = 0; mode < 7; ++mode) {
     cudaMemset(dD, 0, M * N * 4);
     k<<<1, 128, smem>>>(dA, dB, dD, mode, 200, dt);
     cudaError_t e = cudaDeviceSynchronize();
     std::vector<float> hD(M * N); unsigned long long t = 0;
     cudaMemcpy(hD.data(), dD, M * N * 4, cudaMemcpyDeviceToHost); cudaMemcpy(&t, dt, 8, cudaMemcpyDeviceToHost);
     double err = 0, mx = 0;
-    for (int i = 0; i < M * N; ++i) { err = fmax(err, fabs(hD[i] - ref[i])); mx = fmax(mx, fabs(ref[i])); }
-    const char* names[4] = {"SS 1 issuer", "TS 1 issuer", "SS 4 issuers x 2 halves", "TS 4 issuers x 2 halves"};
+    const int rows = mode >= 4 ? 64 : M;
+    for (int i = 0; i < rows * N; ++i) { err = fmax(err, fabs(hD[i] - ref[i])); mx = fmax(mx, fabs(ref[i])); }
+    const char* names[7] = {"SS 1 issuer", "TS 1 issuer", "SS 4 issuers x 2 halves", "TS 4 issuers x 2 halves",
+                            "SS M=64", "TS M=64 row i->lane i", "TS M=64 row 16q+i->lane 32q+i"};
     printf("mode %s: %s  max err %.3e (max |ref| %.3e)  %d MMAs in %llu ns\n", names[mode],
-           cudaGetErrorString(e), mode < 2 ? err : -1.0, mx, NK * (mode >= 2 ? 2 : 1), t);
+           cudaGetErrorString(e), (mode == 2 || mode == 3) ? -1.0 : err, mx, NK * ((mode == 2 || mode == 3) ? 2 : 1), t);
   }
   return 0;
 }
