@@ -535,6 +535,22 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
                   names[role], ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, step / n, (double)(st[0] - t00),
                   (double)(h[((size_t)role * T + T - 1) * 5 + 4] - t00));
         }
+        {
+          double q[3] = {0, 0, 0};
+          int n = 0;
+          for (int t = 2; t < T - 1; ++t) {
+            const unsigned long long* r = &h[((size_t)3 * T + t) * 5];
+            const unsigned long long e0 = h[((size_t)0 * T + t) * 5 + 2];  // R0 TR(t,2): MMA done
+            if (!r[0] || !r[3]) continue;
+            q[0] += (double)(r[0] - e0);
+            q[1] += (double)(r[1] - r[0]);
+            q[2] += (double)(r[2] - r[1]);
+            ++n;
+          }
+          if (n)
+            fprintf(stderr, "[hdp trace] wavefront R0 epilogue: acc load %.0f  act+stage %.0f  cell+stores %.0f ns\n",
+                    q[0] / n, q[1] / n, q[2] / n);
+        }
 
       }
       break;

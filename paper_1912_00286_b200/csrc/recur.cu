@@ -1803,6 +1803,10 @@ struct __align__(64) Fwd2Params {
   CUtensorMap tmW0;    // W0 [4hp][Ip0], box 64 x 128 (fused layer-0 input projection)
   CUtensorMap tmX0;    // X0 rows [T B][Ip0], box (64, Bc)
   CUtensorMap tmG1;    // a1x rows [T B][4hp] fp32, box (256, Bc): R1's gate inputs (r1_tma)
+  // R roles' per-step outputs written by TMA stores from shared staging (TSA variant):
+  CUtensorMap tmCo[2];  // C_l rows [T B][hp] fp32, box (64, Bc)
+  CUtensorMap tmHo[2];  // Hs_l rows [(T+1) B][hp] fp16, box (64, Bc), SWIZZLE_128B (= the push staging)
+  CUtensorMap tmGo[2];  // gates_l rows [T B][4hp] fp16, box (256, Bc)
   const float* Gx0;    // [T][B][4hp]
   float* a1x;          // [T][B][4hp]
   const __half* b1;
@@ -2093,6 +2097,14 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
     float* myAct = sAct + warp * 16 * ACT_LD;
     const float gsc = gate == 2 ? 2.f : 1.f;
     const float bias0 = fx && unit_ok ? __half2float(P.b0[grow]) : 0.f;
+    // debug sub-phase stamps of the epilogue (R0 CTA 0 / group 0, thread 0) in trace role slot 3
+    unsigned long long* trx = (tr && li == 0) ? P.trace + (size_t)3 * T * 5 : nullptr;
+    // TSA: the SMEM A region is free -> stage c_t and the gates there and let one thread
+    // (no MMA issue, no push) write them -- and h_t from the push staging -- by TMA stores
+    constexpr bool TST = TSA;
+    float* sCo = reinterpret_cast<float*>(sU);                          // [2][Bc][64] fp32
+    __half* sGo = reinterpret_cast<__half*>(sU + 2 * Bc * 64 * 4);      // [2][Bc][256] fp16
+    const int st_thr = blockDim.x - 32;
     uint32_t mph = 0;
     // gate inputs of step t (layer 0: G_x0 rows from K1, or the bias when the projection
     // is fused; layer 1: a1x rows from P_k once published), loaded one step ahead so
@@ -2200,9 +2212,11 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
 #pragma unroll
           for (int k = 0; k < 16; ++k) v[k] = 0.f;
         }
+        if (trx) trx[t * 5 + 0] = ptx::globaltimer_ns();
 #pragma unroll
         for (int k = 0; k < 16; ++k) myAct[k * ACT_LD + lane] = act_gate(v[k] + gx[ci][k], gsc);
         __syncwarp();
+        if (trx) trx[t * 5 + 1] = ptx::globaltimer_ns();
         if (unit_ok) {
           const int u = lane >> 2;
           const int ul = (r >> 2);
@@ -2217,19 +2231,32 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
             const float cv = f * creg[ci * 4 + q] + i * g;
             creg[ci * 4 + q] = cv;
             const __half hh = __float2half_rn(o * act_gate(cv, 2.f));
-            cout[b * hp + unit] = cv;                   // R5
-            hout[b * hp + unit] = hh;                   // R6
+            if (!TST) {
+              cout[b * hp + unit] = cv;                 // R5
+              hout[b * hp + unit] = hh;                 // R6
+            } else {
+              sCo[((t & 1) * Bc + bl) * 64 + ul] = cv;
+            }
             *reinterpret_cast<__half*>(stg + bl * 128 + ((c ^ (bl & 7)) << 4) + (ul & 7) * 2) = hh;
             __align__(8) __half2 gg[2] = {__halves2half2(__float2half_rn(i), __float2half_rn(f)),
                                           __halves2half2(__float2half_rn(g), __float2half_rn(o))};
-            *reinterpret_cast<uint2*>(gout + b * fourhp + 4 * unit) = *reinterpret_cast<const uint2*>(gg);  // R4
+            if (!TST)
+              *reinterpret_cast<uint2*>(gout + b * fourhp + 4 * unit) = *reinterpret_cast<const uint2*>(gg);  // R4
+            else
+              *reinterpret_cast<uint2*>(sGo + ((t & 1) * Bc + bl) * 256 + 4 * ul) = *reinterpret_cast<const uint2*>(gg);
           }
         }
         __syncwarp();
       }
+      if (trx) trx[t * 5 + 2] = ptx::globaltimer_ns();
+      if (TST && threadIdx.x == st_thr) {
+        // step t-1's stores must have finished reading their staging (rewritten at step t+1)
+        ptx::bulk_wait_group_read0();
+      }
       ptx::tc_fence_before();
       ptx::fence_async_smem();
       __syncthreads();
+      if (trx) trx[t * 5 + 3] = ptx::globaltimer_ns();
       TR(t, 3);
       if (PIPE) {
 #pragma unroll
@@ -2243,7 +2270,26 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
         const uint32_t mb = ptx::mapa(ptx::smem_u32(fullH + (t & 1)), dst);
         ptx::bulk_copy_to_peer(dsta, sX_addr + (t & 1) * Bc * 128, Bc * 128, mb);
       }
-      if (li == 0) {
+      if (TST) {
+        if (threadIdx.x == st_thr) {
+          // c_t, h_t (the swizzled push staging = Hs' SWIZZLE_128B box) and the gates of step t
+          if (li == 0 && t > 0) {
+            // h0_{t-1}'s store (previous group) complete -> publish it to the projection role
+            ptx::bulk_wait_group0();
+            fence_proxy_async();
+            release_add(P.r0done + grp * 32, 1u);
+          }
+          ptx::tma_store_2d(&P.tmCo[li], sCo + (t & 1) * Bc * 64, rank * 64, t * B + col0);
+          ptx::tma_store_2d(&P.tmHo[li], stg, rank * 64, (t + 1) * B + col0);
+          ptx::tma_store_2d(&P.tmGo[li], sGo + (t & 1) * Bc * 256, rank * 256, t * B + col0);
+          ptx::bulk_commit_group();
+          if (li == 0 && t == T - 1) {
+            ptx::bulk_wait_group0();
+            fence_proxy_async();
+            release_add(P.r0done + grp * 32, 1u);
+          }
+        }
+      } else if (li == 0) {
         // publish h0_t to the projection role after the push (off the recurrence's critical
         // path): every thread's Hs0 stores -> async proxy, then one release
         fence_proxy_async();
@@ -2256,6 +2302,7 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
       }
       TR(t, 4);
     }
+    if (TST && threadIdx.x == st_thr) ptx::bulk_wait_group0();  // all stores done before exit
   }
 #undef TR
   ptx::cluster_arrive();
@@ -2495,6 +2542,20 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
       return cudaErrorInvalidValue;
     }
     if (!a.a1x || !a.flags) return cudaErrorInvalidValue;
+    {
+      const uint64_t TB = (uint64_t)a.T * a.B, TB1 = (uint64_t)(a.T + 1) * a.B;
+      __half* hs[2] = {a.Hs0, a.Hs1};
+      float* cs[2] = {a.C0, a.C1};
+      __half* gs[2] = {a.gates0, a.gates1};
+      for (int l = 0; l < 2; ++l)
+        if (encode_tmap_2d(&P.tmCo[l], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, cs[l], hp, TB, hp * 4, 64, pl.Bc,
+                           CU_TENSOR_MAP_SWIZZLE_NONE) ||
+            encode_tmap_2d(&P.tmHo[l], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, hs[l], hp, TB1, hp * 2, 64, pl.Bc,
+                           CU_TENSOR_MAP_SWIZZLE_128B) ||
+            encode_tmap_2d(&P.tmGo[l], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, gs[l], 4 * hp, TB, 4 * hp * 2, 256, pl.Bc,
+                           CU_TENSOR_MAP_SWIZZLE_NONE))
+          return cudaErrorInvalidValue;
+    }
     P.region = pl.fuse;
     P.Ag[0] = a.U0;
     P.Ag[1] = a.W1;
