@@ -2264,8 +2264,9 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
 #pragma unroll
           for (int k = 0; k < 16; ++k) gx[ci][k] = gxn[ci][k];
       }
-      if (t < T - 1 && threadIdx.x < G) {
-        const int dst = threadIdx.x;
+      // pushers: warp 5 (issues no MMAs: async copies from an MMA-issuing thread delay its commits)
+      if (t < T - 1 && threadIdx.x >= 160 && threadIdx.x < 160 + G) {
+        const int dst = threadIdx.x - 160;
         const uint32_t dsta = ptx::mapa(sH_addr + (t & 1) * hbuf + rank * Bc * 128, dst);
         const uint32_t mb = ptx::mapa(ptx::smem_u32(fullH + (t & 1)), dst);
         ptx::bulk_copy_to_peer(dsta, sX_addr + (t & 1) * Bc * 128, Bc * 128, mb);
