@@ -969,6 +969,7 @@ struct __align__(64) Bwd2Params {
   unsigned* q0done;     // [nbg][32]: layer-0 steps published (x G CTAs)
   int Ip0, wtiles;
   unsigned long long* trace;  // debug: [Q1, Q0, X][T][5] stamps of CTA 0 / group 0, nullable
+  CUtensorMap tmdAo[2];       // dA1 / dA0 rows [T*B][4hp], SWIZZLE_128B box (64, Bc): TMA stores from the push staging
 };
 
 // Weight-gradient role: one CTA per (matrix, 128-gate-row tile) accumulates over all
@@ -1216,7 +1217,7 @@ __device__ __forceinline__ void bwd_proj_role(const Bwd2Params& P, int grp) {
   if (warp == 2) ptx::tmem_dealloc(tbase, tcols);
 }
 
-template <int NC>
+template <int NC, int NKQ>
 __global__ void __launch_bounds__(128, 1)
     recur2_bwd_kernel(const __grid_constant__ Bwd2Params P) {
   const int T = P.T, B = P.B, hp = P.hp;
@@ -1265,9 +1266,14 @@ __global__ void __launch_bounds__(128, 1)
   const int ul = warp * 16 + jl;               // unit within my 64-unit slice
   const int unit = j0 + ul;
   const bool unit_ok = unit < hp;
-  constexpr int NACC = Bc <= 32 ? 8 : 4;
+  // NKQ != 0 (h_p = 208): U^T slice in TMEM (A operand, M = 64 layout), 2 issuing warps x
+  // 1 accumulator each; dA_t written by TMA stores from the push staging; warps 2 / 3
+  // push and store (async copies from an MMA-issuing thread delay its commits)
+  constexpr bool TSQ = NKQ != 0;
+  constexpr int NACC = TSQ ? 2 : (Bc <= 32 ? 8 : 4);
   constexpr int AC = NACC * Bc;
-  constexpr uint32_t tcols = AC <= 32 ? 32 : AC <= 64 ? 64 : AC <= 128 ? 128 : 256;
+  constexpr uint32_t tcols = TSQ ? 512u : (AC <= 32 ? 32u : AC <= 64 ? 64u : AC <= 128 ? 128u : 256u);
+  constexpr int NISQ = TSQ ? 2 : 4;
   // bytes every consumer receives per step: all producers' valid K-blocks
   int total_bytes = 0;
   for (int r = 0; r < G; ++r) total_bytes += max(0, min(64, hp - 64 * r)) / 16 * Bc * 128;
@@ -1276,7 +1282,7 @@ __global__ void __launch_bounds__(128, 1)
   if (threadIdx.x == 0) {
     ptx::tma_prefetch(&tmU);
     ptx::mbar_init(barU, 1);
-    ptx::mbar_init(barM, 4);  // one commit per issuing warp
+    ptx::mbar_init(barM, NISQ);  // one commit per issuing warp
     ptx::mbar_init(fullA, 1);
     ptx::mbar_init(fullA + 1, 1);
     ptx::fence_mbar_init();
@@ -1296,6 +1302,31 @@ __global__ void __launch_bounds__(128, 1)
   }
   ptx::cluster_arrive();  // all CTAs resident, barriers initialised and armed
   ptx::cluster_wait();
+  const uint32_t tA = tbase + 64;  // TSQ: A = U^T slice, columns [64, 64 + 2 h_p)
+  if (TSQ) {
+    // sU (MN-major SWIZZLE_128B: row k = 128 B of 64 units, 16-B chunk (unit/8) ^ (k%8)) -> TMEM:
+    // unit 16q + i -> lane 32q + i (i < 16), two K-elements (gate rows) per column
+    const int i = lane & 15;
+    const int u = warp * 16 + i;
+    const uint32_t tq = tA + (static_cast<uint32_t>(warp * 32) << 16);
+    for (int c0 = 0; c0 < 2 * hp; c0 += 16) {
+      uint32_t v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int kk = 2 * (c0 + j), kb = kk >> 6, kr = kk & 63;
+        const uint8_t* row = sU + kb * 8192 + kr * 128;
+        const uint32_t lo = __half_as_ushort(*reinterpret_cast<const __half*>(row + (((u >> 3) ^ (kr & 7)) << 4) + (u & 7) * 2));
+        const uint32_t hi = __half_as_ushort(*reinterpret_cast<const __half*>(row + 128 + (((u >> 3) ^ ((kr + 1) & 7)) << 4) + (u & 7) * 2));
+        v[j] = lane < 16 ? (lo | (hi << 16)) : 0u;
+      }
+      ptx::tmem_st16(tq + c0, v);
+    }
+    ptx::tmem_wait_st();
+    ptx::tc_fence_before();
+    __syncthreads();
+    ptx::tc_fence_after();
+  }
+  const int st_thr = 96;  // TSQ: TMA stores + publication (warp 3, no MMA issue)
 
   float dcr[NC * 8];
 #pragma unroll
@@ -1349,7 +1380,25 @@ __global__ void __launch_bounds__(128, 1)
       }
     if (t < T - 1) {
       const int p = (t + 1) & 1;
-      if (lane == 0) {
+      if (TSQ) {
+        if (warp < 2) {
+          ptx::mbar_wait(fullA + p, fphase[p]);  // every peer's dA_{t+1} slice landed in sA[p]
+          ptx::tc_fence_after();
+          if (tr) trace[t * 5 + 1] = ptx::globaltimer_ns();
+          const uint64_t bd0 = ptx::smem_desc_sw128(sA_addr + p * abuf, 0, 1024);
+          const uint32_t dacc = tbase + warp * Bc;
+#pragma unroll
+          for (int k = 0; k < (TSQ ? NKQ : 1); k += 2) {
+            const int kw = k + warp;  // this warp's K-steps: warp, warp + 2, ...
+            const uint64_t bd = bd0 + (uint64_t)(((kw >> 2) * Bc * 128 + (kw & 3) * 32) >> 4);
+            // (A from TMEM is K-major: the MN-major bit of the SMEM variant's idesc must be clear)
+            if (ptx::elect_one_sync())
+              ptx::mma_f16_ts(dacc, tA + kw * 8, bd, ptx::idesc_f16_f32(64, Bc, 0, 0), k > 0 ? 1u : 0u);
+          }
+          if (ptx::elect_one_sync()) ptx::mma_commit(barM);
+          __syncwarp();
+        }
+      } else if (lane == 0) {
         ptx::mbar_wait(fullA + p, fphase[p]);  // every peer's dA_{t+1} slice landed in sA[p]
         ptx::tc_fence_after();
         if (tr) trace[t * 5 + 1] = ptx::globaltimer_ns();
@@ -1419,25 +1468,46 @@ __global__ void __launch_bounds__(128, 1)
               __halves2half2(__float2half_rn(d * g * i * (1.f - i)), __float2half_rn(d * cp[idx] * f * (1.f - f))),
               __halves2half2(__float2half_rn(d * i * (1.f - g * g)), __float2half_rn(dh * tc * o * (1.f - o)))};
           const uint2 pk = *reinterpret_cast<const uint2*>(q2);
-          *reinterpret_cast<uint2*>(dAout + b * fourhp + 4 * unit) = pk;  // R10 (for K8 / K9)
+          if (!TSQ) *reinterpret_cast<uint2*>(dAout + b * fourhp + 4 * unit) = pk;  // R10 (for K8 / K9)
           *reinterpret_cast<uint2*>(stg + j * Bc * 128 + bl * 128 + ((c ^ (bl & 7)) << 4) + byo) = pk;
           dcr[idx] = d * f;
         }
       }
     }
+    if (TSQ && threadIdx.x == st_thr) ptx::bulk_wait_group_read0();  // step t+2's store read sX[t & 1]
     ptx::tc_fence_before();
-    ptx::fence_async_smem();  // staging writes (generic) -> bulk copy reads (async proxy)
+    ptx::fence_async_smem();  // staging writes (generic) -> bulk copy / TMA store reads (async proxy)
     __syncthreads();
-    // publish dA_t to the projection / weight-gradient roles: one release (cumulative over
-    // the CTA's stores via the barrier); the consumers order their TMA reads after their
-    // acquire with a consumer-side fence.proxy.async
-    if (threadIdx.x == 64 && (qi == 0 || P.wtiles)) release_add((qi == 0 ? P.q1done : P.q0done) + grp * 32, 1u);
+    const bool publish = qi == 0 || P.wtiles;
+    if (!TSQ) {
+      // publish dA_t to the projection / weight-gradient roles: one release (cumulative over
+      // the CTA's stores via the barrier); the consumers order their TMA reads after their
+      // acquire with a consumer-side fence.proxy.async
+      if (threadIdx.x == 64 && publish) release_add((qi == 0 ? P.q1done : P.q0done) + grp * 32, 1u);
+    } else if (threadIdx.x == st_thr) {
+      if (publish && t < T - 1) {  // dA_{t+1}'s stores complete -> publish step t+1
+        ptx::bulk_wait_group0();
+        fence_proxy_async();
+        release_add((qi == 0 ? P.q1done : P.q0done) + grp * 32, 1u);
+      }
+      for (int kb = 0; kb < 4; ++kb)
+        if (j0 * 4 + kb * 64 < fourhp) ptx::tma_store_2d(&P.tmdAo[qi], stg + kb * Bc * 128, j0 * 4 + kb * 64, t * B + col0);
+      ptx::bulk_commit_group();
+      if (t == 0) {
+        ptx::bulk_wait_group0();
+        if (publish) {
+          fence_proxy_async();
+          release_add((qi == 0 ? P.q1done : P.q0done) + grp * 32, 1u);
+        }
+      }
+    }
     if (tr) trace[t * 5 + 3] = ptx::globaltimer_ns();
     // push dA_t (consumed by step t-1) into every peer's sA[t & 1]: one bulk copy per peer.
     // WAR: a peer writes sA[p] of step s only after consuming my dA_{s+1}, which I produce
     // after my MMA that read sA[p] for step s+2 -- the double buffers need no extra barrier.
-    if (t > 0 && threadIdx.x < G && my_kblocks > 0) {
-      const int dst = threadIdx.x;
+    const int pt = TSQ ? (int)threadIdx.x - 64 : (int)threadIdx.x;  // TSQ: warp 2 pushes
+    if (t > 0 && pt >= 0 && pt < G && my_kblocks > 0) {
+      const int dst = pt;
       const uint32_t dsta = ptx::mapa(sA_addr + (t & 1) * abuf + 4 * rank * Bc * 128, dst);
       const uint32_t mb = ptx::mapa(ptx::smem_u32(fullA + (t & 1)), dst);
       ptx::bulk_copy_to_peer(dsta, sX_addr + (t & 1) * SX, my_kblocks * Bc * 128, mb);
@@ -2628,10 +2698,17 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
 
 namespace hdp {
 
-const void* recur2b_fn(int Bc) {
-  return Bc == 16 ? (const void*)recur2_bwd_kernel<1>
-       : Bc == 32 ? (const void*)recur2_bwd_kernel<2>
-       : Bc == 48 ? (const void*)recur2_bwd_kernel<3> : (const void*)recur2_bwd_kernel<4>;
+// U^T slice in TMEM needs 64 + 2 h_p <= 512 columns (h_p = 208 yes, 256 no): instantiated for
+// 4 h_p / 16 = 52 K-steps; everything else runs the SMEM-A variant (HDP_WAVEFRONT_TS=0 forces it)
+template <int NC>
+const void* recur2b_fn_nk(int hp) {
+  const char* e = getenv("HDP_WAVEFRONT_TS");
+  if (e && e[0] == '0') return (const void*)recur2_bwd_kernel<NC, 0>;
+  return 4 * hp / 16 == 52 ? (const void*)recur2_bwd_kernel<NC, 52> : (const void*)recur2_bwd_kernel<NC, 0>;
+}
+const void* recur2b_fn(int Bc, int hp) {
+  return Bc == 16 ? recur2b_fn_nk<1>(hp) : Bc == 32 ? recur2b_fn_nk<2>(hp) : Bc == 48 ? recur2b_fn_nk<3>(hp)
+                                                                                        : recur2b_fn_nk<4>(hp);
 }
 
 // backward wavefront plan: largest batch-group count whose 3 x G x nbg CTAs are
@@ -2660,7 +2737,7 @@ bool plan_w2b(int B, int hp, bool want_wgrad, W2BPlan* out) {
         if ((Bc & 15) || Bc > 64) continue;
         const size_t smem = std::max(bwd_cl_smem(hp, Bc), wgrad_smem());
         if (smem > 227 * 1024) continue;
-        const void* fn = recur2b_fn(Bc);
+        const void* fn = recur2b_fn(Bc, hp);
         if (cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem) != cudaSuccess) break;
         for (int w = want_wgrad ? 1 : 0; w >= 0 && !best.nbg; --w) {
           const int wrows = w ? wgrad_rows(hp) : 0;
@@ -2764,11 +2841,16 @@ cudaError_t launch_recur2_bwd(const Recur2BwdArgs& a, cudaStream_t s) {
     P.wtiles = 4 * ((4 * a.hp + 127) / 128);
   }
   P.trace = a.trace;
+  if (encode_tmap_2d(&P.tmdAo[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.dA1, 4 * hp, (uint64_t)a.T * a.B, 4 * hp * 2, 64,
+                     Bc, CU_TENSOR_MAP_SWIZZLE_128B) ||
+      encode_tmap_2d(&P.tmdAo[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.dA0, 4 * hp, (uint64_t)a.T * a.B, 4 * hp * 2, 64,
+                     Bc, CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
   cudaError_t e = cudaMemsetAsync(a.flags, 0, (2 * 16 * 32 + 16 * 8 * 32) * sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
   void* args[] = {&P};
   const int rows = 3 * nbg + (wg ? pl.wrows : 0);
-  return launch_cluster(recur2b_fn(Bc), dim3(G, rows), dim3(128), std::max(bwd_cl_smem(a.hp, Bc), wgrad_smem()), G,
+  return launch_cluster(recur2b_fn(Bc, a.hp), dim3(G, rows), dim3(128), std::max(bwd_cl_smem(a.hp, Bc), wgrad_smem()), G,
                         s, args);
 }
 
