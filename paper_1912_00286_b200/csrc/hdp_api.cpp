@@ -774,7 +774,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
     static unsigned long long* b2trace = nullptr;  // debug: HDP_RECUR_TRACE=1 in profile (eager) mode
     const bool want_trace = c->prof && getenv("HDP_RECUR_TRACE") && getenv("HDP_RECUR_TRACE")[0] == '1' && T <= 8192;
     if (want_trace) {
-      if (!b2trace) CK_CUDA(cudaMalloc(&b2trace, 3 * 8192 * 5 * sizeof(unsigned long long)));
+      if (!b2trace) CK_CUDA(cudaMalloc(&b2trace, 4 * 8192 * 5 * sizeof(unsigned long long)));
       wa.trace = b2trace;
     }
     {
@@ -782,9 +782,34 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
       CK_CUDA(hdp::launch_recur2_bwd(wa, s));
     }
     if (want_trace) {
-      std::vector<unsigned long long> h((size_t)3 * T * 5);
+      std::vector<unsigned long long> h((size_t)4 * T * 5);
       CK_CUDA(cudaStreamSynchronize(s));
       CK_CUDA(cudaMemcpy(h.data(), b2trace, h.size() * 8, cudaMemcpyDeviceToHost));
+      {
+        double q[3] = {0, 0, 0};
+        int n = 0;
+        for (int t = T - 2; t >= 1; --t) {
+          const unsigned long long* r = &h[((size_t)3 * T + t) * 5];
+          const unsigned long long e2 = h[((size_t)1 * T + t) * 5 + 2];  // Q0 TR(t,2)
+          if (!r[0] || !r[2]) continue;
+          q[0] += (double)(r[0] - e2);
+          q[1] += (double)(r[1] - r[0]);
+          q[2] += (double)(r[2] - r[1]);
+          ++n;
+        }
+        if (n)
+          fprintf(stderr, "[hdp trace] bwd Q0 epilogue: dX1 wait %.0f  acc load %.0f  cell+stage %.0f ns\n", q[0] / n,
+                  q[1] / n, q[2] / n);
+        double w3 = 0, w4 = 0;
+        int m = 0;
+        for (int t = T - 2; t >= 1; --t) {
+          const unsigned long long* r = &h[((size_t)3 * T + t) * 5];
+          w3 += (double)r[3];
+          w4 += (double)r[4];
+          ++m;
+        }
+        fprintf(stderr, "[hdp trace] bwd Q0 warp 3: store read-wait %.0f  due dX1 fetch %.0f ns\n", w3 / m, w4 / m);
+      }
       const char* names[3] = {"Q1", "Q0", "X"};
       const unsigned long long t00 = h[(size_t)(T - 1) * 5];
       for (int role = 0; role < 3; ++role) {

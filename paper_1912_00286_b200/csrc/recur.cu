@@ -970,6 +970,9 @@ struct __align__(64) Bwd2Params {
   int Ip0, wtiles;
   unsigned long long* trace;  // debug: [Q1, Q0, X][T][5] stamps of CTA 0 / group 0, nullable
   CUtensorMap tmdAo[2];       // dA1 / dA0 rows [T*B][4hp], SWIZZLE_128B box (64, Bc): TMA stores from the push staging
+  CUtensorMap tmDX;           // dX1 rows [T*B][hp] fp32, box (64, Bc): Q0's dH_above prefetch (TSQ)
+  CUtensorMap tmGq[2];        // gates_1 / gates_0 rows [T*B][4hp] fp16, box (256, Bc) (TSQ prefetch)
+  CUtensorMap tmCq[2];        // C_1 / C_0 rows [T*B][hp] fp32, box (64, Bc) (TSQ prefetch)
 };
 
 // Weight-gradient role: one CTA per (matrix, 128-gate-row tile) accumulates over all
@@ -1241,6 +1244,8 @@ __global__ void __launch_bounds__(128, 1)
   constexpr int Bc = 16 * NC;
   // optional phase trace (CTA 0 of batch group 0, thread 0): [t][5] globaltimer stamps
   const bool tr = trace != nullptr && blockIdx.x == 0 && grp == 0 && threadIdx.x == 0;
+  unsigned long long* trq = (tr && qi == 1) ? P.trace + (size_t)3 * T * 5 : nullptr;  // Q0 epilogue sub-phases
+  unsigned long long* trw = (P.trace && qi == 1 && blockIdx.x == 0 && grp == 0) ? P.trace + (size_t)3 * T * 5 : nullptr;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int fourhp = 4 * hp;
@@ -1255,6 +1260,8 @@ __global__ void __launch_bounds__(128, 1)
   uint64_t* barM = bars + 1;
   uint64_t* fullA = bars + 2;                  // [2]: peers' bulk copies into sA[p]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
+  uint64_t* barD = bars + 5;                   // [3] TSQ, Q0: dX1_t slice landed in sD[t % 3]
+  uint64_t* barP = bars + 8;                   // [3] TSQ: gates_t + C_t tiles landed in ring slot t % 3
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
@@ -1285,6 +1292,10 @@ __global__ void __launch_bounds__(128, 1)
     ptx::mbar_init(barM, NISQ);  // one commit per issuing warp
     ptx::mbar_init(fullA, 1);
     ptx::mbar_init(fullA + 1, 1);
+    ptx::mbar_init(barD, 1);
+    ptx::mbar_init(barD + 1, 1);
+    ptx::mbar_init(barD + 2, 1);
+    for (int i = 0; i < 3; ++i) ptx::mbar_init(barP + i, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc(tslot, tcols);
@@ -1323,10 +1334,43 @@ __global__ void __launch_bounds__(128, 1)
     }
     ptx::tmem_wait_st();
     ptx::tc_fence_before();
+    ptx::fence_async_smem();  // generic reads of sU before the TMA writes that reuse it (Q0's dX1 prefetch)
     __syncthreads();
     ptx::tc_fence_after();
   }
   const int st_thr = 96;  // TSQ: TMA stores + publication (warp 3, no MMA issue)
+  // TSQ, Q0: dH_above = dX1 slices prefetched by TMA one step ahead into the (now free) sU
+  // region, by a thread that issues no MMAs; the flag acquire leaves the step's chain
+  const bool dpf = TSQ && qi == 1;
+  float* sD = reinterpret_cast<float*>(sU);    // [3][Bc][64] fp32 (two steps ahead)
+  const int pf_thr = 97;
+  auto fetch_dx = [&](int tt) {  // pf thread: wait for X's slice of step tt, then TMA it
+    spin_until(P.xdone + (grp * 8 + rank) * 32, (unsigned)(T - tt));
+    fence_proxy_async();
+    ptx::mbar_arrive_expect_tx(barD + tt % 3, Bc * 64 * 4);
+    ptx::tma_load_2d(sD + (tt % 3) * Bc * 64, &P.tmDX, barD + tt % 3, j0, tt * B + col0);
+  };
+  // next step whose dX1 slice is still to be fetched (descending); the pf thread fetches
+  // ahead only when X has already published (non-blocking), and blocks only when due
+  int nf = T - 1;
+  if (dpf && threadIdx.x == pf_thr) {
+    fetch_dx(nf--);
+    if (nf >= 0 && nf >= T - 2) fetch_dx(nf--);
+  }
+  // TSQ: the step's saved gates and c (written by the forward kernel, usually no longer in L2)
+  // arrive by TMA two steps ahead into a 3-slot ring, instead of per-thread loads whose HBM
+  // latency the epilogue waited for
+  __half* sGp = reinterpret_cast<__half*>(sU + 3 * Bc * 64 * 4);                 // [3][Bc][256]
+  float* sCp = reinterpret_cast<float*>(sU + 3 * Bc * 64 * 4 + 3 * Bc * 256 * 2);  // [3][Bc][64]
+  auto fetch_gc = [&](int tt) {
+    ptx::mbar_arrive_expect_tx(barP + tt % 3, Bc * 256 * 2 + Bc * 64 * 4);
+    ptx::tma_load_2d(sGp + (tt % 3) * Bc * 256, &P.tmGq[qi], barP + tt % 3, j0 * 4, tt * B + col0);
+    ptx::tma_load_2d(sCp + (tt % 3) * Bc * 64, &P.tmCq[qi], barP + tt % 3, j0, tt * B + col0);
+  };
+  if (TSQ && threadIdx.x == pf_thr) {
+    fetch_gc(T - 1);
+    if (T >= 2) fetch_gc(T - 2);
+  }
 
   float dcr[NC * 8];
 #pragma unroll
@@ -1337,7 +1381,7 @@ __global__ void __launch_bounds__(128, 1)
 
   for (int t = T - 1; t >= 0; --t) {
     if (tr) trace[t * 5 + 0] = ptx::globaltimer_ns();
-    if (qi == 1) {
+    if (qi == 1 && !dpf) {
       // dH_above[t] of layer 0 = dX1_t, produced in this kernel by the projection CTA of my units
       if (threadIdx.x == 0) {
         const unsigned* f = P.xdone + (grp * 8 + rank) * 32;
@@ -1365,13 +1409,15 @@ __global__ void __launch_bounds__(128, 1)
           if (dHa_last_only) {
             if (t == T - 1) d = __ldg(dHa + b * hp + unit);
           } else if (qi == 1) {
-            d = __ldcg(dHa + ((size_t)t * B + b) * hp + unit);  // written in-kernel: L2-coherent load
+            if (!dpf) d = __ldcg(dHa + ((size_t)t * B + b) * hp + unit);  // written in-kernel: L2-coherent load
           } else {
             d = __ldg(dHa + ((size_t)t * B + b) * hp + unit);
           }
-          c1 = __ldg(Cst + ((size_t)t * B + b) * hp + unit);
-          if (t > 0) c0 = __ldg(Cst + ((size_t)(t - 1) * B + b) * hp + unit);
-          gg = __ldg(reinterpret_cast<const uint2*>(gates + ((size_t)t * B + b) * fourhp + 4 * unit));
+          if (!TSQ) {
+            c1 = __ldg(Cst + ((size_t)t * B + b) * hp + unit);
+            if (t > 0) c0 = __ldg(Cst + ((size_t)(t - 1) * B + b) * hp + unit);
+            gg = __ldg(reinterpret_cast<const uint2*>(gates + ((size_t)t * B + b) * fourhp + 4 * unit));
+          }
         }
         dh0[idx] = d;
         cc[idx] = c1;
@@ -1422,6 +1468,33 @@ __global__ void __launch_bounds__(128, 1)
       if (threadIdx.x == 0 && t >= 2) ptx::mbar_arrive_expect_tx(fullA + p, total_bytes);
     }
     if (tr) trace[t * 5 + 2] = ptx::globaltimer_ns();
+    if (TSQ) {
+      ptx::mbar_wait(barP + t % 3, ((T - 1 - t) / 3) & 1);
+      if (t > 0) ptx::mbar_wait(barP + (t - 1) % 3, ((T - t) / 3) & 1);  // c_{t-1} (fetched one step later)
+#pragma unroll
+      for (int ch = 0; ch < NC; ++ch)
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const int bl = ch * 16 + half * 8 + k;
+          cc[ch * 8 + k] = sCp[((t % 3) * Bc + bl) * 64 + ul];
+          cp[ch * 8 + k] = t > 0 ? sCp[(((t + 2) % 3) * Bc + bl) * 64 + ul] : 0.f;  // slot of step t-1
+          gq[ch * 8 + k] = *reinterpret_cast<const uint2*>(sGp + ((t % 3) * Bc + bl) * 256 + 4 * ul);
+        }
+    }
+    if (dpf) {
+      if (threadIdx.x == pf_thr) {
+        const unsigned long long w0 = trw ? ptx::globaltimer_ns() : 0;
+        while (nf >= t) fetch_dx(nf--);  // due now: blocking
+        if (trw) trw[t * 5 + 4] = ptx::globaltimer_ns() - w0;
+      }
+      ptx::mbar_wait(barD + t % 3, ((T - 1 - t) / 3) & 1);
+      if (trq) trq[t * 5 + 0] = ptx::globaltimer_ns();
+#pragma unroll
+      for (int ch = 0; ch < NC; ++ch)
+#pragma unroll
+        for (int k = 0; k < 8; ++k)
+          dh0[ch * 8 + k] = sD[((t % 3) * Bc + ch * 16 + half * 8 + k) * 64 + ul];
+    }
     __half* dAout = dA + (size_t)t * B * fourhp;
     uint8_t* stg = sX + (t & 1) * SX;
 #pragma unroll
@@ -1448,6 +1521,7 @@ __global__ void __launch_bounds__(128, 1)
         const float hi = __shfl_sync(0xffffffffu, v[8 + k], jl);
         rec[k] = half ? hi : v[k];
       }
+      if (trq) trq[t * 5 + 1] = ptx::globaltimer_ns();
       if (unit_ok) {
         // staging position of my unit's 4 gate rows (local gate row 4*ul) in row bl:
         // K-block j = ul/16, 16-B chunk c = (4ul % 64)/8, byte (4ul % 8)*2
@@ -1474,7 +1548,12 @@ __global__ void __launch_bounds__(128, 1)
         }
       }
     }
-    if (TSQ && threadIdx.x == st_thr) ptx::bulk_wait_group_read0();  // step t+2's store read sX[t & 1]
+    if (trq) trq[t * 5 + 2] = ptx::globaltimer_ns();
+    if (TSQ && threadIdx.x == st_thr) {
+      const unsigned long long w0 = trw ? ptx::globaltimer_ns() : 0;
+      ptx::bulk_wait_group_read0();  // all earlier stores finished reading their staging
+      if (trw) trw[t * 5 + 3] = ptx::globaltimer_ns() - w0;
+    }
     ptx::tc_fence_before();
     ptx::fence_async_smem();  // staging writes (generic) -> bulk copy / TMA store reads (async proxy)
     __syncthreads();
@@ -1485,23 +1564,30 @@ __global__ void __launch_bounds__(128, 1)
       // acquire with a consumer-side fence.proxy.async
       if (threadIdx.x == 64 && publish) release_add((qi == 0 ? P.q1done : P.q0done) + grp * 32, 1u);
     } else if (threadIdx.x == st_thr) {
-      if (publish && t < T - 1) {  // dA_{t+1}'s stores complete -> publish step t+1
-        ptx::bulk_wait_group0();
+      unsigned* pubf = (qi == 0 ? P.q1done : P.q0done) + grp * 32;
+      if (publish && t < T - 2) {  // all but step t+1's store group complete -> publish step t+2
+        ptx::bulk_wait_group1();
         fence_proxy_async();
-        release_add((qi == 0 ? P.q1done : P.q0done) + grp * 32, 1u);
+        release_add(pubf, 1u);
       }
       for (int kb = 0; kb < 4; ++kb)
         if (j0 * 4 + kb * 64 < fourhp) ptx::tma_store_2d(&P.tmdAo[qi], stg + kb * Bc * 128, j0 * 4 + kb * 64, t * B + col0);
       ptx::bulk_commit_group();
       if (t == 0) {
         ptx::bulk_wait_group0();
-        if (publish) {
+        if (publish) {  // steps min(1, T-1) .. 0
           fence_proxy_async();
-          release_add((qi == 0 ? P.q1done : P.q0done) + grp * 32, 1u);
+          release_add(pubf, T >= 2 ? 2u : 1u);
         }
       }
     }
     if (tr) trace[t * 5 + 3] = ptx::globaltimer_ns();
+    // ring slot (t-2) % 3 = (t+1) % 3 was last read by the epilogues of steps t+1 and t+2
+    // (steps read slots t % 3 and (t-1) % 3), i.e. before the barrier above
+    if (TSQ && threadIdx.x == pf_thr && t >= 2) fetch_gc(t - 2);
+    if (dpf && threadIdx.x == pf_thr && nf >= 0 && nf >= t - 2 &&
+        acquire_ld(P.xdone + (grp * 8 + rank) * 32) >= (unsigned)(T - nf))
+      fetch_dx(nf--);
     // push dA_t (consumed by step t-1) into every peer's sA[t & 1]: one bulk copy per peer.
     // WAR: a peer writes sA[p] of step s only after consuming my dA_{s+1}, which I produce
     // after my MMA that read sA[p] for step s+2 -- the double buffers need no extra barrier.
@@ -2841,6 +2927,19 @@ cudaError_t launch_recur2_bwd(const Recur2BwdArgs& a, cudaStream_t s) {
     P.wtiles = 4 * ((4 * a.hp + 127) / 128);
   }
   P.trace = a.trace;
+  {
+    const __half* gsrc[2] = {a.gates1, a.gates0};
+    const float* csrc[2] = {a.C1, a.C0};
+    for (int l = 0; l < 2; ++l)
+      if (encode_tmap_2d(&P.tmGq[l], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, gsrc[l], 4 * hp, (uint64_t)a.T * a.B, 4 * hp * 2,
+                         256, Bc, CU_TENSOR_MAP_SWIZZLE_NONE) ||
+          encode_tmap_2d(&P.tmCq[l], CU_TENSOR_MAP_DATA_TYPE_FLOAT32, csrc[l], hp, (uint64_t)a.T * a.B, hp * 4, 64, Bc,
+                         CU_TENSOR_MAP_SWIZZLE_NONE))
+        return cudaErrorInvalidValue;
+  }
+  if (encode_tmap_2d(&P.tmDX, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.dX1, hp, (uint64_t)a.T * a.B, hp * 4, 64, Bc,
+                     CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
   if (encode_tmap_2d(&P.tmdAo[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.dA1, 4 * hp, (uint64_t)a.T * a.B, 4 * hp * 2, 64,
                      Bc, CU_TENSOR_MAP_SWIZZLE_128B) ||
       encode_tmap_2d(&P.tmdAo[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.dA0, 4 * hp, (uint64_t)a.T * a.B, 4 * hp * 2, 64,
