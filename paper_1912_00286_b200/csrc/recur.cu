@@ -973,6 +973,7 @@ struct __align__(64) Bwd2Params {
   CUtensorMap tmDX;           // dX1 rows [T*B][hp] fp32, box (64, Bc): Q0's dH_above prefetch (TSQ)
   CUtensorMap tmGq[2];        // gates_1 / gates_0 rows [T*B][4hp] fp16, box (256, Bc) (TSQ prefetch)
   CUtensorMap tmCq[2];        // C_1 / C_0 rows [T*B][hp] fp32, box (64, Bc) (TSQ prefetch)
+  CUtensorMap tmDXo;          // dX1 rows [T*B][hp] fp32, box (64, Bc): X's TMA stores (TSQ)
 };
 
 // Weight-gradient role: one CTA per (matrix, 128-gate-row tile) accumulates over all
@@ -1100,6 +1101,158 @@ __device__ __forceinline__ void bwd_wgrad_role(const Bwd2Params& P, int tile) {
 
 // Projection role: dX1_t[b][unit] = sum_r dA1_t[b][r] W1[r][unit] for my 64 units
 // (swap-AB tcgen05, A = W1^T slice MN-major resident, B = dA1_t rows via TMA).
+// Projection role, A-from-TMEM variant (h_p = 208): W1^T slice copied from SMEM into TMEM
+// (M = 64 layout), dA1_t operands TMA-prefetched into a 3-slot ring (reusing the W1 slice's
+// SMEM) as Q1 publishes them, 2 issuing warps, dX1_t staged and written by TMA stores,
+// xdone published lazily once a store group is complete.
+template <int NC, int NKQ>
+__device__ __forceinline__ void bwd_proj_role_ts(const Bwd2Params& P, int grp) {
+  constexpr int Bc = 16 * NC;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  const int T = P.T, B = P.B, hp = P.hp;
+  const int fourhp = 4 * hp;
+  const int nkb = fourhp / 64;
+  const int abytes = nkb * Bc * 128;
+  uint8_t* sW = smem;                              // nkb x 8 KB, then (after the TMEM copy) the dA1 ring
+  uint8_t* sRing = sW;                             // [3][abytes]
+  float* sO = reinterpret_cast<float*>(sW + nkb * 8192);  // [2][Bc][64] dX1 staging
+  uint64_t* bars = reinterpret_cast<uint64_t*>(sW + nkb * 8192 + 2 * Bc * 64 * 4);
+  uint64_t* barU = bars;
+  uint64_t* barM = bars + 1;
+  uint64_t* barA = bars + 2;                       // [3]
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 5);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int rank = blockIdx.x, G = gridDim.x;
+  const int j0 = rank * 64, col0 = grp * Bc;
+  const int jl = lane & 15, half = lane >> 4;
+  const int ul = warp * 16 + jl;
+  if (threadIdx.x == 0) {
+    ptx::tma_prefetch(&P.tmW1);
+    ptx::tma_prefetch(&P.tmA1);
+    ptx::mbar_init(barU, 1);
+    ptx::mbar_init(barM, 2);
+    for (int i = 0; i < 3; ++i) ptx::mbar_init(barA + i, 1);
+    ptx::fence_mbar_init();
+  }
+  if (warp == 2) ptx::tmem_alloc(tslot, 512);
+  ptx::tc_fence_before();
+  __syncthreads();
+  ptx::tc_fence_after();
+  const uint32_t tbase = *tslot;
+  const uint32_t tA = tbase + 64;
+  if (threadIdx.x == 0) {
+    ptx::mbar_arrive_expect_tx(barU, nkb * 8192);
+    for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sW + kb * 8192, &P.tmW1, barU, j0, kb * 64);
+  }
+  ptx::mbar_wait(barU, 0);
+  {
+    // W1^T slice -> TMEM: unit 16q + i -> lane 32q + i, two gate rows per column
+    const int i = lane & 15;
+    const int u = warp * 16 + i;
+    const uint32_t tq = tA + (static_cast<uint32_t>(warp * 32) << 16);
+    for (int c0 = 0; c0 < 2 * hp; c0 += 16) {
+      uint32_t v[16];
+#pragma unroll
+      for (int j = 0; j < 16; ++j) {
+        const int kk = 2 * (c0 + j), kb = kk >> 6, kr = kk & 63;
+        const uint8_t* row = sW + kb * 8192 + kr * 128;
+        const uint32_t lo = __half_as_ushort(*reinterpret_cast<const __half*>(row + (((u >> 3) ^ (kr & 7)) << 4) + (u & 7) * 2));
+        const uint32_t hi = __half_as_ushort(*reinterpret_cast<const __half*>(row + 128 + (((u >> 3) ^ ((kr + 1) & 7)) << 4) + (u & 7) * 2));
+        v[j] = lane < 16 ? (lo | (hi << 16)) : 0u;
+      }
+      ptx::tmem_st16(tq + c0, v);
+    }
+    ptx::tmem_wait_st();
+  }
+  ptx::tc_fence_before();
+  ptx::fence_async_smem();  // generic reads of sW before the TMA writes of the ring that reuses it
+  __syncthreads();
+  ptx::tc_fence_after();
+
+  const int pf_thr = 97, st_thr = 96;
+  const unsigned* q1f = P.q1done + grp * 32;
+  auto fetch = [&](int tt) {  // pf thread
+    spin_until(q1f, (unsigned)(G * (T - tt)));
+    fence_proxy_async();
+    ptx::mbar_arrive_expect_tx(barA + tt % 3, abytes);
+    for (int kb = 0; kb < nkb; ++kb)
+      ptx::tma_load_2d(sRing + (tt % 3) * abytes + kb * Bc * 128, &P.tmA1, barA + tt % 3, kb * 64, tt * B + col0);
+  };
+  int nf = T - 1;
+  if (threadIdx.x == pf_thr) {
+    fetch(nf--);
+    if (nf >= 0 && nf >= T - 2) fetch(nf--);
+  }
+  unsigned long long* xtr = (P.trace && rank == 0 && grp == 0 && threadIdx.x == 0) ? P.trace + (size_t)2 * T * 5 : nullptr;
+  unsigned* xf = P.xdone + (grp * 8 + rank) * 32;
+  uint32_t mph = 0;
+  for (int t = T - 1; t >= 0; --t) {
+    if (xtr) xtr[t * 5 + 0] = ptx::globaltimer_ns();
+    if (threadIdx.x == pf_thr)
+      while (nf >= t) fetch(nf--);  // due now
+    if (warp < 2) {
+      ptx::mbar_wait(barA + t % 3, ((T - 1 - t) / 3) & 1);
+      ptx::tc_fence_after();
+      if (xtr) xtr[t * 5 + 1] = ptx::globaltimer_ns();
+      const uint64_t bd0 = ptx::smem_desc_sw128(ptx::smem_u32(sRing + (t % 3) * abytes), 0, 1024);
+      const uint32_t idesc = ptx::idesc_f16_f32(64, Bc, 0, 0);
+#pragma unroll
+      for (int k = 0; k < NKQ; k += 2) {
+        const int kw = k + warp;
+        const uint64_t bd = bd0 + (uint64_t)(((kw >> 2) * Bc * 128 + (kw & 3) * 32) >> 4);
+        if (ptx::elect_one_sync()) ptx::mma_f16_ts(tbase + warp * Bc, tA + kw * 8, bd, idesc, k > 0 ? 1u : 0u);
+      }
+      if (ptx::elect_one_sync()) ptx::mma_commit(barM);
+      __syncwarp();
+    }
+    ptx::mbar_wait_relaxed(barM, mph);
+    mph ^= 1u;
+    ptx::tc_fence_after();
+    if (xtr) xtr[t * 5 + 2] = ptx::globaltimer_ns();
+    float* so = sO + (t & 1) * Bc * 64;
+#pragma unroll
+    for (int ch = 0; ch < NC; ++ch) {
+      float v[16], w[16];
+      const uint32_t ta = tbase + (static_cast<uint32_t>(warp * 32) << 16) + ch * 16;
+      ptx::tmem_ld16(ta, v);
+      ptx::tmem_ld16(ta + Bc, w);
+#pragma unroll
+      for (int q = 0; q < 16; ++q) v[q] += w[q];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        const float hi = __shfl_sync(0xffffffffu, v[8 + q], jl);
+        so[(ch * 16 + half * 8 + q) * 64 + ul] = half ? hi : v[q];  // R11 (fp32)
+      }
+    }
+    if (threadIdx.x == st_thr) ptx::bulk_wait_group_read0();  // earlier stores finished reading sO
+    ptx::tc_fence_before();
+    ptx::fence_async_smem();
+    __syncthreads();  // MMA reads of the ring slot done (barM), staging complete
+    if (xtr) xtr[t * 5 + 3] = ptx::globaltimer_ns();
+    if (threadIdx.x == st_thr) {
+      if (t < T - 2) {  // all but step t+1's group complete -> publish step t+2
+        ptx::bulk_wait_group1();
+        fence_proxy_async();
+        release_add(xf, 1u);
+      }
+      ptx::tma_store_2d(&P.tmDXo, so, j0, t * B + col0);
+      ptx::bulk_commit_group();
+      if (t == 0) {
+        ptx::bulk_wait_group0();
+        fence_proxy_async();
+        release_add(xf, T >= 2 ? 2u : 1u);
+      }
+    }
+    // ring slot (t-2) % 3 = (t+1) % 3 was read by step t+1's MMAs (complete): prefetch ahead
+    if (threadIdx.x == pf_thr && nf >= 0 && nf >= t - 2 && acquire_ld(q1f) >= (unsigned)(G * (T - nf))) fetch(nf--);
+    if (xtr) xtr[t * 5 + 4] = ptx::globaltimer_ns();
+  }
+  ptx::tc_fence_after();
+  __syncthreads();
+  if (warp == 2) ptx::tmem_dealloc(tbase, 512);
+}
+
 template <int NC>
 __device__ __forceinline__ void bwd_proj_role(const Bwd2Params& P, int grp) {
   constexpr int Bc = 16 * NC;
@@ -1230,7 +1383,10 @@ __global__ void __launch_bounds__(128, 1)
   }
   const int role = blockIdx.y / P.nbg, grp = blockIdx.y % P.nbg;
   if (role == 1) {
-    bwd_proj_role<NC>(P, grp);
+    if (NKQ != 0)
+      bwd_proj_role_ts<NC, (NKQ != 0 ? NKQ : 52)>(P, grp);
+    else
+      bwd_proj_role<NC>(P, grp);
     return;
   }
   const int qi = role == 0 ? 0 : 1;  // 0: layer 1 (Q1), 1: layer 0 (Q0)
@@ -2937,6 +3093,9 @@ cudaError_t launch_recur2_bwd(const Recur2BwdArgs& a, cudaStream_t s) {
                          CU_TENSOR_MAP_SWIZZLE_NONE))
         return cudaErrorInvalidValue;
   }
+  if (encode_tmap_2d(&P.tmDXo, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.dX1, hp, (uint64_t)a.T * a.B, hp * 4, 64, Bc,
+                     CU_TENSOR_MAP_SWIZZLE_NONE))
+    return cudaErrorInvalidValue;
   if (encode_tmap_2d(&P.tmDX, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.dX1, hp, (uint64_t)a.T * a.B, hp * 4, 64, Bc,
                      CU_TENSOR_MAP_SWIZZLE_NONE))
     return cudaErrorInvalidValue;
