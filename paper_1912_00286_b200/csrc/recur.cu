@@ -1206,7 +1206,17 @@ __device__ __forceinline__ void bwd_proj_role_ts(const Bwd2Params& P, int grp) {
       if (ptx::elect_one_sync()) ptx::mma_commit(barM);
       __syncwarp();
     }
-    ptx::mbar_wait_relaxed(barM, mph);
+    if (warp == 3) {
+      // idle during the MMAs: keep prefetching dA1 operands as soon as Q1 publishes them
+      // (warp-uniform exit: lane 0's observation decides for the whole warp)
+      while (!__shfl_sync(0xffffffffu, (int)ptx::mbar_try_wait_relaxed(barM, mph), 0)) {
+        if (lane == 1 && nf >= 0 && nf >= t - 2 && acquire_ld(q1f) >= (unsigned)(G * (T - nf))) fetch(nf--);
+        __syncwarp();
+      }
+      ptx::mbar_wait_relaxed(barM, mph);
+    } else {
+      ptx::mbar_wait_relaxed(barM, mph);
+    }
     mph ^= 1u;
     ptx::tc_fence_after();
     if (xtr) xtr[t * 5 + 2] = ptx::globaltimer_ns();
@@ -1616,7 +1626,18 @@ __global__ void __launch_bounds__(128, 1)
         ptx::mma_commit(barM);
       }
       __syncwarp();
-      ptx::mbar_wait_relaxed(barM, (T - 2 - t) & 1);
+      if (dpf && warp == 3) {
+        // idle during the MMAs: keep prefetching dX1 slices as soon as X publishes them
+        // (warp-uniform exit: lane 0's observation decides for the whole warp)
+        while (!__shfl_sync(0xffffffffu, (int)ptx::mbar_try_wait_relaxed(barM, (T - 2 - t) & 1), 0)) {
+          if (lane == 1 && nf >= 0 && nf >= t - 2 && acquire_ld(P.xdone + (grp * 8 + rank) * 32) >= (unsigned)(T - nf))
+            fetch_dx(nf--);
+          __syncwarp();
+        }
+        ptx::mbar_wait_relaxed(barM, (T - 2 - t) & 1);
+      } else {
+        ptx::mbar_wait_relaxed(barM, (T - 2 - t) & 1);
+      }
       ptx::tc_fence_after();
       fphase[p] ^= 1u;
       // re-arm slot p for its next use (peers can deliver into it only after
