@@ -131,8 +131,9 @@ struct hdp_ctx {
   std::vector<Slot> slot;
   float *Gx = nullptr, *Gh = nullptr, *dH[2] = {nullptr, nullptr}, *dhrec = nullptr, *dc = nullptr;
   char *dA = nullptr, *dz = nullptr;
-  char* dA2 = nullptr;
-  float* Gx1 = nullptr;  // layer-1 G_x of the split forward wavefront  // layer-0 dA of the 2-layer backward wavefront (layer 1 keeps dA)
+  char* dA2 = nullptr;  // layer-0 dA of the 2-layer backward wavefront (layer 1 keeps dA)
+  bool wave_bwd = false;  // the backward ran as one wavefront launch: layer buckets are ready together
+  float* Gx1 = nullptr;  // layer-1 G_x of the split forward wavefront
   float* crp = nullptr;
   size_t crp_floats = 0;
   float* ws = nullptr;
@@ -316,7 +317,7 @@ void carve(hdp_ctx* c, char* base) {
   c->s1 = (float*)cv.take(c->M_own * 4);
   c->s2 = (float*)cv.take(d.optimizer == HDP_OPT_ADAM ? c->M_own * 4 : 0);
   c->grads = cv.take((size_t)c->nslots * P * c->gsz);
-  c->recv = cv.take(c->world > 1 ? c->max_bucket * c->gsz : 0);
+  c->recv = cv.take(c->world > 1 ? c->P * c->gsz : 0);  // bucket bi received at its own offset
   c->status = (int*)cv.take(32768);  // [0] non-finite count; +1024 B: recurrence barrier counters;
                                        // +4096 B: backward-wavefront hand-off counters
   c->slot.assign(c->nslots, hdp_ctx::Slot{});
@@ -742,6 +743,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
   const bool wave = L == 2 && !f32 && c->persistent && hdp::recur2_bwd_supported(B, (int)hp);
   // ... and, on the SMs the recurrences leave idle, the A8 weight gradients of both layers
   const bool wgrad = wave && !gf && hdp::recur2_bwd_wgrad(B, (int)hp, (int)c->Ip0);
+  if (wave) c->wave_bwd = true;
   char* dAl = wave && l == 0 ? c->dA2 : c->dA;
   if (wave && l == 1) {
     hdp::Recur2BwdArgs wa;
@@ -1335,46 +1337,68 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
     CK_CUDA(cudaStreamWaitEvent(cs, c->ev_done, 0));
   }
   CK_CUDA(cudaMemsetAsync(c->status, 0, sizeof(int), cs));
-  for (size_t bi = 0; bi < c->buckets.size(); ++bi) {
-    const Bucket& bk = c->buckets[bi];
-    if (c->world > 1 && c->d.n_layers > 0) CK_CUDA(cudaStreamWaitEvent(cs, c->ev_bucket[bi], 0));
-    a.count = bk.shard;
-    a.W = c->master + bk.moff;
-    a.S1 = c->s1 + bk.moff;
-    a.S2 = c->s2 ? c->s2 + bk.moff : nullptr;
-    a.w16 = c->f32 ? nullptr : (__half*)(c->w + (bk.off + (long)c->rank * bk.shard) * 2);
-    a.w32 = c->f32 ? (float*)(c->w + (bk.off + (long)c->rank * bk.shard) * 4) : nullptr;
-    int grad_f32 = c->gf32;
-    if (c->world == 1) {
-      a.g = c->grads + bk.off * c->gsz;  // slot r at + r*P
-      a.g_stride = c->P;
-      a.nsrc = c->nslots;
-    } else if (c->d.wire == HDP_WIRE_FP16_A2A) {
-      // A9: owner j receives every rank's shard j, rank-ordered
+  // Exchange groups: buckets become ready in order (head, layer L-1 .. 0, embedding); with the
+  // backward wavefront every layer bucket is ready at once, so buckets 1.. form one group whose
+  // collectives are issued as single NCCL groups (one kernel each instead of one per bucket).
+  const size_t nb = c->buckets.size();
+  std::vector<std::pair<size_t, size_t>> groups;
+  if (c->world > 1 && c->wave_bwd && nb > 2) {
+    groups.push_back({0, 1});
+    groups.push_back({1, nb});
+  } else {
+    for (size_t bi = 0; bi < nb; ++bi) groups.push_back({bi, bi + 1});
+  }
+  for (size_t gi = 0; gi < groups.size(); ++gi) {
+    const size_t b0 = groups[gi].first, b1 = groups[gi].second;
+    const bool last = gi + 1 == groups.size();
+    if (c->world > 1 && c->d.n_layers > 0)
+      for (size_t bi = b0; bi < b1; ++bi) CK_CUDA(cudaStreamWaitEvent(cs, c->ev_bucket[bi], 0));
+    if (c->world > 1) {
       KScope ks_(c, HDP_K_COMM, 0, cs);
-      CK_NCCL(ncclAlltoAll(c->grads + bk.off * c->gsz, c->recv, bk.shard, gtype(c), c->comm, cs));
-      a.g = c->recv;
-      a.g_stride = bk.shard;
-      a.nsrc = c->world;
-    } else {
-      // NCCL-native reduction (fp16 sum, or fp32 wire)
-      KScope ks_(c, HDP_K_COMM, 0, cs);
-      CK_NCCL(ncclReduceScatter(c->grads + bk.off * c->gsz, c->recv, bk.shard, gtype(c), ncclSum, c->comm, cs));
-      a.g = c->recv;
-      a.g_stride = bk.shard;
-      a.nsrc = 1;
+      CK_NCCL(ncclGroupStart());
+      for (size_t bi = b0; bi < b1; ++bi) {
+        const Bucket& bk = c->buckets[bi];
+        if (c->d.wire == HDP_WIRE_FP16_A2A)  // A9: owner j receives every rank's shard j, rank-ordered
+          CK_NCCL(ncclAlltoAll(c->grads + bk.off * c->gsz, c->recv + bk.off * c->gsz, bk.shard, gtype(c), c->comm, cs));
+        else  // NCCL-native reduction (fp16 sum, or fp32 wire)
+          CK_NCCL(ncclReduceScatter(c->grads + bk.off * c->gsz, c->recv + bk.off * c->gsz, bk.shard, gtype(c), ncclSum,
+                                    c->comm, cs));
+      }
+      CK_NCCL(ncclGroupEnd());
     }
-    {
+    for (size_t bi = b0; bi < b1; ++bi) {
+      const Bucket& bk = c->buckets[bi];
+      a.count = bk.shard;
+      a.W = c->master + bk.moff;
+      a.S1 = c->s1 + bk.moff;
+      a.S2 = c->s2 ? c->s2 + bk.moff : nullptr;
+      a.w16 = c->f32 ? nullptr : (__half*)(c->w + (bk.off + (long)c->rank * bk.shard) * 2);
+      a.w32 = c->f32 ? (float*)(c->w + (bk.off + (long)c->rank * bk.shard) * 4) : nullptr;
+      const int grad_f32 = c->gf32;
+      if (c->world == 1) {
+        a.g = c->grads + bk.off * c->gsz;  // slot r at + r*P
+        a.g_stride = c->P;
+        a.nsrc = c->nslots;
+      } else {
+        a.g = c->recv + bk.off * c->gsz;
+        a.g_stride = bk.shard;
+        a.nsrc = c->d.wire == HDP_WIRE_FP16_A2A ? c->world : 1;
+      }
       KScope ks_(c, HDP_K_UPDATE, 1, cs);
       CK_CUDA(hdp::launch_avg_update(a, grad_f32, opt, cs));  // A10 / K11
     }
-    if (c->world > 1) {                                     // A11: step 6 "broadcast"
-      char* mine = c->w + (bk.off + (long)c->rank * bk.shard) * c->esz;
+    if (c->world > 1) {  // A11: step 6 "broadcast" (+ the non-finite count, with the last group)
       KScope ks_(c, HDP_K_COMM, 0, cs);
-      CK_NCCL(ncclAllGather(mine, c->w + bk.off * c->esz, bk.shard, wtype(c), c->comm, cs));
+      CK_NCCL(ncclGroupStart());
+      for (size_t bi = b0; bi < b1; ++bi) {
+        const Bucket& bk = c->buckets[bi];
+        char* mine = c->w + (bk.off + (long)c->rank * bk.shard) * c->esz;
+        CK_NCCL(ncclAllGather(mine, c->w + bk.off * c->esz, bk.shard, wtype(c), c->comm, cs));
+      }
+      if (last) CK_NCCL(ncclAllReduce(c->status, c->status, 1, ncclInt32, ncclSum, c->comm, cs));
+      CK_NCCL(ncclGroupEnd());
     }
   }
-  if (c->world > 1) CK_NCCL(ncclAllReduce(c->status, c->status, 1, ncclInt32, ncclSum, c->comm, cs));
   CK_CUDA(cudaMemcpyAsync(c->count_host, c->status, sizeof(int), cudaMemcpyDeviceToHost, cs));
   CK_CUDA(cudaEventRecord(c->ev_count, cs));
   if (c->world > 1) {
