@@ -25,6 +25,7 @@
 #include "gemm.cuh"
 #include "kernels.cuh"
 #include "recur.cuh"
+#include "p2p_exchange.cuh"
 
 namespace {
 
@@ -133,6 +134,14 @@ struct hdp_ctx {
   char *dA = nullptr, *dz = nullptr;
   char* dA2 = nullptr;  // layer-0 dA of the 2-layer backward wavefront (layer 1 keeps dA)
   bool wave_bwd = false;  // the backward ran as one wavefront launch: layer buckets are ready together
+  // NEXT-2 NVLink exchange: library-owned, IPC-shared windows (gradients, fp16 weights, flags)
+  bool p2p = false;
+  char *gwin = nullptr, *wwin = nullptr;
+  unsigned* fwin = nullptr;
+  std::vector<void*> peer_open;       // IPC mappings to close
+  hdp::P2PArgs p2pa;                  // peer tables + bucket table (step / scalars filled per call)
+  int p2p_grid = 0;
+  unsigned p2p_step = 0;
   float* Gx1 = nullptr;  // layer-1 G_x of the split forward wavefront
   float* crp = nullptr;
   size_t crp_floats = 0;
@@ -964,6 +973,83 @@ __attribute__((unused)) int nccl_async_check(hdp_ctx* c) {
 ncclDataType_t gtype(const hdp_ctx* c) { return c->gf32 ? ncclFloat : ncclHalf; }
 ncclDataType_t wtype(const hdp_ctx* c) { return c->f32 ? ncclFloat : ncclHalf; }
 
+// NEXT-2: gradients and fp16 working weights move into library-owned cudaMalloc windows
+// whose CUDA IPC handles are exchanged over the NCCL communicator; every rank maps every
+// peer's windows, so one kernel can read the N contributions and write the N weight
+// copies over NVLink (HDP_P2P=0 keeps the NCCL collectives).
+int setup_p2p(hdp_ctx* c) {
+  const char* e = getenv("HDP_P2P");
+  if (c->world < 2 || (e && e[0] == '0')) return HDP_OK;
+  if (c->f32 || c->gsz != 2 || c->d.wire != HDP_WIRE_FP16_A2A || c->world > hdp::P2P_MAX_RANKS ||
+      (int)c->buckets.size() > hdp::P2P_MAX_BUCKETS)
+    return HDP_OK;
+  const size_t gbytes = (size_t)c->P * c->gsz, wbytes = (size_t)c->P * c->esz;
+  CK_CUDA(cudaMalloc(&c->gwin, gbytes));
+  CK_CUDA(cudaMalloc(&c->wwin, wbytes));
+  CK_CUDA(cudaMalloc(&c->fwin, hdp::P2P_FLAG_WORDS * sizeof(unsigned)));
+  CK_CUDA(cudaMemset(c->gwin, 0, gbytes));
+  CK_CUDA(cudaMemcpy(c->wwin, c->w, wbytes, cudaMemcpyDeviceToDevice));
+  CK_CUDA(cudaMemset(c->fwin, 0, hdp::P2P_FLAG_WORDS * sizeof(unsigned)));
+  cudaIpcMemHandle_t h[3];
+  CK_CUDA(cudaIpcGetMemHandle(&h[0], c->gwin));
+  CK_CUDA(cudaIpcGetMemHandle(&h[1], c->wwin));
+  CK_CUDA(cudaIpcGetMemHandle(&h[2], c->fwin));
+  const size_t hb = sizeof(h);
+  char* dh = nullptr;
+  CK_CUDA(cudaMalloc(&dh, hb * c->world));
+  CK_CUDA(cudaMemcpy(dh + hb * c->rank, h, hb, cudaMemcpyHostToDevice));
+  CK_NCCL(ncclAllGather(dh + hb * c->rank, dh, hb, ncclChar, c->comm, 0));  // also the setup barrier
+  CK_CUDA(cudaStreamSynchronize(0));
+  std::vector<cudaIpcMemHandle_t> all((size_t)3 * c->world);
+  CK_CUDA(cudaMemcpy(all.data(), dh, hb * c->world, cudaMemcpyDeviceToHost));
+  CK_CUDA(cudaFree(dh));
+  hdp::P2PArgs& a = c->p2pa;
+  a.N = c->world;
+  a.rank = c->rank;
+  for (int r = 0; r < c->world; ++r) {
+    void* ptr[3];
+    for (int k = 0; k < 3; ++k) {
+      if (r == c->rank) {
+        ptr[k] = k == 0 ? (void*)c->gwin : k == 1 ? (void*)c->wwin : (void*)c->fwin;
+      } else {
+        CK_CUDA(cudaIpcOpenMemHandle(&ptr[k], all[(size_t)3 * r + k], cudaIpcMemLazyEnablePeerAccess));
+        c->peer_open.push_back(ptr[k]);
+      }
+    }
+    a.g_peer[r] = (const __half*)ptr[0];
+    a.w_peer[r] = (__half*)ptr[1];
+    a.flag_peer[r] = (unsigned*)ptr[2];
+    a.status_peer[r] = (int*)((unsigned*)ptr[2] + hdp::P2P_STATUS);
+  }
+  a.flag_local = c->fwin;
+  a.nb = (int)c->buckets.size();
+  long vtot = 0;
+  for (int bi = 0; bi < a.nb; ++bi) {
+    const Bucket& bk = c->buckets[bi];
+    a.off[bi] = bk.off;
+    a.shard[bi] = bk.shard;
+    a.moff[bi] = bk.moff;
+    a.vpre[bi] = vtot;
+    vtot += bk.shard / 8;
+  }
+  a.vpre[a.nb] = vtot;
+  a.W = c->master;
+  a.S1 = c->s1;
+  a.S2 = c->s2;
+  c->p2p_grid = (int)std::max(1L, std::min((vtot + 255) / 256, 4L * 148));
+  // the arena's gradient and weight regions are replaced by the shared windows
+  c->grads = c->gwin;
+  c->w = c->wwin;
+  c->p2p = true;
+  // all peers mapped (and their flags zeroed) before anyone's first exchange
+  int* one = nullptr;
+  CK_CUDA(cudaMalloc(&one, sizeof(int)));
+  CK_NCCL(ncclAllReduce(one, one, 1, ncclInt32, ncclSum, c->comm, 0));
+  CK_CUDA(cudaStreamSynchronize(0));
+  CK_CUDA(cudaFree(one));
+  return HDP_OK;
+}
+
 }  // namespace
 
 // ====================================================================== C-ABI
@@ -1018,6 +1104,10 @@ int hdp_destroy(hdp_ctx* c) {
   if (c->cap) cudaStreamDestroy(c->cap);
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->count_host) cudaFreeHost(c->count_host);
+  for (void* ptr : c->peer_open) cudaIpcCloseMemHandle(ptr);
+  if (c->gwin) cudaFree(c->gwin);
+  if (c->wwin) cudaFree(c->wwin);
+  if (c->fwin) cudaFree(c->fwin);
   if (c->comm) ncclCommDestroy(c->comm);
   delete c;
   return HDP_OK;
@@ -1086,6 +1176,7 @@ int hdp_bind(hdp_ctx* c, void* arena, long long bytes) {
   CK_CUDA(cudaMallocHost(&c->count_host, sizeof(int)));
   *c->count_host = 0;
   c->st.assign(c->nslots, SlotState{});
+  CK(setup_p2p(c));
   CK_CUDA(cudaDeviceSynchronize());
   c->bound = true;
   return HDP_OK;
@@ -1336,70 +1427,99 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
     CK_CUDA(cudaEventRecord(c->ev_done, s));
     CK_CUDA(cudaStreamWaitEvent(cs, c->ev_done, 0));
   }
-  CK_CUDA(cudaMemsetAsync(c->status, 0, sizeof(int), cs));
-  // Exchange groups: buckets become ready in order (head, layer L-1 .. 0, embedding); with the
-  // backward wavefront every layer bucket is ready at once, so buckets 1.. form one group whose
-  // collectives are issued as single NCCL groups (one kernel each instead of one per bucket).
-  const size_t nb = c->buckets.size();
-  std::vector<std::pair<size_t, size_t>> groups;
-  if (c->world > 1 && c->wave_bwd && nb > 2) {
-    groups.push_back({0, 1});
-    groups.push_back({1, nb});
-  } else {
-    for (size_t bi = 0; bi < nb; ++bi) groups.push_back({bi, bi + 1});
-  }
-  for (size_t gi = 0; gi < groups.size(); ++gi) {
-    const size_t b0 = groups[gi].first, b1 = groups[gi].second;
-    const bool last = gi + 1 == groups.size();
-    if (c->world > 1 && c->d.n_layers > 0)
-      for (size_t bi = b0; bi < b1; ++bi) CK_CUDA(cudaStreamWaitEvent(cs, c->ev_bucket[bi], 0));
-    if (c->world > 1) {
-      KScope ks_(c, HDP_K_COMM, 0, cs);
-      CK_NCCL(ncclGroupStart());
-      for (size_t bi = b0; bi < b1; ++bi) {
-        const Bucket& bk = c->buckets[bi];
-        if (c->d.wire == HDP_WIRE_FP16_A2A)  // A9: owner j receives every rank's shard j, rank-ordered
-          CK_NCCL(ncclAlltoAll(c->grads + bk.off * c->gsz, c->recv + bk.off * c->gsz, bk.shard, gtype(c), c->comm, cs));
-        else  // NCCL-native reduction (fp16 sum, or fp32 wire)
-          CK_NCCL(ncclReduceScatter(c->grads + bk.off * c->gsz, c->recv + bk.off * c->gsz, bk.shard, gtype(c), ncclSum,
-                                    c->comm, cs));
-      }
-      CK_NCCL(ncclGroupEnd());
-    }
-    for (size_t bi = b0; bi < b1; ++bi) {
-      const Bucket& bk = c->buckets[bi];
-      a.count = bk.shard;
-      a.W = c->master + bk.moff;
-      a.S1 = c->s1 + bk.moff;
-      a.S2 = c->s2 ? c->s2 + bk.moff : nullptr;
-      a.w16 = c->f32 ? nullptr : (__half*)(c->w + (bk.off + (long)c->rank * bk.shard) * 2);
-      a.w32 = c->f32 ? (float*)(c->w + (bk.off + (long)c->rank * bk.shard) * 4) : nullptr;
-      const int grad_f32 = c->gf32;
-      if (c->world == 1) {
-        a.g = c->grads + bk.off * c->gsz;  // slot r at + r*P
-        a.g_stride = c->P;
-        a.nsrc = c->nslots;
-      } else {
-        a.g = c->recv + bk.off * c->gsz;
-        a.g_stride = bk.shard;
-        a.nsrc = c->d.wire == HDP_WIRE_FP16_A2A ? c->world : 1;
-      }
+  const int* count_src = c->status;
+  if (c->p2p) {
+    // NEXT-2: one kernel does the exchange, the fused average + update and the all-gather
+    // over NVLink peer memory (p2p_exchange.cu); it starts once every bucket is complete
+    if (c->d.n_layers > 0)
+      for (size_t bi = 0; bi < c->buckets.size(); ++bi) CK_CUDA(cudaStreamWaitEvent(cs, c->ev_bucket[bi], 0));
+    const unsigned step = ++c->p2p_step;
+    hdp::P2PArgs& p = c->p2pa;
+    p.step = step;
+    p.inv_scale = a.inv_scale;
+    p.lam = a.lam;
+    p.mom = a.mom;
+    p.b1 = a.b1;
+    p.omb1 = a.omb1;
+    p.b2 = a.b2;
+    p.omb2 = a.omb2;
+    p.c1 = a.c1;
+    p.c2 = a.c2;
+    p.eps = a.eps;
+    // the other status slot is next step's: zero it now (peers add to it only after my next "ready")
+    CK_CUDA(cudaMemsetAsync(c->fwin + hdp::P2P_STATUS + ((step + 1) & 1), 0, sizeof(int), cs));
+    {
       KScope ks_(c, HDP_K_UPDATE, 1, cs);
-      CK_CUDA(hdp::launch_avg_update(a, grad_f32, opt, cs));  // A10 / K11
+      CK_CUDA(hdp::launch_exch_update(p, opt, c->p2p_grid, cs));
     }
-    if (c->world > 1) {  // A11: step 6 "broadcast" (+ the non-finite count, with the last group)
-      KScope ks_(c, HDP_K_COMM, 0, cs);
-      CK_NCCL(ncclGroupStart());
+    count_src = (const int*)(c->fwin + hdp::P2P_STATUS + (step & 1));
+  } else {
+    CK_CUDA(cudaMemsetAsync(c->status, 0, sizeof(int), cs));
+    // Exchange groups: buckets become ready in order (head, layer L-1 .. 0, embedding); with the
+    // backward wavefront every layer bucket is ready at once, so buckets 1.. form one group whose
+    // collectives are issued as single NCCL groups (one kernel each instead of one per bucket).
+    const size_t nb = c->buckets.size();
+    std::vector<std::pair<size_t, size_t>> groups;
+    if (c->world > 1 && c->wave_bwd && nb > 2) {
+      groups.push_back({0, 1});
+      groups.push_back({1, nb});
+    } else {
+      for (size_t bi = 0; bi < nb; ++bi) groups.push_back({bi, bi + 1});
+    }
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+      const size_t b0 = groups[gi].first, b1 = groups[gi].second;
+      const bool last = gi + 1 == groups.size();
+      if (c->world > 1 && c->d.n_layers > 0)
+        for (size_t bi = b0; bi < b1; ++bi) CK_CUDA(cudaStreamWaitEvent(cs, c->ev_bucket[bi], 0));
+      if (c->world > 1) {
+        KScope ks_(c, HDP_K_COMM, 0, cs);
+        CK_NCCL(ncclGroupStart());
+        for (size_t bi = b0; bi < b1; ++bi) {
+          const Bucket& bk = c->buckets[bi];
+          if (c->d.wire == HDP_WIRE_FP16_A2A)  // A9: owner j receives every rank's shard j, rank-ordered
+            CK_NCCL(ncclAlltoAll(c->grads + bk.off * c->gsz, c->recv + bk.off * c->gsz, bk.shard, gtype(c), c->comm, cs));
+          else  // NCCL-native reduction (fp16 sum, or fp32 wire)
+            CK_NCCL(ncclReduceScatter(c->grads + bk.off * c->gsz, c->recv + bk.off * c->gsz, bk.shard, gtype(c), ncclSum,
+                                      c->comm, cs));
+        }
+        CK_NCCL(ncclGroupEnd());
+      }
       for (size_t bi = b0; bi < b1; ++bi) {
         const Bucket& bk = c->buckets[bi];
-        char* mine = c->w + (bk.off + (long)c->rank * bk.shard) * c->esz;
-        CK_NCCL(ncclAllGather(mine, c->w + bk.off * c->esz, bk.shard, wtype(c), c->comm, cs));
+        a.count = bk.shard;
+        a.W = c->master + bk.moff;
+        a.S1 = c->s1 + bk.moff;
+        a.S2 = c->s2 ? c->s2 + bk.moff : nullptr;
+        a.w16 = c->f32 ? nullptr : (__half*)(c->w + (bk.off + (long)c->rank * bk.shard) * 2);
+        a.w32 = c->f32 ? (float*)(c->w + (bk.off + (long)c->rank * bk.shard) * 4) : nullptr;
+        const int grad_f32 = c->gf32;
+        if (c->world == 1) {
+          a.g = c->grads + bk.off * c->gsz;  // slot r at + r*P
+          a.g_stride = c->P;
+          a.nsrc = c->nslots;
+        } else {
+          a.g = c->recv + bk.off * c->gsz;
+          a.g_stride = bk.shard;
+          a.nsrc = c->d.wire == HDP_WIRE_FP16_A2A ? c->world : 1;
+        }
+        KScope ks_(c, HDP_K_UPDATE, 1, cs);
+        CK_CUDA(hdp::launch_avg_update(a, grad_f32, opt, cs));  // A10 / K11
       }
-      if (last) CK_NCCL(ncclAllReduce(c->status, c->status, 1, ncclInt32, ncclSum, c->comm, cs));
-      CK_NCCL(ncclGroupEnd());
+      if (c->world > 1) {  // A11: step 6 "broadcast" (+ the non-finite count, with the last group)
+        KScope ks_(c, HDP_K_COMM, 0, cs);
+        CK_NCCL(ncclGroupStart());
+        for (size_t bi = b0; bi < b1; ++bi) {
+          const Bucket& bk = c->buckets[bi];
+          char* mine = c->w + (bk.off + (long)c->rank * bk.shard) * c->esz;
+          CK_NCCL(ncclAllGather(mine, c->w + bk.off * c->esz, bk.shard, wtype(c), c->comm, cs));
+        }
+        if (last) CK_NCCL(ncclAllReduce(c->status, c->status, 1, ncclInt32, ncclSum, c->comm, cs));
+        CK_NCCL(ncclGroupEnd());
+      }
     }
+
   }
-  CK_CUDA(cudaMemcpyAsync(c->count_host, c->status, sizeof(int), cudaMemcpyDeviceToHost, cs));
+  CK_CUDA(cudaMemcpyAsync(c->count_host, count_src, sizeof(int), cudaMemcpyDeviceToHost, cs));
   CK_CUDA(cudaEventRecord(c->ev_count, cs));
   if (c->world > 1) {
     CK_CUDA(cudaEventRecord(c->ev_done, cs));
