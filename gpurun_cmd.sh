@@ -1,2 +1,2 @@
-timeout -s KILL 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29538 bench.py --gpus 4 --steps 20 --warmup 5 > gpurun_out/b91_n4.log 2>&1; echo bench_exit=$? >> gpurun_out/b91_n4.log
-timeout -s KILL 600 python -m torch.distributed.run --nnodes=1 --nproc-per-node 4 --master-addr 127.0.0.1 --master-port 29539 bench.py --config C5 --gpus 4 --steps 10 --warmup 3 > gpurun_out/b91_c5n4.log 2>&1; echo bench_exit=$? >> gpurun_out/b91_c5n4.log
+timeout -s KILL 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_kernels.py -x -q > gpurun_out/t92.log 2>&1; echo pytest_exit=$? >> gpurun_out/t92.log
+timeout -s KILL 300 python bench.py --steps 20 --warmup 5 --no-cpu-baseline > gpurun_out/b92.log 2>&1

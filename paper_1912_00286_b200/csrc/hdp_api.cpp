@@ -124,6 +124,7 @@ struct hdp_ctx {
     float* C;
     char* gates;
     char* Z;
+    char* dz;
     float* y;
     float* dy;
     float* loss;
@@ -343,6 +344,7 @@ void carve(hdp_ctx* c, char* base) {
       S.C = (float*)cv.take(L * T * B * hp * 4);
       S.gates = cv.take(L * T * B * 4 * hp * e);
       S.Z = cv.take(c->Fp ? rows * c->Fp * e : 0);
+      S.dz = cv.take(c->Fp ? rows * c->Fp * e : 0);  // A5's ReLU' output, written by the forward's head_out
       S.y = (float*)cv.take(rows * 4);
       S.dy = (float*)cv.take(rows * 4);
       S.loss = (float*)cv.take(4);
@@ -358,8 +360,8 @@ void carve(hdp_ctx* c, char* base) {
     c->dH[1] = (float*)cv.take(rows * dw * 4);
     c->dhrec = (float*)cv.take(B * hp * 4);
     c->dc = (float*)cv.take(B * hp * 4);
-    c->dz = cv.take(c->Fp ? rows * c->Fp * e : 0);
-    const long maxcols = std::max(std::max(4 * hp, c->Fp), std::max(hp, 1L));
+    c->dz = nullptr;  // (per slot: S.dz)
+    const long maxcols = std::max(std::max(4 * hp, 2 * c->Fp + 1), std::max(hp, 1L));
     c->crp_floats = hdp::colreduce_partials_floats((int)rows, (int)maxcols);
     c->crp = (float*)cv.take(c->crp_floats * 4);
     // split-K workspace for the weight-gradient GEMMs (K = B*T)
@@ -632,7 +634,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
     {
       KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
       CK_CUDA(hdp::launch_head_out(f32, S.Z, (int)rows, (int)c->Fp, c->Fp, c->W(iwo), c->W(ibo), S.stage_t, 0, B, T,
-                                   c->alpha, 1.f / (float)rows, S.y, S.dy, S.partials, s));
+                                   c->alpha, 1.f / (float)rows, S.y, S.dy, S.partials, s, S.dz));
     }
     {
       KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
@@ -680,26 +682,16 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
     if (d.fc_hidden > 0) {
       const int iF = c->find("F"), ifb = c->find("fb");
       const long Fp = c->Fp;
-      {
-        KScope ks_(c, HDP_K_HEAD_BWD, 1, s);
-        CK_CUDA(hdp::launch_relu_dz(f32, S.dy, c->W(iwo), S.Z, c->dz, (int)rows, (int)Fp, s));          // R9
-      }
+      // dz (R9) was written by the forward's head_out; dwo, dfb, dbo in one fused column pass
       {
         KScope ks_(c, HDP_K_HEAD_BWD, 2, s);
-        CK_CUDA(hdp::launch_colreduce(f32, S.Z, Fp, (int)rows, (int)Fp, S.dy, c->crp, gf, c->G(si, iwo), s));
-      }
-      {
-        KScope ks_(c, HDP_K_HEAD_BWD, 2, s);
-        CK_CUDA(hdp::launch_colreduce(1, S.dy, 1, (int)rows, 1, nullptr, c->crp, gf, c->G(si, ibo), s));
-      }
-      {
-        KScope ks_(c, HDP_K_HEAD_BWD, 2, s);
-        CK_CUDA(hdp::launch_colreduce(f32, c->dz, Fp, (int)rows, (int)Fp, nullptr, c->crp, gf, c->G(si, ifb), s));
+        CK_CUDA(hdp::launch_colreduce3(f32, S.Z, S.dz, Fp, (int)rows, (int)Fp, S.dy, c->crp, gf, c->G(si, iwo),
+                                       c->G(si, ifb), c->G(si, ibo), s));
       }
       // dF = dz^T H   (M = Fp, N = hp, K = B*T; both operands MN-major)
-      CK(gemm(c, HDP_K_HEAD_BWD, c->dz, Fp, 1, Htop, hp, 1, Fp, hp, rows, epi_elem(gf, c->G(si, iF), hp), s));
+      CK(gemm(c, HDP_K_HEAD_BWD, S.dz, Fp, 1, Htop, hp, 1, Fp, hp, rows, epi_elem(gf, c->G(si, iF), hp), s));
       // dH_top = dz F (M = B*T, N = hp, K = Fp; F read MN-major)
-      CK(gemm(c, HDP_K_HEAD_BWD, c->dz, Fp, 0, c->W(iF), hp, 1, rows, hp, Fp, epi_f32(c->dH[0], hp), s));
+      CK(gemm(c, HDP_K_HEAD_BWD, S.dz, Fp, 0, c->W(iF), hp, 1, rows, hp, Fp, epi_f32(c->dH[0], hp), s));
     } else if (d.head_last_step) {
       const char* Hlast = S.Hs + ((L - 1) * hs_layer + (long)T * B * hp) * e;
       {

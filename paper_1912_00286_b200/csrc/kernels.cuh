@@ -46,9 +46,10 @@ cudaError_t launch_cell_bwd(int f32, const float* dHa_t, const float* dh_rec, co
 // y[r] = sum_k Z[r][k] wo[k] + bo; hinge (Eq. 6) -> dy[r], per-block partial sums.
 // tgt_mode 0: row r = t*B + b <-> tgt[b*T + t];  1: row r = b <-> tgt[b]
 int head_partials_count(int rows);
+// dz (nullable): also writes dz = (Z > 0) * dy * wo (A5's ReLU', R9) for the FC head
 cudaError_t launch_head_out(int f32, const void* Z, int rows, int Kd, long ldz, const void* wo, const void* bo,
                             const int8_t* tgt, int tgt_mode, int B, int T, float alpha, float inv_terms, float* y,
-                            float* dy, float* partials, cudaStream_t s);
+                            float* dy, float* partials, cudaStream_t s, void* dz = nullptr);
 // loss = (sum of partials) * inv_terms   (unscaled mean hinge), deterministic
 cudaError_t launch_loss_final(const float* partials, int n, float inv_terms, float* loss, cudaStream_t s);
 // dz[r][f] = (Z[r][f] > 0) ? dy[r]*wo[f] : 0   (ReLU', R9)
@@ -61,8 +62,11 @@ cudaError_t launch_outer(int f32, const float* dy, const void* wo, float* dH, in
 // out[c] = sum_r X[r*ldx + c] * (w ? w[r] : 1)   over rows in a fixed order.
 // out is fp16 (RNE) when out_f32 == 0, else fp32.  partials: RS*cols floats.
 size_t colreduce_partials_floats(int rows, int cols);
+// FC head: dwo = Z^T dy, dfb = colsum(dz), dbo = sum(dy) in one fused pass (partials: (2F+1)*RS doubles)
 cudaError_t launch_colreduce(int x_f32, const void* X, long ldx, int rows, int cols, const float* w,
                              float* partials, int out_f32, void* out, cudaStream_t s);
+cudaError_t launch_colreduce3(int x_f32, const void* Z, const void* dz, long ld, int rows, int F, const float* dy,
+                              float* partials, int out_f32, void* dwo, void* dfb, void* dbo, cudaStream_t s);
 
 // ---------------------------------------------------------------- embedding backward (K10)
 size_t embed_sort_temp_bytes(int n);

@@ -120,12 +120,20 @@ __global__ void cell_bwd_kernel(const float* __restrict__ dHa, const float* __re
 // ---------------------------------------------------------------- head
 constexpr int HEAD_WARPS = 8;
 
+// dy of row r as head_out computed it (valid on lane 0, which holds the row's sum path)
+__device__ __forceinline__ float margin_dy(int lane, float hinge, float alpha, float inv_terms, const int8_t* tgt,
+                                           int tgt_mode, int r, int B, int Tn) {
+  if (lane != 0) return 0.f;
+  const int8_t tv = tgt_mode == 0 ? tgt[(long)(r % B) * Tn + r / B] : tgt[r];
+  return hinge > 0.f ? -alpha * (float)tv * inv_terms : 0.f;
+}
+
 template <typename T>
 __global__ void __launch_bounds__(HEAD_WARPS * 32)
     head_out_kernel(const T* __restrict__ Z, int rows, int Kd, long ldz, const T* __restrict__ wo,
                     const T* __restrict__ bo, const int8_t* __restrict__ tgt, int tgt_mode, int B, int Tn,
                     float alpha, float inv_terms, float* __restrict__ y, float* __restrict__ dy,
-                    float* __restrict__ partials) {
+                    float* __restrict__ partials, T* __restrict__ dz) {
   __shared__ float part[HEAD_WARPS];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * HEAD_WARPS + warp;
@@ -150,6 +158,14 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32)
       // d/dy alpha*mean(max(0, 1 - t y)) ; subgradient 0 at the kink (reading Q5)
       dy[r] = margin > 0.f ? -alpha * tf * inv_terms : 0.f;
       hinge = margin > 0.f ? margin : 0.f;
+    }
+    if (dz) {
+      // A5's ReLU' (R9) fused here: dz = (z > 0) dy wo, the same fp32 product relu_dz forms
+      const float dyr = __shfl_sync(0xffffffffu, margin_dy(lane, hinge, alpha, inv_terms, tgt, tgt_mode, r, B, Tn), 0);
+      for (int k = lane; k < Kd; k += 32) {
+        const float z = ld<T>(Z, (long)r * ldz + k);
+        dz[(long)r * ldz + k] = cvt<T>(z > 0.f ? dyr * ld<T>(wo, k) : 0.f);
+      }
     }
   }
   if (lane == 0) part[warp] = hinge;
@@ -230,6 +246,50 @@ __global__ void __launch_bounds__(CR_WARPS * 32)
     for (int q = 0; q < CR_WARPS; ++q) s += sm[q][lane];
     partials[(long)blockIdx.y * cols + c] = s;
   }
+}
+
+// FC head (A5): dwo = Z^T dy, dfb = colsum(dz), dbo = sum(dy) in one pass over Z and dz:
+// combined columns [0, F) -> Z*dy, [F, 2F) -> dz, 2F -> dy; same fp64 fixed-order sums
+// as colreduce_pass1 (rows r0 + warp, r0 + warp + 8, ... then the 8 warps in order)
+template <typename XT>
+__global__ void __launch_bounds__(CR_WARPS * 32)
+    colreduce3_pass1(const XT* __restrict__ Z, const XT* __restrict__ dz, long ldx, int rows, int F,
+                     const float* __restrict__ dy, int rs, double* __restrict__ partials) {
+  __shared__ double sm[CR_WARPS][33];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int cols = 2 * F + 1;
+  const int c = blockIdx.x * 32 + lane;
+  const int per = (rows + rs - 1) / rs;
+  const int r0 = blockIdx.y * per, r1 = min(rows, r0 + per);
+  double acc = 0.0;
+  if (c < F) {
+    for (int r = r0 + warp; r < r1; r += CR_WARPS) acc += (double)ld<XT>(Z, (long)r * ldx + c) * (double)dy[r];
+  } else if (c < 2 * F) {
+    for (int r = r0 + warp; r < r1; r += CR_WARPS) acc += (double)ld<XT>(dz, (long)r * ldx + c - F);
+  } else if (c == 2 * F) {
+    for (int r = r0 + warp; r < r1; r += CR_WARPS) acc += (double)dy[r];
+  }
+  sm[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0 && c < cols) {
+    double s = 0.0;
+    for (int q = 0; q < CR_WARPS; ++q) s += sm[q][lane];
+    partials[(long)blockIdx.y * cols + c] = s;
+  }
+}
+__global__ void colreduce3_pass2(const double* __restrict__ partials, int rs, int F, int out_f32, void* dwo, void* dfb,
+                                 void* dbo) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int cols = 2 * F + 1;
+  if (c >= cols) return;
+  double s = 0.0;
+  for (int q = 0; q < rs; ++q) s += partials[(long)q * cols + c];
+  void* out = c < F ? dwo : c < 2 * F ? dfb : dbo;
+  const int i = c < F ? c : c < 2 * F ? c - F : 0;
+  if (out_f32)
+    reinterpret_cast<float*>(out)[i] = (float)s;
+  else
+    reinterpret_cast<__half*>(out)[i] = __float2half_rn((float)s);  // R12
 }
 
 __global__ void colreduce_pass2(const double* __restrict__ partials, int rs, int cols, int out_f32, void* out) {
@@ -386,16 +446,16 @@ int head_partials_count(int rows) { return (rows + HEAD_WARPS - 1) / HEAD_WARPS;
 
 cudaError_t launch_head_out(int f32, const void* Z, int rows, int Kd, long ldz, const void* wo, const void* bo,
                             const int8_t* tgt, int tgt_mode, int B, int T, float alpha, float inv_terms, float* y,
-                            float* dy, float* partials, cudaStream_t s) {
+                            float* dy, float* partials, cudaStream_t s, void* dz) {
   const int g = head_partials_count(rows);
   if (f32)
     head_out_kernel<float><<<g, HEAD_WARPS * 32, 0, s>>>((const float*)Z, rows, Kd, ldz, (const float*)wo,
                                                         (const float*)bo, tgt, tgt_mode, B, T, alpha, inv_terms, y,
-                                                        dy, partials);
+                                                        dy, partials, (float*)dz);
   else
     head_out_kernel<__half><<<g, HEAD_WARPS * 32, 0, s>>>((const __half*)Z, rows, Kd, ldz, (const __half*)wo,
                                                          (const __half*)bo, tgt, tgt_mode, B, T, alpha, inv_terms,
-                                                         y, dy, partials);
+                                                         y, dy, partials, (__half*)dz);
   return cudaGetLastError();
 }
 
@@ -429,6 +489,20 @@ cudaError_t launch_colreduce(int x_f32, const void* X, long ldx, int rows, int c
   if (x_f32) colreduce_pass1<float><<<g1, CR_WARPS * 32, 0, s>>>((const float*)X, ldx, rows, cols, w, rs, part);
   else colreduce_pass1<__half><<<g1, CR_WARPS * 32, 0, s>>>((const __half*)X, ldx, rows, cols, w, rs, part);
   colreduce_pass2<<<(cols + 255) / 256, 256, 0, s>>>(part, rs, cols, out_f32, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_colreduce3(int x_f32, const void* Z, const void* dz, long ld, int rows, int F, const float* dy,
+                              float* partials, int out_f32, void* dwo, void* dfb, void* dbo, cudaStream_t s) {
+  const int rs = cr_splits(rows);
+  const int cols = 2 * F + 1;
+  dim3 g1((cols + 31) / 32, rs);
+  double* part = reinterpret_cast<double*>(partials);
+  if (x_f32)
+    colreduce3_pass1<float><<<g1, CR_WARPS * 32, 0, s>>>((const float*)Z, (const float*)dz, ld, rows, F, dy, rs, part);
+  else
+    colreduce3_pass1<__half><<<g1, CR_WARPS * 32, 0, s>>>((const __half*)Z, (const __half*)dz, ld, rows, F, dy, rs, part);
+  colreduce3_pass2<<<(cols + 255) / 256, 256, 0, s>>>(part, rs, F, out_f32, dwo, dfb, dbo);
   return cudaGetLastError();
 }
 
