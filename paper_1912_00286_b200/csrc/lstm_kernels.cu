@@ -138,7 +138,47 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32)
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * HEAD_WARPS + warp;
   float hinge = 0.f;
-  if (r < rows) {
+  // fp16 rows of <= 256 elements (multiple of 8): one 16-B vector per lane, kept for dz
+  const bool vec = sizeof(T) == 2 && (Kd & 7) == 0 && Kd <= 256 && (ldz & 7) == 0;
+  if (r < rows && vec) {
+    float acc = 0.f;
+    float zv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, wv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
+    const int k0 = lane * 8;
+    if (k0 < Kd) {
+      const uint4 zu = *reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(Z) + (long)r * ldz + k0);
+      const uint4 wu = *reinterpret_cast<const uint4*>(reinterpret_cast<const __half*>(wo) + k0);
+      const __half2* zh = reinterpret_cast<const __half2*>(&zu);
+      const __half2* wh = reinterpret_cast<const __half2*>(&wu);
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const float2 zf = __half22float2(zh[q]), wf = __half22float2(wh[q]);
+        zv[2 * q] = zf.x;
+        zv[2 * q + 1] = zf.y;
+        wv[2 * q] = wf.x;
+        wv[2 * q + 1] = wf.y;
+      }
+#pragma unroll
+      for (int q = 0; q < 8; ++q) acc += zv[q] * wv[q];
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(0xffffffffu, acc, o);
+    const float yy = acc + ld<T>(bo, 0);
+    const int8_t tv = tgt_mode == 0 ? tgt[(long)(r % B) * Tn + r / B] : tgt[r];
+    const float tf = (float)tv;
+    const float margin = 1.f - tf * yy;
+    const float dyr = margin > 0.f ? -alpha * tf * inv_terms : 0.f;
+    if (lane == 0) {
+      y[r] = yy;
+      dy[r] = dyr;  // subgradient 0 at the kink (reading Q5)
+      hinge = margin > 0.f ? margin : 0.f;
+    }
+    if (dz && k0 < Kd) {  // A5's ReLU' (R9), the same fp32 product relu_dz forms
+      __align__(16) __half o[8];
+#pragma unroll
+      for (int q = 0; q < 8; ++q) o[q] = __float2half_rn(zv[q] > 0.f ? dyr * wv[q] : 0.f);
+      *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(dz) + (long)r * ldz + k0) = *reinterpret_cast<const uint4*>(o);
+    }
+  } else if (r < rows) {
     float acc = 0.f;
     for (int k = lane; k < Kd; k += 32) acc += ld<T>(Z, (long)r * ldz + k) * ld<T>(wo, k);
 #pragma unroll
