@@ -777,7 +777,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
     static unsigned long long* b2trace = nullptr;  // debug: HDP_RECUR_TRACE=1 in profile (eager) mode
     const bool want_trace = c->prof && getenv("HDP_RECUR_TRACE") && getenv("HDP_RECUR_TRACE")[0] == '1' && T <= 8192;
     if (want_trace) {
-      if (!b2trace) CK_CUDA(cudaMalloc(&b2trace, 4 * 8192 * 5 * sizeof(unsigned long long)));
+      if (!b2trace) CK_CUDA(cudaMalloc(&b2trace, 6 * 8192 * 5 * sizeof(unsigned long long)));
       wa.trace = b2trace;
     }
     {
@@ -785,9 +785,32 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
       CK_CUDA(hdp::launch_recur2_bwd(wa, s));
     }
     if (want_trace) {
-      std::vector<unsigned long long> h((size_t)4 * T * 5);
+      std::vector<unsigned long long> h((size_t)6 * T * 5);
       CK_CUDA(cudaStreamSynchronize(s));
       CK_CUDA(cudaMemcpy(h.data(), b2trace, h.size() * 8, cudaMemcpyDeviceToHost));
+      {
+        {
+          double wsum[4] = {0, 0, 0, 0};
+          int n = 0;
+          for (int t = T - 2; t >= 1; --t) {
+            const unsigned long long e2 = h[((size_t)1 * T + t) * 5 + 2];  // Q0 TR(t,2)
+            const unsigned long long* r = &h[((size_t)5 * T + t) * 5];
+            if (!r[0]) continue;
+            for (int w = 0; w < 4; ++w) wsum[w] += (double)r[w] - (double)e2;
+            ++n;
+          }
+          if (n)
+            fprintf(stderr, "[hdp trace] bwd Q0 warps reach the epilogue barrier at +%.0f +%.0f +%.0f +%.0f ns after MMA done\n",
+                    wsum[0] / n, wsum[1] / n, wsum[2] / n, wsum[3] / n);
+        }
+        // dX1 hand-off timeline (group 0, units 0..63): X publishes -> Q0 fetch issued -> Q0 needs
+        const unsigned long long z0 = h[(size_t)(T - 1) * 5];
+        for (int t = T - 3; t >= 0; t -= (T > 40 ? 20 : 5)) {
+          const unsigned long long* r = &h[((size_t)4 * T + t) * 5];
+          fprintf(stderr, "[hdp trace] Q0 t=%d: gates/c fetch issued +%.0f  needed +%.0f  slot t landed +%.0f  slot t-1 landed +%.0f ns\n", t,
+                  (double)(r[0] - z0), (double)(r[2] - z0), (double)(r[3] - z0), (double)(r[4] - z0));
+        }
+      }
       {
         double q[3] = {0, 0, 0};
         int n = 0;

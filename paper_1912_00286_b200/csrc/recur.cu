@@ -1172,8 +1172,8 @@ __device__ __forceinline__ void bwd_proj_role_ts(const Bwd2Params& P, int grp) {
 
   const int pf_thr = 97, st_thr = 96;
   const unsigned* q1f = P.q1done + grp * 32;
-  auto fetch = [&](int tt) {  // pf thread
-    spin_until(q1f, (unsigned)(G * (T - tt)));
+  auto fetch = [&](int tt, bool known_ready = false) {  // pf thread
+    if (!known_ready) spin_until(q1f, (unsigned)(G * (T - tt)));
     fence_proxy_async();
     ptx::mbar_arrive_expect_tx(barA + tt % 3, abytes);
     for (int kb = 0; kb < nkb; ++kb)
@@ -1206,15 +1206,7 @@ __device__ __forceinline__ void bwd_proj_role_ts(const Bwd2Params& P, int grp) {
       if (ptx::elect_one_sync()) ptx::mma_commit(barM);
       __syncwarp();
     }
-    if (warp == 3) {
-      // idle during the MMAs: keep prefetching dA1 operands as soon as Q1 publishes them
-      // (warp-uniform exit: lane 0's observation decides for the whole warp)
-      while (!__shfl_sync(0xffffffffu, (int)ptx::mbar_try_wait_relaxed(barM, mph), 0)) {
-        if (lane == 1 && nf >= 0 && nf >= t - 2 && acquire_ld(q1f) >= (unsigned)(G * (T - nf))) fetch(nf--);
-        __syncwarp();
-      }
-      ptx::mbar_wait_relaxed(barM, mph);
-    } else {
+    {
       ptx::mbar_wait_relaxed(barM, mph);
     }
     mph ^= 1u;
@@ -1245,6 +1237,7 @@ __device__ __forceinline__ void bwd_proj_role_ts(const Bwd2Params& P, int grp) {
         ptx::bulk_wait_group1();
         fence_proxy_async();
         release_add(xf, 1u);
+        if (P.trace && rank == 0 && grp == 0) P.trace[(size_t)4 * T * 5 + (t + 2) * 5 + 1] = ptx::globaltimer_ns();
       }
       ptx::tma_store_2d(&P.tmDXo, so, j0, t * B + col0);
       ptx::bulk_commit_group();
@@ -1255,7 +1248,7 @@ __device__ __forceinline__ void bwd_proj_role_ts(const Bwd2Params& P, int grp) {
       }
     }
     // ring slot (t-2) % 3 = (t+1) % 3 was read by step t+1's MMAs (complete): prefetch ahead
-    if (threadIdx.x == pf_thr && nf >= 0 && nf >= t - 2 && acquire_ld(q1f) >= (unsigned)(G * (T - nf))) fetch(nf--);
+    if (threadIdx.x == pf_thr && nf >= 0 && nf >= t - 2 && acquire_ld(q1f) >= (unsigned)(G * (T - nf))) fetch(nf--, true);
     if (xtr) xtr[t * 5 + 4] = ptx::globaltimer_ns();
   }
   ptx::tc_fence_after();
@@ -1427,7 +1420,8 @@ __global__ void __launch_bounds__(128, 1)
   uint64_t* fullA = bars + 2;                  // [2]: peers' bulk copies into sA[p]
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 4);
   uint64_t* barD = bars + 5;                   // [3] TSQ, Q0: dX1_t slice landed in sD[t % 3]
-  uint64_t* barP = bars + 8;                   // [3] TSQ: gates_t + C_t tiles landed in ring slot t % 3
+  constexpr int RG = 5;                        // gates / c ring depth (fetched RG-1 steps ahead)
+  uint64_t* barP = bars + 8;                   // [RG] TSQ: gates_t + C_t tiles landed in ring slot t % RG
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int G = gridDim.x;
@@ -1461,7 +1455,7 @@ __global__ void __launch_bounds__(128, 1)
     ptx::mbar_init(barD, 1);
     ptx::mbar_init(barD + 1, 1);
     ptx::mbar_init(barD + 2, 1);
-    for (int i = 0; i < 3; ++i) ptx::mbar_init(barP + i, 1);
+    for (int i = 0; i < RG; ++i) ptx::mbar_init(barP + i, 1);
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc(tslot, tcols);
@@ -1510,8 +1504,9 @@ __global__ void __launch_bounds__(128, 1)
   const bool dpf = TSQ && qi == 1;
   float* sD = reinterpret_cast<float*>(sU);    // [3][Bc][64] fp32 (two steps ahead)
   const int pf_thr = 97;
-  auto fetch_dx = [&](int tt) {  // pf thread: wait for X's slice of step tt, then TMA it
-    spin_until(P.xdone + (grp * 8 + rank) * 32, (unsigned)(T - tt));
+  unsigned long long* tr4 = (P.trace && qi == 1 && blockIdx.x == 0 && grp == 0) ? P.trace + (size_t)4 * T * 5 : nullptr;
+  auto fetch_dx = [&](int tt, bool known_ready = false) {  // pf thread: wait for X's slice of step tt, then TMA it
+    if (!known_ready) spin_until(P.xdone + (grp * 8 + rank) * 32, (unsigned)(T - tt));
     fence_proxy_async();
     ptx::mbar_arrive_expect_tx(barD + tt % 3, Bc * 64 * 4);
     ptx::tma_load_2d(sD + (tt % 3) * Bc * 64, &P.tmDX, barD + tt % 3, j0, tt * B + col0);
@@ -1526,17 +1521,17 @@ __global__ void __launch_bounds__(128, 1)
   // TSQ: the step's saved gates and c (written by the forward kernel, usually no longer in L2)
   // arrive by TMA two steps ahead into a 3-slot ring, instead of per-thread loads whose HBM
   // latency the epilogue waited for
-  __half* sGp = reinterpret_cast<__half*>(sU + 3 * Bc * 64 * 4);                 // [3][Bc][256]
-  float* sCp = reinterpret_cast<float*>(sU + 3 * Bc * 64 * 4 + 3 * Bc * 256 * 2);  // [3][Bc][64]
+  // (measured: these loads take ~4 us to land -- far-die HBM under the wavefront's traffic)
+  __half* sGp = reinterpret_cast<__half*>(sU + 3 * Bc * 64 * 4);                  // [RG][Bc][256]
+  float* sCp = reinterpret_cast<float*>(sU + 3 * Bc * 64 * 4 + RG * Bc * 256 * 2);  // [RG][Bc][64]
   auto fetch_gc = [&](int tt) {
-    ptx::mbar_arrive_expect_tx(barP + tt % 3, Bc * 256 * 2 + Bc * 64 * 4);
-    ptx::tma_load_2d(sGp + (tt % 3) * Bc * 256, &P.tmGq[qi], barP + tt % 3, j0 * 4, tt * B + col0);
-    ptx::tma_load_2d(sCp + (tt % 3) * Bc * 64, &P.tmCq[qi], barP + tt % 3, j0, tt * B + col0);
+    if (tr4) tr4[tt * 5 + 0] = ptx::globaltimer_ns();
+    ptx::mbar_arrive_expect_tx(barP + tt % RG, Bc * 256 * 2 + Bc * 64 * 4);
+    ptx::tma_load_2d(sGp + (tt % RG) * Bc * 256, &P.tmGq[qi], barP + tt % RG, j0 * 4, tt * B + col0);
+    ptx::tma_load_2d(sCp + (tt % RG) * Bc * 64, &P.tmCq[qi], barP + tt % RG, j0, tt * B + col0);
   };
-  if (TSQ && threadIdx.x == pf_thr) {
-    fetch_gc(T - 1);
-    if (T >= 2) fetch_gc(T - 2);
-  }
+  if (TSQ && threadIdx.x == pf_thr)
+    for (int tt = T - 1; tt >= 0 && tt >= T - (RG - 1); --tt) fetch_gc(tt);
 
   float dcr[NC * 8];
 #pragma unroll
@@ -1626,16 +1621,7 @@ __global__ void __launch_bounds__(128, 1)
         ptx::mma_commit(barM);
       }
       __syncwarp();
-      if (dpf && warp == 3) {
-        // idle during the MMAs: keep prefetching dX1 slices as soon as X publishes them
-        // (warp-uniform exit: lane 0's observation decides for the whole warp)
-        while (!__shfl_sync(0xffffffffu, (int)ptx::mbar_try_wait_relaxed(barM, (T - 2 - t) & 1), 0)) {
-          if (lane == 1 && nf >= 0 && nf >= t - 2 && acquire_ld(P.xdone + (grp * 8 + rank) * 32) >= (unsigned)(T - nf))
-            fetch_dx(nf--);
-          __syncwarp();
-        }
-        ptx::mbar_wait_relaxed(barM, (T - 2 - t) & 1);
-      } else {
+      {
         ptx::mbar_wait_relaxed(barM, (T - 2 - t) & 1);
       }
       ptx::tc_fence_after();
@@ -1646,19 +1632,23 @@ __global__ void __launch_bounds__(128, 1)
     }
     if (tr) trace[t * 5 + 2] = ptx::globaltimer_ns();
     if (TSQ) {
-      ptx::mbar_wait(barP + t % 3, ((T - 1 - t) / 3) & 1);
-      if (t > 0) ptx::mbar_wait(barP + (t - 1) % 3, ((T - t) / 3) & 1);  // c_{t-1} (fetched one step later)
+      if (tr4 && threadIdx.x == 0) tr4[t * 5 + 2] = ptx::globaltimer_ns();
+      ptx::mbar_wait(barP + t % RG, ((T - 1 - t) / RG) & 1);
+      if (tr4 && threadIdx.x == 0) tr4[t * 5 + 3] = ptx::globaltimer_ns();
+      if (t > 0) ptx::mbar_wait(barP + (t - 1) % RG, ((T - t) / RG) & 1);  // c_{t-1} (fetched one step later)
+      if (tr4 && threadIdx.x == 0) tr4[t * 5 + 4] = ptx::globaltimer_ns();
 #pragma unroll
       for (int ch = 0; ch < NC; ++ch)
 #pragma unroll
         for (int k = 0; k < 8; ++k) {
           const int bl = ch * 16 + half * 8 + k;
-          cc[ch * 8 + k] = sCp[((t % 3) * Bc + bl) * 64 + ul];
-          cp[ch * 8 + k] = t > 0 ? sCp[(((t + 2) % 3) * Bc + bl) * 64 + ul] : 0.f;  // slot of step t-1
-          gq[ch * 8 + k] = *reinterpret_cast<const uint2*>(sGp + ((t % 3) * Bc + bl) * 256 + 4 * ul);
+          cc[ch * 8 + k] = sCp[((t % RG) * Bc + bl) * 64 + ul];
+          cp[ch * 8 + k] = t > 0 ? sCp[(((t + RG - 1) % RG) * Bc + bl) * 64 + ul] : 0.f;  // slot of step t-1
+          gq[ch * 8 + k] = *reinterpret_cast<const uint2*>(sGp + ((t % RG) * Bc + bl) * 256 + 4 * ul);
         }
     }
     if (dpf) {
+
       if (threadIdx.x == pf_thr) {
         const unsigned long long w0 = trw ? ptx::globaltimer_ns() : 0;
         while (nf >= t) fetch_dx(nf--);  // due now: blocking
@@ -1726,6 +1716,7 @@ __global__ void __launch_bounds__(128, 1)
       }
     }
     if (trq) trq[t * 5 + 2] = ptx::globaltimer_ns();
+    if (tr4 && lane == 0) P.trace[(size_t)5 * T * 5 + t * 5 + warp] = ptx::globaltimer_ns();  // per-warp arrival
     if (TSQ && threadIdx.x == st_thr) {
       const unsigned long long w0 = trw ? ptx::globaltimer_ns() : 0;
       ptx::bulk_wait_group_read0();  // all earlier stores finished reading their staging
@@ -1761,10 +1752,11 @@ __global__ void __launch_bounds__(128, 1)
     if (tr) trace[t * 5 + 3] = ptx::globaltimer_ns();
     // ring slot (t-2) % 3 = (t+1) % 3 was last read by the epilogues of steps t+1 and t+2
     // (steps read slots t % 3 and (t-1) % 3), i.e. before the barrier above
-    if (TSQ && threadIdx.x == pf_thr && t >= 2) fetch_gc(t - 2);
+    // slot (t-(RG-1)) % RG = (t+1) % RG was last read by steps t+1 and t+2
+    if (TSQ && threadIdx.x == pf_thr && t >= RG - 1) fetch_gc(t - (RG - 1));
     if (dpf && threadIdx.x == pf_thr && nf >= 0 && nf >= t - 2 &&
         acquire_ld(P.xdone + (grp * 8 + rank) * 32) >= (unsigned)(T - nf))
-      fetch_dx(nf--);
+      fetch_dx(nf--, true);
     // push dA_t (consumed by step t-1) into every peer's sA[t & 1]: one bulk copy per peer.
     // WAR: a peer writes sA[p] of step s only after consuming my dA_{s+1}, which I produce
     // after my MMA that read sA[p] for step s+2 -- the double buffers need no extra barrier.
