@@ -150,6 +150,36 @@ int hdp_set_lr_schedule(hdp_ctx* ctx, double lambda0, double gamma, double n_hal
 double hdp_lr(const hdp_ctx* ctx, int epoch);
 /* Loss scale alpha > 0 (PAPER.md:177; default 10, :127).              */
 int hdp_set_loss_scale(hdp_ctx* ctx, float alpha);
+/* L2 regularisation coefficient l2 >= 0 ("application of L2
+ * regularization"; SPEC.md:171 loss = alpha*mean hinge + alpha*l2*||W||^2;
+ * DESIGN.md reading Q16).  Applies to every parameter w of the working
+ * weights (fp16 copy in mixed mode, R1):
+ *   - hdp_lstm_forward's loss_out gains l2 * sum(w^2) (fp64 partial sums,
+ *     deterministic order);
+ *   - hdp_grad_average_update adds fp32(2*l2) * w to the descaled average
+ *     gradient before the optimizer step (K11; the alpha the term would carry
+ *     inside the scaled loss cancels in the descale).
+ * Default 0 (off).  Errors: l2 < 0 or not finite -> HDP_ERR_ARG, nothing
+ * changed.  Changing it drops the captured forward graphs.               */
+int hdp_set_l2(hdp_ctx* ctx, double l2);
+/* Dynamic loss scaling (NEXT-3; PAPER.md:134 names fp16 overflow as the hazard
+ * of the static alpha of :177; reading Q14b).  growth_interval > 0
+ * switches it on (0 = static alpha, the default): alpha moves to the device,
+ * starting at the current hdp_set_loss_scale value, and every
+ * hdp_grad_average_update first counts the non-finite values of all ranks'
+ * fp16 gradients (all-reduced across ranks), then
+ *   - count > 0: the update is skipped (fp32 master, optimizer state and fp16
+ *     weights unchanged on every rank), alpha /= 2 (not below 1); the call does
+ *     NOT return HDP_ERR_NONFINITE and the context is not poisoned;
+ *   - count = 0: the update runs with inv_scale = fp32(1/(N*alpha)); after
+ *     growth_interval consecutive finite steps alpha *= 2.
+ * alpha stays on the device (no host synchronisation per step).  Requires a
+ * bound context; toggling drops the captured forward graphs.
+ * Errors: growth_interval < 0 -> HDP_ERR_ARG; unbound -> HDP_ERR_STATE.      */
+int hdp_set_dynamic_loss_scale(hdp_ctx* ctx, int growth_interval);
+/* Current alpha and the number of skipped steps since dynamic scaling was
+ * enabled (synchronises the device).  With static alpha: the set value, 0.   */
+int hdp_loss_scale_state(hdp_ctx* ctx, float* alpha, int* skipped_steps);
 
 /* fprop of slot `slot`'s mini-batch and the scaled hinge
  * loss Eq. 6 (:179).
@@ -225,10 +255,12 @@ void* hdp_debug_buffer(hdp_ctx* ctx, int slot, const char* name);
  * copy (either may be NULL).  count % 8 == 0 and 16-byte aligned pointers
  * use 128-bit accesses (any count is accepted).  nonfinite_dev (device
  * int, nullable) is incremented by the number of Inf/NaN contributions.
- * adam = {b1, b2, eps, step k >= 1} (ignored for SGD-m).                  */
+ * adam = {b1, b2, eps, step k >= 1} (ignored for SGD-m).  l2x2 = fp32(2*l2)
+ * adds the L2 gradient l2x2 * w_work after the descale (w_work = fp16(W) if
+ * w16 is given, else W; 0 = off; hdp_set_l2).                             */
 int hdp_fused_avg_update(const void* grads, long long src_stride, int nsrc, int grads_f32, long long count,
                          float* W, float* S1, float* S2, void* w16, float* w32, float inv_scale, float lr,
-                         float momentum, int optimizer, const double* adam, int* nonfinite_dev, void* stream);
+                         float momentum, int optimizer, const double* adam, int* nonfinite_dev, float l2x2, void* stream);
 
 /* Gate-contraction GEMM, C[m][n] = sum_k A(m,k) B(n,k) (+bias, ReLU),
  * fp16 operands on the tcgen05 tensor cores, fp32 accumulate.

@@ -60,16 +60,28 @@ def scalars_f32(N: int, alpha: float, lam: float, m: float):
     return F32(1.0 / (N * alpha)), F32(lam), F32(m)
 
 
-def fused_avg_update_f32(grads, W, H, inv_scale, lam, m):
+def l2_term_f32(g, W, l2x2, mixed: bool):
+    """g + fp32(2*l2) * w_work, each op rounded to fp32; w_work is the working
+    weight the step's fprop used: fp16(W) in mixed mode (R1), W in FP32 mode."""
+    if not l2x2:
+        return g
+    Wf = np.asarray(W, F32)
+    wk = Wf.astype(np.float16).astype(F32) if mixed else Wf
+    return (g + (F32(l2x2) * wk).astype(F32)).astype(F32)
+
+
+def fused_avg_update_f32(grads, W, H, inv_scale, lam, m, l2x2=0.0, mixed=True):
     """float32 emulation of the fused average + SGD-m update.
 
     grads: list (rank order) of fp16 or fp32 arrays; W, H: float32 arrays.
+    l2x2 = fp32(2*l2) adds the L2 gradient (``l2_term_f32``) after the descale.
     Returns (W', H', w16', nonfinite_count).
     """
     s = np.asarray(grads[0]).astype(F32)
     for g in grads[1:]:
         s = (s + np.asarray(g).astype(F32)).astype(F32)
     g = (s * F32(inv_scale)).astype(F32)
+    g = l2_term_f32(g, W, l2x2, mixed)
     t1 = (F32(m) * np.asarray(H, F32)).astype(F32)
     t2 = (F32(lam) * g).astype(F32)
     Hn = (t1 - t2).astype(F32)
@@ -83,13 +95,14 @@ def adam_consts_f32(lam, k, b1=0.9, b2=0.999, eps=1e-8):
                 c1=F32(1.0 / (1.0 - b1 ** k)), c2=F32(1.0 / (1.0 - b2 ** k)), eps=F32(eps))
 
 
-def fused_avg_adam_f32(grads, W, m1, v, inv_scale, c):
+def fused_avg_adam_f32(grads, W, m1, v, inv_scale, c, l2x2=0.0, mixed=True):
     """float32 emulation of the fused average + Adam update (same op order
     as the kernel: every product and sum separately rounded)."""
     s = np.asarray(grads[0]).astype(F32)
     for gr in grads[1:]:
         s = (s + np.asarray(gr).astype(F32)).astype(F32)
     g = (s * F32(inv_scale)).astype(F32)
+    g = l2_term_f32(g, W, l2x2, mixed)
     m1n = ((c["b1"] * np.asarray(m1, F32)).astype(F32) + (c["omb1"] * g).astype(F32)).astype(F32)
     gg = (g * g).astype(F32)
     vn = ((c["b2"] * np.asarray(v, F32)).astype(F32) + (c["omb2"] * gg).astype(F32)).astype(F32)
@@ -101,3 +114,21 @@ def fused_avg_adam_f32(grads, W, m1, v, inv_scale, c):
     Wn = (np.asarray(W, F32) - stp).astype(F32)
     nonfinite = int(sum(np.count_nonzero(~np.isfinite(np.asarray(gr))) for gr in grads))
     return Wn, m1n, vn, Wn.astype(np.float16), nonfinite
+
+
+def dynamic_loss_scale(alpha: float, good: int, nonfinite: int, interval: int, factor: float = 2.0,
+                       min_alpha: float = 1.0):
+    """Dynamic loss scaling (NEXT-3; PAPER.md:134 names fp16 overflow as the hazard
+    the static alpha of :177 leaves open; reading Q14b in DESIGN.md).
+
+    A step whose gradients contain a non-finite fp16 value is skipped (weights and
+    optimizer state unchanged) and alpha is divided by ``factor`` (not below
+    ``min_alpha``); after ``interval`` consecutive finite steps alpha is multiplied
+    by ``factor``.  Returns (alpha', good', skipped)."""
+    if nonfinite:
+        return max(alpha / factor, min_alpha), 0, True
+    good += 1
+    if good >= interval:
+        return alpha * factor, 0, False
+    return alpha, good, False
+

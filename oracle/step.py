@@ -10,6 +10,13 @@
 The global batch is split contiguously: worker r gets rows
 [r*B/N, (r+1)*B/N).  The learning rate is passed in (``schedule``
 computes it); the oracle does not decide N-dependence itself.
+
+L2 regularisation ("application of L2 regularization"; SPEC.md:171
+"loss = alpha*mean hinge + alpha*l2*||W||^2"; reading Q16 in DESIGN.md): the
+penalty l2 * sum(w^2) runs over every parameter w of the working weights used
+by this step's fprop (R1), is part of the reported loss, and its gradient
+2*l2*w is added to the averaged data gradient (the alpha it would carry inside
+the scaled loss cancels in the descale, so it is added after step 4).
 """
 from __future__ import annotations
 
@@ -37,7 +44,7 @@ def worker_grads(cfg, wflat, x, targets, alpha, mode, abs_terms=None):
 def train_step(cfg, master, state: Dict[str, np.ndarray], x_global, t_global, N: int,
                alpha: float, lam: float, mode: str, optimizer: str = "sgdm",
                momentum: float = 0.9, adam_k: int = 1,
-               grads_override: Optional[list] = None):
+               grads_override: Optional[list] = None, l2: float = 0.0, skip_nonfinite: bool = False):
     """Returns a dict with loss (unscaled mean over workers), per-worker
     gradients (carrying alpha), the averaged gradient, new master/state,
     the fp16 working copy and the non-finite count."""
@@ -57,14 +64,19 @@ def train_step(cfg, master, state: Dict[str, np.ndarray], x_global, t_global, N:
         grads = grads_override
     nonfinite = sum(count_nonfinite(g) for g in grads)
     avg = optim.average(grads, N, alpha)
-    if optimizer == "sgdm":
+    if l2:
+        avg = avg + 2.0 * l2 * w
+    if skip_nonfinite and nonfinite:
+        # dynamic loss scaling (optim.dynamic_loss_scale): the step is skipped
+        W, new_state = np.asarray(master, np.float64), dict(state)
+    elif optimizer == "sgdm":
         W, H = optim.sgdm(master, state["H"], avg, lam, momentum)
         new_state = {"H": H}
     else:
         W, m1, v = optim.adam(master, state["m1"], state["v"], avg, lam, adam_k)
         new_state = {"m1": m1, "v": v}
     return {
-        "loss": float(np.sum(losses) / (N * alpha)),
+        "loss": float(np.sum(losses) / (N * alpha)) + (float(l2 * np.dot(w, w)) if l2 else 0.0),
         "losses_scaled": losses,
         "grads": grads,
         "abs_terms": abs_terms,

@@ -4,6 +4,7 @@
 // Per owned element, in this exact fp32 operation order (R14/R15):
 //   s  = fp32(g_0) + fp32(g_1) + ... + fp32(g_{N-1})     rank order, each add RNE
 //   g  = s * inv_scale                                  inv_scale = fp32(1/(N*alpha))
+//   g  = g + l2x2 * w_work     (only if l2 > 0; w_work = fp16(W) in mixed mode)
 //   SGD-m:  H = m*H - lam*g ;  W = W + H                (each op separately RNE, no FMA)
 //   Adam :  m1 = b1*m1 + (1-b1)*g ; v = b2*v + (1-b2)*g*g ;
 //           W  = W - lam * (m1*c1) / (sqrt(v*c2) + eps)
@@ -71,8 +72,15 @@ __device__ __forceinline__ float upd_adam(const UpdateArgs& a, float g, float& W
   return W;
 }
 
+__device__ __forceinline__ float l2_term(const UpdateArgs& a, float g, float W) {
+  const float wk = a.w16 ? __half2float(__float2half_rn(W)) : W;
+  return __fadd_rn(g, __fmul_rn(a.l2x2, wk));
+}
+
 template <typename GT, int OPT>
 __global__ void __launch_bounds__(256) avg_update_kernel(UpdateArgs a) {
+  if (a.skip && *a.skip) return;  // dynamic loss scaling: non-finite step, nothing changes
+  if (a.alpha_dev) a.inv_scale = (float)(1.0 / (a.n_workers * (double)*a.alpha_dev));  // R14
   const GT* __restrict__ g = static_cast<const GT*>(a.g);
   const long nvec = a.count >> 3;
   int nf = 0;
@@ -90,14 +98,19 @@ __global__ void __launch_bounds__(256) avg_update_kernel(UpdateArgs a) {
     float4 S0 = *reinterpret_cast<const float4*>(a.S1 + e), S1 = *reinterpret_cast<const float4*>(a.S1 + e + 4);
     float w[8] = {W0.x, W0.y, W0.z, W0.w, W1.x, W1.y, W1.z, W1.w};
     float h[8] = {S0.x, S0.y, S0.z, S0.w, S1.x, S1.y, S1.z, S1.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      s[i] = __fmul_rn(s[i], a.inv_scale);
+      if (a.l2x2 != 0.f) s[i] = l2_term(a, s[i], w[i]);
+    }
     if (OPT == 0) {
 #pragma unroll
-      for (int i = 0; i < 8; ++i) upd_sgdm(a, __fmul_rn(s[i], a.inv_scale), w[i], h[i]);
+      for (int i = 0; i < 8; ++i) upd_sgdm(a, s[i], w[i], h[i]);
     } else {
       float4 V0 = *reinterpret_cast<const float4*>(a.S2 + e), V1 = *reinterpret_cast<const float4*>(a.S2 + e + 4);
       float vv[8] = {V0.x, V0.y, V0.z, V0.w, V1.x, V1.y, V1.z, V1.w};
 #pragma unroll
-      for (int i = 0; i < 8; ++i) upd_adam(a, __fmul_rn(s[i], a.inv_scale), w[i], h[i], vv[i]);
+      for (int i = 0; i < 8; ++i) upd_adam(a, s[i], w[i], h[i], vv[i]);
       *reinterpret_cast<float4*>(a.S2 + e) = make_float4(vv[0], vv[1], vv[2], vv[3]);
       *reinterpret_cast<float4*>(a.S2 + e + 4) = make_float4(vv[4], vv[5], vv[6], vv[7]);
     }
@@ -126,11 +139,13 @@ __global__ void __launch_bounds__(256) avg_update_kernel(UpdateArgs a) {
       s = r == 0 ? t : __fadd_rn(s, t);
     }
     float w = a.W[e], h = a.S1[e];
+    s = __fmul_rn(s, a.inv_scale);
+    if (a.l2x2 != 0.f) s = l2_term(a, s, w);
     if (OPT == 0) {
-      upd_sgdm(a, __fmul_rn(s, a.inv_scale), w, h);
+      upd_sgdm(a, s, w, h);
     } else {
       float vv = a.S2[e];
-      upd_adam(a, __fmul_rn(s, a.inv_scale), w, h, vv);
+      upd_adam(a, s, w, h, vv);
       a.S2[e] = vv;
     }
     a.W[e] = w;
@@ -144,7 +159,49 @@ __global__ void __launch_bounds__(256) avg_update_kernel(UpdateArgs a) {
   }
 }
 
+template <typename GT>
+__global__ void __launch_bounds__(256) count_nonfinite_kernel(const GT* __restrict__ g, long n, int* count) {
+  int nf = 0;
+  const long nvec = n >> 3;
+  for (long v = blockIdx.x * (long)blockDim.x + threadIdx.x; v < nvec; v += (long)gridDim.x * blockDim.x) {
+    float t[8];
+    Vec8<GT>::load(g + (v << 3), t, nf);
+  }
+  for (long e = (nvec << 3) + blockIdx.x * (long)blockDim.x + threadIdx.x; e < n; e += (long)gridDim.x * blockDim.x)
+    nf += !isfinite(static_cast<float>(g[e]));
+  nf = __reduce_add_sync(0xffffffffu, nf);
+  if ((threadIdx.x & 31) == 0 && nf) atomicAdd(count, nf);
+}
+
+__global__ void loss_scale_update_kernel(int* st, float* alpha, int interval, float factor, float min_alpha) {
+  if (threadIdx.x != 0) return;
+  if (st[0] > 0) {
+    *alpha = fmaxf(*alpha / factor, min_alpha);
+    st[1] = 0;
+    st[2] += 1;
+  } else if (++st[1] >= interval) {
+    *alpha = *alpha * factor;
+    st[1] = 0;
+  }
+}
+
 }  // namespace
+
+cudaError_t launch_count_nonfinite(const void* g, long n, int g_f32, int* count, cudaStream_t s) {
+  if (n <= 0) return cudaSuccess;
+  long blocks = ((n >> 3) + 255) / 256;
+  if (blocks > 148L * 8) blocks = 148L * 8;
+  if (blocks < 1) blocks = 1;
+  if (g_f32) count_nonfinite_kernel<float><<<(int)blocks, 256, 0, s>>>((const float*)g, n, count);
+  else count_nonfinite_kernel<__half><<<(int)blocks, 256, 0, s>>>((const __half*)g, n, count);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_loss_scale_update(int* st, float* alpha, int interval, float factor, float min_alpha,
+                                     cudaStream_t s) {
+  loss_scale_update_kernel<<<1, 32, 0, s>>>(st, alpha, interval, factor, min_alpha);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_avg_update(const UpdateArgs& a, int grad_is_f32, int optimizer, cudaStream_t s) {
   if (a.count <= 0) return cudaSuccess;

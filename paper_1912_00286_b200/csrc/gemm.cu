@@ -10,6 +10,7 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstdio>
 #include <mutex>
 
@@ -117,6 +118,105 @@ __device__ __forceinline__ void epi_store16(const Epilogue& epi, float* ws, int 
   }
 }
 
+// ---------------------------------------------------------------- fused cell epilogues
+// Same cell as K3 / K6 (lstm_kernels.cu; PAPER.md:60-62 cell, :82 BPTT) with the SFU
+// activations of the persistent recurrence kernels (recur.cu): sigma via __expf, tanh(x) =
+// 2 sigma(2x) - 1; relative error ~1e-6, far below the fp16 rounding of everything stored.
+__device__ __forceinline__ float lstm_sigmoid(float x) { return __fdividef(1.f, 1.f + __expf(-x)); }
+__device__ __forceinline__ float lstm_tanh(float x) {
+  const float xc = fminf(fmaxf(x, -15.f), 15.f);
+  return fmaf(2.f, lstm_sigmoid(2.f * xc), -1.f);
+}
+
+// A3 for 8 units of row m: columns [n, n+32) of the gate pre-activation (n = 4 u0).
+__device__ __forceinline__ void lstm_fwd_chunk(const Epilogue& e, int m, int n, const float (&v)[32]) {
+  const int u0 = n >> 2;
+  const float4* gx = reinterpret_cast<const float4*>(e.gx + (size_t)m * 4 * e.hp + n);
+  float cp[8];
+  if (e.cprev) {
+    const float4* p = reinterpret_cast<const float4*>(e.cprev + (size_t)m * e.hp + u0);
+    const float4 a = p[0], b = p[1];
+    cp[0] = a.x; cp[1] = a.y; cp[2] = a.z; cp[3] = a.w; cp[4] = b.x; cp[5] = b.y; cp[6] = b.z; cp[7] = b.w;
+  } else {
+#pragma unroll
+    for (int j = 0; j < 8; ++j) cp[j] = 0.f;
+  }
+  __align__(16) __half gh[32];
+  __align__(16) __half hh[8];
+  float cn[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float4 g4 = gx[j];
+    const float i = lstm_sigmoid(g4.x + v[4 * j]), f = lstm_sigmoid(g4.y + v[4 * j + 1]);
+    const float g = lstm_tanh(g4.z + v[4 * j + 2]), o = lstm_sigmoid(g4.w + v[4 * j + 3]);
+    const float c = f * cp[j] + i * g;
+    cn[j] = c;
+    hh[j] = __float2half_rn(o * lstm_tanh(c));  // R6
+    gh[4 * j] = __float2half_rn(i);         // R4
+    gh[4 * j + 1] = __float2half_rn(f);
+    gh[4 * j + 2] = __float2half_rn(g);
+    gh[4 * j + 3] = __float2half_rn(o);
+  }
+  uint4* go = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(e.gates) + (size_t)m * 4 * e.hp + n);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) go[q] = reinterpret_cast<const uint4*>(gh)[q];
+  float4* co = reinterpret_cast<float4*>(e.cout + (size_t)m * e.hp + u0);
+  co[0] = make_float4(cn[0], cn[1], cn[2], cn[3]);
+  co[1] = make_float4(cn[4], cn[5], cn[6], cn[7]);
+  *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(e.hout) + (size_t)m * e.hp + u0) =
+      *reinterpret_cast<const uint4*>(hh);
+}
+
+// Same, with G_x and c_{t-1} already in registers.
+__device__ __forceinline__ void lstm_fwd_chunk_reg(const Epilogue& e, int m, int n, const float (&v)[32],
+                                                   const float4 (&gx)[8], const float4 (&cp4)[2]) {
+  const int u0 = n >> 2;
+  const float cp[8] = {cp4[0].x, cp4[0].y, cp4[0].z, cp4[0].w, cp4[1].x, cp4[1].y, cp4[1].z, cp4[1].w};
+  __align__(16) __half gh[32];
+  __align__(16) __half hh[8];
+  float cn[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j) {
+    const float i = lstm_sigmoid(gx[j].x + v[4 * j]), f = lstm_sigmoid(gx[j].y + v[4 * j + 1]);
+    const float g = lstm_tanh(gx[j].z + v[4 * j + 2]), o = lstm_sigmoid(gx[j].w + v[4 * j + 3]);
+    const float c = f * cp[j] + i * g;
+    cn[j] = c;
+    hh[j] = __float2half_rn(o * lstm_tanh(c));  // R6
+    gh[4 * j] = __float2half_rn(i);         // R4
+    gh[4 * j + 1] = __float2half_rn(f);
+    gh[4 * j + 2] = __float2half_rn(g);
+    gh[4 * j + 3] = __float2half_rn(o);
+  }
+  uint4* go = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(e.gates) + (size_t)m * 4 * e.hp + n);
+#pragma unroll
+  for (int q = 0; q < 4; ++q) go[q] = reinterpret_cast<const uint4*>(gh)[q];
+  float4* co = reinterpret_cast<float4*>(e.cout + (size_t)m * e.hp + u0);
+  co[0] = make_float4(cn[0], cn[1], cn[2], cn[3]);
+  co[1] = make_float4(cn[4], cn[5], cn[6], cn[7]);
+  *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(e.hout) + (size_t)m * e.hp + u0) =
+      *reinterpret_cast<const uint4*>(hh);
+}
+
+// A6 for unit idx = m * hp + u given dh_rec (the reduced K7 result).
+__device__ __forceinline__ void lstm_bwd_unit(const Epilogue& e, size_t idx, float dh_rec) {
+  float dh = 0.f;
+  if (e.dha) dh += e.dha[idx];
+  dh += dh_rec;
+  const uint2 gu = reinterpret_cast<const uint2*>(e.gates)[idx];
+  const float2 g01 = __half22float2(*reinterpret_cast<const __half2*>(&gu.x));
+  const float2 g23 = __half22float2(*reinterpret_cast<const __half2*>(&gu.y));
+  const float i = g01.x, f = g01.y, g = g23.x, o = g23.y;
+  const float c = e.ct[idx];
+  const float cp = e.cprev ? e.cprev[idx] : 0.f;
+  const float tc = lstm_tanh(c);
+  const float d = e.dc[idx] + dh * o * (1.f - tc * tc);
+  __align__(8) __half2 hv[2] = {
+      __halves2half2(__float2half_rn(d * g * i * (1.f - i)), __float2half_rn(d * cp * f * (1.f - f))),
+      __halves2half2(__float2half_rn(d * i * (1.f - g * g)), __float2half_rn(dh * tc * o * (1.f - o)))};
+  reinterpret_cast<uint2*>(e.dA)[idx] = *reinterpret_cast<const uint2*>(hv);  // R10
+  e.dc[idx] = d * f;
+}
+
 // Persistent, warp-specialised: each CTA walks tiles blockIdx.x, +gridDim.x, ...
 //   warp 0 (one lane): TMA producer over a continuous k-block stream (STAGES ring)
 //   warp 1           : TMEM allocation; one lane issues tcgen05.mma into one of two
@@ -169,6 +269,8 @@ __global__ void __launch_bounds__(320, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = *tslot;
+  ptx::griddep_wait();  // (PDL) the setup above overlapped the previous kernel's tail
+  ptx::griddep_launch();
 
   if (warp == 0) {
     if (lane == 0) {
@@ -250,11 +352,55 @@ __global__ void __launch_bounds__(320, 1)
       int m0, n0, z, kb0, nkb;
       decode(tile, m0, n0, z, kb0, nkb);
       const int b = lt & 1;
+      const int m = m0 + q * 32 + lane;
+      if constexpr (BN <= 128) {
+        if (epi.mode == EPI_LSTM_FWD) {
+          // fused cell: this lane's G_x and c_{t-1} are loaded while the MMAs run
+          constexpr int NCH = BN / 64;  // 32-column chunks per warp
+          float4 gx[NCH][8], cp[NCH][2];
+#pragma unroll
+          for (int h = 0; h < NCH; ++h) {
+            const int n = n0 + c_lo + 32 * h;
+            const bool ok = m < M && n < N;
+            const float4* gp = reinterpret_cast<const float4*>(epi.gx + (size_t)m * 4 * epi.hp + n);
+#pragma unroll
+            for (int j = 0; j < 8; ++j) gx[h][j] = ok ? gp[j] : make_float4(0.f, 0.f, 0.f, 0.f);
+            const float4* cq = reinterpret_cast<const float4*>(epi.cprev + (size_t)m * epi.hp + (n >> 2));
+            cp[h][0] = ok && epi.cprev ? cq[0] : make_float4(0.f, 0.f, 0.f, 0.f);
+            cp[h][1] = ok && epi.cprev ? cq[1] : make_float4(0.f, 0.f, 0.f, 0.f);
+          }
+          ptx::mbar_wait(accf + b, (lt >> 1) & 1);
+          ptx::tc_fence_after();
+          const uint32_t tq = tbase + b * BN + (static_cast<uint32_t>(q * 32) << 16);
+#pragma unroll
+          for (int h = 0; h < NCH; ++h) {
+            const int c = c_lo + 32 * h;
+            float v[32];
+            ptx::tmem_ld16_nowait(tq + c, *reinterpret_cast<float(*)[16]>(v));
+            ptx::tmem_ld16_nowait(tq + c + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+            ptx::tmem_wait_ld();
+            if (m < M && n0 + c < N) lstm_fwd_chunk_reg(epi, m, n0 + c, v, gx[h], cp[h]);
+          }
+          ptx::tc_fence_before();
+          __syncwarp();
+          if (lane == 0) ptx::mbar_arrive(acce + b);
+          continue;
+        }
+      }
       ptx::mbar_wait(accf + b, (lt >> 1) & 1);
       ptx::tc_fence_after();
       const uint32_t tq = tbase + b * BN + (static_cast<uint32_t>(q * 32) << 16);
-      const int m = m0 + q * 32 + lane;
-      if (fast) {
+      if (epi.mode == EPI_LSTM_FWD) {
+#pragma unroll 1
+        for (int c = c_lo; c < c_hi; c += 32) {
+          if (n0 + c >= N) break;
+          float v[32];
+          ptx::tmem_ld16_nowait(tq + c, *reinterpret_cast<float(*)[16]>(v));
+          ptx::tmem_ld16_nowait(tq + c + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+          ptx::tmem_wait_ld();
+          if (m < M) lstm_fwd_chunk(epi, m, n0 + c, v);
+        }
+      } else if (fast) {
         // 32 x 32 chunk through shared memory; every store instruction then writes
         // 4 whole rows (lane -> row i*4 + lane/8, 4 consecutive columns)
         float* o32 = epi.mode == EPI_SPLITK ? ws + (size_t)z * M * N : reinterpret_cast<float*>(epi.out);
@@ -344,11 +490,17 @@ __global__ void __launch_bounds__(320, 1)
 
 // Deterministic split-K reduction + the requested epilogue.
 __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, int M, int N, Epilogue epi) {
+  ptx::griddep_wait();
+  ptx::griddep_launch();
   const size_t total = (size_t)M * N;
   int nf = 0;
   for (size_t idx = blockIdx.x * (size_t)blockDim.x + threadIdx.x; idx < total; idx += (size_t)gridDim.x * blockDim.x) {
     float s = ws[idx];
     for (int z = 1; z < splits; ++z) s += ws[(size_t)z * total + idx];
+    if (epi.mode == EPI_LSTM_BWD) {
+      lstm_bwd_unit(epi, idx, s);
+      continue;
+    }
     const int m = (int)(idx / N), n = (int)(idx % N);
     if (epi.bias) s += epi.bias_on_m ? bias_at(epi, m) : bias_at(epi, n);
     if (epi.relu) s = fmaxf(s, 0.f);
@@ -493,15 +645,35 @@ int num_sms() {
   return n;
 }
 
+// programmatic dependent launch of the GEMM / split-K kernels: opt-in (HDP_PDL=1); measured
+// on the C4 per-step chain it did not shorten the step (37.6 vs 37.3 ms), the prologue it
+// overlaps is short next to the predecessor's drain + flush
+bool use_pdl() {
+  static const bool on = [] {
+    const char* e = getenv("HDP_PDL");
+    return e && e[0] == '1';
+  }();
+  return on;
+}
+
 template <int BN, int AMN, int BMN>
 cudaError_t launch_tc(const GemmPlan& p, cudaStream_t s) {
   using C = TileCfg<BN>;
   const int ntiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN) * p.splits;
   Epilogue e = p.epi;
-  if (p.splits > 1) e.mode = EPI_SPLITK;
-  gemm_tc_kernel<BN, AMN, BMN><<<std::min(ntiles, num_sms()), 320, C::SMEM, s>>>(p.ta, p.tb, p.M, p.N, p.K, p.kbps,
-                                                                                  p.splits, e, p.ws);
-  return cudaGetLastError();
+  if (p.splits > 1 || e.mode == EPI_LSTM_BWD) e.mode = EPI_SPLITK;
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(std::min(ntiles, num_sms()));
+  cfg.blockDim = dim3(320);
+  cfg.dynamicSmemBytes = C::SMEM;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = use_pdl() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, AMN, BMN>, p.ta, p.tb, p.M, p.N, p.K, p.kbps, p.splits, e,
+                            p.ws);
 }
 
 template <int BN, int AMN, int BMN>
@@ -529,7 +701,9 @@ cudaError_t launch_tc_bn(const GemmPlan& p, cudaStream_t s) {
 int choose_bn(int M, int N) {
   const int mt = (M + BM - 1) / BM;
   if (N <= 64) return 64;
-  if (mt * ((N + 127) / 128) < 148) return 64;     // latency-bound: more CTAs
+  // latency-bound: more CTAs -- unless 128-wide tiles already cover most SMs
+  // (C4 K2, 256 x 8192 x 2048: 128 tiles of 128 x 128 take 17 us, 256 of 128 x 64 27 us)
+  if (mt * ((N + 127) / 128) < 100) return 64;
   if (mt * ((N + 255) / 256) >= 148) return 256;
   return 128;
 }
@@ -590,9 +764,24 @@ int gemm_plan_tc(GemmPlan* p, const __half* A, long lda, int a_mn, const __half*
   if (splits > kb) splits = kb;
   int kbps = (kb + splits - 1) / splits;
   splits = (kb + kbps - 1) / kbps;
+  if (epi.mode == EPI_LSTM_FWD) {
+    splits = 1;
+    kbps = kb;
+  }
   if (splits > 1 && (!ws || ws_floats < (size_t)splits * M * N)) {
     splits = 1;
     kbps = kb;
+  }
+  if (epi.mode == EPI_LSTM_FWD || epi.mode == EPI_LSTM_BWD) {
+    if (epi.hp <= 0 || (epi.hp & 7) || N != (epi.mode == EPI_LSTM_FWD ? 4 * epi.hp : epi.hp)) {
+      snprintf(g_gemm_err, sizeof g_gemm_err, "fused cell epilogue: N %d does not match hp %d", N, epi.hp);
+      return -1;
+    }
+    if (epi.mode == EPI_LSTM_BWD && (!ws || ws_floats < (size_t)splits * M * N)) {
+      snprintf(g_gemm_err, sizeof g_gemm_err, "fused cell backward needs %zu workspace floats",
+               (size_t)splits * M * N);
+      return -1;
+    }
   }
   p->splits = splits;
   p->kbps = kbps;
@@ -646,12 +835,20 @@ cudaError_t gemm_run(const GemmPlan& p, cudaStream_t s) {
     case 128: e = launch_tc_bn<128>(p, s); break;
     default: e = launch_tc_bn<256>(p, s); break;
   }
-  if (e != cudaSuccess || p.splits <= 1) return e;
+  if (e != cudaSuccess || (p.splits <= 1 && p.epi.mode != EPI_LSTM_BWD)) return e;
   const size_t total = (size_t)p.M * p.N;
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;
-  splitk_reduce_kernel<<<blocks, 256, 0, s>>>(p.ws, p.splits, p.M, p.N, p.epi);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(blocks);
+  cfg.blockDim = dim3(256);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = use_pdl() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, splitk_reduce_kernel, (const float*)p.ws, p.splits, p.M, p.N, p.epi);
 }
 
 }  // namespace hdp

@@ -21,6 +21,13 @@ enum EpiMode : int {
   EPI_F32_T = 1,   // out32[n*ldo + m]      (transposed store, coalesced for swap-AB)
   EPI_F16 = 2,     // out16[m*ldo + n]      (RNE, counts non-finite results)
   EPI_SPLITK = 3,  // internal: fp32 partials for the deterministic split-K reduction
+  // A3 fused into K2 (mixed mode, gate-interleaved columns n = 4u + gate):
+  //   a = acc + gx[m][n]; i,f,o = sigma, g = tanh; c = f c_prev + i g; h = o tanh(c)
+  //   -> gates[m][n] fp16 (R4), cout[m][u] fp32 (R5), hout[m][u] fp16 (R6).  splits = 1.
+  EPI_LSTM_FWD = 4,
+  // A6 of step t-1 fused into K7 (acc = dh_rec[m][u], N = hp): the split-K reduction
+  // adds dha[m][u] and runs the cell backward -> dA[m][4u..4u+3] fp16 (R10), dc[m][u].
+  EPI_LSTM_BWD = 5,
 };
 
 struct Epilogue {
@@ -33,6 +40,17 @@ struct Epilogue {
   int relu = 0;
   int accumulate = 0;           // fp32 modes: out += result
   int* nonfinite = nullptr;     // EPI_F16: += number of non-finite outputs
+  // EPI_LSTM_FWD / EPI_LSTM_BWD operands (row stride hp for [M][hp], 4 hp for [M][4hp])
+  int hp = 0;
+  const float* gx = nullptr;    // FWD: this step's G_x (bias included)
+  const float* cprev = nullptr; // c_{t-1} (FWD) / c_{t-2} (BWD); nullptr = zeros
+  float* cout = nullptr;        // FWD: c_t
+  void* hout = nullptr;         // FWD: h_t (fp16)
+  void* gates = nullptr;        // FWD: saved gates out; BWD: saved gates of step t-1 in
+  const float* dha = nullptr;   // BWD: dH from the layer above at t-1 (nullable)
+  const float* ct = nullptr;    // BWD: c_{t-1}
+  float* dc = nullptr;          // BWD: cell-gradient carry (in/out)
+  void* dA = nullptr;           // BWD: dA_{t-1} (fp16)
 };
 
 struct GemmPlan {

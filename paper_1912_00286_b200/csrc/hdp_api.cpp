@@ -180,6 +180,12 @@ struct hdp_ctx {
   bool lr_set = false;
   double lam0 = 0, gamma = 1, n_half = 1, max_eff = 0.1, mom = 0.9, b1 = 0.9, b2 = 0.999, eps = 1e-8;
   float alpha = 10.f;
+  int dyn_interval = 0;       // dynamic loss scaling: growth interval (0 = static alpha)
+  float* alpha_dev() const { return reinterpret_cast<float*>(status + 11); }  // device alpha
+  const float* dyn_alpha() const { return dyn_interval > 0 ? alpha_dev() : nullptr; }
+  int* dyn_state() const { return status + 8; }  // [0] step count, [1] good run, [2] skipped
+  double l2 = 0.0;            // L2 coefficient (reading Q16), 0 = off
+  double* l2part = nullptr;   // partial sums of the L2 loss term
   long adam_k = 0;
 
   int L() const { return d.n_layers; }
@@ -330,6 +336,7 @@ void carve(hdp_ctx* c, char* base) {
   c->recv = cv.take(c->world > 1 ? c->P * c->gsz : 0);  // bucket bi received at its own offset
   c->status = (int*)cv.take(32768);  // [0] non-finite count; +1024 B: recurrence barrier counters;
                                        // +4096 B: backward-wavefront hand-off counters
+  c->l2part = (double*)cv.take(hdp::l2_partials_doubles() * sizeof(double));
   c->slot.assign(c->nslots, hdp_ctx::Slot{});
   if (d.n_layers > 0) {
     const long B = d.max_batch, T = d.max_seq, L = d.n_layers, hp = c->hp, e = c->esz;
@@ -371,6 +378,7 @@ void carve(hdp_ctx* c, char* base) {
       ws = std::max(ws, gemm_need((int)(4 * hp), (int)hp, (int)rows));
     }
     if (c->Fp) ws = std::max(ws, gemm_need((int)c->Fp, (int)hp, (int)rows));
+    ws = std::max(ws, (size_t)16 * B * hp);  // K7 partials of the fused cell backward
     if (c->f32) ws = 0;
     c->ws_floats = ws;
     c->ws = (float*)cv.take(ws * 4);
@@ -421,16 +429,16 @@ struct KScope {
 
 // ---------------------------------------------------------------- GEMM helper
 int gemm(hdp_ctx* c, int tag, const void* A, long lda, int amn, const void* B, long ldb, int bmn, long M, long N,
-         long K, const hdp::Epilogue& epi, cudaStream_t s) {
+         long K, const hdp::Epilogue& epi, cudaStream_t s, int force_bn = 0, int force_splits = 0) {
   hdp::GemmPlan p;
   int r;
   if (c->f32)
     r = hdp::gemm_plan_f32(&p, (const float*)A, lda, amn, (const float*)B, ldb, bmn, (int)M, (int)N, (int)K, epi);
   else
     r = hdp::gemm_plan_tc(&p, (const __half*)A, lda, amn, (const __half*)B, ldb, bmn, (int)M, (int)N, (int)K, epi,
-                          c->ws, c->ws_floats);
+                          c->ws, c->ws_floats, force_bn, force_splits);
   if (r) return fail(HDP_ERR_ARG, "gemm plan %ldx%ldx%ld: %s", M, N, K, hdp::gemm_last_error());
-  KScope ks(c, tag, p.tc && p.splits > 1 ? 2 : 1, s);
+  KScope ks(c, tag, p.tc && (p.splits > 1 || epi.mode == hdp::EPI_LSTM_BWD) ? 2 : 1, s);
   CK_CUDA(hdp::gemm_run(p, s));
   return HDP_OK;
 }
@@ -610,6 +618,19 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
       continue;
     }
     for (int t = 0; t < T; ++t) {
+      if (t > 0 && !f32) {
+        // K2 with A3 in its epilogue: gates = h_{t-1} U^T + G_x[t] -> cell -> gates, c_t, h_t
+        hdp::Epilogue ef;
+        ef.mode = hdp::EPI_LSTM_FWD;
+        ef.hp = (int)hp;
+        ef.gx = c->Gx + (long)t * B * 4 * hp;
+        ef.cprev = Cl + (long)(t - 1) * B * hp;
+        ef.cout = Cl + (long)t * B * hp;
+        ef.gates = Gl + (long)t * B * 4 * hp * e;
+        ef.hout = Hs + (long)(t + 1) * B * hp * e;
+        CK(gemm(c, HDP_K_GEMM_H, Hs + (long)t * B * hp * e, hp, 0, c->W(iU), hp, 0, B, 4 * hp, hp, ef, s));
+        continue;
+      }
       if (t > 0)  // K2: G_h = h_{t-1} U^T (A2)
         CK(gemm(c, HDP_K_GEMM_H, Hs + (long)t * B * hp * e, hp, 0, c->W(iU), hp, 0, B, 4 * hp, hp, epi_f32(c->Gh, 4 * hp), s));
       // K3 (A3)
@@ -634,7 +655,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
     {
       KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
       CK_CUDA(hdp::launch_head_out(f32, S.Z, (int)rows, (int)c->Fp, c->Fp, c->W(iwo), c->W(ibo), S.stage_t, 0, B, T,
-                                   c->alpha, 1.f / (float)rows, S.y, S.dy, S.partials, s, S.dz));
+                                   c->alpha, 1.f / (float)rows, S.y, S.dy, S.partials, s, S.dz, c->dyn_alpha()));
     }
     {
       KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
@@ -645,7 +666,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
     {
       KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
       CK_CUDA(hdp::launch_head_out(f32, Hlast, B, (int)hp, hp, c->W(iwo), c->W(ibo), S.stage_t, 1, B, T, c->alpha,
-                                   1.f / (float)B, S.y, S.dy, S.partials, s));
+                                   1.f / (float)B, S.y, S.dy, S.partials, s, nullptr, c->dyn_alpha()));
     }
     {
       KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
@@ -655,12 +676,16 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
     {
       KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
       CK_CUDA(hdp::launch_head_out(f32, Htop, (int)rows, (int)hp, hp, c->W(iwo), c->W(ibo), S.stage_t, 0, B, T,
-                                   c->alpha, 1.f / (float)rows, S.y, S.dy, S.partials, s));
+                                   c->alpha, 1.f / (float)rows, S.y, S.dy, S.partials, s, nullptr, c->dyn_alpha()));
     }
     {
       KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
       CK_CUDA(hdp::launch_loss_final(S.partials, hdp::head_partials_count((int)rows), 1.f / (float)rows, S.loss, s));
     }
+  }
+  if (c->l2 > 0) {  // reported loss += l2 * ||w||^2 over the working weights
+    KScope ks_(c, HDP_K_HEAD_FWD, 2, s);
+    CK_CUDA(hdp::launch_l2_loss(f32, c->w, c->P, c->l2part, c->l2, S.loss, s));
   }
   return HDP_OK;
 }
@@ -898,6 +923,40 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
   } else
   for (int t = T - 1; t >= 0; --t) {
     const float* dHa_t = last_only ? (t == T - 1 ? dHa : nullptr) : dHa + (long)t * B * hp;
+    if (!f32) {
+      // mixed mode: K6 of step T-1 alone, then K7(t) with K6(t-1) fused into its split-K reduction
+      if (t == T - 1) {
+        KScope ks_(c, HDP_K_CELL_BWD, 1, s);
+        CK_CUDA(hdp::launch_cell_bwd(f32, dHa_t, nullptr, Gl + (long)t * B * 4 * hp * e, Cl + (long)t * B * hp,
+                                     t > 0 ? Cl + (long)(t - 1) * B * hp : nullptr, c->dc,
+                                     c->dA + (long)t * B * 4 * hp * e, B, (int)hp, 1, s));
+      }
+      if (t > 0) {
+        const int u = t - 1;
+        hdp::Epilogue eb;
+        eb.mode = hdp::EPI_LSTM_BWD;
+        eb.hp = (int)hp;
+        eb.dha = last_only ? nullptr : dHa + (long)u * B * hp;
+        eb.gates = const_cast<char*>(Gl) + (long)u * B * 4 * hp * e;
+        eb.ct = Cl + (long)u * B * hp;
+        eb.cprev = u > 0 ? Cl + (long)(u - 1) * B * hp : nullptr;
+        eb.dc = c->dc;
+        eb.dA = c->dA + (long)u * B * 4 * hp * e;
+        // K = 4 hp is long and M = B small: 256-wide tiles, split K over ~120 CTAs
+        int fbn = 0, fsp = 0;
+        if (hp >= 1024) {  // C4 sweep (tools/c4_gemm_sweep.py, HDP_K7_CFG): 256-wide tiles, ~128 CTAs
+          const int tiles = (int)(((B + 127) / 128) * ((hp + 255) / 256));
+          fbn = 256;
+          fsp = std::max(1, std::min(128 / tiles, (int)(4 * hp / 64 / 4)));
+          fsp = std::min(fsp, 16);
+        }
+        static const char* k7cfg = getenv("HDP_K7_CFG");  // tuning override "bn,splits"
+        if (k7cfg) sscanf(k7cfg, "%d,%d", &fbn, &fsp);
+        CK(gemm(c, HDP_K_GEMM_DH, c->dA + (long)t * B * 4 * hp * e, 4 * hp, 0, c->W(iU), hp, 1, B, hp, 4 * hp, eb, s,
+                fbn, fsp));
+      }
+      continue;
+    }
     // K6 (A6)
     {
       KScope ks_(c, HDP_K_CELL_BWD, 1, s);
@@ -1342,6 +1401,51 @@ double hdp_lr(const hdp_ctx* c, int epoch) {
   return sched(c, epoch);
 }
 
+int hdp_set_l2(hdp_ctx* c, double l2) {
+  if (!c) return fail(HDP_ERR_ARG, "null context");
+  if (!(l2 >= 0) || !std::isfinite(l2)) return fail(HDP_ERR_ARG, "l2 must be a finite number >= 0");
+  if (c->l2 != l2) {  // the loss term is part of captured forward graphs
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+  }
+  c->l2 = l2;
+  return HDP_OK;
+}
+
+int hdp_set_dynamic_loss_scale(hdp_ctx* c, int growth_interval) {
+  if (!c) return fail(HDP_ERR_ARG, "null context");
+  if (growth_interval < 0) return fail(HDP_ERR_ARG, "growth_interval must be >= 0");
+  if (!c->bound) return fail(HDP_ERR_STATE, "context not bound");
+  CK_CUDA(cudaSetDevice(c->device));
+  if ((c->dyn_interval > 0) != (growth_interval > 0)) {  // alpha source is baked into captured graphs
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+  }
+  if (growth_interval > 0) {
+    const int zero[3] = {0, 0, 0};
+    CK_CUDA(cudaMemcpy(c->dyn_state(), zero, sizeof zero, cudaMemcpyHostToDevice));
+    CK_CUDA(cudaMemcpy(c->alpha_dev(), &c->alpha, sizeof(float), cudaMemcpyHostToDevice));
+  }
+  c->dyn_interval = growth_interval;
+  return HDP_OK;
+}
+
+int hdp_loss_scale_state(hdp_ctx* c, float* alpha, int* skipped_steps) {
+  if (!c || !alpha || !skipped_steps) return fail(HDP_ERR_ARG, "null argument");
+  if (c->dyn_interval > 0) {
+    CK_CUDA(cudaSetDevice(c->device));
+    CK_CUDA(cudaDeviceSynchronize());
+    int st[3];
+    CK_CUDA(cudaMemcpy(st, c->dyn_state(), sizeof st, cudaMemcpyDeviceToHost));
+    CK_CUDA(cudaMemcpy(alpha, c->alpha_dev(), sizeof(float), cudaMemcpyDeviceToHost));
+    *skipped_steps = st[2];
+  } else {
+    *alpha = c->alpha;
+    *skipped_steps = 0;
+  }
+  return HDP_OK;
+}
+
 int hdp_set_loss_scale(hdp_ctx* c, float alpha) {
   if (!c) return fail(HDP_ERR_ARG, "null context");
   if (!(alpha > 0) || !std::isfinite(alpha)) return fail(HDP_ERR_ARG, "alpha must be a positive finite number");
@@ -1350,6 +1454,10 @@ int hdp_set_loss_scale(hdp_ctx* c, float alpha) {
     c->graphs.clear();
   }
   c->alpha = alpha;
+  if (c->dyn_interval > 0) {
+    CK_CUDA(cudaSetDevice(c->device));
+    CK_CUDA(cudaMemcpy(c->alpha_dev(), &alpha, sizeof(float), cudaMemcpyHostToDevice));
+  }
   return HDP_OK;
 }
 
@@ -1410,7 +1518,7 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
   if (c->count_pending) {
     CK_CUDA(cudaEventSynchronize(c->ev_count));
     c->count_pending = false;
-    if (*c->count_host > 0) {
+    if (*c->count_host > 0 && c->dyn_interval == 0) {
       c->poisoned = true;
       return fail(HDP_ERR_NONFINITE, "%d non-finite gradient values in the previous step (loss scale %g)",
                   *c->count_host, (double)c->alpha);
@@ -1435,12 +1543,32 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
     a.eps = (float)c->eps;
   }
   a.nonfinite = c->status;
+  a.l2x2 = (float)(2.0 * c->l2);
   cudaStream_t cs = c->world > 1 ? c->comm_stream : s;
   if (c->world > 1) {
     // the comm stream must see everything enqueued on `s` so far (incl. the
     // flat-model gradients written by the caller) before bucket 0
     CK_CUDA(cudaEventRecord(c->ev_done, s));
     CK_CUDA(cudaStreamWaitEvent(cs, c->ev_done, 0));
+  }
+  const bool dyn = c->dyn_interval > 0;
+  if (dyn) {
+    // NEXT-3 dynamic loss scaling: the step's global non-finite count (all ranks' fp16
+    // gradients) decides before any update whether the step is applied; alpha, kept on
+    // the device, then follows the scale rule (oracle/optim.py dynamic_loss_scale)
+    int* st = c->dyn_state();
+    CK_CUDA(cudaMemsetAsync(st, 0, sizeof(int), cs));
+    {
+      KScope ks_(c, HDP_K_UPDATE, 1, cs);
+      CK_CUDA(hdp::launch_count_nonfinite(c->grads, (long)c->nslots * c->P, c->gf32, st, cs));
+    }
+    if (c->world > 1) {
+      KScope ks_(c, HDP_K_COMM, 0, cs);
+      CK_NCCL(ncclAllReduce(st, st, 1, ncclInt32, ncclSum, c->comm, cs));
+    }
+    a.skip = st;
+    a.alpha_dev = c->alpha_dev();
+    a.n_workers = (double)N;
   }
   const int* count_src = c->status;
   if (c->p2p) {
@@ -1461,6 +1589,10 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
     p.c1 = a.c1;
     p.c2 = a.c2;
     p.eps = a.eps;
+    p.l2x2 = a.l2x2;
+    p.skip = a.skip;
+    p.alpha_dev = a.alpha_dev;
+    p.n_workers = a.n_workers;
     // the other status slot is next step's: zero it now (peers add to it only after my next "ready")
     CK_CUDA(cudaMemsetAsync(c->fwin + hdp::P2P_STATUS + ((step + 1) & 1), 0, sizeof(int), cs));
     {
@@ -1534,6 +1666,11 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
     }
 
   }
+  if (dyn) {
+    KScope ks_(c, HDP_K_UPDATE, 1, cs);
+    CK_CUDA(hdp::launch_loss_scale_update(c->dyn_state(), c->alpha_dev(), c->dyn_interval, 2.f, 1.f, cs));
+    count_src = c->dyn_state();
+  }
   CK_CUDA(cudaMemcpyAsync(c->count_host, count_src, sizeof(int), cudaMemcpyDeviceToHost, cs));
   CK_CUDA(cudaEventRecord(c->ev_count, cs));
   if (c->world > 1) {
@@ -1544,7 +1681,7 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
   if (nonfinite_host) {
     CK_CUDA(cudaEventSynchronize(c->ev_count));
     *nonfinite_host = *c->count_host;
-    if (*c->count_host > 0) {
+    if (*c->count_host > 0 && !dyn) {
       c->poisoned = true;
       return fail(HDP_ERR_NONFINITE, "%d non-finite gradient values (loss scale %g)", *c->count_host,
                   (double)c->alpha);
@@ -1608,7 +1745,7 @@ void* hdp_debug_buffer(hdp_ctx* c, int slot, const char* name) {
 
 int hdp_fused_avg_update(const void* grads, long long src_stride, int nsrc, int grads_f32, long long count, float* W,
                          float* S1, float* S2, void* w16, float* w32, float inv_scale, float lr, float momentum,
-                         int optimizer, const double* adam, int* nonfinite_dev, void* stream) {
+                         int optimizer, const double* adam, int* nonfinite_dev, float l2x2, void* stream) {
   if (!grads || !W || !S1 || nsrc < 1 || count < 0 || (optimizer == HDP_OPT_ADAM && (!S2 || !adam)) ||
       optimizer < 0 || optimizer > 1)
     return fail(HDP_ERR_ARG, "hdp_fused_avg_update: bad arguments");
@@ -1626,6 +1763,7 @@ int hdp_fused_avg_update(const void* grads, long long src_stride, int nsrc, int 
   a.lam = lr;
   a.mom = momentum;
   a.nonfinite = nonfinite_dev;
+  a.l2x2 = l2x2;
   if (optimizer == HDP_OPT_ADAM) {
     const double b1 = adam[0], b2 = adam[1], eps = adam[2], k = adam[3];
     a.b1 = (float)b1;

@@ -23,8 +23,25 @@ struct UpdateArgs {
   float inv_scale = 1.f, lam = 0.f, mom = 0.f;
   float b1 = 0.9f, omb1 = 0.1f, b2 = 0.999f, omb2 = 0.001f, c1 = 1.f, c2 = 1.f, eps = 1e-8f;
   int* nonfinite = nullptr;
+  // L2 (reading Q16): g += fp32(2*l2) * w_work after the descale, w_work =
+  // fp16(W) when a w16 copy is written (mixed mode, R1), else W
+  float l2x2 = 0.f;
+  // dynamic loss scaling (NEXT-3): alpha lives on the device; inv_scale is then
+  // fp32(1 / (n_workers * alpha)) computed in fp64 like the host does, and the whole
+  // update is skipped when *skip != 0 (the step's global non-finite count)
+  const float* alpha_dev = nullptr;
+  double n_workers = 1.0;
+  const int* skip = nullptr;
 };
 cudaError_t launch_avg_update(const UpdateArgs& a, int grad_is_f32, int optimizer, cudaStream_t s);
+// *count += number of Inf/NaN values in g[0..n) (fp16, or fp32 if g_f32)
+cudaError_t launch_count_nonfinite(const void* g, long n, int g_f32, int* count, cudaStream_t s);
+// dynamic loss-scale rule after the (possibly skipped) update, one thread:
+//   st[0] = global non-finite count of the step, st[1] = consecutive finite steps,
+//   st[2] = skipped steps (total);  alpha /= factor (>= min_alpha) on a non-finite step,
+//   alpha *= factor after `interval` finite steps
+cudaError_t launch_loss_scale_update(int* st, float* alpha, int interval, float factor, float min_alpha,
+                                     cudaStream_t s);
 
 // ---------------------------------------------------------------- input
 // x [B][T][I] (fp16 or fp32)  ->  X0 [T][B][Ip] (time-major, zero padded)
@@ -49,8 +66,12 @@ int head_partials_count(int rows);
 // dz (nullable): also writes dz = (Z > 0) * dy * wo (A5's ReLU', R9) for the FC head
 cudaError_t launch_head_out(int f32, const void* Z, int rows, int Kd, long ldz, const void* wo, const void* bo,
                             const int8_t* tgt, int tgt_mode, int B, int T, float alpha, float inv_terms, float* y,
-                            float* dy, float* partials, cudaStream_t s, void* dz = nullptr);
+                            float* dy, float* partials, cudaStream_t s, void* dz = nullptr,
+                            const float* alpha_dev = nullptr /* dynamic loss scale: alpha read on the device */);
 // loss = (sum of partials) * inv_terms   (unscaled mean hinge), deterministic
+// loss += l2 * sum(w[0..n)^2)  (deterministic; part: l2_partials_doubles() doubles)
+cudaError_t launch_l2_loss(int f32, const void* w, long n, double* part, double l2, float* loss, cudaStream_t s);
+size_t l2_partials_doubles();
 cudaError_t launch_loss_final(const float* partials, int n, float inv_terms, float* loss, cudaStream_t s);
 // dz[r][f] = (Z[r][f] > 0) ? dy[r]*wo[f] : 0   (ReLU', R9)
 cudaError_t launch_relu_dz(int f32, const float* dy, const void* wo, const void* Z, void* dz, int rows, int Fp,

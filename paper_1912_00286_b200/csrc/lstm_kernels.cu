@@ -133,8 +133,9 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32)
     head_out_kernel(const T* __restrict__ Z, int rows, int Kd, long ldz, const T* __restrict__ wo,
                     const T* __restrict__ bo, const int8_t* __restrict__ tgt, int tgt_mode, int B, int Tn,
                     float alpha, float inv_terms, float* __restrict__ y, float* __restrict__ dy,
-                    float* __restrict__ partials, T* __restrict__ dz) {
+                    float* __restrict__ partials, T* __restrict__ dz, const float* __restrict__ alpha_dev) {
   __shared__ float part[HEAD_WARPS];
+  if (alpha_dev) alpha = *alpha_dev;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int r = blockIdx.x * HEAD_WARPS + warp;
   float hinge = 0.f;
@@ -228,6 +229,33 @@ __global__ void loss_final_kernel(const float* __restrict__ partials, int n, flo
     __syncthreads();
   }
   if (threadIdx.x == 0) *loss = sm[0] * inv_terms;
+}
+
+// L2 penalty of the reported loss: loss += l2 * sum(w^2) over the
+// working weights; fixed grid + fp64 partials summed in block order (deterministic)
+constexpr int L2_BLOCKS = 296;
+template <typename T>
+__global__ void __launch_bounds__(256) sumsq_partial_kernel(const T* __restrict__ w, long n, double* part) {
+  __shared__ double sm[256];
+  double s = 0.0;
+  for (long i = blockIdx.x * 256L + threadIdx.x; i < n; i += (long)gridDim.x * 256) {
+    const double v = (double)ld<T>(w, i);
+    s += v * v;
+  }
+  sm[threadIdx.x] = s;
+  __syncthreads();
+  for (int k = 128; k > 0; k >>= 1) {
+    if (threadIdx.x < k) sm[threadIdx.x] += sm[threadIdx.x + k];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[blockIdx.x] = sm[0];
+}
+__global__ void l2_loss_final_kernel(const double* __restrict__ part, int n, double l2, float* loss) {
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < n; ++i) s += part[i];
+    *loss = (float)((double)*loss + l2 * s);
+  }
 }
 
 template <typename T>
@@ -486,16 +514,16 @@ int head_partials_count(int rows) { return (rows + HEAD_WARPS - 1) / HEAD_WARPS;
 
 cudaError_t launch_head_out(int f32, const void* Z, int rows, int Kd, long ldz, const void* wo, const void* bo,
                             const int8_t* tgt, int tgt_mode, int B, int T, float alpha, float inv_terms, float* y,
-                            float* dy, float* partials, cudaStream_t s, void* dz) {
+                            float* dy, float* partials, cudaStream_t s, void* dz, const float* alpha_dev) {
   const int g = head_partials_count(rows);
   if (f32)
     head_out_kernel<float><<<g, HEAD_WARPS * 32, 0, s>>>((const float*)Z, rows, Kd, ldz, (const float*)wo,
                                                         (const float*)bo, tgt, tgt_mode, B, T, alpha, inv_terms, y,
-                                                        dy, partials, (float*)dz);
+                                                        dy, partials, (float*)dz, alpha_dev);
   else
     head_out_kernel<__half><<<g, HEAD_WARPS * 32, 0, s>>>((const __half*)Z, rows, Kd, ldz, (const __half*)wo,
                                                          (const __half*)bo, tgt, tgt_mode, B, T, alpha, inv_terms,
-                                                         y, dy, partials, (__half*)dz);
+                                                         y, dy, partials, (__half*)dz, alpha_dev);
   return cudaGetLastError();
 }
 
@@ -503,6 +531,14 @@ cudaError_t launch_loss_final(const float* partials, int n, float inv_terms, flo
   loss_final_kernel<<<1, 256, 0, s>>>(partials, n, inv_terms, loss);
   return cudaGetLastError();
 }
+
+cudaError_t launch_l2_loss(int f32, const void* w, long n, double* part, double l2, float* loss, cudaStream_t s) {
+  if (f32) sumsq_partial_kernel<float><<<L2_BLOCKS, 256, 0, s>>>((const float*)w, n, part);
+  else sumsq_partial_kernel<__half><<<L2_BLOCKS, 256, 0, s>>>((const __half*)w, n, part);
+  l2_loss_final_kernel<<<1, 32, 0, s>>>(part, L2_BLOCKS, l2, loss);
+  return cudaGetLastError();
+}
+size_t l2_partials_doubles() { return L2_BLOCKS; }
 
 cudaError_t launch_relu_dz(int f32, const float* dy, const void* wo, const void* Z, void* dz, int rows, int Fp,
                            cudaStream_t s) {

@@ -71,9 +71,10 @@ __global__ void __launch_bounds__(256) exch_update_kernel(const __grid_constant_
     wait_all(a.flag_local + P2P_FLAG_READY, N, a.step);
   }
   __syncthreads();
-  // ---- B: owned 8-element vectors of every bucket
+  // ---- B: owned 8-element vectors of every bucket (none on a skipped step)
   int nf = 0;
-  const long total = a.vpre[a.nb];
+  const long total = (a.skip && *a.skip) ? 0 : a.vpre[a.nb];
+  const float inv_scale = a.alpha_dev ? (float)(1.0 / (a.n_workers * (double)*a.alpha_dev)) : a.inv_scale;
   for (long v = blockIdx.x * (long)blockDim.x + threadIdx.x; v < total; v += (long)gridDim.x * blockDim.x) {
     int bi = 0;
     while (v >= a.vpre[bi + 1]) ++bi;
@@ -92,10 +93,16 @@ __global__ void __launch_bounds__(256) exch_update_kernel(const __grid_constant_
     float4 H0 = *reinterpret_cast<const float4*>(a.S1 + m), H1 = *reinterpret_cast<const float4*>(a.S1 + m + 4);
     float w[8] = {W0.x, W0.y, W0.z, W0.w, W1.x, W1.y, W1.z, W1.w};
     float h[8] = {H0.x, H0.y, H0.z, H0.w, H1.x, H1.y, H1.z, H1.w};
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      s[i] = __fmul_rn(s[i], inv_scale);
+      // L2 (reading Q16): + fp32(2 l2) * fp16(W), the working weight of this step
+      if (a.l2x2 != 0.f) s[i] = __fadd_rn(s[i], __fmul_rn(a.l2x2, __half2float(__float2half_rn(w[i]))));
+    }
     if (OPT == 0) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float g = __fmul_rn(s[i], a.inv_scale);
+        const float g = s[i];
         h[i] = __fsub_rn(__fmul_rn(a.mom, h[i]), __fmul_rn(a.lam, g));
         w[i] = __fadd_rn(w[i], h[i]);
       }
@@ -104,7 +111,7 @@ __global__ void __launch_bounds__(256) exch_update_kernel(const __grid_constant_
       float vv[8] = {V0.x, V0.y, V0.z, V0.w, V1.x, V1.y, V1.z, V1.w};
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float g = __fmul_rn(s[i], a.inv_scale);
+        const float g = s[i];
         h[i] = __fadd_rn(__fmul_rn(a.b1, h[i]), __fmul_rn(a.omb1, g));
         vv[i] = __fadd_rn(__fmul_rn(a.b2, vv[i]), __fmul_rn(a.omb2, __fmul_rn(g, g)));
         const float den = __fadd_rn(__fsqrt_rn(__fmul_rn(vv[i], a.c2)), a.eps);

@@ -28,6 +28,10 @@ struct P2PArgs {
   float *W = nullptr, *S1 = nullptr, *S2 = nullptr;
   float inv_scale = 1.f, lam = 0.f, mom = 0.f;
   float b1 = 0.9f, omb1 = 0.1f, b2 = 0.999f, omb2 = 0.001f, c1 = 1.f, c2 = 1.f, eps = 1e-8f;
+  float l2x2 = 0.f;  // fp32(2 * l2), see UpdateArgs
+  const float* alpha_dev = nullptr;  // dynamic loss scaling, see UpdateArgs
+  double n_workers = 1.0;
+  const int* skip = nullptr;
 };
 
 cudaError_t launch_exch_update(const P2PArgs& a, int optimizer, int grid, cudaStream_t s);

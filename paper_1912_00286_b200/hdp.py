@@ -26,7 +26,8 @@ OPT_SGDM, OPT_ADAM = 0, 1
 EXPORTED = [
     "hdp_nccl_unique_id", "hdp_init", "hdp_destroy", "hdp_last_error", "hdp_configure", "hdp_bind",
     "hdp_num_blocks", "hdp_param_block", "hdp_load_params", "hdp_gather_master", "hdp_read_weights",
-    "hdp_read_grads", "hdp_set_lr_schedule", "hdp_lr", "hdp_set_loss_scale", "hdp_lstm_forward",
+    "hdp_read_grads", "hdp_set_lr_schedule", "hdp_lr", "hdp_set_loss_scale", "hdp_set_l2", "hdp_set_dynamic_loss_scale",
+    "hdp_loss_scale_state", "hdp_lstm_forward",
     "hdp_lstm_backward", "hdp_grad_average_update", "hdp_weights_ptr", "hdp_grads_ptr", "hdp_master_ptr",
     "hdp_fused_avg_update", "hdp_gemm_f16", "hdp_gemm_f32", "hdp_profile", "hdp_profile_read",
     "hdp_kernel_launches", "hdp_debug_buffer",
@@ -80,6 +81,9 @@ def _load():
         "hdp_set_lr_schedule": ([vp, d, d, d, d, d, d, d, d], i),
         "hdp_lr": ([vp, i], d),
         "hdp_set_loss_scale": ([vp, f], i),
+        "hdp_set_l2": ([vp, d], i),
+        "hdp_set_dynamic_loss_scale": ([vp, i], i),
+        "hdp_loss_scale_state": ([vp, C.POINTER(f), C.POINTER(i)], i),
         "hdp_lstm_forward": ([vp, vp, vp, i, i, i, vp, vp, vp], i),
         "hdp_lstm_backward": ([vp, i, vp], i),
         "hdp_grad_average_update": ([vp, i, vp, C.POINTER(i)], i),
@@ -87,7 +91,7 @@ def _load():
         "hdp_grads_ptr": ([vp, i], vp),
         "hdp_master_ptr": ([vp], vp),
         "hdp_debug_buffer": ([vp, i, C.c_char_p], vp),
-        "hdp_fused_avg_update": ([vp, ll, i, i, ll, vp, vp, vp, vp, vp, f, f, f, i, vp, vp, vp], i),
+        "hdp_fused_avg_update": ([vp, ll, i, i, ll, vp, vp, vp, vp, vp, f, f, f, i, vp, vp, f, vp], i),
         "hdp_gemm_f16": ([vp, ll, i, vp, ll, i, i, i, i, vp, ll, i, vp, i, i, i, vp, ll, i, i, vp], i),
         "hdp_gemm_f32": ([vp, ll, i, vp, ll, i, i, i, i, vp, ll, i, vp, i, i, i, vp], i),
         "hdp_profile": ([vp, i], i),
@@ -212,6 +216,21 @@ def set_loss_scale(ctx: int, alpha: float):
     _ck(_lib.hdp_set_loss_scale(ctx, alpha))
 
 
+def set_l2(ctx: int, l2: float):
+    _ck(_lib.hdp_set_l2(ctx, l2))
+
+
+def set_dynamic_loss_scale(ctx: int, growth_interval: int):
+    _ck(_lib.hdp_set_dynamic_loss_scale(ctx, growth_interval))
+
+
+def loss_scale_state(ctx: int):
+    """(alpha, skipped_steps) -- synchronises the device."""
+    a, k = C.c_float(), C.c_int()
+    _ck(_lib.hdp_loss_scale_state(ctx, C.byref(a), C.byref(k)))
+    return a.value, k.value
+
+
 def lstm_forward(ctx, x, targets, B, T, slot=0, y_out=None, loss_out=None, stream=None):
     _ck(_lib.hdp_lstm_forward(ctx, _ptr(x), _ptr(targets), B, T, slot, _ptr(y_out), _ptr(loss_out),
                               _stream(stream)))
@@ -252,14 +271,14 @@ def master_ptr(ctx) -> int:
 
 def fused_avg_update(grads, src_stride, nsrc, grads_f32, count, W, S1, S2=None, w16=None, w32=None,
                      inv_scale=1.0, lr=0.0, momentum=0.0, optimizer=OPT_SGDM, adam=None, nonfinite=None,
-                     stream=None):
+                     stream=None, l2x2=0.0):
     adam_arr = None
     if adam is not None:
         adam_arr = (C.c_double * 4)(*adam)
     _ck(_lib.hdp_fused_avg_update(_ptr(grads), src_stride, nsrc, int(grads_f32), count, _ptr(W), _ptr(S1),
                                   _ptr(S2), _ptr(w16), _ptr(w32), inv_scale, lr, momentum, optimizer,
                                   C.cast(adam_arr, C.c_void_p) if adam_arr is not None else None,
-                                  _ptr(nonfinite), _stream(stream)))
+                                  _ptr(nonfinite), l2x2, _stream(stream)))
 
 
 def gemm_f16(A, lda, a_mn, B, ldb, b_mn, M, N, K, Cout, ldc, c_mode=0, bias=None, bias_on_m=0, relu=0,
@@ -291,7 +310,7 @@ class Trainer:
 
     def __init__(self, desc: ModelDesc, params: Optional[np.ndarray], lambda0: float, alpha: float = 10.0,
                  gamma: float = 0.8, n_half: float = 100.0, momentum: float = 0.9, world: int = 1, rank: int = 0,
-                 uid: Optional[bytes] = None, device: int = 0, max_eff_lr: float = 0.1):
+                 uid: Optional[bytes] = None, device: int = 0, max_eff_lr: float = 0.1, l2: float = 0.0):
         import torch
         self.torch = torch
         self.ctx = init(world, rank, uid, device)
@@ -305,6 +324,8 @@ class Trainer:
         load_params(self.ctx, params, 0)
         set_lr_schedule(self.ctx, lambda0, gamma, n_half, max_eff_lr, momentum)
         set_loss_scale(self.ctx, alpha)
+        if l2:
+            set_l2(self.ctx, l2)
         self.loss = torch.zeros(max(1, desc.sim_workers), dtype=torch.float32, device=f"cuda:{device}")
 
     def step(self, xs, ts, B, T, epoch=0, stream=None, sync=False):

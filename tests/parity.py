@@ -35,7 +35,7 @@ def block_errors(cfg, got: np.ndarray, ref: np.ndarray, abs_terms: dict = None) 
 
 
 def run_parity(cfg, global_batch: int, n_workers: int, steps: int, mixed: bool, lambda0=None, alpha=None,
-               optimizer="sgdm", seed=synth.DATA_SEED, epochs=None, compare_grads=True):
+               optimizer="sgdm", seed=synth.DATA_SEED, epochs=None, compare_grads=True, l2=0.0):
     """Returns a list of per-step records with GPU-vs-oracle errors."""
     import torch
 
@@ -50,7 +50,7 @@ def run_parity(cfg, global_batch: int, n_workers: int, steps: int, mixed: bool, 
                                 sim_workers=n_workers)
     params = synth.init_params(cfg)
     tr = hdp.Trainer(desc, params, lambda0=lambda0, alpha=alpha, gamma=cfg.gamma, n_half=cfg.n_half,
-                     momentum=cfg.momentum)
+                     momentum=cfg.momentum, l2=l2)
     n = tr.n
     master = params.astype(np.float64)
     state = {"H": np.zeros(n)} if optimizer == "sgdm" else {"m1": np.zeros(n), "v": np.zeros(n)}
@@ -81,7 +81,7 @@ def run_parity(cfg, global_batch: int, n_workers: int, steps: int, mixed: bool, 
             lam = osched.rate_for_epoch(lambda0, n_workers, cfg.n_half, cfg.gamma, epoch, cfg.max_eff_lr)
             lam32 = float(np.float32(lam))
             ref = ostep.train_step(cfg, master, state, x, t, n_workers, alpha, lam32, mode, optimizer,
-                                   cfg.momentum, adam_k=k + 1)
+                                   cfg.momentum, adam_k=k + 1, l2=l2)
             rec = {
                 "step": k,
                 "loss_gpu": float(np.mean(gpu_losses)),

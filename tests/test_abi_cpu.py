@@ -51,8 +51,11 @@ def test_host_argument_errors(hdp):
     assert L.hdp_configure(None, None, None) == hdp.HDP_ERR_ARG
     assert L.hdp_lr(None, 0) < 0
     assert L.hdp_set_loss_scale(None, 1.0) == hdp.HDP_ERR_ARG
+    assert L.hdp_set_l2(None, 0.0) == hdp.HDP_ERR_ARG
+    assert L.hdp_set_dynamic_loss_scale(None, 100) == hdp.HDP_ERR_ARG
+    assert L.hdp_loss_scale_state(None, None, None) == hdp.HDP_ERR_ARG
     assert L.hdp_fused_avg_update(None, 0, 1, 0, 8, None, None, None, None, None, 1.0, 0.0, 0.0, 0, None, None,
-                                  None) == hdp.HDP_ERR_ARG
+                                  0.0, None) == hdp.HDP_ERR_ARG
     assert L.hdp_gemm_f16(None, 8, 0, None, 8, 0, 8, 8, 8, None, 8, 0, None, 0, 0, 0, None, 0, 0, 0,
                           None) == hdp.HDP_ERR_ARG
 

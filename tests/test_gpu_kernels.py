@@ -186,3 +186,40 @@ def test_k11_counts_nonfinite(hdp):
                          torch.zeros(count).cuda(), None, None, None, 0.05, 0.1, 0.9, hdp.OPT_SGDM, None, nf)
     torch.cuda.synchronize()
     assert nf.item() == 3 == ooptim.fused_avg_update_f32(list(g), W, W, 0.05, 0.1, 0.9)[3]
+
+
+@pytest.mark.parametrize("mixed", [True, False])
+@pytest.mark.parametrize("opt", ["sgdm", "adam"])
+def test_k11_l2_bit_exact(hdp, mixed, opt):
+    # NEXT-3 L2 term inside K11: g = s*inv + fp32(2 l2) * w_work, w_work = fp16(W) when a
+    # w16 copy is written (mixed, R1) else W -- bit-exact vs the float32 emulation
+    import synth
+    count, nsrc = 8192 + 8, 2
+    grads, W, H = synth.update_sweep_inputs(count, nsrc, seed=91)
+    W = (W * 20).astype(np.float32)    # weights large enough that the decay term matters
+    l2x2 = np.float32(2 * 0.01)
+    inv = np.float32(1.0 / (nsrc * 10.0))
+    g_dev = torch.from_numpy(np.concatenate(grads)).cuda()
+    W_dev = torch.from_numpy(W.copy()).cuda()
+    S1 = torch.from_numpy(H.copy()).cuda()
+    w16 = torch.zeros(count, dtype=torch.float16, device="cuda") if mixed else None
+    w32 = None if mixed else torch.zeros(count, dtype=torch.float32, device="cuda")
+    if opt == "sgdm":
+        _, lam32, m32 = ooptim.scalars_f32(nsrc, 10.0, 0.05, 0.9)
+        Wr, S1r, _, _ = ooptim.fused_avg_update_f32(grads, W, H, inv, lam32, m32, l2x2=l2x2, mixed=mixed)
+        hdp.fused_avg_update(g_dev, count, nsrc, False, count, W_dev, S1, None, w16, w32, float(inv), float(lam32),
+                             float(m32), hdp.OPT_SGDM, None, None, l2x2=float(l2x2))
+    else:
+        v = np.abs(np.random.default_rng(2).normal(0, 1e-4, count)).astype(np.float32)
+        c = ooptim.adam_consts_f32(1e-3, 3)
+        Wr, S1r, vr, _, _ = ooptim.fused_avg_adam_f32(grads, W, H, v, inv, c, l2x2=l2x2, mixed=mixed)
+        v_dev = torch.from_numpy(v.copy()).cuda()
+        hdp.fused_avg_update(g_dev, count, nsrc, False, count, W_dev, S1, v_dev, w16, w32, float(inv),
+                             float(c["lam"]), 0.0, hdp.OPT_ADAM, (0.9, 0.999, 1e-8, 3), None, l2x2=float(l2x2))
+    torch.cuda.synchronize()
+    assert np.array_equal(W_dev.cpu().numpy().view(np.uint32), Wr.view(np.uint32))
+    assert np.array_equal(S1.cpu().numpy().view(np.uint32), S1r.view(np.uint32))
+    # the L2 term changed the result (the check bites)
+    if opt == "sgdm":
+        W0, _, _, _ = ooptim.fused_avg_update_f32(grads, W, H, inv, lam32, m32)
+        assert not np.array_equal(W0, Wr)

@@ -65,6 +65,20 @@ def test_c1_mixed_stress_lr():
     assert _max(recs[-1]["dmaster_err"]) <= 5e-2, recs[-1]["dmaster_err"]
 
 
+@pytest.mark.parametrize("mixed", [False, True])
+def test_c1_l2_stress(mixed):
+    # NEXT-3 L2 (reading Q16): loss term l2*||w||^2 and gradient 2*l2*w fused
+    # into the average + update; large lambda and l2 so the decay dominates the update
+    cfg = synth.CONFIGS["C1"].with_(lambda0=0.05, n_half=1e9)
+    recs = run_parity(cfg, synth.C1_GLOBAL_BATCH, synth.C1_SIM_WORKERS, steps=5, mixed=mixed, l2=0.05)
+    tol = 2e-2 if mixed else 1e-5
+    for r in recs:
+        assert abs(r["loss_gpu"] - r["loss_ref"]) <= (1e-2 if mixed else 1e-5) * max(1.0, abs(r["loss_ref"])), r
+        assert _max(r["master_err"]) <= tol, r["master_err"]
+        assert r["w_matches_master"]
+    assert _max(recs[-1]["dmaster_err"]) <= (5e-2 if mixed else 1e-4), recs[-1]["dmaster_err"]
+
+
 def test_c1_adam_fp32():
     cfg = synth.CONFIGS["C1"]
     recs = run_parity(cfg, synth.C1_GLOBAL_BATCH, synth.C1_SIM_WORKERS, steps=3, mixed=False, optimizer="adam",
@@ -131,6 +145,19 @@ def test_c4_stacked_reduced_mixed():
     assert _max(r["master_err"]) <= 2e-2
 
 
+@pytest.mark.parametrize("batch,seq", [(256, 4), (136, 3)])
+def test_c4_full_width_batches_mixed(batch, seq):
+    # full per-rank batch (beta0 = 256, SURVEY.md §8(c) parity plan) and a ragged
+    # one: the per-step K2 / K7 GEMMs with the cell forward / backward fused into
+    # their epilogues run at their C4 tile shapes (K7 split-K over ~120 CTAs)
+    cfg = synth.CONFIGS["C4"].with_(seq=seq)
+    recs = run_parity(cfg, batch, 1, steps=1, mixed=True)
+    r = recs[0]
+    assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
+    assert _max(r["grad_err"][0]) <= 2e-2, r["grad_err"]
+    assert _max(r["master_err"]) <= 2e-2
+
+
 # ---------------------------------------------------------------- persistent recurrence path
 # B >= 16 and small h select the persistent fused recurrence kernel (one
 # cooperative launch per layer); these cases cover 1 CTA (h = 32), 8 CTAs
@@ -189,3 +216,52 @@ def test_c2_wavefront_matches_layerwise(monkeypatch, batch, fusex):
             assert _max(r["grad_err"][0]) <= 2e-2, (flag, r["grad_err"])
         assert _max(recs[-1]["master_err"]) <= 2e-2
     assert abs(out["1"][0]["loss_gpu"] - out["0"][0]["loss_gpu"]) <= 1e-4
+
+
+def test_c1_dynamic_loss_scale_skips_and_recovers():
+    # NEXT-3 dynamic loss scaling (reading Q14b): start from an alpha so large that the
+    # fp16 gradients overflow; every such step is skipped (master bit-identical) and
+    # alpha halves until the step fits, then doubles after `interval` finite steps.
+    # The GPU's skip decisions and alpha trajectory equal the oracle's rule on the
+    # oracle's own (rounding-emulating) gradients.
+    from paper_1912_00286_b200 import hdp
+    from oracle import optim as ooptim
+    from oracle import schedule as osched
+    from oracle import step as ostep
+    from parity import block_errors
+    cfg = synth.CONFIGS["C1"]
+    N, Bg = synth.C1_SIM_WORKERS, synth.C1_GLOBAL_BATCH
+    B = Bg // N
+    alpha0, interval, steps = 10.0 * 2.0 ** 16, 2, 10
+    params = synth.init_params(cfg)
+    desc = hdp.desc_from_config(cfg, B, hdp.MATH_MIXED16, sim_workers=N)
+    tr = hdp.Trainer(desc, params, lambda0=0.05, alpha=alpha0, gamma=cfg.gamma, n_half=1e9, momentum=cfg.momentum)
+    dev = torch.device("cuda:0")
+    master, state = params.astype(np.float64), {"H": np.zeros(tr.n)}
+    a_ref, good, skips_ref, skips_gpu = alpha0, 0, [], []
+    try:
+        hdp.set_dynamic_loss_scale(tr.ctx, interval)
+        for k in range(steps):
+            x, t = synth.model_batch(cfg, Bg, synth.DATA_SEED + k)
+            xs = [torch.from_numpy(np.ascontiguousarray(x[r * B:(r + 1) * B])).to(dev) for r in range(N)]
+            ts = [torch.from_numpy(np.ascontiguousarray(t[r * B:(r + 1) * B])).to(dev) for r in range(N)]
+            before = hdp.gather_master(tr.ctx, tr.n)
+            nf = tr.step(xs, ts, B, cfg.seq, epoch=0, stream=torch.cuda.current_stream(), sync=True)
+            after = hdp.gather_master(tr.ctx, tr.n)
+            skips_gpu.append(nf > 0)
+            if nf > 0:
+                assert np.array_equal(before, after)       # skipped: nothing changed
+            lam = float(np.float32(osched.rate_for_epoch(0.05, N, 1e9, cfg.gamma, 0)))
+            ref = ostep.train_step(cfg, master, state, x, t, N, a_ref, lam, "mixed", skip_nonfinite=True)
+            a_ref, good, sk = ooptim.dynamic_loss_scale(a_ref, good, ref["nonfinite"], interval)
+            skips_ref.append(sk)
+            master, state = ref["master"], ref["state"]
+        a_gpu, nskip = hdp.loss_scale_state(tr.ctx)
+        got = hdp.gather_master(tr.ctx, tr.n).astype(np.float64)
+    finally:
+        tr.close()
+    assert skips_gpu == skips_ref, (skips_gpu, skips_ref)
+    assert any(skips_ref) and not all(skips_ref)               # both branches exercised
+    assert nskip == sum(skips_ref)
+    assert a_gpu == np.float32(a_ref), (a_gpu, a_ref)
+    assert max(block_errors(cfg, got, master).values()) <= 2e-2

@@ -325,3 +325,48 @@ def test_mixed_step_invariants_c1():
     assert np.array_equal(out["w16"], r16(out["master"]))
     assert np.array_equal(out["master"], out["master"].astype(np.float32).astype(np.float64))
     assert 0.0 < out["loss"] < 10.0
+
+
+# ---------------------------------------------------------------- L2 regularisation (NEXT-3)
+
+def test_l2_gradient_matches_central_differences_of_reported_loss():
+    # PAPER.md:80 L2; SPEC.md:171 loss = alpha*mean hinge + alpha*l2*||W||^2 (reported
+    # unscaled): the gradient the update uses (avg) is d(loss)/dw of that loss
+    cfg = TINY["fc"].with_(batch=4)
+    l2, N, alpha = 3e-2, 2, 10.0
+    seed = 0
+    while True:
+        w = _params(cfg, 300 + seed, 0.5)
+        x, t = _inputs(cfg, 4, 400 + seed)
+        caches = [lstm.forward(cfg, lstm.unpack(cfg, w), x[r * 2:(r + 1) * 2], t[r * 2:(r + 1) * 2], alpha, "fp64")[2]
+                  for r in range(N)]
+        if not any(_near_kink(cfg, c) for c in caches):
+            break
+        seed += 1
+    out = step.train_step(cfg, w, {"H": np.zeros_like(w)}, x, t, N, alpha, 0.0, "fp64", l2=l2)
+    loss = lambda v: step.train_step(cfg, v, {"H": np.zeros_like(v)}, x, t, N, alpha, 0.0, "fp64", l2=l2)["loss"]
+    eps = 1e-5
+    fd = np.array([(loss(w + eps * e) - loss(w - eps * e)) / (2 * eps) for e in np.eye(w.size)])
+    floor = 1e-9 * max(1.0, abs(out["loss"]))
+    assert np.all(np.abs(out["avg"] - fd) <= 1e-6 * np.abs(out["avg"]) + floor)
+    # the penalty is really in there: without it the gradient differs by 2*l2*w
+    out0 = step.train_step(cfg, w, {"H": np.zeros_like(w)}, x, t, N, alpha, 0.0, "fp64")
+    assert np.allclose(out["avg"] - out0["avg"], 2 * l2 * w, rtol=1e-12, atol=1e-15)
+    assert out["loss"] - out0["loss"] == pytest.approx(l2 * np.dot(w, w), rel=1e-12)
+
+
+def test_l2_inactive_hinge_is_weight_decay_closed_form():
+    # all margins met -> data gradient 0, so Eqs. 1-2
+    # reduce to H1 = -lambda*2*l2*w, W1 = w*(1 - 2*lambda*l2)
+    cfg = TINY["lin"]
+    flat = _params(cfg, 3)
+    P = lstm.unpack(cfg, flat)
+    P["bo"][0] = 50.0
+    w = lstm.pack(cfg, P)
+    x, _ = _inputs(cfg, 4, 4)
+    t = np.ones((4, cfg.seq), np.int8)
+    lam, l2 = 0.1, 0.05
+    out = step.train_step(cfg, w, {"H": np.zeros_like(w)}, x, t, 2, 10.0, lam, "fp64", l2=l2)
+    assert np.array_equal(out["avg"], 2 * l2 * w)
+    assert np.allclose(out["state"]["H"], -lam * 2 * l2 * w, rtol=1e-7, atol=0)
+    assert np.allclose(out["master"], w * (1 - 2 * lam * l2), rtol=1e-7, atol=0)

@@ -120,3 +120,59 @@ def test_adam_f32_emulation_vs_fp64():
     Wr, m1r, vr = optim.adam(W.astype(np.float64), m1.astype(np.float64), v.astype(np.float64), avg, lam, k)
     assert np.max(np.abs(Wn - Wr)) <= 1e-6 * np.max(np.abs(Wr))
     assert np.max(np.abs(m1n - m1r)) <= 1e-6 * np.max(np.abs(m1r))
+
+
+def test_fused_f32_l2_term_vs_fp64():
+    # the L2 gradient 2*l2*w_work is added after the descale; w_work = fp16(W) in mixed
+    # mode (R1) -- float32 emulation within 1e-6 of the float64 update
+    rng = np.random.default_rng(5)
+    n, N, alpha, l2 = 4096, 2, 10.0, 1e-3
+    gs = [rng.normal(0, 0.05, n).astype(np.float16) for _ in range(N)]
+    W = rng.uniform(-0.5, 0.5, n).astype(np.float32)
+    H = np.zeros(n, np.float32)
+    inv, lam, m = optim.scalars_f32(N, alpha, 0.05, 0.9)
+    for mixed in (True, False):
+        Wn, Hn, _, _ = optim.fused_avg_update_f32(gs, W, H, inv, lam, m, l2x2=np.float32(2 * l2), mixed=mixed)
+        wk = W.astype(np.float16).astype(np.float64) if mixed else W.astype(np.float64)
+        g = optim.average([x.astype(np.float64) for x in gs], N, alpha) + 2 * l2 * wk
+        Hr = -0.05 * g
+        assert np.max(np.abs(Hn - Hr)) <= 1e-6 * np.max(np.abs(Hr))
+        assert np.max(np.abs(Wn - (W + Hr))) <= 1e-6
+    # l2x2 = 0 is the plain update, bit for bit
+    a = optim.fused_avg_update_f32(gs, W, H, inv, lam, m)
+    b = optim.fused_avg_update_f32(gs, W, H, inv, lam, m, l2x2=0.0)
+    assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
+
+
+def test_dynamic_loss_scale_closed_form_trajectory():
+    # halve on a non-finite step (and skip it), double after `interval` finite steps
+    seq = [1, 1, 0, 0, 0, 1, 0, 0, 0, 0]
+    a, g = 80.0, 0
+    alphas, skips = [], []
+    for nf in seq:
+        a, g, sk = optim.dynamic_loss_scale(a, g, nf, interval=3)
+        alphas.append(a)
+        skips.append(sk)
+    assert alphas == [40.0, 20.0, 20.0, 20.0, 40.0, 20.0, 20.0, 20.0, 40.0, 40.0]
+    assert skips == [bool(x) for x in seq]
+    # floor at min_alpha
+    assert optim.dynamic_loss_scale(1.5, 0, 5, 10)[0] == 1.0
+    # alpha * 2^k stays exact in fp32 (10 * 2^k)
+    assert np.float32(10.0 * 2 ** 20) / np.float32(2 ** 20) == np.float32(10.0)
+
+
+def test_skipped_step_leaves_state_unchanged():
+    import synth
+    from oracle import lstm, step
+    cfg = synth.ModelConfig("t", n_layers=1, input_dim=3, hidden=4, seq=4, batch=2)
+    rng = np.random.default_rng(0)
+    w = rng.uniform(-0.5, 0.5, lstm.count(cfg))
+    x = rng.standard_normal((2, 4, 3))
+    t = np.where(rng.random((2, 4)) < 0.5, 1, -1).astype(np.int8)
+    H = rng.normal(0, 1e-3, w.size)
+    # alpha so large that the fp16 gradients overflow (R12)
+    out = step.train_step(cfg, w, {"H": H}, x, t, 1, 1e12, 0.1, "mixed", skip_nonfinite=True)
+    assert out["nonfinite"] > 0
+    assert np.array_equal(out["master"], w) and np.array_equal(out["state"]["H"], H)
+    ok = step.train_step(cfg, w, {"H": H}, x, t, 1, 10.0, 0.1, "mixed", skip_nonfinite=True)
+    assert ok["nonfinite"] == 0 and not np.array_equal(ok["master"], w)
