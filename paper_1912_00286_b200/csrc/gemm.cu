@@ -32,7 +32,7 @@ struct TileCfg {
   static constexpr int A_BYTES = BM * BK * 2;
   static constexpr int B_BYTES = BN * BK * 2;
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 3 : (BN == 128 ? 4 : 6);
+  static constexpr int STAGES = BN == 256 ? 3 : (BN == 128 ? 5 : 7);  // as deep as the 227 KB allow
   static constexpr int EPI_LD = 36;  // staging row stride (floats): conflict-free float4 rows
   static constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quadrant, each half of the columns
   static constexpr int EPI_BYTES = EPI_WARPS * 32 * EPI_LD * 4;
