@@ -224,10 +224,17 @@ __device__ __forceinline__ void lstm_bwd_unit(const Epilogue& e, size_t idx, flo
 //   warps 2..9       : epilogue of tile i (TMEM -> registers -> smem -> coalesced
 //                      global stores) while the MMAs of tile i+1 run; warp w drains
 //                      TMEM lane quadrant w % 4, column half (w - 2) / 4
-template <int BN, int AMN, int BMN>
+//
+// CN > 1 (K-major A only): clusters of CN CTAs walk tile groups that share the M tile and
+// the K range (consecutive N tiles); every CTA TMA-loads 1/CN of the A rows and multicasts
+// them to the whole cluster, so A (the operand every N tile re-reads) leaves L2 once per
+// cluster.  A slot is refilled only after all CN CTAs' MMAs consumed it (each commit
+// arrives on every CTA's empty barrier).
+template <int BN, int AMN, int BMN, int CN = 1>
 __global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, int M, int N,
                    int K, int kbps, int splits, Epilogue epi, float* ws) {
+  static_assert(CN == 1 || AMN == 0, "A multicast needs K-major A");
   using C = TileCfg<BN>;
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -240,23 +247,28 @@ __global__ void __launch_bounds__(320, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN;
-  const int ntiles = mt * nt * splits;
+  const int ngr = (nt + CN - 1) / CN;               // N-tile groups (one per cluster pass)
+  const int ntiles = mt * ngr * splits;             // = tiles when CN == 1
   const int kb_total = (K + BK - 1) / BK;
+  const int crank = CN > 1 ? (int)(blockIdx.x % CN) : 0;
+  const int tile0 = CN > 1 ? (int)(blockIdx.x / CN) : (int)blockIdx.x;
+  const int tstep = CN > 1 ? (int)(gridDim.x / CN) : (int)gridDim.x;
   auto decode = [&](int tile, int& m0, int& n0, int& z, int& kb0, int& nkb) {
-    z = tile / (mt * nt);
-    const int r = tile % (mt * nt);
+    z = tile / (mt * ngr);
+    const int r = tile % (mt * ngr);
     m0 = (r % mt) * BM;  // consecutive CTAs share the B tile (n): better L2 reuse of the smaller operand
-    n0 = (r / mt) * BN;
+    n0 = ((r / mt) * CN + crank) * BN;
     kb0 = z * kbps;
     nkb = min(kb_total, kb0 + kbps) - kb0;
   };
+  constexpr uint16_t cmask = (uint16_t)((1u << CN) - 1u);
 
   if (threadIdx.x == 0) {
     ptx::tma_prefetch(&tma);
     ptx::tma_prefetch(&tmb);
     for (int s = 0; s < C::STAGES; ++s) {
       ptx::mbar_init(full + s, 1);
-      ptx::mbar_init(empty + s, 1);
+      ptx::mbar_init(empty + s, CN);
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(accf + b, 1);
@@ -266,7 +278,8 @@ __global__ void __launch_bounds__(320, 1)
   }
   if (warp == 1) ptx::tmem_alloc(tslot, 2 * BN);
   ptx::tc_fence_before();
-  __syncthreads();
+  if constexpr (CN > 1) ptx::cluster_sync_all();  // peers' barriers exist before any multicast
+  else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = *tslot;
   ptx::griddep_wait();  // (PDL) the setup above overlapped the previous kernel's tail
@@ -276,7 +289,7 @@ __global__ void __launch_bounds__(320, 1)
     if (lane == 0) {
       // ---------------- TMA producer
       int it = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+      for (int tile = tile0; tile < ntiles; tile += tstep) {
         int m0, n0, z, kb0, nkb;
         decode(tile, m0, n0, z, kb0, nkb);
         for (int i = 0; i < nkb; ++i, ++it) {
@@ -287,7 +300,9 @@ __global__ void __launch_bounds__(320, 1)
           uint8_t* sb = sa + C::A_BYTES;
           const int k0 = (kb0 + i) * BK;
           ptx::mbar_arrive_expect_tx(full + s, C::STAGE);
-          if (AMN == 0) {
+          if (CN > 1) {
+            ptx::tma_load_2d_mc(sa + crank * (BM / CN) * 128, &tma, full + s, k0, m0 + crank * (BM / CN), cmask);
+          } else if (AMN == 0) {
             ptx::tma_load_2d(sa, &tma, full + s, k0, m0);
           } else {
             ptx::tma_load_2d(sa, &tma, full + s, m0, k0);
@@ -301,13 +316,16 @@ __global__ void __launch_bounds__(320, 1)
           }
         }
       }
+      if (CN > 1)  // drain: every slot's last use consumed by all CN MMAs (their commits have
+        for (int i = 0; i < C::STAGES; ++i, ++it)  // landed here) before the cluster may exit
+          ptx::mbar_wait(empty + it % C::STAGES, ((it / C::STAGES) & 1) ^ 1);
     }
   } else if (warp == 1) {
     if (lane == 0) {
       // ---------------- MMA issuer
       constexpr uint32_t idesc = ptx::idesc_f16_f32(BM, BN, AMN, BMN);
       int it = 0, lt = 0;
-      for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+      for (int tile = tile0; tile < ntiles; tile += tstep, ++lt) {
         int m0, n0, z, kb0, nkb;
         decode(tile, m0, n0, z, kb0, nkb);
         const int b = lt & 1;
@@ -332,7 +350,8 @@ __global__ void __launch_bounds__(320, 1)
                                     : ptx::smem_desc_sw128(sb + k * 32, 0, 1024);
             ptx::mma_f16(tacc, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
           }
-          ptx::mma_commit(empty + s);  // frees the smem slot once these MMAs retire
+          if (CN > 1) ptx::mma_commit_mc(empty + s, cmask);  // every CTA's slot s was written by all
+          else ptx::mma_commit(empty + s);  // frees the smem slot once these MMAs retire
         }
         ptx::mma_commit(accf + b);     // accumulator b complete
       }
@@ -348,7 +367,7 @@ __global__ void __launch_bounds__(320, 1)
     __half* o16 = reinterpret_cast<__half*>(epi.out);
     const bool post = epi.mode != EPI_SPLITK;  // bias / relu belong to the reduction for split-K
     int nf = 0, lt = 0;
-    for (int tile = blockIdx.x; tile < ntiles; tile += gridDim.x, ++lt) {
+    for (int tile = tile0; tile < ntiles; tile += tstep, ++lt) {
       int m0, n0, z, kb0, nkb;
       decode(tile, m0, n0, z, kb0, nkb);
       const int b = lt & 1;
@@ -481,7 +500,9 @@ __global__ void __launch_bounds__(320, 1)
     }
   }
   ptx::tc_fence_before();
-  __syncthreads();
+  __syncwarp();
+  if constexpr (CN > 1) ptx::cluster_sync_all();
+  else __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
     ptx::tmem_dealloc(tbase, 2 * BN);
@@ -656,29 +677,40 @@ bool use_pdl() {
   return on;
 }
 
-template <int BN, int AMN, int BMN>
+template <int BN, int AMN, int BMN, int CN = 1>
 cudaError_t launch_tc(const GemmPlan& p, cudaStream_t s) {
   using C = TileCfg<BN>;
-  const int ntiles = ((p.M + BM - 1) / BM) * ((p.N + BN - 1) / BN) * p.splits;
+  const int groups = ((p.M + BM - 1) / BM) * ((((p.N + BN - 1) / BN) + CN - 1) / CN) * p.splits;
   Epilogue e = p.epi;
   if (p.splits > 1 || e.mode == EPI_LSTM_BWD) e.mode = EPI_SPLITK;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(std::min(ntiles, num_sms()));
+  cfg.gridDim = dim3(std::min(groups, num_sms() / CN) * CN);
   cfg.blockDim = dim3(320);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
-  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchAttribute at[2];
+  int na = 0;
+  if (CN > 1) {
+    at[na].id = cudaLaunchAttributeClusterDimension;
+    at[na].val.clusterDim.x = CN;
+    at[na].val.clusterDim.y = 1;
+    at[na].val.clusterDim.z = 1;
+    ++na;
+  }
+  if (use_pdl()) {
+    at[na].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[na].val.programmaticStreamSerializationAllowed = 1;
+    ++na;
+  }
   cfg.attrs = at;
-  cfg.numAttrs = use_pdl() ? 1 : 0;
-  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, AMN, BMN>, p.ta, p.tb, p.M, p.N, p.K, p.kbps, p.splits, e,
+  cfg.numAttrs = na;
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, AMN, BMN, CN>, p.ta, p.tb, p.M, p.N, p.K, p.kbps, p.splits, e,
                             p.ws);
 }
 
-template <int BN, int AMN, int BMN>
+template <int BN, int AMN, int BMN, int CN = 1>
 cudaError_t set_attr() {
-  return cudaFuncSetAttribute(gemm_tc_kernel<BN, AMN, BMN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(gemm_tc_kernel<BN, AMN, BMN, CN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               TileCfg<BN>::SMEM);
 }
 template <int BN>
@@ -687,11 +719,17 @@ cudaError_t set_attr_bn() {
   if ((e = set_attr<BN, 0, 0>()) != cudaSuccess) return e;
   if ((e = set_attr<BN, 0, 1>()) != cudaSuccess) return e;
   if ((e = set_attr<BN, 1, 0>()) != cudaSuccess) return e;
+  if ((e = set_attr<BN, 0, 0, 2>()) != cudaSuccess) return e;
+  if ((e = set_attr<BN, 0, 1, 2>()) != cudaSuccess) return e;
+  if ((e = set_attr<BN, 0, 0, 4>()) != cudaSuccess) return e;
+  if ((e = set_attr<BN, 0, 1, 4>()) != cudaSuccess) return e;
   return set_attr<BN, 1, 1>();
 }
 
 template <int BN>
 cudaError_t launch_tc_bn(const GemmPlan& p, cudaStream_t s) {
+  if (p.amn == 0 && p.cn == 2) return p.bmn ? launch_tc<BN, 0, 1, 2>(p, s) : launch_tc<BN, 0, 0, 2>(p, s);
+  if (p.amn == 0 && p.cn == 4) return p.bmn ? launch_tc<BN, 0, 1, 4>(p, s) : launch_tc<BN, 0, 0, 4>(p, s);
   if (p.amn == 0 && p.bmn == 0) return launch_tc<BN, 0, 0>(p, s);
   if (p.amn == 0 && p.bmn == 1) return launch_tc<BN, 0, 1>(p, s);
   if (p.amn == 1 && p.bmn == 0) return launch_tc<BN, 1, 0>(p, s);
@@ -785,9 +823,22 @@ int gemm_plan_tc(GemmPlan* p, const __half* A, long lda, int a_mn, const __half*
   }
   p->splits = splits;
   p->kbps = kbps;
+  // A multicast across a cluster of CN CTAs sharing the M tile (K-major A only), opt-in via
+  // HDP_GEMM_CN=2|4.  Measured on the C4 per-step shapes it does not pay (K2 256x8192x2048:
+  // 16.7 / 17.6 / 18.4 us at CN = 1 / 2 / 4): those GEMMs are bound by the chip's L2 -> SM
+  // operand throughput (~46 B/clk/SM, the same rate the 8192^3 GEMM streams at), which
+  // unicast already reaches -- L2 de-duplicates the concurrent reads of the shared A tile
+  int cn = 1;
+  {
+    const char* ev = getenv("HDP_GEMM_CN");
+    if (ev) cn = atoi(ev);
+    if (cn != 2 && cn != 4) cn = 1;
+    if (a_mn != 0) cn = 1;
+  }
+  p->cn = cn;
   int r;
   if (a_mn == 0)
-    r = make_tmap(&p->ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BM);
+    r = make_tmap(&p->ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BM / cn);
   else
     r = make_tmap(&p->ta, A, (uint64_t)M, (uint64_t)K, (uint64_t)lda, BK);
   if (r) return r;

@@ -62,6 +62,7 @@ struct GemmPlan {
   int M = 0, N = 0, K = 0;
   int bn = 128, amn = 0, bmn = 0;
   int splits = 1, kbps = 0;
+  int cn = 1;      // CTAs per cluster sharing (multicasting) the A tile
   Epilogue epi;
   float* ws = nullptr;
 };

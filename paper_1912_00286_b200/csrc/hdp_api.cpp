@@ -151,6 +151,7 @@ struct hdp_ctx {
   int32_t *keys_in = nullptr, *keys_out = nullptr, *vals_in = nullptr, *vals_out = nullptr;
   void* sort_temp = nullptr;
   float* emb_part = nullptr;
+  int32_t* emb_range = nullptr;  // [2][vocab]: first / last sorted position of each token
   size_t sort_bytes = 0;
   int* status = nullptr;  // [0] nonfinite count
   float* loadbuf = nullptr;
@@ -390,6 +391,7 @@ void carve(hdp_ctx* c, char* base) {
       c->sort_bytes = hdp::embed_sort_temp_bytes((int)rows);
       c->sort_temp = cv.take(c->sort_bytes);
       c->emb_part = (float*)cv.take(hdp::embed_part_floats((int)rows, (int)c->Ip0) * 4);
+      c->emb_range = (int32_t*)cv.take((size_t)2 * d.vocab * 4);
     }
   }
   c->arena_bytes = rup(cv.off, 256);
@@ -985,7 +987,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
       KScope ks_(c, HDP_K_EMBED_BWD, 2, s);
       CK_CUDA(hdp::launch_embed_backward((const int32_t*)S.stage_x, B, T, d.vocab, dHnext, (int)c->Ip0, c->keys_in,
                                          c->keys_out, c->vals_in, c->vals_out, c->sort_temp, c->sort_bytes,
-                                         c->emb_part, c->G(si, iE), gf, s));
+                                         c->emb_part, c->G(si, iE), gf, c->emb_range, s));
     }
   }
   return HDP_OK;

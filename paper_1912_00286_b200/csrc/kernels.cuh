@@ -95,7 +95,7 @@ size_t embed_part_floats(int n, int Ep);
 // dE[v][:] = sum over positions p (ascending, p = t*B+b) with tok = v of dX0[p][:]
 cudaError_t launch_embed_backward(const int32_t* tok, int B, int T, int vocab, const float* dX0, int Ep,
                                   int32_t* keys_in, int32_t* keys_out, int32_t* vals_in, int32_t* vals_out,
-                                  void* sort_temp, size_t sort_temp_bytes, float* part, void* dE, int out_f32,
+                                  void* sort_temp, size_t sort_temp_bytes, float* part, void* dE, int out_f32, int32_t* range /* 2*vocab ints */,
                                   cudaStream_t s);
 
 }  // namespace hdp

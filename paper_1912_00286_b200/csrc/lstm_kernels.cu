@@ -380,23 +380,27 @@ __global__ void embed_keys_kernel(const int32_t* __restrict__ tok, int B, int Tn
   vals[p] = p;
 }
 
-__device__ __forceinline__ int lower_bound_(const int32_t* a, int n, int v) {
-  int lo = 0, hi = n;
-  while (lo < hi) {
-    const int mid = (lo + hi) >> 1;
-    if (a[mid] < v) lo = mid + 1; else hi = mid;
-  }
-  return lo;
-}
-
 // Deterministic two-level segmented sum over the token-sorted positions:
 // (1) one warp per fixed chunk of EMB_CHUNK sorted positions sums each run of
 //     equal tokens inside its chunk (ascending position order) and stores the
-//     partial at the run's first index;
+//     partial at the run's first index; the chunk's keys / positions come in
+//     with one coalesced load and the dX rows of EMB_BATCH positions are
+//     loaded before they are accumulated (independent loads in flight);
 // (2) one warp per vocabulary row adds its partials (at its first index and
-//     at every chunk start inside its range) in index order.
+//     at every chunk start inside its range) in index order; the row's range
+//     [first, last) of sorted positions was recorded by embed_range_kernel.
 // No atomics; load-balanced for Zipf-frequent tokens.
 constexpr int EMB_CHUNK = 32;
+constexpr int EMB_BATCH = 8;
+
+__global__ void embed_range_kernel(const int32_t* __restrict__ keys, int n, int32_t* __restrict__ first,
+                                   int32_t* __restrict__ last) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int k = keys[i];
+  if (i == 0 || keys[i - 1] != k) first[k] = i;
+  if (i == n - 1 || keys[i + 1] != k) last[k] = i + 1;
+}
 
 __global__ void embed_chunk_kernel(const int32_t* __restrict__ keys, const int32_t* __restrict__ vals, int n,
                                    const float* __restrict__ dX0, int Ep, float* __restrict__ part) {
@@ -404,44 +408,57 @@ __global__ void embed_chunk_kernel(const int32_t* __restrict__ keys, const int32
   const int lane = threadIdx.x & 31;
   const long i0 = w * EMB_CHUNK;
   if (i0 >= n) return;
-  const long i1 = min((long)n, i0 + EMB_CHUNK);
+  const int cnt = (int)min((long)EMB_CHUNK, (long)n - i0);
+  const int my_key = lane < cnt ? keys[i0 + lane] : -1;
+  const int my_val = lane < cnt ? vals[i0 + lane] : 0;
   for (int k0 = 0; k0 < Ep; k0 += 128) {
     float acc[4] = {0.f, 0.f, 0.f, 0.f};
-    long start = i0;
-    int cur = keys[i0];
-    for (long i = i0; i < i1; ++i) {
-      const int key = keys[i];
-      if (key != cur) {
+    int start = 0;
+    int cur = __shfl_sync(0xffffffffu, my_key, 0);
+    for (int j0 = 0; j0 < cnt; j0 += EMB_BATCH) {
+      float rv[EMB_BATCH][4];
+#pragma unroll
+      for (int b = 0; b < EMB_BATCH; ++b) {
+        const int val = __shfl_sync(0xffffffffu, my_val, (j0 + b) & 31);
+        const float* row = dX0 + (long)val * Ep;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
           const int k = k0 + lane + 32 * q;
-          if (k < Ep) part[start * Ep + k] = acc[q];
-          acc[q] = 0.f;
+          rv[b][q] = (j0 + b < cnt && k < Ep) ? row[k] : 0.f;
         }
-        start = i;
-        cur = key;
       }
-      const float* row = dX0 + (long)vals[i] * Ep;
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int k = k0 + lane + 32 * q;
-        if (k < Ep) acc[q] += row[k];
+      for (int b = 0; b < EMB_BATCH; ++b) {
+        const int key = __shfl_sync(0xffffffffu, my_key, (j0 + b) & 31);
+        if (j0 + b >= cnt) break;
+        if (key != cur) {
+#pragma unroll
+          for (int q = 0; q < 4; ++q) {
+            const int k = k0 + lane + 32 * q;
+            if (k < Ep) part[(i0 + start) * Ep + k] = acc[q];
+            acc[q] = 0.f;
+          }
+          start = j0 + b;
+          cur = key;
+        }
+#pragma unroll
+        for (int q = 0; q < 4; ++q) acc[q] += rv[b][q];
       }
     }
 #pragma unroll
     for (int q = 0; q < 4; ++q) {
       const int k = k0 + lane + 32 * q;
-      if (k < Ep) part[start * Ep + k] = acc[q];
+      if (k < Ep) part[(i0 + start) * Ep + k] = acc[q];
     }
   }
 }
 
-__global__ void embed_segsum_kernel(const int32_t* __restrict__ keys, int n, int vocab,
+__global__ void embed_segsum_kernel(const int32_t* __restrict__ first, const int32_t* __restrict__ last, int vocab,
                                     const float* __restrict__ part, int Ep, int out_f32, void* dE) {
   const long v = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (v >= vocab) return;
-  const int lo = lower_bound_(keys, n, (int)v), hi = lower_bound_(keys, n, (int)v + 1);
+  const int lo = first[v], hi = last[v];  // [0, 0) for tokens that do not occur
   for (int k = lane; k < Ep; k += 32) {
     float s = 0.f;
     if (lo < hi) {
@@ -594,7 +611,7 @@ size_t embed_part_floats(int n, int Ep) { return (size_t)n * Ep; }
 cudaError_t launch_embed_backward(const int32_t* tok, int B, int T, int vocab, const float* dX0, int Ep,
                                   int32_t* keys_in, int32_t* keys_out, int32_t* vals_in, int32_t* vals_out,
                                   void* sort_temp, size_t sort_temp_bytes, float* part, void* dE, int out_f32,
-                                  cudaStream_t s) {
+                                  int32_t* range, cudaStream_t s) {
   const int n = B * T;
   embed_keys_kernel<<<(n + 255) / 256, 256, 0, s>>>(tok, B, T, keys_in, vals_in);
   int bits = 1;
@@ -602,10 +619,14 @@ cudaError_t launch_embed_backward(const int32_t* tok, int B, int T, int vocab, c
   size_t tb = sort_temp_bytes;
   cudaError_t e = cub::DeviceRadixSort::SortPairs(sort_temp, tb, keys_in, keys_out, vals_in, vals_out, n, 0, bits, s);
   if (e != cudaSuccess) return e;
+  e = cudaMemsetAsync(range, 0, (size_t)2 * vocab * sizeof(int32_t), s);
+  if (e != cudaSuccess) return e;
+  embed_range_kernel<<<(n + 255) / 256, 256, 0, s>>>(keys_out, n, range, range + vocab);
   const long cw = ((long)n + EMB_CHUNK - 1) / EMB_CHUNK * 32;
   embed_chunk_kernel<<<(int)((cw + 255) / 256), 256, 0, s>>>(keys_out, vals_out, n, dX0, Ep, part);
   const long threads = (long)vocab * 32;
-  embed_segsum_kernel<<<(int)((threads + 255) / 256), 256, 0, s>>>(keys_out, n, vocab, part, Ep, out_f32, dE);
+  embed_segsum_kernel<<<(int)((threads + 255) / 256), 256, 0, s>>>(range, range + vocab, vocab, part, Ep, out_f32,
+                                                                   dE);
   return cudaGetLastError();
 }
 
