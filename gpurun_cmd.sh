@@ -1,4 +1,2 @@
-timeout -s KILL 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/v10_gpu_tests.log 2>&1; echo exit=$? >> gpurun_out/v10_gpu_tests.log
-timeout -s KILL 300 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/v10_c3.json 2> gpurun_out/v10_c3.err
-timeout -s KILL 300 python bench.py --config C4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/v10_c4.json 2> gpurun_out/v10_c4.err
-timeout -s KILL 300 python bench.py --config C4 --steps 1 --warmup 3 --no-cpu-baseline > /dev/null 2>&1 && timeout -s KILL 900 ncu --set full --clock-control none --import-source on -k regex:gemm_tc_kernel -s 1100 -c 3 -o gpurun_out/v10_c4_k2 python bench.py --config C4 --steps 1 --warmup 3 --no-cpu-baseline > gpurun_out/v10_ncu.log 2>&1; echo ncu_exit=$? >> gpurun_out/v10_ncu.log
+timeout -s KILL 1200 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/v13_gpu_tests.log 2>&1; echo exit=$? >> gpurun_out/v13_gpu_tests.log
+timeout -s KILL 300 python bench.py --config C3 --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/v13_c3.json 2> gpurun_out/v13_c3.err

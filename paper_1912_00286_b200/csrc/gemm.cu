@@ -27,12 +27,13 @@ namespace {
 constexpr int BM = 128;
 constexpr int BK = 64;
 
-template <int BN>
+template <int BN, int CG = 1>
 struct TileCfg {
   static constexpr int A_BYTES = BM * BK * 2;
-  static constexpr int B_BYTES = BN * BK * 2;
+  static constexpr int B_BYTES = (BN / CG) * BK * 2;  // a CTA pair splits the B tile along N
   static constexpr int STAGE = A_BYTES + B_BYTES;
-  static constexpr int STAGES = BN == 256 ? 3 : (BN == 128 ? 5 : 7);  // as deep as the 227 KB allow
+  // as deep as the 227 KB allow
+  static constexpr int STAGES = STAGE >= 49152 ? 3 : (STAGE >= 32768 ? 5 : 7);
   static constexpr int EPI_LD = 36;  // staging row stride (floats): conflict-free float4 rows
   static constexpr int EPI_WARPS = 8;  // 2 per TMEM lane quadrant, each half of the columns
   static constexpr int EPI_BYTES = EPI_WARPS * 32 * EPI_LD * 4;
@@ -230,12 +231,21 @@ __device__ __forceinline__ void lstm_bwd_unit(const Epilogue& e, size_t idx, flo
 // them to the whole cluster, so A (the operand every N tile re-reads) leaves L2 once per
 // cluster.  A slot is refilled only after all CN CTAs' MMAs consumed it (each commit
 // arrives on every CTA's empty barrier).
-template <int BN, int AMN, int BMN, int CN = 1>
+//
+// CG = 2: CTA pairs (cta_group::2).  A pair owns a 256 x BN tile: each CTA loads its 128
+// A rows and half of the B tile, the leader (rank 0) issues M = 256 MMAs over both CTAs'
+// shared memory, and each CTA's TMEM receives its 128 rows -- per SM half the B bytes of
+// a 128 x BN tile for the same flops.  Both CTAs' TMA loads complete on the leader's
+// full barrier; the leader's commits arrive on both CTAs' empty / accumulator barriers;
+// both epilogues arrive on the leader's drain barrier.
+template <int BN, int AMN, int BMN, int CN = 1, int CG = 1>
 __global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, int M, int N,
                    int K, int kbps, int splits, Epilogue epi, float* ws) {
   static_assert(CN == 1 || AMN == 0, "A multicast needs K-major A");
-  using C = TileCfg<BN>;
+  static_assert(CG == 1 || (CN == 1 && AMN == 0), "CTA pairs: K-major A, no multicast");
+  using C = TileCfg<BN, CG>;
+  constexpr int CL = CN * CG;  // cluster size
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + C::STAGES * C::STAGE);
@@ -246,17 +256,18 @@ __global__ void __launch_bounds__(320, 1)
   float* epi_stage = reinterpret_cast<float*>(smem + C::STAGES * C::STAGE + 256);  // [8 warps][32][EPI_LD]
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int mt = (M + BM - 1) / BM, nt = (N + BN - 1) / BN;
+  const int mt = (M + BM * CG - 1) / (BM * CG), nt = (N + BN - 1) / BN;
   const int ngr = (nt + CN - 1) / CN;               // N-tile groups (one per cluster pass)
   const int ntiles = mt * ngr * splits;             // = tiles when CN == 1
   const int kb_total = (K + BK - 1) / BK;
   const int crank = CN > 1 ? (int)(blockIdx.x % CN) : 0;
-  const int tile0 = CN > 1 ? (int)(blockIdx.x / CN) : (int)blockIdx.x;
-  const int tstep = CN > 1 ? (int)(gridDim.x / CN) : (int)gridDim.x;
+  const int prank = CG > 1 ? (int)(blockIdx.x % CG) : 0;  // 0 = pair leader
+  const int tile0 = CL > 1 ? (int)(blockIdx.x / CL) : (int)blockIdx.x;
+  const int tstep = CL > 1 ? (int)(gridDim.x / CL) : (int)gridDim.x;
   auto decode = [&](int tile, int& m0, int& n0, int& z, int& kb0, int& nkb) {
     z = tile / (mt * ngr);
     const int r = tile % (mt * ngr);
-    m0 = (r % mt) * BM;  // consecutive CTAs share the B tile (n): better L2 reuse of the smaller operand
+    m0 = (r % mt) * BM * CG + prank * BM;  // this CTA's 128 rows of the (pair) tile
     n0 = ((r / mt) * CN + crank) * BN;
     kb0 = z * kbps;
     nkb = min(kb_total, kb0 + kbps) - kb0;
@@ -272,13 +283,16 @@ __global__ void __launch_bounds__(320, 1)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(accf + b, 1);
-      ptx::mbar_init(acce + b, C::EPI_WARPS);
+      ptx::mbar_init(acce + b, C::EPI_WARPS * CG);
     }
     ptx::fence_mbar_init();
   }
-  if (warp == 1) ptx::tmem_alloc(tslot, 2 * BN);
+  if (warp == 1) {
+    if constexpr (CG > 1) ptx::tmem_alloc2(tslot, 2 * BN);
+    else ptx::tmem_alloc(tslot, 2 * BN);
+  }
   ptx::tc_fence_before();
-  if constexpr (CN > 1) ptx::cluster_sync_all();  // peers' barriers exist before any multicast
+  if constexpr (CL > 1) ptx::cluster_sync_all();  // peers' barriers exist before any multicast
   else __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = *tslot;
@@ -299,6 +313,19 @@ __global__ void __launch_bounds__(320, 1)
           uint8_t* sa = smem + s * C::STAGE;
           uint8_t* sb = sa + C::A_BYTES;
           const int k0 = (kb0 + i) * BK;
+          if constexpr (CG > 1) {
+            // both CTAs' bytes complete on the leader's full barrier
+            if (prank == 0) ptx::mbar_arrive_expect_tx(full + s, 2 * C::STAGE);
+            ptx::tma_load_2d_cg2(sa, &tma, full + s, k0, m0);
+            if (BMN == 0) {
+              ptx::tma_load_2d_cg2(sb, &tmb, full + s, k0, n0 + prank * (BN / 2));
+            } else {
+#pragma unroll
+              for (int j = 0; j < BN / 128; ++j)
+                ptx::tma_load_2d_cg2(sb + j * 8192, &tmb, full + s, n0 + prank * (BN / 2) + 64 * j, k0);
+            }
+            continue;
+          }
           ptx::mbar_arrive_expect_tx(full + s, C::STAGE);
           if (CN > 1) {
             ptx::tma_load_2d_mc(sa + crank * (BM / CN) * 128, &tma, full + s, k0, m0 + crank * (BM / CN), cmask);
@@ -316,14 +343,15 @@ __global__ void __launch_bounds__(320, 1)
           }
         }
       }
-      if (CN > 1)  // drain: every slot's last use consumed by all CN MMAs (their commits have
+      if (CL > 1)  // drain: every slot's last use consumed by all the MMAs (their commits have
         for (int i = 0; i < C::STAGES; ++i, ++it)  // landed here) before the cluster may exit
           ptx::mbar_wait(empty + it % C::STAGES, ((it / C::STAGES) & 1) ^ 1);
     }
   } else if (warp == 1) {
-    if (lane == 0) {
-      // ---------------- MMA issuer
-      constexpr uint32_t idesc = ptx::idesc_f16_f32(BM, BN, AMN, BMN);
+    if (lane == 0 && prank == 0) {
+      // ---------------- MMA issuer (the pair leader for CG = 2)
+      constexpr uint32_t idesc = ptx::idesc_f16_f32(BM * CG, BN, AMN, BMN);
+      constexpr uint16_t pmask = 3;
       int it = 0, lt = 0;
       for (int tile = tile0; tile < ntiles; tile += tstep, ++lt) {
         int m0, n0, z, kb0, nkb;
@@ -348,12 +376,15 @@ __global__ void __launch_bounds__(320, 1)
                                     : ptx::smem_desc_sw128(sa + k * 32, 0, 1024);
             const uint64_t bd = BMN ? ptx::smem_desc_sw128(sb + k * 2048, 8192, 1024)
                                     : ptx::smem_desc_sw128(sb + k * 32, 0, 1024);
-            ptx::mma_f16(tacc, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+            if constexpr (CG > 1) ptx::mma_f16_cg2(tacc, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
+            else ptx::mma_f16(tacc, ad, bd, idesc, (i > 0 || k > 0) ? 1u : 0u);
           }
-          if (CN > 1) ptx::mma_commit_mc(empty + s, cmask);  // every CTA's slot s was written by all
+          if (CG > 1) ptx::mma_commit_cg2_mc(empty + s, pmask);      // both CTAs' slot s
+          else if (CN > 1) ptx::mma_commit_mc(empty + s, cmask);  // every CTA's slot s was written by all
           else ptx::mma_commit(empty + s);  // frees the smem slot once these MMAs retire
         }
-        ptx::mma_commit(accf + b);     // accumulator b complete
+        if (CG > 1) ptx::mma_commit_cg2_mc(accf + b, pmask);  // both CTAs' accumulators complete
+        else ptx::mma_commit(accf + b);     // accumulator b complete
       }
     }
   } else {
@@ -366,6 +397,11 @@ __global__ void __launch_bounds__(320, 1)
     const bool fast = !epi.accumulate && (epi.mode == EPI_F32 || epi.mode == EPI_SPLITK || f16);
     __half* o16 = reinterpret_cast<__half*>(epi.out);
     const bool post = epi.mode != EPI_SPLITK;  // bias / relu belong to the reduction for split-K
+    // accumulator b drained: the MMA issuer's (leader's) barrier
+    auto drained = [&](int b) {
+      if (CG > 1 && prank != 0) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(acce + b), 0));
+      else ptx::mbar_arrive(acce + b);
+    };
     int nf = 0, lt = 0;
     for (int tile = tile0; tile < ntiles; tile += tstep, ++lt) {
       int m0, n0, z, kb0, nkb;
@@ -402,7 +438,7 @@ __global__ void __launch_bounds__(320, 1)
           }
           ptx::tc_fence_before();
           __syncwarp();
-          if (lane == 0) ptx::mbar_arrive(acce + b);
+          if (lane == 0) drained(b);
           continue;
         }
       }
@@ -492,7 +528,7 @@ __global__ void __launch_bounds__(320, 1)
       }
       ptx::tc_fence_before();
       __syncwarp();
-      if (lane == 0) ptx::mbar_arrive(acce + b);
+      if (lane == 0) drained(b);
     }
     if (epi.mode == EPI_F16 && epi.nonfinite) {
       nf = __reduce_add_sync(0xffffffffu, nf);
@@ -501,11 +537,12 @@ __global__ void __launch_bounds__(320, 1)
   }
   ptx::tc_fence_before();
   __syncwarp();
-  if constexpr (CN > 1) ptx::cluster_sync_all();
+  if constexpr (CL > 1) ptx::cluster_sync_all();
   else __syncthreads();
   if (warp == 1) {
     ptx::tc_fence_after();
-    ptx::tmem_dealloc(tbase, 2 * BN);
+    if constexpr (CG > 1) ptx::tmem_dealloc2(tbase, 2 * BN);
+    else ptx::tmem_dealloc(tbase, 2 * BN);
   }
 }
 
@@ -677,22 +714,23 @@ bool use_pdl() {
   return on;
 }
 
-template <int BN, int AMN, int BMN, int CN = 1>
+template <int BN, int AMN, int BMN, int CN = 1, int CG = 1>
 cudaError_t launch_tc(const GemmPlan& p, cudaStream_t s) {
-  using C = TileCfg<BN>;
-  const int groups = ((p.M + BM - 1) / BM) * ((((p.N + BN - 1) / BN) + CN - 1) / CN) * p.splits;
+  using C = TileCfg<BN, CG>;
+  constexpr int CL = CN * CG;
+  const int groups = ((p.M + BM * CG - 1) / (BM * CG)) * ((((p.N + BN - 1) / BN) + CN - 1) / CN) * p.splits;
   Epilogue e = p.epi;
   if (p.splits > 1 || e.mode == EPI_LSTM_BWD) e.mode = EPI_SPLITK;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(std::min(groups, num_sms() / CN) * CN);
+  cfg.gridDim = dim3(std::min(groups, num_sms() / CL) * CL);
   cfg.blockDim = dim3(320);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
   cudaLaunchAttribute at[2];
   int na = 0;
-  if (CN > 1) {
+  if (CL > 1) {
     at[na].id = cudaLaunchAttributeClusterDimension;
-    at[na].val.clusterDim.x = CN;
+    at[na].val.clusterDim.x = CL;
     at[na].val.clusterDim.y = 1;
     at[na].val.clusterDim.z = 1;
     ++na;
@@ -704,14 +742,14 @@ cudaError_t launch_tc(const GemmPlan& p, cudaStream_t s) {
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, AMN, BMN, CN>, p.ta, p.tb, p.M, p.N, p.K, p.kbps, p.splits, e,
-                            p.ws);
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, AMN, BMN, CN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.kbps, p.splits,
+                            e, p.ws);
 }
 
-template <int BN, int AMN, int BMN, int CN = 1>
+template <int BN, int AMN, int BMN, int CN = 1, int CG = 1>
 cudaError_t set_attr() {
-  return cudaFuncSetAttribute(gemm_tc_kernel<BN, AMN, BMN, CN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              TileCfg<BN>::SMEM);
+  return cudaFuncSetAttribute(gemm_tc_kernel<BN, AMN, BMN, CN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              TileCfg<BN, CG>::SMEM);
 }
 template <int BN>
 cudaError_t set_attr_bn() {
@@ -723,11 +761,14 @@ cudaError_t set_attr_bn() {
   if ((e = set_attr<BN, 0, 1, 2>()) != cudaSuccess) return e;
   if ((e = set_attr<BN, 0, 0, 4>()) != cudaSuccess) return e;
   if ((e = set_attr<BN, 0, 1, 4>()) != cudaSuccess) return e;
+  if ((e = set_attr<BN, 0, 0, 1, 2>()) != cudaSuccess) return e;
+  if ((e = set_attr<BN, 0, 1, 1, 2>()) != cudaSuccess) return e;
   return set_attr<BN, 1, 1>();
 }
 
 template <int BN>
 cudaError_t launch_tc_bn(const GemmPlan& p, cudaStream_t s) {
+  if (p.amn == 0 && p.cg == 2) return p.bmn ? launch_tc<BN, 0, 1, 1, 2>(p, s) : launch_tc<BN, 0, 0, 1, 2>(p, s);
   if (p.amn == 0 && p.cn == 2) return p.bmn ? launch_tc<BN, 0, 1, 2>(p, s) : launch_tc<BN, 0, 0, 2>(p, s);
   if (p.amn == 0 && p.cn == 4) return p.bmn ? launch_tc<BN, 0, 1, 4>(p, s) : launch_tc<BN, 0, 0, 4>(p, s);
   if (p.amn == 0 && p.bmn == 0) return launch_tc<BN, 0, 0>(p, s);
@@ -762,7 +803,8 @@ size_t gemm_ws_floats(int M, int N, int K) {
 }
 
 int gemm_plan_tc(GemmPlan* p, const __half* A, long lda, int a_mn, const __half* B, long ldb, int b_mn, int M,
-                 int N, int K, const Epilogue& epi, float* ws, size_t ws_floats, int force_bn, int force_splits) {
+                 int N, int K, const Epilogue& epi, float* ws, size_t ws_floats, int force_bn, int force_splits,
+                 int force_cg) {
   *p = GemmPlan();
   p->tc = true;
   p->A = A;
@@ -836,6 +878,14 @@ int gemm_plan_tc(GemmPlan* p, const __half* A, long lda, int a_mn, const __half*
     if (a_mn != 0) cn = 1;
   }
   p->cn = cn;
+  // CTA pairs (cta_group::2, 256-row tiles): forced by the caller (force_cg) or HDP_GEMM_CG=2
+  int cg = force_cg;
+  {
+    const char* ev = getenv("HDP_GEMM_CG");
+    if (ev) cg = atoi(ev);
+    if (cg != 2 || a_mn != 0 || cn != 1 || bn < 128) cg = 1;
+  }
+  p->cg = cg;
   int r;
   if (a_mn == 0)
     r = make_tmap(&p->ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BM / cn);
@@ -843,7 +893,7 @@ int gemm_plan_tc(GemmPlan* p, const __half* A, long lda, int a_mn, const __half*
     r = make_tmap(&p->ta, A, (uint64_t)M, (uint64_t)K, (uint64_t)lda, BK);
   if (r) return r;
   if (b_mn == 0)
-    r = make_tmap(&p->tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, (uint32_t)bn);
+    r = make_tmap(&p->tb, B, (uint64_t)K, (uint64_t)N, (uint64_t)ldb, (uint32_t)(bn / cg));
   else
     r = make_tmap(&p->tb, B, (uint64_t)N, (uint64_t)K, (uint64_t)ldb, BK);
   return r;

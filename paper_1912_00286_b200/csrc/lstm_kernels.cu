@@ -453,23 +453,41 @@ __global__ void embed_chunk_kernel(const int32_t* __restrict__ keys, const int32
   }
 }
 
+// one warp per (vocabulary row, 32-column slice); a Zipf-frequent token spans ~200 chunk
+// partials: 16 independent chains, combined in a fixed order (deterministic)
 __global__ void embed_segsum_kernel(const int32_t* __restrict__ first, const int32_t* __restrict__ last, int vocab,
                                     const float* __restrict__ part, int Ep, int out_f32, void* dE) {
-  const long v = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  constexpr int CH = 16;
+  const long w = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (v >= vocab) return;
+  const int slices = (Ep + 31) >> 5;
+  const long v = w / slices;
+  const int k = (int)(w % slices) * 32 + lane;
+  if (v >= vocab || k >= Ep) return;
   const int lo = first[v], hi = last[v];  // [0, 0) for tokens that do not occur
-  for (int k = lane; k < Ep; k += 32) {
-    float s = 0.f;
-    if (lo < hi) {
-      s = part[(long)lo * Ep + k];
-      for (long c = ((long)lo / EMB_CHUNK + 1) * EMB_CHUNK; c < hi; c += EMB_CHUNK) s += part[c * Ep + k];
+  float s = 0.f;
+  if (lo < hi) {
+    float a[CH];
+#pragma unroll
+    for (int j = 0; j < CH; ++j) a[j] = 0.f;
+    long c = ((long)lo / EMB_CHUNK + 1) * EMB_CHUNK;
+    for (; c + (CH - 1) * EMB_CHUNK < hi; c += CH * EMB_CHUNK) {
+#pragma unroll
+      for (int j = 0; j < CH; ++j) a[j] += part[(c + j * EMB_CHUNK) * Ep + k];
     }
-    if (out_f32)
-      reinterpret_cast<float*>(dE)[v * Ep + k] = s;
-    else
-      reinterpret_cast<__half*>(dE)[v * Ep + k] = __float2half_rn(s);  // R12
+#pragma unroll
+    for (int j = 0; j < CH; ++j)
+      if (c + j * EMB_CHUNK < hi) a[j] += part[(c + j * EMB_CHUNK) * Ep + k];
+#pragma unroll
+    for (int m = CH / 2; m > 0; m >>= 1)
+#pragma unroll
+      for (int j = 0; j < m; ++j) a[j] += a[j + m];
+    s = part[(long)lo * Ep + k] + a[0];
   }
+  if (out_f32)
+    reinterpret_cast<float*>(dE)[v * Ep + k] = s;
+  else
+    reinterpret_cast<__half*>(dE)[v * Ep + k] = __float2half_rn(s);  // R12
 }
 
 inline int grid_for(long n, int threads, int cap = 148 * 16) {
@@ -624,7 +642,7 @@ cudaError_t launch_embed_backward(const int32_t* tok, int B, int T, int vocab, c
   embed_range_kernel<<<(n + 255) / 256, 256, 0, s>>>(keys_out, n, range, range + vocab);
   const long cw = ((long)n + EMB_CHUNK - 1) / EMB_CHUNK * 32;
   embed_chunk_kernel<<<(int)((cw + 255) / 256), 256, 0, s>>>(keys_out, vals_out, n, dX0, Ep, part);
-  const long threads = (long)vocab * 32;
+  const long threads = (long)vocab * ((Ep + 31) / 32) * 32;
   embed_segsum_kernel<<<(int)((threads + 255) / 256), 256, 0, s>>>(range, range + vocab, vocab, part, Ep, out_f32,
                                                                    dE);
   return cudaGetLastError();

@@ -32,16 +32,27 @@ def main():
     steps = int(os.environ.get("HDP_MP_STEPS", "3"))
     gb = int(os.environ.get("HDP_MP_GB", "8"))
     seq = int(os.environ.get("HDP_MP_SEQ", "0"))
+    l2 = float(os.environ.get("HDP_MP_L2", "0"))           # NEXT-3 L2 (reading Q16)
+    dyn = int(os.environ.get("HDP_MP_DYN", "0"))           # NEXT-3 dynamic loss scale interval (Q14b)
+    lam0 = float(os.environ.get("HDP_MP_LAMBDA0", "0"))
     cfg = synth.CONFIGS[cfg_name]
     if seq:
         cfg = cfg.with_(seq=seq)
+    if lam0:
+        cfg = cfg.with_(lambda0=lam0, n_half=1e9)
+    alpha = float(os.environ.get("HDP_MP_ALPHA", str(cfg.alpha)))
     B = gb // world
     obj = [hdp.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
     desc = hdp.desc_from_config(cfg, B, hdp.MATH_MIXED16 if mixed else hdp.MATH_FP32, wire, hdp.OPT_SGDM, 1)
     params = synth.init_params(cfg)
-    tr = hdp.Trainer(desc, params if rank == 0 else None, lambda0=cfg.lambda0, alpha=cfg.alpha, gamma=cfg.gamma,
-                     n_half=cfg.n_half, momentum=cfg.momentum, world=world, rank=rank, uid=obj[0], device=local)
+    tr = hdp.Trainer(desc, params if rank == 0 else None, lambda0=cfg.lambda0, alpha=alpha, gamma=cfg.gamma,
+                     n_half=cfg.n_half, momentum=cfg.momentum, world=world, rank=rank, uid=obj[0], device=local,
+                     l2=l2)
+    if dyn:
+        hdp.set_dynamic_loss_scale(tr.ctx, dyn)
+    a_ref, good = alpha, 0
+    from oracle import optim as ooptim
     n = tr.n
     dev = torch.device(f"cuda:{local}")
     stream = torch.cuda.current_stream(dev)
@@ -69,11 +80,18 @@ def main():
         dist.all_gather_object(hs, hashlib.sha256(w.tobytes()).hexdigest())
         if rank == 0:
             lam = float(np.float32(osched.rate_for_epoch(cfg.lambda0, world, cfg.n_half, cfg.gamma, 0)))
-            ref = ostep.train_step(cfg, master_ref, state, x, t, world, cfg.alpha, lam, "mixed" if mixed else "fp32")
+            ref = ostep.train_step(cfg, master_ref, state, x, t, world, a_ref, lam, "mixed" if mixed else "fp32",
+                                   l2=l2, skip_nonfinite=bool(dyn))
+            skip_ref = False
+            if dyn:
+                a_ref, good, skip_ref = ooptim.dynamic_loss_scale(a_ref, good, ref["nonfinite"], dyn)
             recs.append({"step": k, "loss_gpu": loss.item() / world, "loss_ref": ref["loss"], "nonfinite": nf,
+                         "skip_gpu": bool(dyn and nf > 0), "skip_ref": bool(skip_ref), "alpha_ref": a_ref,
                          "weights_identical": len(set(hs)) == 1,
                          "master_err": block_errors(cfg, master.astype(np.float64), ref["master"])})
             master_ref, state = ref["master"], ref["state"]
+    if dyn and rank == 0 and recs:
+        recs[-1]["alpha_gpu"] = hdp.loss_scale_state(tr.ctx)[0]
     tr.close()
     if rank == 0:
         print("MPRESULT " + json.dumps(recs), flush=True)

@@ -223,3 +223,22 @@ def test_k11_l2_bit_exact(hdp, mixed, opt):
     if opt == "sgdm":
         W0, _, _, _ = ooptim.fused_avg_update_f32(grads, W, H, inv, lam32, m32)
         assert not np.array_equal(W0, Wr)
+
+
+@pytest.mark.parametrize("cg,bn,bmn", [(2, 128, 0), (2, 256, 1)])
+def test_gemm_cta_pair_and_multicast_variants(hdp, monkeypatch, cg, bn, bmn):
+    # opt-in GEMM variants: CTA pairs (cta_group::2, 256-row tiles) and A
+    # multicast across 4-CTA clusters; ragged M and N, against an fp64 reference
+    for env, val in (("HDP_GEMM_CG", str(cg)), ("HDP_GEMM_CN", "4")):
+        monkeypatch.setenv(env, val)
+        M, N, K = 300, 1000, 320
+        A = (torch.randn(M, K, device="cuda") * 0.1).half()
+        B = (torch.randn(N, K, device="cuda") * 0.1).half()
+        Bs, ldb = (B.T.contiguous(), N) if bmn else (B, K)
+        C = torch.empty(M, N, device="cuda")
+        ws = torch.empty(16 * M * N, device="cuda")
+        hdp.gemm_f16(A, K, 0, Bs, ldb, bmn, M, N, K, C, N, 0, ws=ws, ws_floats=ws.numel(), bn=bn, splits=2)
+        torch.cuda.synchronize()
+        ref = A.double() @ B.double().T
+        assert (C.double() - ref).abs().max().item() <= 1e-5 * ref.abs().max().item(), env
+        monkeypatch.delenv(env)

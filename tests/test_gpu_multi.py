@@ -51,3 +51,19 @@ def test_c3_multi_gpu_parity_reduced():
     for r in recs:
         assert r["weights_identical"]
         assert max(r["master_err"].values()) <= 2e-2, r["master_err"]
+
+
+def test_c1_multi_gpu_l2_and_dynamic_loss_scale():
+    # NEXT-3 across real ranks: the L2 term inside the NVLink / NCCL update and the
+    # dynamic loss scale (all-reduced non-finite count -> the same skip on every rank)
+    world = _world()
+    recs = _run(world, {"HDP_MP_CFG": "C1", "HDP_MP_MIXED": "1", "HDP_MP_WIRE": "0", "HDP_MP_GB": str(2 * world),
+                        "HDP_MP_STEPS": "8", "HDP_MP_L2": "0.05", "HDP_MP_LAMBDA0": "0.05",
+                        "HDP_MP_DYN": "2", "HDP_MP_ALPHA": str(10.0 * 2 ** 16)})
+    for r in recs:
+        assert r["weights_identical"], r
+        assert r["skip_gpu"] == r["skip_ref"], r
+        assert max(r["master_err"].values()) <= 2e-2, r["master_err"]
+    assert any(r["skip_ref"] for r in recs) and not all(r["skip_ref"] for r in recs)
+    assert recs[-1]["alpha_gpu"] == recs[-1]["alpha_ref"]
+
