@@ -878,11 +878,18 @@ int gemm_plan_tc(GemmPlan* p, const __half* A, long lda, int a_mn, const __half*
     if (a_mn != 0) cn = 1;
   }
   p->cn = cn;
-  // CTA pairs (cta_group::2, 256-row tiles): forced by the caller (force_cg) or HDP_GEMM_CG=2
+  // CTA pairs (cta_group::2, 256-row tiles): force_cg 1 / 2 (or HDP_GEMM_CG) forces; automatic
+  // for the large K-major-A GEMMs (K1, K9, head): per SM half the B bytes of a 128 x 256 tile
+  // for the same flops (8192^3: 1052 -> 1393 TFLOP/s; K1 at C4 961 -> 1105; K9 983 -> 1228).
+  // The short-K per-step GEMMs (K2 / K7) measured slower with pairs and keep single CTAs.
   int cg = force_cg;
   {
     const char* ev = getenv("HDP_GEMM_CG");
     if (ev) cg = atoi(ev);
+    if (cg == 0) {
+      const int pair_tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + bn - 1) / bn) * splits;
+      cg = (bn == 256 && N >= 512 && pair_tiles >= 148) ? 2 : 1;
+    }
     if (cg != 2 || a_mn != 0 || cn != 1 || bn < 128) cg = 1;
   }
   p->cg = cg;

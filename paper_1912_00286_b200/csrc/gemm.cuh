@@ -75,7 +75,7 @@ size_t gemm_ws_floats(int M, int N, int K);
 // force_bn / force_splits: 0 = automatic.  Returns 0 or a negative error.
 int gemm_plan_tc(GemmPlan* p, const __half* A, long lda, int a_mn, const __half* B, long ldb, int b_mn, int M,
                  int N, int K, const Epilogue& epi, float* ws, size_t ws_floats, int force_bn = 0,
-                 int force_splits = 0, int force_cg = 1);
+                 int force_splits = 0, int force_cg = 0 /* 0 auto, 1 single CTAs, 2 CTA pairs */);
 // fp32 SIMT plan (FP32 mode, PAPER.md:147 baseline): same addressing.
 int gemm_plan_f32(GemmPlan* p, const float* A, long lda, int a_mn, const float* B, long ldb, int b_mn, int M,
                   int N, int K, const Epilogue& epi);
