@@ -23,6 +23,11 @@ import statistics
 import sys
 import time
 
+# the JSON line must be the only thing on stdout: NCCL's version banner (printed at
+# communicator init when NCCL_DEBUG asks for it) would precede it
+if os.environ.get("NCCL_DEBUG", "").upper() in ("", "VERSION", "INFO", "TRACE") and not os.environ.get("HDP_KEEP_NCCL_DEBUG"):
+    os.environ["NCCL_DEBUG"] = "WARN"
+
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
 
