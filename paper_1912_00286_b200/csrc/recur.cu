@@ -1605,6 +1605,15 @@ __global__ void __launch_bounds__(128, 1)
           if (ptx::elect_one_sync()) ptx::mma_commit(barM);
           __syncwarp();
         }
+        // Q0 publishes dA_{t+2} (for the weight-gradient role only, off the critical path)
+        // here, inside the MMA wait every warp sits in anyway: the store-group wait + the
+        // gpu-scope release cost ~0.7 us, which at the end of the step held the epilogue
+        // barrier of the hosting warp back (measured: warp 3 +0.7 us behind warps 0-2)
+        if (qi == 1 && threadIdx.x == st_thr && (qi == 0 || P.wtiles) && t + 2 <= T - 1) {
+          ptx::bulk_wait_group1();  // all but step t+1's store group complete
+          fence_proxy_async();
+          release_add(P.q0done + grp * 32, 1u);
+        }
       } else if (lane == 0) {
         ptx::mbar_wait(fullA + p, fphase[p]);  // every peer's dA_{t+1} slice landed in sA[p]
         ptx::tc_fence_after();
@@ -1733,7 +1742,8 @@ __global__ void __launch_bounds__(128, 1)
       if (threadIdx.x == 64 && publish) release_add((qi == 0 ? P.q1done : P.q0done) + grp * 32, 1u);
     } else if (threadIdx.x == st_thr) {
       unsigned* pubf = (qi == 0 ? P.q1done : P.q0done) + grp * 32;
-      if (publish && t < T - 2) {  // all but step t+1's store group complete -> publish step t+2
+      if (qi == 0 && publish && t < T - 2) {  // all but step t+1's store group complete -> publish step t+2
+                                              // (Q0: at the top of step t-1, see above)
         ptx::bulk_wait_group1();
         fence_proxy_async();
         release_add(pubf, 1u);
