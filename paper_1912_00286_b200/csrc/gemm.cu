@@ -243,7 +243,7 @@ __global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, int M, int N,
                    int K, int kbps, int splits, Epilogue epi, float* ws) {
   static_assert(CN == 1 || AMN == 0, "A multicast needs K-major A");
-  static_assert(CG == 1 || (CN == 1 && AMN == 0), "CTA pairs: K-major A, no multicast");
+  static_assert(CG == 1 || CN == 1, "CTA pairs: no multicast");
   using C = TileCfg<BN, CG>;
   constexpr int CL = CN * CG;  // cluster size
   extern __shared__ uint8_t smem_raw[];
@@ -316,7 +316,12 @@ __global__ void __launch_bounds__(320, 1)
           if constexpr (CG > 1) {
             // both CTAs' bytes complete on the leader's full barrier
             if (prank == 0) ptx::mbar_arrive_expect_tx(full + s, 2 * C::STAGE);
-            ptx::tma_load_2d_cg2(sa, &tma, full + s, k0, m0);
+            if (AMN == 0) {
+              ptx::tma_load_2d_cg2(sa, &tma, full + s, k0, m0);
+            } else {  // MN-major A: this CTA's 128 M columns as two 64-wide atoms
+              ptx::tma_load_2d_cg2(sa, &tma, full + s, m0, k0);
+              ptx::tma_load_2d_cg2(sa + 8192, &tma, full + s, m0 + 64, k0);
+            }
             if (BMN == 0) {
               ptx::tma_load_2d_cg2(sb, &tmb, full + s, k0, n0 + prank * (BN / 2));
             } else {
@@ -763,12 +768,15 @@ cudaError_t set_attr_bn() {
   if ((e = set_attr<BN, 0, 1, 4>()) != cudaSuccess) return e;
   if ((e = set_attr<BN, 0, 0, 1, 2>()) != cudaSuccess) return e;
   if ((e = set_attr<BN, 0, 1, 1, 2>()) != cudaSuccess) return e;
+  if ((e = set_attr<BN, 1, 0, 1, 2>()) != cudaSuccess) return e;
+  if ((e = set_attr<BN, 1, 1, 1, 2>()) != cudaSuccess) return e;
   return set_attr<BN, 1, 1>();
 }
 
 template <int BN>
 cudaError_t launch_tc_bn(const GemmPlan& p, cudaStream_t s) {
   if (p.amn == 0 && p.cg == 2) return p.bmn ? launch_tc<BN, 0, 1, 1, 2>(p, s) : launch_tc<BN, 0, 0, 1, 2>(p, s);
+  if (p.amn == 1 && p.cg == 2) return p.bmn ? launch_tc<BN, 1, 1, 1, 2>(p, s) : launch_tc<BN, 1, 0, 1, 2>(p, s);
   if (p.amn == 0 && p.cn == 2) return p.bmn ? launch_tc<BN, 0, 1, 2>(p, s) : launch_tc<BN, 0, 0, 2>(p, s);
   if (p.amn == 0 && p.cn == 4) return p.bmn ? launch_tc<BN, 0, 1, 4>(p, s) : launch_tc<BN, 0, 0, 4>(p, s);
   if (p.amn == 0 && p.bmn == 0) return launch_tc<BN, 0, 0>(p, s);
@@ -879,8 +887,8 @@ int gemm_plan_tc(GemmPlan* p, const __half* A, long lda, int a_mn, const __half*
   }
   p->cn = cn;
   // CTA pairs (cta_group::2, 256-row tiles): force_cg 1 / 2 (or HDP_GEMM_CG) forces; automatic
-  // for the large K-major-A GEMMs (K1, K9, head): per SM half the B bytes of a 128 x 256 tile
-  // for the same flops (8192^3: 1052 -> 1393 TFLOP/s; K1 at C4 961 -> 1105; K9 983 -> 1228).
+  // for the large GEMMs (K1, K8, K9): per SM half the B bytes of a 128 x 256 tile for the same
+  // flops (8192^3: 1052 -> 1393 TFLOP/s; K1 at C4 961 -> 1105; K9 983 -> 1228).
   // The short-K per-step GEMMs (K2 / K7) measured slower with pairs and keep single CTAs.
   int cg = force_cg;
   {
@@ -890,7 +898,7 @@ int gemm_plan_tc(GemmPlan* p, const __half* A, long lda, int a_mn, const __half*
       const int pair_tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + bn - 1) / bn) * splits;
       cg = (bn == 256 && N >= 512 && pair_tiles >= 148) ? 2 : 1;
     }
-    if (cg != 2 || a_mn != 0 || cn != 1 || bn < 128) cg = 1;
+    if (cg != 2 || cn != 1 || bn < 128) cg = 1;
   }
   p->cg = cg;
   int r;
