@@ -93,8 +93,12 @@ def _q16(mode):
 # forward
 # ----------------------------------------------------------------------------
 
-def forward(cfg, P: Dict[str, np.ndarray], x, targets, alpha: float, mode: str):
+def forward(cfg, P: Dict[str, np.ndarray], x, targets, alpha: float, mode: str, drop=None):
     """fprop + scaled loss for one worker's mini-batch.
+
+    drop (optional, NEXT-3 recurrent dropout, oracle/dropout.py): {"masks": [per layer
+    {0,1} [B][h]], "scale": fp32(1/keep)}; layer l's recurrent GEMM then reads
+    h~_{t-1} = r16(h_{t-1} * scale) on kept units, 0 elsewhere (R6d).
 
     x: float [B][T][I] (fp16-representable, R0) or int tokens [B][T] (C3).
     targets: {-1,+1} [B][T] (per-step heads) or [B] (last-step head).
@@ -121,8 +125,11 @@ def forward(cfg, P: Dict[str, np.ndarray], x, targets, alpha: float, mode: str):
         gates = np.zeros((T, B, 4 * h))
         C = np.zeros((T, B, h))
         H = np.zeros((T, B, h))
+        Hin = np.zeros((T, B, h))                # recurrent input of each step (h~_{t-1})
         for t in range(T):
-            a = Xin[t] @ W.T + h_prev @ U.T + b
+            h_in = h_prev if drop is None else q(h_prev * drop["scale"]) * drop["masks"][l]
+            Hin[t] = h_in
+            a = Xin[t] @ W.T + h_in @ U.T + b
             i = _sigmoid(a[:, 0:h])
             f = _sigmoid(a[:, h:2 * h])
             g = np.tanh(a[:, 2 * h:3 * h])
@@ -135,7 +142,8 @@ def forward(cfg, P: Dict[str, np.ndarray], x, targets, alpha: float, mode: str):
             C[t] = c
             H[t] = hh
             h_prev, c_prev = hh, c
-        layers.append({"X": Xin, "gates": gates, "C": C, "H": H})
+        layers.append({"X": Xin, "gates": gates, "C": C, "H": H, "Hin": Hin,
+                       "rmask": None if drop is None else drop["masks"][l] * drop["scale"]})
         Xin = H
     Htop = Xin
     cache = {"layers": layers, "B": B, "tokens": np.asarray(x) if cfg.vocab > 0 else None}
@@ -222,8 +230,10 @@ def backward(cfg, P: Dict[str, np.ndarray], cache, alpha: float, mode: str,
             dA = q(dA)                           # R10
             dA_all[t] = dA
             dh_rec = dA @ U                      # R11
+            if Lc["rmask"] is not None:          # gradient of h~_{t-1} -> h_{t-1}
+                dh_rec = dh_rec * Lc["rmask"]
             dc = dc * f
-        Hprev = np.concatenate([np.zeros((1, B, h)), H[:-1]], axis=0)
+        Hprev = Lc["Hin"]                        # h~_{t-1} (= h_{t-1} without dropout; zeros at t = 0)
         # sums over (t, b) written as one matrix product each
         dA2 = dA_all.reshape(-1, 4 * h)
         G[f"W{l}"] = dA2.T @ X.reshape(-1, X.shape[-1])

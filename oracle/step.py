@@ -24,6 +24,7 @@ from typing import Dict, Optional
 
 import numpy as np
 
+from . import dropout as dropout_mod
 from . import lstm, optim
 from .binary16 import count_nonfinite, r16
 
@@ -33,10 +34,10 @@ def working_weights(master: np.ndarray, mode: str) -> np.ndarray:
     return r16(master) if mode == "mixed" else np.asarray(master, np.float64)
 
 
-def worker_grads(cfg, wflat, x, targets, alpha, mode, abs_terms=None):
+def worker_grads(cfg, wflat, x, targets, alpha, mode, abs_terms=None, drop=None):
     """Steps 3 for one worker: returns (L_r scaled, flat gradient, y)."""
     P = lstm.unpack(cfg, wflat)
-    L, y, cache = lstm.forward(cfg, P, x, targets, alpha, mode)
+    L, y, cache = lstm.forward(cfg, P, x, targets, alpha, mode, drop)
     G = lstm.backward(cfg, P, cache, alpha, mode, abs_terms)
     return L, lstm.pack(cfg, G), y
 
@@ -44,7 +45,8 @@ def worker_grads(cfg, wflat, x, targets, alpha, mode, abs_terms=None):
 def train_step(cfg, master, state: Dict[str, np.ndarray], x_global, t_global, N: int,
                alpha: float, lam: float, mode: str, optimizer: str = "sgdm",
                momentum: float = 0.9, adam_k: int = 1,
-               grads_override: Optional[list] = None, l2: float = 0.0, skip_nonfinite: bool = False):
+               grads_override: Optional[list] = None, l2: float = 0.0, skip_nonfinite: bool = False,
+               dropout: Optional[dict] = None):
     """Returns a dict with loss (unscaled mean over workers), per-worker
     gradients (carrying alpha), the averaged gradient, new master/state,
     the fp16 working copy and the non-finite count."""
@@ -56,7 +58,14 @@ def train_step(cfg, master, state: Dict[str, np.ndarray], x_global, t_global, N:
     for r in range(N):
         sl = slice(r * b, (r + 1) * b)
         at = {}
-        L, g, _ = worker_grads(cfg, w, x_global[sl], t_global[sl], alpha, mode, at)
+        drop = None
+        if dropout is not None and dropout["keep"] < 1.0:
+            # recurrent dropout (oracle/dropout.py): masks keyed by the global sequence index
+            seqs = np.arange(r * b, (r + 1) * b)
+            drop = {"scale": dropout_mod.scale(dropout["keep"]),
+                    "masks": [dropout_mod.mask(dropout["seed"], dropout["step"], l, seqs, cfg.hidden, dropout["keep"])
+                              for l in range(cfg.n_layers)]}
+        L, g, _ = worker_grads(cfg, w, x_global[sl], t_global[sl], alpha, mode, at, drop)
         losses.append(L)
         grads.append(g)
         abs_terms.append(at)
