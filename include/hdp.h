@@ -162,6 +162,23 @@ int hdp_set_loss_scale(hdp_ctx* ctx, float alpha);
  * Default 0 (off).  Errors: l2 < 0 or not finite -> HDP_ERR_ARG, nothing
  * changed.  Changing it drops the captured forward graphs.               */
 int hdp_set_l2(hdp_ctx* ctx, double l2);
+/* Variational recurrent dropout (NEXT-3; "recurrent dropout";
+ * DESIGN.md reading Q16b; oracle/dropout.py).  keep in (0, 1]; keep = 1 turns
+ * it off (the default).  One Bernoulli(keep) mask per (update count, layer,
+ * sequence, unit), fixed over the time steps: the recurrent GEMM of layer l
+ * reads h~_{t-1} = fp16(fp32(h_{t-1}) * fp32(1/keep)) on kept units and 0
+ * elsewhere; the next layer and the head see the unmasked h; BPTT multiplies
+ * the recurrent gradient by the same mask and scale and dU accumulates
+ * dA_t^T h~_{t-1}.  The mask is the counter-based hash of dropout.cuh keyed by
+ * `seed`, the number of completed hdp_grad_average_update calls since this
+ * call, the layer, the sequence's global index ((rank * slots + slot) * B + b)
+ * and the unit.  Mixed mode only; the per-step GEMM path runs (the fused
+ * recurrence kernels have no dropout).  The library allocates (cudaMalloc)
+ * the masked-input buffers, slots * L * (T+1) * B * h_p fp16, freed by
+ * hdp_destroy.  Synchronises the device; drops the captured graphs.
+ * Errors: keep outside (0, 1] -> HDP_ERR_ARG; FP32 mode -> HDP_ERR_UNSUPPORTED;
+ * unbound -> HDP_ERR_STATE.                                                 */
+int hdp_set_recurrent_dropout(hdp_ctx* ctx, double keep, unsigned int seed);
 /* Dynamic loss scaling (NEXT-3; PAPER.md:134 names fp16 overflow as the hazard
  * of the static alpha of :177; reading Q14b).  growth_interval > 0
  * switches it on (0 = static alpha, the default): alpha moves to the device,

@@ -14,6 +14,7 @@
 #include <cstdio>
 #include <mutex>
 
+#include "dropout.cuh"
 #include "gemm.cuh"
 #include "ptx.cuh"
 
@@ -129,6 +130,19 @@ __device__ __forceinline__ float lstm_tanh(float x) {
   return fmaf(2.f, lstm_sigmoid(2.f * xc), -1.f);
 }
 
+// recurrent dropout: the masked copy h~ of 8 units of row m (R6d: fp16 of fp32(h) * scale)
+__device__ __forceinline__ void lstm_drop_store(const Epilogue& e, int m, int u0, const __half (&hh)[8]) {
+  const uint32_t sk = drop_seq_key(drop_layer_key(e.drop_seed, (uint32_t)*e.drop_step, e.drop_layer),
+                                   e.drop_seq0 + (uint32_t)m);
+  __align__(16) __half ht[8];
+#pragma unroll
+  for (int j = 0; j < 8; ++j)
+    ht[j] = drop_kept(sk, (uint32_t)(u0 + j), e.drop_thr) ? __float2half_rn(__half2float(hh[j]) * e.drop_scale)
+                                                          : __float2half_rn(0.f);
+  *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(e.htout) + (size_t)m * e.hp + u0) =
+      *reinterpret_cast<const uint4*>(ht);
+}
+
 // A3 for 8 units of row m: columns [n, n+32) of the gate pre-activation (n = 4 u0).
 __device__ __forceinline__ void lstm_fwd_chunk(const Epilogue& e, int m, int n, const float (&v)[32]) {
   const int u0 = n >> 2;
@@ -166,6 +180,7 @@ __device__ __forceinline__ void lstm_fwd_chunk(const Epilogue& e, int m, int n, 
   co[1] = make_float4(cn[4], cn[5], cn[6], cn[7]);
   *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(e.hout) + (size_t)m * e.hp + u0) =
       *reinterpret_cast<const uint4*>(hh);
+  if (e.drop_step) lstm_drop_store(e, m, u0, hh);
 }
 
 // Same, with G_x and c_{t-1} already in registers.
@@ -196,12 +211,19 @@ __device__ __forceinline__ void lstm_fwd_chunk_reg(const Epilogue& e, int m, int
   co[1] = make_float4(cn[4], cn[5], cn[6], cn[7]);
   *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(e.hout) + (size_t)m * e.hp + u0) =
       *reinterpret_cast<const uint4*>(hh);
+  if (e.drop_step) lstm_drop_store(e, m, u0, hh);
 }
 
 // A6 for unit idx = m * hp + u given dh_rec (the reduced K7 result).
 __device__ __forceinline__ void lstm_bwd_unit(const Epilogue& e, size_t idx, float dh_rec) {
   float dh = 0.f;
   if (e.dha) dh += e.dha[idx];
+  if (e.drop_step) {  // dh_rec is the gradient of h~_{t-1}: back through the mask and scale
+    const uint32_t mrow = (uint32_t)(idx / e.hp), u = (uint32_t)(idx % e.hp);
+    const uint32_t sk = drop_seq_key(drop_layer_key(e.drop_seed, (uint32_t)*e.drop_step, e.drop_layer),
+                                     e.drop_seq0 + mrow);
+    dh_rec = drop_kept(sk, u, e.drop_thr) ? dh_rec * e.drop_scale : 0.f;
+  }
   dh += dh_rec;
   const uint2 gu = reinterpret_cast<const uint2*>(e.gates)[idx];
   const float2 g01 = __half22float2(*reinterpret_cast<const __half2*>(&gu.x));

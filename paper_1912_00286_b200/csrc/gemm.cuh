@@ -51,6 +51,13 @@ struct Epilogue {
   const float* ct = nullptr;    // BWD: c_{t-1}
   float* dc = nullptr;          // BWD: cell-gradient carry (in/out)
   void* dA = nullptr;           // BWD: dA_{t-1} (fp16)
+  // recurrent dropout (NEXT-3, dropout.cuh): active iff drop_step != nullptr.  FWD also
+  // writes h~_t = fp16(fp32(h_t) * drop_scale) on kept units (0 elsewhere) to htout; BWD
+  // multiplies dh_rec by the same mask * drop_scale.  Row m is sequence drop_seq0 + m.
+  void* htout = nullptr;
+  const int* drop_step = nullptr;  // device counter of completed updates
+  uint32_t drop_seed = 0, drop_thr = 0, drop_layer = 0, drop_seq0 = 0;
+  float drop_scale = 1.f;
 };
 
 struct GemmPlan {

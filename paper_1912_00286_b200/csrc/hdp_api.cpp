@@ -186,6 +186,17 @@ struct hdp_ctx {
   const float* dyn_alpha() const { return dyn_interval > 0 ? alpha_dev() : nullptr; }
   int* dyn_state() const { return status + 8; }  // [0] step count, [1] good run, [2] skipped
   double l2 = 0.0;            // L2 coefficient (reading Q16), 0 = off
+  // recurrent dropout (NEXT-3; reading Q16b): keep < 1 switches it on
+  double keep = 1.0;
+  uint32_t drop_seed = 0, drop_thr = 0;
+  float drop_scale = 1.f;
+  char* hst = nullptr;        // library-owned: per slot [L][T+1][B][hp] fp16 masked recurrent inputs
+  bool drop_on() const { return keep < 1.0; }
+  bool recur_ok() const { return persistent && !drop_on(); }  // the fused recurrences have no dropout
+  int* drop_step() const { return status + 14; }  // completed updates (mask counter)
+  char* Hst(int slot, int l) const {
+    return hst + ((size_t)slot * d.n_layers + l) * (size_t)(d.max_seq + 1) * d.max_batch * hp * 2;
+  }
   double* l2part = nullptr;   // partial sums of the L2 loss term
   long adam_k = 0;
 
@@ -497,7 +508,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
     char* Hs = S.Hs + l * hs_layer * e;
     float* Cl = S.C + l * c_layer;
     char* Gl = S.gates + l * g_layer * e;
-    const bool wave = l == 0 && L == 2 && !f32 && c->persistent && hdp::recur2_fwd_supported(B, (int)hp);
+    const bool wave = l == 0 && L == 2 && !f32 && c->recur_ok() && hdp::recur2_fwd_supported(B, (int)hp);
     const bool fusex = wave && hdp::recur2_fwd_fuses_x(B, (int)hp, (int)Ipl);
     // K1: G_x = X W^T + b for all t (A1); inside the wavefront's layer-0 role when fused
     if (!fusex)
@@ -577,7 +588,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
       }
       break;
     }
-    if (!f32 && c->persistent && hdp::recur_fwd_supported(B, (int)hp)) {
+    if (!f32 && c->recur_ok() && hdp::recur_fwd_supported(B, (int)hp)) {
       // A2 + A3 for all t in one persistent kernel (U resident in SMEM)
       hdp::RecurFwdArgs ra;
       ra.U = (const __half*)c->W(iU);
@@ -622,7 +633,18 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
     for (int t = 0; t < T; ++t) {
       if (t > 0 && !f32) {
         // K2 with A3 in its epilogue: gates = h_{t-1} U^T + G_x[t] -> cell -> gates, c_t, h_t
+        // (recurrent dropout: the GEMM reads h~_{t-1}, the epilogue also writes h~_t)
         hdp::Epilogue ef;
+        const char* hin = c->drop_on() ? c->Hst(si, l) : Hs;
+        if (c->drop_on()) {
+          ef.htout = c->Hst(si, l) + (long)(t + 1) * B * hp * e;
+          ef.drop_step = c->drop_step();
+          ef.drop_seed = c->drop_seed;
+          ef.drop_thr = c->drop_thr;
+          ef.drop_layer = (uint32_t)l;
+          ef.drop_seq0 = (uint32_t)((c->rank * c->nslots + si) * B);
+          ef.drop_scale = c->drop_scale;
+        }
         ef.mode = hdp::EPI_LSTM_FWD;
         ef.hp = (int)hp;
         ef.gx = c->Gx + (long)t * B * 4 * hp;
@@ -630,7 +652,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
         ef.cout = Cl + (long)t * B * hp;
         ef.gates = Gl + (long)t * B * 4 * hp * e;
         ef.hout = Hs + (long)(t + 1) * B * hp * e;
-        CK(gemm(c, HDP_K_GEMM_H, Hs + (long)t * B * hp * e, hp, 0, c->W(iU), hp, 0, B, 4 * hp, hp, ef, s));
+        CK(gemm(c, HDP_K_GEMM_H, hin + (long)t * B * hp * e, hp, 0, c->W(iU), hp, 0, B, 4 * hp, hp, ef, s));
         continue;
       }
       if (t > 0)  // K2: G_h = h_{t-1} U^T (A2)
@@ -641,6 +663,12 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
         CK_CUDA(hdp::launch_cell_fwd(f32, c->Gx + (long)t * B * 4 * hp, t > 0 ? c->Gh : nullptr,
                                      t > 0 ? Cl + (long)(t - 1) * B * hp : nullptr, Gl + (long)t * B * 4 * hp * e,
                                      Cl + (long)t * B * hp, Hs + (long)(t + 1) * B * hp * e, B, (int)hp, s));
+      }
+      if (c->drop_on()) {  // h~_0 (the fused epilogues write the later ones)
+        KScope ks_(c, HDP_K_CELL_FWD, 1, s);
+        CK_CUDA(hdp::launch_drop_mask(Hs + (long)(t + 1) * B * hp * e, c->Hst(si, l) + (long)(t + 1) * B * hp * e, B,
+                                      (int)hp, c->drop_step(), c->drop_seed, (uint32_t)l,
+                                      (uint32_t)((c->rank * c->nslots + si) * B), c->drop_thr, c->drop_scale, s));
       }
     }
   }
@@ -768,7 +796,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
   const bool last_only = d.head_last_step && l == L - 1;
   // 2 layers, mixed mode: both layers' BPTT and the dX1 projection in one wavefront
   // launch (segment for layer 1); layer 0's segment then only has its K8 / K9 work
-  const bool wave = L == 2 && !f32 && c->persistent && hdp::recur2_bwd_supported(B, (int)hp);
+  const bool wave = L == 2 && !f32 && c->recur_ok() && hdp::recur2_bwd_supported(B, (int)hp);
   // ... and, on the SMs the recurrences leave idle, the A8 weight gradients of both layers
   const bool wgrad = wave && !gf && hdp::recur2_bwd_wgrad(B, (int)hp, (int)c->Ip0);
   if (wave) c->wave_bwd = true;
@@ -881,7 +909,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
     }
   } else if (wave) {
     // layer 0: already done by the wavefront launch of the layer-1 segment
-  } else if (!f32 && c->persistent && hdp::recur_bwd_supported(B, (int)hp)) {
+  } else if (!f32 && c->recur_ok() && hdp::recur_bwd_supported(B, (int)hp)) {
     // A6 + A7 for all t in one persistent kernel (U^T slice resident in SMEM)
     hdp::RecurBwdArgs ra;
     ra.U = (const __half*)c->W(iU);
@@ -944,6 +972,14 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
         eb.cprev = u > 0 ? Cl + (long)(u - 1) * B * hp : nullptr;
         eb.dc = c->dc;
         eb.dA = c->dA + (long)u * B * 4 * hp * e;
+        if (c->drop_on()) {
+          eb.drop_step = c->drop_step();
+          eb.drop_seed = c->drop_seed;
+          eb.drop_thr = c->drop_thr;
+          eb.drop_layer = (uint32_t)l;
+          eb.drop_seq0 = (uint32_t)((c->rank * c->nslots + si) * B);
+          eb.drop_scale = c->drop_scale;
+        }
         // K = 4 hp is long and M = B small: 256-wide tiles, split K over ~120 CTAs
         int fbn = 0, fsp = 0;
         if (hp >= 1024) {  // C4 sweep (tools/c4_gemm_sweep.py, HDP_K7_CFG): 256-wide tiles, ~128 CTAs
@@ -973,7 +1009,8 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
   if (!wgrad) {  // (else A8 was done inside the wavefront launch)
     // K8 (A8): dW = dA^T X, dU = dA^T H_{-1}, db = sum dA
     CK(gemm(c, HDP_K_GEMM_DW, dAl, 4 * hp, 1, X, Ipl, 1, 4 * hp, Ipl, rows, epi_elem(gf, c->G(si, iW), Ipl), s));
-    CK(gemm(c, HDP_K_GEMM_DW, dAl, 4 * hp, 1, Hs, hp, 1, 4 * hp, hp, rows, epi_elem(gf, c->G(si, iU), hp), s));
+    CK(gemm(c, HDP_K_GEMM_DW, dAl, 4 * hp, 1, c->drop_on() ? c->Hst(si, l) : Hs, hp, 1, 4 * hp, hp, rows,
+            epi_elem(gf, c->G(si, iU), hp), s));  // dU = sum_t dA_t^T h~_{t-1}
     KScope ks_(c, HDP_K_GEMM_DW, 2, s);
     CK_CUDA(hdp::launch_colreduce(f32, dAl, 4 * hp, (int)rows, (int)(4 * hp), nullptr, c->crp, gf, c->G(si, ib), s));
   }
@@ -1184,6 +1221,7 @@ int hdp_destroy(hdp_ctx* c) {
   if (c->gwin) cudaFree(c->gwin);
   if (c->wwin) cudaFree(c->wwin);
   if (c->fwin) cudaFree(c->fwin);
+  if (c->hst) cudaFree(c->hst);
   if (c->comm) ncclCommDestroy(c->comm);
   delete c;
   return HDP_OK;
@@ -1401,6 +1439,29 @@ int hdp_set_lr_schedule(hdp_ctx* c, double lambda0, double gamma, double n_half,
 double hdp_lr(const hdp_ctx* c, int epoch) {
   if (!c || !c->lr_set || !c->configured || epoch < 0) return -1.0;
   return sched(c, epoch);
+}
+
+int hdp_set_recurrent_dropout(hdp_ctx* c, double keep, unsigned int seed) {
+  if (!c) return fail(HDP_ERR_ARG, "null context");
+  if (!(keep > 0.0 && keep <= 1.0)) return fail(HDP_ERR_ARG, "keep must be in (0, 1]");
+  if (!c->bound) return fail(HDP_ERR_STATE, "context not bound");
+  if (keep < 1.0 && c->f32) return fail(HDP_ERR_UNSUPPORTED, "recurrent dropout is implemented for mixed mode only");
+  if (keep < 1.0 && c->d.n_layers == 0) return fail(HDP_ERR_ARG, "no LSTM layers");
+  CK_CUDA(cudaSetDevice(c->device));
+  CK_CUDA(cudaDeviceSynchronize());
+  for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);  // kernel choice and operands change
+  c->graphs.clear();
+  if (keep < 1.0 && !c->hst) {
+    const size_t bytes = (size_t)c->nslots * c->d.n_layers * (c->d.max_seq + 1) * c->d.max_batch * c->hp * 2;
+    CK_CUDA(cudaMalloc(&c->hst, bytes));
+    CK_CUDA(cudaMemset(c->hst, 0, bytes));  // slot t = 0 of every layer stays h~_{-1} = 0
+  }
+  CK_CUDA(cudaMemset(c->drop_step(), 0, sizeof(int)));
+  c->keep = keep;
+  c->drop_seed = seed;
+  c->drop_thr = keep < 1.0 ? (uint32_t)std::floor(keep * 4294967296.0) : 0u;
+  c->drop_scale = (float)(1.0 / keep);
+  return HDP_OK;
 }
 
 int hdp_set_l2(hdp_ctx* c, double l2) {
@@ -1672,6 +1733,10 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
     KScope ks_(c, HDP_K_UPDATE, 1, cs);
     CK_CUDA(hdp::launch_loss_scale_update(c->dyn_state(), c->alpha_dev(), c->dyn_interval, 2.f, 1.f, cs));
     count_src = c->dyn_state();
+  }
+  if (c->drop_on()) {  // next step's dropout masks
+    KScope ks_(c, HDP_K_UPDATE, 1, cs);
+    CK_CUDA(hdp::launch_increment(c->drop_step(), cs));
   }
   CK_CUDA(cudaMemcpyAsync(c->count_host, count_src, sizeof(int), cudaMemcpyDeviceToHost, cs));
   CK_CUDA(cudaEventRecord(c->ev_count, cs));

@@ -51,6 +51,12 @@ cudaError_t launch_pack_input(const void* x, int x_f32, int B, int T, int I, int
 cudaError_t launch_embed_gather(const int32_t* tok, int B, int T, const void* E, int Ep, void* X0, int f32,
                                 cudaStream_t s);
 
+// recurrent dropout (NEXT-3, dropout.cuh): ht[b][u] = kept(seq0 + b, u) ? fp16(h * scale) : 0
+cudaError_t launch_drop_mask(const void* h, void* ht, int B, int hp, const int* step, uint32_t seed, uint32_t layer,
+                             uint32_t seq0, uint32_t thr, float scale, cudaStream_t s);
+// *p += 1 (device counter, stream-ordered)
+cudaError_t launch_increment(int* p, cudaStream_t s);
+
 // ---------------------------------------------------------------- cell (K3 / K6)
 // gate rows interleaved per unit: row 4*j + {i,f,g,o}
 cudaError_t launch_cell_fwd(int f32, const float* Gx_t, const float* Gh, const float* c_prev, void* gates_t,

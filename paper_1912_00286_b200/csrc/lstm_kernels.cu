@@ -12,6 +12,7 @@
 #include <cub/device/device_radix_sort.cuh>
 #include <cuda_fp16.h>
 
+#include "dropout.cuh"
 #include "kernels.cuh"
 
 namespace hdp {
@@ -61,6 +62,18 @@ __global__ void pack_input_kernel(const XT* __restrict__ x, int B, int Tn, int I
     const float v = k < I ? ld<XT>(x, ((long)b * Tn + t) * I + k) : 0.f;
     X0[idx] = cvt<T>(v);
   }
+}
+
+// recurrent dropout (NEXT-3): h~ = fp16(fp32(h) * scale) on kept units, 0 elsewhere, for the
+// step whose h the fused GEMM epilogue did not produce (t = 0)
+__global__ void drop_mask_kernel(const __half* __restrict__ h, __half* __restrict__ ht, int B, int hp,
+                                 const int* __restrict__ step, uint32_t seed, uint32_t layer, uint32_t seq0,
+                                 uint32_t thr, float scale) {
+  const int idx = blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= B * hp) return;
+  const int b = idx / hp, u = idx % hp;
+  const uint32_t sk = drop_seq_key(drop_layer_key(seed, (uint32_t)*step, layer), seq0 + (uint32_t)b);
+  ht[idx] = drop_kept(sk, (uint32_t)u, thr) ? __float2half_rn(__half2float(h[idx]) * scale) : __float2half_rn(0.f);
 }
 
 // same-type rows with I == Ip and 16-B aligned rows: one warp per (t, b) row, 16-B vectors
@@ -529,6 +542,20 @@ cudaError_t launch_pack_input(const void* x, int x_f32, int B, int T, int I, int
     if (x_f32) pack_input_kernel<float, __half><<<g, 256, 0, s>>>((const float*)x, B, T, I, Ip, (__half*)X0);
     else pack_input_kernel<__half, __half><<<g, 256, 0, s>>>((const __half*)x, B, T, I, Ip, (__half*)X0);
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_drop_mask(const void* h, void* ht, int B, int hp, const int* step, uint32_t seed, uint32_t layer,
+                             uint32_t seq0, uint32_t thr, float scale, cudaStream_t s) {
+  const int n = B * hp;
+  drop_mask_kernel<<<(n + 255) / 256, 256, 0, s>>>((const __half*)h, (__half*)ht, B, hp, step, seed, layer, seq0, thr,
+                                                   scale);
+  return cudaGetLastError();
+}
+
+__global__ void incr_kernel(int* p) { *p += 1; }
+cudaError_t launch_increment(int* p, cudaStream_t s) {
+  incr_kernel<<<1, 1, 0, s>>>(p);
   return cudaGetLastError();
 }
 

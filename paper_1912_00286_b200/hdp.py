@@ -26,7 +26,7 @@ OPT_SGDM, OPT_ADAM = 0, 1
 EXPORTED = [
     "hdp_nccl_unique_id", "hdp_init", "hdp_destroy", "hdp_last_error", "hdp_configure", "hdp_bind",
     "hdp_num_blocks", "hdp_param_block", "hdp_load_params", "hdp_gather_master", "hdp_read_weights",
-    "hdp_read_grads", "hdp_set_lr_schedule", "hdp_lr", "hdp_set_loss_scale", "hdp_set_l2", "hdp_set_dynamic_loss_scale",
+    "hdp_read_grads", "hdp_set_lr_schedule", "hdp_lr", "hdp_set_loss_scale", "hdp_set_l2", "hdp_set_dynamic_loss_scale", "hdp_set_recurrent_dropout",
     "hdp_loss_scale_state", "hdp_lstm_forward",
     "hdp_lstm_backward", "hdp_grad_average_update", "hdp_weights_ptr", "hdp_grads_ptr", "hdp_master_ptr",
     "hdp_fused_avg_update", "hdp_gemm_f16", "hdp_gemm_f32", "hdp_profile", "hdp_profile_read",
@@ -83,6 +83,7 @@ def _load():
         "hdp_set_loss_scale": ([vp, f], i),
         "hdp_set_l2": ([vp, d], i),
         "hdp_set_dynamic_loss_scale": ([vp, i], i),
+        "hdp_set_recurrent_dropout": ([vp, d, C.c_uint], i),
         "hdp_loss_scale_state": ([vp, C.POINTER(f), C.POINTER(i)], i),
         "hdp_lstm_forward": ([vp, vp, vp, i, i, i, vp, vp, vp], i),
         "hdp_lstm_backward": ([vp, i, vp], i),
@@ -218,6 +219,10 @@ def set_loss_scale(ctx: int, alpha: float):
 
 def set_l2(ctx: int, l2: float):
     _ck(_lib.hdp_set_l2(ctx, l2))
+
+
+def set_recurrent_dropout(ctx: int, keep: float, seed: int = 0):
+    _ck(_lib.hdp_set_recurrent_dropout(ctx, keep, seed))
 
 
 def set_dynamic_loss_scale(ctx: int, growth_interval: int):

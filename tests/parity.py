@@ -35,7 +35,7 @@ def block_errors(cfg, got: np.ndarray, ref: np.ndarray, abs_terms: dict = None) 
 
 
 def run_parity(cfg, global_batch: int, n_workers: int, steps: int, mixed: bool, lambda0=None, alpha=None,
-               optimizer="sgdm", seed=synth.DATA_SEED, epochs=None, compare_grads=True, l2=0.0):
+               optimizer="sgdm", seed=synth.DATA_SEED, epochs=None, compare_grads=True, l2=0.0, dropout=None):
     """Returns a list of per-step records with GPU-vs-oracle errors."""
     import torch
 
@@ -52,6 +52,8 @@ def run_parity(cfg, global_batch: int, n_workers: int, steps: int, mixed: bool, 
     tr = hdp.Trainer(desc, params, lambda0=lambda0, alpha=alpha, gamma=cfg.gamma, n_half=cfg.n_half,
                      momentum=cfg.momentum, l2=l2)
     n = tr.n
+    if dropout is not None:                     # (keep, seed): NEXT-3 recurrent dropout
+        hdp.set_recurrent_dropout(tr.ctx, dropout[0], dropout[1])
     master = params.astype(np.float64)
     state = {"H": np.zeros(n)} if optimizer == "sgdm" else {"m1": np.zeros(n), "v": np.zeros(n)}
     recs = []
@@ -81,7 +83,9 @@ def run_parity(cfg, global_batch: int, n_workers: int, steps: int, mixed: bool, 
             lam = osched.rate_for_epoch(lambda0, n_workers, cfg.n_half, cfg.gamma, epoch, cfg.max_eff_lr)
             lam32 = float(np.float32(lam))
             ref = ostep.train_step(cfg, master, state, x, t, n_workers, alpha, lam32, mode, optimizer,
-                                   cfg.momentum, adam_k=k + 1, l2=l2)
+                                   cfg.momentum, adam_k=k + 1, l2=l2,
+                                   dropout=None if dropout is None else
+                                   {"keep": dropout[0], "seed": dropout[1], "step": k})
             rec = {
                 "step": k,
                 "loss_gpu": float(np.mean(gpu_losses)),

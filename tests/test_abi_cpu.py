@@ -53,6 +53,7 @@ def test_host_argument_errors(hdp):
     assert L.hdp_set_loss_scale(None, 1.0) == hdp.HDP_ERR_ARG
     assert L.hdp_set_l2(None, 0.0) == hdp.HDP_ERR_ARG
     assert L.hdp_set_dynamic_loss_scale(None, 100) == hdp.HDP_ERR_ARG
+    assert L.hdp_set_recurrent_dropout(None, 0.5, 1) == hdp.HDP_ERR_ARG
     assert L.hdp_loss_scale_state(None, None, None) == hdp.HDP_ERR_ARG
     assert L.hdp_fused_avg_update(None, 0, 1, 0, 8, None, None, None, None, None, 1.0, 0.0, 0.0, 0, None, None,
                                   0.0, None) == hdp.HDP_ERR_ARG

@@ -79,6 +79,24 @@ def test_c1_l2_stress(mixed):
     assert _max(recs[-1]["dmaster_err"]) <= (5e-2 if mixed else 1e-4), recs[-1]["dmaster_err"]
 
 
+@pytest.mark.parametrize("cfg_name,gb,nw,seq", [("C1", 8, 2, None), ("C2", 32, 1, 12), ("C4", 16, 2, 4)])
+def test_recurrent_dropout_mixed(cfg_name, gb, nw, seq):
+    # NEXT-3 recurrent dropout (reading Q16b): the same counter-based masks on both sides;
+    # C2 / C4 shapes run the per-step GEMM path with the masked-input epilogues
+    cfg = synth.CONFIGS[cfg_name]
+    if seq:
+        cfg = cfg.with_(seq=seq)
+    cfg = cfg.with_(lambda0=0.05, n_half=1e9)
+    recs = run_parity(cfg, gb, nw, steps=3, mixed=True, dropout=(0.7, 1234))
+    for r in recs:
+        assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"])), r
+        for ge in r["grad_err"]:
+            assert _max(ge) <= 2e-2, (r["step"], ge)
+        assert _max(r["master_err"]) <= 2e-2
+        assert r["w_matches_master"]
+    assert _max(recs[-1]["dmaster_err"]) <= 5e-2, recs[-1]["dmaster_err"]
+
+
 def test_c1_adam_fp32():
     cfg = synth.CONFIGS["C1"]
     recs = run_parity(cfg, synth.C1_GLOBAL_BATCH, synth.C1_SIM_WORKERS, steps=3, mixed=False, optimizer="adam",
