@@ -35,6 +35,7 @@ def main():
     l2 = float(os.environ.get("HDP_MP_L2", "0"))           # NEXT-3 L2 (reading Q16)
     dyn = int(os.environ.get("HDP_MP_DYN", "0"))           # NEXT-3 dynamic loss scale interval (Q14b)
     lam0 = float(os.environ.get("HDP_MP_LAMBDA0", "0"))
+    keep = float(os.environ.get("HDP_MP_KEEP", "1"))       # NEXT-3 recurrent dropout (Q16b)
     cfg = synth.CONFIGS[cfg_name]
     if seq:
         cfg = cfg.with_(seq=seq)
@@ -51,6 +52,8 @@ def main():
                      l2=l2)
     if dyn:
         hdp.set_dynamic_loss_scale(tr.ctx, dyn)
+    if keep < 1.0:
+        hdp.set_recurrent_dropout(tr.ctx, keep, 99)
     a_ref, good = alpha, 0
     from oracle import optim as ooptim
     n = tr.n
@@ -81,7 +84,8 @@ def main():
         if rank == 0:
             lam = float(np.float32(osched.rate_for_epoch(cfg.lambda0, world, cfg.n_half, cfg.gamma, 0)))
             ref = ostep.train_step(cfg, master_ref, state, x, t, world, a_ref, lam, "mixed" if mixed else "fp32",
-                                   l2=l2, skip_nonfinite=bool(dyn))
+                                   l2=l2, skip_nonfinite=bool(dyn),
+                                   dropout={"keep": keep, "seed": 99, "step": k} if keep < 1.0 else None)
             skip_ref = False
             if dyn:
                 a_ref, good, skip_ref = ooptim.dynamic_loss_scale(a_ref, good, ref["nonfinite"], dyn)

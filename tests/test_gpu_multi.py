@@ -67,3 +67,14 @@ def test_c1_multi_gpu_l2_and_dynamic_loss_scale():
     assert any(r["skip_ref"] for r in recs) and not all(r["skip_ref"] for r in recs)
     assert recs[-1]["alpha_gpu"] == recs[-1]["alpha_ref"]
 
+
+def test_c1_multi_gpu_recurrent_dropout():
+    # masks keyed by the global sequence index: rank r's rows are r*B + b on both sides
+    world = _world()
+    recs = _run(world, {"HDP_MP_CFG": "C1", "HDP_MP_MIXED": "1", "HDP_MP_WIRE": "0", "HDP_MP_GB": str(4 * world),
+                        "HDP_MP_STEPS": "3", "HDP_MP_KEEP": "0.7", "HDP_MP_LAMBDA0": "0.05"})
+    for r in recs:
+        assert r["weights_identical"], r
+        assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1, abs(r["loss_ref"])), r
+        assert max(r["master_err"].values()) <= 2e-2, r["master_err"]
+
