@@ -1807,6 +1807,7 @@ void* hdp_debug_buffer(hdp_ctx* c, int slot, const char* name) {
   if (n == "dA2") return c->dA2;
   if (n == "dH0") return c->dH[0];
   if (n == "dH1") return c->dH[1];
+  if (n == "Hst") return c->hst ? c->Hst(slot, 0) : nullptr;  // recurrent dropout: h~ [L][T+1][B][hp]
   return nullptr;
 }
 

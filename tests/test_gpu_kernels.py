@@ -243,3 +243,44 @@ def test_gemm_cta_pair_and_multicast_variants(hdp, monkeypatch, cg, bn, amn, bmn
         ref = A.double() @ B.double().T
         assert (C.double() - ref).abs().max().item() <= 1e-5 * ref.abs().max().item(), env
         monkeypatch.delenv(env)
+
+
+def _dev_f16(ptr, n):
+    """host copy of n fp16 values of library-owned device memory (CUDA array interface)"""
+    class _CAI:
+        __cuda_array_interface__ = {"shape": (n,), "typestr": "<f2", "data": (ptr, False), "version": 3}
+    return torch.as_tensor(_CAI(), device="cuda").cpu().numpy()
+
+
+def test_recurrent_dropout_masks_bit_exact(hdp):
+    # the CUDA mask hash (csrc/dropout.cuh) against the oracle's (oracle/dropout.py), bit for
+    # bit: after one forward, h~_t = fp16(fp32(h_t) * fp32(1/keep)) on kept units, 0 elsewhere
+    import synth
+    from oracle import dropout as odrop
+    cfg = synth.CONFIGS["C1"].with_(n_layers=2)
+    B, keep, seed = 4, 0.7, 4321
+    desc = hdp.desc_from_config(cfg, B, hdp.MATH_MIXED16, sim_workers=2)
+    tr = hdp.Trainer(desc, synth.init_params(cfg), lambda0=cfg.lambda0)
+    try:
+        hdp.set_recurrent_dropout(tr.ctx, keep, seed)
+        x, t = synth.model_batch(cfg, 2 * B, synth.DATA_SEED)
+        T, hp, L = cfg.seq, 32, cfg.n_layers
+        sc = np.float32(odrop.scale(keep))
+        for slot in (0, 1):
+            xs = torch.from_numpy(np.ascontiguousarray(x[slot * B:(slot + 1) * B])).cuda()
+            ts = torch.from_numpy(np.ascontiguousarray(t[slot * B:(slot + 1) * B])).cuda()
+            hdp.lstm_forward(tr.ctx, xs, ts, B, T, slot, None, tr.loss[slot:slot + 1])
+            torch.cuda.synchronize()
+            h = _dev_f16(hdp.debug_buffer(tr.ctx, slot, "Hs"), L * (T + 1) * B * hp).reshape(L, T + 1, B, hp)
+            # Hst: per layer (T_max + 1) * B_max rows; here T = T_max and B = B_max
+            h_t = _dev_f16(hdp.debug_buffer(tr.ctx, slot, "Hst"), L * (T + 1) * B * hp).reshape(L, T + 1, B, hp)
+            for l in range(L):
+                m = odrop.mask(seed, 0, l, np.arange(slot * B, (slot + 1) * B), cfg.hidden, keep)  # [B][h]
+                assert 0 < m.mean() < 1
+                exp = np.where(m[None] > 0, (h[l, 1:, :, :cfg.hidden].astype(np.float32) * sc).astype(np.float16),
+                               np.float16(0))
+                got = h_t[l, 1:, :, :cfg.hidden]
+                assert np.array_equal(got.view(np.uint16), exp.view(np.uint16)), (slot, l)
+                assert not np.any(h_t[l, 0])                     # h~_{-1} = 0
+    finally:
+        tr.close()
