@@ -315,7 +315,8 @@ def run_hdp(args, rank, world, local_rank):
                    "hidden": cfg.hidden, "layers": cfg.n_layers, "fc_hidden": cfg.fc_hidden,
                    "parallelism": f"dp{world}", "math": "fp16 (fp32 accumulate, fp32 master)",
                    "wire": "fp16 all-to-all", "optimizer": "sgd-momentum", "loss_scale": cfg.alpha,
-                   "l2": "flushed between timed steps (256 MiB memset, outside the events)"},
+                   "l2_cache": "flushed between timed steps (256 MiB memset, outside the events)",
+                   "l2_regularisation": 0.0, "recurrent_dropout_keep": 1.0, "loss_scale_mode": "static"},
         "e2e": {"value": samples / (e2e_ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": x_bytes + t_bytes,
                 "d2h_bytes_per_step": 4},
         "gpu_launches": int(launches),
@@ -433,7 +434,7 @@ def run_c5(args, rank, world, local_rank):
             "data": "synthetic gradients N(0, 0.05^2)",
             "config": {"workload": "C5-avg-update", "sizes_mib": sizes_mib, "wire": args.wire,
                        "contributions": nsim if world == 1 else world, "parallelism": f"dp{world}",
-                       "l2": "flushed between timed steps"},
+                       "l2_cache": "flushed between timed steps"},
             "roofline": {"bound": "hbm", "achieved": big["k11_gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
                          "frac": big["k11_gbs"] / pk["hbm_gbs"], "traffic": None, "kernel": "update(K11)",
                          "peak_src": pk["src"], "avg_launch_us": big["k11_launch_us"], "per_launch": big["k11_bytes"],
