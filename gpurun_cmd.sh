@@ -1,2 +1,5 @@
-HDP_CONV_STEPS=600 HDP_CONV_LAMBDA0=0.05 timeout -s KILL 900 python -m pytest tests/test_gpu_convergence.py -q -p no:cacheprovider -x > gpurun_out/v19_conv_sgd.log 2>&1; cp gpurun_out/convergence_auc.json gpurun_out/v19_auc_sgd.json
-HDP_CONV_STEPS=600 HDP_CONV_LAMBDA0=0.002 HDP_CONV_OPT=adam timeout -s KILL 900 python -m pytest tests/test_gpu_convergence.py -q -p no:cacheprovider -x > gpurun_out/v19_conv_adam.log 2>&1; cp gpurun_out/convergence_auc.json gpurun_out/v19_auc_adam.json
+timeout -s KILL 1500 python -m pytest tests -m gpu -q -p no:cacheprovider > gpurun_out/v42_gpu_tests.log 2>&1; echo exit=$? >> gpurun_out/v42_gpu_tests.log
+timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/v42_smoke.log 2>&1; echo exit=$? >> gpurun_out/v42_smoke.log
+timeout -s KILL 400 python bench.py > gpurun_out/v42_c2_default.json 2> gpurun_out/v42_c2_default.err
+timeout -s KILL 400 python bench.py --impl reference > gpurun_out/v42_reference.json 2> gpurun_out/v42_reference.err
+timeout -s KILL 300 python bench.py --config C4 --steps 5 --warmup 3 --no-cpu-baseline > gpurun_out/v42_c4.json 2> gpurun_out/v42_c4.err
