@@ -309,8 +309,8 @@ __global__ void outer_kernel(const float* __restrict__ dy, const T* __restrict__
 constexpr int CR_WARPS = 8;
 
 int cr_splits(int rows) {
-  int rs = (rows + 511) / 512;
-  if (rs > 64) rs = 64;
+  int rs = (rows + 127) / 128;  // row chunks of 128 (16 rows per warp): enough blocks to fill the GPU
+  if (rs > 128) rs = 128;
   if (rs < 1) rs = 1;
   return rs;
 }
@@ -370,13 +370,23 @@ __global__ void __launch_bounds__(CR_WARPS * 32)
     partials[(long)blockIdx.y * cols + c] = s;
   }
 }
+// pass 2: one warp per column, lane-strided partial sums then a fixed xor-butterfly
+// (deterministic order), so the up to 128 partials of a column are not one serial chain
+__device__ __forceinline__ double warp_col_sum(const double* __restrict__ partials, int rs, int cols, int c, int lane) {
+  double s = 0.0;
+  for (int q = lane; q < rs; q += 32) s += partials[(long)q * cols + c];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+  return s;
+}
+
 __global__ void colreduce3_pass2(const double* __restrict__ partials, int rs, int F, int out_f32, void* dwo, void* dfb,
                                  void* dbo) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   const int cols = 2 * F + 1;
   if (c >= cols) return;
-  double s = 0.0;
-  for (int q = 0; q < rs; ++q) s += partials[(long)q * cols + c];
+  const double s = warp_col_sum(partials, rs, cols, c, lane);
+  if (lane != 0) return;
   void* out = c < F ? dwo : c < 2 * F ? dfb : dbo;
   const int i = c < F ? c : c < 2 * F ? c - F : 0;
   if (out_f32)
@@ -386,10 +396,10 @@ __global__ void colreduce3_pass2(const double* __restrict__ partials, int rs, in
 }
 
 __global__ void colreduce_pass2(const double* __restrict__ partials, int rs, int cols, int out_f32, void* out) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int c = (blockIdx.x * blockDim.x + threadIdx.x) >> 5, lane = threadIdx.x & 31;
   if (c >= cols) return;
-  double s = 0.0;
-  for (int q = 0; q < rs; ++q) s += partials[(long)q * cols + c];
+  const double s = warp_col_sum(partials, rs, cols, c, lane);
+  if (lane != 0) return;
   if (out_f32)
     reinterpret_cast<float*>(out)[c] = (float)s;
   else
@@ -645,7 +655,7 @@ cudaError_t launch_colreduce(int x_f32, const void* X, long ldx, int rows, int c
   double* part = reinterpret_cast<double*>(partials);
   if (x_f32) colreduce_pass1<float><<<g1, CR_WARPS * 32, 0, s>>>((const float*)X, ldx, rows, cols, w, rs, part);
   else colreduce_pass1<__half><<<g1, CR_WARPS * 32, 0, s>>>((const __half*)X, ldx, rows, cols, w, rs, part);
-  colreduce_pass2<<<(cols + 255) / 256, 256, 0, s>>>(part, rs, cols, out_f32, out);
+  colreduce_pass2<<<(cols * 32 + 255) / 256, 256, 0, s>>>(part, rs, cols, out_f32, out);
   return cudaGetLastError();
 }
 
@@ -659,7 +669,7 @@ cudaError_t launch_colreduce3(int x_f32, const void* Z, const void* dz, long ld,
     colreduce3_pass1<float><<<g1, CR_WARPS * 32, 0, s>>>((const float*)Z, (const float*)dz, ld, rows, F, dy, rs, part);
   else
     colreduce3_pass1<__half><<<g1, CR_WARPS * 32, 0, s>>>((const __half*)Z, (const __half*)dz, ld, rows, F, dy, rs, part);
-  colreduce3_pass2<<<(cols + 255) / 256, 256, 0, s>>>(part, rs, F, out_f32, dwo, dfb, dbo);
+  colreduce3_pass2<<<(cols * 32 + 255) / 256, 256, 0, s>>>(part, rs, F, out_f32, dwo, dfb, dbo);
   return cudaGetLastError();
 }
 
