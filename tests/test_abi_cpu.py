@@ -69,3 +69,15 @@ def test_no_cpu_fallback_in_product_path():
             if f.endswith((".py", ".cpp", ".cu", ".cuh", ".h")):
                 txt = open(os.path.join(dirpath, f)).read()
                 assert "import oracle" not in txt and "from oracle" not in txt, f
+
+
+def test_import_fails_loudly_without_library(tmp_path):
+    # a copy of the binding next to no libhdp.so must refuse to import
+    import shutil
+    import subprocess
+    import sys
+    shutil.copy(os.path.join(ROOT, "paper_1912_00286_b200", "hdp.py"), tmp_path / "hdp_copy.py")
+    r = subprocess.run([sys.executable, "-c", "import hdp_copy"], cwd=tmp_path,
+                       capture_output=True, text=True, timeout=300)
+    assert r.returncode != 0
+    assert "libhdp.so not built" in r.stderr and "no CPU fallback" in r.stderr
