@@ -215,7 +215,7 @@ def test_persistent_matches_per_step_path(monkeypatch):
     assert abs(out["1"]["loss_gpu"] - out["0"]["loss_gpu"]) <= 1e-4
 
 
-@pytest.mark.parametrize("batch,fusex", [(128, "1"), (32, "1"), (64, "0")])
+@pytest.mark.parametrize("batch,fusex", [(128, "1"), (32, "1"), (64, "0"), (40, "1"), (100, "1"), (72, "0")])
 def test_c2_wavefront_matches_layerwise(monkeypatch, batch, fusex):
     """The 2-layer wavefront kernels (forward: R0/P/R1 roles, layer-0 input
     projection fused into R0 or read from the K1 GEMM; backward: Q1/X/Q0 roles,
