@@ -194,6 +194,7 @@ def run_hdp(args, rank, world, local_rank):
     params = synth.init_params(cfg) if rank == 0 else None
     tr = hdp.Trainer(desc, params, lambda0=cfg.lambda0, alpha=cfg.alpha, gamma=cfg.gamma, n_half=cfg.n_half,
                      momentum=cfg.momentum, world=world, rank=rank, uid=uid, device=local_rank)
+    exchange = hdp.EXCHANGE_KINDS.get(hdp.exchange_kind(tr.ctx), "?")
     x, t = synth.model_batch(cfg, B, synth.DATA_SEED + 1000 * rank)
     xd = torch.from_numpy(np.ascontiguousarray(x)).to(dev)
     td = torch.from_numpy(np.ascontiguousarray(t)).to(dev)
@@ -314,7 +315,7 @@ def run_hdp(args, rank, world, local_rank):
         "config": {"workload": cfg.name, "per_rank_batch": B, "global_batch": samples, "seq_len": cfg.seq,
                    "hidden": cfg.hidden, "layers": cfg.n_layers, "fc_hidden": cfg.fc_hidden,
                    "parallelism": f"dp{world}", "math": "fp16 (fp32 accumulate, fp32 master)",
-                   "wire": "fp16 all-to-all", "optimizer": "sgd-momentum", "loss_scale": cfg.alpha,
+                   "wire": "fp16", "exchange": exchange, "optimizer": "sgd-momentum", "loss_scale": cfg.alpha,
                    "l2_cache": "flushed between timed steps (256 MiB memset, outside the events)",
                    "l2_regularisation": 0.0, "recurrent_dropout_keep": 1.0, "loss_scale_mode": "static"},
         "e2e": {"value": samples / (e2e_ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": x_bytes + t_bytes,
@@ -442,17 +443,40 @@ def run_c5(args, rank, world, local_rank):
             "sweep": rows, "clocks": clocks, "gpu_launches": None}
 
 
+def host_cpu():
+    """CPU model and the cores this process may run on (for the cpu_baseline lines)."""
+    model = "unknown"
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        cores = len(os.sched_getaffinity(0))
+    except Exception:  # noqa: BLE001
+        cores = os.cpu_count()
+    return model, cores
+
+
+def blas_threads():
+    try:
+        from threadpoolctl import threadpool_info
+        return max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
+    except Exception:  # noqa: BLE001
+        return os.cpu_count()
+
+
 def cpu_baseline(args, seconds=15.0, max_steps=4):
     """The oracle as it stands, on the host cores, on a bounded sample."""
     import numpy as np
 
     import synth
     from oracle import step as ostep
-    try:
-        from threadpoolctl import threadpool_info
-        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        threads = os.cpu_count()
+    threads = blas_threads()
+    model, cores = host_cpu()
     cfg = synth.CONFIGS[args.config]
     B = args.batch or cfg.batch
     if args.config == "C4":
@@ -471,7 +495,9 @@ def cpu_baseline(args, seconds=15.0, max_steps=4):
     dt = time.perf_counter() - t0
     return {"value": n * B / dt, "unit": "samples/s", "cores": threads, "kind": "oracle",
             "sample": f"{n} oracle.step.train_step of {cfg.name} ({B} sequences x T={cfg.seq}, mixed mode, N=1) "
-                      f"in {dt:.1f} s"}
+                      f"in {dt:.1f} s",
+            "cpu": model, "host_cores": cores,
+            "threads_note": "cores = BLAS threads of the matrix products; elementwise phases single-threaded"}
 
 
 def run_reference(args):
@@ -498,11 +524,8 @@ def run_reference(args):
     for _ in range(args.steps):
         one()
     dt = time.perf_counter() - t0
-    try:
-        from threadpoolctl import threadpool_info
-        threads = max([i.get("num_threads", 1) for i in threadpool_info()] + [1])
-    except Exception:
-        threads = os.cpu_count()
+    threads = blas_threads()
+    model, cores = host_cpu()
     v = Bs * args.steps / dt
     sample = f"{Bs} sequences of {cfgs.name} (T={cfgs.seq}) per step, oracle.step.train_step, mixed mode"
     return {"impl": "reference", "metric": METRIC, "value": v, "unit": "samples/s", "n_gpus": args.gpus,
@@ -510,7 +533,8 @@ def run_reference(args):
             "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic", "config": {"workload": cfg.name, "per_rank_batch": Bs, "seq_len": cfgs.seq,
                                               "parallelism": "host"},
-            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": "oracle", "sample": sample},
+            "cpu_baseline": {"value": v, "unit": "samples/s", "cores": threads, "kind": "oracle", "sample": sample,
+                             "cpu": model, "host_cores": cores},
             "e2e": {"value": v, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 

@@ -60,6 +60,22 @@ enum { HDP_WIRE_FP16_A2A = 0,     /* fp16 all-to-all, fp32 rank-ordered sum in K
 enum { HDP_OPT_SGDM = 0,  /* Eqs. 1-2                              */
        HDP_OPT_ADAM = 1   /* "any optimizer" (:98), Kingma & Ba with bias correction  */
 };
+/* How steps 4-6 move the data (hdp_model_desc.exchange).       */
+enum { HDP_EXCH_AUTO = 0,  /* world >= 2: HDP_EXCH_P2P where it applies, else NCCL;
+                              world == 1: K11 over the local gradient slots             */
+       HDP_EXCH_NCCL = 1,  /* NCCL collectives per bucket (all-to-all / reduce-scatter,
+                              K11, all-gather), or K11 alone at world == 1              */
+       HDP_EXCH_P2P = 2    /* NEXT-2: one kernel reads every rank's fp16 gradient shard
+                              over NVLink peer memory (CUDA IPC), does the K11 arithmetic
+                              and stores the fp16 weights into every rank's copy.  Needs
+                              mixed math, the fp16 all-to-all wire and world <= 8.  At
+                              world == 1 with 2 <= sim_workers <= 8 it runs as a LOOPBACK:
+                              the contributions are the simulated workers' gradient slots
+                              and the kernel writes sim_workers weight copies (copy 0 is the
+                              working copy, the others are readable as debug buffer
+                              "Wcopy"), so the kernel's arithmetic and protocol are tested
+                              on one GPU.  HDP_ERR_UNSUPPORTED where it does not apply.   */
+};
 
 typedef struct hdp_ctx hdp_ctx;
 
@@ -81,6 +97,7 @@ typedef struct {
   int optimizer;       /* HDP_OPT_*                                               */
   int sim_workers;     /* >= 1; > 1 only when world == 1 (simulated workers)      */
   long long flat_params; /* n_layers == 0 only                                    */
+  int exchange;        /* HDP_EXCH_*                                              */
 } hdp_model_desc;
 
 typedef struct {
@@ -117,11 +134,19 @@ int hdp_destroy(hdp_ctx* ctx);
 const char* hdp_last_error(void);
 
 /* Validate the model and compute the device layout and arena size.
- * All ranks must pass identical descriptions.                         */
+ * All ranks must pass identical descriptions: at world > 1 a 64-bit hash of
+ * the description is all-reduced (min and max over the ranks) and a
+ * mismatch returns HDP_ERR_ARG on every rank (collective call).          */
 int hdp_configure(hdp_ctx* ctx, const hdp_model_desc* desc, hdp_sizes* out);
 /* Bind the caller-owned device arena (>= arena_bytes, 256-B aligned).
  * Zero-fills it, sets up kernels and streams.                         */
 int hdp_bind(hdp_ctx* ctx, void* arena, long long arena_bytes);
+
+/* The exchange path configure resolved desc.exchange to:
+ * 0 = K11 over the local gradient slots (world 1), 1 = NCCL collectives + K11,
+ * 2 = the one-kernel NVLink exchange across ranks, 3 = its world-1 loopback;
+ * negative if not configured.                                          */
+int hdp_exchange_kind(const hdp_ctx* ctx);
 
 int hdp_num_blocks(const hdp_ctx* ctx);
 int hdp_param_block(const hdp_ctx* ctx, int i, hdp_block* out);
@@ -192,7 +217,9 @@ int hdp_set_recurrent_dropout(hdp_ctx* ctx, double keep, unsigned int seed);
  *     growth_interval consecutive finite steps alpha *= 2.
  * alpha stays on the device (no host synchronisation per step).  Requires a
  * bound context; toggling drops the captured forward graphs.
- * Errors: growth_interval < 0 -> HDP_ERR_ARG; unbound -> HDP_ERR_STATE.      */
+ * Errors: growth_interval < 0 -> HDP_ERR_ARG; unbound -> HDP_ERR_STATE;
+ * the Adam optimizer -> HDP_ERR_UNSUPPORTED (its bias-correction step count
+ * is kept on the host and would also count skipped steps).                  */
 int hdp_set_dynamic_loss_scale(hdp_ctx* ctx, int growth_interval);
 /* Current alpha and the number of skipped steps since dynamic scaling was
  * enabled (synchronises the device).  With static alpha: the set value, 0.   */
@@ -202,6 +229,10 @@ int hdp_loss_scale_state(hdp_ctx* ctx, float* alpha, int* skipped_steps);
  * loss Eq. 6 (:179).
  *   x       : dense input [B][T][input_dim], fp16 (mixed) or fp32 (FP32
  *             mode), or int32 tokens [B][T] when vocab > 0; host or device.
+ *             Token ids must lie in [0, vocab): an id outside it is read as
+ *             id 0 (no out-of-bounds access) and counted on the device; the
+ *             next hdp_grad_average_update returns HDP_ERR_ARG for that step
+ *             (its update has run) and poisons the context.
  *   targets : int8 in {-1,+1}, [B][T] (per-step heads) or [B] (last-step).
  *   y_out   : device fp32 [T][B] (or [B]); nullable.
  *   loss_out: device fp32 scalar = mean hinge WITHOUT alpha; nullable.
@@ -260,7 +291,10 @@ void* hdp_master_ptr(hdp_ctx* ctx);            /* this rank's fp32 master shards
  * (fp16 [L][T][B][4hp]), "X0" (fp16 [T][B][Ip0]), "dA" (fp16 [T][B][4hp]; the
  * top layer's in the 2-layer wavefront), "dA2" (layer 0's in the wavefront),
  * "dH0"/"dH1" (fp32), "Hst" (recurrent dropout's masked inputs h~, fp16
- * [L][T_max+1][B_max][hp] with rows [t][B][hp] of the actual B inside).  Returns NULL for an unknown name or unbound context.  */
+ * [L][T_max+1][B_max][hp] with rows [t][B][hp] of the actual B inside),
+ * "Wcopy" (HDP_EXCH_P2P loopback: weight copies 1..sim_workers-1, each a
+ * device-layout fp16 vector of n_params_padded elements; slot argument
+ * ignored).  Returns NULL for an unknown name or unbound context.  */
 void* hdp_debug_buffer(hdp_ctx* ctx, int slot, const char* name);
 
 /* ---------------------------------------------------------------------

@@ -136,6 +136,9 @@ struct hdp_ctx {
   char* dA2 = nullptr;  // layer-0 dA of the 2-layer backward wavefront (layer 1 keeps dA)
   bool wave_bwd = false;  // the backward ran as one wavefront launch: layer buckets are ready together
   // NEXT-2 NVLink exchange: library-owned, IPC-shared windows (gradients, fp16 weights, flags)
+  bool want_p2p = false;  // desc.exchange resolved at configure time
+  bool loopback = false;  // HDP_EXCH_P2P at world 1: simulated workers' slots as the peers
+  char* wcopies = nullptr;  // loopback: weight copies 1..nslots-1 [nslots-1][P]
   bool p2p = false;
   char *gwin = nullptr, *wwin = nullptr;
   unsigned* fwin = nullptr;
@@ -159,7 +162,7 @@ struct hdp_ctx {
   cudaStream_t cap = nullptr, comm_stream = nullptr;
   cudaEvent_t ev_done = nullptr, ev_count = nullptr;
   std::vector<cudaEvent_t> ev_bucket;
-  int* count_host = nullptr;  // pinned
+  int* count_host = nullptr;  // pinned [0] non-finite count, [1] out-of-range token ids
   bool count_pending = false;
   std::map<GraphKey, cudaGraphExec_t> graphs;
   std::map<GraphKey, long long> graph_kernels;  // kernels per captured graph
@@ -346,8 +349,10 @@ void carve(hdp_ctx* c, char* base) {
   c->s2 = (float*)cv.take(d.optimizer == HDP_OPT_ADAM ? c->M_own * 4 : 0);
   c->grads = cv.take((size_t)c->nslots * P * c->gsz);
   c->recv = cv.take(c->world > 1 ? c->P * c->gsz : 0);  // bucket bi received at its own offset
-  c->status = (int*)cv.take(32768);  // [0] non-finite count; +1024 B: recurrence barrier counters;
+  c->status = (int*)cv.take(32768);  // [0] non-finite count, [16] out-of-range token ids;
+                                       // +1024 B: recurrence barrier counters;
                                        // +4096 B: backward-wavefront hand-off counters
+  c->wcopies = cv.take(c->loopback ? (size_t)(c->nslots - 1) * P * c->esz : 0);
   c->l2part = (double*)cv.take(hdp::l2_partials_doubles() * sizeof(double));
   c->slot.assign(c->nslots, hdp_ctx::Slot{});
   if (d.n_layers > 0) {
@@ -488,7 +493,8 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
   if (d.vocab > 0)
     {
       KScope ks_(c, HDP_K_INPUT, 1, s);
-      CK_CUDA(hdp::launch_embed_gather((const int32_t*)S.stage_x, B, T, c->W(c->find("E")), (int)c->Ip0, S.X0, f32, s));
+      CK_CUDA(hdp::launch_embed_gather((const int32_t*)S.stage_x, B, T, c->W(c->find("E")), (int)c->Ip0, S.X0, f32,
+                                       d.vocab, c->status + 16, s));
     }
   else
     {
@@ -1075,7 +1081,7 @@ double sched(const hdp_ctx* c, int epoch) {
   return lam * std::pow(c->gamma, (double)epoch); // Eq. 3
 }
 
-__attribute__((unused)) int nccl_async_check(hdp_ctx* c) {
+int nccl_async_check(hdp_ctx* c) {
   if (!c->comm) return HDP_OK;
   ncclResult_t ar;
   CK_NCCL(ncclCommGetAsyncError(c->comm, &ar));
@@ -1086,16 +1092,54 @@ __attribute__((unused)) int nccl_async_check(hdp_ctx* c) {
 ncclDataType_t gtype(const hdp_ctx* c) { return c->gf32 ? ncclFloat : ncclHalf; }
 ncclDataType_t wtype(const hdp_ctx* c) { return c->f32 ? ncclFloat : ncclHalf; }
 
+void p2p_bucket_table(hdp_ctx* c) {
+  hdp::P2PArgs& a = c->p2pa;
+  a.nb = (int)c->buckets.size();
+  long vtot = 0;
+  for (int bi = 0; bi < a.nb; ++bi) {
+    const Bucket& bk = c->buckets[bi];
+    a.off[bi] = bk.off;
+    a.shard[bi] = bk.shard;
+    a.moff[bi] = bk.moff;
+    a.vpre[bi] = vtot;
+    vtot += bk.shard / 8;
+  }
+  a.vpre[a.nb] = vtot;
+  a.W = c->master;
+  a.S1 = c->s1;
+  a.S2 = c->s2;
+  c->p2p_grid = (int)std::max(1L, std::min((vtot + 255) / 256, 4L * 148));
+}
+
+// NEXT-2 loopback (world 1, HDP_EXCH_P2P): the exchange kernel's peers are the simulated
+// workers' gradient slots and nslots weight copies in the arena; the flag protocol runs
+// with one rank (its own flag block, library-owned).
+int setup_loopback(hdp_ctx* c) {
+  CK_CUDA(cudaMalloc(&c->fwin, hdp::P2P_FLAG_WORDS * sizeof(unsigned)));
+  CK_CUDA(cudaMemset(c->fwin, 0, hdp::P2P_FLAG_WORDS * sizeof(unsigned)));
+  hdp::P2PArgs& a = c->p2pa;
+  a.N = c->nslots;
+  a.NR = 1;
+  a.rank = 0;
+  for (int r = 0; r < c->nslots; ++r) {
+    a.g_peer[r] = (const __half*)(c->grads + (size_t)r * c->P * c->gsz);
+    a.w_peer[r] = (__half*)(r == 0 ? c->w : c->wcopies + (size_t)(r - 1) * c->P * c->esz);
+  }
+  a.flag_peer[0] = c->fwin;
+  a.status_peer[0] = (int*)(c->fwin + hdp::P2P_STATUS);
+  a.flag_local = c->fwin;
+  p2p_bucket_table(c);
+  c->p2p = true;
+  return HDP_OK;
+}
+
 // NEXT-2: gradients and fp16 working weights move into library-owned cudaMalloc windows
 // whose CUDA IPC handles are exchanged over the NCCL communicator; every rank maps every
 // peer's windows, so one kernel can read the N contributions and write the N weight
-// copies over NVLink (HDP_P2P=0 keeps the NCCL collectives).
+// copies over NVLink (desc.exchange = HDP_EXCH_NCCL keeps the NCCL collectives).
 int setup_p2p(hdp_ctx* c) {
-  const char* e = getenv("HDP_P2P");
-  if (c->world < 2 || (e && e[0] == '0')) return HDP_OK;
-  if (c->f32 || c->gsz != 2 || c->d.wire != HDP_WIRE_FP16_A2A || c->world > hdp::P2P_MAX_RANKS ||
-      (int)c->buckets.size() > hdp::P2P_MAX_BUCKETS)
-    return HDP_OK;
+  if (!c->want_p2p) return HDP_OK;
+  if (c->loopback) return setup_loopback(c);
   const size_t gbytes = (size_t)c->P * c->gsz, wbytes = (size_t)c->P * c->esz;
   CK_CUDA(cudaMalloc(&c->gwin, gbytes));
   CK_CUDA(cudaMalloc(&c->wwin, wbytes));
@@ -1118,6 +1162,7 @@ int setup_p2p(hdp_ctx* c) {
   CK_CUDA(cudaFree(dh));
   hdp::P2PArgs& a = c->p2pa;
   a.N = c->world;
+  a.NR = c->world;
   a.rank = c->rank;
   for (int r = 0; r < c->world; ++r) {
     void* ptr[3];
@@ -1135,21 +1180,7 @@ int setup_p2p(hdp_ctx* c) {
     a.status_peer[r] = (int*)((unsigned*)ptr[2] + hdp::P2P_STATUS);
   }
   a.flag_local = c->fwin;
-  a.nb = (int)c->buckets.size();
-  long vtot = 0;
-  for (int bi = 0; bi < a.nb; ++bi) {
-    const Bucket& bk = c->buckets[bi];
-    a.off[bi] = bk.off;
-    a.shard[bi] = bk.shard;
-    a.moff[bi] = bk.moff;
-    a.vpre[bi] = vtot;
-    vtot += bk.shard / 8;
-  }
-  a.vpre[a.nb] = vtot;
-  a.W = c->master;
-  a.S1 = c->s1;
-  a.S2 = c->s2;
-  c->p2p_grid = (int)std::max(1L, std::min((vtot + 255) / 256, 4L * 148));
+  p2p_bucket_table(c);
   // the arena's gradient and weight regions are replaced by the shared windows
   c->grads = c->gwin;
   c->w = c->wwin;
@@ -1160,6 +1191,35 @@ int setup_p2p(hdp_ctx* c) {
   CK_NCCL(ncclAllReduce(one, one, 1, ncclInt32, ncclSum, c->comm, 0));
   CK_CUDA(cudaStreamSynchronize(0));
   CK_CUDA(cudaFree(one));
+  return HDP_OK;
+}
+
+// Every rank must configure the same model (hdp.h): a 64-bit FNV-1a hash of the
+// description's fields, all-reduced with min and max, must agree.
+int check_desc_across_ranks(hdp_ctx* c, const hdp_model_desc& d) {
+  if (c->world < 2 || c->host_only || !c->comm) return HDP_OK;
+  const long long f[] = {d.n_layers, d.input_dim, d.hidden, d.fc_hidden, d.head_last_step, d.vocab, d.embed_dim,
+                         d.max_batch, d.max_seq, d.math, d.wire, d.optimizer, d.sim_workers, d.flat_params,
+                         d.exchange};
+  unsigned long long h = 1469598103934665603ull;
+  for (long long v : f)
+    for (int b = 0; b < 8; ++b) {
+      h ^= (unsigned long long)((v >> (8 * b)) & 0xff);
+      h *= 1099511628211ull;
+    }
+  CK_CUDA(cudaSetDevice(c->device));
+  unsigned long long* buf = nullptr;
+  CK_CUDA(cudaMalloc(&buf, 2 * sizeof h));
+  std::unique_ptr<unsigned long long, void (*)(unsigned long long*)> guard(buf, [](unsigned long long* p) { cudaFree(p); });
+  const unsigned long long hh[2] = {h, h};
+  CK_CUDA(cudaMemcpy(buf, hh, sizeof hh, cudaMemcpyHostToDevice));
+  CK_NCCL(ncclGroupStart());
+  CK_NCCL(ncclAllReduce(buf, buf, 1, ncclUint64, ncclMin, c->comm, 0));
+  CK_NCCL(ncclAllReduce(buf + 1, buf + 1, 1, ncclUint64, ncclMax, c->comm, 0));
+  CK_NCCL(ncclGroupEnd());
+  unsigned long long mm[2];
+  CK_CUDA(cudaMemcpy(mm, buf, sizeof mm, cudaMemcpyDeviceToHost));
+  if (mm[0] != mm[1]) return fail(HDP_ERR_ARG, "hdp_configure: the ranks passed different model descriptions");
   return HDP_OK;
 }
 
@@ -1218,7 +1278,7 @@ int hdp_destroy(hdp_ctx* c) {
   if (c->comm_stream) cudaStreamDestroy(c->comm_stream);
   if (c->count_host) cudaFreeHost(c->count_host);
   for (void* ptr : c->peer_open) cudaIpcCloseMemHandle(ptr);
-  if (c->gwin) cudaFree(c->gwin);
+  if (c->gwin) cudaFree(c->gwin);  // (loopback: gwin / wwin stay null, the arena holds them)
   if (c->wwin) cudaFree(c->wwin);
   if (c->fwin) cudaFree(c->fwin);
   if (c->hst) cudaFree(c->hst);
@@ -1247,6 +1307,8 @@ int hdp_configure(hdp_ctx* c, const hdp_model_desc* desc, hdp_sizes* out) {
   }
   if (d.math == HDP_MATH_FP32 && d.wire == HDP_WIRE_FP16_NCCLSUM)
     return fail(HDP_ERR_ARG, "FP32 math cannot use the fp16 NCCL-sum wire");
+  if (d.exchange < HDP_EXCH_AUTO || d.exchange > HDP_EXCH_P2P) return fail(HDP_ERR_ARG, "bad exchange mode");
+  CK(check_desc_across_ranks(c, d));
   c->d = d;
   {
     const char* ev = getenv("HDP_PERSISTENT");
@@ -1258,6 +1320,18 @@ int hdp_configure(hdp_ctx* c, const hdp_model_desc* desc, hdp_sizes* out) {
   c->gsz = c->gf32 ? 4 : 2;
   c->nslots = d.sim_workers;
   build_layout(c);
+  {
+    // NEXT-2 one-kernel exchange: fp16 gradients on the all-to-all wire, fp16 weights
+    const bool fits = !c->f32 && !c->gf32 && d.wire == HDP_WIRE_FP16_A2A &&
+                      (int)c->buckets.size() <= hdp::P2P_MAX_BUCKETS &&
+                      ((c->world >= 2 && c->world <= hdp::P2P_MAX_RANKS) ||
+                       (c->world == 1 && c->nslots >= 2 && c->nslots <= hdp::P2P_MAX_RANKS));
+    if (d.exchange == HDP_EXCH_P2P && !fits)
+      return fail(HDP_ERR_UNSUPPORTED, "HDP_EXCH_P2P needs mixed math, the fp16 all-to-all wire and 2..%d ranks "
+                  "(or simulated workers at world 1)", hdp::P2P_MAX_RANKS);
+    c->want_p2p = fits && (d.exchange == HDP_EXCH_P2P || (d.exchange == HDP_EXCH_AUTO && c->world >= 2));
+    c->loopback = c->want_p2p && c->world == 1;
+  }
   carve(c, nullptr);
   c->configured = true;
   if (out) {
@@ -1287,8 +1361,8 @@ int hdp_bind(hdp_ctx* c, void* arena, long long bytes) {
   CK_CUDA(cudaEventCreateWithFlags(&c->ev_count, cudaEventDisableTiming));
   c->ev_bucket.resize(c->buckets.size());
   for (auto& ev : c->ev_bucket) CK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
-  CK_CUDA(cudaMallocHost(&c->count_host, sizeof(int)));
-  *c->count_host = 0;
+  CK_CUDA(cudaMallocHost(&c->count_host, 2 * sizeof(int)));
+  c->count_host[0] = c->count_host[1] = 0;
   c->st.assign(c->nslots, SlotState{});
   CK(setup_p2p(c));
   CK_CUDA(cudaDeviceSynchronize());
@@ -1297,6 +1371,12 @@ int hdp_bind(hdp_ctx* c, void* arena, long long bytes) {
 }
 
 int hdp_num_blocks(const hdp_ctx* c) { return c ? (int)c->blocks.size() : 0; }
+
+int hdp_exchange_kind(const hdp_ctx* c) {
+  if (!c || !c->configured) return -1;
+  if (c->want_p2p) return c->loopback ? 3 : 2;
+  return c->world > 1 ? 1 : 0;
+}
 
 int hdp_param_block(const hdp_ctx* c, int i, hdp_block* out) {
   if (!c || !out || !c->configured || i < 0 || i >= (int)c->blocks.size()) return fail(HDP_ERR_ARG, "bad block index");
@@ -1479,6 +1559,9 @@ int hdp_set_dynamic_loss_scale(hdp_ctx* c, int growth_interval) {
   if (!c) return fail(HDP_ERR_ARG, "null context");
   if (growth_interval < 0) return fail(HDP_ERR_ARG, "growth_interval must be >= 0");
   if (!c->bound) return fail(HDP_ERR_STATE, "context not bound");
+  if (growth_interval > 0 && c->d.optimizer == HDP_OPT_ADAM)
+    return fail(HDP_ERR_UNSUPPORTED, "dynamic loss scaling with Adam: the host-side bias-correction step count "
+                "would also count skipped steps");
   CK_CUDA(cudaSetDevice(c->device));
   if ((c->dyn_interval > 0) != (growth_interval > 0)) {  // alpha source is baked into captured graphs
     for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
@@ -1577,10 +1660,15 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
     for (int sl = 0; sl < c->nslots; ++sl)
       if (!c->st[sl].bwd) return fail(HDP_ERR_STATE, "slot %d has no backward", sl);
   CK_CUDA(cudaSetDevice(c->device));
+  CK(nccl_async_check(c));
   // deferred report of the previous step's count (not synchronised then)
   if (c->count_pending) {
     CK_CUDA(cudaEventSynchronize(c->ev_count));
     c->count_pending = false;
+    if (c->count_host[1] > 0) {
+      c->poisoned = true;
+      return fail(HDP_ERR_ARG, "%d token ids outside [0, %d) in the previous step", c->count_host[1], c->d.vocab);
+    }
     if (*c->count_host > 0 && c->dyn_interval == 0) {
       c->poisoned = true;
       return fail(HDP_ERR_NONFINITE, "%d non-finite gradient values in the previous step (loss scale %g)",
@@ -1739,6 +1827,10 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
     CK_CUDA(hdp::launch_increment(c->drop_step(), cs));
   }
   CK_CUDA(cudaMemcpyAsync(c->count_host, count_src, sizeof(int), cudaMemcpyDeviceToHost, cs));
+  if (c->d.vocab > 0) {  // out-of-range token ids counted by this step's forward passes
+    CK_CUDA(cudaMemcpyAsync(c->count_host + 1, c->status + 16, sizeof(int), cudaMemcpyDeviceToHost, cs));
+    CK_CUDA(cudaMemsetAsync(c->status + 16, 0, sizeof(int), cs));
+  }
   CK_CUDA(cudaEventRecord(c->ev_count, cs));
   if (c->world > 1) {
     CK_CUDA(cudaEventRecord(c->ev_done, cs));
@@ -1747,7 +1839,12 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
   for (auto& st : c->st) st.bwd = false;
   if (nonfinite_host) {
     CK_CUDA(cudaEventSynchronize(c->ev_count));
+    CK(nccl_async_check(c));
     *nonfinite_host = *c->count_host;
+    if (c->count_host[1] > 0) {
+      c->poisoned = true;
+      return fail(HDP_ERR_ARG, "%d token ids outside [0, %d)", c->count_host[1], c->d.vocab);
+    }
     if (*c->count_host > 0 && !dyn) {
       c->poisoned = true;
       return fail(HDP_ERR_NONFINITE, "%d non-finite gradient values (loss scale %g)", *c->count_host,
@@ -1808,6 +1905,7 @@ void* hdp_debug_buffer(hdp_ctx* c, int slot, const char* name) {
   if (n == "dH0") return c->dH[0];
   if (n == "dH1") return c->dH[1];
   if (n == "Hst") return c->hst ? c->Hst(slot, 0) : nullptr;  // recurrent dropout: h~ [L][T+1][B][hp]
+  if (n == "Wcopy") return c->wcopies;                        // P2P loopback: weight copies 1..nslots-1
   return nullptr;
 }
 

@@ -47,9 +47,10 @@ cudaError_t launch_loss_scale_update(int* st, float* alpha, int interval, float 
 // x [B][T][I] (fp16 or fp32)  ->  X0 [T][B][Ip] (time-major, zero padded)
 cudaError_t launch_pack_input(const void* x, int x_f32, int B, int T, int I, int Ip, void* X0, int f32,
                               cudaStream_t s);
-// tokens [B][T] -> X0[t][b][:] = E[tok[b][t]][:]  (K10 gather)
+// tokens [B][T] -> X0[t][b][:] = E[tok[b][t]][:]  (K10 gather); a token outside
+// [0, vocab) reads row 0 and increments *bad
 cudaError_t launch_embed_gather(const int32_t* tok, int B, int T, const void* E, int Ep, void* X0, int f32,
-                                cudaStream_t s);
+                                int vocab, int* bad, cudaStream_t s);
 
 // recurrent dropout (NEXT-3, dropout.cuh): ht[b][u] = kept(seq0 + b, u) ? fp16(h * scale) : 0
 cudaError_t launch_drop_mask(const void* h, void* ht, int B, int hp, const int* step, uint32_t seed, uint32_t layer,
@@ -96,6 +97,7 @@ cudaError_t launch_colreduce3(int x_f32, const void* Z, const void* dz, long ld,
                               float* partials, int out_f32, void* dwo, void* dfb, void* dbo, cudaStream_t s);
 
 // ---------------------------------------------------------------- embedding backward (K10)
+// scratch of the library's own stable radix sort (per-tile digit histograms)
 size_t embed_sort_temp_bytes(int n);
 size_t embed_part_floats(int n, int Ep);
 // dE[v][:] = sum over positions p (ascending, p = t*B+b) with tok = v of dX0[p][:]

@@ -9,8 +9,8 @@
 //   dh = dH_above + dh_rec;  dc += dh o (1 - tanh^2 c_t)
 //   dA = [dc g i(1-i), dc c_{t-1} f(1-f), dc i (1-g^2), dh tanh(c_t) o(1-o)]
 //   dc_{t-1} = dc f
-#include <cub/device/device_radix_sort.cuh>
 #include <cuda_fp16.h>
+#include <utility>
 
 #include "dropout.cuh"
 #include "kernels.cuh"
@@ -90,13 +90,18 @@ __global__ void pack_rows_kernel(const uint4* __restrict__ x, int B, int Tn, int
 
 template <typename T>
 __global__ void embed_gather_kernel(const int32_t* __restrict__ tok, int B, int Tn, const T* __restrict__ E,
-                                    int Ep, T* __restrict__ X0) {
-  // one warp per position p = t*B + b
+                                    int Ep, T* __restrict__ X0, int vocab, int* __restrict__ bad) {
+  // one warp per position p = t*B + b; a token outside [0, vocab) reads row 0 and is
+  // counted in *bad (reported as HDP_ERR_ARG by the next hdp_grad_average_update)
   const long p = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (p >= (long)Tn * B) return;
   const int b = (int)(p % B), t = (int)(p / B);
-  const long row = tok[(long)b * Tn + t];
+  long row = tok[(long)b * Tn + t];
+  if (row < 0 || row >= vocab) {
+    if (lane == 0) atomicAdd(bad, 1);
+    row = 0;
+  }
   for (int k = lane; k < Ep; k += 32) X0[p * Ep + k] = E[row * Ep + k];
 }
 
@@ -407,12 +412,108 @@ __global__ void colreduce_pass2(const double* __restrict__ partials, int rs, int
 }
 
 // ---------------------------------------------------------------- embedding backward
-__global__ void embed_keys_kernel(const int32_t* __restrict__ tok, int B, int Tn, int32_t* keys, int32_t* vals) {
+__global__ void embed_keys_kernel(const int32_t* __restrict__ tok, int B, int Tn, int vocab, int32_t* keys,
+                                  int32_t* vals) {
   const int p = blockIdx.x * blockDim.x + threadIdx.x;
   if (p >= B * Tn) return;
   const int b = p % B, t = p / B;
-  keys[p] = tok[(long)b * Tn + t];
+  const int k = tok[(long)b * Tn + t];
+  keys[p] = (k < 0 || k >= vocab) ? 0 : k;  // as the gather did (the forward counted it)
   vals[p] = p;
+}
+
+// Stable LSD radix sort of the (token, position) pairs by token, 8-bit digits
+// (ceil(log2 vocab) / 8 passes; C3's vocab 20000 -> 2).  One pass:
+//   radix_hist_kernel    per tile of RS_TILE positions, the 256-bin digit histogram,
+//                        stored bin-major: hist[bin][tile];
+//   radix_scan_kernel    exclusive scan of hist (bin-major order = global output
+//                        offset of each (bin, tile) block);
+//   radix_scatter_kernel per tile: rank of each element among the elements of its
+//                        tile with the same digit and a smaller position (in-warp:
+//                        __match_any_sync + popc of the lower lanes; across warps:
+//                        per-warp bin counts scanned in warp order), written to
+//                        offset[bin][tile] + rank.
+// Element order inside a tile is position order, tiles are visited in order and the
+// scan is bin-major, so every pass is stable and the sort is deterministic.
+constexpr int RS_TILE = 1024;
+
+__global__ void __launch_bounds__(RS_TILE) radix_hist_kernel(const int32_t* __restrict__ keys, int n, int shift,
+                                                            int ntiles, int32_t* __restrict__ hist) {
+  __shared__ int h[256];
+  if (threadIdx.x < 256) h[threadIdx.x] = 0;
+  __syncthreads();
+  const int p = blockIdx.x * RS_TILE + threadIdx.x;
+  if (p < n) atomicAdd(&h[(keys[p] >> shift) & 255], 1);
+  __syncthreads();
+  if (threadIdx.x < 256) hist[(long)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
+}
+
+__global__ void __launch_bounds__(1024) radix_scan_kernel(int32_t* __restrict__ v, int m) {
+  __shared__ int wsum[32];
+  const int tid = threadIdx.x, per = (m + 1023) / 1024;
+  const int lo = min(m, tid * per), hi = min(m, lo + per);
+  int s = 0;
+  for (int i = lo; i < hi; ++i) s += v[i];
+  // exclusive block scan of the per-thread sums
+  const int lane = tid & 31, w = tid >> 5;
+  int x = s;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int y = __shfl_up_sync(0xffffffffu, x, o);
+    if (lane >= o) x += y;
+  }
+  if (lane == 31) wsum[w] = x;
+  __syncthreads();
+  if (w == 0) {
+    int z = wsum[lane];
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, z, o);
+      if (lane >= o) z += y;
+    }
+    wsum[lane] = z;
+  }
+  __syncthreads();
+  int run = x - s + (w > 0 ? wsum[w - 1] : 0);
+  for (int i = lo; i < hi; ++i) {
+    const int c = v[i];
+    v[i] = run;
+    run += c;
+  }
+}
+
+__global__ void __launch_bounds__(RS_TILE) radix_scatter_kernel(const int32_t* __restrict__ kin,
+                                                               const int32_t* __restrict__ vin, int n, int shift,
+                                                               int ntiles, const int32_t* __restrict__ offs,
+                                                               int32_t* __restrict__ kout,
+                                                               int32_t* __restrict__ vout) {
+  __shared__ int wc[RS_TILE / 32][256];
+  const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
+  for (int i = tid; i < (RS_TILE / 32) * 256; i += RS_TILE) (&wc[0][0])[i] = 0;
+  __syncthreads();
+  const int p = blockIdx.x * RS_TILE + tid;
+  const bool valid = p < n;
+  const int key = valid ? kin[p] : 0;
+  const int d = (key >> shift) & 255;
+  const unsigned same = __match_any_sync(0xffffffffu, valid ? d : -1);
+  const unsigned lower = (1u << lane) - 1u;
+  const int rank = __popc(same & lower);
+  if (valid && rank == 0) wc[w][d] = __popc(same);
+  __syncthreads();
+  if (tid < 256) {  // per-bin exclusive scan over the warps, in warp (= position) order
+    int run = 0;
+    for (int j = 0; j < RS_TILE / 32; ++j) {
+      const int c = wc[j][tid];
+      wc[j][tid] = run;
+      run += c;
+    }
+  }
+  __syncthreads();
+  if (valid) {
+    const int dst = offs[(long)d * ntiles + blockIdx.x] + wc[w][d] + rank;
+    kout[dst] = key;
+    vout[dst] = vin[p];
+  }
 }
 
 // Deterministic two-level segmented sum over the token-sorted positions:
@@ -570,11 +671,11 @@ cudaError_t launch_increment(int* p, cudaStream_t s) {
 }
 
 cudaError_t launch_embed_gather(const int32_t* tok, int B, int T, const void* E, int Ep, void* X0, int f32,
-                                cudaStream_t s) {
+                                int vocab, int* bad, cudaStream_t s) {
   const long warps = (long)B * T;
   const int g = (int)((warps * 32 + 255) / 256);
-  if (f32) embed_gather_kernel<float><<<g, 256, 0, s>>>(tok, B, T, (const float*)E, Ep, (float*)X0);
-  else embed_gather_kernel<__half><<<g, 256, 0, s>>>(tok, B, T, (const __half*)E, Ep, (__half*)X0);
+  if (f32) embed_gather_kernel<float><<<g, 256, 0, s>>>(tok, B, T, (const float*)E, Ep, (float*)X0, vocab, bad);
+  else embed_gather_kernel<__half><<<g, 256, 0, s>>>(tok, B, T, (const __half*)E, Ep, (__half*)X0, vocab, bad);
   return cudaGetLastError();
 }
 
@@ -674,10 +775,8 @@ cudaError_t launch_colreduce3(int x_f32, const void* Z, const void* dz, long ld,
 }
 
 size_t embed_sort_temp_bytes(int n) {
-  size_t bytes = 0;
-  cub::DeviceRadixSort::SortPairs(nullptr, bytes, (const int32_t*)nullptr, (int32_t*)nullptr,
-                                  (const int32_t*)nullptr, (int32_t*)nullptr, n);
-  return bytes;
+  const size_t ntiles = ((size_t)n + RS_TILE - 1) / RS_TILE;
+  return 256 * ntiles * sizeof(int32_t);
 }
 
 size_t embed_part_floats(int n, int Ep) { return (size_t)n * Ep; }
@@ -687,17 +786,26 @@ cudaError_t launch_embed_backward(const int32_t* tok, int B, int T, int vocab, c
                                   void* sort_temp, size_t sort_temp_bytes, float* part, void* dE, int out_f32,
                                   int32_t* range, cudaStream_t s) {
   const int n = B * T;
-  embed_keys_kernel<<<(n + 255) / 256, 256, 0, s>>>(tok, B, T, keys_in, vals_in);
+  const int ntiles = (n + RS_TILE - 1) / RS_TILE;
+  if (sort_temp_bytes < embed_sort_temp_bytes(n)) return cudaErrorInvalidValue;
+  embed_keys_kernel<<<(n + 255) / 256, 256, 0, s>>>(tok, B, T, vocab, keys_in, vals_in);
   int bits = 1;
   while ((1 << bits) < vocab) ++bits;
-  size_t tb = sort_temp_bytes;
-  cudaError_t e = cub::DeviceRadixSort::SortPairs(sort_temp, tb, keys_in, keys_out, vals_in, vals_out, n, 0, bits, s);
+  int32_t* hist = (int32_t*)sort_temp;
+  int32_t *ka = keys_in, *va = vals_in, *kb = keys_out, *vb = vals_out;
+  for (int shift = 0; shift < bits; shift += 8) {
+    radix_hist_kernel<<<ntiles, RS_TILE, 0, s>>>(ka, n, shift, ntiles, hist);
+    radix_scan_kernel<<<1, 1024, 0, s>>>(hist, 256 * ntiles);
+    radix_scatter_kernel<<<ntiles, RS_TILE, 0, s>>>(ka, va, n, shift, ntiles, hist, kb, vb);
+    std::swap(ka, kb);
+    std::swap(va, vb);
+  }
+  // (ka, va) = the sorted keys / positions
+  cudaError_t e = cudaMemsetAsync(range, 0, (size_t)2 * vocab * sizeof(int32_t), s);
   if (e != cudaSuccess) return e;
-  e = cudaMemsetAsync(range, 0, (size_t)2 * vocab * sizeof(int32_t), s);
-  if (e != cudaSuccess) return e;
-  embed_range_kernel<<<(n + 255) / 256, 256, 0, s>>>(keys_out, n, range, range + vocab);
+  embed_range_kernel<<<(n + 255) / 256, 256, 0, s>>>(ka, n, range, range + vocab);
   const long cw = ((long)n + EMB_CHUNK - 1) / EMB_CHUNK * 32;
-  embed_chunk_kernel<<<(int)((cw + 255) / 256), 256, 0, s>>>(keys_out, vals_out, n, dX0, Ep, part);
+  embed_chunk_kernel<<<(int)((cw + 255) / 256), 256, 0, s>>>(ka, va, n, dX0, Ep, part);
   const long threads = (long)vocab * ((Ep + 31) / 32) * 32;
   embed_segsum_kernel<<<(int)((threads + 255) / 256), 256, 0, s>>>(range, range + vocab, vocab, part, Ep, out_f32,
                                                                    dE);

@@ -60,15 +60,15 @@ template <int OPT>
 __global__ void __launch_bounds__(256) exch_update_kernel(const __grid_constant__ P2PArgs a) {
   __shared__ int s_nf;
   __shared__ int s_last;
-  const int N = a.N;
+  const int N = a.N, NR = a.NR;
   // ---- A: my gradients are complete (stream order: this kernel runs after the backward)
-  if (blockIdx.x == 0 && threadIdx.x < N) {
+  if (blockIdx.x == 0 && threadIdx.x < NR) {
     __threadfence_system();
     st_release_sys(a.flag_peer[threadIdx.x] + P2P_FLAG_READY + a.rank, a.step);
   }
   if (threadIdx.x == 0) {
     s_nf = 0;
-    wait_all(a.flag_local + P2P_FLAG_READY, N, a.step);
+    wait_all(a.flag_local + P2P_FLAG_READY, NR, a.step);
   }
   __syncthreads();
   // ---- B: owned 8-element vectors of every bucket (none on a skipped step)
@@ -135,17 +135,17 @@ __global__ void __launch_bounds__(256) exch_update_kernel(const __grid_constant_
   __syncthreads();
   if (threadIdx.x == 0) {
     if (s_nf)
-      for (int r = 0; r < N; ++r) atomicAdd_system(a.status_peer[r] + (a.step & 1), s_nf);
+      for (int r = 0; r < NR; ++r) atomicAdd_system(a.status_peer[r] + (a.step & 1), s_nf);
     __threadfence_system();
     const unsigned prev = atomicAdd(a.flag_local + P2P_CTR, 1u);
     s_last = prev == a.step * gridDim.x - 1;
   }
   __syncthreads();
-  if (s_last && threadIdx.x < N) {
+  if (s_last && threadIdx.x < NR) {
     __threadfence_system();
     st_release_sys(a.flag_peer[threadIdx.x] + P2P_FLAG_DONE + a.rank, a.step);
   }
-  if (s_last && threadIdx.x == 0) wait_all(a.flag_local + P2P_FLAG_DONE, N, a.step);
+  if (s_last && threadIdx.x == 0) wait_all(a.flag_local + P2P_FLAG_DONE, NR, a.step);
 }
 
 }  // namespace

@@ -15,7 +15,11 @@ constexpr int P2P_STATUS = 96;       // [2] ints: non-finite count of step s in 
 constexpr int P2P_FLAG_WORDS = 128;
 
 struct P2PArgs {
-  int N = 1, rank = 0;
+  // N = gradient contributions summed (and weight copies written); NR = ranks in the
+  // flag protocol.  Across processes N = NR = world.  Loopback (world 1, N simulated
+  // workers): the contributions are the local gradient slots, the weight copies local
+  // buffers, and the protocol runs with NR = 1.
+  int N = 1, NR = 1, rank = 0;
   unsigned step = 0;
   int nb = 0;
   long off[P2P_MAX_BUCKETS] = {}, shard[P2P_MAX_BUCKETS] = {}, moff[P2P_MAX_BUCKETS] = {};

@@ -22,10 +22,11 @@ HDP_OK, HDP_ERR_ARG, HDP_ERR_CUDA, HDP_ERR_NCCL, HDP_ERR_NONFINITE, HDP_ERR_STAT
 MATH_FP32, MATH_MIXED16 = 0, 1
 WIRE_FP16_A2A, WIRE_FP16_NCCLSUM, WIRE_FP32 = 0, 1, 2
 OPT_SGDM, OPT_ADAM = 0, 1
+EXCH_AUTO, EXCH_NCCL, EXCH_P2P = 0, 1, 2
 
 EXPORTED = [
     "hdp_nccl_unique_id", "hdp_init", "hdp_destroy", "hdp_last_error", "hdp_configure", "hdp_bind",
-    "hdp_num_blocks", "hdp_param_block", "hdp_load_params", "hdp_gather_master", "hdp_read_weights",
+    "hdp_num_blocks", "hdp_exchange_kind", "hdp_param_block", "hdp_load_params", "hdp_gather_master", "hdp_read_weights",
     "hdp_read_grads", "hdp_set_lr_schedule", "hdp_lr", "hdp_set_loss_scale", "hdp_set_l2", "hdp_set_dynamic_loss_scale", "hdp_set_recurrent_dropout",
     "hdp_loss_scale_state", "hdp_lstm_forward",
     "hdp_lstm_backward", "hdp_grad_average_update", "hdp_weights_ptr", "hdp_grads_ptr", "hdp_master_ptr",
@@ -45,7 +46,8 @@ class ModelDesc(C.Structure):
     _fields_ = [("n_layers", C.c_int), ("input_dim", C.c_int), ("hidden", C.c_int), ("fc_hidden", C.c_int),
                 ("head_last_step", C.c_int), ("vocab", C.c_int), ("embed_dim", C.c_int),
                 ("max_batch", C.c_int), ("max_seq", C.c_int), ("math", C.c_int), ("wire", C.c_int),
-                ("optimizer", C.c_int), ("sim_workers", C.c_int), ("flat_params", C.c_longlong)]
+                ("optimizer", C.c_int), ("sim_workers", C.c_int), ("flat_params", C.c_longlong),
+                ("exchange", C.c_int)]
 
 
 class Sizes(C.Structure):
@@ -73,6 +75,7 @@ def _load():
         "hdp_configure": ([vp, C.POINTER(ModelDesc), C.POINTER(Sizes)], i),
         "hdp_bind": ([vp, vp, ll], i),
         "hdp_num_blocks": ([vp], i),
+        "hdp_exchange_kind": ([vp], i),
         "hdp_param_block": ([vp, i, C.POINTER(Block)], i),
         "hdp_load_params": ([vp, vp, i], i),
         "hdp_gather_master": ([vp, vp], i),
@@ -169,6 +172,14 @@ def configure(ctx: int, desc: ModelDesc) -> Sizes:
 
 def bind(ctx: int, arena, nbytes: int):
     _ck(_lib.hdp_bind(ctx, _ptr(arena), nbytes))
+
+
+EXCHANGE_KINDS = {0: "K11 over local gradient slots", 1: "NCCL all-to-all + K11 + all-gather",
+                  2: "one-kernel NVLink exchange (peer loads/stores)", 3: "one-kernel exchange, 1-GPU loopback"}
+
+
+def exchange_kind(ctx: int) -> int:
+    return _lib.hdp_exchange_kind(ctx)
 
 
 def param_blocks(ctx: int) -> List[dict]:
@@ -300,12 +311,12 @@ def gemm_f32(A, lda, a_mn, B, ldb, b_mn, M, N, K, Cout, ldc, c_mode=0, bias=None
 
 # ------------------------------------------------------------------ convenience
 def desc_from_config(cfg, max_batch: int, math: int = MATH_MIXED16, wire: int = WIRE_FP16_A2A,
-                     optimizer: int = OPT_SGDM, sim_workers: int = 1) -> ModelDesc:
+                     optimizer: int = OPT_SGDM, sim_workers: int = 1, exchange: int = EXCH_AUTO) -> ModelDesc:
     """Build a ModelDesc from a synth.ModelConfig-like object (shape fields only)."""
     return ModelDesc(n_layers=cfg.n_layers, input_dim=cfg.input_dim, hidden=cfg.hidden, fc_hidden=cfg.fc_hidden,
                      head_last_step=int(cfg.head_last_step), vocab=cfg.vocab, embed_dim=cfg.embed_dim,
                      max_batch=max_batch, max_seq=cfg.seq, math=math, wire=wire, optimizer=optimizer,
-                     sim_workers=sim_workers, flat_params=0)
+                     sim_workers=sim_workers, flat_params=0, exchange=exchange)
 
 
 class Trainer:

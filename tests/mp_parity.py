@@ -36,6 +36,7 @@ def main():
     dyn = int(os.environ.get("HDP_MP_DYN", "0"))           # NEXT-3 dynamic loss scale interval (Q14b)
     lam0 = float(os.environ.get("HDP_MP_LAMBDA0", "0"))
     keep = float(os.environ.get("HDP_MP_KEEP", "1"))       # NEXT-3 recurrent dropout (Q16b)
+    exch = int(os.environ.get("HDP_MP_EXCH", "0"))         # hdp.EXCH_* (0 auto = NVLink kernel for fp16 a2a)
     cfg = synth.CONFIGS[cfg_name]
     if seq:
         cfg = cfg.with_(seq=seq)
@@ -45,7 +46,8 @@ def main():
     B = gb // world
     obj = [hdp.nccl_unique_id() if rank == 0 else None]
     dist.broadcast_object_list(obj, src=0)
-    desc = hdp.desc_from_config(cfg, B, hdp.MATH_MIXED16 if mixed else hdp.MATH_FP32, wire, hdp.OPT_SGDM, 1)
+    desc = hdp.desc_from_config(cfg, B, hdp.MATH_MIXED16 if mixed else hdp.MATH_FP32, wire, hdp.OPT_SGDM, 1,
+                                exchange=exch)
     params = synth.init_params(cfg)
     tr = hdp.Trainer(desc, params if rank == 0 else None, lambda0=cfg.lambda0, alpha=alpha, gamma=cfg.gamma,
                      n_half=cfg.n_half, momentum=cfg.momentum, world=world, rank=rank, uid=obj[0], device=local,
@@ -61,6 +63,7 @@ def main():
     stream = torch.cuda.current_stream(dev)
     recs = []
     master_ref = params.astype(np.float64)
+    master_prev = params.astype(np.float64)
     state = {"H": np.zeros(n)}
     from oracle import schedule as osched
     from oracle import step as ostep
@@ -73,6 +76,10 @@ def main():
         ts = torch.from_numpy(np.ascontiguousarray(t[rank * B:(rank + 1) * B])).to(dev)
         hdp.lstm_forward(tr.ctx, xs, ts, B, cfg.seq, 0, None, tr.loss[0:1], stream)
         hdp.lstm_backward(tr.ctx, 0, stream)
+        torch.cuda.synchronize()
+        g_mine = hdp.read_grads(tr.ctx, 0, n)           # this rank's fp16 gradients (carry alpha)
+        g_all = [None] * world
+        dist.all_gather_object(g_all, g_mine)
         nf = hdp.grad_average_update(tr.ctx, 0, stream, sync=True)
         torch.cuda.synchronize()
         loss = torch.tensor([tr.loss.item()], device=dev)
@@ -92,7 +99,16 @@ def main():
             recs.append({"step": k, "loss_gpu": loss.item() / world, "loss_ref": ref["loss"], "nonfinite": nf,
                          "skip_gpu": bool(dyn and nf > 0), "skip_ref": bool(skip_ref), "alpha_ref": a_ref,
                          "weights_identical": len(set(hs)) == 1,
-                         "master_err": block_errors(cfg, master.astype(np.float64), ref["master"])})
+                         "exchange_kind": hdp.exchange_kind(tr.ctx),
+                         "master_sha": hashlib.sha256(master.tobytes()).hexdigest(),
+                         "master_err": block_errors(cfg, master.astype(np.float64), ref["master"]),
+                         # the step's update: (master_k - master_{k-1}) on both sides (not vacuous at small lambda)
+                         "dmaster_err": block_errors(cfg, master.astype(np.float64) - master_prev,
+                                                     ref["master"] - master_ref),
+                         # every rank's own gradients against the oracle's worker r (R-cond metric)
+                         "grad_err": [block_errors(cfg, g_all[r].astype(np.float64), ref["grads"][r],
+                                                   ref["abs_terms"][r]) for r in range(world)]})
+            master_prev = master.astype(np.float64)
             master_ref, state = ref["master"], ref["state"]
     if dyn and rank == 0 and recs:
         recs[-1]["alpha_gpu"] = hdp.loss_scale_state(tr.ctx)[0]

@@ -34,9 +34,24 @@ def block_errors(cfg, got: np.ndarray, ref: np.ndarray, abs_terms: dict = None) 
     return out
 
 
+def _copy_dev(dst, src_ptr: int, nbytes: int):
+    """Device-to-device copy from a raw library pointer into a torch tensor."""
+    import ctypes
+    import torch
+    if not hasattr(_copy_dev, "rt"):
+        _copy_dev.rt = ctypes.CDLL("libcudart.so.12")   # the runtime torch loaded
+    cudart = _copy_dev.rt
+    torch.cuda.synchronize()
+    rc = cudart.cudaMemcpy(ctypes.c_void_p(dst.data_ptr()), ctypes.c_void_p(src_ptr), ctypes.c_size_t(nbytes), 3)
+    assert rc == 0, rc
+
+
 def run_parity(cfg, global_batch: int, n_workers: int, steps: int, mixed: bool, lambda0=None, alpha=None,
-               optimizer="sgdm", seed=synth.DATA_SEED, epochs=None, compare_grads=True, l2=0.0, dropout=None):
-    """Returns a list of per-step records with GPU-vs-oracle errors."""
+               optimizer="sgdm", seed=synth.DATA_SEED, epochs=None, compare_grads=True, l2=0.0, dropout=None,
+               exchange=0, keep_state=False):
+    """Returns a list of per-step records with GPU-vs-oracle errors.
+    exchange: hdp.EXCH_* (EXCH_P2P at 1 GPU = the NVLink kernel's loopback).
+    keep_state: also return the GPU master / weights of every step (bit comparisons)."""
     import torch
 
     from paper_1912_00286_b200 import hdp
@@ -47,7 +62,7 @@ def run_parity(cfg, global_batch: int, n_workers: int, steps: int, mixed: bool, 
     B = global_batch // n_workers
     desc = hdp.desc_from_config(cfg, B, hdp.MATH_MIXED16 if mixed else hdp.MATH_FP32,
                                 hdp.WIRE_FP16_A2A, hdp.OPT_SGDM if optimizer == "sgdm" else hdp.OPT_ADAM,
-                                sim_workers=n_workers)
+                                sim_workers=n_workers, exchange=exchange)
     params = synth.init_params(cfg)
     tr = hdp.Trainer(desc, params, lambda0=lambda0, alpha=alpha, gamma=cfg.gamma, n_half=cfg.n_half,
                      momentum=cfg.momentum, l2=l2)
@@ -98,6 +113,16 @@ def run_parity(cfg, global_batch: int, n_workers: int, steps: int, mixed: bool, 
                 "w_matches_master": bool(np.array_equal(
                     gpu_w, gpu_master.astype(np.float16).astype(np.float32) if mixed else gpu_master)),
             }
+            if keep_state:
+                rec["gpu_master"], rec["gpu_w"] = gpu_master, gpu_w
+                if exchange == hdp.EXCH_P2P and n_workers > 1:
+                    P = tr.sizes.n_params_padded
+                    wc = torch.empty((n_workers - 1) * P, dtype=torch.float16, device=dev)
+                    _copy_dev(wc, hdp.debug_buffer(tr.ctx, 0, "Wcopy"), wc.numel() * 2)
+                    wbase = torch.empty(P, dtype=torch.float16, device=dev)
+                    _copy_dev(wbase, hdp.weights_ptr(tr.ctx), P * 2)
+                    rec["copies_equal"] = bool(all(torch.equal(wc[i * P:(i + 1) * P], wbase)
+                                                   for i in range(n_workers - 1)))
             if compare_grads:
                 rec["grad_err"] = [block_errors(cfg, gpu_grads[r].astype(np.float64), ref["grads"][r],
                                                 ref["abs_terms"][r]) for r in range(n_workers)]
@@ -108,4 +133,25 @@ def run_parity(cfg, global_batch: int, n_workers: int, steps: int, mixed: bool, 
             master, state = ref["master"], ref["state"]
     finally:
         tr.close()
+    _log_errors(recs)
     return recs
+
+
+def _log_errors(recs):
+    """Observed errors of a parity run, appended to gpurun_out/parity_errors.jsonl
+    with the current test's name (evidence for the tolerances; not an assertion)."""
+    import json
+    import os
+    if not recs:
+        return
+    mx = lambda d: max(d.values())  # noqa: E731
+    row = {"case": os.environ.get("PYTEST_CURRENT_TEST", "?").split(" ")[0], "steps": len(recs),
+           "max_grad_err": max((mx(g) for r in recs for g in r.get("grad_err", [])), default=None),
+           "max_grad_err_plain": max((mx(g) for r in recs for g in r.get("grad_err_plain", [])), default=None),
+           "max_master_err": max(mx(r["master_err"]) for r in recs),
+           "max_dmaster_err": max(mx(r["dmaster_err"]) for r in recs),
+           "max_loss_diff": max(abs(r["loss_gpu"] - r["loss_ref"]) for r in recs)}
+    d = os.path.join(os.path.dirname(os.path.dirname(os.path.abspath(__file__))), "gpurun_out")
+    os.makedirs(d, exist_ok=True)
+    with open(os.path.join(d, "parity_errors.jsonl"), "a") as f:
+        f.write(json.dumps(row) + "\n")

@@ -31,26 +31,50 @@ def _world():
     return 4 if n >= 4 else 2
 
 
-@pytest.mark.parametrize("mixed,wire", [(1, 0), (0, 0), (1, 1), (1, 2)])
-def test_c1_multi_gpu_parity(mixed, wire):
+@pytest.mark.parametrize("mixed,wire,exch", [(1, 0, 0), (1, 0, 1), (0, 0, 0), (1, 1, 0), (1, 2, 0)])
+def test_c1_multi_gpu_parity(mixed, wire, exch):
+    """Every rank's gradients, the step's update and the weights against the oracle's
+    N-worker step, stress rate (lambda0 = 0.05, n = inf) so the update is not lost in
+    the weights' magnitude.  Mixed fp16 all-to-all: the NVLink kernel (exch 0 = auto)
+    and the NCCL path (exch 1)."""
     world = _world()
     recs = _run(world, {"HDP_MP_CFG": "C1", "HDP_MP_MIXED": str(mixed), "HDP_MP_WIRE": str(wire),
-                        "HDP_MP_GB": str(2 * world), "HDP_MP_STEPS": "3"})
+                        "HDP_MP_GB": str(2 * world), "HDP_MP_STEPS": "3", "HDP_MP_LAMBDA0": "0.05",
+                        "HDP_MP_EXCH": str(exch)})
     tol = 2e-2 if mixed else 1e-5
     for r in recs:
         assert r["weights_identical"], r
         assert r["nonfinite"] == 0
+        assert r["exchange_kind"] == (2 if (mixed and wire == 0 and exch == 0) else 1)
         assert abs(r["loss_gpu"] - r["loss_ref"]) <= (1e-2 if mixed else 1e-5) * max(1, abs(r["loss_ref"]))
         assert max(r["master_err"].values()) <= tol, r["master_err"]
+        assert max(r["dmaster_err"].values()) <= (5e-2 if mixed else 1e-4), r["dmaster_err"]
+        for ge in r["grad_err"]:
+            assert max(ge.values()) <= (2e-2 if mixed else 1e-5), ge
+
+
+def test_c1_multi_gpu_exchanges_bit_identical():
+    """The one-kernel NVLink exchange and the NCCL all-to-all + K11 + all-gather path
+    compute the same rank-ordered fp32 sum and update: bit-identical masters."""
+    world = _world()
+    env = {"HDP_MP_CFG": "C1", "HDP_MP_MIXED": "1", "HDP_MP_WIRE": "0", "HDP_MP_GB": str(2 * world),
+           "HDP_MP_STEPS": "3", "HDP_MP_LAMBDA0": "0.05"}
+    a = _run(world, dict(env, HDP_MP_EXCH="2"))
+    b = _run(world, dict(env, HDP_MP_EXCH="1"))
+    assert [r["exchange_kind"] for r in a] == [2] * 3 and [r["exchange_kind"] for r in b] == [1] * 3
+    assert [r["master_sha"] for r in a] == [r["master_sha"] for r in b]
 
 
 def test_c3_multi_gpu_parity_reduced():
     world = _world()
     recs = _run(world, {"HDP_MP_CFG": "C3", "HDP_MP_MIXED": "1", "HDP_MP_WIRE": "0", "HDP_MP_GB": str(4 * world),
-                        "HDP_MP_SEQ": "32", "HDP_MP_STEPS": "2"})
+                        "HDP_MP_SEQ": "32", "HDP_MP_STEPS": "2", "HDP_MP_LAMBDA0": "0.05"})
     for r in recs:
         assert r["weights_identical"]
         assert max(r["master_err"].values()) <= 2e-2, r["master_err"]
+        assert max(r["dmaster_err"].values()) <= 5e-2, r["dmaster_err"]
+        for ge in r["grad_err"]:
+            assert max(ge.values()) <= 2e-2, ge
 
 
 def test_c1_multi_gpu_l2_and_dynamic_loss_scale():

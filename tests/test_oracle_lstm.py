@@ -101,13 +101,13 @@ def test_hinge_examples():
 
 # ------------------------------------------------------- torch.nn.LSTM special case
 
-def _torch_reference(cfg, flat, x, t, alpha):
+def _torch_reference(cfg, flat, x, t, alpha, dtype=torch.float64):
     """Independent library computation: torch.nn.LSTM (gate order i,f,g,o,
     bias_hh = 0) + head + alpha*mean hinge, autograd for the gradients."""
-    P = {k: torch.tensor(v, dtype=torch.float64) for k, v in lstm.unpack(cfg, flat).items()}
+    P = {k: torch.tensor(v, dtype=dtype) for k, v in lstm.unpack(cfg, flat).items()}
     h = cfg.hidden
     in0 = cfg.embed_dim if cfg.vocab else cfg.input_dim
-    net = torch.nn.LSTM(in0, h, num_layers=cfg.n_layers, batch_first=True, dtype=torch.float64)
+    net = torch.nn.LSTM(in0, h, num_layers=cfg.n_layers, batch_first=True, dtype=dtype)
     leaf = {}
     with torch.no_grad():
         for l in range(cfg.n_layers):
@@ -121,7 +121,7 @@ def _torch_reference(cfg, flat, x, t, alpha):
     if cfg.vocab:
         inp = leaf["E"][torch.tensor(x, dtype=torch.long)]
     else:
-        inp = torch.tensor(x, dtype=torch.float64)
+        inp = torch.tensor(x, dtype=dtype)
     out, _ = net(inp)                                  # [B][T][h]
     if cfg.fc_hidden:
         z = torch.relu(out @ leaf["F"].T + leaf["fb"])
@@ -130,17 +130,17 @@ def _torch_reference(cfg, flat, x, t, alpha):
         y = out[:, -1] @ leaf["wo"] + leaf["bo"][0]    # [B]
     else:
         y = out @ leaf["wo"] + leaf["bo"][0]
-    tt = torch.tensor(t, dtype=torch.float64)
+    tt = torch.tensor(t, dtype=dtype)
     L = alpha * torch.clamp(1.0 - tt * y, min=0.0).mean()
     L.backward()
     grads = {}
     for l in range(cfg.n_layers):
-        grads[f"W{l}"] = getattr(net, f"weight_ih_l{l}").grad.numpy()
-        grads[f"U{l}"] = getattr(net, f"weight_hh_l{l}").grad.numpy()
-        grads[f"b{l}"] = getattr(net, f"bias_ih_l{l}").grad.numpy()
+        grads[f"W{l}"] = getattr(net, f"weight_ih_l{l}").grad.double().numpy()
+        grads[f"U{l}"] = getattr(net, f"weight_hh_l{l}").grad.double().numpy()
+        grads[f"b{l}"] = getattr(net, f"bias_ih_l{l}").grad.double().numpy()
     for k, v in leaf.items():
-        grads[k] = v.grad.numpy()
-    yy = y.detach().numpy()
+        grads[k] = v.grad.double().numpy()
+    yy = y.detach().double().numpy()
     return L.item(), (yy if cfg.head_last_step else yy.T), grads
 
 
@@ -370,3 +370,42 @@ def test_l2_inactive_hinge_is_weight_decay_closed_form():
     assert np.array_equal(out["avg"], 2 * l2 * w)
     assert np.allclose(out["state"]["H"], -lam * 2 * l2 * w, rtol=1e-7, atol=0)
     assert np.allclose(out["master"], w * (1 - 2 * lam * l2), rtol=1e-7, atol=0)
+
+
+# ------------------------------------------- reading R-cond: float32 evidence
+
+def test_rcond_float32_evidence():
+    """DESIGN.md reading R-cond: the bias-type gradients are sums of B*T
+    back-propagated terms that cancel at these shapes, so the plain relative
+    metric max|err| / max|ref| <= 1e-5 is out of reach of ANY float32
+    evaluation, not only of the kernels.  Evidence from an independent float32
+    implementation (torch.nn.LSTM float32 + autograd on the CPU) on the input
+    of the GPU test ``test_c3_imdb_reduced_fp32`` (C3, T = 24, global batch 8,
+    2 workers, step 1): the plain metric exceeds 1e-5 on a bias block, while
+    with the R-cond denominator max(max|ref|, max_j sum_i |term_ij|) -- the
+    scale of the Higham bound of a float32 sum -- every block is far below
+    1e-5, and the non-bias blocks meet the plain metric."""
+    from oracle import schedule as osched
+    from parity import block_errors
+    cfg = synth.CONFIGS["C3"].with_(seq=24)
+    params = synth.init_params(cfg)
+    N, Bg = 2, 8
+    lam = float(np.float32(osched.rate_for_epoch(cfg.lambda0, N, cfg.n_half, cfg.gamma, 0)))
+    x0, t0 = synth.model_batch(cfg, Bg, synth.DATA_SEED)
+    ref0 = step.train_step(cfg, params.astype(np.float64), {"H": np.zeros(params.size)}, x0, t0, N, 10.0, lam,
+                           "fp32")
+    x1, t1 = synth.model_batch(cfg, Bg, synth.DATA_SEED + 1)
+    ref1 = step.train_step(cfg, ref0["master"], ref0["state"], x1, t1, N, 10.0, lam, "fp32")
+    worst_plain_bias = 0.0
+    for r in range(N):
+        sl = slice(r * Bg // N, (r + 1) * Bg // N)
+        _, _, g32 = _torch_reference(cfg, ref0["master"], x1[sl], t1[sl], 10.0, dtype=torch.float32)
+        flat = lstm.pack(cfg, g32)
+        plain = block_errors(cfg, flat, ref1["grads"][r])
+        cond = block_errors(cfg, flat, ref1["grads"][r], ref1["abs_terms"][r])
+        assert max(cond.values()) <= 1e-6, cond
+        for k in plain:
+            if k not in ("b0", "b1"):
+                assert plain[k] <= 1e-5, (k, plain)
+        worst_plain_bias = max(worst_plain_bias, plain["b0"], plain["b1"])
+    assert worst_plain_bias > 1e-5, worst_plain_bias

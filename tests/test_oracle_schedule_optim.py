@@ -106,6 +106,41 @@ def test_adam_first_step_closed_form():
     assert np.allclose(W1, ref, rtol=1e-6, atol=0)
 
 
+def test_adam_constant_gradient_closed_form():
+    # a constant gradient g makes the bias-corrected moments exact at every step:
+    # m_k = (1 - b1^k) g and v_k = (1 - b2^k) g^2 (geometric sums of the recurrences),
+    # so mhat = g, vhat = g^2 and W_k = W_0 - k * lambda * g / (|g| + eps) for k = 1..5.
+    # A wrong decay (e.g. (1 - b1) * m instead of b1 * m) breaks this from k = 2 on.
+    rng = np.random.default_rng(7)
+    g = rng.choice([-1.0, 1.0], 64) * rng.uniform(0.5, 2.0, 64)
+    W, m1, v = np.zeros(64), np.zeros(64), np.zeros(64)
+    lam, eps = 1e-3, 1e-8
+    for k in range(1, 6):
+        W, m1, v = optim.adam(W, m1, v, g, lam=lam, k=k, eps=eps)
+        assert np.allclose(m1, (1 - 0.9 ** k) * g, rtol=1e-6, atol=0), k
+        assert np.allclose(v, (1 - 0.999 ** k) * g * g, rtol=1e-6, atol=0), k
+        assert np.allclose(W, -k * lam * g / (np.abs(g) + eps), rtol=1e-6, atol=0), k
+
+
+def test_adam_impulse_closed_form():
+    # g_1 = g, then g_k = 0: m_k = b1^(k-1) (1 - b1) g, v_k = b2^(k-1) (1 - b2) g^2, so
+    #   mhat_k = b1^(k-1) (1 - b1) / (1 - b1^k) * g,  sqrt(vhat_k) = sqrt(b2^(k-1) (1 - b2) / (1 - b2^k)) |g|
+    # and (eps negligible against |g| = 1) the k-th step moves W by
+    #   -lambda sign(g) * [b1^(k-1)(1-b1)/(1-b1^k)] / sqrt(b2^(k-1)(1-b2)/(1-b2^k)).
+    # Hand values for b1 = 0.9, b2 = 0.999: k = 2: (0.09/0.19) / sqrt(0.000999/0.001999)
+    #   = 0.4736842 / 0.7069298 = 0.6700583; k = 3: (0.081/0.271) / sqrt(0.000998001/0.002997001)
+    #   = 0.2988930 / 0.5770614 = 0.5179570
+    lam = 1e-2
+    W, m1, v = np.zeros(2), np.zeros(2), np.zeros(2)
+    g = np.array([1.0, -1.0])
+    W1, m1, v = optim.adam(W, m1, v, g, lam=lam, k=1)
+    assert np.allclose(W1, -lam * g, rtol=1e-6)
+    W2, m1, v = optim.adam(W1, m1, v, np.zeros(2), lam=lam, k=2)
+    assert np.allclose(W2 - W1, -lam * 0.6700583 * g, rtol=2e-6)
+    W3, m1, v = optim.adam(W2, m1, v, np.zeros(2), lam=lam, k=3)
+    assert np.allclose(W3 - W2, -lam * 0.5179570 * g, rtol=2e-6)
+
+
 def test_adam_f32_emulation_vs_fp64():
     rng = np.random.default_rng(6)
     n, N, alpha = 5000, 2, 10.0
@@ -176,3 +211,23 @@ def test_skipped_step_leaves_state_unchanged():
     assert np.array_equal(out["master"], w) and np.array_equal(out["state"]["H"], H)
     ok = step.train_step(cfg, w, {"H": H}, x, t, 1, 10.0, 0.1, "mixed", skip_nonfinite=True)
     assert ok["nonfinite"] == 0 and not np.array_equal(ok["master"], w)
+
+
+def test_library_lr_matches_golden(golden):
+    """hdp_lr (include/hdp.h) on a host-only context (device -1: no CUDA) reproduces
+    every row of the golden schedule, the clip rows included.  N is
+    the context's world size (flat model, one worker per rank)."""
+    import ctypes
+    from paper_1912_00286_b200 import hdp
+    L = hdp.lib()
+    for lam0, N, n, gamma, e, expected in golden("lr_schedule.txt"):
+        h = ctypes.c_void_p()
+        assert L.hdp_init(int(N), 0, None, -1, ctypes.byref(h)) == 0
+        try:
+            desc = hdp.ModelDesc(n_layers=0, sim_workers=1, flat_params=4096)
+            hdp.configure(h.value, desc)
+            hdp.set_lr_schedule(h.value, float(lam0), float(gamma), float(n))
+            assert hdp.lr(h.value, int(e)) == pytest.approx(float(expected), rel=1e-15, abs=0), (lam0, N, n, gamma, e)
+            assert hdp.lr(h.value, -1) < 0
+        finally:
+            hdp.destroy(h.value)
