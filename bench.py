@@ -410,17 +410,27 @@ def run_c5(args, rank, world, local_rank):
             hdp.grad_average_update(ctx, 0, stream)
         hdp.lib().hdp_profile_read(ctx, ms_by, n_by, 1)
         hdp.lib().hdp_profile(ctx, 0)
-        k11_ms = ms_by[11] / max(1, n_by[11]) * (n_by[11] / 3.0)     # per step
+        kind = hdp.exchange_kind(ctx)
+        k11_ms = ms_by[11] / 3.0                       # per step (K11, or the one-kernel exchange)
         k11_launch_ms = ms_by[11] / max(1, n_by[11])
-        comm_ms = ms_by[12] / 3.0
+        comm_ms = ms_by[12] / 3.0                      # NCCL collectives (0 on the one-kernel path)
         own = P // world
         nsrc = world if (world > 1 and wire != hdp.WIRE_FP16_NCCLSUM and wire != hdp.WIRE_FP32) else (1 if world > 1 else nsim)
+        if kind == 2:
+            nsrc = world
+        # HBM bytes of the update arithmetic per rank (contributions + W, H read/write + fp16 w)
         k11_bytes = own * (nsrc * gsz + 18)
-        wire_bytes = 2 * (world - 1) / world * P * gsz if world > 1 else 0
-        rows.append({"mib": mib, "elements": P, "step_ms": ms, "k11_ms": k11_ms, "comm_ms": comm_ms,
-                     "k11_gbs": k11_bytes / (k11_ms * 1e-3) / 1e9,
+        # NVLink bytes per rank per direction: the owned shard's contributions from the N-1
+        # peers (gradient wire) + the N-1 peers' fp16 weight shards (all-gather / peer stores)
+        nvl_bytes = (world - 1) / world * P * (gsz + 2) if world > 1 else 0
+        xch_ms = k11_ms if kind == 2 else comm_ms     # the time the NVLink traffic has to fit in
+        rows.append({"mib": mib, "elements": P, "step_ms": ms, "exchange": hdp.EXCHANGE_KINDS.get(kind, "?"),
+                     "k11_ms": k11_ms, "comm_ms": comm_ms,
+                     "k11_gbs": k11_bytes / (k11_ms * 1e-3) / 1e9 if kind != 2 else None,
                      "k11_launch_us": k11_launch_ms * 1e3, "k11_bytes": k11_bytes,
-                     "busbw_gbs": (wire_bytes / (comm_ms * 1e-3) / 1e9) if world > 1 and comm_ms > 0 else None})
+                     "nvlink_bytes_per_direction": nvl_bytes,
+                     "busbw_gbs": (nvl_bytes / (xch_ms * 1e-3) / 1e9) if world > 1 and xch_ms > 0 else None,
+                     "busbw_step_gbs": (nvl_bytes / (ms * 1e-3) / 1e9) if world > 1 else None})
         hdp.destroy(ctx)
         del arena
         torch.cuda.synchronize(dev)
@@ -429,18 +439,32 @@ def run_c5(args, rank, world, local_rank):
         return None
     pk = peaks()
     big = rows[-1]
-    return {"metric": METRIC, "value": big["k11_gbs"], "unit": "GB/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": big["step_ms"], "higher_is_better": True, "scaling": "weak",
-            "vs_baseline": None, "dtype": "f32 (fp16 wire)" if gsz == 2 else "f32",
-            "data": "synthetic gradients N(0, 0.05^2)",
-            "config": {"workload": "C5-avg-update", "sizes_mib": sizes_mib, "wire": args.wire,
-                       "contributions": nsim if world == 1 else world, "parallelism": f"dp{world}",
-                       "l2_cache": "flushed between timed steps"},
-            "roofline": {"bound": "hbm", "achieved": big["k11_gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
-                         "frac": big["k11_gbs"] / pk["hbm_gbs"], "traffic": None, "kernel": "update(K11)",
-                         "peak_src": pk["src"], "avg_launch_us": big["k11_launch_us"], "per_launch": big["k11_bytes"],
-                         "per_launch_unit": "byte"},
-            "sweep": rows, "clocks": clocks, "gpu_launches": None}
+    out = {"metric": METRIC, "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": big["step_ms"], "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+           "dtype": "f32 (fp16 wire)" if gsz == 2 else "f32 (fp32 wire)", "data": "synthetic gradients N(0, 0.05^2)",
+           "config": {"workload": "C5-avg-update", "sizes_mib": sizes_mib, "wire": args.wire,
+                      "contributions": nsim if world == 1 else world, "parallelism": f"dp{world}",
+                      "exchange": big["exchange"], "l2_cache": "flushed between timed steps"},
+           "sweep": rows, "clocks": clocks, "gpu_launches": None}
+    if world == 1:
+        # one GPU: the fused average + update is HBM-bound (the metric's "avg+update GB/s vs HBM peak")
+        out.update({"value": big["k11_gbs"], "unit": "GB/s",
+                    "roofline": {"bound": "hbm", "achieved": big["k11_gbs"], "peak": pk["hbm_gbs"], "unit": "GB/s",
+                                 "frac": big["k11_gbs"] / pk["hbm_gbs"], "traffic": None, "kernel": "update(K11)",
+                                 "peak_src": pk["src"], "avg_launch_us": big["k11_launch_us"],
+                                 "per_launch": big["k11_bytes"], "per_launch_unit": "byte"}})
+    else:
+        # N GPUs: what binds is NVLink -- bytes per rank per direction over the exchange time,
+        # against the measured peer-copy rate (B200_PROFILING.md: 770 GB/s; 900 nominal)
+        bw = big["busbw_gbs"]
+        out.update({"value": bw, "unit": "GB/s (NVLink per GPU per direction)",
+                    "roofline": {"bound": "nvlink", "achieved": bw, "peak": 770.0, "unit": "GB/s",
+                                 "frac": bw / 770.0 if bw else None, "traffic": None,
+                                 "kernel": "exch_update" if "kernel" in big["exchange"] else "nccl",
+                                 "peak_src": "measured peer copy per direction (B200_PROFILING.md), 900 nominal",
+                                 "per_launch": big["nvlink_bytes_per_direction"], "per_launch_unit": "byte",
+                                 "frac_of_nominal_900": bw / 900.0 if bw else None}})
+    return out
 
 
 def host_cpu():

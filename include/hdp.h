@@ -255,6 +255,30 @@ int hdp_lstm_backward(hdp_ctx* ctx, int slot, void* stream);
  * until hdp_load_params).  HDP_ERR_STATE if a slot has no backward.      */
 int hdp_grad_average_update(hdp_ctx* ctx, int epoch, void* stream, int* nonfinite_host);
 
+/* Runtime options by name.
+ * Context-scoped (ctx required, bound):
+ *   "partial_fraction" f in (0, 1] -- NEXT-2 partial collection ("collecting
+ *        a fraction of gradients (normally at 90-95%) before proceeding to averaging";
+ *        SPEC.md:320-328): the exchange proceeds once q = ceil(f*N) of the N contributors'
+ *        gradients are ready (rank 0 decides and publishes the set), averages exactly
+ *        those -- fp32 rank-ordered sum times fp32(1/(count*alpha)) -- and discards the
+ *        late ones for that step.  f = 1 (default) is the lock-step of :94.  Needs the
+ *        one-kernel exchange (hdp_exchange_kind 2 or 3) and a static alpha, else
+ *        HDP_ERR_UNSUPPORTED.  hdp_partial_state reads the last decision.
+ *   "straggler_mask" (bits of contributor ids), "straggler_us" -- test injection: those
+ *        contributors publish their readiness that much later (exercises the above).
+ * Process-wide kernel selection (ctx may be NULL; kernels of graphs captured before the
+ * call are kept -- a ctx passed here has its graphs dropped): "persistent",
+ *   "wavefront", "wavefront_fusex", "wavefront_wgrad", "wavefront_tmem", "recur_nbg",
+ *   "recur_cluster", "gemm_cta_group", "gemm_cluster_n", "pdl", "k7_bn", "k7_splits",
+ *   "recur_trace" (integers; see csrc/options.h).  They choose between implementations
+ *   of the same arithmetic (ablations, tuning); the defaults are the measured best.
+ * Errors: unknown name, value out of range -> HDP_ERR_ARG.                      */
+int hdp_set_option(hdp_ctx* ctx, const char* name, double value);
+/* The last partial-collection decision (synchronises): bit r of *mask set if
+ * contributor r's gradients were averaged; *count = their number.             */
+int hdp_partial_state(hdp_ctx* ctx, unsigned* mask, int* count);
+
 /* Live profiler.  Kernel classes: */
 enum { HDP_K_INPUT = 0,     /* input packing / embedding gather (A1 prologue, K10) */
        HDP_K_GEMM_X = 1,    /* K1  input projection X W^T + b (A1)                 */

@@ -38,6 +38,22 @@ def average(grads, N: int, alpha: float) -> np.ndarray:
     return s / (N * alpha)
 
 
+def quorum(fraction: float, N: int) -> int:
+    """Partial collection ("collecting a fraction of gradients (normally at
+    90-95%) before proceeding to averaging"): proceed once ceil(f*N)
+    contributions have arrived."""
+    assert 0.0 < fraction <= 1.0
+    return max(1, min(N, int(np.ceil(fraction * N - 1e-9))))
+
+
+def partial_average(grads, contributors, alpha: float) -> np.ndarray:
+    """float64: the average over the contributors that arrived ("returns
+    their sum and the count so the caller averages by the actual contributor count;
+    late arrivals are discarded for this step"): sum_{r in S} g_r / (|S| * alpha)."""
+    S = sorted(contributors)
+    return average([grads[r] for r in S], len(S), alpha)
+
+
 def sgdm(W, H, dW, lam: float, m: float):
     """Eqs. 1-2 with fp32 state (r32)."""
     H = r32(m * H - lam * dW)

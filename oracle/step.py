@@ -11,6 +11,10 @@ The global batch is split contiguously: worker r gets rows
 [r*B/N, (r+1)*B/N).  The learning rate is passed in (``schedule``
 computes it); the oracle does not decide N-dependence itself.
 
+Partial collection: ``contributors`` lists the
+workers whose gradients arrived in time; the step averages exactly those
+(``optim.partial_average``) and discards the rest.
+
 L2 regularisation ("application of L2 regularization"; SPEC.md:171
 "loss = alpha*mean hinge + alpha*l2*||W||^2"; reading Q16 in DESIGN.md): the
 penalty l2 * sum(w^2) runs over every parameter w of the working weights used
@@ -46,7 +50,7 @@ def train_step(cfg, master, state: Dict[str, np.ndarray], x_global, t_global, N:
                alpha: float, lam: float, mode: str, optimizer: str = "sgdm",
                momentum: float = 0.9, adam_k: int = 1,
                grads_override: Optional[list] = None, l2: float = 0.0, skip_nonfinite: bool = False,
-               dropout: Optional[dict] = None):
+               dropout: Optional[dict] = None, contributors: Optional[list] = None):
     """Returns a dict with loss (unscaled mean over workers), per-worker
     gradients (carrying alpha), the averaged gradient, new master/state,
     the fp16 working copy and the non-finite count."""
@@ -71,8 +75,12 @@ def train_step(cfg, master, state: Dict[str, np.ndarray], x_global, t_global, N:
         abs_terms.append(at)
     if grads_override is not None:
         grads = grads_override
-    nonfinite = sum(count_nonfinite(g) for g in grads)
-    avg = optim.average(grads, N, alpha)
+    if contributors is None:
+        nonfinite = sum(count_nonfinite(g) for g in grads)
+        avg = optim.average(grads, N, alpha)
+    else:  # partial collection: only the contributors that arrived are averaged
+        nonfinite = sum(count_nonfinite(grads[r]) for r in contributors)
+        avg = optim.partial_average(grads, contributors, alpha)
     if l2:
         avg = avg + 2.0 * l2 * w
     if skip_nonfinite and nonfinite:

@@ -16,6 +16,7 @@
 
 #include "dropout.cuh"
 #include "gemm.cuh"
+#include "options.h"
 #include "ptx.cuh"
 
 namespace hdp {
@@ -730,16 +731,10 @@ int num_sms() {
   return n;
 }
 
-// programmatic dependent launch of the GEMM / split-K kernels: opt-in (HDP_PDL=1); measured
+// programmatic dependent launch of the GEMM / split-K kernels: opt-in (option "pdl"); measured
 // on the C4 per-step chain it did not shorten the step (37.6 vs 37.3 ms), the prologue it
 // overlaps is short next to the predecessor's drain + flush
-bool use_pdl() {
-  static const bool on = [] {
-    const char* e = getenv("HDP_PDL");
-    return e && e[0] == '1';
-  }();
-  return on;
-}
+bool use_pdl() { return opt(OPT_PDL) == 1; }
 
 template <int BN, int AMN, int BMN, int CN = 1, int CG = 1>
 cudaError_t launch_tc(const GemmPlan& p, cudaStream_t s) {
@@ -896,26 +891,24 @@ int gemm_plan_tc(GemmPlan* p, const __half* A, long lda, int a_mn, const __half*
   p->splits = splits;
   p->kbps = kbps;
   // A multicast across a cluster of CN CTAs sharing the M tile (K-major A only), opt-in via
-  // HDP_GEMM_CN=2|4.  Measured on the C4 per-step shapes it does not pay (K2 256x8192x2048:
+  // the gemm_cluster_n option (2 or 4).  Measured on the C4 per-step shapes it does not pay (K2 256x8192x2048:
   // 16.7 / 17.6 / 18.4 us at CN = 1 / 2 / 4): those GEMMs are bound by the chip's L2 -> SM
   // operand throughput (~46 B/clk/SM, the same rate the 8192^3 GEMM streams at), which
   // unicast already reaches -- L2 de-duplicates the concurrent reads of the shared A tile
   int cn = 1;
   {
-    const char* ev = getenv("HDP_GEMM_CN");
-    if (ev) cn = atoi(ev);
+    cn = opt(OPT_GEMM_CLUSTER_N);
     if (cn != 2 && cn != 4) cn = 1;
     if (a_mn != 0) cn = 1;
   }
   p->cn = cn;
-  // CTA pairs (cta_group::2, 256-row tiles): force_cg 1 / 2 (or HDP_GEMM_CG) forces; automatic
+  // CTA pairs (cta_group::2, 256-row tiles): force_cg 1 / 2 (or the gemm_cta_group option) forces; automatic
   // for the large GEMMs (K1, K8, K9): per SM half the B bytes of a 128 x 256 tile for the same
   // flops (8192^3: 1052 -> 1393 TFLOP/s; K1 at C4 961 -> 1105; K9 983 -> 1228).
   // The short-K per-step GEMMs (K2 / K7) measured slower with pairs and keep single CTAs.
   int cg = force_cg;
   {
-    const char* ev = getenv("HDP_GEMM_CG");
-    if (ev) cg = atoi(ev);
+    if (opt(OPT_GEMM_CTA_GROUP)) cg = opt(OPT_GEMM_CTA_GROUP);
     if (cg == 0) {
       const int pair_tiles = ((M + 2 * BM - 1) / (2 * BM)) * ((N + bn - 1) / bn) * splits;
       cg = (bn == 256 && N >= 512 && pair_tiles >= 148) ? 2 : 1;

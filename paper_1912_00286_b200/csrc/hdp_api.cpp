@@ -26,6 +26,8 @@
 #include "kernels.cuh"
 #include "recur.cuh"
 #include "p2p_exchange.cuh"
+#include "options.h"
+#include "recur_trace.h"
 
 namespace {
 
@@ -99,7 +101,6 @@ struct hdp_ctx {
   bool configured = false, bound = false, loaded = false, poisoned = false;
   hdp_model_desc d{};
   bool f32 = false;       // FP32 math mode
-  bool persistent = true; // persistent fused recurrence kernels where they fit (env HDP_PERSISTENT=0 disables)
   bool gf32 = false;      // fp32 gradients / wire
   int nslots = 1;
   long hp = 0, Ip0 = 0, Fp = 0, esz = 2, gsz = 2;
@@ -144,8 +145,13 @@ struct hdp_ctx {
   unsigned* fwin = nullptr;
   std::vector<void*> peer_open;       // IPC mappings to close
   hdp::P2PArgs p2pa;                  // peer tables + bucket table (step / scalars filled per call)
-  int p2p_grid = 0;
-  unsigned p2p_step = 0;
+  unsigned p2p_step = 0;              // updates so far (status slot)
+  unsigned p2p_seq = 0;               // exchange launches so far (flag values)
+  unsigned p2p_ctr = 0;               // CTAs of those launches (completion counter target)
+  int quorum = 0;                     // NEXT-2 partial collection: contributors to wait for (0 = all)
+  double partial_fraction = 1.0;
+  unsigned straggler_mask = 0;        // test injection (hdp_set_option)
+  unsigned long long straggler_ns = 0;
   float* Gx1 = nullptr;  // layer-1 G_x of the split forward wavefront
   float* crp = nullptr;
   size_t crp_floats = 0;
@@ -195,12 +201,13 @@ struct hdp_ctx {
   float drop_scale = 1.f;
   char* hst = nullptr;        // library-owned: per slot [L][T+1][B][hp] fp16 masked recurrent inputs
   bool drop_on() const { return keep < 1.0; }
-  bool recur_ok() const { return persistent && !drop_on(); }  // the fused recurrences have no dropout
+  bool recur_ok() const { return hdp::opt(hdp::OPT_PERSISTENT) != 0 && !drop_on(); }  // (no dropout in them)
   int* drop_step() const { return status + 14; }  // completed updates (mask counter)
   char* Hst(int slot, int l) const {
     return hst + ((size_t)slot * d.n_layers + l) * (size_t)(d.max_seq + 1) * d.max_batch * hp * 2;
   }
   double* l2part = nullptr;   // partial sums of the L2 loss term
+  unsigned long long* trace = nullptr;  // recurrence phase trace (option recur_trace, profile mode)
   long adam_k = 0;
 
   int L() const { return d.n_layers; }
@@ -445,6 +452,28 @@ struct KScope {
   }
 };
 
+// ---------------------------------------------------------------- recurrence phase trace
+// Option recur_trace = 1 in profile (eager) mode: the persistent / wavefront kernels stamp
+// %globaltimer per phase; trace_report (recur_trace.cpp) prints the per-step means.
+unsigned long long* trace_buffer(hdp_ctx* c, size_t words) {
+  if (!c->prof || !hdp::opt(hdp::OPT_RECUR_TRACE)) return nullptr;
+  if (!c->trace && cudaMalloc(&c->trace, (size_t)6 * 8192 * 5 * sizeof(unsigned long long)) != cudaSuccess) {
+    c->trace = nullptr;
+    return nullptr;
+  }
+  (void)words;
+  return c->trace;
+}
+int trace_report(hdp_ctx* c, hdp::TraceKind kind, const unsigned long long* dev, int T, int layer, cudaStream_t s) {
+  (void)c;
+  if (T > 8192) return HDP_OK;
+  std::vector<unsigned long long> h((size_t)6 * T * 5);
+  CK_CUDA(cudaStreamSynchronize(s));
+  CK_CUDA(cudaMemcpy(h.data(), dev, h.size() * 8, cudaMemcpyDeviceToHost));
+  hdp::print_trace(kind, h.data(), T, layer);
+  return HDP_OK;
+}
+
 // ---------------------------------------------------------------- GEMM helper
 int gemm(hdp_ctx* c, int tag, const void* A, long lda, int amn, const void* B, long ldb, int bmn, long M, long N,
          long K, const hdp::Epilogue& epi, cudaStream_t s, int force_bn = 0, int force_splits = 0) {
@@ -544,54 +573,12 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
       ra.T = T;
       ra.B = B;
       ra.hp = (int)hp;
-      static unsigned long long* w2trace = nullptr;  // debug: HDP_RECUR_TRACE=1 in profile (eager) mode
-      const bool want_trace = c->prof && getenv("HDP_RECUR_TRACE") && getenv("HDP_RECUR_TRACE")[0] == '1';
-      if (want_trace) {
-        if (!w2trace) CK_CUDA(cudaMalloc(&w2trace, 4 * 8192 * 5 * sizeof(unsigned long long)));
-        ra.trace = w2trace;
-      }
+      ra.trace = trace_buffer(c, 4 * 8192 * 5);
       {
         KScope ks_(c, HDP_K_RECUR_FWD, 1, s);
         CK_CUDA(hdp::launch_recur2_fwd(ra, s));
       }
-      if (want_trace && T <= 8192) {
-        std::vector<unsigned long long> h((size_t)4 * T * 5);
-        CK_CUDA(cudaStreamSynchronize(s));
-        CK_CUDA(cudaMemcpy(h.data(), w2trace, h.size() * 8, cudaMemcpyDeviceToHost));
-        const unsigned long long t00 = h[0];
-        const char* names[3] = {"R0", "P", "R1"};
-        for (int role = 0; role < 3; ++role) {
-          double ph[4] = {0, 0, 0, 0}, step = 0;
-          int n = 0;
-          for (int t = 2; t < T - 1; ++t) {
-            const unsigned long long* r = &h[((size_t)role * T + t) * 5];
-            for (int q = 0; q < 4; ++q) ph[q] += (double)(r[q + 1] - r[q]);
-            step += (double)(h[((size_t)role * T + t + 1) * 5] - r[0]);
-            ++n;
-          }
-          const unsigned long long* st = &h[((size_t)role * T + 1) * 5];
-          fprintf(stderr, "[hdp trace] wavefront %s: per step ns: %.0f %.0f %.0f %.0f | step %.0f | t=1 starts at +%.0f ns, t=T-1 ends at +%.0f\n",
-                  names[role], ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, step / n, (double)(st[0] - t00),
-                  (double)(h[((size_t)role * T + T - 1) * 5 + 4] - t00));
-        }
-        {
-          double q[3] = {0, 0, 0};
-          int n = 0;
-          for (int t = 2; t < T - 1; ++t) {
-            const unsigned long long* r = &h[((size_t)3 * T + t) * 5];
-            const unsigned long long e0 = h[((size_t)0 * T + t) * 5 + 2];  // R0 TR(t,2): MMA done
-            if (!r[0] || !r[3]) continue;
-            q[0] += (double)(r[0] - e0);
-            q[1] += (double)(r[1] - r[0]);
-            q[2] += (double)(r[2] - r[1]);
-            ++n;
-          }
-          if (n)
-            fprintf(stderr, "[hdp trace] wavefront R0 epilogue: acc load %.0f  act+stage %.0f  cell+stores %.0f ns\n",
-                    q[0] / n, q[1] / n, q[2] / n);
-        }
-
-      }
+      if (ra.trace) CK(trace_report(c, hdp::TRACE_FWD_WAVEFRONT, ra.trace, T, l, s));
       break;
     }
     if (!f32 && c->recur_ok() && hdp::recur_fwd_supported(B, (int)hp)) {
@@ -606,34 +593,12 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
       ra.T = T;
       ra.B = B;
       ra.hp = (int)hp;
-      static unsigned long long* ftrace = nullptr;  // debug: HDP_RECUR_TRACE=1 in profile (eager) mode
-      const bool want_trace = c->prof && getenv("HDP_RECUR_TRACE") && getenv("HDP_RECUR_TRACE")[0] == '1';
-      if (want_trace) {
-        if (!ftrace) CK_CUDA(cudaMalloc(&ftrace, 8192 * 5 * sizeof(unsigned long long)));
-        ra.trace = ftrace;
-      }
+      ra.trace = trace_buffer(c, 8192 * 5);
       {
         KScope ks_(c, HDP_K_RECUR_FWD, 1, s);
         CK_CUDA(hdp::launch_recur_fwd(ra, s));
       }
-      if (want_trace && T <= 8192) {
-        std::vector<unsigned long long> h((size_t)T * 5);
-        CK_CUDA(cudaStreamSynchronize(s));
-        CK_CUDA(cudaMemcpy(h.data(), ftrace, h.size() * 8, cudaMemcpyDeviceToHost));
-        double ph[4] = {0, 0, 0, 0}, step = 0;
-        int n = 0;
-        for (int t = 1; t < T - 1; ++t) {
-          const unsigned long long* r = &h[(size_t)t * 5];
-          ph[0] += (double)(r[1] - r[0]);
-          ph[1] += (double)(r[2] - r[1]);
-          ph[2] += (double)(r[3] - r[2]);
-          ph[3] += (double)(r[4] - r[3]);
-          step += (double)(h[(size_t)(t + 1) * 5] - r[0]);
-          ++n;
-        }
-        fprintf(stderr, "[hdp trace] recur_fwd layer %d: per step ns: wait %.0f mma %.0f epilogue %.0f push %.0f | step %.0f\n",
-                l, ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, step / n);
-      }
+      if (ra.trace) CK(trace_report(c, hdp::TRACE_FWD_LAYER, ra.trace, T, l, s));
       continue;
     }
     for (int t = 0; t < T; ++t) {
@@ -835,84 +800,12 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
       wa.gb[0] = (__half*)c->G(si, c->find("b1"));
       wa.gb[1] = (__half*)c->G(si, c->find("b0"));
     }
-    static unsigned long long* b2trace = nullptr;  // debug: HDP_RECUR_TRACE=1 in profile (eager) mode
-    const bool want_trace = c->prof && getenv("HDP_RECUR_TRACE") && getenv("HDP_RECUR_TRACE")[0] == '1' && T <= 8192;
-    if (want_trace) {
-      if (!b2trace) CK_CUDA(cudaMalloc(&b2trace, 6 * 8192 * 5 * sizeof(unsigned long long)));
-      wa.trace = b2trace;
-    }
+    wa.trace = trace_buffer(c, 6 * 8192 * 5);
     {
       KScope ks_(c, HDP_K_RECUR_BWD, 1, s);
       CK_CUDA(hdp::launch_recur2_bwd(wa, s));
     }
-    if (want_trace) {
-      std::vector<unsigned long long> h((size_t)6 * T * 5);
-      CK_CUDA(cudaStreamSynchronize(s));
-      CK_CUDA(cudaMemcpy(h.data(), b2trace, h.size() * 8, cudaMemcpyDeviceToHost));
-      {
-        {
-          double wsum[4] = {0, 0, 0, 0};
-          int n = 0;
-          for (int t = T - 2; t >= 1; --t) {
-            const unsigned long long e2 = h[((size_t)1 * T + t) * 5 + 2];  // Q0 TR(t,2)
-            const unsigned long long* r = &h[((size_t)5 * T + t) * 5];
-            if (!r[0]) continue;
-            for (int w = 0; w < 4; ++w) wsum[w] += (double)r[w] - (double)e2;
-            ++n;
-          }
-          if (n)
-            fprintf(stderr, "[hdp trace] bwd Q0 warps reach the epilogue barrier at +%.0f +%.0f +%.0f +%.0f ns after MMA done\n",
-                    wsum[0] / n, wsum[1] / n, wsum[2] / n, wsum[3] / n);
-        }
-        // dX1 hand-off timeline (group 0, units 0..63): X publishes -> Q0 fetch issued -> Q0 needs
-        const unsigned long long z0 = h[(size_t)(T - 1) * 5];
-        for (int t = T - 3; t >= 0; t -= (T > 40 ? 20 : 5)) {
-          const unsigned long long* r = &h[((size_t)4 * T + t) * 5];
-          fprintf(stderr, "[hdp trace] Q0 t=%d: gates/c fetch issued +%.0f  needed +%.0f  slot t landed +%.0f  slot t-1 landed +%.0f ns\n", t,
-                  (double)(r[0] - z0), (double)(r[2] - z0), (double)(r[3] - z0), (double)(r[4] - z0));
-        }
-      }
-      {
-        double q[3] = {0, 0, 0};
-        int n = 0;
-        for (int t = T - 2; t >= 1; --t) {
-          const unsigned long long* r = &h[((size_t)3 * T + t) * 5];
-          const unsigned long long e2 = h[((size_t)1 * T + t) * 5 + 2];  // Q0 TR(t,2)
-          if (!r[0] || !r[2]) continue;
-          q[0] += (double)(r[0] - e2);
-          q[1] += (double)(r[1] - r[0]);
-          q[2] += (double)(r[2] - r[1]);
-          ++n;
-        }
-        if (n)
-          fprintf(stderr, "[hdp trace] bwd Q0 epilogue: dX1 wait %.0f  acc load %.0f  cell+stage %.0f ns\n", q[0] / n,
-                  q[1] / n, q[2] / n);
-        double w3 = 0, w4 = 0;
-        int m = 0;
-        for (int t = T - 2; t >= 1; --t) {
-          const unsigned long long* r = &h[((size_t)3 * T + t) * 5];
-          w3 += (double)r[3];
-          w4 += (double)r[4];
-          ++m;
-        }
-        fprintf(stderr, "[hdp trace] bwd Q0 warp 3: store read-wait %.0f  due dX1 fetch %.0f ns\n", w3 / m, w4 / m);
-      }
-      const char* names[3] = {"Q1", "Q0", "X"};
-      const unsigned long long t00 = h[(size_t)(T - 1) * 5];
-      for (int role = 0; role < 3; ++role) {
-        double ph[4] = {0, 0, 0, 0}, step = 0;
-        int n = 0;
-        for (int t = T - 2; t >= 1; --t) {
-          const unsigned long long* r = &h[((size_t)role * T + t) * 5];
-          for (int q = 0; q < 4; ++q) ph[q] += (double)(r[q + 1] - r[q]);
-          step += (double)(h[((size_t)role * T + t - 1) * 5] - r[0]);
-          ++n;
-        }
-        fprintf(stderr, "[hdp trace] bwd wavefront %s: per step ns: %.0f %.0f %.0f %.0f | step %.0f | t=T-2 starts at +%.0f ns, t=0 ends at +%.0f\n",
-                names[role], ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, step / n,
-                (double)(h[((size_t)role * T + T - 2) * 5] - t00), (double)(h[((size_t)role * T) * 5 + 4] - t00));
-      }
-    }
+    if (wa.trace) CK(trace_report(c, hdp::TRACE_BWD_WAVEFRONT, wa.trace, T, l, s));
   } else if (wave) {
     // layer 0: already done by the wavefront launch of the layer-1 segment
   } else if (!f32 && c->recur_ok() && hdp::recur_bwd_supported(B, (int)hp)) {
@@ -928,34 +821,12 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
     ra.T = T;
     ra.B = B;
     ra.hp = (int)hp;
-    static unsigned long long* trace_buf = nullptr;  // debug: HDP_RECUR_TRACE=1 in profile (eager) mode
-    const bool want_trace = c->prof && getenv("HDP_RECUR_TRACE") && getenv("HDP_RECUR_TRACE")[0] == '1';
-    if (want_trace) {
-      if (!trace_buf) CK_CUDA(cudaMalloc(&trace_buf, 8192 * 5 * sizeof(unsigned long long)));
-      ra.trace = trace_buf;
-    }
+    ra.trace = trace_buffer(c, 8192 * 5);
     {
       KScope ks_(c, HDP_K_RECUR_BWD, 1, s);
       CK_CUDA(hdp::launch_recur_bwd(ra, s));
     }
-    if (want_trace && T <= 8192) {
-      std::vector<unsigned long long> h((size_t)T * 5);
-      CK_CUDA(cudaStreamSynchronize(s));
-      CK_CUDA(cudaMemcpy(h.data(), trace_buf, h.size() * 8, cudaMemcpyDeviceToHost));
-      double ph[4] = {0, 0, 0, 0}, step = 0;
-      int n = 0;
-      for (int t = T - 2; t >= 1; --t) {  // steps with an MMA; t+1 -> t gap is the step time
-        const unsigned long long* r = &h[(size_t)t * 5];
-        ph[0] += (double)(r[1] - r[0]);   // prefetch issue + cluster wait
-        ph[1] += (double)(r[2] - r[1]);   // MMA issue + completion
-        ph[2] += (double)(r[3] - r[2]);   // epilogue + syncthreads
-        ph[3] += (double)(r[4] - r[3]);   // DSMEM push + arrive
-        step += (double)(h[(size_t)(t - 1) * 5] - r[0]);
-        ++n;
-      }
-      fprintf(stderr, "[hdp trace] recur_bwd layer %d: per step ns: wait %.0f mma %.0f epilogue %.0f push %.0f | step %.0f\n",
-              l, ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, step / n);
-    }
+    if (ra.trace) CK(trace_report(c, hdp::TRACE_BWD_LAYER, ra.trace, T, l, s));
   } else
   for (int t = T - 1; t >= 0; --t) {
     const float* dHa_t = last_only ? (t == T - 1 ? dHa : nullptr) : dHa + (long)t * B * hp;
@@ -988,14 +859,14 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
         }
         // K = 4 hp is long and M = B small: 256-wide tiles, split K over ~120 CTAs
         int fbn = 0, fsp = 0;
-        if (hp >= 1024) {  // C4 sweep (tools/c4_gemm_sweep.py, HDP_K7_CFG): 256-wide tiles, ~128 CTAs
+        if (hp >= 1024) {  // C4 sweep (tools/c4_gemm_sweep.py): 256-wide tiles, ~128 CTAs
           const int tiles = (int)(((B + 127) / 128) * ((hp + 255) / 256));
           fbn = 256;
           fsp = std::max(1, std::min(128 / tiles, (int)(4 * hp / 64 / 4)));
           fsp = std::min(fsp, 16);
         }
-        static const char* k7cfg = getenv("HDP_K7_CFG");  // tuning override "bn,splits"
-        if (k7cfg) sscanf(k7cfg, "%d,%d", &fbn, &fsp);
+        if (hdp::opt(hdp::OPT_K7_BN)) fbn = hdp::opt(hdp::OPT_K7_BN);  // tuning overrides
+        if (hdp::opt(hdp::OPT_K7_SPLITS)) fsp = hdp::opt(hdp::OPT_K7_SPLITS);
         CK(gemm(c, HDP_K_GEMM_DH, c->dA + (long)t * B * 4 * hp * e, 4 * hp, 0, c->W(iU), hp, 1, B, hp, 4 * hp, eb, s,
                 fbn, fsp));
       }
@@ -1108,7 +979,6 @@ void p2p_bucket_table(hdp_ctx* c) {
   a.W = c->master;
   a.S1 = c->s1;
   a.S2 = c->s2;
-  c->p2p_grid = (int)std::max(1L, std::min((vtot + 255) / 256, 4L * 148));
 }
 
 // NEXT-2 loopback (world 1, HDP_EXCH_P2P): the exchange kernel's peers are the simulated
@@ -1121,8 +991,9 @@ int setup_loopback(hdp_ctx* c) {
   a.N = c->nslots;
   a.NR = 1;
   a.rank = 0;
+  a.loopback = 1;
   for (int r = 0; r < c->nslots; ++r) {
-    a.g_peer[r] = (const __half*)(c->grads + (size_t)r * c->P * c->gsz);
+    a.g_peer[r] = c->grads + (size_t)r * c->P * c->gsz;
     a.w_peer[r] = (__half*)(r == 0 ? c->w : c->wcopies + (size_t)(r - 1) * c->P * c->esz);
   }
   a.flag_peer[0] = c->fwin;
@@ -1174,7 +1045,7 @@ int setup_p2p(hdp_ctx* c) {
         c->peer_open.push_back(ptr[k]);
       }
     }
-    a.g_peer[r] = (const __half*)ptr[0];
+    a.g_peer[r] = ptr[0];
     a.w_peer[r] = (__half*)ptr[1];
     a.flag_peer[r] = (unsigned*)ptr[2];
     a.status_peer[r] = (int*)((unsigned*)ptr[2] + hdp::P2P_STATUS);
@@ -1224,6 +1095,22 @@ int check_desc_across_ranks(hdp_ctx* c, const hdp_model_desc& d) {
 }
 
 }  // namespace
+
+// ====================================================================== options
+namespace hdp {
+int g_opt[OPT_COUNT] = {1, 1, 1, 1, 1, 0, 1, 0, 1, 0, 0, 0, 0};
+namespace {
+const char* const kOptNames[OPT_COUNT] = {"persistent",     "wavefront",      "wavefront_fusex", "wavefront_wgrad",
+                                          "wavefront_tmem", "recur_nbg",      "recur_cluster",   "gemm_cta_group",
+                                          "gemm_cluster_n", "pdl",            "k7_bn",           "k7_splits",
+                                          "recur_trace"};
+}
+int opt_find(const char* name) {
+  for (int i = 0; i < OPT_COUNT; ++i)
+    if (!strcmp(name, kOptNames[i])) return i;
+  return -1;
+}
+}  // namespace hdp
 
 // ====================================================================== C-ABI
 extern "C" {
@@ -1282,6 +1169,7 @@ int hdp_destroy(hdp_ctx* c) {
   if (c->wwin) cudaFree(c->wwin);
   if (c->fwin) cudaFree(c->fwin);
   if (c->hst) cudaFree(c->hst);
+  if (c->trace) cudaFree(c->trace);
   if (c->comm) ncclCommDestroy(c->comm);
   delete c;
   return HDP_OK;
@@ -1310,10 +1198,6 @@ int hdp_configure(hdp_ctx* c, const hdp_model_desc* desc, hdp_sizes* out) {
   if (d.exchange < HDP_EXCH_AUTO || d.exchange > HDP_EXCH_P2P) return fail(HDP_ERR_ARG, "bad exchange mode");
   CK(check_desc_across_ranks(c, d));
   c->d = d;
-  {
-    const char* ev = getenv("HDP_PERSISTENT");
-    c->persistent = !(ev && ev[0] == '0');
-  }
   c->f32 = d.math == HDP_MATH_FP32;
   c->gf32 = c->f32 || d.wire == HDP_WIRE_FP32;
   c->esz = c->f32 ? 4 : 2;
@@ -1322,12 +1206,12 @@ int hdp_configure(hdp_ctx* c, const hdp_model_desc* desc, hdp_sizes* out) {
   build_layout(c);
   {
     // NEXT-2 one-kernel exchange: fp16 gradients on the all-to-all wire, fp16 weights
-    const bool fits = !c->f32 && !c->gf32 && d.wire == HDP_WIRE_FP16_A2A &&
+    const bool fits = !c->f32 && (d.wire == HDP_WIRE_FP16_A2A || d.wire == HDP_WIRE_FP32) &&
                       (int)c->buckets.size() <= hdp::P2P_MAX_BUCKETS &&
                       ((c->world >= 2 && c->world <= hdp::P2P_MAX_RANKS) ||
                        (c->world == 1 && c->nslots >= 2 && c->nslots <= hdp::P2P_MAX_RANKS));
     if (d.exchange == HDP_EXCH_P2P && !fits)
-      return fail(HDP_ERR_UNSUPPORTED, "HDP_EXCH_P2P needs mixed math, the fp16 all-to-all wire and 2..%d ranks "
+      return fail(HDP_ERR_UNSUPPORTED, "HDP_EXCH_P2P needs mixed math, the fp16 all-to-all or fp32 wire and 2..%d ranks "
                   "(or simulated workers at world 1)", hdp::P2P_MAX_RANKS);
     c->want_p2p = fits && (d.exchange == HDP_EXCH_P2P || (d.exchange == HDP_EXCH_AUTO && c->world >= 2));
     c->loopback = c->want_p2p && c->world == 1;
@@ -1559,6 +1443,8 @@ int hdp_set_dynamic_loss_scale(hdp_ctx* c, int growth_interval) {
   if (!c) return fail(HDP_ERR_ARG, "null context");
   if (growth_interval < 0) return fail(HDP_ERR_ARG, "growth_interval must be >= 0");
   if (!c->bound) return fail(HDP_ERR_STATE, "context not bound");
+  if (growth_interval > 0 && c->quorum > 0)
+    return fail(HDP_ERR_UNSUPPORTED, "dynamic loss scaling with partial collection");
   if (growth_interval > 0 && c->d.optimizer == HDP_OPT_ADAM)
     return fail(HDP_ERR_UNSUPPORTED, "dynamic loss scaling with Adam: the host-side bias-correction step count "
                 "would also count skipped steps");
@@ -1695,14 +1581,17 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
   }
   a.nonfinite = c->status;
   a.l2x2 = (float)(2.0 * c->l2);
-  cudaStream_t cs = c->world > 1 ? c->comm_stream : s;
-  if (c->world > 1) {
-    // the comm stream must see everything enqueued on `s` so far (incl. the
-    // flat-model gradients written by the caller) before bucket 0
+  // Steps 4-6 run on the comm stream, each bucket group gated by the event its backward
+  // segment recorded, so the update of the top layers overlaps the BPTT of the lower ones
+  // (north_star "overlapped with BPTT on a side stream").  A flat model (C5: the caller wrote
+  // the gradients) or a dynamic loss scale (the skip decision needs every gradient first)
+  // makes the comm stream wait for everything enqueued on `s` instead.
+  cudaStream_t cs = c->comm_stream;
+  const bool dyn = c->dyn_interval > 0;
+  if (c->d.n_layers == 0 || dyn) {
     CK_CUDA(cudaEventRecord(c->ev_done, s));
     CK_CUDA(cudaStreamWaitEvent(cs, c->ev_done, 0));
   }
-  const bool dyn = c->dyn_interval > 0;
   if (dyn) {
     // NEXT-3 dynamic loss scaling: the step's global non-finite count (all ranks' fp16
     // gradients) decides before any update whether the step is applied; alpha, kept on
@@ -1721,12 +1610,21 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
     a.alpha_dev = c->alpha_dev();
     a.n_workers = (double)N;
   }
+  // Exchange groups: buckets become ready in order (head, layer L-1 .. 0, embedding); with the
+  // backward wavefront every layer bucket is ready at once, so buckets 1.. form one group (one
+  // launch / one NCCL group each instead of one per bucket).
+  const size_t nb = c->buckets.size();
+  std::vector<std::pair<size_t, size_t>> groups;
+  if (c->wave_bwd && nb > 2) {
+    groups.push_back({0, 1});
+    groups.push_back({1, nb});
+  } else {
+    for (size_t bi = 0; bi < nb; ++bi) groups.push_back({bi, bi + 1});
+  }
   const int* count_src = c->status;
   if (c->p2p) {
-    // NEXT-2: one kernel does the exchange, the fused average + update and the all-gather
-    // over NVLink peer memory (p2p_exchange.cu); it starts once every bucket is complete
-    if (c->d.n_layers > 0)
-      for (size_t bi = 0; bi < c->buckets.size(); ++bi) CK_CUDA(cudaStreamWaitEvent(cs, c->ev_bucket[bi], 0));
+    // NEXT-2: one kernel per group does the exchange, the fused average + update and the
+    // all-gather over NVLink peer memory (p2p_exchange.cu)
     const unsigned step = ++c->p2p_step;
     hdp::P2PArgs& p = c->p2pa;
     p.step = step;
@@ -1744,30 +1642,32 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
     p.skip = a.skip;
     p.alpha_dev = a.alpha_dev;
     p.n_workers = a.n_workers;
+    p.alpha = (double)c->alpha;
+    p.quorum = c->quorum;
+    p.straggler_mask = c->straggler_mask;
+    p.straggler_ns = c->straggler_ns;
     // the other status slot is next step's: zero it now (peers add to it only after my next "ready")
     CK_CUDA(cudaMemsetAsync(c->fwin + hdp::P2P_STATUS + ((step + 1) & 1), 0, sizeof(int), cs));
-    {
+    for (const auto& gr : groups) {
+      if (c->d.n_layers > 0)
+        for (size_t bi = gr.first; bi < gr.second; ++bi) CK_CUDA(cudaStreamWaitEvent(cs, c->ev_bucket[bi], 0));
+      p.bk0 = (int)gr.first;
+      p.bk1 = (int)gr.second;
+      p.seq = ++c->p2p_seq;
+      const long vec = p.vpre[p.bk1] - p.vpre[p.bk0];
+      const int grid = (int)std::max(1L, std::min((vec + 255) / 256, 4L * 148));
+      c->p2p_ctr += (unsigned)grid;
+      p.ctr_target = c->p2p_ctr;
       KScope ks_(c, HDP_K_UPDATE, 1, cs);
-      CK_CUDA(hdp::launch_exch_update(p, opt, c->p2p_grid, cs));
+      CK_CUDA(hdp::launch_exch_update(p, opt, c->gf32, grid, cs));
     }
     count_src = (const int*)(c->fwin + hdp::P2P_STATUS + (step & 1));
   } else {
     CK_CUDA(cudaMemsetAsync(c->status, 0, sizeof(int), cs));
-    // Exchange groups: buckets become ready in order (head, layer L-1 .. 0, embedding); with the
-    // backward wavefront every layer bucket is ready at once, so buckets 1.. form one group whose
-    // collectives are issued as single NCCL groups (one kernel each instead of one per bucket).
-    const size_t nb = c->buckets.size();
-    std::vector<std::pair<size_t, size_t>> groups;
-    if (c->world > 1 && c->wave_bwd && nb > 2) {
-      groups.push_back({0, 1});
-      groups.push_back({1, nb});
-    } else {
-      for (size_t bi = 0; bi < nb; ++bi) groups.push_back({bi, bi + 1});
-    }
     for (size_t gi = 0; gi < groups.size(); ++gi) {
       const size_t b0 = groups[gi].first, b1 = groups[gi].second;
       const bool last = gi + 1 == groups.size();
-      if (c->world > 1 && c->d.n_layers > 0)
+      if (c->d.n_layers > 0)
         for (size_t bi = b0; bi < b1; ++bi) CK_CUDA(cudaStreamWaitEvent(cs, c->ev_bucket[bi], 0));
       if (c->world > 1) {
         KScope ks_(c, HDP_K_COMM, 0, cs);
@@ -1815,7 +1715,6 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
         CK_NCCL(ncclGroupEnd());
       }
     }
-
   }
   if (dyn) {
     KScope ks_(c, HDP_K_UPDATE, 1, cs);
@@ -1832,10 +1731,8 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
     CK_CUDA(cudaMemsetAsync(c->status + 16, 0, sizeof(int), cs));
   }
   CK_CUDA(cudaEventRecord(c->ev_count, cs));
-  if (c->world > 1) {
-    CK_CUDA(cudaEventRecord(c->ev_done, cs));
-    CK_CUDA(cudaStreamWaitEvent(s, c->ev_done, 0));  // next forward sees the new weights
-  }
+  CK_CUDA(cudaEventRecord(c->ev_done, cs));
+  CK_CUDA(cudaStreamWaitEvent(s, c->ev_done, 0));  // next forward sees the new weights
   for (auto& st : c->st) st.bwd = false;
   if (nonfinite_host) {
     CK_CUDA(cudaEventSynchronize(c->ev_count));
@@ -1853,6 +1750,61 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
   } else {
     c->count_pending = true;
   }
+  return HDP_OK;
+}
+
+int hdp_set_option(hdp_ctx* c, const char* name, double value) {
+  if (!name) return fail(HDP_ERR_ARG, "null option name");
+  const std::string n(name);
+  if (n == "partial_fraction" || n == "straggler_mask" || n == "straggler_us") {
+    if (!c || !c->bound) return fail(HDP_ERR_STATE, "option %s needs a bound context", name);
+    if (n == "partial_fraction") {
+      if (!(value > 0.0 && value <= 1.0)) return fail(HDP_ERR_ARG, "partial_fraction must be in (0, 1]");
+      const int N = c->Nw();
+      const int q = (int)std::ceil(value * N - 1e-9);  // SPEC.md:322 ceil(f*N)
+      if (q < N) {
+        if (!c->p2p) return fail(HDP_ERR_UNSUPPORTED, "partial collection needs the one-kernel exchange");
+        if (c->dyn_interval > 0) return fail(HDP_ERR_UNSUPPORTED, "partial collection with dynamic loss scaling");
+      }
+      c->partial_fraction = value;
+      c->quorum = q < N ? std::max(q, 1) : 0;
+    } else if (n == "straggler_mask") {
+      if (!(value >= 0 && value < 4294967296.0)) return fail(HDP_ERR_ARG, "straggler_mask out of range");
+      c->straggler_mask = (unsigned)value;
+    } else {
+      if (!(value >= 0 && value <= 10e6)) return fail(HDP_ERR_ARG, "straggler_us must be in [0, 1e7]");
+      c->straggler_ns = (unsigned long long)(value * 1000.0);
+    }
+    return HDP_OK;
+  }
+  const int id = hdp::opt_find(name);
+  if (id < 0) return fail(HDP_ERR_ARG, "unknown option %s", name);
+  if (!(value >= -1 && value <= 1 << 20) || value != std::floor(value))
+    return fail(HDP_ERR_ARG, "option %s takes an integer value", name);
+  hdp::g_opt[id] = (int)value;
+  if (c && !c->host_only) {
+    CK_CUDA(cudaSetDevice(c->device));
+    CK_CUDA(cudaDeviceSynchronize());
+    for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
+    c->graphs.clear();
+  }
+  return HDP_OK;
+}
+
+int hdp_partial_state(hdp_ctx* c, unsigned* mask, int* count) {
+  CK(check_ready(c));
+  if (!mask || !count) return fail(HDP_ERR_ARG, "null argument");
+  if (!c->p2p || c->quorum == 0) {
+    *mask = c->Nw() >= 32 ? 0xffffffffu : (1u << c->Nw()) - 1u;
+    *count = c->Nw();
+    return HDP_OK;
+  }
+  CK_CUDA(cudaSetDevice(c->device));
+  CK_CUDA(cudaDeviceSynchronize());
+  unsigned w[2];
+  CK_CUDA(cudaMemcpy(w, c->fwin + hdp::P2P_DECISION, sizeof w, cudaMemcpyDeviceToHost));
+  *mask = w[0];  // little-endian low word of (seq << 32) | mask
+  *count = __builtin_popcount(w[0]);
   return HDP_OK;
 }
 

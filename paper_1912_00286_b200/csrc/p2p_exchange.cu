@@ -1,21 +1,26 @@
 // NEXT-2: the gradient exchange and the fused average + update (A9 + K11 + A11,
-// PAPER.md:94-96 steps 4-6) as ONE kernel over NVLink peer memory.
+// PAPER.md:94-96 steps 4-6) as ONE kernel over NVLink peer memory, launched once per
+// bucket group as soon as the group's gradients are complete (the update of the top
+// layers overlaps the BPTT of the lower ones, north_star "overlapped with BPTT").
 //
-// Every rank exposes (CUDA IPC) its fp16 gradient vector, its fp16 working
-// weights and a small flag / counter block.  Owner r of each bucket shard:
-//   A. publishes "my gradients of step s are complete" to every peer (st.release.sys)
-//      and waits until all N ranks have published step s (ld.acquire.sys);
-//   B. reads the N contributions of its shard straight from the peers' gradient
-//      vectors over NVLink (16-B loads, rank order), sums them in fp32 (R14 order,
-//      identical to K11), applies SGD-m / Adam to its fp32 master shard, rounds
-//      to fp16 and stores the result into EVERY rank's weight vector (16-B peer
-//      stores) -- the all-to-all, the update and the all-gather in one pass;
-//   C. the last CTA to finish (threadfence-reduction pattern, system scope)
-//      publishes "my shards are written" and waits for all N ranks' publication,
-//      so that kernel completion means: every weight everywhere is final and no
-//      peer still reads my gradients (the next step may overwrite them).
+// Every rank exposes (CUDA IPC) its gradient vector (fp16, or fp32 on the fp32 wire),
+// its fp16 working weights and a small flag / counter block.  One launch, owner r of
+// each shard of the launch's buckets:
+//   A. publishes "my gradients for launch `seq` are complete" to every peer
+//      (st.release.sys) and waits until every contributor has published `seq`
+//      (ld.acquire.sys); with partial collection rank 0 instead waits
+//      for `quorum` contributors, publishes that set, and every owner uses it;
+//   B. reads the contributions of its shard straight from the peers' gradient vectors
+//      over NVLink (all loads of a vector issued before the sum), sums them in fp32 in
+//      rank order (R14, identical to K11), applies SGD-m / Adam to its fp32 master
+//      shard, rounds to fp16 and stores the result into EVERY rank's weight vector --
+//      the all-to-all, the update and the all-gather in one pass;
+//   C. the last CTA to finish (threadfence-reduction pattern, system scope) publishes
+//      "my shards are written" and waits for all ranks, so kernel completion means:
+//      every weight of the launch's buckets is final everywhere and no peer still reads
+//      my gradients of those buckets.
 // Non-finite contribution counts are added into every rank's per-step counter.
-// Flags hold monotonically increasing step numbers: no resets between steps.
+// Flags hold monotonically increasing launch numbers: no resets between steps.
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -29,85 +34,183 @@ namespace {
 __device__ __forceinline__ void st_release_sys(unsigned* p, unsigned v) {
   asm volatile("st.release.sys.global.u32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
+__device__ __forceinline__ void st_release_sys64(unsigned* p, unsigned long long v) {
+  asm volatile("st.release.sys.global.u64 [%0], %1;" ::"l"(p), "l"(v) : "memory");
+}
 __device__ __forceinline__ unsigned ld_acquire_sys(const unsigned* p) {
   unsigned v;
   asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
   return v;
 }
-__device__ __forceinline__ void wait_all(const unsigned* f, int n, unsigned step) {
-  const long long t0 = clock64();
+__device__ __forceinline__ unsigned long long ld_acquire_sys64(const unsigned* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+// ~20 s without progress: a peer died or the protocol broke
+__device__ __forceinline__ void check_timeout(unsigned long long t0) {
+  if (gtimer() - t0 > 20000000000ull) __trap();
+}
+__device__ __forceinline__ void wait_all(const unsigned* f, int n, unsigned seq) {
+  const unsigned long long t0 = gtimer();
   for (int r = 0; r < n; ++r)
-    while (ld_acquire_sys(f + r) < step) {
-      if (clock64() - t0 > 40000000000ll) __trap();  // ~20 s: a peer died or the protocol broke
-    }
+    while (ld_acquire_sys(f + r) < seq) check_timeout(t0);
 }
-
-__device__ __forceinline__ void load8h(const __half* p, float (&o)[8], int& nf) {
-  const uint4 u = __ldcv(reinterpret_cast<const uint4*>(p));  // peer memory: no stale L1 / L2 lines
-  const __half2* h = reinterpret_cast<const __half2*>(&u);
-#pragma unroll
-  for (int i = 0; i < 4; ++i) {
-    const float2 f = __half22float2(h[i]);
-    o[2 * i] = f.x;
-    o[2 * i + 1] = f.y;
+__device__ __forceinline__ void spin_ns(unsigned long long ns) {
+  const unsigned long long t0 = gtimer();
+  while (gtimer() - t0 < ns) {
   }
-  const uint32_t w[4] = {u.x, u.y, u.z, u.w};
-#pragma unroll
-  for (int i = 0; i < 4; ++i) nf += ((w[i] & 0x7C00u) == 0x7C00u) + ((w[i] & 0x7C000000u) == 0x7C000000u);
 }
 
-template <int OPT>
+// 8 consecutive contributions of one contributor: raw registers, then fp32
+template <typename GT>
+struct PV;
+template <>
+struct PV<__half> {
+  struct raw_t { uint4 u; };
+  __device__ static raw_t load(const void* base, long e) {
+    return {__ldcg(reinterpret_cast<const uint4*>(static_cast<const __half*>(base) + e))};
+  }
+  __device__ static void cvt(const raw_t& r, float (&o)[8], int& nf) {
+    const __half2* h = reinterpret_cast<const __half2*>(&r.u);
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      const float2 f = __half22float2(h[i]);
+      o[2 * i] = f.x;
+      o[2 * i + 1] = f.y;
+    }
+    const uint32_t w[4] = {r.u.x, r.u.y, r.u.z, r.u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) nf += ((w[i] & 0x7C00u) == 0x7C00u) + ((w[i] & 0x7C000000u) == 0x7C000000u);
+  }
+};
+template <>
+struct PV<float> {
+  struct raw_t { float4 a, b; };
+  __device__ static raw_t load(const void* base, long e) {
+    const float4* p = reinterpret_cast<const float4*>(static_cast<const float*>(base) + e);
+    return {__ldcg(p), __ldcg(p + 1)};
+  }
+  __device__ static void cvt(const raw_t& r, float (&o)[8], int& nf) {
+    o[0] = r.a.x; o[1] = r.a.y; o[2] = r.a.z; o[3] = r.a.w;
+    o[4] = r.b.x; o[5] = r.b.y; o[6] = r.b.z; o[7] = r.b.w;
+#pragma unroll
+    for (int i = 0; i < 8; ++i) nf += !isfinite(o[i]);
+  }
+};
+
+// EXT = 0: plain SGD-m / Adam with every contributor (the hot configuration);
+// EXT = 1: L2 term, dynamic-loss-scale skip / device alpha, partial collection.
+template <typename GT, int OPT, bool EXT>
 __global__ void __launch_bounds__(256) exch_update_kernel(const __grid_constant__ P2PArgs a) {
   __shared__ int s_nf;
   __shared__ int s_last;
-  const int N = a.N, NR = a.NR;
-  // ---- A: my gradients are complete (stream order: this kernel runs after the backward)
-  if (blockIdx.x == 0 && threadIdx.x < NR) {
-    __threadfence_system();
-    st_release_sys(a.flag_peer[threadIdx.x] + P2P_FLAG_READY + a.rank, a.step);
+  __shared__ unsigned s_mask;
+  const int N = a.N, NR = a.NR, tid = threadIdx.x;
+  // ---- A: my gradients are complete (stream order: this kernel runs after them)
+  if (blockIdx.x == 0 && tid < 32) {
+    if (a.loopback) {
+      if (tid < N) {  // contributor tid = gradient slot tid
+        if (EXT && ((a.straggler_mask >> tid) & 1u)) spin_ns(a.straggler_ns);
+        __threadfence_system();
+        st_release_sys(a.flag_local + P2P_FLAG_READY + tid, a.seq);
+      }
+    } else if (tid < NR) {
+      if (EXT && ((a.straggler_mask >> a.rank) & 1u)) spin_ns(a.straggler_ns);
+      __threadfence_system();
+      st_release_sys(a.flag_peer[tid] + P2P_FLAG_READY + a.rank, a.seq);
+    }
   }
-  if (threadIdx.x == 0) {
+  if (EXT && a.quorum > 0 && a.rank == 0 && blockIdx.x == 0 && tid == 32) {
+    // partial collection, rank 0 decides: the first `quorum` contributors seen ready
+    const unsigned long long t0 = gtimer();
+    unsigned m = 0;
+    for (;;) {
+      m = 0;
+      for (int r = 0; r < N; ++r)
+        if (ld_acquire_sys(a.flag_local + P2P_FLAG_READY + r) >= a.seq) m |= 1u << r;
+      if (__popc(m) >= a.quorum) break;
+      check_timeout(t0);
+    }
+    const unsigned long long dec = ((unsigned long long)a.seq << 32) | m;
+    for (int r = 0; r < NR; ++r)
+      st_release_sys64((a.loopback ? a.flag_local : a.flag_peer[r]) + P2P_DECISION, dec);
+  }
+  if (tid == 0) {
     s_nf = 0;
-    wait_all(a.flag_local + P2P_FLAG_READY, NR, a.step);
+    if (EXT && a.quorum > 0) {
+      const unsigned long long t0 = gtimer();
+      unsigned long long dec;
+      while (((dec = ld_acquire_sys64(a.flag_local + P2P_DECISION)) >> 32) < a.seq) check_timeout(t0);
+      s_mask = (unsigned)(dec & 0xffffffffu);
+    } else {
+      wait_all(a.flag_local + P2P_FLAG_READY, N, a.seq);
+      s_mask = (N >= 32) ? 0xffffffffu : ((1u << N) - 1u);
+    }
   }
   __syncthreads();
-  // ---- B: owned 8-element vectors of every bucket (none on a skipped step)
+  // ---- B: owned 8-element vectors of the launch's buckets (none on a skipped step)
+  const unsigned mask = s_mask;
   int nf = 0;
-  const long total = (a.skip && *a.skip) ? 0 : a.vpre[a.nb];
-  const float inv_scale = a.alpha_dev ? (float)(1.0 / (a.n_workers * (double)*a.alpha_dev)) : a.inv_scale;
-  for (long v = blockIdx.x * (long)blockDim.x + threadIdx.x; v < total; v += (long)gridDim.x * blockDim.x) {
-    int bi = 0;
-    while (v >= a.vpre[bi + 1]) ++bi;
-    const long k = (v - a.vpre[bi]) << 3;
+  const long v0 = a.vpre[a.bk0];
+  const long total = (EXT && a.skip && *a.skip) ? 0 : a.vpre[a.bk1] - v0;
+  float inv_scale = a.inv_scale;
+  if (EXT) {
+    if (a.quorum > 0) inv_scale = (float)(1.0 / ((double)__popc(mask) * a.alpha));  // divide by the actual count
+    else if (a.alpha_dev) inv_scale = (float)(1.0 / (a.n_workers * (double)*a.alpha_dev));
+  }
+  int bi = a.bk0;
+  for (long v = blockIdx.x * (long)blockDim.x + tid; v < total; v += (long)gridDim.x * blockDim.x) {
+    const long vg = v0 + v;
+    while (vg >= a.vpre[bi + 1]) ++bi;
+    const long k = (vg - a.vpre[bi]) << 3;
     const long e = a.off[bi] + (long)a.rank * a.shard[bi] + k;  // element in the parameter vector
     const long m = a.moff[bi] + k;                              // element in my master shard
-    float s[8];
-    load8h(a.g_peer[0] + e, s, nf);
-    for (int r = 1; r < N; ++r) {
-      float t[8];
-      load8h(a.g_peer[r] + e, t, nf);
+    // every contribution's load in flight before the first add
+    typename PV<GT>::raw_t raw[P2P_MAX_RANKS];
 #pragma unroll
-      for (int i = 0; i < 8; ++i) s[i] = __fadd_rn(s[i], t[i]);
+    for (int r = 0; r < P2P_MAX_RANKS; ++r)
+      if (r < N && ((mask >> r) & 1u)) raw[r] = PV<GT>::load(a.g_peer[r], e);
+    const float4 W0 = *reinterpret_cast<const float4*>(a.W + m), W1 = *reinterpret_cast<const float4*>(a.W + m + 4);
+    const float4 H0 = *reinterpret_cast<const float4*>(a.S1 + m), H1 = *reinterpret_cast<const float4*>(a.S1 + m + 4);
+    float s[8];
+    bool first = true;
+#pragma unroll
+    for (int r = 0; r < P2P_MAX_RANKS; ++r) {
+      if (r < N && ((mask >> r) & 1u)) {
+        float t[8];
+        PV<GT>::cvt(raw[r], t, nf);
+        if (first) {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) s[i] = t[i];
+          first = false;
+        } else {
+#pragma unroll
+          for (int i = 0; i < 8; ++i) s[i] = __fadd_rn(s[i], t[i]);  // rank order (R14)
+        }
+      }
     }
-    float4 W0 = *reinterpret_cast<const float4*>(a.W + m), W1 = *reinterpret_cast<const float4*>(a.W + m + 4);
-    float4 H0 = *reinterpret_cast<const float4*>(a.S1 + m), H1 = *reinterpret_cast<const float4*>(a.S1 + m + 4);
     float w[8] = {W0.x, W0.y, W0.z, W0.w, W1.x, W1.y, W1.z, W1.w};
     float h[8] = {H0.x, H0.y, H0.z, H0.w, H1.x, H1.y, H1.z, H1.w};
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       s[i] = __fmul_rn(s[i], inv_scale);
       // L2 (reading Q16): + fp32(2 l2) * fp16(W), the working weight of this step
-      if (a.l2x2 != 0.f) s[i] = __fadd_rn(s[i], __fmul_rn(a.l2x2, __half2float(__float2half_rn(w[i]))));
+      if (EXT && a.l2x2 != 0.f) s[i] = __fadd_rn(s[i], __fmul_rn(a.l2x2, __half2float(__float2half_rn(w[i]))));
     }
     if (OPT == 0) {
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
-        const float g = s[i];
-        h[i] = __fsub_rn(__fmul_rn(a.mom, h[i]), __fmul_rn(a.lam, g));
+        h[i] = __fsub_rn(__fmul_rn(a.mom, h[i]), __fmul_rn(a.lam, s[i]));
         w[i] = __fadd_rn(w[i], h[i]);
       }
     } else {
-      float4 V0 = *reinterpret_cast<const float4*>(a.S2 + m), V1 = *reinterpret_cast<const float4*>(a.S2 + m + 4);
+      const float4 V0 = *reinterpret_cast<const float4*>(a.S2 + m), V1 = *reinterpret_cast<const float4*>(a.S2 + m + 4);
       float vv[8] = {V0.x, V0.y, V0.z, V0.w, V1.x, V1.y, V1.z, V1.w};
 #pragma unroll
       for (int i = 0; i < 8; ++i) {
@@ -128,33 +231,44 @@ __global__ void __launch_bounds__(256) exch_update_kernel(const __grid_constant_
 #pragma unroll
     for (int i = 0; i < 4; ++i) o[i] = __halves2half2(__float2half_rn(w[2 * i]), __float2half_rn(w[2 * i + 1]));
     const uint4 ov = *reinterpret_cast<const uint4*>(o);
-    for (int r = 0; r < N; ++r) __stcg(reinterpret_cast<uint4*>(a.w_peer[r] + e), ov);  // all-gather by peer stores
+#pragma unroll
+    for (int r = 0; r < P2P_MAX_RANKS; ++r)
+      if (r < N) __stcg(reinterpret_cast<uint4*>(a.w_peer[r] + e), ov);  // all-gather by peer stores
   }
   // ---- C: completion
-  if (nf) atomicAdd(&s_nf, nf);
+  nf = __reduce_add_sync(0xffffffffu, nf);
+  if ((tid & 31) == 0 && nf) atomicAdd(&s_nf, nf);
   __syncthreads();
-  if (threadIdx.x == 0) {
+  if (tid == 0) {
     if (s_nf)
       for (int r = 0; r < NR; ++r) atomicAdd_system(a.status_peer[r] + (a.step & 1), s_nf);
     __threadfence_system();
     const unsigned prev = atomicAdd(a.flag_local + P2P_CTR, 1u);
-    s_last = prev == a.step * gridDim.x - 1;
+    s_last = prev == a.ctr_target - 1;
   }
   __syncthreads();
-  if (s_last && threadIdx.x < NR) {
+  if (s_last && tid < NR) {
     __threadfence_system();
-    st_release_sys(a.flag_peer[threadIdx.x] + P2P_FLAG_DONE + a.rank, a.step);
+    st_release_sys(a.flag_peer[tid] + P2P_FLAG_DONE + a.rank, a.seq);
   }
-  if (s_last && threadIdx.x == 0) wait_all(a.flag_local + P2P_FLAG_DONE, NR, a.step);
+  if (s_last && tid == 0) wait_all(a.flag_local + P2P_FLAG_DONE, NR, a.seq);
 }
 
 }  // namespace
 
-cudaError_t launch_exch_update(const P2PArgs& a, int optimizer, int grid, cudaStream_t s) {
-  if (optimizer == 0)
-    exch_update_kernel<0><<<grid, 256, 0, s>>>(a);
-  else
-    exch_update_kernel<1><<<grid, 256, 0, s>>>(a);
+cudaError_t launch_exch_update(const P2PArgs& a, int optimizer, int grad_f32, int grid, cudaStream_t s) {
+  const bool ext = a.l2x2 != 0.f || a.alpha_dev || a.skip || a.quorum > 0 || a.straggler_mask;
+#define HDP_EXCH(GT, OPT)                                                                  \
+  (ext ? (exch_update_kernel<GT, OPT, true><<<grid, 256, 0, s>>>(a), 0)                    \
+       : (exch_update_kernel<GT, OPT, false><<<grid, 256, 0, s>>>(a), 0))
+  if (grad_f32) {
+    if (optimizer == 0) HDP_EXCH(float, 0);
+    else HDP_EXCH(float, 1);
+  } else {
+    if (optimizer == 0) HDP_EXCH(__half, 0);
+    else HDP_EXCH(__half, 1);
+  }
+#undef HDP_EXCH
   return cudaGetLastError();
 }
 

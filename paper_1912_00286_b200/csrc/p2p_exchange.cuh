@@ -8,23 +8,29 @@ namespace hdp {
 constexpr int P2P_MAX_RANKS = 8;
 constexpr int P2P_MAX_BUCKETS = 16;
 // per-rank flag block (unsigned words)
-constexpr int P2P_FLAG_READY = 0;    // [8]: rank r's gradients of step s complete
-constexpr int P2P_FLAG_DONE = 32;    // [8]: rank r's owned shards written everywhere
+constexpr int P2P_FLAG_READY = 0;    // [8]: contributor r's gradients of launch `seq` complete
+constexpr int P2P_FLAG_DONE = 32;    // [8]: rank r's owned shards of launch `seq` written everywhere
 constexpr int P2P_CTR = 64;          // this rank's CTA completion counter (monotonic)
+constexpr int P2P_DECISION = 80;     // 2 words (8-byte aligned): (seq << 32) | contributor mask, from rank 0
 constexpr int P2P_STATUS = 96;       // [2] ints: non-finite count of step s in slot s & 1
 constexpr int P2P_FLAG_WORDS = 128;
 
 struct P2PArgs {
-  // N = gradient contributions summed (and weight copies written); NR = ranks in the
-  // flag protocol.  Across processes N = NR = world.  Loopback (world 1, N simulated
-  // workers): the contributions are the local gradient slots, the weight copies local
-  // buffers, and the protocol runs with NR = 1.
+  // N = gradient contributors summed (and weight copies written); NR = ranks in the
+  // flag protocol.  Across processes N = NR = world and contributor r is rank r.
+  // Loopback (world 1, N simulated workers): the contributions are the local gradient
+  // slots, the weight copies local buffers, every READY flag is published by this
+  // process (contributor r = slot r) and NR = 1.
   int N = 1, NR = 1, rank = 0;
-  unsigned step = 0;
+  int loopback = 0;
+  unsigned seq = 0;                      // launch sequence number (flags; monotonic, same on every rank)
+  unsigned step = 0;                     // update count (non-finite status slot step & 1)
+  unsigned ctr_target = 0;               // cumulative CTA count after this launch (last-CTA detection)
+  int bk0 = 0, bk1 = 0;                  // buckets [bk0, bk1) of this launch
   int nb = 0;
   long off[P2P_MAX_BUCKETS] = {}, shard[P2P_MAX_BUCKETS] = {}, moff[P2P_MAX_BUCKETS] = {};
   long vpre[P2P_MAX_BUCKETS + 1] = {};   // prefix sums of owned 8-element vectors per bucket
-  const __half* g_peer[P2P_MAX_RANKS] = {};
+  const void* g_peer[P2P_MAX_RANKS] = {};  // fp16 or fp32 gradient vectors (wire type)
   __half* w_peer[P2P_MAX_RANKS] = {};
   unsigned* flag_peer[P2P_MAX_RANKS] = {};
   int* status_peer[P2P_MAX_RANKS] = {};
@@ -36,8 +42,17 @@ struct P2PArgs {
   const float* alpha_dev = nullptr;  // dynamic loss scaling, see UpdateArgs
   double n_workers = 1.0;
   const int* skip = nullptr;
+  // NEXT-2 partial collection: 0 < quorum < N makes rank 0
+  // proceed once `quorum` contributors are ready and publish their set; every owner sums
+  // exactly that set (rank order) and divides by its size.  0 = all N (lock-step).
+  int quorum = 0;
+  double alpha = 10.0;               // static alpha (partial collection descale in fp64)
+  // test injection: contributors in straggler_mask publish READY straggler_ns late
+  unsigned straggler_mask = 0;
+  unsigned long long straggler_ns = 0;
 };
 
-cudaError_t launch_exch_update(const P2PArgs& a, int optimizer, int grid, cudaStream_t s);
+// grad_f32: the wire carries fp32 gradients (HDP_WIRE_FP32) instead of fp16
+cudaError_t launch_exch_update(const P2PArgs& a, int optimizer, int grad_f32, int grid, cudaStream_t s);
 
 }  // namespace hdp

@@ -30,6 +30,7 @@
 #include <algorithm>
 
 #include "gemm.cuh"
+#include "options.h"
 #include "ptx.cuh"
 #include "recur.cuh"
 
@@ -263,7 +264,7 @@ bool plan_fwd(int B, int hp, FwdPlan* p) {
   if (B < 16 || (B & 15) || (hp & 15)) return false;
   p->G = (4 * hp + 127) / 128;
   int force = 0;
-  if (const char* e = getenv("HDP_RECUR_NBG")) force = atoi(e);
+  force = opt(OPT_RECUR_NBG);
   int best = 0;
   for (int nbg = 16; nbg >= 1; nbg >>= 1) {
     if (force && nbg != force) continue;
@@ -497,7 +498,7 @@ bool plan_bwd(int B, int hp, int* Bc_out, int* nbg_out) {
   if (B < 16 || (B & 15) || (hp & 15)) return false;
   const int G = (hp + 63) / 64;
   int force = 0;
-  if (const char* e = getenv("HDP_RECUR_NBG")) force = atoi(e);
+  force = opt(OPT_RECUR_NBG);
   for (int nbg = 16; nbg >= 1; nbg >>= 1) {
     if (force && nbg != force) continue;
     if (B % nbg) continue;
@@ -1811,8 +1812,7 @@ cudaError_t launch_cluster(const void* fn, dim3 grid, dim3 block, size_t smem, i
 }
 
 bool use_cluster() {
-  const char* e = getenv("HDP_RECUR_CLUSTER");
-  return !(e && e[0] == '0');
+  return opt(OPT_RECUR_CLUSTER) != 0;
 }
 
 int pow2ceil(int v) {
@@ -1822,303 +1822,6 @@ int pow2ceil(int v) {
 }
 
 
-// ============================================================== 2-layer wavefront (forward)
-// One cluster of 3G CTAs per batch group of 16 columns (G = ceil(hp/64)):
-//   role 0 (R0_k): layer-0 recurrence, units [64k, 64k+64)
-//   role 1 (P_k) : layer-1 input projection a1x_t = W1 h0_t + b1, gate rows [256k, 256k+256)
-//   role 2 (R1_k): layer-1 recurrence, units [64k, 64k+64), a1x from P_k
-// Layer 1 runs one step behind layer 0, so the two layers' T-step chains
-// overlap (critical path ~T+2 steps instead of 2T).  Hand-offs:
-//   R0_k --h0_t (its K-block)--> all R0 peers (sH) and all P (sIn)   [bulk copy + fullH / fullIn]
-//   P_k  --a1x_t (256 x 16 fp32)--> R1_k (sGx)                        [bulk copy + fullGx]
-//   R1_k --h1_t (its K-block)--> all R1 peers (sH)                     [bulk copy + fullH]
-// Back-pressure (double buffers): P acks R0's emptyIn after its MMA read sIn;
-// R1 acks P's emptyOut after its epilogue read sGx (remote mbarrier arrives).
-template <int BC>
-__global__ void __launch_bounds__(BC * 16, 1)
-    recur2_fwd_kernel(const __grid_constant__ CUtensorMap tmU0, const __grid_constant__ CUtensorMap tmW1,
-                      const __grid_constant__ CUtensorMap tmU1, const float* __restrict__ Gx0,
-                      const __half* __restrict__ b1, int T, int B, int hp, __half* __restrict__ Hs0,
-                      float* __restrict__ C0, __half* __restrict__ gates0, __half* __restrict__ Hs1,
-                      float* __restrict__ C1, __half* __restrict__ gates1, unsigned long long* __restrict__ trace) {
-  constexpr int Bc = BC;
-  constexpr int NC = 1;        // each warp handles one 16-column chunk: chunk = cg
-  constexpr int NACC = 4;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int nkb = (hp + 63) / 64;
-  const int nk16 = (hp + 15) / 16;
-  const int G = nkb;
-  const int hbuf = nkb * Bc * 128;
-  uint8_t* sA = smem;                          // [2 halves][nkb][16 KB] resident A slice (U0 / W1 / U1)
-  uint8_t* sB = sA + 2 * nkb * 16384;          // [2][hbuf] B operand (h of the previous / same step)
-  uint8_t* sX = sB + 2 * hbuf;                 // [2][Bc][128 B] staging of my h_t K-block
-  float* sAct = reinterpret_cast<float*>(sX + 2 * Bc * 128);   // [warps][8 columns][ACT_LD]
-  float* sG = sAct + (BC / 2) * 8 * ACT_LD;          // [Bc][256] fp32: P out staging / R1 a1x input (single buffer)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sG + Bc * 256);
-  uint64_t* barU = bars;
-  uint64_t* barM = bars + 1;
-  uint64_t* fullB = bars + 2;                  // [2] B operand delivered
-  uint64_t* fullG = bars + 4;                  // R1: a1x delivered (single slot)
-  uint64_t* emptyA = bars + 6;                 // [2] R0: P consumed my slice (count G); P: [0] R1 consumed a1x (count 1)
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 8);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int quarter = warp & 3, hf = (warp >> 2) & 1, cg = warp >> 3;  // BC/16 column groups
-  const int rank = blockIdx.x;
-  const int role = rank / G, k = rank % G;
-  const int col0 = blockIdx.y * Bc + cg * 16;  // this warp's 16 batch columns
-  const int r = hf * 128 + quarter * 32 + lane;
-  const int grow = k * 256 + r;
-  const int gate = r & 3;
-  const int unit = grow >> 2;
-  const bool unit_ok = unit < hp;
-  const int fourhp = 4 * hp;
-  const int nis = min(NACC, nk16);
-  const int total_bytes = nkb * Bc * 128;
-  const CUtensorMap* tmA = role == 0 ? &tmU0 : role == 1 ? &tmW1 : &tmU1;
-  // debug trace: CTA k == 0 of each role, batch group 0, thread 0: [role][t][5]
-  const bool tr = trace != nullptr && k == 0 && blockIdx.y == 0 && threadIdx.x == 0;
-  unsigned long long* trr = trace ? trace + (size_t)role * T * 5 : nullptr;
-#define TR(t, i) \
-  if (tr) trr[(t) * 5 + (i)] = ptx::globaltimer_ns()
-
-  if (threadIdx.x == 0) {
-    ptx::tma_prefetch(tmA);
-    ptx::mbar_init(barU, 1);
-    ptx::mbar_init(barM, nis);
-    for (int i = 0; i < 2; ++i) {
-      ptx::mbar_init(fullB + i, 1);
-      ptx::mbar_init(fullG + i, 1);
-      ptx::mbar_init(emptyA + i, role == 0 ? G : 1);
-    }
-    ptx::fence_mbar_init();
-  }
-  constexpr uint32_t TCOLS = 2 * NACC * Bc <= 128 ? 128 : 256;
-  if (warp == 2) ptx::tmem_alloc(tslot, TCOLS);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tbase = *tslot;
-  if (threadIdx.x == 0) {
-    // arm first uses; load the resident A slice
-    ptx::mbar_arrive_expect_tx(fullB, total_bytes);
-    ptx::mbar_arrive_expect_tx(fullB + 1, total_bytes);
-    if (role == 2) ptx::mbar_arrive_expect_tx(fullG, Bc * 256 * 4);
-    ptx::mbar_arrive_expect_tx(barU, 2 * nkb * 16384);
-    for (int h2 = 0; h2 < 2; ++h2)
-      for (int kb = 0; kb < nkb; ++kb)
-        ptx::tma_load_2d(sA + (h2 * nkb + kb) * 16384, tmA, barU, kb * 64, k * 256 + h2 * 128);
-    ptx::mbar_wait(barU, 0);
-  }
-  ptx::cluster_arrive();
-  ptx::cluster_wait();
-
-  const uint32_t idesc = ptx::idesc_f16_f32(128, Bc, 0, 0);
-  float* myAct = sAct + warp * 8 * ACT_LD;  // 8 columns staged at a time
-  const float gsc = gate == 2 ? 2.f : 1.f;
-  const uint32_t sB_addr = ptx::smem_u32(sB), sX_addr = ptx::smem_u32(sX), sG_addr = ptx::smem_u32(sG);
-  uint32_t fph[2] = {0u, 0u}, eph[2] = {0u, 0u};
-  uint32_t gph = 0, oph = 0, mph = 0;
-  float creg[NC * 4];
-#pragma unroll
-  for (int i = 0; i < NC * 4; ++i) creg[i] = 0.f;
-
-  // MMA over the resident A slice (two M=128 halves) and B operand slot p
-  auto issue_mma = [&](int p) {
-    const uint32_t aA = ptx::smem_u32(sA), aB = sB_addr + p * hbuf;
-    const uint64_t ad0 = ptx::smem_desc_sw128(aA, 0, 1024), bd0 = ptx::smem_desc_sw128(aB, 0, 1024);
-    for (int kk = warp; kk < nk16; kk += nis) {
-      const int kb = kk >> 2, kq = kk & 3;
-      const uint64_t bd = bd0 + (uint64_t)((kb * Bc * 128 + kq * 32) >> 4);
-#pragma unroll
-      for (int h2 = 0; h2 < 2; ++h2) {
-        const uint64_t ad = ad0 + (uint64_t)(((h2 * nkb + kb) * 16384 + kq * 32) >> 4);
-        ptx::mma_f16(tbase + (h2 * NACC + warp) * Bc, ad, bd, idesc, kk >= nis ? 1u : 0u);
-      }
-    }
-    ptx::mma_commit(barM);
-  };
-  auto load_acc = [&](float (&v)[16], int c0) {
-    const uint32_t ta = tbase + (static_cast<uint32_t>(quarter * 32) << 16) + hf * NACC * Bc + c0;
-    float w[NACC - 1][16];
-    ptx::tmem_ld16_nowait(ta, v);
-#pragma unroll
-    for (int a = 1; a < NACC; ++a)
-      if (a < nis) ptx::tmem_ld16_nowait(ta + a * Bc, w[a - 1]);
-    ptx::tmem_wait_ld();
-#pragma unroll
-    for (int a = 1; a < NACC; ++a)
-      if (a < nis)
-#pragma unroll
-        for (int q = 0; q < 16; ++q) v[q] += w[a - 1][q];
-  };
-
-  if (role == 1) {
-    // ---------------------------------------------------------------- projection P_k
-    float bias = unit_ok ? __half2float(b1[grow]) : 0.f;
-    for (int t = 0; t < T; ++t) {
-      const int p = t & 1;
-      TR(t, 0);
-      if (lane == 0 && warp < nis) {
-        ptx::mbar_wait(fullB + p, fph[p]);  // h0_t from every R0
-        TR(t, 1);
-        ptx::tc_fence_after();
-        issue_mma(p);
-      }
-      __syncwarp();
-      ptx::mbar_wait_relaxed(barM, mph);
-      mph ^= 1u;
-      ptx::tc_fence_after();
-      fph[p] ^= 1u;
-      if (threadIdx.x == 0) {
-        if (t + 2 <= T - 1) ptx::mbar_arrive_expect_tx(fullB + p, total_bytes);
-        // sIn[p] consumed: ack every R0 (they may overwrite it / their staging)
-        for (int j = 0; j < G; ++j) ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(emptyA + p), j));
-      }
-      TR(t, 2);
-      // out staging free? (R1 consumed a1x_{t-1}, so its copy from my staging completed too)
-      if (t >= 1) {
-        ptx::mbar_wait_cluster(emptyA, oph);
-        oph ^= 1u;
-      }
-      TR(t, 3);
-      {
-        float v[16];
-        load_acc(v, cg * 16);
-#pragma unroll
-        for (int q = 0; q < 16; ++q) sG[(cg * 16 + q) * 256 + r] = v[q] + bias;
-      }
-      ptx::tc_fence_before();
-      ptx::fence_async_smem();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        const int dst = 2 * G + k;  // R1_k
-        ptx::bulk_copy_to_peer(ptx::mapa(sG_addr, dst), sG_addr, Bc * 256 * 4, ptx::mapa(ptx::smem_u32(fullG), dst));
-      }
-      TR(t, 4);
-    }
-  } else {
-    // ---------------------------------------------------------------- recurrence R0_k / R1_k
-    const bool L1 = role == 2;
-    __half* Hs = L1 ? Hs1 : Hs0;
-    float* Cst = L1 ? C1 : C0;
-    __half* gts = L1 ? gates1 : gates0;
-    const int peer0 = role * G;  // first CTA of my layer
-    for (int t = 0; t < T; ++t) {
-      const int p = t & 1;
-      TR(t, 0);
-      float gx[NC][16];
-      if (!L1) {
-        const float* gp = Gx0 + ((size_t)t * B + col0) * fourhp + grow;
-#pragma unroll
-        for (int ch = 0; ch < NC; ++ch)
-#pragma unroll
-          for (int q = 0; q < 16; ++q) gx[ch][q] = unit_ok ? __ldg(gp + (size_t)(ch * 16 + q) * fourhp) : 0.f;
-      }
-      if (t > 0) {
-        const int pp = (t - 1) & 1;
-        if (lane == 0 && warp < nis) {
-          ptx::mbar_wait(fullB + pp, fph[pp]);  // h_{t-1} of my layer from every peer
-          TR(t, 1);
-          ptx::tc_fence_after();
-          issue_mma(pp);
-        }
-        __syncwarp();
-        ptx::mbar_wait_relaxed(barM, mph);
-        mph ^= 1u;
-        ptx::tc_fence_after();
-        fph[pp] ^= 1u;
-        if (threadIdx.x == 0 && t + 2 <= T - 1) ptx::mbar_arrive_expect_tx(fullB + pp, total_bytes);
-      }
-      TR(t, 2);
-      if (L1) {
-        ptx::mbar_wait(fullG, gph);  // a1x_t from P_k
-        gph ^= 1u;
-#pragma unroll
-        for (int ch = 0; ch < NC; ++ch)
-#pragma unroll
-          for (int q = 0; q < 16; ++q) gx[ch][q] = sG[(cg * 16 + q) * 256 + r];
-      } else if (t >= 2) {
-        // my staging slot p and P's sIn slot p are free once every P consumed step t-2
-        ptx::mbar_wait_cluster(emptyA + p, eph[p]);
-        eph[p] ^= 1u;
-      }
-      TR(t, 3);
-      __half* hout = Hs + (size_t)(t + 1) * B * hp;
-      float* cout = Cst + (size_t)t * B * hp;
-      __half* gout = gts + (size_t)t * B * fourhp;
-      uint8_t* stg = sX + p * Bc * 128;
-#pragma unroll
-      for (int ch = 0; ch < NC; ++ch) {
-        float v[16];
-        if (t > 0) {
-          load_acc(v, cg * 16);
-        } else {
-#pragma unroll
-          for (int q = 0; q < 16; ++q) v[q] = 0.f;
-        }
-#pragma unroll
-        for (int hh8 = 0; hh8 < 2; ++hh8) {
-        // stage columns [8*hh8, 8*hh8 + 8) of the chunk, then each lane takes q = 2*hh8, 2*hh8 + 1
-#pragma unroll
-        for (int q = 0; q < 8; ++q) myAct[q * ACT_LD + lane] = act_gate(v[hh8 * 8 + q] + gx[ch][hh8 * 8 + q], gsc);
-        __syncwarp();
-        if (unit_ok) {
-          const int u = lane >> 2;
-          const int ul = r >> 2;
-          const int c = ul >> 3;
-#pragma unroll
-          for (int q = 2 * hh8; q < 2 * hh8 + 2; ++q) {
-            const int col = 4 * q + gate;
-            const float4 a4 = *reinterpret_cast<const float4*>(myAct + (col - 8 * hh8) * ACT_LD + 4 * u);
-            const int bl = cg * 16 + col;                 // row within the CTA's Bc batch rows
-            const size_t b = (size_t)blockIdx.y * Bc + bl;
-            const float i = a4.x, f = a4.y, g = a4.z, o = a4.w;
-            const float cv = f * creg[ch * 4 + q] + i * g;
-            creg[ch * 4 + q] = cv;
-            const __half hh = __float2half_rn(o * act_gate(cv, 2.f));
-            cout[b * hp + unit] = cv;                   // R5
-            hout[b * hp + unit] = hh;                   // R6
-            *reinterpret_cast<__half*>(stg + bl * 128 + ((c ^ (bl & 7)) << 4) + (ul & 7) * 2) = hh;
-            __align__(8) __half2 gg[2] = {__halves2half2(__float2half_rn(i), __float2half_rn(f)),
-                                          __halves2half2(__float2half_rn(g), __float2half_rn(o))};
-            *reinterpret_cast<uint2*>(gout + b * fourhp + 4 * unit) = *reinterpret_cast<const uint2*>(gg);  // R4
-          }
-        }
-        __syncwarp();
-        }
-      }
-      ptx::tc_fence_before();
-      ptx::fence_async_smem();
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        if (L1) {
-          // a1x read: re-arm for step t+1, then ack P_k (its next copy may land only after the re-arm)
-          if (t + 1 <= T - 1) ptx::mbar_arrive_expect_tx(fullG, Bc * 256 * 4);
-          ptx::mbar_arrive_remote(ptx::mapa(ptx::smem_u32(emptyA), G + k));
-        }
-      }
-      // push h_t: my K-block to my layer's peers (consumed at t+1), and h0_t to every P (consumed at t)
-      if (threadIdx.x < G) {
-        const int dst = peer0 + threadIdx.x;
-        if (t < T - 1)
-          ptx::bulk_copy_to_peer(ptx::mapa(sB_addr + p * hbuf + k * Bc * 128, dst), sX_addr + p * Bc * 128,
-                                 Bc * 128, ptx::mapa(ptx::smem_u32(fullB + p), dst));
-      } else if (!L1 && threadIdx.x >= 32 && threadIdx.x < 32 + G) {
-        const int dst = G + (threadIdx.x - 32);
-        ptx::bulk_copy_to_peer(ptx::mapa(sB_addr + p * hbuf + k * Bc * 128, dst), sX_addr + p * Bc * 128, Bc * 128,
-                               ptx::mapa(ptx::smem_u32(fullB + p), dst));
-      }
-      TR(t, 4);
-    }
-  }
-#undef TR
-  ptx::cluster_arrive();
-  ptx::cluster_wait();
-  ptx::tc_fence_after();
-  if (warp == 2) ptx::tmem_dealloc(tbase, TCOLS);
-}
 
 
 // ============================================================== 2-layer wavefront (forward, split clusters)
@@ -2647,11 +2350,6 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
   if (warp == 2) ptx::tmem_dealloc(tbase, tcols);
 }
 
-size_t recur2_fwd_smem(int hp, int Bc) {
-  const int nkb = (hp + 63) / 64;
-  return 1024 + 2 * (size_t)nkb * 16384 + 2 * (size_t)nkb * Bc * 128 + 2 * (size_t)Bc * 128 +
-         (size_t)(Bc / 2) * 8 * ACT_LD * 4 + (size_t)Bc * 256 * 4 + 128;
-}
 
 }  // namespace
 
@@ -2747,8 +2445,7 @@ const void* recur2f_fn_nks(int nk16) {
        : nk16 == 16 ? (const void*)recur2f_kernel<NCI, 16> : (const void*)recur2f_kernel<NCI, 0>;
 }
 const void* recur2f_fn(int nci, int hp) {
-  const char* e = getenv("HDP_WAVEFRONT_TS");
-  const int nk16 = (e && e[0] == '0') ? -1 : (hp + 15) / 16;  // -1: the generic (SMEM-A) instantiation
+  const int nk16 = opt(OPT_WAVEFRONT_TMEM) == 0 ? -1 : (hp + 15) / 16;  // -1: the generic (SMEM-A) instantiation
   return nci == 1 ? recur2f_fn_nks<1>(nk16) : nci == 2 ? recur2f_fn_nks<2>(nk16) : nullptr;
 }
 bool plan_w2f(int B, int hp, W2Plan* out) {
@@ -2773,8 +2470,7 @@ bool plan_w2f(int B, int hp, W2Plan* out) {
       p.nci = 1;
       size_t smem = fwd_cl_smem(hp, Bc, 8 * p.cgN);
       if (smem > 227 * 1024) continue;
-      const char* fe = getenv("HDP_WAVEFRONT_FUSEX");
-      if (!(fe && fe[0] == '0') && smem + w2f_fuse_bytes(Bc) <= 227 * 1024) {
+      if (opt(OPT_WAVEFRONT_FUSEX) != 0 && smem + w2f_fuse_bytes(Bc) <= 227 * 1024) {
         smem += w2f_fuse_bytes(Bc);
         p.fuse = 1;
       }
@@ -2804,36 +2500,23 @@ bool plan_w2f(int B, int hp, W2Plan* out) {
   return best.nbg > 0;
 }
 
-bool w2f_split_enabled() {
-  const char* e = getenv("HDP_WAVEFRONT_FWD");
-  return !(e && e[0] == '1');  // HDP_WAVEFRONT_FWD=1: the single-cluster variant
-}
-
 bool recur2_fwd_fuses_x(int B, int hp, int Ip0) {
   W2Plan p;
   // (with the A slices in TMEM, columns [256, 256 + 2*KCP) + 2 x 16 for W0 must fit in 512)
-  return recur2_fwd_supported(B, hp) && w2f_split_enabled() && plan_w2f(B, hp, &p) && p.fuse && Ip0 <= 16 &&
+  return recur2_fwd_supported(B, hp) && plan_w2f(B, hp, &p) && p.fuse && Ip0 <= 16 &&
          256 + 2 * ((hp + 31) / 32 * 16) + 32 <= 512 &&
-         !(getenv("HDP_WAVEFRONT_FUSEX") && getenv("HDP_WAVEFRONT_FUSEX")[0] == '0');
+         opt(OPT_WAVEFRONT_FUSEX) != 0;
 }
 
 bool recur2_fwd_supported(int B, int hp) {
-  const char* e = getenv("HDP_WAVEFRONT");
-  if (e && e[0] == '0') return false;
-  if (w2f_split_enabled()) {
-    W2Plan p;
-    return plan_w2f(B, hp, &p);
-  }
-  if (B % 32 || (hp & 15) || hp > 256) return false;
-  const int G = (hp + 63) / 64;
-  if (3 * G > 16) return false;
-  if ((size_t)G * 3 * (B / 32) > 148) return false;
-  return recur2_fwd_smem(hp, 32) <= 227 * 1024;
+  if (opt(OPT_WAVEFRONT) == 0) return false;
+  W2Plan p;
+  return plan_w2f(B, hp, &p);
 }
 
 cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
   if (!recur2_fwd_supported(a.B, a.hp)) return cudaErrorInvalidConfiguration;
-  if (w2f_split_enabled()) {
+  {
     W2Plan pl;
     plan_w2f(a.B, a.hp, &pl);
     const int G = (a.hp + 63) / 64;
@@ -2908,55 +2591,6 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
     return launch_cluster(recur2f_fn(pl.nci, a.hp), dim3(G, 3 * pl.nbg), dim3(256 * pl.cgN),
                           fwd_cl_smem(a.hp, pl.Bc, 8 * pl.cgN) + (pl.fuse ? w2f_fuse_bytes(pl.Bc) : 0), G, s, args);
   }
-  CUtensorMap mU0, mW1, mU1;
-  const uint64_t hp = a.hp;
-  if (encode_tmap_2d(&mU0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U0, hp, 4 * hp, hp * 2, 64, 128,
-                     CU_TENSOR_MAP_SWIZZLE_128B) ||
-      encode_tmap_2d(&mW1, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.W1, hp, 4 * hp, hp * 2, 64, 128,
-                     CU_TENSOR_MAP_SWIZZLE_128B) ||
-      encode_tmap_2d(&mU1, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U1, hp, 4 * hp, hp * 2, 64, 128,
-                     CU_TENSOR_MAP_SWIZZLE_128B))
-    return cudaErrorInvalidValue;
-  const int G = (a.hp + 63) / 64;
-  // batch group width: 16 if all B/16 clusters can be co-resident, else 32
-  int Bc = 16;
-  if (const char* e = getenv("HDP_WAVEFRONT_BC")) Bc = atoi(e) == 32 ? 32 : 16;
-  const void* fn16 = (const void*)recur2_fwd_kernel<16>;
-  const void* fn32 = (const void*)recur2_fwd_kernel<32>;
-  for (const void* f : {fn16, fn32}) {
-    cudaError_t e = cudaFuncSetAttribute(f, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         (int)recur2_fwd_smem(a.hp, f == fn16 ? 16 : 32));
-    if (e != cudaSuccess) return e;
-    if (3 * G > 8) {
-      e = cudaFuncSetAttribute(f, cudaFuncAttributeNonPortableClusterSizeAllowed, 1);
-      if (e != cudaSuccess) return e;
-    }
-  }
-  if (!getenv("HDP_WAVEFRONT_BC")) {
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3(3 * G, a.B / 16);
-    cfg.blockDim = dim3(256);  // BC = 16 -> 8 warps
-    cfg.dynamicSmemBytes = recur2_fwd_smem(a.hp, 16);
-    cudaLaunchAttribute at[1];
-    at[0].id = cudaLaunchAttributeClusterDimension;
-    at[0].val.clusterDim.x = 3 * G;
-    at[0].val.clusterDim.y = 1;
-    at[0].val.clusterDim.z = 1;
-    cfg.attrs = at;
-    cfg.numAttrs = 1;
-    int nclusters = 0;
-    if (cudaOccupancyMaxActiveClusters(&nclusters, fn16, &cfg) != cudaSuccess) nclusters = 0;
-    Bc = (nclusters >= a.B / 16) ? 16 : 32;
-  }
-  const float* gx = a.Gx0;
-  const __half* b1 = a.b1;
-  int T = a.T, B = a.B, hpi = a.hp;
-  __half *hs0 = a.Hs0, *g0 = a.gates0, *hs1 = a.Hs1, *g1 = a.gates1;
-  float *c0 = a.C0, *c1 = a.C1;
-  unsigned long long* trace = a.trace;
-  void* args[] = {&mU0, &mW1, &mU1, &gx, &b1, &T, &B, &hpi, &hs0, &c0, &g0, &hs1, &c1, &g1, &trace};
-  return launch_cluster(Bc == 16 ? fn16 : fn32, dim3(3 * G, a.B / Bc), dim3(16 * Bc), recur2_fwd_smem(a.hp, Bc), 3 * G,
-                        s, args);
 }
 
 }  // namespace hdp
@@ -2967,8 +2601,7 @@ namespace hdp {
 // 4 h_p / 16 = 52 K-steps; everything else runs the SMEM-A variant (HDP_WAVEFRONT_TS=0 forces it)
 template <int NC>
 const void* recur2b_fn_nk(int hp) {
-  const char* e = getenv("HDP_WAVEFRONT_TS");
-  if (e && e[0] == '0') return (const void*)recur2_bwd_kernel<NC, 0>;
+  if (opt(OPT_WAVEFRONT_TMEM) == 0) return (const void*)recur2_bwd_kernel<NC, 0>;
   return 4 * hp / 16 == 52 ? (const void*)recur2_bwd_kernel<NC, 52> : (const void*)recur2_bwd_kernel<NC, 0>;
 }
 const void* recur2b_fn(int Bc, int hp) {
@@ -3039,13 +2672,11 @@ bool plan_w2b(int B, int hp, bool want_wgrad, W2BPlan* out) {
 }
 
 bool wgrad_wanted(int Ip0) {
-  const char* e = getenv("HDP_WAVEFRONT_WGRAD");
-  return !(e && e[0] == '0') && Ip0 > 0 && Ip0 <= 256 && !(Ip0 & 15);
+  return opt(OPT_WAVEFRONT_WGRAD) != 0 && Ip0 > 0 && Ip0 <= 256 && !(Ip0 & 15);
 }
 
 bool recur2_bwd_supported(int B, int hp) {
-  const char* e = getenv("HDP_WAVEFRONT");
-  if (e && e[0] == '0') return false;
+  if (opt(OPT_WAVEFRONT) == 0) return false;
   W2BPlan p;
   return plan_w2b(B, hp, false, &p);
 }

@@ -31,7 +31,7 @@ EXPORTED = [
     "hdp_loss_scale_state", "hdp_lstm_forward",
     "hdp_lstm_backward", "hdp_grad_average_update", "hdp_weights_ptr", "hdp_grads_ptr", "hdp_master_ptr",
     "hdp_fused_avg_update", "hdp_gemm_f16", "hdp_gemm_f32", "hdp_profile", "hdp_profile_read",
-    "hdp_kernel_launches", "hdp_debug_buffer",
+    "hdp_kernel_launches", "hdp_debug_buffer", "hdp_set_option", "hdp_partial_state",
 ]
 NTAGS = 15
 
@@ -101,6 +101,8 @@ def _load():
         "hdp_profile": ([vp, i], i),
         "hdp_profile_read": ([vp, vp, vp, i], i),
         "hdp_kernel_launches": ([vp], ll),
+        "hdp_set_option": ([vp, C.c_char_p, d], i),
+        "hdp_partial_state": ([vp, C.POINTER(C.c_uint), C.POINTER(i)], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -245,6 +247,24 @@ def loss_scale_state(ctx: int):
     a, k = C.c_float(), C.c_int()
     _ck(_lib.hdp_loss_scale_state(ctx, C.byref(a), C.byref(k)))
     return a.value, k.value
+
+
+# process-wide kernel switches and their defaults (csrc/options.h, hdp_set_option)
+KERNEL_OPTION_DEFAULTS = {"persistent": 1, "wavefront": 1, "wavefront_fusex": 1, "wavefront_wgrad": 1,
+                          "wavefront_tmem": 1, "recur_nbg": 0, "recur_cluster": 1, "gemm_cta_group": 0,
+                          "gemm_cluster_n": 0, "pdl": 0, "k7_bn": 0, "k7_splits": 0, "recur_trace": 0}
+
+
+def set_option(ctx, name: str, value: float):
+    """hdp_set_option: context options (ctx) or process-wide kernel switches (ctx may be None)."""
+    _ck(_lib.hdp_set_option(ctx, name.encode(), float(value)))
+
+
+def partial_state(ctx):
+    """(contributor mask, count) of the last partial-collection decision."""
+    m, n = C.c_uint(), C.c_int()
+    _ck(_lib.hdp_partial_state(ctx, C.byref(m), C.byref(n)))
+    return m.value, n.value
 
 
 def lstm_forward(ctx, x, targets, B, T, slot=0, y_out=None, loss_out=None, stream=None):

@@ -37,6 +37,8 @@ def main():
     lam0 = float(os.environ.get("HDP_MP_LAMBDA0", "0"))
     keep = float(os.environ.get("HDP_MP_KEEP", "1"))       # NEXT-3 recurrent dropout (Q16b)
     exch = int(os.environ.get("HDP_MP_EXCH", "0"))         # hdp.EXCH_* (0 auto = NVLink kernel for fp16 a2a)
+    partial = float(os.environ.get("HDP_MP_PARTIAL", "1"))  # NEXT-2 partial collection fraction
+    straggler = int(os.environ.get("HDP_MP_STRAGGLER", "0"))  # ranks that publish readiness 3 ms late
     cfg = synth.CONFIGS[cfg_name]
     if seq:
         cfg = cfg.with_(seq=seq)
@@ -56,6 +58,10 @@ def main():
         hdp.set_dynamic_loss_scale(tr.ctx, dyn)
     if keep < 1.0:
         hdp.set_recurrent_dropout(tr.ctx, keep, 99)
+    if partial < 1.0 or straggler:
+        hdp.set_option(tr.ctx, "partial_fraction", partial)
+        hdp.set_option(tr.ctx, "straggler_mask", straggler)
+        hdp.set_option(tr.ctx, "straggler_us", 3000)
     a_ref, good = alpha, 0
     from oracle import optim as ooptim
     n = tr.n
@@ -82,6 +88,7 @@ def main():
         dist.all_gather_object(g_all, g_mine)
         nf = hdp.grad_average_update(tr.ctx, 0, stream, sync=True)
         torch.cuda.synchronize()
+        pmask, pcount = hdp.partial_state(tr.ctx)
         loss = torch.tensor([tr.loss.item()], device=dev)
         dist.all_reduce(loss)
         master = hdp.gather_master(tr.ctx, n)
@@ -92,7 +99,9 @@ def main():
             lam = float(np.float32(osched.rate_for_epoch(cfg.lambda0, world, cfg.n_half, cfg.gamma, 0)))
             ref = ostep.train_step(cfg, master_ref, state, x, t, world, a_ref, lam, "mixed" if mixed else "fp32",
                                    l2=l2, skip_nonfinite=bool(dyn),
-                                   dropout={"keep": keep, "seed": 99, "step": k} if keep < 1.0 else None)
+                                   dropout={"keep": keep, "seed": 99, "step": k} if keep < 1.0 else None,
+                                   contributors=[r for r in range(world) if (pmask >> r) & 1] if partial < 1.0
+                                   else None)
             skip_ref = False
             if dyn:
                 a_ref, good, skip_ref = ooptim.dynamic_loss_scale(a_ref, good, ref["nonfinite"], dyn)
@@ -100,6 +109,7 @@ def main():
                          "skip_gpu": bool(dyn and nf > 0), "skip_ref": bool(skip_ref), "alpha_ref": a_ref,
                          "weights_identical": len(set(hs)) == 1,
                          "exchange_kind": hdp.exchange_kind(tr.ctx),
+                         "partial_mask": pmask, "partial_count": pcount,
                          "master_sha": hashlib.sha256(master.tobytes()).hexdigest(),
                          "master_err": block_errors(cfg, master.astype(np.float64), ref["master"]),
                          # the step's update: (master_k - master_{k-1}) on both sides (not vacuous at small lambda)

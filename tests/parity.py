@@ -6,6 +6,8 @@ and compare them with the north_star metrics:
 """
 from __future__ import annotations
 
+import contextlib
+
 import numpy as np
 
 import synth
@@ -32,6 +34,20 @@ def block_errors(cfg, got: np.ndarray, ref: np.ndarray, abs_terms: dict = None) 
         num = np.max(np.abs(g[k] - r[k]))
         out[k] = float(num / den) if den > 0 else float(num)
     return out
+
+
+@contextlib.contextmanager
+def kernel_options(**kw):
+    """Process-wide kernel switches (hdp_set_option) for the duration of a block,
+    restored to the library defaults afterwards."""
+    from paper_1912_00286_b200 import hdp
+    for k, v in kw.items():
+        hdp.set_option(None, k, v)
+    try:
+        yield
+    finally:
+        for k in kw:
+            hdp.set_option(None, k, hdp.KERNEL_OPTION_DEFAULTS[k])
 
 
 def _copy_dev(dst, src_ptr: int, nbytes: int):

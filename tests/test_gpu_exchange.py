@@ -175,3 +175,64 @@ def test_out_of_range_token_reported(hdp, bad):
         assert hdp.grad_average_update(tr.ctx, 0, s, sync=True) == 0
     finally:
         tr.close()
+
+
+@pytest.mark.parametrize("nw,frac,straggler,expect", [(4, 0.75, 0b0100, 0b1011), (2, 0.5, 0b01, 0b10),
+                                                      (4, 1.0, 0b0010, 0b1111)])
+def test_partial_collection_loopback(hdp, nw, frac, straggler, expect):
+    """NEXT-2 partial collection in the loopback: the
+    simulated contributor(s) in `straggler` publish readiness 3 ms late, so with quorum
+    ceil(f*N) < N the decision is exactly the others; the update averages only them
+    (divided by their count), against the oracle's step over the same contributors.
+    f = 1 keeps the lock-step (the straggler is waited for)."""
+    from oracle import schedule as osched
+    from oracle import step as ostep
+    from parity import block_errors
+    cfg = synth.CONFIGS["C1"].with_(lambda0=0.05, n_half=1e9)
+    Bg = 4 * nw
+    B = Bg // nw
+    params = synth.init_params(cfg)
+    desc = hdp.desc_from_config(cfg, B, hdp.MATH_MIXED16, sim_workers=nw, exchange=hdp.EXCH_P2P)
+    tr = hdp.Trainer(desc, params, lambda0=cfg.lambda0, alpha=cfg.alpha, gamma=cfg.gamma, n_half=cfg.n_half,
+                     momentum=cfg.momentum)
+    dev = torch.device("cuda:0")
+    master, state = params.astype(np.float64), {"H": np.zeros(tr.n)}
+    try:
+        hdp.set_option(tr.ctx, "partial_fraction", frac)
+        hdp.set_option(tr.ctx, "straggler_mask", straggler)
+        hdp.set_option(tr.ctx, "straggler_us", 3000)
+        for k in range(3):
+            x, t = synth.model_batch(cfg, Bg, synth.DATA_SEED + k)
+            xs = [torch.from_numpy(np.ascontiguousarray(x[r * B:(r + 1) * B])).to(dev) for r in range(nw)]
+            ts = [torch.from_numpy(np.ascontiguousarray(t[r * B:(r + 1) * B])).to(dev) for r in range(nw)]
+            assert tr.step(xs, ts, B, cfg.seq, epoch=0, stream=torch.cuda.current_stream(), sync=True) == 0
+            mask, count = hdp.partial_state(tr.ctx)
+            assert mask == expect and count == bin(expect).count("1"), (mask, count)
+            contributors = [r for r in range(nw) if (mask >> r) & 1]
+            lam = float(np.float32(osched.rate_for_epoch(cfg.lambda0, nw, cfg.n_half, cfg.gamma, 0)))
+            ref = ostep.train_step(cfg, master, state, x, t, nw, cfg.alpha, lam, "mixed",
+                                   contributors=None if frac == 1.0 else contributors)
+            got = hdp.gather_master(tr.ctx, tr.n).astype(np.float64)
+            assert max(block_errors(cfg, got, ref["master"]).values()) <= 2e-2
+            assert max(block_errors(cfg, got - master, ref["master"] - master).values()) <= 5e-2
+            master, state = ref["master"], ref["state"]
+    finally:
+        tr.close()
+
+
+def test_partial_collection_option_errors(hdp):
+    cfg = synth.CONFIGS["C1"]
+    desc = hdp.desc_from_config(cfg, 4, hdp.MATH_MIXED16, sim_workers=2, exchange=hdp.EXCH_NCCL)
+    tr = hdp.Trainer(desc, synth.init_params(cfg), lambda0=cfg.lambda0)
+    try:
+        with pytest.raises(hdp.HDPError) as e:      # K11 path: no partial collection
+            hdp.set_option(tr.ctx, "partial_fraction", 0.5)
+        assert e.value.code == hdp.HDP_ERR_UNSUPPORTED
+        hdp.set_option(tr.ctx, "partial_fraction", 1.0)  # lock-step is always fine
+        for bad in (0.0, 1.5, -1.0):
+            with pytest.raises(hdp.HDPError):
+                hdp.set_option(tr.ctx, "partial_fraction", bad)
+        with pytest.raises(hdp.HDPError):
+            hdp.set_option(tr.ctx, "no_such_option", 1)
+    finally:
+        tr.close()

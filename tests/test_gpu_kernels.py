@@ -226,11 +226,11 @@ def test_k11_l2_bit_exact(hdp, mixed, opt):
 
 
 @pytest.mark.parametrize("cg,bn,amn,bmn", [(2, 128, 0, 0), (2, 256, 0, 1), (2, 256, 1, 1), (2, 128, 1, 0)])
-def test_gemm_cta_pair_and_multicast_variants(hdp, monkeypatch, cg, bn, amn, bmn):
+def test_gemm_cta_pair_and_multicast_variants(hdp, cg, bn, amn, bmn):
     # opt-in GEMM variants: CTA pairs (cta_group::2, 256-row tiles) and A
     # multicast across 4-CTA clusters; ragged M and N, against an fp64 reference
-    for env, val in (("HDP_GEMM_CG", str(cg)), ("HDP_GEMM_CN", "4")):
-        monkeypatch.setenv(env, val)
+    for env, val in (("gemm_cta_group", cg), ("gemm_cluster_n", 4)):
+        hdp.set_option(None, env, val)
         M, N, K = 304, 1000, 320   # ragged against 128 / 256-row tiles; 16-B aligned rows
         A = (torch.randn(M, K, device="cuda") * 0.1).half()
         B = (torch.randn(N, K, device="cuda") * 0.1).half()
@@ -241,8 +241,8 @@ def test_gemm_cta_pair_and_multicast_variants(hdp, monkeypatch, cg, bn, amn, bmn
         hdp.gemm_f16(As, lda, amn, Bs, ldb, bmn, M, N, K, C, N, 0, ws=ws, ws_floats=ws.numel(), bn=bn, splits=2)
         torch.cuda.synchronize()
         ref = A.double() @ B.double().T
+        hdp.set_option(None, env, hdp.KERNEL_OPTION_DEFAULTS[env])
         assert (C.double() - ref).abs().max().item() <= 1e-5 * ref.abs().max().item(), env
-        monkeypatch.delenv(env)
 
 
 def _dev_f16(ptr, n):

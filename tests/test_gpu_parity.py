@@ -17,7 +17,7 @@ pytestmark = pytest.mark.gpu
 
 import synth  # noqa: E402
 
-from parity import run_parity  # noqa: E402
+from parity import kernel_options, run_parity  # noqa: E402
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -249,40 +249,38 @@ def test_c3_persistent_b48_mixed():
     assert _max(recs[-1]["master_err"]) <= 2e-2
 
 
-def test_persistent_matches_per_step_path(monkeypatch):
+def test_persistent_matches_per_step_path():
     """The persistent kernel and the per-step GEMM + cell path compute the
     same thing (fp32 accumulation order is the only difference)."""
-    import numpy as np
     cfg = synth.CONFIGS["C2"].with_(seq=32)
     out = {}
-    for flag in ("1", "0"):
-        monkeypatch.setenv("HDP_PERSISTENT", flag)
-        recs = run_parity(cfg, 64, 1, steps=1, mixed=True)
+    for flag in (1, 0):
+        with kernel_options(persistent=flag):
+            recs = run_parity(cfg, 64, 1, steps=1, mixed=True)
         out[flag] = recs[0]
-    for k in out["1"]["grad_err"][0]:
-        assert out["1"]["grad_err"][0][k] <= 2e-2 and out["0"]["grad_err"][0][k] <= 2e-2
-    assert abs(out["1"]["loss_gpu"] - out["0"]["loss_gpu"]) <= 1e-4
+    for k in out[1]["grad_err"][0]:
+        assert out[1]["grad_err"][0][k] <= 2e-2 and out[0]["grad_err"][0][k] <= 2e-2
+    assert abs(out[1]["loss_gpu"] - out[0]["loss_gpu"]) <= 1e-4
 
 
-@pytest.mark.parametrize("batch,fusex", [(128, "1"), (32, "1"), (64, "0"), (40, "1"), (100, "1"), (72, "0")])
-def test_c2_wavefront_matches_layerwise(monkeypatch, batch, fusex):
+@pytest.mark.parametrize("batch,fusex", [(128, 1), (32, 1), (64, 0), (40, 1), (100, 1), (72, 0)])
+def test_c2_wavefront_matches_layerwise(batch, fusex):
     """The 2-layer wavefront kernels (forward: R0/P/R1 roles, layer-0 input
     projection fused into R0 or read from the K1 GEMM; backward: Q1/X/Q0 roles,
     weight gradients in the wavefront's W role or by the K8 GEMMs)
     against the oracle and against the layer-by-layer persistent path."""
     cfg = synth.CONFIGS["C2"].with_(seq=24)
-    monkeypatch.setenv("HDP_WAVEFRONT_FUSEX", fusex)
-    monkeypatch.setenv("HDP_WAVEFRONT_WGRAD", fusex)  # "0": K8 GEMMs after the wavefront
     out = {}
-    for flag in ("1", "0"):
-        monkeypatch.setenv("HDP_WAVEFRONT", flag)
-        recs = run_parity(cfg, batch, 1, steps=2, mixed=True)
+    for flag in (1, 0):
+        # wavefront_wgrad = 0: K8 GEMMs after the wavefront
+        with kernel_options(wavefront=flag, wavefront_fusex=fusex, wavefront_wgrad=fusex):
+            recs = run_parity(cfg, batch, 1, steps=2, mixed=True)
         out[flag] = recs
         for r in recs:
             assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
             assert _max(r["grad_err"][0]) <= 2e-2, (flag, r["grad_err"])
         assert _max(recs[-1]["master_err"]) <= 2e-2
-    assert abs(out["1"][0]["loss_gpu"] - out["0"][0]["loss_gpu"]) <= 1e-4
+    assert abs(out[1][0]["loss_gpu"] - out[0][0]["loss_gpu"]) <= 1e-4
 
 
 def test_c1_dynamic_loss_scale_skips_and_recovers():

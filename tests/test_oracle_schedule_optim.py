@@ -231,3 +231,22 @@ def test_library_lr_matches_golden(golden):
             assert hdp.lr(h.value, -1) < 0
         finally:
             hdp.destroy(h.value)
+
+
+def test_partial_collection_spec_examples():
+    # f = 1 -> all N; N = 10, f = 0.9, one straggler -> count 9, sum over
+    # the 9; N = 2, f = 0.95 -> ceil(1.9) = 2 (a full barrier)
+    assert optim.quorum(1.0, 7) == 7
+    assert optim.quorum(0.9, 10) == 9
+    assert optim.quorum(0.95, 2) == 2
+    assert optim.quorum(0.5, 2) == 1 and optim.quorum(0.75, 4) == 3 and optim.quorum(0.01, 8) == 1
+    rng = np.random.default_rng(11)
+    gs = [rng.standard_normal(5) for _ in range(10)]
+    arrived = [r for r in range(10) if r != 6]             # rank 6 is the straggler
+    got = optim.partial_average(gs, arrived, alpha=10.0)
+    assert np.allclose(got * 9 * 10.0, sum(gs[r] for r in arrived), rtol=1e-14)
+    # every contributor present: identical to the plain average
+    assert np.array_equal(optim.partial_average(gs, range(10), 10.0), optim.average(gs, 10, 10.0))
+    # duplicated gradients: the partial average equals any single one (the count divides)
+    same = [gs[0]] * 4
+    assert np.allclose(optim.partial_average(same, [0, 2, 3], 1.0), gs[0], rtol=1e-15)
