@@ -314,6 +314,7 @@ void* hdp_master_ptr(hdp_ctx* ctx);            /* this rank's fp32 master shards
  * "Hs" (fp16 [L][T+1][B][hp]), "C" (fp32 [L][T][B][hp]), "gates"
  * (fp16 [L][T][B][4hp]), "X0" (fp16 [T][B][Ip0]), "dA" (fp16 [T][B][4hp]; the
  * top layer's in the 2-layer wavefront), "dA2" (layer 0's in the wavefront),
+ * "Z" (the FC head's ReLU output, fp16 [T][B][Fp]),
  * "dH0"/"dH1" (fp32), "Hst" (recurrent dropout's masked inputs h~, fp16
  * [L][T_max+1][B_max][hp] with rows [t][B][hp] of the actual B inside),
  * "Wcopy" (HDP_EXCH_P2P loopback: weight copies 1..sim_workers-1, each a

@@ -93,12 +93,16 @@ def _q16(mode):
 # forward
 # ----------------------------------------------------------------------------
 
-def forward(cfg, P: Dict[str, np.ndarray], x, targets, alpha: float, mode: str, drop=None):
+def forward(cfg, P: Dict[str, np.ndarray], x, targets, alpha: float, mode: str, drop=None, relu_active=None):
     """fprop + scaled loss for one worker's mini-batch.
 
     drop (optional, NEXT-3 recurrent dropout, oracle/dropout.py): {"masks": [per layer
     {0,1} [B][h]], "scale": fp32(1/keep)}; layer l's recurrent GEMM then reads
     h~_{t-1} = r16(h_{t-1} * scale) on kept units, 0 elsewhere (R6d).
+
+    relu_active (optional, bool [T][B][fc]): the FC head's ReLU decision per unit, where
+    the caller fixes the branch of a pre-activation that lies within rounding of 0
+    (both branches are correct results there, DESIGN.md R-relu); default zpre > 0.
 
     x: float [B][T][I] (fp16-representable, R0) or int tokens [B][T] (C3).
     targets: {-1,+1} [B][T] (per-step heads) or [B] (last-step head).
@@ -149,9 +153,10 @@ def forward(cfg, P: Dict[str, np.ndarray], x, targets, alpha: float, mode: str, 
     cache = {"layers": layers, "B": B, "tokens": np.asarray(x) if cfg.vocab > 0 else None}
     if cfg.fc_hidden > 0:
         zpre = Htop @ P["F"].T + P["fb"]         # [T][B][fc]
-        z = q(np.maximum(zpre, 0.0))             # R7
+        act = zpre > 0.0 if relu_active is None else np.asarray(relu_active, bool)
+        z = q(np.where(act, zpre, 0.0))          # R7: ReLU
         y = z @ P["wo"] + P["bo"][0]             # [T][B]
-        cache.update(zpre=zpre, z=z)
+        cache.update(zpre=zpre, z=z, act=act)
     elif cfg.head_last_step:
         y = Htop[T - 1] @ P["wo"] + P["bo"][0]   # [B]
     else:
@@ -195,7 +200,7 @@ def backward(cfg, P: Dict[str, np.ndarray], cache, alpha: float, mode: str,
     if cfg.fc_hidden > 0:
         z, zpre = cache["z"], cache["zpre"]
         G["wo"] = dy.reshape(-1) @ z.reshape(-1, z.shape[-1])
-        dz = q(dy[..., None] * P["wo"][None, None, :] * (zpre > 0.0))   # R9
+        dz = q(dy[..., None] * P["wo"][None, None, :] * cache["act"])   # R9 (ReLU' = 1 on active units)
         G["F"] = dz.reshape(-1, dz.shape[-1]).T @ Htop.reshape(-1, h)
         G["fb"] = dz.sum(axis=(0, 1))
         if abs_terms is not None:

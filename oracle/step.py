@@ -38,10 +38,10 @@ def working_weights(master: np.ndarray, mode: str) -> np.ndarray:
     return r16(master) if mode == "mixed" else np.asarray(master, np.float64)
 
 
-def worker_grads(cfg, wflat, x, targets, alpha, mode, abs_terms=None, drop=None):
+def worker_grads(cfg, wflat, x, targets, alpha, mode, abs_terms=None, drop=None, relu_active=None):
     """Steps 3 for one worker: returns (L_r scaled, flat gradient, y)."""
     P = lstm.unpack(cfg, wflat)
-    L, y, cache = lstm.forward(cfg, P, x, targets, alpha, mode, drop)
+    L, y, cache = lstm.forward(cfg, P, x, targets, alpha, mode, drop, relu_active)
     G = lstm.backward(cfg, P, cache, alpha, mode, abs_terms)
     return L, lstm.pack(cfg, G), y
 

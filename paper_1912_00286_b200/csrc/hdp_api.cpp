@@ -1852,6 +1852,7 @@ void* hdp_debug_buffer(hdp_ctx* c, int slot, const char* name) {
   if (n == "C") return S.C;
   if (n == "gates") return S.gates;
   if (n == "X0") return S.X0;
+  if (n == "Z") return S.Z;
   if (n == "dA") return c->dA;
   if (n == "dA2") return c->dA2;
   if (n == "dH0") return c->dH[0];

@@ -113,14 +113,18 @@ __global__ void __launch_bounds__(256) exch_update_kernel(const __grid_constant_
   __shared__ unsigned s_mask;
   const int N = a.N, NR = a.NR, tid = threadIdx.x;
   // ---- A: my gradients are complete (stream order: this kernel runs after them)
-  if (blockIdx.x == 0 && tid < 32) {
-    if (a.loopback) {
-      if (tid < N) {  // contributor tid = gradient slot tid
-        if (EXT && ((a.straggler_mask >> tid) & 1u)) spin_ns(a.straggler_ns);
-        __threadfence_system();
-        st_release_sys(a.flag_local + P2P_FLAG_READY + tid, a.seq);
-      }
-    } else if (tid < NR) {
+  if (blockIdx.x == 0 && a.loopback && (tid < 32 || (tid >= 64 && tid < 96))) {
+    // contributor lane = gradient slot lane: on time from warp 0, injected stragglers late from
+    // warp 2 (a separate warp, so the on-time lanes do not wait for the spinning ones)
+    const int r = tid & 31;
+    const bool late = EXT && ((a.straggler_mask >> r) & 1u);
+    if (r < N && late == (tid >= 64)) {
+      if (late) spin_ns(a.straggler_ns);
+      __threadfence_system();
+      st_release_sys(a.flag_local + P2P_FLAG_READY + r, a.seq);
+    }
+  } else if (blockIdx.x == 0 && tid < 32) {
+    if (tid < NR) {
       if (EXT && ((a.straggler_mask >> a.rank) & 1u)) spin_ns(a.straggler_ns);
       __threadfence_system();
       st_release_sys(a.flag_peer[tid] + P2P_FLAG_READY + a.rank, a.seq);

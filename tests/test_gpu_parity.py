@@ -30,6 +30,17 @@ def _max(d):
     return max(d.values())
 
 
+# Mixed-mode per-gradient bound (∞-norm relative, R-cond denominators).  The north_star
+# fixes 2e-2 for the WEIGHTS after 10 steps and 1e-2 for the loss; the gradients get a
+# tighter bound derived from the observed rounding-order spread (fp16 R10 / R6 rounding of
+# a value the oracle computes in fp64 from different upstream roundings: <= 8.5e-3 over
+# every case, gpurun_out/parity_errors.jsonl of round 2), so a dropped or mis-signed term
+# -- an O(1) error -- cannot hide under it.  Full-size runs of the bench shapes: 5e-3
+# (observed <= 1.8e-3).
+GRAD_MIXED = 1e-2
+GRAD_MIXED_FULL = 5e-3
+
+
 
 def test_c1_fp32_two_workers():
     cfg = synth.CONFIGS["C1"]
@@ -51,7 +62,7 @@ def test_c1_mixed_two_workers():
         assert r["nonfinite_gpu"] == r["nonfinite_ref"] == 0
         assert r["w_matches_master"]
         for ge in r["grad_err"]:
-            assert _max(ge) <= 2e-2, (r["step"], ge)
+            assert _max(ge) <= GRAD_MIXED, (r["step"], ge)
     assert _max(recs[-1]["master_err"]) <= 2e-2
 
 
@@ -92,7 +103,7 @@ def test_recurrent_dropout_mixed(cfg_name, gb, nw, seq):
     for r in recs:
         assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"])), r
         for ge in r["grad_err"]:
-            assert _max(ge) <= 2e-2, (r["step"], ge)
+            assert _max(ge) <= GRAD_MIXED, (r["step"], ge)
         assert _max(r["master_err"]) <= 2e-2
         assert r["w_matches_master"]
     assert _max(recs[-1]["dmaster_err"]) <= 5e-2, recs[-1]["dmaster_err"]
@@ -123,7 +134,7 @@ def test_c2_jet_mixed():
     for r in recs:
         assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"])), r
         assert r["nonfinite_gpu"] == 0
-        assert _max(r["grad_err"][0]) <= 2e-2, r["grad_err"]
+        assert _max(r["grad_err"][0]) <= GRAD_MIXED_FULL, r["grad_err"]
     assert _max(recs[-1]["master_err"]) <= 2e-2
 
 
@@ -145,7 +156,7 @@ def test_c3_imdb_full_shape_mixed():
     recs = run_parity(cfg, cfg.batch, 1, steps=2, mixed=True)
     for r in recs:
         assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"])), r
-        assert _max(r["grad_err"][0]) <= 2e-2, r["grad_err"]
+        assert _max(r["grad_err"][0]) <= GRAD_MIXED_FULL, r["grad_err"]
     assert _max(recs[-1]["master_err"]) <= 2e-2
 
 
@@ -157,19 +168,19 @@ def test_c4_cta_pair_gemms_mixed():
     recs = run_parity(cfg, 128, 1, steps=1, mixed=True)
     r = recs[0]
     assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
-    assert _max(r["grad_err"][0]) <= 2e-2, r["grad_err"]
+    assert _max(r["grad_err"][0]) <= GRAD_MIXED_FULL, r["grad_err"]
     assert _max(r["master_err"]) <= 2e-2
 
 
 def test_c4_beta32_ten_steps_mixed():
     """C4 with beta0 = 32 per worker, 2 simulated workers, 10 steps (SURVEY §8(c) parity
-    plan; T reduced to 12 so the oracle finishes in seconds)."""
-    cfg = synth.CONFIGS["C4"].with_(seq=12)
+    plan; T reduced to 4 so the oracle finishes in about a minute)."""
+    cfg = synth.CONFIGS["C4"].with_(seq=4)
     recs = run_parity(cfg, 64, 2, steps=10, mixed=True)
     for r in recs:
         assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"])), r
         for ge in r["grad_err"]:
-            assert _max(ge) <= 2e-2, ge
+            assert _max(ge) <= GRAD_MIXED, ge
     assert _max(recs[-1]["master_err"]) <= 2e-2
 
 
@@ -179,7 +190,7 @@ def test_c3_imdb_reduced_mixed():
     for r in recs:
         assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"])), r
         for ge in r["grad_err"]:
-            assert _max(ge) <= 2e-2, ge
+            assert _max(ge) <= GRAD_MIXED, ge
     assert _max(recs[-1]["master_err"]) <= 2e-2
 
 
@@ -190,7 +201,7 @@ def test_c3_wavefront_b128_mixed():
     recs = run_parity(cfg, 128, 1, steps=2, mixed=True)
     for r in recs:
         assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
-        assert _max(r["grad_err"][0]) <= 2e-2, r["grad_err"]
+        assert _max(r["grad_err"][0]) <= GRAD_MIXED, r["grad_err"]
     assert _max(recs[-1]["master_err"]) <= 2e-2
 
 
@@ -208,7 +219,7 @@ def test_c4_stacked_reduced_mixed():
     recs = run_parity(cfg, 8, 1, steps=1, mixed=True)
     r = recs[0]
     assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
-    assert _max(r["grad_err"][0]) <= 2e-2, r["grad_err"]
+    assert _max(r["grad_err"][0]) <= GRAD_MIXED, r["grad_err"]
     assert _max(r["master_err"]) <= 2e-2
 
 
@@ -221,7 +232,7 @@ def test_c4_full_width_batches_mixed(batch, seq):
     recs = run_parity(cfg, batch, 1, steps=1, mixed=True)
     r = recs[0]
     assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
-    assert _max(r["grad_err"][0]) <= 2e-2, r["grad_err"]
+    assert _max(r["grad_err"][0]) <= GRAD_MIXED, r["grad_err"]
     assert _max(r["master_err"]) <= 2e-2
 
 
@@ -236,7 +247,7 @@ def test_c1_persistent_b16_mixed():
     for r in recs:
         assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
         for ge in r["grad_err"]:
-            assert _max(ge) <= 2e-2, ge
+            assert _max(ge) <= GRAD_MIXED, ge
     assert _max(recs[-1]["master_err"]) <= 2e-2
 
 
@@ -245,7 +256,7 @@ def test_c3_persistent_b48_mixed():
     recs = run_parity(cfg, 48, 1, steps=2, mixed=True)
     for r in recs:
         assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
-        assert _max(r["grad_err"][0]) <= 2e-2, r["grad_err"]
+        assert _max(r["grad_err"][0]) <= GRAD_MIXED, r["grad_err"]
     assert _max(recs[-1]["master_err"]) <= 2e-2
 
 
@@ -259,7 +270,7 @@ def test_persistent_matches_per_step_path():
             recs = run_parity(cfg, 64, 1, steps=1, mixed=True)
         out[flag] = recs[0]
     for k in out[1]["grad_err"][0]:
-        assert out[1]["grad_err"][0][k] <= 2e-2 and out[0]["grad_err"][0][k] <= 2e-2
+        assert out[1]["grad_err"][0][k] <= GRAD_MIXED and out[0]["grad_err"][0][k] <= GRAD_MIXED
     assert abs(out[1]["loss_gpu"] - out[0]["loss_gpu"]) <= 1e-4
 
 
@@ -278,7 +289,7 @@ def test_c2_wavefront_matches_layerwise(batch, fusex):
         out[flag] = recs
         for r in recs:
             assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
-            assert _max(r["grad_err"][0]) <= 2e-2, (flag, r["grad_err"])
+            assert _max(r["grad_err"][0]) <= GRAD_MIXED, (flag, r["grad_err"])
         assert _max(recs[-1]["master_err"]) <= 2e-2
     assert abs(out[1][0]["loss_gpu"] - out[0][0]["loss_gpu"]) <= 1e-4
 
@@ -339,14 +350,57 @@ def test_degenerate_shapes(cfg_name, batch, seq, mixed):
     """Degenerate cases of the method: one sequence, one time step (no
     recurrence: h_{-1} = 0, so dU = 0 and BPTT is a single cell).
 
-    C2 at B = 1, T = 2 runs in fp32 mode only: in mixed mode its seeded batch
-    has an FC pre-activation at -1.0e-6 (1.3e-5 of sum|terms|), inside the
-    fp16 rounding of h, so the ReLU decision differs between the oracle and
-    the kernel and, with two loss terms, moves dF by 0.29 (DESIGN.md R-relu)."""
+    C2 at B = 1, T = 2 in mixed mode is test_c2_relu_decision_within_rounding
+    (DESIGN.md R-relu)."""
     cfg = synth.CONFIGS[cfg_name].with_(seq=seq)
     recs = run_parity(cfg, batch, 1, steps=1, mixed=mixed)
-    tol = 2e-2 if mixed else 1e-5
+    tol = GRAD_MIXED if mixed else 1e-5
     for r in recs:
         assert abs(r["loss_gpu"] - r["loss_ref"]) <= (1e-2 if mixed else 1e-5) * max(1.0, abs(r["loss_ref"])), r
         assert _max(r["grad_err"][0]) <= tol, r["grad_err"]
     assert _max(recs[-1]["master_err"]) <= tol
+
+
+def test_c2_relu_decision_within_rounding():
+    """DESIGN.md R-relu: where an FC pre-activation lies within the fp16 rounding of h
+    of zero, both ReLU branches are correct results.  C2 at B = 1, T = 2 (mixed) has
+    one at -1.0e-6 in its seeded batch.  The kernel's decisions (Z > 0, debug buffer
+    "Z") must agree with the oracle's wherever |zpre| exceeds that rounding bound
+    (sum_k |F_jk| |h_k| 2^-11); the gradients are then compared with the oracle run
+    on the kernel's decisions (lstm.forward relu_active), within the mixed bound."""
+    from paper_1912_00286_b200 import hdp
+    from oracle import lstm as olstm
+    from oracle import step as ostep
+    from parity import _copy_dev, block_errors
+    cfg = synth.CONFIGS["C2"].with_(seq=2)
+    B, T, fc = 1, 2, cfg.fc_hidden
+    params = synth.init_params(cfg)
+    desc = hdp.desc_from_config(cfg, B, hdp.MATH_MIXED16)
+    tr = hdp.Trainer(desc, params, lambda0=cfg.lambda0, alpha=cfg.alpha)
+    dev = torch.device("cuda:0")
+    try:
+        x, t = synth.model_batch(cfg, B, synth.DATA_SEED)
+        s = torch.cuda.current_stream()
+        hdp.lstm_forward(tr.ctx, torch.from_numpy(x).to(dev), torch.from_numpy(t).to(dev), B, T, 0, None,
+                         tr.loss[0:1], s)
+        hdp.lstm_backward(tr.ctx, 0, s)
+        torch.cuda.synchronize()
+        Fp = (fc + 15) // 16 * 16
+        Z = torch.empty(T * B * Fp, dtype=torch.float16, device=dev)
+        _copy_dev(Z, hdp.debug_buffer(tr.ctx, 0, "Z"), Z.numel() * 2)
+        act_gpu = (Z.view(T, B, Fp)[:, :, :fc] > 0).cpu().numpy()
+        g_gpu = hdp.read_grads(tr.ctx, 0, tr.n).astype(np.float64)
+    finally:
+        tr.close()
+    P = olstm.unpack(cfg, params.astype(np.float64))
+    _, _, cache = olstm.forward(cfg, P, x, t, cfg.alpha, "mixed")
+    zpre, Htop = cache["zpre"], cache["Htop"]
+    bound = (np.abs(Htop) * 2.0 ** -11) @ np.abs(P["F"]).T + 1e-12
+    ambiguous = np.abs(zpre) <= bound
+    assert ambiguous.any()                                      # the case exercises the reading
+    assert np.all((act_gpu == (zpre > 0)) | ambiguous)          # validity of the kernel's branches
+    at = {}
+    _, g_ref, _ = ostep.worker_grads(cfg, params.astype(np.float64), x, t, cfg.alpha, "mixed", at,
+                                     relu_active=act_gpu)
+    err = block_errors(cfg, g_gpu, g_ref, at)
+    assert _max(err) <= GRAD_MIXED, err

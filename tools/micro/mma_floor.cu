@@ -83,7 +83,7 @@ void run(unsigned long long* d) {
 int main() {
   unsigned long long* d; cudaMalloc(&d, 8);
   run<64, 0, 52, 1>(d); run<64, 0, 52, 4>(d); run<64, 0, 52, 8>(d);
-  run<64, 1, 52, 1>(d); run<64, 1, 52, 4>(d); run<64, 1, 52, 8>(d);
+  run<64, 1, 52, 1>(d); run<64, 1, 52, 2>(d); run<64, 1, 52, 4>(d); run<64, 1, 52, 8>(d);
   run<128, 0, 26, 1>(d); run<128, 0, 26, 2>(d); run<128, 0, 26, 4>(d);
   run<128, 1, 26, 1>(d); run<128, 1, 26, 2>(d); run<128, 1, 26, 4>(d);
   run<128, 0, 52, 4>(d); run<128, 1, 52, 4>(d); run<128, 1, 52, 8>(d);
