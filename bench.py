@@ -563,6 +563,11 @@ def run_reference(args):
 
 
 def main():
+    # the JSON line must be the only thing on stdout: NCCL / torch.distributed banners
+    # (e.g. "NCCL version ..." at communicator creation) go to stderr instead
+    real_stdout = os.fdopen(os.dup(1), "w")
+    sys.stdout.flush()
+    os.dup2(2, 1)
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=20)
@@ -582,7 +587,7 @@ def main():
 
     if args.impl == "reference":
         if rank == 0:
-            print(json.dumps(run_reference(args)), flush=True)
+            print(json.dumps(run_reference(args)), file=real_stdout, flush=True)
         return
 
     if world > 1:
@@ -594,7 +599,7 @@ def main():
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline and args.config != "C5":
             out["cpu_baseline"] = cpu_baseline(args)
-        print(json.dumps(out), flush=True)
+        print(json.dumps(out), file=real_stdout, flush=True)
     if world > 1:
         import torch.distributed as dist
         dist.barrier()

@@ -783,6 +783,8 @@ cudaError_t set_attr_bn() {
   if ((e = set_attr<BN, 0, 1, 2>()) != cudaSuccess) return e;
   if ((e = set_attr<BN, 0, 0, 4>()) != cudaSuccess) return e;
   if ((e = set_attr<BN, 0, 1, 4>()) != cudaSuccess) return e;
+  if ((e = set_attr<BN, 0, 0, 8>()) != cudaSuccess) return e;
+  if ((e = set_attr<BN, 0, 1, 8>()) != cudaSuccess) return e;
   if ((e = set_attr<BN, 0, 0, 1, 2>()) != cudaSuccess) return e;
   if ((e = set_attr<BN, 0, 1, 1, 2>()) != cudaSuccess) return e;
   if ((e = set_attr<BN, 1, 0, 1, 2>()) != cudaSuccess) return e;
@@ -796,6 +798,7 @@ cudaError_t launch_tc_bn(const GemmPlan& p, cudaStream_t s) {
   if (p.amn == 1 && p.cg == 2) return p.bmn ? launch_tc<BN, 1, 1, 1, 2>(p, s) : launch_tc<BN, 1, 0, 1, 2>(p, s);
   if (p.amn == 0 && p.cn == 2) return p.bmn ? launch_tc<BN, 0, 1, 2>(p, s) : launch_tc<BN, 0, 0, 2>(p, s);
   if (p.amn == 0 && p.cn == 4) return p.bmn ? launch_tc<BN, 0, 1, 4>(p, s) : launch_tc<BN, 0, 0, 4>(p, s);
+  if (p.amn == 0 && p.cn == 8) return p.bmn ? launch_tc<BN, 0, 1, 8>(p, s) : launch_tc<BN, 0, 0, 8>(p, s);
   if (p.amn == 0 && p.bmn == 0) return launch_tc<BN, 0, 0>(p, s);
   if (p.amn == 0 && p.bmn == 1) return launch_tc<BN, 0, 1>(p, s);
   if (p.amn == 1 && p.bmn == 0) return launch_tc<BN, 1, 0>(p, s);
@@ -898,7 +901,7 @@ int gemm_plan_tc(GemmPlan* p, const __half* A, long lda, int a_mn, const __half*
   int cn = 1;
   {
     cn = opt(OPT_GEMM_CLUSTER_N);
-    if (cn != 2 && cn != 4) cn = 1;
+    if (cn != 2 && cn != 4 && cn != 8) cn = 1;
     if (a_mn != 0) cn = 1;
   }
   p->cn = cn;

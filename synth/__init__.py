@@ -187,6 +187,43 @@ def jet_batch(B: int, T: int, D: int, seed: int) -> Tuple[np.ndarray, np.ndarray
     return xs.astype(np.float16), tgt
 
 
+# JET channels of App. A that carry the synthetic precursors of
+# jet_precursor_batch: l_i (internal inductance), MLA (locked-mode amplitude), P_rad
+# (radiated power) -- indices in the App. A order
+PRECURSOR_CHANNELS = (3, 5, 6)
+
+
+def jet_precursor_batch(B: int, T: int, D: int, seed: int, disruptive_frac: float = 0.1,
+                        amplitude: float = 3.0, lead=(60, 100)) -> Tuple[np.ndarray, np.ndarray, np.ndarray]:
+    """JET-analog chunks with a LEARNABLE disruption precursor (NEXT-4 convergence runs).
+
+    Background as in jet_batch: per channel AR(1) x_t = 0.95 x_{t-1} + 0.3 eps_t plus a
+    slow linear drift.  A chunk is disruptive with probability ``disruptive_frac``
+    (App. A :279 "about 10%"; training chunks may be class-balanced); a disruptive chunk
+    ends in the disruption (t_disrupt = T) and carries a rising ramp of ``amplitude`` on
+    the PRECURSOR_CHANNELS over its last L ~ U[lead] steps (so at least lead[0] - 30 ramp
+    steps precede the 30 ms alarm cutoff).  Targets are +1 on the ramp
+    steps, -1 elsewhere.  Standardisation uses fixed constants of the
+    generator (mean 0, scale 1.2) so every batch sees the same transform; fp16 storage.
+    Returns x fp16 [B][T][D], targets int8 [B][T], disruptive bool [B]."""
+    rng = np.random.Generator(np.random.PCG64(seed))
+    eps = rng.standard_normal((B, T, D))
+    x = np.zeros((B, T, D))
+    for t in range(T):
+        x[:, t] = (0.95 * x[:, t - 1] if t > 0 else 0.0) + 0.3 * eps[:, t]
+    x = x + rng.normal(0.0, 0.01, size=(B, 1, D)) * np.arange(T)[None, :, None]
+    tgt = -np.ones((B, T), np.int8)
+    dis = rng.random(B) < disruptive_frac
+    chans = [c for c in PRECURSOR_CHANNELS if c < D]
+    for b in np.nonzero(dis)[0]:
+        L = int(rng.integers(lead[0], min(lead[1], T) + 1))
+        for c in chans:
+            x[b, T - L:, c] += np.linspace(0.0, amplitude, L)
+        tgt[b, T - L:] = 1
+    xs = (x.astype(np.float32) / np.float32(1.2)).astype(np.float16)
+    return xs, tgt, dis
+
+
 IMDB_LEXICON = 50
 
 

@@ -1,24 +1,26 @@
-"""NEXT-4: training at convergence scale on synthetic data.
+"""NEXT-4: convergence of the CUDA training step on synthetic
+JET-analog data, scored with the paper's shot-level alarm AUC (
+oracle/metrics.py), reproducing the SHAPE of Figs. 3-4 (PAPER.md:123-127,
+:171-175, :185) without the real datasets.
 
-The CUDA path trains the C2 (JET-shaped) model for 600 steps on the seeded
-JET-analog generator (a fresh batch every step) and scores a held-out set with
-the paper's shot-level alarm AUC (oracle/metrics.py) from the
-disruptivity traces `hdp_lstm_forward` writes (y_out).  Checks:
-  * fp16 (mixed) and fp32 training on the same batches follow the same loss
-    trajectory (every logged step within 5 %) and reach AUCs within 0.03 of
-    each other (the paper's Fig. 4: half precision converges like
-    single precision);
-  * the worker-count-dependent schedule trains N = 1, 2, 4
-    simulated workers (per-worker batch beta0 fixed): the scaled
-    hinge loss falls below 20 % of its initial value in every run.
-Measured on B200 (gpurun_out/convergence_auc.json): the loss falls from 1.03 to
-~0.095 but within 600-3000 steps (SGD-m or Adam) the model settles near the
-majority solution (every step "not disruptive"); the ramps of the synthetic
-disruptive shots are not yet separated, so the AUC stays near 0.42-0.47 for both
-precisions -- an AUC-learning claim is "parity unpinned" (Q27).
-Shots are disruptive iff their targets contain +1 (synth.jet_batch); the
-disruption is taken at the end of the chunk, t_disrupt = T, so the legal alarm
-window is t <= T - 30.
+Data (synth.jet_precursor_batch): AR(1) background on 9 channels with a learnable
+precursor -- a rising ramp on the l_i / MLA / P_rad channels over the last 60-100
+steps of a disruptive chunk, which ends in the disruption.  Training chunks are
+class-balanced (a harness choice, fresh seeded batch every step); the held-out set
+has the paper's ~10 % disruptive chunks (App. A :279).  Every held-out chunk is
+scored over the same legal alarm window t <= T - 30 (30 ms cutoff, :171), whatever its
+class (reading Q27b: the round-1 runs scored non-disruptive chunks over all
+T steps, which biased the AUC below chance).
+
+Runs: C2-shaped model (2 x LSTM 200, FC 200 ReLU, per-step hinge x alpha = 10),
+beta0 = 32 sequences per worker, SGD-m under the paper's worker-count schedule
+lambda_0' = min(lambda_0 / (1 + N/n), 0.1/N) * gamma^epoch (Eqs. 3-4, :109-121),
+N = 1, 2, 4, 8 simulated workers (global batch N * beta0, "keeping batch
+size beta0 and base learning rate lambda0 the same"), fp16 (mixed) at every N and fp32
+at N = 1.  Checks (the "done" bar of round 2's VERDICT): held-out AUC > 0.8 in every
+run; fp16 and fp32 AUCs within 0.03 (SPEC.md:382; Fig. 4, :173 "similar shapes") and
+their loss trajectories within 5 % at every logged step; AUC-per-epoch curves written
+to gpurun_out/convergence_auc.json.
 """
 import json
 import os
@@ -34,9 +36,11 @@ from oracle import metrics  # noqa: E402
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 BETA0, NVAL = 32, 512
-STEPS = int(os.environ.get("HDP_CONV_STEPS", "600"))
+STEPS = int(os.environ.get("HDP_CONV_STEPS", "400"))
+STEPS_PER_EPOCH = 100
 LAMBDA0 = float(os.environ.get("HDP_CONV_LAMBDA0", "0.05"))
-OPT = os.environ.get("HDP_CONV_OPT", "sgdm")
+GAMMA = 0.8
+WORKERS = (1, 2, 4, 8)
 
 
 @pytest.fixture(scope="module", autouse=True)
@@ -45,7 +49,7 @@ def _need_gpu():
         pytest.skip("no CUDA device")
 
 
-def _val_auc(hdp, tr, cfg, xv, tv):
+def _val_auc(hdp, tr, cfg, xv, tv, dv):
     dev = torch.device("cuda:0")
     T = cfg.seq
     ys = []
@@ -58,58 +62,55 @@ def _val_auc(hdp, tr, cfg, xv, tv):
         hdp.lstm_forward(tr.ctx, x, t, BETA0, T, 0, y, tr.loss[0:1], torch.cuda.current_stream())
         ys.append(y.cpu().numpy().T)                      # [B][T]
     y = np.concatenate(ys)
-    dis = (tv == 1).any(axis=1)
-    scores = [metrics.shot_score(y[b], bool(dis[b]), t_disrupt=T) for b in range(y.shape[0])]
-    return metrics.auc_trapezoid(scores, dis)
+    # window-symmetric scoring (reading Q27b): every chunk over t <= T - 30
+    scores = [metrics.shot_score(y[b], True, t_disrupt=T) for b in range(y.shape[0])]
+    return metrics.auc_trapezoid(scores, dv)
 
 
 def _train(mixed, N, steps=STEPS):
     from paper_1912_00286_b200 import hdp
     cfg = synth.CONFIGS["C2"]
-    desc = hdp.desc_from_config(cfg, BETA0, hdp.MATH_MIXED16 if mixed else hdp.MATH_FP32,
-                                optimizer=hdp.OPT_ADAM if OPT == "adam" else hdp.OPT_SGDM, sim_workers=N)
-    tr = hdp.Trainer(desc, synth.init_params(cfg), lambda0=LAMBDA0, alpha=cfg.alpha, gamma=1.0,
+    desc = hdp.desc_from_config(cfg, BETA0, hdp.MATH_MIXED16 if mixed else hdp.MATH_FP32, sim_workers=N)
+    tr = hdp.Trainer(desc, synth.init_params(cfg), lambda0=LAMBDA0, alpha=cfg.alpha, gamma=GAMMA,
                      n_half=cfg.n_half, momentum=cfg.momentum)
-    xv, tv = synth.jet_batch(NVAL, cfg.seq, cfg.input_dim, 777)
+    xv, tv, dv = synth.jet_precursor_batch(NVAL, cfg.seq, cfg.input_dim, 777, disruptive_frac=0.1)
     dev = torch.device("cuda:0")
-    losses = []
+    losses, curve = [], []
     try:
-        auc0 = _val_auc(hdp, tr, cfg, xv, tv)
+        curve.append(_val_auc(hdp, tr, cfg, xv, tv, dv))
         for k in range(steps):
-            x, t = synth.jet_batch(N * BETA0, cfg.seq, cfg.input_dim, 5000 + k)
+            x, t, _ = synth.jet_precursor_batch(N * BETA0, cfg.seq, cfg.input_dim, 5000 + k, disruptive_frac=0.5)
             xs, ts = [], []
             for r in range(N):
                 xr = torch.from_numpy(np.ascontiguousarray(x[r * BETA0:(r + 1) * BETA0])).to(dev)
                 xs.append(xr if mixed else xr.float())
                 ts.append(torch.from_numpy(np.ascontiguousarray(t[r * BETA0:(r + 1) * BETA0])).to(dev))
-            nf = tr.step(xs, ts, BETA0, cfg.seq, epoch=0, stream=torch.cuda.current_stream(), sync=True)
+            nf = tr.step(xs, ts, BETA0, cfg.seq, epoch=k // STEPS_PER_EPOCH, stream=torch.cuda.current_stream(),
+                         sync=True)
             assert nf == 0
-            if k % 50 == 0 or k == steps - 1:
+            if k % 25 == 0 or k == steps - 1:
                 losses.append(round(float(tr.loss.mean().item()), 5))
-        auc = _val_auc(hdp, tr, cfg, xv, tv)
+            if (k + 1) % STEPS_PER_EPOCH == 0:
+                curve.append(_val_auc(hdp, tr, cfg, xv, tv, dv))
     finally:
         tr.close()
-    _train.losses[(mixed, N)] = losses
-    return auc0, auc
+    from oracle import schedule
+    return {"auc_per_epoch": curve, "losses": losses,
+            "lambda_epoch0": schedule.rate_for_epoch(LAMBDA0, N, cfg.n_half, GAMMA, 0)}
 
 
-_train.losses = {}
-
-
-def test_c2_fp16_vs_fp32_auc_and_worker_counts():
-    res = {}
-    for mixed in (True, False):
-        res[f"N1_{'fp16' if mixed else 'fp32'}"] = _train(mixed, 1)
-    for N in (() if os.environ.get("HDP_CONV_ONLY_N1") else (2, 4)):
+def test_c2_convergence_auc_fp16_fp32_and_worker_counts():
+    res = {"N1_fp32": _train(False, 1)}
+    for N in WORKERS:
         res[f"N{N}_fp16"] = _train(True, N)
     os.makedirs(os.path.join(ROOT, "gpurun_out"), exist_ok=True)
     with open(os.path.join(ROOT, "gpurun_out", "convergence_auc.json"), "w") as f:
-        json.dump({k: {"auc_init": a0, "auc": a} for k, (a0, a) in res.items()} |
-                  {"losses": {str(k): v for k, v in _train.losses.items()}}, f, indent=1)
-    a16, a32 = res["N1_fp16"][1], res["N1_fp32"][1]
-    assert abs(a16 - a32) <= 0.03, res
-    l16, l32 = _train.losses[(True, 1)], _train.losses[(False, 1)]
+        json.dump({"steps": STEPS, "steps_per_epoch": STEPS_PER_EPOCH, "lambda0": LAMBDA0, "gamma": GAMMA,
+                   "beta0": BETA0, "runs": res}, f, indent=1)
+    for key, r in res.items():
+        assert r["auc_per_epoch"][-1] > 0.8, (key, r["auc_per_epoch"])
+    a16, a32 = res["N1_fp16"]["auc_per_epoch"][-1], res["N1_fp32"]["auc_per_epoch"][-1]
+    assert abs(a16 - a32) <= 0.03, (a16, a32)
+    l16, l32 = res["N1_fp16"]["losses"], res["N1_fp32"]["losses"]
     assert len(l16) == len(l32) > 5
     assert all(abs(a - b) <= 0.05 * max(a, b) for a, b in zip(l16, l32)), (l16, l32)
-    for key, ls in _train.losses.items():
-        assert ls[-1] < 0.2 * ls[0], (key, ls)             # every run trained
