@@ -173,6 +173,25 @@ def algorithmic_work(cfg, B, world, prof=None):
     return w
 
 
+def latency_floor(cfg, kclass):
+    """Dependency-chain floor of a recurrence launch: T + 2 steps of
+    (tcgen05 MMA chain + one DSMEM hand-off), both measured by the micro-benchmarks in
+    profiles/r02_latency_floor.json; the cell epilogue is not in it (a lower bound).
+    The MMA part scales with the K-steps for h_p other than the measured 208."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r02_latency_floor.json")) as f:
+            m = json.load(f)["model"]
+    except Exception:  # noqa: BLE001
+        return None
+    hp = (cfg.hidden + 15) // 16 * 16
+    key = "backward step (Q roles)" if kclass.startswith("recur_bwd") else "forward step (R roles)"
+    step_ns = m[key]["mma_ns"] * hp / 208.0 + m[key]["hop_ns"]
+    steps = cfg.seq + 2
+    return {"per_step_ns": round(step_ns, 1), "steps": steps, "floor_us": steps * step_ns / 1e3,
+            "model": "(T + 2) x (MMA chain + DSMEM hop), epilogue excluded",
+            "source": "profiles/r02_latency_floor.json (tools/micro on B200)"}
+
+
 def run_hdp(args, rank, world, local_rank):
     import numpy as np
     import torch
@@ -292,6 +311,11 @@ def run_hdp(args, rank, world, local_rank):
         roof = {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                 "traffic": None}
     roof["traffic"] = committed_traffic(cfg.name, dom)
+    if dom in ("recur_bwd(K6+K7)", "recur_fwd(K2+K3)"):
+        lf = latency_floor(cfg, dom)
+        if lf:
+            roof["latency_floor"] = lf
+            roof["latency_floor_frac"] = lf["floor_us"] / (avg_launch_ms * 1e3)
     roof.update({"kernel": dom, "peak_src": pk["src"] + (" sustained" if kind == "flop" else ""),
                  "avg_launch_us": avg_launch_ms * 1e3, "per_launch": per_launch,
                  "per_launch_unit": "flop" if kind == "flop" else "byte",

@@ -197,8 +197,11 @@ int hdp_set_l2(hdp_ctx* ctx, double l2);
  * dA_t^T h~_{t-1}.  The mask is the counter-based hash of dropout.cuh keyed by
  * `seed`, the number of completed hdp_grad_average_update calls since this
  * call, the layer, the sequence's global index ((rank * slots + slot) * B + b)
- * and the unit.  Mixed mode only; the per-step GEMM path runs (the fused
- * recurrence kernels have no dropout).  The library allocates (cudaMalloc)
+ * and the unit.  Mixed mode only.  The two-layer wavefront kernels apply it in
+ * their epilogues (masked recurrent operand pushed to the peers, masked dh_rec,
+ * dU from h~); other shapes run the per-step GEMM path with the fused cell
+ * epilogues (the per-layer persistent kernels have no dropout and are bypassed).
+ * The library allocates (cudaMalloc)
  * the masked-input buffers, slots * L * (T+1) * B * h_p fp16, freed by
  * hdp_destroy.  Synchronises the device; drops the captured graphs.
  * Errors: keep outside (0, 1] -> HDP_ERR_ARG; FP32 mode -> HDP_ERR_UNSUPPORTED;

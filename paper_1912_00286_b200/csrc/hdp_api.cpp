@@ -201,7 +201,9 @@ struct hdp_ctx {
   float drop_scale = 1.f;
   char* hst = nullptr;        // library-owned: per slot [L][T+1][B][hp] fp16 masked recurrent inputs
   bool drop_on() const { return keep < 1.0; }
-  bool recur_ok() const { return hdp::opt(hdp::OPT_PERSISTENT) != 0 && !drop_on(); }  // (no dropout in them)
+  // the per-layer persistent recurrences have no dropout; the two-layer wavefronts do
+  bool recur_ok() const { return hdp::opt(hdp::OPT_PERSISTENT) != 0 && !drop_on(); }
+  bool wave_ok() const { return hdp::opt(hdp::OPT_PERSISTENT) != 0; }
   int* drop_step() const { return status + 14; }  // completed updates (mask counter)
   char* Hst(int slot, int l) const {
     return hst + ((size_t)slot * d.n_layers + l) * (size_t)(d.max_seq + 1) * d.max_batch * hp * 2;
@@ -543,7 +545,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
     char* Hs = S.Hs + l * hs_layer * e;
     float* Cl = S.C + l * c_layer;
     char* Gl = S.gates + l * g_layer * e;
-    const bool wave = l == 0 && L == 2 && !f32 && c->recur_ok() && hdp::recur2_fwd_supported(B, (int)hp);
+    const bool wave = l == 0 && L == 2 && !f32 && c->wave_ok() && hdp::recur2_fwd_supported(B, (int)hp);
     const bool fusex = wave && hdp::recur2_fwd_fuses_x(B, (int)hp, (int)Ipl);
     // K1: G_x = X W^T + b for all t (A1); inside the wavefront's layer-0 role when fused
     if (!fusex)
@@ -573,6 +575,15 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
       ra.T = T;
       ra.B = B;
       ra.hp = (int)hp;
+      if (c->drop_on()) {  // recurrent dropout inside the wavefront (NEXT-3)
+        ra.Ht0 = (__half*)c->Hst(si, 0);
+        ra.Ht1 = (__half*)c->Hst(si, 1);
+        ra.drop_step = c->drop_step();
+        ra.drop_seed = c->drop_seed;
+        ra.drop_thr = c->drop_thr;
+        ra.drop_seq0 = (uint32_t)((c->rank * c->nslots + si) * B);
+        ra.drop_scale = c->drop_scale;
+      }
       ra.trace = trace_buffer(c, 4 * 8192 * 5);
       {
         KScope ks_(c, HDP_K_RECUR_FWD, 1, s);
@@ -767,7 +778,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
   const bool last_only = d.head_last_step && l == L - 1;
   // 2 layers, mixed mode: both layers' BPTT and the dX1 projection in one wavefront
   // launch (segment for layer 1); layer 0's segment then only has its K8 / K9 work
-  const bool wave = L == 2 && !f32 && c->recur_ok() && hdp::recur2_bwd_supported(B, (int)hp);
+  const bool wave = L == 2 && !f32 && c->wave_ok() && hdp::recur2_bwd_supported(B, (int)hp);
   // ... and, on the SMs the recurrences leave idle, the A8 weight gradients of both layers
   const bool wgrad = wave && !gf && hdp::recur2_bwd_wgrad(B, (int)hp, (int)c->Ip0);
   if (wave) c->wave_bwd = true;
@@ -790,6 +801,15 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
     wa.T = T;
     wa.B = B;
     wa.hp = (int)hp;
+    if (c->drop_on()) {  // recurrent dropout inside the wavefront (NEXT-3)
+      wa.Ht0 = (const __half*)c->Hst(si, 0);
+      wa.Ht1 = (const __half*)c->Hst(si, 1);
+      wa.drop_step = c->drop_step();
+      wa.drop_seed = c->drop_seed;
+      wa.drop_thr = c->drop_thr;
+      wa.drop_seq0 = (uint32_t)((c->rank * c->nslots + si) * B);
+      wa.drop_scale = c->drop_scale;
+    }
     if (wgrad) {
       wa.Hs0 = (const __half*)S.Hs;
       wa.Hs1 = (const __half*)Hs;

@@ -32,6 +32,7 @@
 #include "gemm.cuh"
 #include "options.h"
 #include "ptx.cuh"
+#include "dropout.cuh"
 #include "recur.cuh"
 
 namespace hdp {
@@ -975,6 +976,12 @@ struct __align__(64) Bwd2Params {
   CUtensorMap tmGq[2];        // gates_1 / gates_0 rows [T*B][4hp] fp16, box (256, Bc) (TSQ prefetch)
   CUtensorMap tmCq[2];        // C_1 / C_0 rows [T*B][hp] fp32, box (64, Bc) (TSQ prefetch)
   CUtensorMap tmDXo;          // dX1 rows [T*B][hp] fp32, box (64, Bc): X's TMA stores (TSQ)
+  // recurrent dropout (reading Q16b): mask x scale on dh_rec; dU from Hst (tmHt = tmHs when off)
+  CUtensorMap tmHt[2];        // Hst1 / Hst0 rows [(T+1)*B][hp], MN-major B operand boxes (64, 64)
+  int drop;
+  const int* drop_step;
+  uint32_t drop_seed, drop_thr, drop_seq0;
+  float drop_scale;
 };
 
 // Weight-gradient role: one CTA per (matrix, 128-gate-row tile) accumulates over all
@@ -1028,7 +1035,8 @@ __device__ __forceinline__ void bwd_wgrad_role(const Bwd2Params& P, int tile) {
   const uint32_t tbase = *tslot;               // [0, N): weight grad; [256, 272): bias grad
   if (threadIdx.x == 0) {
     // ---- producer
-    const CUtensorMap* tb = mat == 3 ? &P.tmX0 : &P.tmHs[mat == 0 ? 0 : 1];
+    // dU: h~_{t-1} (Hst with recurrent dropout, else Hs); dW1: the unmasked h0_t; dW0: x_t
+    const CUtensorMap* tb = mat == 3 ? &P.tmX0 : mat == 1 ? &P.tmHs[1] : &P.tmHt[mat == 0 ? 0 : 1];
     for (int it = 0; it < nitems; ++it) {
       const int t = T - 1 - it / nbc, bc = it % nbc;
       const int s = it & 1;
@@ -1537,6 +1545,20 @@ __global__ void __launch_bounds__(128, 1)
   float dcr[NC * 8];
 #pragma unroll
   for (int i = 0; i < NC * 8; ++i) dcr[i] = 0.f;
+  // recurrent dropout: dh_rec (the gradient of h~_{t-1}) x mask x scale, per (unit, column)
+  float dsc[NC * 8];
+#pragma unroll
+  for (int i = 0; i < NC * 8; ++i) dsc[i] = 1.f;
+  if (P.drop) {
+    const uint32_t lk = drop_layer_key(P.drop_seed, (uint32_t)*P.drop_step, qi == 0 ? 1u : 0u);
+#pragma unroll
+    for (int ch = 0; ch < NC; ++ch)
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const uint32_t seq = P.drop_seq0 + (uint32_t)(col0 + ch * 16 + half * 8 + k);
+        dsc[ch * 8 + k] = unit_ok && drop_kept(drop_seq_key(lk, seq), (uint32_t)unit, P.drop_thr) ? P.drop_scale : 0.f;
+      }
+  }
   const uint32_t idesc = ptx::idesc_f16_f32(64, Bc, 1, 0);
   const uint32_t sA_addr = ptx::smem_u32(sA), sX_addr = ptx::smem_u32(sX);
   uint32_t fphase[2] = {0u, 0u};
@@ -1708,7 +1730,7 @@ __global__ void __launch_bounds__(128, 1)
           const int idx = ch * 8 + k;
           const int bl = ch * 16 + half * 8 + k;
           const size_t b = (size_t)col0 + bl;
-          const float dh = dh0[idx] + rec[k];
+          const float dh = dh0[idx] + (P.drop ? rec[k] * dsc[idx] : rec[k]);
           const float2 if2 = __half22float2(*reinterpret_cast<const __half2*>(&gq[idx].x));
           const float2 go2 = __half22float2(*reinterpret_cast<const __half2*>(&gq[idx].y));
           const float i = if2.x, f = if2.y, g = go2.x, o = go2.y;
@@ -1860,6 +1882,15 @@ struct __align__(64) Fwd2Params {
   const __half* Ag[3]; // row-major U0, W1, U1 [4hp][hp] (A operands copied into TMEM, NKS != 0)
   const __half* W0g;   // W0 [4hp][Ip0] (fused projection, TMEM copy)
   int Ip0;
+  // recurrent dropout (NEXT-3, reading Q16b): the recurrent operand pushed to the peers is
+  // h~_t = fp16(fp32(h_t) * scale) on kept units, 0 elsewhere, and is stored to Ht[l]
+  // (the W role's dU operand); Hs keeps the unmasked h_t (next layer, head)
+  int drop;
+  CUtensorMap tmHt[2];  // Hst_l rows [(T+1) B][hp] fp16, box (64, Bc), SWIZZLE_128B (TMA stores)
+  __half* Ht[2];
+  const int* drop_step;
+  uint32_t drop_seed, drop_thr, drop_seq0;
+  float drop_scale;
 };
 
 // Copy rows [row0 + half*128 + 32*quadrant + lane] of a row-major fp16 matrix (ncols K
@@ -1930,6 +1961,9 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
   uint64_t* fullH = bars + 2;                 // [2]
   uint64_t* barX = bars + 4;                  // [2] x_t landed (fuse_x)
   uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 6);
+  // recurrent dropout: [2][Bc][128 B] staging of the UNMASKED h_t for the Hs TMA store (the
+  // push staging sX then holds h~_t); 1024-aligned for SWIZZLE_128B
+  uint8_t* sXu = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(bars + 16) + 1023) & ~uintptr_t(1023));
   const bool fx = role == 0 && P.fuse_x;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int quarter = warp & 3, hf = (warp >> 2) & 1, cg = warp >> 3;
@@ -2135,6 +2169,20 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
     float* myAct = sAct + warp * 16 * ACT_LD;
     const float gsc = gate == 2 ? 2.f : 1.f;
     const float bias0 = fx && unit_ok ? __half2float(P.b0[grow]) : 0.f;
+    // recurrent dropout: mask x scale of this lane's (unit, column) pairs, fixed over t
+    float dsc[NCI * 4];
+#pragma unroll
+    for (int i = 0; i < NCI * 4; ++i) dsc[i] = 1.f;
+    if (P.drop) {
+      const uint32_t lk = drop_layer_key(P.drop_seed, (uint32_t)*P.drop_step, (uint32_t)li);
+#pragma unroll
+      for (int ci = 0; ci < NCI; ++ci)
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+          const uint32_t seq = P.drop_seq0 + (uint32_t)(col0 + (ci * cgN + cg) * 16 + 4 * q + gate);
+          dsc[ci * 4 + q] = unit_ok && drop_kept(drop_seq_key(lk, seq), (uint32_t)unit, P.drop_thr) ? P.drop_scale : 0.f;
+        }
+    }
     // debug sub-phase stamps of the epilogue (R0 CTA 0 / group 0, thread 0) in trace role slot 3
     unsigned long long* trx = (tr && li == 0) ? P.trace + (size_t)3 * T * 5 : nullptr;
     // TSA: the SMEM A region is free -> stage c_t and the gates there and let one thread
@@ -2269,13 +2317,18 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
             const float cv = f * creg[ci * 4 + q] + i * g;
             creg[ci * 4 + q] = cv;
             const __half hh = __float2half_rn(o * act_gate(cv, 2.f));
+            // the recurrent operand: h_t, or h~_t = fp16(fp32(h_t) * scale) / 0 (R6d)
+            const __half hm = P.drop ? __float2half_rn(__half2float(hh) * dsc[ci * 4 + q]) : hh;
+            const int so = bl * 128 + ((c ^ (bl & 7)) << 4) + (ul & 7) * 2;
             if (!TST) {
               cout[b * hp + unit] = cv;                 // R5
               hout[b * hp + unit] = hh;                 // R6
+              if (P.drop) P.Ht[li][(size_t)(t + 1) * B * hp + b * hp + unit] = hm;
             } else {
               sCo[((t & 1) * Bc + bl) * 64 + ul] = cv;
+              if (P.drop) *reinterpret_cast<__half*>(sXu + (t & 1) * Bc * 128 + so) = hh;
             }
-            *reinterpret_cast<__half*>(stg + bl * 128 + ((c ^ (bl & 7)) << 4) + (ul & 7) * 2) = hh;
+            *reinterpret_cast<__half*>(stg + so) = hm;
             __align__(8) __half2 gg[2] = {__halves2half2(__float2half_rn(i), __float2half_rn(f)),
                                           __halves2half2(__float2half_rn(g), __float2half_rn(o))};
             if (!TST)
@@ -2319,7 +2372,12 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
             release_add(P.r0done + grp * 32, 1u);
           }
           ptx::tma_store_2d(&P.tmCo[li], sCo + (t & 1) * Bc * 64, rank * 64, t * B + col0);
-          ptx::tma_store_2d(&P.tmHo[li], stg, rank * 64, (t + 1) * B + col0);
+          if (P.drop) {  // h~_t (the push staging) -> Hst, unmasked h_t -> Hs
+            ptx::tma_store_2d(&P.tmHt[li], stg, rank * 64, (t + 1) * B + col0);
+            ptx::tma_store_2d(&P.tmHo[li], sXu + (t & 1) * Bc * 128, rank * 64, (t + 1) * B + col0);
+          } else {
+            ptx::tma_store_2d(&P.tmHo[li], stg, rank * 64, (t + 1) * B + col0);
+          }
           ptx::tma_store_2d(&P.tmGo[li], sGo + (t & 1) * Bc * 256, rank * 256, t * B + col0);
           ptx::bulk_commit_group();
           if (li == 0 && t == T - 1) {
@@ -2434,6 +2492,8 @@ namespace hdp {
 // CTAs fit on the GPU as co-resident clusters (cached per shape)
 // extra shared memory of the fused layer-0 input projection (W0 slice + x_t double buffer)
 size_t w2f_fuse_bytes(int Bc) { return 32768 + 2 * (size_t)Bc * 128; }
+// the dropout staging sXu behind the barriers (reserved whether or not dropout is on)
+size_t w2f_drop_bytes(int Bc) { return 1024 + 128 + 2 * (size_t)Bc * 128; }
 
 struct W2Plan {
   int Bc = 0, nbg = 0, cgN = 0, nci = 0, fuse = 0;
@@ -2468,7 +2528,7 @@ bool plan_w2f(int B, int hp, W2Plan* out) {
       p.nbg = nbg;
       p.cgN = Bc / 16;
       p.nci = 1;
-      size_t smem = fwd_cl_smem(hp, Bc, 8 * p.cgN);
+      size_t smem = fwd_cl_smem(hp, Bc, 8 * p.cgN) + w2f_drop_bytes(Bc);
       if (smem > 227 * 1024) continue;
       if (opt(OPT_WAVEFRONT_FUSEX) != 0 && smem + w2f_fuse_bytes(Bc) <= 227 * 1024) {
         smem += w2f_fuse_bytes(Bc);
@@ -2585,11 +2645,30 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
     if (P.r1_tma && encode_tmap_2d(&P.tmG1, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, a.a1x, 4 * hp, (uint64_t)a.T * a.B,
                                    4 * hp * 4, 256, pl.Bc, CU_TENSOR_MAP_SWIZZLE_NONE))
       return cudaErrorInvalidValue;
+    if (a.Ht0) {  // recurrent dropout
+      if (!a.Ht1 || !a.drop_step) return cudaErrorInvalidValue;
+      const uint64_t TB1 = (uint64_t)(a.T + 1) * a.B;
+      __half* ht[2] = {a.Ht0, a.Ht1};
+      for (int l = 0; l < 2; ++l)
+        if (encode_tmap_2d(&P.tmHt[l], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, ht[l], hp, TB1, hp * 2, 64, pl.Bc,
+                           CU_TENSOR_MAP_SWIZZLE_128B))
+          return cudaErrorInvalidValue;
+      P.drop = 1;
+      P.Ht[0] = a.Ht0;
+      P.Ht[1] = a.Ht1;
+      P.drop_step = a.drop_step;
+      P.drop_seed = a.drop_seed;
+      P.drop_thr = a.drop_thr;
+      P.drop_seq0 = a.drop_seq0;
+      P.drop_scale = a.drop_scale;
+    }
     cudaError_t e = cudaMemsetAsync(a.flags, 0, (16 * 32 + 16 * 8 * 32) * sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
     void* args[] = {&P};
     return launch_cluster(recur2f_fn(pl.nci, a.hp), dim3(G, 3 * pl.nbg), dim3(256 * pl.cgN),
-                          fwd_cl_smem(a.hp, pl.Bc, 8 * pl.cgN) + (pl.fuse ? w2f_fuse_bytes(pl.Bc) : 0), G, s, args);
+                          fwd_cl_smem(a.hp, pl.Bc, 8 * pl.cgN) + w2f_drop_bytes(pl.Bc) +
+                              (pl.fuse ? w2f_fuse_bytes(pl.Bc) : 0),
+                          G, s, args);
   }
 }
 
@@ -2730,6 +2809,16 @@ cudaError_t launch_recur2_bwd(const Recur2BwdArgs& a, cudaStream_t s) {
         encode_tmap_2d(&P.tmX0, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.X0, a.Ip0, TB, (uint64_t)a.Ip0 * 2, 64, 64,
                        CU_TENSOR_MAP_SWIZZLE_128B))
       return cudaErrorInvalidValue;
+    if (a.Ht0) {
+      if (encode_tmap_2d(&P.tmHt[0], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.Ht1, hp, TB1, hp * 2, 64, 64,
+                         CU_TENSOR_MAP_SWIZZLE_128B) ||
+          encode_tmap_2d(&P.tmHt[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.Ht0, hp, TB1, hp * 2, 64, 64,
+                         CU_TENSOR_MAP_SWIZZLE_128B))
+        return cudaErrorInvalidValue;
+    } else {
+      P.tmHt[0] = P.tmHs[0];
+      P.tmHt[1] = P.tmHs[1];
+    }
     for (int i = 0; i < 4; ++i) P.gW[i] = a.gW[i];
     P.gb[0] = a.gb[0];
     P.gb[1] = a.gb[1];
@@ -2758,6 +2847,15 @@ cudaError_t launch_recur2_bwd(const Recur2BwdArgs& a, cudaStream_t s) {
       encode_tmap_2d(&P.tmdAo[1], CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.dA0, 4 * hp, (uint64_t)a.T * a.B, 4 * hp * 2, 64,
                      Bc, CU_TENSOR_MAP_SWIZZLE_128B))
     return cudaErrorInvalidValue;
+  if (a.Ht0) {
+    if (!a.Ht1 || !a.drop_step) return cudaErrorInvalidValue;
+    P.drop = 1;
+    P.drop_step = a.drop_step;
+    P.drop_seed = a.drop_seed;
+    P.drop_thr = a.drop_thr;
+    P.drop_seq0 = a.drop_seq0;
+    P.drop_scale = a.drop_scale;
+  }
   cudaError_t e = cudaMemsetAsync(a.flags, 0, (2 * 16 * 32 + 16 * 8 * 32) * sizeof(unsigned), s);
   if (e != cudaSuccess) return e;
   void* args[] = {&P};

@@ -48,6 +48,13 @@ struct Recur2FwdArgs {
   const __half *X0 = nullptr, *W0 = nullptr, *b0 = nullptr;  // X0 [T][B][Ip0], W0 [4hp][Ip0]
   int Ip0 = 0;
   unsigned* flags = nullptr;            // >= 16*32 + 16*8*32 uints (split-cluster variant)
+  // recurrent dropout (NEXT-3, reading Q16b; Ht0 == nullptr: off): the recurrent operand is
+  // h~_t, written to Ht_l [T+1][B][hp] (slot 0 = h~_{-1} = 0, not written); masks from the
+  // dropout.cuh hash of (seed, *drop_step, layer, drop_seq0 + b, unit)
+  __half *Ht0 = nullptr, *Ht1 = nullptr;
+  const int* drop_step = nullptr;
+  uint32_t drop_seed = 0, drop_thr = 0, drop_seq0 = 0;
+  float drop_scale = 1.f;
 };
 bool recur2_fwd_supported(int B, int hp);
 bool recur2_fwd_fuses_x(int B, int hp, int Ip0);
@@ -72,6 +79,12 @@ struct Recur2BwdArgs {
   __half* gW[4] = {nullptr, nullptr, nullptr, nullptr};  // dU1, dW1, dU0, dW0
   __half* gb[2] = {nullptr, nullptr};                    // db1, db0
   unsigned long long* trace = nullptr;  // debug: [Q1, Q0, X][T][5] timestamps, nullable
+  // recurrent dropout (Ht0 == nullptr: off): dh_rec of layer l is multiplied by its mask x
+  // scale (the gradient of h~_{t-1}), and dU_l accumulates dA_t^T h~_{t-1} from Ht_l
+  const __half *Ht0 = nullptr, *Ht1 = nullptr;
+  const int* drop_step = nullptr;
+  uint32_t drop_seed = 0, drop_thr = 0, drop_seq0 = 0;
+  float drop_scale = 1.f;
 };
 bool recur2_bwd_supported(int B, int hp);
 bool recur2_bwd_wgrad(int B, int hp, int Ip0);  // the launch can also produce the A8 weight gradients

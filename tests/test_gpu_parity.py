@@ -109,6 +109,26 @@ def test_recurrent_dropout_mixed(cfg_name, gb, nw, seq):
     assert _max(recs[-1]["dmaster_err"]) <= 5e-2, recs[-1]["dmaster_err"]
 
 
+def test_c2_recurrent_dropout_full_size_wavefront():
+    """NEXT-3 recurrent dropout inside the two-layer wavefront kernels (reading Q16b) at
+    C2's full size (B = 128, T = 128): masked recurrent operand pushed between the CTAs,
+    h~ stored for dU, dh_rec through mask x scale -- against the oracle's counter-based
+    masks, and against the per-step GEMM path (persistent = 0) with the same masks."""
+    cfg = synth.CONFIGS["C2"].with_(lambda0=0.05, n_half=1e9)
+    out = {}
+    for flag in (1, 0):
+        with kernel_options(persistent=flag):
+            out[flag] = run_parity(cfg, cfg.batch, 1, steps=2, mixed=True, dropout=(0.7, 77))
+    for flag, recs in out.items():
+        for r in recs:
+            assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"])), (flag, r)
+            assert _max(r["grad_err"][0]) <= GRAD_MIXED_FULL, (flag, r["grad_err"])
+            assert r["w_matches_master"]
+        assert _max(recs[-1]["master_err"]) <= 2e-2
+        assert _max(recs[-1]["dmaster_err"]) <= 5e-2, (flag, recs[-1]["dmaster_err"])
+    assert abs(out[1][0]["loss_gpu"] - out[0][0]["loss_gpu"]) <= 1e-4
+
+
 def test_c1_adam_fp32():
     cfg = synth.CONFIGS["C1"]
     recs = run_parity(cfg, synth.C1_GLOBAL_BATCH, synth.C1_SIM_WORKERS, steps=3, mixed=False, optimizer="adam",
