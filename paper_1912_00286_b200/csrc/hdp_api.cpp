@@ -1675,7 +1675,8 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
       p.bk1 = (int)gr.second;
       p.seq = ++c->p2p_seq;
       const long vec = p.vpre[p.bk1] - p.vpre[p.bk0];
-      const int grid = (int)std::max(1L, std::min((vec + 255) / 256, 4L * 148));
+      // one wave of co-resident CTAs (register-limited occupancy), grid-striding over the vectors
+      const int grid = (int)std::max(1L, std::min((vec + 255) / 256, (long)hdp::exch_resident_ctas(p, opt, c->gf32)));
       c->p2p_ctr += (unsigned)grid;
       p.ctr_target = c->p2p_ctr;
       KScope ks_(c, HDP_K_UPDATE, 1, cs);

@@ -106,8 +106,10 @@ struct PV<float> {
 
 // EXT = 0: plain SGD-m / Adam with every contributor (the hot configuration);
 // EXT = 1: L2 term, dynamic-loss-scale skip / device alpha, partial collection.
-template <typename GT, int OPT, bool EXT>
-__global__ void __launch_bounds__(256) exch_update_kernel(const __grid_constant__ P2PArgs a) {
+// NMAX >= N: register arrays sized for at most NMAX contributions (2 / 4 / 8), so a
+// 2-rank exchange keeps occupancy (every contribution's load is in flight at once).
+template <typename GT, int OPT, bool EXT, int NMAX>
+__global__ void __launch_bounds__(256, NMAX <= 2 ? 4 : NMAX <= 4 ? 3 : 2) exch_update_kernel(const __grid_constant__ P2PArgs a) {
   __shared__ int s_nf;
   __shared__ int s_last;
   __shared__ unsigned s_mask;
@@ -176,16 +178,16 @@ __global__ void __launch_bounds__(256) exch_update_kernel(const __grid_constant_
     const long e = a.off[bi] + (long)a.rank * a.shard[bi] + k;  // element in the parameter vector
     const long m = a.moff[bi] + k;                              // element in my master shard
     // every contribution's load in flight before the first add
-    typename PV<GT>::raw_t raw[P2P_MAX_RANKS];
+    typename PV<GT>::raw_t raw[NMAX];
 #pragma unroll
-    for (int r = 0; r < P2P_MAX_RANKS; ++r)
+    for (int r = 0; r < NMAX; ++r)
       if (r < N && ((mask >> r) & 1u)) raw[r] = PV<GT>::load(a.g_peer[r], e);
     const float4 W0 = *reinterpret_cast<const float4*>(a.W + m), W1 = *reinterpret_cast<const float4*>(a.W + m + 4);
     const float4 H0 = *reinterpret_cast<const float4*>(a.S1 + m), H1 = *reinterpret_cast<const float4*>(a.S1 + m + 4);
     float s[8];
     bool first = true;
 #pragma unroll
-    for (int r = 0; r < P2P_MAX_RANKS; ++r) {
+    for (int r = 0; r < NMAX; ++r) {
       if (r < N && ((mask >> r) & 1u)) {
         float t[8];
         PV<GT>::cvt(raw[r], t, nf);
@@ -236,7 +238,7 @@ __global__ void __launch_bounds__(256) exch_update_kernel(const __grid_constant_
     for (int i = 0; i < 4; ++i) o[i] = __halves2half2(__float2half_rn(w[2 * i]), __float2half_rn(w[2 * i + 1]));
     const uint4 ov = *reinterpret_cast<const uint4*>(o);
 #pragma unroll
-    for (int r = 0; r < P2P_MAX_RANKS; ++r)
+    for (int r = 0; r < NMAX; ++r)
       if (r < N) __stcg(reinterpret_cast<uint4*>(a.w_peer[r] + e), ov);  // all-gather by peer stores
   }
   // ---- C: completion
@@ -260,20 +262,32 @@ __global__ void __launch_bounds__(256) exch_update_kernel(const __grid_constant_
 
 }  // namespace
 
-cudaError_t launch_exch_update(const P2PArgs& a, int optimizer, int grad_f32, int grid, cudaStream_t s) {
+template <typename GT, int OPT, bool EXT>
+const void* exch_fn_n(int N) {
+  return N <= 2 ? (const void*)exch_update_kernel<GT, OPT, EXT, 2>
+       : N <= 4 ? (const void*)exch_update_kernel<GT, OPT, EXT, 4> : (const void*)exch_update_kernel<GT, OPT, EXT, 8>;
+}
+const void* exch_fn(const P2PArgs& a, int optimizer, int grad_f32) {
   const bool ext = a.l2x2 != 0.f || a.alpha_dev || a.skip || a.quorum > 0 || a.straggler_mask;
-#define HDP_EXCH(GT, OPT)                                                                  \
-  (ext ? (exch_update_kernel<GT, OPT, true><<<grid, 256, 0, s>>>(a), 0)                    \
-       : (exch_update_kernel<GT, OPT, false><<<grid, 256, 0, s>>>(a), 0))
-  if (grad_f32) {
-    if (optimizer == 0) HDP_EXCH(float, 0);
-    else HDP_EXCH(float, 1);
-  } else {
-    if (optimizer == 0) HDP_EXCH(__half, 0);
-    else HDP_EXCH(__half, 1);
-  }
+#define HDP_EXCH(GT, OPT) (ext ? exch_fn_n<GT, OPT, true>(a.N) : exch_fn_n<GT, OPT, false>(a.N))
+  if (grad_f32) return optimizer == 0 ? HDP_EXCH(float, 0) : HDP_EXCH(float, 1);
+  return optimizer == 0 ? HDP_EXCH(__half, 0) : HDP_EXCH(__half, 1);
 #undef HDP_EXCH
-  return cudaGetLastError();
+}
+
+cudaError_t launch_exch_update(const P2PArgs& a, int optimizer, int grad_f32, int grid, cudaStream_t s) {
+  void* args[] = {const_cast<P2PArgs*>(&a)};
+  return cudaLaunchKernel(exch_fn(a, optimizer, grad_f32), dim3(grid), dim3(256), args, 0, s);
+}
+
+int exch_resident_ctas(const P2PArgs& a, int optimizer, int grad_f32) {
+  int per_sm = 0;
+  if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, exch_fn(a, optimizer, grad_f32), 256, 0) != cudaSuccess ||
+      per_sm < 1)
+    per_sm = 1;
+  int dev = 0, sms = 148;
+  if (cudaGetDevice(&dev) == cudaSuccess) cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+  return per_sm * sms;
 }
 
 }  // namespace hdp

@@ -54,5 +54,7 @@ struct P2PArgs {
 
 // grad_f32: the wire carries fp32 gradients (HDP_WIRE_FP32) instead of fp16
 cudaError_t launch_exch_update(const P2PArgs& a, int optimizer, int grad_f32, int grid, cudaStream_t s);
+// CTAs of the launch's instantiation that are co-resident on the whole GPU (the grid cap)
+int exch_resident_ctas(const P2PArgs& a, int optimizer, int grad_f32);
 
 }  // namespace hdp

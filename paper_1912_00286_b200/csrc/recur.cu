@@ -1937,7 +1937,7 @@ __device__ __forceinline__ void fwd_issue_unrolled(uint32_t tbase, uint32_t tA, 
   __syncwarp();
 }
 
-template <int NCI, int NKS>
+template <int NCI, int NKS, bool DROP>
 __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__ Fwd2Params P) {
   extern __shared__ uint8_t smem_raw[];
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
@@ -2173,7 +2173,7 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
     float dsc[NCI * 4];
 #pragma unroll
     for (int i = 0; i < NCI * 4; ++i) dsc[i] = 1.f;
-    if (P.drop) {
+    if (DROP) {
       const uint32_t lk = drop_layer_key(P.drop_seed, (uint32_t)*P.drop_step, (uint32_t)li);
 #pragma unroll
       for (int ci = 0; ci < NCI; ++ci)
@@ -2318,15 +2318,15 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
             creg[ci * 4 + q] = cv;
             const __half hh = __float2half_rn(o * act_gate(cv, 2.f));
             // the recurrent operand: h_t, or h~_t = fp16(fp32(h_t) * scale) / 0 (R6d)
-            const __half hm = P.drop ? __float2half_rn(__half2float(hh) * dsc[ci * 4 + q]) : hh;
+            const __half hm = DROP ? __float2half_rn(__half2float(hh) * dsc[ci * 4 + q]) : hh;
             const int so = bl * 128 + ((c ^ (bl & 7)) << 4) + (ul & 7) * 2;
             if (!TST) {
               cout[b * hp + unit] = cv;                 // R5
               hout[b * hp + unit] = hh;                 // R6
-              if (P.drop) P.Ht[li][(size_t)(t + 1) * B * hp + b * hp + unit] = hm;
+              if (DROP) P.Ht[li][(size_t)(t + 1) * B * hp + b * hp + unit] = hm;
             } else {
               sCo[((t & 1) * Bc + bl) * 64 + ul] = cv;
-              if (P.drop) *reinterpret_cast<__half*>(sXu + (t & 1) * Bc * 128 + so) = hh;
+              if (DROP) *reinterpret_cast<__half*>(sXu + (t & 1) * Bc * 128 + so) = hh;
             }
             *reinterpret_cast<__half*>(stg + so) = hm;
             __align__(8) __half2 gg[2] = {__halves2half2(__float2half_rn(i), __float2half_rn(f)),
@@ -2372,7 +2372,7 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
             release_add(P.r0done + grp * 32, 1u);
           }
           ptx::tma_store_2d(&P.tmCo[li], sCo + (t & 1) * Bc * 64, rank * 64, t * B + col0);
-          if (P.drop) {  // h~_t (the push staging) -> Hst, unmasked h_t -> Hs
+          if (DROP) {  // h~_t (the push staging) -> Hst, unmasked h_t -> Hs
             ptx::tma_store_2d(&P.tmHt[li], stg, rank * 64, (t + 1) * B + col0);
             ptx::tma_store_2d(&P.tmHo[li], sXu + (t & 1) * Bc * 128, rank * 64, (t + 1) * B + col0);
           } else {
@@ -2499,14 +2499,16 @@ struct W2Plan {
   int Bc = 0, nbg = 0, cgN = 0, nci = 0, fuse = 0;
 };
 // K-step counts with an unrolled MMA-issue instantiation (h_p = 208, 256); others generic
-template <int NCI>
+// DROP: the recurrent-dropout instantiation (its epilogue differs; kept out of the plain one)
+template <int NCI, bool DROP>
 const void* recur2f_fn_nks(int nk16) {
-  return nk16 == 13 ? (const void*)recur2f_kernel<NCI, 13>
-       : nk16 == 16 ? (const void*)recur2f_kernel<NCI, 16> : (const void*)recur2f_kernel<NCI, 0>;
+  return nk16 == 13 ? (const void*)recur2f_kernel<NCI, 13, DROP>
+       : nk16 == 16 ? (const void*)recur2f_kernel<NCI, 16, DROP> : (const void*)recur2f_kernel<NCI, 0, DROP>;
 }
-const void* recur2f_fn(int nci, int hp) {
+const void* recur2f_fn(int nci, int hp, bool drop = false) {
   const int nk16 = opt(OPT_WAVEFRONT_TMEM) == 0 ? -1 : (hp + 15) / 16;  // -1: the generic (SMEM-A) instantiation
-  return nci == 1 ? recur2f_fn_nks<1>(nk16) : nci == 2 ? recur2f_fn_nks<2>(nk16) : nullptr;
+  if (drop) return nci == 1 ? recur2f_fn_nks<1, true>(nk16) : nci == 2 ? recur2f_fn_nks<2, true>(nk16) : nullptr;
+  return nci == 1 ? recur2f_fn_nks<1, false>(nk16) : nci == 2 ? recur2f_fn_nks<2, false>(nk16) : nullptr;
 }
 bool plan_w2f(int B, int hp, W2Plan* out) {
   static std::map<std::pair<int, int>, W2Plan> cache;
@@ -2665,7 +2667,7 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
     cudaError_t e = cudaMemsetAsync(a.flags, 0, (16 * 32 + 16 * 8 * 32) * sizeof(unsigned), s);
     if (e != cudaSuccess) return e;
     void* args[] = {&P};
-    return launch_cluster(recur2f_fn(pl.nci, a.hp), dim3(G, 3 * pl.nbg), dim3(256 * pl.cgN),
+    return launch_cluster(recur2f_fn(pl.nci, a.hp, P.drop != 0), dim3(G, 3 * pl.nbg), dim3(256 * pl.cgN),
                           fwd_cl_smem(a.hp, pl.Bc, 8 * pl.cgN) + w2f_drop_bytes(pl.Bc) +
                               (pl.fuse ? w2f_fuse_bytes(pl.Bc) : 0),
                           G, s, args);

