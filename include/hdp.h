@@ -65,7 +65,7 @@ enum { HDP_EXCH_AUTO = 0,  /* world >= 2: HDP_EXCH_P2P where it applies, else NC
                               world == 1: K11 over the local gradient slots             */
        HDP_EXCH_NCCL = 1,  /* NCCL collectives per bucket (all-to-all / reduce-scatter,
                               K11, all-gather), or K11 alone at world == 1              */
-       HDP_EXCH_P2P = 2    /* NEXT-2: one kernel reads every rank's fp16 gradient shard
+       HDP_EXCH_P2P = 2,   /* NEXT-2: one kernel reads every rank's fp16 gradient shard
                               over NVLink peer memory (CUDA IPC), does the K11 arithmetic
                               and stores the fp16 weights into every rank's copy.  Needs
                               mixed math, the fp16 all-to-all wire and world <= 8.  At
@@ -75,6 +75,14 @@ enum { HDP_EXCH_AUTO = 0,  /* world >= 2: HDP_EXCH_P2P where it applies, else NC
                               working copy, the others are readable as debug buffer
                               "Wcopy"), so the kernel's arithmetic and protocol are tested
                               on one GPU.  HDP_ERR_UNSUPPORTED where it does not apply.   */
+       HDP_EXCH_TASK0 = 3  /* ablation, the paper's steps 4-6 literally:
+                              every worker's gradients go to task 0 (NCCL grouped sends),
+                              task 0 sums them in fp32 rank order and updates the WHOLE
+                              model (K11, master and optimizer state on rank 0 only), then
+                              broadcasts the weights.  Same per-element arithmetic as the
+                              owner-sharded paths (bit-identical results), N times the
+                              update work and memory on rank 0.  fp16 all-to-all or fp32
+                              wire; world == 1 behaves as HDP_EXCH_NCCL.                */
 };
 
 typedef struct hdp_ctx hdp_ctx;
@@ -144,8 +152,8 @@ int hdp_bind(hdp_ctx* ctx, void* arena, long long arena_bytes);
 
 /* The exchange path configure resolved desc.exchange to:
  * 0 = K11 over the local gradient slots (world 1), 1 = NCCL collectives + K11,
- * 2 = the one-kernel NVLink exchange across ranks, 3 = its world-1 loopback;
- * negative if not configured.                                          */
+ * 2 = the one-kernel NVLink exchange across ranks, 3 = its world-1 loopback,
+ * 4 = the task-0 ablation; negative if not configured.                 */
 int hdp_exchange_kind(const hdp_ctx* ctx);
 
 int hdp_num_blocks(const hdp_ctx* ctx);

@@ -138,6 +138,7 @@ struct hdp_ctx {
   bool wave_bwd = false;  // the backward ran as one wavefront launch: layer buckets are ready together
   // NEXT-2 NVLink exchange: library-owned, IPC-shared windows (gradients, fp16 weights, flags)
   bool want_p2p = false;  // desc.exchange resolved at configure time
+  bool task0 = false;     // HDP_EXCH_TASK0 at world > 1: the paper-literal reduce-to-task-0 ablation
   bool loopback = false;  // HDP_EXCH_P2P at world 1: simulated workers' slots as the peers
   char* wcopies = nullptr;  // loopback: weight copies 1..nslots-1 [nslots-1][P]
   bool p2p = false;
@@ -213,6 +214,7 @@ struct hdp_ctx {
   long adam_k = 0;
 
   int L() const { return d.n_layers; }
+  int owner_index() const { return task0 ? 0 : rank; }  // which shard of each bucket this rank owns
   int Nw() const { return world * nslots; }
   void* W(int bi) const { return w + blocks[bi].dev_off * esz; }
   void* G(int s, int bi) const { return grads + ((long)s * P + blocks[bi].dev_off) * gsz; }
@@ -294,7 +296,10 @@ void build_layout(hdp_ctx* c) {
     for (int l = d.n_layers - 1; l >= 0; --l) groups.push_back(lay[l]);
     if (!emb.empty()) groups.push_back(emb);
   }
-  const long align_bucket = 64L * c->world;
+  // owner-sharded: every bucket split into `world` shards; task 0 (the paper-literal
+  // ablation) owns whole buckets
+  const int nshard = c->task0 ? 1 : c->world;
+  const long align_bucket = 64L * nshard;
   long off = 0, moff = 0;
   c->max_bucket = 0;
   for (size_t g = 0; g < groups.size(); ++g) {
@@ -309,7 +314,7 @@ void build_layout(hdp_ctx* c) {
       p += b.dev_rows * b.dev_cols;
     }
     bk.len = rup(p - off, align_bucket);
-    bk.shard = bk.len / c->world;
+    bk.shard = bk.len / nshard;
     bk.moff = moff;
     moff += bk.shard;
     off += bk.len;
@@ -357,7 +362,8 @@ void carve(hdp_ctx* c, char* base) {
   c->s1 = (float*)cv.take(c->M_own * 4);
   c->s2 = (float*)cv.take(d.optimizer == HDP_OPT_ADAM ? c->M_own * 4 : 0);
   c->grads = cv.take((size_t)c->nslots * P * c->gsz);
-  c->recv = cv.take(c->world > 1 ? c->P * c->gsz : 0);  // bucket bi received at its own offset
+  // bucket bi received at its own offset (task 0: every rank's whole vector, [world][P] on rank 0)
+  c->recv = cv.take(c->world > 1 ? (c->task0 ? (c->rank == 0 ? (size_t)c->world : 0) : 1) * c->P * c->gsz : 0);
   c->status = (int*)cv.take(32768);  // [0] non-finite count, [16] out-of-range token ids;
                                        // +1024 B: recurrence barrier counters;
                                        // +4096 B: backward-wavefront hand-off counters
@@ -1215,7 +1221,9 @@ int hdp_configure(hdp_ctx* c, const hdp_model_desc* desc, hdp_sizes* out) {
   }
   if (d.math == HDP_MATH_FP32 && d.wire == HDP_WIRE_FP16_NCCLSUM)
     return fail(HDP_ERR_ARG, "FP32 math cannot use the fp16 NCCL-sum wire");
-  if (d.exchange < HDP_EXCH_AUTO || d.exchange > HDP_EXCH_P2P) return fail(HDP_ERR_ARG, "bad exchange mode");
+  if (d.exchange < HDP_EXCH_AUTO || d.exchange > HDP_EXCH_TASK0) return fail(HDP_ERR_ARG, "bad exchange mode");
+  if (d.exchange == HDP_EXCH_TASK0 && d.wire == HDP_WIRE_FP16_NCCLSUM)
+    return fail(HDP_ERR_UNSUPPORTED, "task-0 ablation gathers the gradients unreduced (fp16 all-to-all or fp32 wire)");
   CK(check_desc_across_ranks(c, d));
   c->d = d;
   c->f32 = d.math == HDP_MATH_FP32;
@@ -1223,6 +1231,7 @@ int hdp_configure(hdp_ctx* c, const hdp_model_desc* desc, hdp_sizes* out) {
   c->esz = c->f32 ? 4 : 2;
   c->gsz = c->gf32 ? 4 : 2;
   c->nslots = d.sim_workers;
+  c->task0 = d.exchange == HDP_EXCH_TASK0 && c->world > 1;
   build_layout(c);
   {
     // NEXT-2 one-kernel exchange: fp16 gradients on the all-to-all wire, fp16 weights
@@ -1278,6 +1287,7 @@ int hdp_num_blocks(const hdp_ctx* c) { return c ? (int)c->blocks.size() : 0; }
 
 int hdp_exchange_kind(const hdp_ctx* c) {
   if (!c || !c->configured) return -1;
+  if (c->task0) return 4;
   if (c->want_p2p) return c->loopback ? 3 : 2;
   return c->world > 1 ? 1 : 0;
 }
@@ -1328,7 +1338,7 @@ int hdp_load_params(hdp_ctx* c, const float* params, int root) {
   }
   // master shard <- owned slices; optimizer state <- 0; working copy <- params
   for (const Bucket& bk : c->buckets)
-    CK_CUDA(cudaMemcpyAsync(c->master + bk.moff, buf + bk.off + (long)c->rank * bk.shard, bk.shard * 4,
+    CK_CUDA(cudaMemcpyAsync(c->master + bk.moff, buf + bk.off + (long)c->owner_index() * bk.shard, bk.shard * 4,
                             cudaMemcpyDeviceToDevice, s));
   CK_CUDA(cudaMemsetAsync(c->s1, 0, c->M_own * 4, s));
   if (c->s2) CK_CUDA(cudaMemsetAsync(c->s2, 0, c->M_own * 4, s));
@@ -1361,7 +1371,9 @@ int hdp_gather_master(hdp_ctx* c, float* out) {
   std::unique_ptr<float, void (*)(float*)> guard(buf, [](float* p) { cudaFree(p); });
   cudaStream_t s = c->comm_stream;
   for (const Bucket& bk : c->buckets) {
-    if (c->world > 1)
+    if (c->task0)  // task 0 holds the whole master
+      CK_NCCL(ncclBroadcast(c->master + bk.moff, buf + bk.off, bk.shard, ncclFloat, 0, c->comm, s));
+    else if (c->world > 1)
       CK_NCCL(ncclAllGather(c->master + bk.moff, buf + bk.off, bk.shard, ncclFloat, c->comm, s));
     else
       CK_CUDA(cudaMemcpyAsync(buf + bk.off, c->master + bk.moff, bk.shard * 4, cudaMemcpyDeviceToDevice, s));
@@ -1690,7 +1702,20 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
       const bool last = gi + 1 == groups.size();
       if (c->d.n_layers > 0)
         for (size_t bi = b0; bi < b1; ++bi) CK_CUDA(cudaStreamWaitEvent(cs, c->ev_bucket[bi], 0));
-      if (c->world > 1) {
+      if (c->task0) {
+        // the paper's step 4 literally: every worker's gradients of the group
+        // go to task 0 (grouped sends / receives, rank order kept by position)
+        KScope ks_(c, HDP_K_COMM, 0, cs);
+        CK_NCCL(ncclGroupStart());
+        for (size_t bi = b0; bi < b1; ++bi) {
+          const Bucket& bk = c->buckets[bi];
+          if (c->rank == 0)
+            for (int r = 0; r < c->world; ++r)
+              CK_NCCL(ncclRecv(c->recv + ((size_t)r * c->P + bk.off) * c->gsz, bk.len, gtype(c), r, c->comm, cs));
+          CK_NCCL(ncclSend(c->grads + bk.off * c->gsz, bk.len, gtype(c), 0, c->comm, cs));
+        }
+        CK_NCCL(ncclGroupEnd());
+      } else if (c->world > 1) {
         KScope ks_(c, HDP_K_COMM, 0, cs);
         CK_NCCL(ncclGroupStart());
         for (size_t bi = b0; bi < b1; ++bi) {
@@ -1704,18 +1729,23 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
         CK_NCCL(ncclGroupEnd());
       }
       for (size_t bi = b0; bi < b1; ++bi) {
+        if (c->task0 && c->rank != 0) break;  // step 5 runs on task 0 only
         const Bucket& bk = c->buckets[bi];
         a.count = bk.shard;
         a.W = c->master + bk.moff;
         a.S1 = c->s1 + bk.moff;
         a.S2 = c->s2 ? c->s2 + bk.moff : nullptr;
-        a.w16 = c->f32 ? nullptr : (__half*)(c->w + (bk.off + (long)c->rank * bk.shard) * 2);
-        a.w32 = c->f32 ? (float*)(c->w + (bk.off + (long)c->rank * bk.shard) * 4) : nullptr;
+        a.w16 = c->f32 ? nullptr : (__half*)(c->w + (bk.off + (long)c->owner_index() * bk.shard) * 2);
+        a.w32 = c->f32 ? (float*)(c->w + (bk.off + (long)c->owner_index() * bk.shard) * 4) : nullptr;
         const int grad_f32 = c->gf32;
         if (c->world == 1) {
           a.g = c->grads + bk.off * c->gsz;  // slot r at + r*P
           a.g_stride = c->P;
           a.nsrc = c->nslots;
+        } else if (c->task0) {
+          a.g = c->recv + bk.off * c->gsz;   // worker r's gradients at + r*P
+          a.g_stride = c->P;
+          a.nsrc = c->world;
         } else {
           a.g = c->recv + bk.off * c->gsz;
           a.g_stride = bk.shard;
@@ -1729,6 +1759,10 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
         CK_NCCL(ncclGroupStart());
         for (size_t bi = b0; bi < b1; ++bi) {
           const Bucket& bk = c->buckets[bi];
+          if (c->task0) {  // task 0 broadcasts the updated parameters
+            CK_NCCL(ncclBroadcast(c->w + bk.off * c->esz, c->w + bk.off * c->esz, bk.len, wtype(c), 0, c->comm, cs));
+            continue;
+          }
           char* mine = c->w + (bk.off + (long)c->rank * bk.shard) * c->esz;
           CK_NCCL(ncclAllGather(mine, c->w + bk.off * c->esz, bk.shard, wtype(c), c->comm, cs));
         }

@@ -22,7 +22,7 @@ HDP_OK, HDP_ERR_ARG, HDP_ERR_CUDA, HDP_ERR_NCCL, HDP_ERR_NONFINITE, HDP_ERR_STAT
 MATH_FP32, MATH_MIXED16 = 0, 1
 WIRE_FP16_A2A, WIRE_FP16_NCCLSUM, WIRE_FP32 = 0, 1, 2
 OPT_SGDM, OPT_ADAM = 0, 1
-EXCH_AUTO, EXCH_NCCL, EXCH_P2P = 0, 1, 2
+EXCH_AUTO, EXCH_NCCL, EXCH_P2P, EXCH_TASK0 = 0, 1, 2, 3
 
 EXPORTED = [
     "hdp_nccl_unique_id", "hdp_init", "hdp_destroy", "hdp_last_error", "hdp_configure", "hdp_bind",
@@ -177,7 +177,8 @@ def bind(ctx: int, arena, nbytes: int):
 
 
 EXCHANGE_KINDS = {0: "K11 over local gradient slots", 1: "NCCL all-to-all + K11 + all-gather",
-                  2: "one-kernel NVLink exchange (peer loads/stores)", 3: "one-kernel exchange, 1-GPU loopback"}
+                  2: "one-kernel NVLink exchange (peer loads/stores)", 3: "one-kernel exchange, 1-GPU loopback",
+                  4: "task-0 ablation (gather to rank 0, full update, broadcast)"}
 
 
 def exchange_kind(ctx: int) -> int:

@@ -54,15 +54,34 @@ def test_c1_multi_gpu_parity(mixed, wire, exch):
 
 
 def test_c1_multi_gpu_exchanges_bit_identical():
-    """The one-kernel NVLink exchange and the NCCL all-to-all + K11 + all-gather path
-    compute the same rank-ordered fp32 sum and update: bit-identical masters."""
+    """The one-kernel NVLink exchange, the NCCL all-to-all + K11 + all-gather path and the
+    paper-literal task-0 ablation (gather to rank 0, whole-model update, broadcast;
+    PAPER.md:94-96) compute the same rank-ordered fp32 sum and update: bit-identical
+    masters; the task-0 run also against the oracle."""
     world = _world()
     env = {"HDP_MP_CFG": "C1", "HDP_MP_MIXED": "1", "HDP_MP_WIRE": "0", "HDP_MP_GB": str(2 * world),
            "HDP_MP_STEPS": "3", "HDP_MP_LAMBDA0": "0.05"}
     a = _run(world, dict(env, HDP_MP_EXCH="2"))
     b = _run(world, dict(env, HDP_MP_EXCH="1"))
+    c = _run(world, dict(env, HDP_MP_EXCH="3"))
     assert [r["exchange_kind"] for r in a] == [2] * 3 and [r["exchange_kind"] for r in b] == [1] * 3
-    assert [r["master_sha"] for r in a] == [r["master_sha"] for r in b]
+    assert [r["exchange_kind"] for r in c] == [4] * 3
+    assert [r["master_sha"] for r in a] == [r["master_sha"] for r in b] == [r["master_sha"] for r in c]
+    for r in c:
+        assert r["weights_identical"]
+        assert max(r["master_err"].values()) <= 2e-2 and max(r["dmaster_err"].values()) <= 5e-2
+
+
+def test_c3_multi_gpu_task0_fp32_wire():
+    """Task-0 ablation with the fp32 wire on the embedding model (mixed math): parity
+    with the oracle's N-worker step."""
+    world = _world()
+    recs = _run(world, {"HDP_MP_CFG": "C3", "HDP_MP_MIXED": "1", "HDP_MP_WIRE": "2", "HDP_MP_GB": str(4 * world),
+                        "HDP_MP_SEQ": "16", "HDP_MP_STEPS": "2", "HDP_MP_LAMBDA0": "0.05", "HDP_MP_EXCH": "3"})
+    for r in recs:
+        assert r["exchange_kind"] == 4 and r["weights_identical"]
+        assert max(r["master_err"].values()) <= 2e-2, r["master_err"]
+        assert max(r["dmaster_err"].values()) <= 5e-2, r["dmaster_err"]
 
 
 def test_c3_multi_gpu_parity_reduced():
