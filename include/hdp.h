@@ -281,7 +281,7 @@ int hdp_grad_average_update(hdp_ctx* ctx, int epoch, void* stream, int* nonfinit
  * Process-wide kernel selection (ctx may be NULL; kernels of graphs captured before the
  * call are kept -- a ctx passed here has its graphs dropped): "persistent",
  *   "wavefront", "wavefront_fusex", "wavefront_wgrad", "wavefront_tmem", "recur_nbg",
- *   "recur_cluster", "gemm_cta_group", "gemm_cluster_n", "pdl", "k7_bn", "k7_splits",
+ *   "gemm_cta_group", "gemm_cluster_n", "pdl", "k7_bn", "k7_splits",
  *   "recur_trace" (integers; see csrc/options.h).  They choose between implementations
  *   of the same arithmetic (ablations, tuning); the defaults are the measured best.
  * Errors: unknown name, value out of range -> HDP_ERR_ARG.                      */

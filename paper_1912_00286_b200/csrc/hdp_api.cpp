@@ -606,7 +606,6 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
       ra.Hs = (__half*)Hs;
       ra.C = Cl;
       ra.gates = (__half*)Gl;
-      ra.counter = (unsigned*)((char*)c->status + 1024);
       ra.T = T;
       ra.B = B;
       ra.hp = (int)hp;
@@ -843,7 +842,6 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
     ra.gates = (const __half*)Gl;
     ra.C = Cl;
     ra.dA = (__half*)c->dA;
-    ra.counter = (unsigned*)((char*)c->status + 1024);
     ra.T = T;
     ra.B = B;
     ra.hp = (int)hp;
@@ -1124,12 +1122,11 @@ int check_desc_across_ranks(hdp_ctx* c, const hdp_model_desc& d) {
 
 // ====================================================================== options
 namespace hdp {
-int g_opt[OPT_COUNT] = {1, 1, 1, 1, 1, 0, 1, 0, 1, 0, 0, 0, 0};
+int g_opt[OPT_COUNT] = {1, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0};
 namespace {
-const char* const kOptNames[OPT_COUNT] = {"persistent",     "wavefront",      "wavefront_fusex", "wavefront_wgrad",
-                                          "wavefront_tmem", "recur_nbg",      "recur_cluster",   "gemm_cta_group",
-                                          "gemm_cluster_n", "pdl",            "k7_bn",           "k7_splits",
-                                          "recur_trace"};
+const char* const kOptNames[OPT_COUNT] = {"persistent",     "wavefront", "wavefront_fusex", "wavefront_wgrad",
+                                          "wavefront_tmem", "recur_nbg", "gemm_cta_group",  "gemm_cluster_n",
+                                          "pdl",            "k7_bn",     "k7_splits",       "recur_trace"};
 }
 int opt_find(const char* name) {
   for (int i = 0; i < OPT_COUNT; ++i)

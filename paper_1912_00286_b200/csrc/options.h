@@ -12,9 +12,8 @@ enum OptId {
   OPT_WAVEFRONT_WGRAD,   // 1: A8 weight gradients inside the backward wavefront (W role)
   OPT_WAVEFRONT_TMEM,    // 1: TMEM-resident A operand instantiations where they exist; 0: SMEM-A
   OPT_RECUR_NBG,         // batch groups of the recurrence plans (0 = automatic)
-  OPT_RECUR_CLUSTER,     // 1: cluster / DSMEM hand-offs in the per-layer persistent kernels
   OPT_GEMM_CTA_GROUP,    // 0 automatic, 1 single CTAs, 2 CTA pairs (cta_group::2)
-  OPT_GEMM_CLUSTER_N,    // TMA multicast of the A tile over 1 / 2 / 4 CTAs
+  OPT_GEMM_CLUSTER_N,    // TMA multicast of the A tile over 1 / 2 / 4 / 8 CTAs (0 = unicast)
   OPT_PDL,               // 1: programmatic dependent launch of the GEMM chain
   OPT_K7_BN,             // per-step K7 tile width override (0 = automatic)
   OPT_K7_SPLITS,         // per-step K7 split-K override (0 = automatic)

@@ -1,23 +1,15 @@
-// Persistent fused LSTM recurrence for small h:
-// one cooperative kernel runs all T steps of one layer's forward pass.
+// Persistent fused LSTM recurrences for small h: one launch
+// runs all T steps of a layer (per-layer cluster kernels) or of both layers of a
+// two-layer model (the wavefronts, recur2f_kernel / recur2_bwd_kernel).
 //
 //   a_t = G_x[t] + h_{t-1} U^T ;  i,f,o = sigma(a), g = tanh(a)
 //   c_t = f c_{t-1} + i g ;  h_t = o tanh(c_t)          (reading Q1)
 //
-// CTA k owns 128 interleaved gate rows = 32 units [32k, 32k+32).  Its U slice
-// (128 x h_p fp16, K-major SWIZZLE_128B) is loaded ONCE by TMA and stays in
-// shared memory for all T steps.  Per step:
-//   1. TMA prefetch of this CTA's G_x[t] slice (B x 128 fp32) -- independent of
-//      the recurrence, issued before the grid barrier;
-//   2. grid barrier: wait until every CTA published h_{t-1} (monotonic counter,
-//      release/acquire at gpu scope);
-//   3. TMA load of h_{t-1} (B x h_p fp16) and tcgen05.mma (M=128 gate rows,
-//      N=B, K=h_p) into TMEM;
-//   4. epilogue: tcgen05.ld -> a = acc + G_x; each lane activates its own gate,
-//      a 4x4 shuffle transpose inside each quad gives every lane all four
-//      gates of its unit for 1/4 of the columns; c stays in registers across
-//      steps; h_t (fp16), c_t (fp32) and the rounded gates are stored;
-//   5. publish: fence + release-add on the step counter.
+// One thread-block cluster per batch group: each CTA keeps its U (or U^T) slice
+// resident in shared memory / TMEM for all T steps, runs the step's tcgen05.mma into
+// TMEM, applies the cell in the epilogue, and pushes its slice of h_t (dA_t backward)
+// into every peer's operand buffer by cp.async.bulk shared::cta -> shared::cluster,
+// completing on the peer's mbarrier (double-buffered by step parity).
 // Layout conventions are those of hdp_api.cpp (gate row 4j+g).
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
@@ -83,175 +75,6 @@ __device__ __forceinline__ void spin_until(const unsigned* f, unsigned target) {
 // smem: [U: nkb x 16 KB][H: nkb x Bc*128 B][act: nwarps x 16 x ACT_LD fp32][barriers]
 constexpr int ACT_LD = 40;  // 32 rows + 8 pad: conflict-free float4 reads (see epilogue)
 
-// Grid (G row tiles) x (NBG batch groups).  Batch rows are independent
-// recurrences, so each batch group synchronises only its own G CTAs on its
-// own counter.  Block = 4 lane quarters x cgN column groups of warps; each
-// warp handles NCI chunks of 16 batch columns.
-template <int NCI>
-__global__ void __launch_bounds__(512, 1)
-    recur_fwd_kernel(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmH,
-                     const float* __restrict__ Gx, int T, int B, int Bc, int hp, __half* __restrict__ Hs,
-                     float* __restrict__ Cst, __half* __restrict__ gates, unsigned* __restrict__ counters) {
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int nkb = (hp + 63) / 64;
-  const int nk16 = (hp + 15) / 16;
-  const int nwarps = blockDim.x >> 5;
-  const int cgN = nwarps >> 2;
-  uint8_t* sU = smem;
-  uint8_t* sH = sU + nkb * 16384;
-  float* sAct = reinterpret_cast<float*>(sH + (size_t)nkb * Bc * 128);
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sAct + nwarps * 16 * ACT_LD);
-  uint64_t* barU = bars;
-  uint64_t* barH = bars + 1;
-  uint64_t* barM = bars + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int quarter = warp & 3;                // TMEM lane quarter this warp may access
-  const int cg = warp >> 2;                    // column group: chunks ch = ci*cgN + cg
-  const int G = gridDim.x;
-  const int row0 = blockIdx.x * 128;          // first gate row of this CTA
-  const int col0 = blockIdx.y * Bc;           // first batch column of this CTA
-  unsigned* counter = counters + blockIdx.y * 32;
-  const int r = quarter * 32 + lane;           // tile row = TMEM lane
-  const int grow = row0 + r;                   // gate row
-  const int gate = r & 3;
-  const int unit = grow >> 2;
-  const bool unit_ok = unit < hp;
-  const int fourhp = 4 * hp;
-  const uint32_t tcols = Bc <= 32 ? 32 : Bc <= 64 ? 64 : Bc <= 128 ? 128 : 256;
-
-  if (threadIdx.x == 0) {
-    ptx::tma_prefetch(&tmU);
-    ptx::tma_prefetch(&tmH);
-    for (int i = 0; i < 3; ++i) ptx::mbar_init(bars + i, 1);
-    ptx::fence_mbar_init();
-  }
-  if (warp == 2) ptx::tmem_alloc(tslot, tcols);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tbase = *tslot;
-
-  if (threadIdx.x == 0) {
-    ptx::mbar_arrive_expect_tx(barU, nkb * 16384);
-    for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sU + kb * 16384, &tmU, barU, kb * 64, row0);
-    ptx::mbar_wait(barU, 0);
-  }
-
-  // per-lane cell state for its (unit, column) pairs: columns c0 + 4q + gate
-  float creg[NCI * 4];
-#pragma unroll
-  for (int i = 0; i < NCI * 4; ++i) creg[i] = 0.f;
-
-  const uint32_t idesc = ptx::idesc_f16_f32(128, Bc, 0, 0);
-  const int nchunk = Bc / 16;
-  float* myAct = sAct + warp * 16 * ACT_LD;
-  const float gsc = gate == 2 ? 2.f : 1.f;
-
-  for (int t = 0; t < T; ++t) {
-    // (1) G_x[t] for this warp's chunks -> registers (independent of the
-    //     recurrence; issued before the grid barrier so its latency overlaps it)
-    float gx[NCI][16];
-#pragma unroll
-    for (int ci = 0; ci < NCI; ++ci) {
-      const int ch = ci * cgN + cg;
-      const bool ok = ch < nchunk && grow < fourhp;
-      const float* gp = Gx + ((size_t)t * B + col0 + ch * 16) * fourhp + grow;
-#pragma unroll
-      for (int k = 0; k < 16; ++k) gx[ci][k] = ok ? __ldg(gp + (size_t)k * fourhp) : 0.f;
-    }
-    if (t > 0) {
-      // (2) grid barrier of this batch group: all its CTAs published h_{t-1}
-      if (threadIdx.x == 0) {
-        const unsigned target = (unsigned)(G * t);
-        if (acquire_ld(counter) < target) {
-          const uint64_t t0 = ptx::globaltimer_ns();
-          while (acquire_ld(counter) < target) {
-            if (ptx::globaltimer_ns() - t0 > 10000000000ull) __trap();
-          }
-        }
-        fence_proxy_async();
-        // (3) h_{t-1} (Hs slot t, this group's rows) -> smem, then MMA
-        ptx::mbar_arrive_expect_tx(barH, nkb * Bc * 128);
-        for (int kb = 0; kb < nkb; ++kb)
-          ptx::tma_load_2d(sH + kb * Bc * 128, &tmH, barH, kb * 64, t * B + col0);
-        ptx::mbar_wait(barH, (t - 1) & 1);
-        ptx::tc_fence_after();
-        const uint32_t aU = ptx::smem_u32(sU), aH = ptx::smem_u32(sH);
-        for (int k = 0; k < nk16; ++k) {
-          const int kb = k >> 2, kk = k & 3;
-          const uint64_t ad = ptx::smem_desc_sw128(aU + kb * 16384 + kk * 32, 0, 1024);
-          const uint64_t bd = ptx::smem_desc_sw128(aH + kb * Bc * 128 + kk * 32, 0, 1024);
-          ptx::mma_f16(tbase, ad, bd, idesc, k > 0 ? 1u : 0u);
-        }
-        ptx::mma_commit(barM);
-      }
-      __syncwarp();
-      ptx::mbar_wait_relaxed(barM, (t - 1) & 1);
-      ptx::tc_fence_after();
-    }
-
-    // (4) epilogue
-    __half* hout = Hs + (size_t)(t + 1) * B * hp;
-    float* cout = Cst + (size_t)t * B * hp;
-    __half* gout = gates + (size_t)t * B * fourhp;
-#pragma unroll
-    for (int ci = 0; ci < NCI; ++ci) {
-      const int ch = ci * cgN + cg;
-      if (ch >= nchunk) break;
-      const int c0 = ch * 16;
-      float v[16];
-      if (t > 0) {
-        ptx::tmem_ld16(tbase + (static_cast<uint32_t>(quarter * 32) << 16) + c0, v);
-      } else {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = 0.f;
-      }
-      // activate own gate, stage [col][row] in this warp's smem tile (its 32 gate rows)
-#pragma unroll
-      for (int k = 0; k < 16; ++k) myAct[k * ACT_LD + lane] = act_gate(v[k] + gx[ci][k], gsc);
-      __syncwarp();
-      if (unit_ok) {
-        // lane = (unit u = lane>>2, column class g = lane&3): columns c0 + 4q + g.
-        // float4 at [col][4u]: 16-B slot (10*col + u) mod 8 is distinct in every 8-lane phase
-        const int u = lane >> 2;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-          const int col = 4 * q + gate;
-          const float4 a4 = *reinterpret_cast<const float4*>(myAct + col * ACT_LD + 4 * u);
-          const size_t b = (size_t)col0 + c0 + col;
-          const float i = a4.x, f = a4.y, g = a4.z, o = a4.w;
-          const float c = f * creg[ci * 4 + q] + i * g;
-          creg[ci * 4 + q] = c;
-          const float h = o * act_gate(c, 2.f);   // o * tanh(c)
-          cout[b * hp + unit] = c;                   // R5
-          hout[b * hp + unit] = __float2half_rn(h);  // R6
-          __align__(8) __half2 gg[2] = {__halves2half2(__float2half_rn(i), __float2half_rn(f)),
-                                        __halves2half2(__float2half_rn(g), __float2half_rn(o))};
-          *reinterpret_cast<uint2*>(gout + b * fourhp + 4 * unit) = *reinterpret_cast<const uint2*>(gg);  // R4
-        }
-      }
-      __syncwarp();
-    }
-    // (5) publish h_t
-    ptx::tc_fence_before();
-    fence_proxy_async();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      release_add(counter, 1u);
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tbase, tcols);
-  }
-}
-
 size_t fwd_smem(int hp, int Bc, int nwarps) {
   const int nkb = (hp + 63) / 64;
   return 1024 + (size_t)nkb * 16384 + (size_t)nkb * Bc * 128 + (size_t)nwarps * 16 * ACT_LD * 4 + 128;
@@ -286,210 +109,8 @@ bool plan_fwd(int B, int hp, FwdPlan* p) {
   return fwd_smem(hp, p->Bc, 4 * p->cgN) <= 227 * 1024;
 }
 
-template <int NCI>
-cudaError_t launch_fwd_t(const RecurFwdArgs& a, const FwdPlan& p, cudaStream_t s) {
-  CUtensorMap mU, mH;
-  if (encode_tmap_2d(&mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U, a.hp, 4 * a.hp, a.hp * 2, 64, 128,
-                     CU_TENSOR_MAP_SWIZZLE_128B))
-    return cudaErrorInvalidValue;
-  if (encode_tmap_2d(&mH, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.Hs, a.hp, (uint64_t)(a.T + 1) * a.B, a.hp * 2, 64,
-                     p.Bc, CU_TENSOR_MAP_SWIZZLE_128B))
-    return cudaErrorInvalidValue;
-  const int nwarps = 4 * p.cgN;
-  const size_t smem = fwd_smem(a.hp, p.Bc, nwarps);
-  cudaError_t e = cudaFuncSetAttribute(recur_fwd_kernel<NCI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)p.G, (unsigned)p.nbg);
-  cfg.blockDim = dim3((unsigned)(32 * nwarps));
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, recur_fwd_kernel<NCI>, mU, mH, a.Gx, a.T, a.B, p.Bc, a.hp, a.Hs, a.C, a.gates,
-                            a.counter);
-}
-
 
 // ============================================================== backward
-// BPTT over all t of one layer (A6 + A7):
-//   dh_t = dH_above[t] + dA_{t+1} U ;  dc = dc + dh o (1 - tanh^2 c_t)
-//   dA_t = [dc g i(1-i), dc c_{t-1} f(1-f), dc i (1-g^2), dh tanh(c_t) o(1-o)] ; dc <- dc f
-// CTA (x = 64-unit tile, y = batch group of Bc columns).  Swap-AB tcgen05:
-//   D[unit][b] = sum_r U[r][unit] dA_{t+1}[b][r]     M = 64 units, N = Bc, K = 4hp
-// A = U^T slice read MN-major straight from U (resident in SMEM for all t),
-// B = dA_{t+1} rows of the group (K-major), streamed by TMA each step.
-// M = 64 accumulator layout (1-SM): row 16q + i lives in TMEM lane 32q + i.
-// Epilogue: lane i < 16 takes columns [0, 8) of each 16-column chunk of unit
-// row 16*warp + i, lane i + 16 the columns [8, 16) (shuffled over).
-template <int NC>  // 16-column chunks per CTA (Bc = 16 * NC)
-__global__ void __launch_bounds__(128, 1)
-    recur_bwd_kernel(const __grid_constant__ CUtensorMap tmU, const __grid_constant__ CUtensorMap tmA,
-                     const float* __restrict__ dHa, int dHa_last_only, const __half* __restrict__ gates,
-                     const float* __restrict__ Cst, __half* __restrict__ dA, int T, int B, int hp,
-                     unsigned* __restrict__ counters) {
-  constexpr int Bc = 16 * NC;
-  extern __shared__ uint8_t smem_raw[];
-  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int fourhp = 4 * hp;
-  const int nkb = fourhp / 64;           // K blocks (4hp is a multiple of 64)
-  uint8_t* sU = smem;                    // nkb x 8 KB  (64 units x 64 K-rows, MN-major SW128)
-  uint8_t* sA = sU + nkb * 8192;         // nkb x Bc*128 B (K-major SW128)
-  uint64_t* bars = reinterpret_cast<uint64_t*>(sA + (size_t)nkb * Bc * 128);
-  uint64_t* barU = bars;
-  uint64_t* barA = bars + 1;
-  uint64_t* barM = bars + 2;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 3);
-
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int G = gridDim.x;
-  const int j0 = blockIdx.x * 64;
-  const int col0 = blockIdx.y * Bc;
-  unsigned* counter = counters + blockIdx.y * 32;
-  const int jl = lane & 15;
-  const int half = lane >> 4;            // 0: columns [0,8) of a chunk, 1: [8,16)
-  const int unit = j0 + warp * 16 + jl;
-  const bool unit_ok = unit < hp;
-  constexpr uint32_t tcols = Bc <= 32 ? 32 : Bc <= 64 ? 64 : 128;
-
-  if (threadIdx.x == 0) {
-    ptx::tma_prefetch(&tmU);
-    ptx::tma_prefetch(&tmA);
-    for (int i = 0; i < 3; ++i) ptx::mbar_init(bars + i, 1);
-    ptx::fence_mbar_init();
-  }
-  if (warp == 2) ptx::tmem_alloc(tslot, tcols);
-  ptx::tc_fence_before();
-  __syncthreads();
-  ptx::tc_fence_after();
-  const uint32_t tbase = *tslot;
-
-  if (threadIdx.x == 0) {
-    ptx::mbar_arrive_expect_tx(barU, nkb * 8192);
-    for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sU + kb * 8192, &tmU, barU, j0, kb * 64);
-    ptx::mbar_wait(barU, 0);
-  }
-
-  float dcr[NC * 8];  // dc state of (unit, column) pairs this lane owns
-#pragma unroll
-  for (int i = 0; i < NC * 8; ++i) dcr[i] = 0.f;
-  const uint32_t idesc = ptx::idesc_f16_f32(64, Bc, 1, 0);
-
-  for (int t = T - 1; t >= 0; --t) {
-    // (1) inputs independent of the recurrence -> registers, before the barrier
-    float dh0[NC * 8], cc[NC * 8], cp[NC * 8];
-    uint2 gq[NC * 8];
-#pragma unroll
-    for (int ch = 0; ch < NC; ++ch)
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int idx = ch * 8 + k;
-        const size_t b = (size_t)col0 + ch * 16 + half * 8 + k;
-        float d = 0.f, c1 = 0.f, c0 = 0.f;
-        uint2 gg = make_uint2(0u, 0u);
-        if (unit_ok) {
-          if (dHa_last_only) {
-            if (t == T - 1) d = __ldg(dHa + b * hp + unit);
-          } else {
-            d = __ldg(dHa + ((size_t)t * B + b) * hp + unit);
-          }
-          c1 = __ldg(Cst + ((size_t)t * B + b) * hp + unit);
-          if (t > 0) c0 = __ldg(Cst + ((size_t)(t - 1) * B + b) * hp + unit);
-          gg = __ldg(reinterpret_cast<const uint2*>(gates + ((size_t)t * B + b) * fourhp + 4 * unit));
-        }
-        dh0[idx] = d;
-        cc[idx] = c1;
-        cp[idx] = c0;
-        gq[idx] = gg;
-      }
-    if (t < T - 1) {
-      // (2) barrier: every CTA of this batch group published dA_{t+1}
-      if (threadIdx.x == 0) {
-        const unsigned target = (unsigned)(G * (T - 1 - t));
-        if (acquire_ld(counter) < target) {
-          const uint64_t t0 = ptx::globaltimer_ns();
-          while (acquire_ld(counter) < target) {
-            if (ptx::globaltimer_ns() - t0 > 10000000000ull) __trap();
-          }
-        }
-        fence_proxy_async();
-        // (3) dA_{t+1} rows of the group -> smem; MMA D[unit][b] = sum_r U[r][unit] dA[b][r]
-        const uint32_t ph = (T - 2 - t) & 1;
-        ptx::mbar_arrive_expect_tx(barA, nkb * Bc * 128);
-        for (int kb = 0; kb < nkb; ++kb)
-          ptx::tma_load_2d(sA + kb * Bc * 128, &tmA, barA, kb * 64, (t + 1) * B + col0);
-        ptx::mbar_wait(barA, ph);
-        ptx::tc_fence_after();
-        const uint32_t aU = ptx::smem_u32(sU), aA = ptx::smem_u32(sA);
-        for (int k = 0; k < nkb * 4; ++k) {
-          const int kb = k >> 2, kk = k & 3;
-          const uint64_t ad = ptx::smem_desc_sw128(aU + kb * 8192 + kk * 2048, 8192, 1024);
-          const uint64_t bd = ptx::smem_desc_sw128(aA + kb * Bc * 128 + kk * 32, 0, 1024);
-          ptx::mma_f16(tbase, ad, bd, idesc, k > 0 ? 1u : 0u);
-        }
-        ptx::mma_commit(barM);
-      }
-      __syncwarp();
-      ptx::mbar_wait_relaxed(barM, (T - 2 - t) & 1);
-      ptx::tc_fence_after();
-    }
-    // (4) epilogue: dh_rec from TMEM, cell backward, dA_t stores
-    __half* dAout = dA + (size_t)t * B * fourhp;
-#pragma unroll
-    for (int ch = 0; ch < NC; ++ch) {
-      float v[16];
-      if (t < T - 1) {
-        ptx::tmem_ld16(tbase + (static_cast<uint32_t>(warp * 32) << 16) + ch * 16, v);
-      } else {
-#pragma unroll
-        for (int k = 0; k < 16; ++k) v[k] = 0.f;
-      }
-      // lane i+16 takes columns 8..15 of lane i's row
-      float rec[8];
-#pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const float hi = __shfl_sync(0xffffffffu, v[8 + k], jl);
-        rec[k] = half ? hi : v[k];
-      }
-      if (unit_ok) {
-#pragma unroll
-        for (int k = 0; k < 8; ++k) {
-          const int idx = ch * 8 + k;
-          const size_t b = (size_t)col0 + ch * 16 + half * 8 + k;
-          const float dh = dh0[idx] + rec[k];
-          const float2 if2 = __half22float2(*reinterpret_cast<const __half2*>(&gq[idx].x));
-          const float2 go2 = __half22float2(*reinterpret_cast<const __half2*>(&gq[idx].y));
-          const float i = if2.x, f = if2.y, g = go2.x, o = go2.y;
-          const float tc = tanhf(cc[idx]);
-          const float d = dcr[idx] + dh * o * (1.f - tc * tc);
-          __align__(8) __half2 q2[2] = {
-              __halves2half2(__float2half_rn(d * g * i * (1.f - i)), __float2half_rn(d * cp[idx] * f * (1.f - f))),
-              __halves2half2(__float2half_rn(d * i * (1.f - g * g)), __float2half_rn(dh * tc * o * (1.f - o)))};
-          *reinterpret_cast<uint2*>(dAout + b * fourhp + 4 * unit) = *reinterpret_cast<const uint2*>(q2);  // R10
-          dcr[idx] = d * f;
-        }
-      }
-    }
-    // (5) publish dA_t
-    ptx::tc_fence_before();
-    fence_proxy_async();
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      __threadfence();
-      release_add(counter, 1u);
-    }
-  }
-  ptx::tc_fence_before();
-  __syncthreads();
-  if (warp == 2) {
-    ptx::tc_fence_after();
-    ptx::tmem_dealloc(tbase, tcols);
-  }
-}
-
 size_t bwd_smem(int hp, int Bc) {
   const int nkb = 4 * hp / 64;
   return 1024 + (size_t)nkb * 8192 + (size_t)nkb * Bc * 128 + 128;
@@ -514,44 +135,15 @@ bool plan_bwd(int B, int hp, int* Bc_out, int* nbg_out) {
   return false;
 }
 
-template <int NC>
-cudaError_t launch_bwd_t(const RecurBwdArgs& a, int nbg, cudaStream_t s) {
-  constexpr int Bc = 16 * NC;
-  CUtensorMap mU, mA;
-  // A operand: U^T slice, MN-major = U rows (K = 4hp) with units contiguous
-  if (encode_tmap_2d(&mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U, a.hp, 4 * a.hp, a.hp * 2, 64, 64,
-                     CU_TENSOR_MAP_SWIZZLE_128B))
-    return cudaErrorInvalidValue;
-  // B operand: dA rows [T*B][4hp], K-major
-  if (encode_tmap_2d(&mA, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.dA, 4 * a.hp, (uint64_t)a.T * a.B, 4 * a.hp * 2, 64, Bc,
-                     CU_TENSOR_MAP_SWIZZLE_128B))
-    return cudaErrorInvalidValue;
-  const size_t smem = bwd_smem(a.hp, Bc);
-  cudaError_t e = cudaFuncSetAttribute(recur_bwd_kernel<NC>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
-  if (e != cudaSuccess) return e;
-  cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3((unsigned)((a.hp + 63) / 64), (unsigned)nbg);
-  cfg.blockDim = dim3(128);
-  cfg.dynamicSmemBytes = smem;
-  cfg.stream = s;
-  cudaLaunchAttribute at[1];
-  at[0].id = cudaLaunchAttributeCooperative;
-  at[0].val.cooperative = 1;
-  cfg.attrs = at;
-  cfg.numAttrs = 1;
-  return cudaLaunchKernelEx(&cfg, recur_bwd_kernel<NC>, mU, mA, a.dHa, a.dHa_last_only, a.gates, a.C, a.dA, a.T,
-                            a.B, a.hp, a.counter);
-}
 
-
-// ============================================================== cluster variants
+// ============================================================== per-layer cluster kernels
 // One thread-block cluster per batch group (cluster = all row / unit tiles of
 // the layer, <= 8 CTAs).  The per-step exchange never leaves the chip: each
 // CTA pushes its slice of h_t (forward) or dA_t (backward) into every peer's
-// shared-memory operand buffer with st.shared::cluster (double-buffered by
-// step parity), then one barrier.cluster.arrive/wait replaces the L2 counter
-// barrier and the TMA reload.  Global copies (needed by later kernels) are
-// still written, off the critical path.
+// shared-memory operand buffer (double-buffered by step parity).  Global copies
+// (needed by later kernels) are still written, off the critical path.
+// (Round 1's grid-barrier variants -- an L2 counter barrier per step and a TMA
+// reload of h_{t-1} -- were superseded by these and removed in round 2.)
 
 // CTA = 64 units = 256 interleaved gate rows (two M=128 MMAs per K-step) =
 // one full 64-wide K-block of h, so its h_t slice is one contiguous region of
@@ -1833,10 +1425,6 @@ cudaError_t launch_cluster(const void* fn, dim3 grid, dim3 block, size_t smem, i
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
-bool use_cluster() {
-  return opt(OPT_RECUR_CLUSTER) != 0;
-}
-
 int pow2ceil(int v) {
   int p = 1;
   while (p < v) p <<= 1;
@@ -2413,35 +2001,30 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
 
 bool recur_fwd_supported(int B, int hp) {
   FwdPlan p;
-  return plan_fwd(B, hp, &p);
+  if (!plan_fwd(B, hp, &p)) return false;
+  const int nw = 8 * p.cgN;
+  return (hp + 63) / 64 <= 8 && nw <= 16 && fwd_cl_smem(hp, p.Bc, nw) <= 227 * 1024;  // one cluster per group
 }
 
 cudaError_t launch_recur_fwd(const RecurFwdArgs& a, cudaStream_t s) {
   FwdPlan p;
-  if (!plan_fwd(a.B, a.hp, &p)) return cudaErrorInvalidConfiguration;
+  if (!recur_fwd_supported(a.B, a.hp) || !plan_fwd(a.B, a.hp, &p)) return cudaErrorInvalidConfiguration;
   const int Gc = (a.hp + 63) / 64;  // CTAs of 64 units = cluster size
   const int nw = 8 * p.cgN;
-  if (use_cluster() && Gc <= 8 && nw <= 16 && fwd_cl_smem(a.hp, p.Bc, nw) <= 227 * 1024) {
-    CUtensorMap mU;
-    if (encode_tmap_2d(&mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U, a.hp, 4 * a.hp, a.hp * 2, 64, 128,
-                       CU_TENSOR_MAP_SWIZZLE_128B))
-      return cudaErrorInvalidValue;
-    const float* gx = a.Gx;
-    int T = a.T, B = a.B, Bc = p.Bc, hp = a.hp;
-    __half* hs = a.Hs;
-    float* cst = a.C;
-    __half* gt = a.gates;
-    unsigned long long* trace = a.trace;
-    void* args[] = {&mU, &gx, &T, &B, &Bc, &hp, &hs, &cst, &gt, &trace};
-    const void* fn = p.nci == 1 ? (const void*)recur_fwd_cl_kernel<1>
-                   : p.nci == 2 ? (const void*)recur_fwd_cl_kernel<2> : (const void*)recur_fwd_cl_kernel<4>;
-    return launch_cluster(fn, dim3(Gc, p.nbg), dim3(32 * nw), fwd_cl_smem(a.hp, p.Bc, nw), Gc, s, args);
-  }
-  cudaError_t e = cudaMemsetAsync(a.counter, 0, (size_t)p.nbg * 32 * sizeof(unsigned), s);
-  if (e != cudaSuccess) return e;
-  if (p.nci == 1) return launch_fwd_t<1>(a, p, s);
-  if (p.nci == 2) return launch_fwd_t<2>(a, p, s);
-  return launch_fwd_t<4>(a, p, s);
+  CUtensorMap mU;
+  if (encode_tmap_2d(&mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U, a.hp, 4 * a.hp, a.hp * 2, 64, 128,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  const float* gx = a.Gx;
+  int T = a.T, B = a.B, Bc = p.Bc, hp = a.hp;
+  __half* hs = a.Hs;
+  float* cst = a.C;
+  __half* gt = a.gates;
+  unsigned long long* trace = a.trace;
+  void* args[] = {&mU, &gx, &T, &B, &Bc, &hp, &hs, &cst, &gt, &trace};
+  const void* fn = p.nci == 1 ? (const void*)recur_fwd_cl_kernel<1>
+                 : p.nci == 2 ? (const void*)recur_fwd_cl_kernel<2> : (const void*)recur_fwd_cl_kernel<4>;
+  return launch_cluster(fn, dim3(Gc, p.nbg), dim3(32 * nw), fwd_cl_smem(a.hp, p.Bc, nw), Gc, s, args);
 }
 
 }  // namespace hdp
@@ -2450,38 +2033,29 @@ namespace hdp {
 
 bool recur_bwd_supported(int B, int hp) {
   int Bc, nbg;
-  return plan_bwd(B, hp, &Bc, &nbg);
+  if (!plan_bwd(B, hp, &Bc, &nbg)) return false;
+  return pow2ceil((hp + 63) / 64) <= 8 && bwd_cl_smem(hp, Bc) <= 227 * 1024;  // one cluster per group
 }
 
 cudaError_t launch_recur_bwd(const RecurBwdArgs& a, cudaStream_t s) {
   int Bc = 0, nbg = 0;
-  if (!plan_bwd(a.B, a.hp, &Bc, &nbg)) return cudaErrorInvalidConfiguration;
+  if (!recur_bwd_supported(a.B, a.hp) || !plan_bwd(a.B, a.hp, &Bc, &nbg)) return cudaErrorInvalidConfiguration;
   const int Gc = pow2ceil((a.hp + 63) / 64);
-  if (use_cluster() && Gc <= 8 && bwd_cl_smem(a.hp, Bc) <= 227 * 1024) {
-    CUtensorMap mU;
-    if (encode_tmap_2d(&mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U, a.hp, 4 * a.hp, a.hp * 2, 64, 64,
-                       CU_TENSOR_MAP_SWIZZLE_128B))
-      return cudaErrorInvalidValue;
-    const float* dha = a.dHa;
-    int last = a.dHa_last_only, T = a.T, B = a.B, hp = a.hp;
-    const __half* gt = a.gates;
-    const float* cst = a.C;
-    __half* da = a.dA;
-    unsigned long long* trace = a.trace;
-    void* args[] = {&mU, &dha, &last, &gt, &cst, &da, &T, &B, &hp, &trace};
-    const void* fn = Bc == 16 ? (const void*)recur_bwd_cl_kernel<1>
-                   : Bc == 32 ? (const void*)recur_bwd_cl_kernel<2>
-                   : Bc == 48 ? (const void*)recur_bwd_cl_kernel<3> : (const void*)recur_bwd_cl_kernel<4>;
-    return launch_cluster(fn, dim3(Gc, nbg), dim3(128), bwd_cl_smem(a.hp, Bc), Gc, s, args);
-  }
-  cudaError_t e = cudaMemsetAsync(a.counter, 0, (size_t)nbg * 32 * sizeof(unsigned), s);
-  if (e != cudaSuccess) return e;
-  switch (Bc / 16) {
-    case 1: return launch_bwd_t<1>(a, nbg, s);
-    case 2: return launch_bwd_t<2>(a, nbg, s);
-    case 3: return launch_bwd_t<3>(a, nbg, s);
-    default: return launch_bwd_t<4>(a, nbg, s);
-  }
+  CUtensorMap mU;
+  if (encode_tmap_2d(&mU, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, a.U, a.hp, 4 * a.hp, a.hp * 2, 64, 64,
+                     CU_TENSOR_MAP_SWIZZLE_128B))
+    return cudaErrorInvalidValue;
+  const float* dha = a.dHa;
+  int last = a.dHa_last_only, T = a.T, B = a.B, hp = a.hp;
+  const __half* gt = a.gates;
+  const float* cst = a.C;
+  __half* da = a.dA;
+  unsigned long long* trace = a.trace;
+  void* args[] = {&mU, &dha, &last, &gt, &cst, &da, &T, &B, &hp, &trace};
+  const void* fn = Bc == 16 ? (const void*)recur_bwd_cl_kernel<1>
+                 : Bc == 32 ? (const void*)recur_bwd_cl_kernel<2>
+                 : Bc == 48 ? (const void*)recur_bwd_cl_kernel<3> : (const void*)recur_bwd_cl_kernel<4>;
+  return launch_cluster(fn, dim3(Gc, nbg), dim3(128), bwd_cl_smem(a.hp, Bc), Gc, s, args);
 }
 
 }  // namespace hdp

@@ -11,7 +11,6 @@ struct RecurFwdArgs {
   __half* Hs = nullptr;       // [T+1][B][hp]; slot 0 = h_{-1} = 0 (read), slots 1..T written
   float* C = nullptr;         // [T][B][hp]
   __half* gates = nullptr;    // [T][B][4hp] activated gates, fp16 (R4)
-  unsigned* counter = nullptr;  // grid-barrier counters, 16 x 32 uints (zeroed by the launcher)
   int T = 0, B = 0, hp = 0;
   unsigned long long* trace = nullptr;  // debug: per-step phase timestamps (T x 5), nullable
 };
@@ -26,7 +25,6 @@ struct RecurBwdArgs {
   const __half* gates = nullptr;  // [T][B][4hp] saved fp16 gates
   const float* C = nullptr;       // [T][B][hp]
   __half* dA = nullptr;           // [T][B][4hp] output (fp16, R10)
-  unsigned* counter = nullptr;    // 16 x 32 uints
   int T = 0, B = 0, hp = 0;
   unsigned long long* trace = nullptr;  // debug: per-step phase timestamps (T x 5), nullable
 };

@@ -252,7 +252,7 @@ def loss_scale_state(ctx: int):
 
 # process-wide kernel switches and their defaults (csrc/options.h, hdp_set_option)
 KERNEL_OPTION_DEFAULTS = {"persistent": 1, "wavefront": 1, "wavefront_fusex": 1, "wavefront_wgrad": 1,
-                          "wavefront_tmem": 1, "recur_nbg": 0, "recur_cluster": 1, "gemm_cta_group": 0,
+                          "wavefront_tmem": 1, "recur_nbg": 0, "gemm_cta_group": 0,
                           "gemm_cluster_n": 0, "pdl": 0, "k7_bn": 0, "k7_splits": 0, "recur_trace": 0}
 
 
