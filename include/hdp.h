@@ -50,7 +50,13 @@ enum {
 
 /* Precision modes: math / synchronisation / update.    */
 enum { HDP_MATH_FP32 = 0,     /* the paper's baseline: everything fp32 (:147)      */
-       HDP_MATH_MIXED16 = 1   /* fp16 math + fp16 wire + fp32 master/update         */
+       HDP_MATH_MIXED16 = 1,  /* fp16 math + fp16 wire + fp32 master/update         */
+       HDP_MATH_BF16 = 2      /* NEXT-3 variant (not in the paper): bfloat16 at every
+                                 16-bit rounding point of MIXED16 (weights, inputs,
+                                 h, gates, dA, gradients, wire), fp32 accumulation,
+                                 fp32 master/update (reading Q29); dense
+                                 inputs are bf16; runs the per-step GEMM path (the
+                                 fused recurrences are fp16-only); no recurrent dropout */
 };
 /* Wire format of the gradient exchange.              */
 enum { HDP_WIRE_FP16_A2A = 0,     /* fp16 all-to-all, fp32 rank-ordered sum in K11 (default) */

@@ -28,6 +28,8 @@ Modes
             R9 dz fp16, R10 dA fp16, R12 parameter gradients fp16 (one RNE
             of the float64 accumulation).  R0 (inputs) and R1 (weights) are
             fp16 by construction of the caller.
+  "bf16"  : the same rounding points with bfloat16 in place of fp16 (NEXT-3 bf16
+            math mode, reading Q29; oracle/bfloat16.py); R5 c stays fp32.
 """
 from __future__ import annotations
 
@@ -35,9 +37,11 @@ from typing import Dict, List
 
 import numpy as np
 
+from .bfloat16 import rbf16
 from .binary16 import r16, r32
 
-MODES = ("fp64", "fp32", "mixed")
+MODES = ("fp64", "fp32", "mixed", "bf16")
+LOWP = ("mixed", "bf16")     # modes with 16-bit rounding points
 
 
 # ----------------------------------------------------------------------------
@@ -86,7 +90,8 @@ def _sigmoid(a):
 
 
 def _q16(mode):
-    return r16 if mode == "mixed" else (lambda v: v)
+    """The 16-bit rounding of the mode's rounding points (identity in fp32 / fp64)."""
+    return r16 if mode == "mixed" else rbf16 if mode == "bf16" else (lambda v: v)
 
 
 # ----------------------------------------------------------------------------
@@ -139,7 +144,7 @@ def forward(cfg, P: Dict[str, np.ndarray], x, targets, alpha: float, mode: str, 
             g = np.tanh(a[:, 2 * h:3 * h])
             o = _sigmoid(a[:, 3 * h:4 * h])
             c = f * c_prev + i * g
-            if mode == "mixed":
+            if mode in LOWP:
                 c = r32(c)                       # R5
             hh = q(o * np.tanh(c))               # R6
             gates[t] = q(np.concatenate([i, f, g, o], axis=1))   # R4 (saved)
@@ -254,6 +259,6 @@ def backward(cfg, P: Dict[str, np.ndarray], cache, alpha: float, mode: str,
             tok = cache["tokens"]
             np.add.at(dE, tok.T.reshape(-1), dX0.reshape(-1, dX0.shape[-1]))
             G["E"] = dE
-    if mode == "mixed":
-        G = {k: r16(v) for k, v in G.items()}    # R12
+    if mode in LOWP:
+        G = {k: q(v) for k, v in G.items()}      # R12
     return G

@@ -30,11 +30,14 @@ import numpy as np
 
 from . import dropout as dropout_mod
 from . import lstm, optim
+from .bfloat16 import rbf16
 from .binary16 import count_nonfinite, r16
 
 
 def working_weights(master: np.ndarray, mode: str) -> np.ndarray:
     """R1: the weights used by fprop/bprop (fp16 copy of the master in mixed mode)."""
+    if mode == "bf16":
+        return rbf16(master)
     return r16(master) if mode == "mixed" else np.asarray(master, np.float64)
 
 
@@ -100,6 +103,6 @@ def train_step(cfg, master, state: Dict[str, np.ndarray], x_global, t_global, N:
         "avg": avg,
         "master": W,
         "state": new_state,
-        "w16": r16(W),
+        "w16": rbf16(W) if mode == "bf16" else r16(W),
         "nonfinite": nonfinite,
     }

@@ -12,6 +12,7 @@
 //   nonfinite += number of Inf/NaN contributions
 // HBM traffic per element: N*sizeof(g) + 4+4 (W,H read) + 4+4 (W,H write) + 2 (w16).
 // 128-bit loads/stores, grid-stride over 8-element vectors.
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -38,6 +39,19 @@ struct Vec8<__half> {
     for (int i = 0; i < 4; ++i) {
       nf += ((w[i] & 0x7C00u) == 0x7C00u);
       nf += ((w[i] & 0x7C000000u) == 0x7C000000u);
+    }
+  }
+};
+template <>
+struct Vec8<__nv_bfloat16> {
+  __device__ static void load(const __nv_bfloat16* p, float (&o)[8], int& nf) {
+    const uint4 u = __ldcs(reinterpret_cast<const uint4*>(p));
+    const uint32_t w[4] = {u.x, u.y, u.z, u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {  // bf16 = the upper half of a binary32
+      o[2 * i] = __uint_as_float(w[i] << 16);
+      o[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+      nf += ((w[i] & 0x7F80u) == 0x7F80u) + ((w[i] & 0x7F800000u) == 0x7F800000u);
     }
   }
 };
@@ -72,10 +86,14 @@ __device__ __forceinline__ float upd_adam(const UpdateArgs& a, float g, float& W
   return W;
 }
 
+// the working weight of this step: fp16(W) / bf16(W) (mixed modes, R1) or W
+__device__ __forceinline__ float w_work(const UpdateArgs& a, float W) {
+  if (!a.w16) return W;
+  return a.w_bf16 ? __bfloat162float(__float2bfloat16_rn(W)) : __half2float(__float2half_rn(W));
+}
 __device__ __forceinline__ float l2_term(const UpdateArgs& a, float g, float W) {
   if (a.l2x2 == 0.f) return g;
-  const float wk = a.w16 ? __half2float(__float2half_rn(W)) : W;
-  return __fadd_rn(g, __fmul_rn(a.l2x2, wk));
+  return __fadd_rn(g, __fmul_rn(a.l2x2, w_work(a, W)));
 }
 
 // EXT = 0: the plain SGD-m / Adam step (the hot configuration); EXT = 1 adds the L2 term and
@@ -127,7 +145,12 @@ __global__ void __launch_bounds__(256) avg_update_kernel(UpdateArgs a) {
     *reinterpret_cast<float4*>(a.W + e + 4) = make_float4(w[4], w[5], w[6], w[7]);
     *reinterpret_cast<float4*>(a.S1 + e) = make_float4(h[0], h[1], h[2], h[3]);
     *reinterpret_cast<float4*>(a.S1 + e + 4) = make_float4(h[4], h[5], h[6], h[7]);
-    if (a.w16) {
+    if (a.w16 && a.w_bf16) {
+      __align__(16) __nv_bfloat162 o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[i] = __floats2bfloat162_rn(w[2 * i], w[2 * i + 1]);
+      *reinterpret_cast<uint4*>(a.w16 + e) = *reinterpret_cast<const uint4*>(o);
+    } else if (a.w16) {
       __align__(16) __half2 o[4];
 #pragma unroll
       for (int i = 0; i < 4; ++i) o[i] = __halves2half2(__float2half_rn(w[2 * i]), __float2half_rn(w[2 * i + 1]));
@@ -159,7 +182,8 @@ __global__ void __launch_bounds__(256) avg_update_kernel(UpdateArgs a) {
     }
     a.W[e] = w;
     a.S1[e] = h;
-    if (a.w16) a.w16[e] = __float2half_rn(w);
+    if (a.w16 && a.w_bf16) reinterpret_cast<__nv_bfloat16*>(a.w16)[e] = __float2bfloat16_rn(w);
+    else if (a.w16) a.w16[e] = __float2half_rn(w);
     if (a.w32) a.w32[e] = w;
   }
   if (a.nonfinite) {
@@ -201,7 +225,9 @@ cudaError_t launch_count_nonfinite(const void* g, long n, int g_f32, int* count,
   long blocks = ((n >> 3) + 255) / 256;
   if (blocks > 148L * 8) blocks = 148L * 8;
   if (blocks < 1) blocks = 1;
-  if (g_f32) count_nonfinite_kernel<float><<<(int)blocks, 256, 0, s>>>((const float*)g, n, count);
+  if (g_f32 == ET_F32) count_nonfinite_kernel<float><<<(int)blocks, 256, 0, s>>>((const float*)g, n, count);
+  else if (g_f32 == ET_BF16)
+    count_nonfinite_kernel<__nv_bfloat16><<<(int)blocks, 256, 0, s>>>((const __nv_bfloat16*)g, n, count);
   else count_nonfinite_kernel<__half><<<(int)blocks, 256, 0, s>>>((const __half*)g, n, count);
   return cudaGetLastError();
 }
@@ -223,9 +249,12 @@ cudaError_t launch_avg_update(const UpdateArgs& a, int grad_is_f32, int optimize
 #define HDP_AVG_LAUNCH(GT, OPT)                                                         \
   (ext ? (avg_update_kernel<GT, OPT, true><<<g, 256, 0, s>>>(a), 0)                     \
        : (avg_update_kernel<GT, OPT, false><<<g, 256, 0, s>>>(a), 0))
-  if (grad_is_f32) {
+  if (grad_is_f32 == ET_F32) {
     if (optimizer == 0) HDP_AVG_LAUNCH(float, 0);
     else HDP_AVG_LAUNCH(float, 1);
+  } else if (grad_is_f32 == ET_BF16) {
+    if (optimizer == 0) HDP_AVG_LAUNCH(__nv_bfloat16, 0);
+    else HDP_AVG_LAUNCH(__nv_bfloat16, 1);
   } else {
     if (optimizer == 0) HDP_AVG_LAUNCH(__half, 0);
     else HDP_AVG_LAUNCH(__half, 1);

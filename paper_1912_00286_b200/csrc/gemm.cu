@@ -42,12 +42,22 @@ struct TileCfg {
   static constexpr int SMEM = STAGES * STAGE + 1024 /*align slack*/ + 256 /*barriers*/ + EPI_BYTES;
 };
 
-__device__ __forceinline__ float bias_at(const Epilogue& e, long i) {
-  return e.bias_f16 ? __half2float(reinterpret_cast<const __half*>(e.bias)[i]) : reinterpret_cast<const float*>(e.bias)[i];
+// 16-bit working type of the operands / outputs: fp16, or bfloat16 (Epilogue::bf16, the
+// bf16 math mode).  Values travel as their bit patterns (uint16_t).
+__device__ __forceinline__ uint16_t cvt16(float v, int bf) {
+  return bf ? __bfloat16_as_ushort(__float2bfloat16_rn(v)) : __half_as_ushort(__float2half_rn(v));
+}
+__device__ __forceinline__ float f16v(uint32_t bits, int bf) {
+  bits &= 0xFFFFu;
+  return bf ? __uint_as_float(bits << 16) : __half2float(__ushort_as_half((unsigned short)bits));
+}
+__device__ __forceinline__ int nonfinite16(uint16_t b, int bf) {
+  return bf ? (b & 0x7F80u) == 0x7F80u : (b & 0x7C00u) == 0x7C00u;
 }
 
-__device__ __forceinline__ int f16_nonfinite(__half h) {
-  return (__half_as_ushort(h) & 0x7C00) == 0x7C00;
+__device__ __forceinline__ float bias_at(const Epilogue& e, long i) {
+  return e.bias_f16 ? f16v(reinterpret_cast<const uint16_t*>(e.bias)[i], e.bf16)
+                    : reinterpret_cast<const float*>(e.bias)[i];
 }
 
 // Store 16 consecutive columns [n, n+16) of row m.
@@ -97,24 +107,24 @@ __device__ __forceinline__ void epi_store16(const Epilogue& epi, float* ws, int 
         float* p = o + (size_t)(n + j) * epi.ldo + m;
         *p = epi.accumulate ? *p + v[j] : v[j];
       }
-  } else {  // EPI_F16
-    __half* o = reinterpret_cast<__half*>(epi.out) + (size_t)m * epi.ldo;
+  } else {  // EPI_F16 (fp16, or bf16 in the bf16 mode)
+    uint16_t* o = reinterpret_cast<uint16_t*>(epi.out) + (size_t)m * epi.ldo;
     if (n + 16 <= N && (epi.ldo & 7) == 0) {
 #pragma unroll
       for (int j = 0; j < 16; j += 8) {
-        __align__(16) __half hv[8];
+        __align__(16) uint16_t hv[8];
 #pragma unroll
         for (int q = 0; q < 8; ++q) {
-          hv[q] = __float2half_rn(v[j + q]);
-          nf += f16_nonfinite(hv[q]);
+          hv[q] = cvt16(v[j + q], epi.bf16);
+          nf += nonfinite16(hv[q], epi.bf16);
         }
         *reinterpret_cast<uint4*>(o + n + j) = *reinterpret_cast<const uint4*>(hv);
       }
     } else {
       for (int j = 0; j < 16; ++j)
         if (n + j < N) {
-          __half h = __float2half_rn(v[j]);
-          nf += f16_nonfinite(h);
+          const uint16_t h = cvt16(v[j], epi.bf16);
+          nf += nonfinite16(h, epi.bf16);
           o[n + j] = h;
         }
     }
@@ -132,15 +142,15 @@ __device__ __forceinline__ float lstm_tanh(float x) {
 }
 
 // recurrent dropout: the masked copy h~ of 8 units of row m (R6d: fp16 of fp32(h) * scale)
-__device__ __forceinline__ void lstm_drop_store(const Epilogue& e, int m, int u0, const __half (&hh)[8]) {
+__device__ __forceinline__ void lstm_drop_store(const Epilogue& e, int m, int u0, const uint16_t (&hh)[8]) {
   const uint32_t sk = drop_seq_key(drop_layer_key(e.drop_seed, (uint32_t)*e.drop_step, e.drop_layer),
                                    e.drop_seq0 + (uint32_t)m);
-  __align__(16) __half ht[8];
+  __align__(16) uint16_t ht[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j)
-    ht[j] = drop_kept(sk, (uint32_t)(u0 + j), e.drop_thr) ? __float2half_rn(__half2float(hh[j]) * e.drop_scale)
-                                                          : __float2half_rn(0.f);
-  *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(e.htout) + (size_t)m * e.hp + u0) =
+    ht[j] = drop_kept(sk, (uint32_t)(u0 + j), e.drop_thr) ? cvt16(f16v(hh[j], e.bf16) * e.drop_scale, e.bf16)
+                                                          : (uint16_t)0;
+  *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(e.htout) + (size_t)m * e.hp + u0) =
       *reinterpret_cast<const uint4*>(ht);
 }
 
@@ -157,8 +167,8 @@ __device__ __forceinline__ void lstm_fwd_chunk(const Epilogue& e, int m, int n, 
 #pragma unroll
     for (int j = 0; j < 8; ++j) cp[j] = 0.f;
   }
-  __align__(16) __half gh[32];
-  __align__(16) __half hh[8];
+  __align__(16) uint16_t gh[32];
+  __align__(16) uint16_t hh[8];
   float cn[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -167,19 +177,19 @@ __device__ __forceinline__ void lstm_fwd_chunk(const Epilogue& e, int m, int n, 
     const float g = lstm_tanh(g4.z + v[4 * j + 2]), o = lstm_sigmoid(g4.w + v[4 * j + 3]);
     const float c = f * cp[j] + i * g;
     cn[j] = c;
-    hh[j] = __float2half_rn(o * lstm_tanh(c));  // R6
-    gh[4 * j] = __float2half_rn(i);         // R4
-    gh[4 * j + 1] = __float2half_rn(f);
-    gh[4 * j + 2] = __float2half_rn(g);
-    gh[4 * j + 3] = __float2half_rn(o);
+    hh[j] = cvt16(o * lstm_tanh(c), e.bf16);  // R6
+    gh[4 * j] = cvt16(i, e.bf16);         // R4
+    gh[4 * j + 1] = cvt16(f, e.bf16);
+    gh[4 * j + 2] = cvt16(g, e.bf16);
+    gh[4 * j + 3] = cvt16(o, e.bf16);
   }
-  uint4* go = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(e.gates) + (size_t)m * 4 * e.hp + n);
+  uint4* go = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(e.gates) + (size_t)m * 4 * e.hp + n);
 #pragma unroll
   for (int q = 0; q < 4; ++q) go[q] = reinterpret_cast<const uint4*>(gh)[q];
   float4* co = reinterpret_cast<float4*>(e.cout + (size_t)m * e.hp + u0);
   co[0] = make_float4(cn[0], cn[1], cn[2], cn[3]);
   co[1] = make_float4(cn[4], cn[5], cn[6], cn[7]);
-  *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(e.hout) + (size_t)m * e.hp + u0) =
+  *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(e.hout) + (size_t)m * e.hp + u0) =
       *reinterpret_cast<const uint4*>(hh);
   if (e.drop_step) lstm_drop_store(e, m, u0, hh);
 }
@@ -189,8 +199,8 @@ __device__ __forceinline__ void lstm_fwd_chunk_reg(const Epilogue& e, int m, int
                                                    const float4 (&gx)[8], const float4 (&cp4)[2]) {
   const int u0 = n >> 2;
   const float cp[8] = {cp4[0].x, cp4[0].y, cp4[0].z, cp4[0].w, cp4[1].x, cp4[1].y, cp4[1].z, cp4[1].w};
-  __align__(16) __half gh[32];
-  __align__(16) __half hh[8];
+  __align__(16) uint16_t gh[32];
+  __align__(16) uint16_t hh[8];
   float cn[8];
 #pragma unroll
   for (int j = 0; j < 8; ++j) {
@@ -198,19 +208,19 @@ __device__ __forceinline__ void lstm_fwd_chunk_reg(const Epilogue& e, int m, int
     const float g = lstm_tanh(gx[j].z + v[4 * j + 2]), o = lstm_sigmoid(gx[j].w + v[4 * j + 3]);
     const float c = f * cp[j] + i * g;
     cn[j] = c;
-    hh[j] = __float2half_rn(o * lstm_tanh(c));  // R6
-    gh[4 * j] = __float2half_rn(i);         // R4
-    gh[4 * j + 1] = __float2half_rn(f);
-    gh[4 * j + 2] = __float2half_rn(g);
-    gh[4 * j + 3] = __float2half_rn(o);
+    hh[j] = cvt16(o * lstm_tanh(c), e.bf16);  // R6
+    gh[4 * j] = cvt16(i, e.bf16);         // R4
+    gh[4 * j + 1] = cvt16(f, e.bf16);
+    gh[4 * j + 2] = cvt16(g, e.bf16);
+    gh[4 * j + 3] = cvt16(o, e.bf16);
   }
-  uint4* go = reinterpret_cast<uint4*>(reinterpret_cast<__half*>(e.gates) + (size_t)m * 4 * e.hp + n);
+  uint4* go = reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(e.gates) + (size_t)m * 4 * e.hp + n);
 #pragma unroll
   for (int q = 0; q < 4; ++q) go[q] = reinterpret_cast<const uint4*>(gh)[q];
   float4* co = reinterpret_cast<float4*>(e.cout + (size_t)m * e.hp + u0);
   co[0] = make_float4(cn[0], cn[1], cn[2], cn[3]);
   co[1] = make_float4(cn[4], cn[5], cn[6], cn[7]);
-  *reinterpret_cast<uint4*>(reinterpret_cast<__half*>(e.hout) + (size_t)m * e.hp + u0) =
+  *reinterpret_cast<uint4*>(reinterpret_cast<uint16_t*>(e.hout) + (size_t)m * e.hp + u0) =
       *reinterpret_cast<const uint4*>(hh);
   if (e.drop_step) lstm_drop_store(e, m, u0, hh);
 }
@@ -227,16 +237,14 @@ __device__ __forceinline__ void lstm_bwd_unit(const Epilogue& e, size_t idx, flo
   }
   dh += dh_rec;
   const uint2 gu = reinterpret_cast<const uint2*>(e.gates)[idx];
-  const float2 g01 = __half22float2(*reinterpret_cast<const __half2*>(&gu.x));
-  const float2 g23 = __half22float2(*reinterpret_cast<const __half2*>(&gu.y));
-  const float i = g01.x, f = g01.y, g = g23.x, o = g23.y;
+  const float i = f16v(gu.x, e.bf16), f = f16v(gu.x >> 16, e.bf16);
+  const float g = f16v(gu.y, e.bf16), o = f16v(gu.y >> 16, e.bf16);
   const float c = e.ct[idx];
   const float cp = e.cprev ? e.cprev[idx] : 0.f;
   const float tc = lstm_tanh(c);
   const float d = e.dc[idx] + dh * o * (1.f - tc * tc);
-  __align__(8) __half2 hv[2] = {
-      __halves2half2(__float2half_rn(d * g * i * (1.f - i)), __float2half_rn(d * cp * f * (1.f - f))),
-      __halves2half2(__float2half_rn(d * i * (1.f - g * g)), __float2half_rn(dh * tc * o * (1.f - o)))};
+  __align__(8) uint16_t hv[4] = {cvt16(d * g * i * (1.f - i), e.bf16), cvt16(d * cp * f * (1.f - f), e.bf16),
+                                 cvt16(d * i * (1.f - g * g), e.bf16), cvt16(dh * tc * o * (1.f - o), e.bf16)};
   reinterpret_cast<uint2*>(e.dA)[idx] = *reinterpret_cast<const uint2*>(hv);  // R10
   e.dc[idx] = d * f;
 }
@@ -378,7 +386,8 @@ __global__ void __launch_bounds__(320, 1)
   } else if (warp == 1) {
     if (lane == 0 && prank == 0) {
       // ---------------- MMA issuer (the pair leader for CG = 2)
-      constexpr uint32_t idesc = ptx::idesc_f16_f32(BM * CG, BN, AMN, BMN);
+      // operand format bits [7, 10) / [10, 13): 0 = fp16, 1 = bf16 (the bf16 math mode)
+      const uint32_t idesc = ptx::idesc_f16_f32(BM * CG, BN, AMN, BMN) | (epi.bf16 ? (1u << 7) | (1u << 10) : 0u);
       constexpr uint16_t pmask = 3;
       int it = 0, lt = 0;
       for (int tile = tile0; tile < ntiles; tile += tstep, ++lt) {
@@ -423,7 +432,7 @@ __global__ void __launch_bounds__(320, 1)
     float* st = epi_stage + (warp - 2) * 32 * C::EPI_LD;
     const bool f16 = epi.mode == EPI_F16;
     const bool fast = !epi.accumulate && (epi.mode == EPI_F32 || epi.mode == EPI_SPLITK || f16);
-    __half* o16 = reinterpret_cast<__half*>(epi.out);
+    uint16_t* o16 = reinterpret_cast<uint16_t*>(epi.out);
     const bool post = epi.mode != EPI_SPLITK;  // bias / relu belong to the reduction for split-K
     // accumulator b drained: the MMA issuer's (leader's) barrier
     auto drained = [&](int b) {
@@ -520,13 +529,13 @@ __global__ void __launch_bounds__(320, 1)
               const float4 qq = *reinterpret_cast<const float4*>(st + r * C::EPI_LD + cc);
               const float qv[4] = {qq.x, qq.y, qq.z, qq.w};
               if (f16) {
-                __align__(8) __half h[4];
+                __align__(8) uint16_t h[4];
 #pragma unroll
                 for (int u = 0; u < 4; ++u) {
-                  h[u] = __float2half_rn(qv[u]);
-                  if (n + u < N) nf += f16_nonfinite(h[u]);
+                  h[u] = cvt16(qv[u], epi.bf16);
+                  if (n + u < N) nf += nonfinite16(h[u], epi.bf16);
                 }
-                __half* dst = o16 + (size_t)mr * ldo + n;
+                uint16_t* dst = o16 + (size_t)mr * ldo + n;
                 if (vec && n + 4 <= N) {
                   *reinterpret_cast<uint2*>(dst) = *reinterpret_cast<const uint2*>(h);
                 } else {
@@ -597,9 +606,9 @@ __global__ void splitk_reduce_kernel(const float* __restrict__ ws, int splits, i
       float* o = reinterpret_cast<float*>(epi.out) + (size_t)n * epi.ldo + m;
       *o = epi.accumulate ? *o + s : s;
     } else {
-      __half h = __float2half_rn(s);
-      nf += f16_nonfinite(h);
-      reinterpret_cast<__half*>(epi.out)[(size_t)m * epi.ldo + n] = h;
+      const uint16_t h = cvt16(s, epi.bf16);
+      nf += nonfinite16(h, epi.bf16);
+      reinterpret_cast<uint16_t*>(epi.out)[(size_t)m * epi.ldo + n] = h;
     }
   }
   if (epi.mode == EPI_F16 && epi.nonfinite) {

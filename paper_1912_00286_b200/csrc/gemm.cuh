@@ -9,6 +9,7 @@
 // live -- no transposes.
 #pragma once
 #include <cuda.h>
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <cstddef>
@@ -58,6 +59,7 @@ struct Epilogue {
   const int* drop_step = nullptr;  // device counter of completed updates
   uint32_t drop_seed = 0, drop_thr = 0, drop_layer = 0, drop_seq0 = 0;
   float drop_scale = 1.f;
+  int bf16 = 0;                 // 16-bit operands / outputs are bfloat16 (bf16 math mode), else fp16
 };
 
 struct GemmPlan {

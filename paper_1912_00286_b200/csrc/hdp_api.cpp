@@ -7,6 +7,7 @@
 // bucket b overlaps the BPTT of the layers below it.
 #include "../../include/hdp.h"
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <nccl.h>
 
@@ -101,6 +102,7 @@ struct hdp_ctx {
   bool configured = false, bound = false, loaded = false, poisoned = false;
   hdp_model_desc d{};
   bool f32 = false;       // FP32 math mode
+  bool bf = false;        // bf16 math mode (NEXT-3): bfloat16 in place of fp16 at every rounding point
   bool gf32 = false;      // fp32 gradients / wire
   int nslots = 1;
   long hp = 0, Ip0 = 0, Fp = 0, esz = 2, gsz = 2;
@@ -203,8 +205,9 @@ struct hdp_ctx {
   char* hst = nullptr;        // library-owned: per slot [L][T+1][B][hp] fp16 masked recurrent inputs
   bool drop_on() const { return keep < 1.0; }
   // the per-layer persistent recurrences have no dropout; the two-layer wavefronts do
-  bool recur_ok() const { return hdp::opt(hdp::OPT_PERSISTENT) != 0 && !drop_on(); }
-  bool wave_ok() const { return hdp::opt(hdp::OPT_PERSISTENT) != 0; }
+  // (the fused recurrences are fp16-only: the bf16 mode runs the per-step path)
+  bool recur_ok() const { return hdp::opt(hdp::OPT_PERSISTENT) != 0 && !drop_on() && !bf; }
+  bool wave_ok() const { return hdp::opt(hdp::OPT_PERSISTENT) != 0 && !bf; }
   int* drop_step() const { return status + 14; }  // completed updates (mask counter)
   char* Hst(int slot, int l) const {
     return hst + ((size_t)slot * d.n_layers + l) * (size_t)(d.max_seq + 1) * d.max_batch * hp * 2;
@@ -214,6 +217,9 @@ struct hdp_ctx {
   long adam_k = 0;
 
   int L() const { return d.n_layers; }
+  // element types (kernels.cuh ET_*) of the working copy / activations and of the gradients
+  int et() const { return f32 ? hdp::ET_F32 : bf ? hdp::ET_BF16 : hdp::ET_F16; }
+  int gt() const { return gf32 ? hdp::ET_F32 : bf ? hdp::ET_BF16 : hdp::ET_F16; }
   int owner_index() const { return task0 ? 0 : rank; }  // which shard of each bucket this rank owns
   int Nw() const { return world * nslots; }
   void* W(int bi) const { return w + blocks[bi].dev_off * esz; }
@@ -487,10 +493,12 @@ int gemm(hdp_ctx* c, int tag, const void* A, long lda, int amn, const void* B, l
          long K, const hdp::Epilogue& epi, cudaStream_t s, int force_bn = 0, int force_splits = 0) {
   hdp::GemmPlan p;
   int r;
+  hdp::Epilogue ebf = epi;
+  ebf.bf16 = c->bf ? 1 : 0;  // bf16 math mode: bfloat16 operands (idesc format bits) and 16-bit outputs
   if (c->f32)
     r = hdp::gemm_plan_f32(&p, (const float*)A, lda, amn, (const float*)B, ldb, bmn, (int)M, (int)N, (int)K, epi);
   else
-    r = hdp::gemm_plan_tc(&p, (const __half*)A, lda, amn, (const __half*)B, ldb, bmn, (int)M, (int)N, (int)K, epi,
+    r = hdp::gemm_plan_tc(&p, (const __half*)A, lda, amn, (const __half*)B, ldb, bmn, (int)M, (int)N, (int)K, ebf,
                           c->ws, c->ws_floats, force_bn, force_splits);
   if (r) return fail(HDP_ERR_ARG, "gemm plan %ldx%ldx%ld: %s", M, N, K, hdp::gemm_last_error());
   KScope ks(c, tag, p.tc && (p.splits > 1 || epi.mode == hdp::EPI_LSTM_BWD) ? 2 : 1, s);
@@ -523,6 +531,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
   const long hp = c->hp, e = c->esz, L = d.n_layers;
   const long rows = (long)B * T;
   const int f32 = c->f32;
+  const int et = c->et();  // element type passed to the non-GEMM launchers
   const long hs_layer = (long)(T + 1) * B * hp;  // elements per layer in Hs (actual B, T)
   const long c_layer = (long)T * B * hp;
   const long g_layer = (long)T * B * 4 * hp;
@@ -530,13 +539,13 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
   if (d.vocab > 0)
     {
       KScope ks_(c, HDP_K_INPUT, 1, s);
-      CK_CUDA(hdp::launch_embed_gather((const int32_t*)S.stage_x, B, T, c->W(c->find("E")), (int)c->Ip0, S.X0, f32,
+      CK_CUDA(hdp::launch_embed_gather((const int32_t*)S.stage_x, B, T, c->W(c->find("E")), (int)c->Ip0, S.X0, et,
                                        d.vocab, c->status + 16, s));
     }
   else
     {
       KScope ks_(c, HDP_K_INPUT, 1, s);
-      CK_CUDA(hdp::launch_pack_input(S.stage_x, f32, B, T, d.input_dim, (int)c->Ip0, S.X0, f32, s));
+      CK_CUDA(hdp::launch_pack_input(S.stage_x, et, B, T, d.input_dim, (int)c->Ip0, S.X0, et, s));
     }
   char nm[16];
   for (int l = 0; l < L; ++l) {
@@ -647,7 +656,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
       // K3 (A3)
       {
         KScope ks_(c, HDP_K_CELL_FWD, 1, s);
-        CK_CUDA(hdp::launch_cell_fwd(f32, c->Gx + (long)t * B * 4 * hp, t > 0 ? c->Gh : nullptr,
+        CK_CUDA(hdp::launch_cell_fwd(et, c->Gx + (long)t * B * 4 * hp, t > 0 ? c->Gh : nullptr,
                                      t > 0 ? Cl + (long)(t - 1) * B * hp : nullptr, Gl + (long)t * B * 4 * hp * e,
                                      Cl + (long)t * B * hp, Hs + (long)(t + 1) * B * hp * e, B, (int)hp, s));
       }
@@ -671,7 +680,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
     CK(gemm(c, HDP_K_HEAD_FWD, Htop, hp, 0, c->W(iF), hp, 0, rows, c->Fp, hp, ez, s));
     {
       KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
-      CK_CUDA(hdp::launch_head_out(f32, S.Z, (int)rows, (int)c->Fp, c->Fp, c->W(iwo), c->W(ibo), S.stage_t, 0, B, T,
+      CK_CUDA(hdp::launch_head_out(et, S.Z, (int)rows, (int)c->Fp, c->Fp, c->W(iwo), c->W(ibo), S.stage_t, 0, B, T,
                                    c->alpha, 1.f / (float)rows, S.y, S.dy, S.partials, s, S.dz, c->dyn_alpha()));
     }
     {
@@ -682,7 +691,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
     const char* Hlast = S.Hs + ((L - 1) * hs_layer + (long)T * B * hp) * e;
     {
       KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
-      CK_CUDA(hdp::launch_head_out(f32, Hlast, B, (int)hp, hp, c->W(iwo), c->W(ibo), S.stage_t, 1, B, T, c->alpha,
+      CK_CUDA(hdp::launch_head_out(et, Hlast, B, (int)hp, hp, c->W(iwo), c->W(ibo), S.stage_t, 1, B, T, c->alpha,
                                    1.f / (float)B, S.y, S.dy, S.partials, s, nullptr, c->dyn_alpha()));
     }
     {
@@ -692,7 +701,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
   } else {
     {
       KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
-      CK_CUDA(hdp::launch_head_out(f32, Htop, (int)rows, (int)hp, hp, c->W(iwo), c->W(ibo), S.stage_t, 0, B, T,
+      CK_CUDA(hdp::launch_head_out(et, Htop, (int)rows, (int)hp, hp, c->W(iwo), c->W(ibo), S.stage_t, 0, B, T,
                                    c->alpha, 1.f / (float)rows, S.y, S.dy, S.partials, s, nullptr, c->dyn_alpha()));
     }
     {
@@ -702,7 +711,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
   }
   if (c->l2 > 0) {  // reported loss += l2 * ||w||^2 over the working weights
     KScope ks_(c, HDP_K_HEAD_FWD, 2, s);
-    CK_CUDA(hdp::launch_l2_loss(f32, c->w, c->P, c->l2part, c->l2, S.loss, s));
+    CK_CUDA(hdp::launch_l2_loss(et, c->w, c->P, c->l2part, c->l2, S.loss, s));
   }
   return HDP_OK;
 }
@@ -715,6 +724,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
   const long hp = c->hp, e = c->esz, L = d.n_layers;
   const long rows = (long)B * T;
   const int f32 = c->f32, gf = c->gf32;
+  const int et = c->et(), gt = c->gt();  // element types passed to the non-GEMM launchers
   const long hs_layer = (long)(T + 1) * B * hp;
   const long c_layer = (long)T * B * hp;
   const long g_layer = (long)T * B * 4 * hp;
@@ -727,7 +737,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
       // dz (R9) was written by the forward's head_out; dwo, dfb, dbo in one fused column pass
       {
         KScope ks_(c, HDP_K_HEAD_BWD, 2, s);
-        CK_CUDA(hdp::launch_colreduce3(f32, S.Z, S.dz, Fp, (int)rows, (int)Fp, S.dy, c->crp, gf, c->G(si, iwo),
+        CK_CUDA(hdp::launch_colreduce3(et, S.Z, S.dz, Fp, (int)rows, (int)Fp, S.dy, c->crp, gt, c->G(si, iwo),
                                        c->G(si, ifb), c->G(si, ibo), s));
       }
       // dF = dz^T H   (M = Fp, N = hp, K = B*T; both operands MN-major)
@@ -738,28 +748,28 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
       const char* Hlast = S.Hs + ((L - 1) * hs_layer + (long)T * B * hp) * e;
       {
         KScope ks_(c, HDP_K_HEAD_BWD, 1, s);
-        CK_CUDA(hdp::launch_outer(f32, S.dy, c->W(iwo), c->dH[0], B, (int)hp, s));
+        CK_CUDA(hdp::launch_outer(et, S.dy, c->W(iwo), c->dH[0], B, (int)hp, s));
       }
       {
         KScope ks_(c, HDP_K_HEAD_BWD, 2, s);
-        CK_CUDA(hdp::launch_colreduce(f32, Hlast, hp, B, (int)hp, S.dy, c->crp, gf, c->G(si, iwo), s));
+        CK_CUDA(hdp::launch_colreduce(et, Hlast, hp, B, (int)hp, S.dy, c->crp, gt, c->G(si, iwo), s));
       }
       {
         KScope ks_(c, HDP_K_HEAD_BWD, 2, s);
-        CK_CUDA(hdp::launch_colreduce(1, S.dy, 1, B, 1, nullptr, c->crp, gf, c->G(si, ibo), s));
+        CK_CUDA(hdp::launch_colreduce(1, S.dy, 1, B, 1, nullptr, c->crp, gt, c->G(si, ibo), s));
       }
     } else {
       {
         KScope ks_(c, HDP_K_HEAD_BWD, 1, s);
-        CK_CUDA(hdp::launch_outer(f32, S.dy, c->W(iwo), c->dH[0], (int)rows, (int)hp, s));
+        CK_CUDA(hdp::launch_outer(et, S.dy, c->W(iwo), c->dH[0], (int)rows, (int)hp, s));
       }
       {
         KScope ks_(c, HDP_K_HEAD_BWD, 2, s);
-        CK_CUDA(hdp::launch_colreduce(f32, Htop, hp, (int)rows, (int)hp, S.dy, c->crp, gf, c->G(si, iwo), s));
+        CK_CUDA(hdp::launch_colreduce(et, Htop, hp, (int)rows, (int)hp, S.dy, c->crp, gt, c->G(si, iwo), s));
       }
       {
         KScope ks_(c, HDP_K_HEAD_BWD, 2, s);
-        CK_CUDA(hdp::launch_colreduce(1, S.dy, 1, (int)rows, 1, nullptr, c->crp, gf, c->G(si, ibo), s));
+        CK_CUDA(hdp::launch_colreduce(1, S.dy, 1, (int)rows, 1, nullptr, c->crp, gt, c->G(si, ibo), s));
       }
     }
     return HDP_OK;
@@ -858,7 +868,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
       // mixed mode: K6 of step T-1 alone, then K7(t) with K6(t-1) fused into its split-K reduction
       if (t == T - 1) {
         KScope ks_(c, HDP_K_CELL_BWD, 1, s);
-        CK_CUDA(hdp::launch_cell_bwd(f32, dHa_t, nullptr, Gl + (long)t * B * 4 * hp * e, Cl + (long)t * B * hp,
+        CK_CUDA(hdp::launch_cell_bwd(et, dHa_t, nullptr, Gl + (long)t * B * 4 * hp * e, Cl + (long)t * B * hp,
                                      t > 0 ? Cl + (long)(t - 1) * B * hp : nullptr, c->dc,
                                      c->dA + (long)t * B * 4 * hp * e, B, (int)hp, 1, s));
       }
@@ -899,7 +909,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
     // K6 (A6)
     {
       KScope ks_(c, HDP_K_CELL_BWD, 1, s);
-      CK_CUDA(hdp::launch_cell_bwd(f32, dHa_t, t < T - 1 ? c->dhrec : nullptr, Gl + (long)t * B * 4 * hp * e,
+      CK_CUDA(hdp::launch_cell_bwd(et, dHa_t, t < T - 1 ? c->dhrec : nullptr, Gl + (long)t * B * 4 * hp * e,
                                    Cl + (long)t * B * hp, t > 0 ? Cl + (long)(t - 1) * B * hp : nullptr, c->dc,
                                    c->dA + (long)t * B * 4 * hp * e, B, (int)hp, t == T - 1, s));
     }
@@ -913,7 +923,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
     CK(gemm(c, HDP_K_GEMM_DW, dAl, 4 * hp, 1, c->drop_on() ? c->Hst(si, l) : Hs, hp, 1, 4 * hp, hp, rows,
             epi_elem(gf, c->G(si, iU), hp), s));  // dU = sum_t dA_t^T h~_{t-1}
     KScope ks_(c, HDP_K_GEMM_DW, 2, s);
-    CK_CUDA(hdp::launch_colreduce(f32, dAl, 4 * hp, (int)rows, (int)(4 * hp), nullptr, c->crp, gf, c->G(si, ib), s));
+    CK_CUDA(hdp::launch_colreduce(et, dAl, 4 * hp, (int)rows, (int)(4 * hp), nullptr, c->crp, gt, c->G(si, ib), s));
   }
   if (l > 0 && !wave) {  // (the wavefront computed dX1 itself)
     // K9: dX = dA W  ->  dH_above of layer l-1 (W read MN-major as [K = 4hp][N = Ip])
@@ -925,7 +935,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
       KScope ks_(c, HDP_K_EMBED_BWD, 2, s);
       CK_CUDA(hdp::launch_embed_backward((const int32_t*)S.stage_x, B, T, d.vocab, dHnext, (int)c->Ip0, c->keys_in,
                                          c->keys_out, c->vals_in, c->vals_out, c->sort_temp, c->sort_bytes,
-                                         c->emb_part, c->G(si, iE), gf, c->emb_range, s));
+                                         c->emb_part, c->G(si, iE), gt, c->emb_range, s));
     }
   }
   return HDP_OK;
@@ -984,8 +994,8 @@ int nccl_async_check(hdp_ctx* c) {
   return HDP_OK;
 }
 
-ncclDataType_t gtype(const hdp_ctx* c) { return c->gf32 ? ncclFloat : ncclHalf; }
-ncclDataType_t wtype(const hdp_ctx* c) { return c->f32 ? ncclFloat : ncclHalf; }
+ncclDataType_t gtype(const hdp_ctx* c) { return c->gf32 ? ncclFloat : c->bf ? ncclBfloat16 : ncclHalf; }
+ncclDataType_t wtype(const hdp_ctx* c) { return c->f32 ? ncclFloat : c->bf ? ncclBfloat16 : ncclHalf; }
 
 void p2p_bucket_table(hdp_ctx* c) {
   hdp::P2PArgs& a = c->p2pa;
@@ -1202,7 +1212,7 @@ int hdp_configure(hdp_ctx* c, const hdp_model_desc* desc, hdp_sizes* out) {
   if (!c || !desc) return fail(HDP_ERR_ARG, "null argument");
   if (c->bound) return fail(HDP_ERR_STATE, "already bound");
   const hdp_model_desc& d = *desc;
-  if (d.n_layers < 0 || d.math < 0 || d.math > 1 || d.wire < 0 || d.wire > 2 || d.optimizer < 0 ||
+  if (d.n_layers < 0 || d.math < 0 || d.math > HDP_MATH_BF16 || d.wire < 0 || d.wire > 2 || d.optimizer < 0 ||
       d.optimizer > 1 || d.sim_workers < 1)
     return fail(HDP_ERR_ARG, "bad enum / layer count");
   if (d.sim_workers > 1 && c->world > 1) return fail(HDP_ERR_ARG, "sim_workers > 1 requires world == 1");
@@ -1224,6 +1234,7 @@ int hdp_configure(hdp_ctx* c, const hdp_model_desc* desc, hdp_sizes* out) {
   CK(check_desc_across_ranks(c, d));
   c->d = d;
   c->f32 = d.math == HDP_MATH_FP32;
+  c->bf = d.math == HDP_MATH_BF16;
   c->gf32 = c->f32 || d.wire == HDP_WIRE_FP32;
   c->esz = c->f32 ? 4 : 2;
   c->gsz = c->gf32 ? 4 : 2;
@@ -1347,7 +1358,14 @@ int hdp_load_params(hdp_ctx* c, const float* params, int root) {
     std::vector<float> full(c->P);
     CK_CUDA(cudaMemcpyAsync(full.data(), buf, c->P * 4, cudaMemcpyDeviceToHost, s));
     CK_CUDA(cudaStreamSynchronize(s));
-    for (long i = 0; i < c->P; ++i) h16[i] = __float2half_rn(full[i]);
+    if (c->bf) {
+      for (long i = 0; i < c->P; ++i) {
+        const __nv_bfloat16 b = __float2bfloat16_rn(full[i]);
+        memcpy(&h16[i], &b, 2);
+      }
+    } else {
+      for (long i = 0; i < c->P; ++i) h16[i] = __float2half_rn(full[i]);
+    }
     CK_CUDA(cudaMemcpyAsync(c->w, h16.data(), c->P * 2, cudaMemcpyHostToDevice, s));
   }
   CK_CUDA(cudaStreamSynchronize(s));
@@ -1384,6 +1402,7 @@ int hdp_gather_master(hdp_ctx* c, float* out) {
 
 namespace {
 int read_vec(hdp_ctx* c, const char* src, bool is_f32, float* out) {
+  const bool is_bf = !is_f32 && c->bf;  // 16-bit vectors of the bf16 mode
   CK_CUDA(cudaSetDevice(c->device));
   CK_CUDA(cudaDeviceSynchronize());
   std::vector<float> host(c->P);
@@ -1392,7 +1411,16 @@ int read_vec(hdp_ctx* c, const char* src, bool is_f32, float* out) {
   } else {
     std::vector<__half> h(c->P);
     CK_CUDA(cudaMemcpy(h.data(), src, c->P * 2, cudaMemcpyDeviceToHost));
-    for (long i = 0; i < c->P; ++i) host[i] = __half2float(h[i]);
+    if (is_bf) {
+      for (long i = 0; i < c->P; ++i) {
+        uint16_t b;
+        memcpy(&b, &h[i], 2);
+        const uint32_t u = (uint32_t)b << 16;
+        memcpy(&host[i], &u, 4);
+      }
+    } else {
+      for (long i = 0; i < c->P; ++i) host[i] = __half2float(h[i]);
+    }
   }
   dev_to_canon(c, host, out);
   return HDP_OK;
@@ -1438,7 +1466,8 @@ int hdp_set_recurrent_dropout(hdp_ctx* c, double keep, unsigned int seed) {
   if (!c) return fail(HDP_ERR_ARG, "null context");
   if (!(keep > 0.0 && keep <= 1.0)) return fail(HDP_ERR_ARG, "keep must be in (0, 1]");
   if (!c->bound) return fail(HDP_ERR_STATE, "context not bound");
-  if (keep < 1.0 && c->f32) return fail(HDP_ERR_UNSUPPORTED, "recurrent dropout is implemented for mixed mode only");
+  if (keep < 1.0 && (c->f32 || c->bf))
+    return fail(HDP_ERR_UNSUPPORTED, "recurrent dropout is implemented for the fp16 mixed mode only");
   if (keep < 1.0 && c->d.n_layers == 0) return fail(HDP_ERR_ARG, "no LSTM layers");
   CK_CUDA(cudaSetDevice(c->device));
   CK_CUDA(cudaDeviceSynchronize());
@@ -1629,7 +1658,7 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
     CK_CUDA(cudaMemsetAsync(st, 0, sizeof(int), cs));
     {
       KScope ks_(c, HDP_K_UPDATE, 1, cs);
-      CK_CUDA(hdp::launch_count_nonfinite(c->grads, (long)c->nslots * c->P, c->gf32, st, cs));
+      CK_CUDA(hdp::launch_count_nonfinite(c->grads, (long)c->nslots * c->P, c->gt(), st, cs));
     }
     if (c->world > 1) {
       KScope ks_(c, HDP_K_COMM, 0, cs);
@@ -1668,6 +1697,7 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
     p.c2 = a.c2;
     p.eps = a.eps;
     p.l2x2 = a.l2x2;
+    p.w_bf16 = c->bf ? 1 : 0;
     p.skip = a.skip;
     p.alpha_dev = a.alpha_dev;
     p.n_workers = a.n_workers;
@@ -1685,11 +1715,11 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
       p.seq = ++c->p2p_seq;
       const long vec = p.vpre[p.bk1] - p.vpre[p.bk0];
       // one wave of co-resident CTAs (register-limited occupancy), grid-striding over the vectors
-      const int grid = (int)std::max(1L, std::min((vec + 255) / 256, (long)hdp::exch_resident_ctas(p, opt, c->gf32)));
+      const int grid = (int)std::max(1L, std::min((vec + 255) / 256, (long)hdp::exch_resident_ctas(p, opt, c->gt())));
       c->p2p_ctr += (unsigned)grid;
       p.ctr_target = c->p2p_ctr;
       KScope ks_(c, HDP_K_UPDATE, 1, cs);
-      CK_CUDA(hdp::launch_exch_update(p, opt, c->gf32, grid, cs));
+      CK_CUDA(hdp::launch_exch_update(p, opt, c->gt(), grid, cs));
     }
     count_src = (const int*)(c->fwin + hdp::P2P_STATUS + (step & 1));
   } else {
@@ -1734,7 +1764,8 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
         a.S2 = c->s2 ? c->s2 + bk.moff : nullptr;
         a.w16 = c->f32 ? nullptr : (__half*)(c->w + (bk.off + (long)c->owner_index() * bk.shard) * 2);
         a.w32 = c->f32 ? (float*)(c->w + (bk.off + (long)c->owner_index() * bk.shard) * 4) : nullptr;
-        const int grad_f32 = c->gf32;
+        const int grad_f32 = c->gt();
+        a.w_bf16 = c->bf ? 1 : 0;
         if (c->world == 1) {
           a.g = c->grads + bk.off * c->gsz;  // slot r at + r*P
           a.g_stride = c->P;

@@ -9,6 +9,10 @@
 
 namespace hdp {
 
+// Element type of the working copy / activations / gradients, passed to the launchers
+// in their `f32` / `x_f32` / `out_f32` arguments (0 and 1 keep their round-1 meaning).
+enum ElemType { ET_F16 = 0, ET_F32 = 1, ET_BF16 = 2 };
+
 // ---------------------------------------------------------------- K11
 struct UpdateArgs {
   const void* g = nullptr;  // contribution r at g + r*g_stride (elements), rank order
@@ -18,7 +22,8 @@ struct UpdateArgs {
   float* W = nullptr;       // fp32 master shard
   float* S1 = nullptr;      // momentum H (SGD-m) or first moment (Adam)
   float* S2 = nullptr;      // second moment (Adam)
-  __half* w16 = nullptr;    // fp16 working copy (mixed mode), nullable
+  __half* w16 = nullptr;    // fp16 (or bf16, w_bf16) working copy (mixed modes), nullable
+  int w_bf16 = 0;           // 1: w16 holds bfloat16 (bf16 math mode)
   float* w32 = nullptr;     // fp32 working copy (FP32 mode), nullable
   float inv_scale = 1.f, lam = 0.f, mom = 0.f;
   float b1 = 0.9f, omb1 = 0.1f, b2 = 0.999f, omb2 = 0.001f, c1 = 1.f, c2 = 1.f, eps = 1e-8f;
@@ -33,6 +38,7 @@ struct UpdateArgs {
   double n_workers = 1.0;
   const int* skip = nullptr;
 };
+// grad_is_f32: element type of the contributions (ET_F16 / ET_F32 / ET_BF16)
 cudaError_t launch_avg_update(const UpdateArgs& a, int grad_is_f32, int optimizer, cudaStream_t s);
 // *count += number of Inf/NaN values in g[0..n) (fp16, or fp32 if g_f32)
 cudaError_t launch_count_nonfinite(const void* g, long n, int g_f32, int* count, cudaStream_t s);

@@ -9,7 +9,9 @@
 //   dh = dH_above + dh_rec;  dc += dh o (1 - tanh^2 c_t)
 //   dA = [dc g i(1-i), dc c_{t-1} f(1-f), dc i (1-g^2), dh tanh(c_t) o(1-o)]
 //   dc_{t-1} = dc f
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <type_traits>
 #include <utility>
 
 #include "dropout.cuh"
@@ -24,6 +26,8 @@ template <>
 __device__ __forceinline__ float ld<float>(const float* p, long i) { return p[i]; }
 template <>
 __device__ __forceinline__ float ld<__half>(const __half* p, long i) { return __half2float(p[i]); }
+template <>
+__device__ __forceinline__ float ld<__nv_bfloat16>(const __nv_bfloat16* p, long i) { return __bfloat162float(p[i]); }
 
 template <typename T>
 __device__ __forceinline__ T cvt(float v);
@@ -31,6 +35,15 @@ template <>
 __device__ __forceinline__ float cvt<float>(float v) { return v; }
 template <>
 __device__ __forceinline__ __half cvt<__half>(float v) { return __float2half_rn(v); }
+template <>
+__device__ __forceinline__ __nv_bfloat16 cvt<__nv_bfloat16>(float v) { return __float2bfloat16_rn(v); }
+
+// one R12 output element of element type `et` (ET_F16 / ET_F32 / ET_BF16)
+__device__ __forceinline__ void st_et(void* out, long i, float v, int et) {
+  if (et == ET_F32) reinterpret_cast<float*>(out)[i] = v;
+  else if (et == ET_BF16) reinterpret_cast<__nv_bfloat16*>(out)[i] = __float2bfloat16_rn(v);
+  else reinterpret_cast<__half*>(out)[i] = __float2half_rn(v);
+}
 
 __device__ __forceinline__ float sigmoidf_(float x) { return 1.f / (1.f + expf(-x)); }
 
@@ -50,6 +63,16 @@ __device__ __forceinline__ float4 ld4(const __half* p) {
   return make_float4(x.x, x.y, y.x, y.y);
 }
 __device__ __forceinline__ float4 ld4(const float* p) { return *reinterpret_cast<const float4*>(p); }
+__device__ __forceinline__ void st4(__nv_bfloat16* p, float a, float b, float c, float d) {
+  __align__(8) __nv_bfloat162 v[2] = {__floats2bfloat162_rn(a, b), __floats2bfloat162_rn(c, d)};
+  *reinterpret_cast<uint2*>(p) = *reinterpret_cast<const uint2*>(v);
+}
+__device__ __forceinline__ float4 ld4(const __nv_bfloat16* p) {
+  const uint2 u = *reinterpret_cast<const uint2*>(p);
+  const float2 x = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.x));
+  const float2 y = __bfloat1622float2(*reinterpret_cast<const __nv_bfloat162*>(&u.y));
+  return make_float4(x.x, x.y, y.x, y.y);
+}
 
 // ---------------------------------------------------------------- input
 template <typename XT, typename T>
@@ -170,7 +193,7 @@ __global__ void __launch_bounds__(HEAD_WARPS * 32)
   const int r = blockIdx.x * HEAD_WARPS + warp;
   float hinge = 0.f;
   // fp16 rows of <= 256 elements (multiple of 8): one 16-B vector per lane, kept for dz
-  const bool vec = sizeof(T) == 2 && (Kd & 7) == 0 && Kd <= 256 && (ldz & 7) == 0;
+  const bool vec = std::is_same<T, __half>::value && (Kd & 7) == 0 && Kd <= 256 && (ldz & 7) == 0;
   if (r < rows && vec) {
     float acc = 0.f;
     float zv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f}, wv[8] = {0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f, 0.f};
@@ -394,10 +417,7 @@ __global__ void colreduce3_pass2(const double* __restrict__ partials, int rs, in
   if (lane != 0) return;
   void* out = c < F ? dwo : c < 2 * F ? dfb : dbo;
   const int i = c < F ? c : c < 2 * F ? c - F : 0;
-  if (out_f32)
-    reinterpret_cast<float*>(out)[i] = (float)s;
-  else
-    reinterpret_cast<__half*>(out)[i] = __float2half_rn((float)s);  // R12
+  st_et(out, i, (float)s, out_f32);  // R12: fp32 value, one RNE
 }
 
 __global__ void colreduce_pass2(const double* __restrict__ partials, int rs, int cols, int out_f32, void* out) {
@@ -405,10 +425,7 @@ __global__ void colreduce_pass2(const double* __restrict__ partials, int rs, int
   if (c >= cols) return;
   const double s = warp_col_sum(partials, rs, cols, c, lane);
   if (lane != 0) return;
-  if (out_f32)
-    reinterpret_cast<float*>(out)[c] = (float)s;
-  else
-    reinterpret_cast<__half*>(out)[c] = __float2half_rn((float)s);  // R12: fp32 value, one RNE
+  st_et(out, c, (float)s, out_f32);  // R12: fp32 value, one RNE
 }
 
 // ---------------------------------------------------------------- embedding backward
@@ -620,11 +637,23 @@ __global__ void embed_segsum_kernel(const int32_t* __restrict__ first, const int
       for (int j = 0; j < m; ++j) a[j] += a[j + m];
     s = part[(long)lo * Ep + k] + a[0];
   }
-  if (out_f32)
-    reinterpret_cast<float*>(dE)[v * Ep + k] = s;
-  else
-    reinterpret_cast<__half*>(dE)[v * Ep + k] = __float2half_rn(s);  // R12
+  st_et(dE, v * Ep + k, s, out_f32);  // R12
 }
+
+// element-type dispatch of the launchers: et = ET_F16 (0), ET_F32 (1) or ET_BF16 (2)
+#define HDP_ET(et, T, ...)                                   \
+  do {                                                       \
+    if ((et) == ET_F32) {                                    \
+      using T = float;                                       \
+      __VA_ARGS__;                                           \
+    } else if ((et) == ET_BF16) {                            \
+      using T = __nv_bfloat16;                               \
+      __VA_ARGS__;                                           \
+    } else {                                                 \
+      using T = __half;                                      \
+      __VA_ARGS__;                                           \
+    }                                                        \
+  } while (0)
 
 inline int grid_for(long n, int threads, int cap = 148 * 16) {
   long b = (n + threads - 1) / threads;
@@ -639,14 +668,18 @@ cudaError_t launch_pack_input(const void* x, int x_f32, int B, int T, int I, int
                               cudaStream_t s) {
   const long n = (long)T * B * Ip;
   const int g = grid_for(n, 256);
-  const int esz = f32 ? 4 : 2;
+  const int esz = f32 == ET_F32 ? 4 : 2;
   if (I == Ip && x_f32 == f32 && (I * esz) % 16 == 0 && !(reinterpret_cast<uintptr_t>(x) & 15) &&
       !(reinterpret_cast<uintptr_t>(X0) & 15)) {
     const long threads = (long)T * B * 32;
     pack_rows_kernel<<<(int)((threads + 255) / 256), 256, 0, s>>>((const uint4*)x, B, T, I * esz / 16, (uint4*)X0);
     return cudaGetLastError();
   }
-  if (f32) {
+  if (f32 == ET_BF16) {
+    if (x_f32 != ET_BF16) return cudaErrorInvalidValue;
+    pack_input_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, s>>>((const __nv_bfloat16*)x, B, T, I, Ip,
+                                                                      (__nv_bfloat16*)X0);
+  } else if (f32) {
     if (x_f32) pack_input_kernel<float, float><<<g, 256, 0, s>>>((const float*)x, B, T, I, Ip, (float*)X0);
     else pack_input_kernel<__half, float><<<g, 256, 0, s>>>((const __half*)x, B, T, I, Ip, (float*)X0);
   } else {
@@ -674,8 +707,7 @@ cudaError_t launch_embed_gather(const int32_t* tok, int B, int T, const void* E,
                                 int vocab, int* bad, cudaStream_t s) {
   const long warps = (long)B * T;
   const int g = (int)((warps * 32 + 255) / 256);
-  if (f32) embed_gather_kernel<float><<<g, 256, 0, s>>>(tok, B, T, (const float*)E, Ep, (float*)X0, vocab, bad);
-  else embed_gather_kernel<__half><<<g, 256, 0, s>>>(tok, B, T, (const __half*)E, Ep, (__half*)X0, vocab, bad);
+  HDP_ET(f32, TT, (embed_gather_kernel<TT><<<g, 256, 0, s>>>(tok, B, T, (const TT*)E, Ep, (TT*)X0, vocab, bad)));
   return cudaGetLastError();
 }
 
@@ -683,8 +715,7 @@ cudaError_t launch_cell_fwd(int f32, const float* Gx_t, const float* Gh, const f
                             float* c_t, void* h_t, int B, int hp, cudaStream_t s) {
   const int n = B * hp;
   const int g = (n + 127) / 128;
-  if (f32) cell_fwd_kernel<float><<<g, 128, 0, s>>>(Gx_t, Gh, c_prev, (float*)gates_t, c_t, (float*)h_t, n);
-  else cell_fwd_kernel<__half><<<g, 128, 0, s>>>(Gx_t, Gh, c_prev, (__half*)gates_t, c_t, (__half*)h_t, n);
+  HDP_ET(f32, TT, (cell_fwd_kernel<TT><<<g, 128, 0, s>>>(Gx_t, Gh, c_prev, (TT*)gates_t, c_t, (TT*)h_t, n)));
   return cudaGetLastError();
 }
 
@@ -693,12 +724,8 @@ cudaError_t launch_cell_bwd(int f32, const float* dHa_t, const float* dh_rec, co
                             int first, cudaStream_t s) {
   const int n = B * hp;
   const int g = (n + 127) / 128;
-  if (f32)
-    cell_bwd_kernel<float><<<g, 128, 0, s>>>(dHa_t, dh_rec, (const float*)gates_t, c_t, c_prev, dc, (float*)dA_t,
-                                             n, first);
-  else
-    cell_bwd_kernel<__half><<<g, 128, 0, s>>>(dHa_t, dh_rec, (const __half*)gates_t, c_t, c_prev, dc,
-                                              (__half*)dA_t, n, first);
+  HDP_ET(f32, TT, (cell_bwd_kernel<TT><<<g, 128, 0, s>>>(dHa_t, dh_rec, (const TT*)gates_t, c_t, c_prev, dc,
+                                                         (TT*)dA_t, n, first)));
   return cudaGetLastError();
 }
 
@@ -708,14 +735,9 @@ cudaError_t launch_head_out(int f32, const void* Z, int rows, int Kd, long ldz, 
                             const int8_t* tgt, int tgt_mode, int B, int T, float alpha, float inv_terms, float* y,
                             float* dy, float* partials, cudaStream_t s, void* dz, const float* alpha_dev) {
   const int g = head_partials_count(rows);
-  if (f32)
-    head_out_kernel<float><<<g, HEAD_WARPS * 32, 0, s>>>((const float*)Z, rows, Kd, ldz, (const float*)wo,
-                                                        (const float*)bo, tgt, tgt_mode, B, T, alpha, inv_terms, y,
-                                                        dy, partials, (float*)dz, alpha_dev);
-  else
-    head_out_kernel<__half><<<g, HEAD_WARPS * 32, 0, s>>>((const __half*)Z, rows, Kd, ldz, (const __half*)wo,
-                                                         (const __half*)bo, tgt, tgt_mode, B, T, alpha, inv_terms,
-                                                         y, dy, partials, (__half*)dz, alpha_dev);
+  HDP_ET(f32, TT, (head_out_kernel<TT><<<g, HEAD_WARPS * 32, 0, s>>>((const TT*)Z, rows, Kd, ldz, (const TT*)wo,
+                                                                    (const TT*)bo, tgt, tgt_mode, B, T, alpha,
+                                                                    inv_terms, y, dy, partials, (TT*)dz, alpha_dev)));
   return cudaGetLastError();
 }
 
@@ -725,8 +747,7 @@ cudaError_t launch_loss_final(const float* partials, int n, float inv_terms, flo
 }
 
 cudaError_t launch_l2_loss(int f32, const void* w, long n, double* part, double l2, float* loss, cudaStream_t s) {
-  if (f32) sumsq_partial_kernel<float><<<L2_BLOCKS, 256, 0, s>>>((const float*)w, n, part);
-  else sumsq_partial_kernel<__half><<<L2_BLOCKS, 256, 0, s>>>((const __half*)w, n, part);
+  HDP_ET(f32, TT, (sumsq_partial_kernel<TT><<<L2_BLOCKS, 256, 0, s>>>((const TT*)w, n, part)));
   l2_loss_final_kernel<<<1, 32, 0, s>>>(part, L2_BLOCKS, l2, loss);
   return cudaGetLastError();
 }
@@ -735,15 +756,13 @@ size_t l2_partials_doubles() { return L2_BLOCKS; }
 cudaError_t launch_relu_dz(int f32, const float* dy, const void* wo, const void* Z, void* dz, int rows, int Fp,
                            cudaStream_t s) {
   const int g = grid_for((long)rows * Fp, 256);
-  if (f32) relu_dz_kernel<float><<<g, 256, 0, s>>>(dy, (const float*)wo, (const float*)Z, (float*)dz, rows, Fp);
-  else relu_dz_kernel<__half><<<g, 256, 0, s>>>(dy, (const __half*)wo, (const __half*)Z, (__half*)dz, rows, Fp);
+  HDP_ET(f32, TT, (relu_dz_kernel<TT><<<g, 256, 0, s>>>(dy, (const TT*)wo, (const TT*)Z, (TT*)dz, rows, Fp)));
   return cudaGetLastError();
 }
 
 cudaError_t launch_outer(int f32, const float* dy, const void* wo, float* dH, int rows, int hp, cudaStream_t s) {
   const int g = grid_for((long)rows * hp, 256);
-  if (f32) outer_kernel<float><<<g, 256, 0, s>>>(dy, (const float*)wo, dH, rows, hp);
-  else outer_kernel<__half><<<g, 256, 0, s>>>(dy, (const __half*)wo, dH, rows, hp);
+  HDP_ET(f32, TT, (outer_kernel<TT><<<g, 256, 0, s>>>(dy, (const TT*)wo, dH, rows, hp)));
   return cudaGetLastError();
 }
 
@@ -754,8 +773,7 @@ cudaError_t launch_colreduce(int x_f32, const void* X, long ldx, int rows, int c
   const int rs = cr_splits(rows);
   dim3 g1((cols + 31) / 32, rs);
   double* part = reinterpret_cast<double*>(partials);
-  if (x_f32) colreduce_pass1<float><<<g1, CR_WARPS * 32, 0, s>>>((const float*)X, ldx, rows, cols, w, rs, part);
-  else colreduce_pass1<__half><<<g1, CR_WARPS * 32, 0, s>>>((const __half*)X, ldx, rows, cols, w, rs, part);
+  HDP_ET(x_f32, TT, (colreduce_pass1<TT><<<g1, CR_WARPS * 32, 0, s>>>((const TT*)X, ldx, rows, cols, w, rs, part)));
   colreduce_pass2<<<(cols * 32 + 255) / 256, 256, 0, s>>>(part, rs, cols, out_f32, out);
   return cudaGetLastError();
 }
@@ -766,10 +784,8 @@ cudaError_t launch_colreduce3(int x_f32, const void* Z, const void* dz, long ld,
   const int cols = 2 * F + 1;
   dim3 g1((cols + 31) / 32, rs);
   double* part = reinterpret_cast<double*>(partials);
-  if (x_f32)
-    colreduce3_pass1<float><<<g1, CR_WARPS * 32, 0, s>>>((const float*)Z, (const float*)dz, ld, rows, F, dy, rs, part);
-  else
-    colreduce3_pass1<__half><<<g1, CR_WARPS * 32, 0, s>>>((const __half*)Z, (const __half*)dz, ld, rows, F, dy, rs, part);
+  HDP_ET(x_f32, TT, (colreduce3_pass1<TT><<<g1, CR_WARPS * 32, 0, s>>>((const TT*)Z, (const TT*)dz, ld, rows, F, dy,
+                                                                       rs, part)));
   colreduce3_pass2<<<(cols * 32 + 255) / 256, 256, 0, s>>>(part, rs, F, out_f32, dwo, dfb, dbo);
   return cudaGetLastError();
 }

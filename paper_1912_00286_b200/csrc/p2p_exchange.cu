@@ -21,6 +21,7 @@
 //      my gradients of those buckets.
 // Non-finite contribution counts are added into every rank's per-step counter.
 // Flags hold monotonically increasing launch numbers: no resets between steps.
+#include <cuda_bf16.h>
 #include <cuda_fp16.h>
 #include <cuda_runtime.h>
 
@@ -87,6 +88,22 @@ struct PV<__half> {
     const uint32_t w[4] = {r.u.x, r.u.y, r.u.z, r.u.w};
 #pragma unroll
     for (int i = 0; i < 4; ++i) nf += ((w[i] & 0x7C00u) == 0x7C00u) + ((w[i] & 0x7C000000u) == 0x7C000000u);
+  }
+};
+template <>
+struct PV<__nv_bfloat16> {  // bf16 wire (bf16 math mode): the upper halves of binary32 values
+  struct raw_t { uint4 u; };
+  __device__ static raw_t load(const void* base, long e) {
+    return {__ldcg(reinterpret_cast<const uint4*>(static_cast<const __nv_bfloat16*>(base) + e))};
+  }
+  __device__ static void cvt(const raw_t& r, float (&o)[8], int& nf) {
+    const uint32_t w[4] = {r.u.x, r.u.y, r.u.z, r.u.w};
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+      o[2 * i] = __uint_as_float(w[i] << 16);
+      o[2 * i + 1] = __uint_as_float(w[i] & 0xFFFF0000u);
+      nf += ((w[i] & 0x7F80u) == 0x7F80u) + ((w[i] & 0x7F800000u) == 0x7F800000u);
+    }
   }
 };
 template <>
@@ -206,8 +223,10 @@ __global__ void __launch_bounds__(256, NMAX <= 2 ? 4 : NMAX <= 4 ? 3 : 2) exch_u
 #pragma unroll
     for (int i = 0; i < 8; ++i) {
       s[i] = __fmul_rn(s[i], inv_scale);
-      // L2 (reading Q16): + fp32(2 l2) * fp16(W), the working weight of this step
-      if (EXT && a.l2x2 != 0.f) s[i] = __fadd_rn(s[i], __fmul_rn(a.l2x2, __half2float(__float2half_rn(w[i]))));
+      // L2 (reading Q16): + fp32(2 l2) * fp16(W) (bf16(W) in bf16 mode), the working weight of this step
+      if (EXT && a.l2x2 != 0.f)
+        s[i] = __fadd_rn(s[i], __fmul_rn(a.l2x2, a.w_bf16 ? __bfloat162float(__float2bfloat16_rn(w[i]))
+                                                            : __half2float(__float2half_rn(w[i]))));
     }
     if (OPT == 0) {
 #pragma unroll
@@ -233,10 +252,18 @@ __global__ void __launch_bounds__(256, NMAX <= 2 ? 4 : NMAX <= 4 ? 3 : 2) exch_u
     *reinterpret_cast<float4*>(a.W + m + 4) = make_float4(w[4], w[5], w[6], w[7]);
     *reinterpret_cast<float4*>(a.S1 + m) = make_float4(h[0], h[1], h[2], h[3]);
     *reinterpret_cast<float4*>(a.S1 + m + 4) = make_float4(h[4], h[5], h[6], h[7]);
-    __align__(16) __half2 o[4];
+    uint4 ov;
+    if (a.w_bf16) {
+      __align__(16) __nv_bfloat162 o[4];
 #pragma unroll
-    for (int i = 0; i < 4; ++i) o[i] = __halves2half2(__float2half_rn(w[2 * i]), __float2half_rn(w[2 * i + 1]));
-    const uint4 ov = *reinterpret_cast<const uint4*>(o);
+      for (int i = 0; i < 4; ++i) o[i] = __floats2bfloat162_rn(w[2 * i], w[2 * i + 1]);
+      ov = *reinterpret_cast<const uint4*>(o);
+    } else {
+      __align__(16) __half2 o[4];
+#pragma unroll
+      for (int i = 0; i < 4; ++i) o[i] = __halves2half2(__float2half_rn(w[2 * i]), __float2half_rn(w[2 * i + 1]));
+      ov = *reinterpret_cast<const uint4*>(o);
+    }
 #pragma unroll
     for (int r = 0; r < NMAX; ++r)
       if (r < N) __stcg(reinterpret_cast<uint4*>(a.w_peer[r] + e), ov);  // all-gather by peer stores
@@ -270,6 +297,7 @@ const void* exch_fn_n(int N) {
 const void* exch_fn(const P2PArgs& a, int optimizer, int grad_f32) {
   const bool ext = a.l2x2 != 0.f || a.alpha_dev || a.skip || a.quorum > 0 || a.straggler_mask;
 #define HDP_EXCH(GT, OPT) (ext ? exch_fn_n<GT, OPT, true>(a.N) : exch_fn_n<GT, OPT, false>(a.N))
+  if (grad_f32 == 2) return optimizer == 0 ? HDP_EXCH(__nv_bfloat16, 0) : HDP_EXCH(__nv_bfloat16, 1);
   if (grad_f32) return optimizer == 0 ? HDP_EXCH(float, 0) : HDP_EXCH(float, 1);
   return optimizer == 0 ? HDP_EXCH(__half, 0) : HDP_EXCH(__half, 1);
 #undef HDP_EXCH

@@ -39,6 +39,7 @@ struct P2PArgs {
   float inv_scale = 1.f, lam = 0.f, mom = 0.f;
   float b1 = 0.9f, omb1 = 0.1f, b2 = 0.999f, omb2 = 0.001f, c1 = 1.f, c2 = 1.f, eps = 1e-8f;
   float l2x2 = 0.f;  // fp32(2 * l2), see UpdateArgs
+  int w_bf16 = 0;    // the weight copies hold bfloat16 (bf16 math mode)
   const float* alpha_dev = nullptr;  // dynamic loss scaling, see UpdateArgs
   double n_workers = 1.0;
   const int* skip = nullptr;
@@ -52,7 +53,7 @@ struct P2PArgs {
   unsigned long long straggler_ns = 0;
 };
 
-// grad_f32: the wire carries fp32 gradients (HDP_WIRE_FP32) instead of fp16
+// grad_f32: element type on the wire: 0 fp16, 1 fp32 (HDP_WIRE_FP32), 2 bf16 (bf16 math mode)
 cudaError_t launch_exch_update(const P2PArgs& a, int optimizer, int grad_f32, int grid, cudaStream_t s);
 // CTAs of the launch's instantiation that are co-resident on the whole GPU (the grid cap)
 int exch_resident_ctas(const P2PArgs& a, int optimizer, int grad_f32);

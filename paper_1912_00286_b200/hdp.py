@@ -19,7 +19,7 @@ LIB_PATH = os.path.join(_HERE, "libhdp.so")
 
 HDP_OK, HDP_ERR_ARG, HDP_ERR_CUDA, HDP_ERR_NCCL, HDP_ERR_NONFINITE, HDP_ERR_STATE, HDP_ERR_UNSUPPORTED = \
     0, -1, -2, -3, -4, -5, -6
-MATH_FP32, MATH_MIXED16 = 0, 1
+MATH_FP32, MATH_MIXED16, MATH_BF16 = 0, 1, 2
 WIRE_FP16_A2A, WIRE_FP16_NCCLSUM, WIRE_FP32 = 0, 1, 2
 OPT_SGDM, OPT_ADAM = 0, 1
 EXCH_AUTO, EXCH_NCCL, EXCH_P2P, EXCH_TASK0 = 0, 1, 2, 3

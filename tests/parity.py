@@ -50,6 +50,12 @@ def kernel_options(**kw):
             hdp.set_option(None, k, hdp.KERNEL_OPTION_DEFAULTS[k])
 
 
+def _bf16_of(a):
+    """float32 values rounded to bfloat16 (RNE), via torch (test-side helper)."""
+    import torch
+    return torch.from_numpy(np.asarray(a, np.float32)).to(torch.bfloat16).float().numpy()
+
+
 def _copy_dev(dst, src_ptr: int, nbytes: int):
     """Device-to-device copy from a raw library pointer into a torch tensor."""
     import ctypes
@@ -64,19 +70,20 @@ def _copy_dev(dst, src_ptr: int, nbytes: int):
 
 def run_parity(cfg, global_batch: int, n_workers: int, steps: int, mixed: bool, lambda0=None, alpha=None,
                optimizer="sgdm", seed=synth.DATA_SEED, epochs=None, compare_grads=True, l2=0.0, dropout=None,
-               exchange=0, keep_state=False):
+               exchange=0, keep_state=False, bf16=False):
     """Returns a list of per-step records with GPU-vs-oracle errors.
     exchange: hdp.EXCH_* (EXCH_P2P at 1 GPU = the NVLink kernel's loopback).
-    keep_state: also return the GPU master / weights of every step (bit comparisons)."""
+    keep_state: also return the GPU master / weights of every step (bit comparisons).
+    bf16: the bf16 math mode (HDP_MATH_BF16, oracle mode "bf16"); inputs rounded to bf16."""
     import torch
 
     from paper_1912_00286_b200 import hdp
 
     alpha = cfg.alpha if alpha is None else alpha
     lambda0 = cfg.lambda0 if lambda0 is None else lambda0
-    mode = "mixed" if mixed else "fp32"
+    mode = "bf16" if bf16 else "mixed" if mixed else "fp32"
     B = global_batch // n_workers
-    desc = hdp.desc_from_config(cfg, B, hdp.MATH_MIXED16 if mixed else hdp.MATH_FP32,
+    desc = hdp.desc_from_config(cfg, B, hdp.MATH_BF16 if bf16 else hdp.MATH_MIXED16 if mixed else hdp.MATH_FP32,
                                 hdp.WIRE_FP16_A2A, hdp.OPT_SGDM if optimizer == "sgdm" else hdp.OPT_ADAM,
                                 sim_workers=n_workers, exchange=exchange)
     params = synth.init_params(cfg)
@@ -93,12 +100,15 @@ def run_parity(cfg, global_batch: int, n_workers: int, steps: int, mixed: bool, 
         for k in range(steps):
             epoch = (epochs[k] if epochs is not None else 0)
             x, t = synth.model_batch(cfg, global_batch, seed + k)
-            if not mixed and cfg.vocab == 0:
+            if (bf16 or not mixed) and cfg.vocab == 0:
                 x = x.astype(np.float32)
             xs, ts = [], []
             for r in range(n_workers):
                 sl = slice(r * B, (r + 1) * B)
-                xs.append(torch.from_numpy(np.ascontiguousarray(x[sl])).to(dev))
+                xt = torch.from_numpy(np.ascontiguousarray(x[sl]))
+                if bf16 and cfg.vocab == 0:
+                    xt = xt.to(torch.bfloat16)                       # R0: bf16 inputs
+                xs.append(xt.to(dev))
                 ts.append(torch.from_numpy(np.ascontiguousarray(t[sl])).to(dev))
             stream = torch.cuda.current_stream()
             for r in range(n_workers):
@@ -113,6 +123,9 @@ def run_parity(cfg, global_batch: int, n_workers: int, steps: int, mixed: bool, 
             gpu_w = hdp.read_weights(tr.ctx, n)
             lam = osched.rate_for_epoch(lambda0, n_workers, cfg.n_half, cfg.gamma, epoch, cfg.max_eff_lr)
             lam32 = float(np.float32(lam))
+            if bf16 and cfg.vocab == 0:
+                from oracle.bfloat16 import rbf16
+                x = rbf16(x)
             ref = ostep.train_step(cfg, master, state, x, t, n_workers, alpha, lam32, mode, optimizer,
                                    cfg.momentum, adam_k=k + 1, l2=l2,
                                    dropout=None if dropout is None else
@@ -127,7 +140,8 @@ def run_parity(cfg, global_batch: int, n_workers: int, steps: int, mixed: bool, 
                 "dmaster_err": block_errors(cfg, gpu_master.astype(np.float64) - params,
                                             ref["master"] - params),
                 "w_matches_master": bool(np.array_equal(
-                    gpu_w, gpu_master.astype(np.float16).astype(np.float32) if mixed else gpu_master)),
+                    gpu_w, _bf16_of(gpu_master) if bf16 else
+                    gpu_master.astype(np.float16).astype(np.float32) if mixed else gpu_master)),
             }
             if keep_state:
                 rec["gpu_master"], rec["gpu_w"] = gpu_master, gpu_w

@@ -132,6 +132,31 @@ def test_c2_recurrent_dropout_full_size_wavefront():
     assert abs(out[1][0]["loss_gpu"] - out[0][0]["loss_gpu"]) <= 1e-4
 
 
+# NEXT-3 bf16 math mode (reading Q29): the same rounding points with bfloat16; 8 significant
+# bits instead of fp16's 11 make every rounding ~8x coarser
+GRAD_BF16 = 5e-2
+
+
+@pytest.mark.parametrize("cfg_name,gb,nw,seq,steps", [("C1", 8, 2, None, 5), ("C2", 32, 1, 16, 3),
+                                                      ("C3", 16, 2, 12, 2), ("C4", 16, 2, 4, 2)])
+def test_bf16_math_mode(cfg_name, gb, nw, seq, steps):
+    """bf16 math mode against the oracle's "bf16" mode (bfloat16 rounding at R0-R12,
+    fp32 master): per-step GEMM path with bf16 tcgen05 operands and fused cell epilogues,
+    bf16 gradients through K11 (simulated workers)."""
+    cfg = synth.CONFIGS[cfg_name].with_(lambda0=0.05, n_half=1e9)
+    if seq:
+        cfg = cfg.with_(seq=seq)
+    recs = run_parity(cfg, gb, nw, steps=steps, mixed=True, bf16=True)
+    for r in recs:
+        assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"])), r
+        assert r["nonfinite_gpu"] == r["nonfinite_ref"] == 0
+        assert r["w_matches_master"]
+        for ge in r["grad_err"]:
+            assert _max(ge) <= GRAD_BF16, (r["step"], ge)
+    assert _max(recs[-1]["master_err"]) <= 2e-2
+    assert _max(recs[-1]["dmaster_err"]) <= 1e-1, recs[-1]["dmaster_err"]
+
+
 def test_c1_adam_fp32():
     cfg = synth.CONFIGS["C1"]
     recs = run_parity(cfg, synth.C1_GLOBAL_BATCH, synth.C1_SIM_WORKERS, steps=3, mixed=False, optimizer="adam",

@@ -253,6 +253,37 @@ def test_mixed_mode_rounding_points_are_fp16():
     assert np.max(np.abs(h16 - h32)) <= 2.0 ** -10 * max(np.max(np.abs(h32)), 1e-30)
 
 
+
+def test_bf16_mode_rounding_points_and_bound():
+    """bf16 mode (reading Q29): every 16-bit rounding point holds bfloat16 values (R4, R6,
+    R7, R10 via dA's effect on the gradients, R12), c stays fp32 (R5); one step's hidden
+    state is within 2^-8 relative of the fp32 policy (one bf16 rounding of h); and the
+    bf16 gradients approximate the fp64 ones to the bf16 precision scale."""
+    from oracle.bfloat16 import rbf16
+    cfg = TINY["fc"]
+    flat = rbf16(_params(cfg, 9))
+    x, t = _inputs(cfg, cfg.batch, 9)
+    x = rbf16(x)
+    P = lstm.unpack(cfg, flat)
+    L, y, cache = lstm.forward(cfg, P, x, t, 10.0, "bf16")
+    for Lc in cache["layers"]:
+        assert np.array_equal(Lc["H"], rbf16(Lc["H"]))
+        assert np.array_equal(Lc["gates"], rbf16(Lc["gates"]))
+        assert np.array_equal(Lc["C"], Lc["C"].astype(np.float32).astype(np.float64))
+    assert np.array_equal(cache["z"], rbf16(cache["z"]))
+    _, _, cm = lstm.forward(cfg, P, x, t, 10.0, "mixed")        # a different grid than fp16's
+    assert not np.array_equal(cache["layers"][0]["H"], cm["layers"][0]["H"])
+    G = lstm.backward(cfg, P, cache, 10.0, "bf16")
+    assert all(np.array_equal(v, rbf16(v)) for v in G.values())
+    Lf, yf, cf = lstm.forward(cfg, P, x, t, 10.0, "fp32")
+    hb, h32 = cache["layers"][0]["H"][0], cf["layers"][0]["H"][0]
+    assert np.max(np.abs(hb - h32)) <= 2.0 ** -8 * max(np.max(np.abs(h32)), 1e-30)
+    G64 = lstm.backward(cfg, P, cf, 10.0, "fp32")
+    for k in G:
+        scale = max(np.max(np.abs(G64[k])), 1e-30)
+        assert np.max(np.abs(G[k] - G64[k])) <= 0.1 * scale, k
+
+
 # ---------------------------------------------------------------- data-parallel step
 
 def test_n_workers_equal_single_worker_fp64():
