@@ -1,4 +1,3 @@
-T=r02g
-timeout -s KILL 2700 python -m pytest tests -m gpu -q -p no:cacheprovider --durations=30 > gpurun_out/${T}_gpu_tests.log 2>&1; echo exit=$? >> gpurun_out/${T}_gpu_tests.log
-timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/${T}_smoke.log 2>&1; echo exit=$? >> gpurun_out/${T}_smoke.log
-cp gpurun_out/parity_errors.jsonl gpurun_out/${T}_parity_errors.jsonl 2>/dev/null
+T=r02h
+timeout -s KILL 900 python -m pytest tests/test_gpu_parity.py -k "bf16" -q -p no:cacheprovider > gpurun_out/${T}_bf16.log 2>&1; echo exit=$? >> gpurun_out/${T}_bf16.log
+timeout -s KILL 900 compute-sanitizer --tool memcheck --print-limit 50 python tools/sanitize_small.py perstep > gpurun_out/${T}_memcheck_perstep.log 2>&1; echo exit=$? >> gpurun_out/${T}_memcheck_perstep.log
