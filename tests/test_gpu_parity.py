@@ -134,7 +134,7 @@ def test_c2_recurrent_dropout_full_size_wavefront():
 
 # NEXT-3 bf16 math mode (reading Q29): the same rounding points with bfloat16; 8 significant
 # bits instead of fp16's 11 make every rounding ~8x coarser
-GRAD_BF16 = 5e-2
+GRAD_BF16 = 3e-2   # observed <= 1.6e-2 (C2, B = 32, T = 16)
 
 
 @pytest.mark.parametrize("cfg_name,gb,nw,seq,steps", [("C1", 8, 2, None, 5), ("C2", 32, 1, 16, 3),
@@ -154,7 +154,11 @@ def test_bf16_math_mode(cfg_name, gb, nw, seq, steps):
         for ge in r["grad_err"]:
             assert _max(ge) <= GRAD_BF16, (r["step"], ge)
     assert _max(recs[-1]["master_err"]) <= 2e-2
-    assert _max(recs[-1]["dmaster_err"]) <= 1e-1, recs[-1]["dmaster_err"]
+    # the update of every matrix block; the bias-type blocks are sums that cancel (their
+    # bf16 gradients are checked above with the R-cond scale), so their plain update ratio
+    # is not a precision measure at these batch sizes
+    dm = {k: v for k, v in recs[-1]["dmaster_err"].items() if not (k.startswith("b") or k == "fb")}
+    assert _max(dm) <= 5e-2, dm
 
 
 def test_c1_adam_fp32():
