@@ -977,20 +977,33 @@ __device__ __forceinline__ void bwd_proj_role(const Bwd2Params& P, int grp) {
   if (warp == 2) ptx::tmem_dealloc(tbase, tcols);
 }
 
+// phase trace (option recur_trace): per-CTA entry / exit stamps and role after the [6][T][5]
+// per-step stamps -- where a launch's time goes outside the recurrence chains
+__device__ __forceinline__ void cta_stamp(const Bwd2Params& P, int slot, unsigned long long role) {
+  if (!P.trace || threadIdx.x != 0) return;
+  unsigned long long* b = P.trace + (size_t)6 * P.T * 5 + 3 * (blockIdx.y * gridDim.x + blockIdx.x);
+  b[slot] = ptx::globaltimer_ns();
+  b[2] = role;
+}
+
 template <int NC, int NKQ>
 __global__ void __launch_bounds__(128, 1)
     recur2_bwd_kernel(const __grid_constant__ Bwd2Params P) {
   const int T = P.T, B = P.B, hp = P.hp;
   if ((int)blockIdx.y >= 3 * P.nbg) {
+    cta_stamp(P, 0, 3);
     bwd_wgrad_role(P, (blockIdx.y - 3 * P.nbg) * gridDim.x + blockIdx.x);
+    cta_stamp(P, 1, 3);
     return;
   }
   const int role = blockIdx.y / P.nbg, grp = blockIdx.y % P.nbg;
+  cta_stamp(P, 0, role);  // 0 Q1, 1 X, 2 Q0, 3 W
   if (role == 1) {
     if (NKQ != 0)
       bwd_proj_role_ts<NC, (NKQ != 0 ? NKQ : 52)>(P, grp);
     else
       bwd_proj_role<NC>(P, grp);
+    cta_stamp(P, 1, 1);
     return;
   }
   const int qi = role == 0 ? 0 : 1;  // 0: layer 1 (Q1), 1: layer 0 (Q0)
@@ -1399,6 +1412,7 @@ __global__ void __launch_bounds__(128, 1)
   ptx::cluster_wait();
   ptx::tc_fence_after();
   if (warp == 2) ptx::tmem_dealloc(tbase, tcols);
+  cta_stamp(P, 1, role);
 }
 
 size_t bwd_cl_smem(int hp, int Bc) {

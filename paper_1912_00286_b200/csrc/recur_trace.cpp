@@ -125,6 +125,24 @@ void print_trace(TraceKind kind, const unsigned long long* h, int T, int l) {
                 names[role], ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, step / n,
                 (double)(h[((size_t)role * T + T - 2) * 5] - t00), (double)(h[((size_t)role * T) * 5 + 4] - t00));
       }
+      {  // per-CTA entry / exit per role, relative to Q1's first step
+        const unsigned long long* c = h + (size_t)6 * T * 5;
+        const char* rn[4] = {"Q1", "X", "Q0", "W"};
+        const unsigned long long t00 = h[(size_t)(T - 1) * 5];
+        for (int r = 0; r < 4; ++r) {
+          unsigned long long lo = ~0ull, hi = 0;
+          int n = 0;
+          for (int k = 0; k < 148; ++k) {
+            if (!c[3 * k] || c[3 * k + 2] != (unsigned long long)r) continue;
+            lo = c[3 * k] < lo ? c[3 * k] : lo;
+            hi = c[3 * k + 1] > hi ? c[3 * k + 1] : hi;
+            ++n;
+          }
+          if (n)
+            fprintf(stderr, "[hdp trace] bwd %s: %d CTAs, first entry %+.0f ns, last exit %+.0f ns (vs Q1 step T-1)\n",
+                    rn[r], n, (double)lo - (double)t00, (double)hi - (double)t00);
+        }
+      }
       break;
     }
     case TRACE_BWD_LAYER: {
