@@ -562,6 +562,7 @@ struct __align__(64) Bwd2Params {
   __half* gb[2];        // db1, db0
   unsigned* q0done;     // [nbg][32]: layer-0 steps published (x G CTAs)
   int Ip0, wtiles;
+  int wstages;          // W role TMA ring depth (2..4, as the launch's shared memory allows)
   unsigned long long* trace;  // debug: [Q1, Q0, X][T][5] stamps of CTA 0 / group 0, nullable
   CUtensorMap tmdAo[2];       // dA1 / dA0 rows [T*B][4hp], SWIZZLE_128B box (64, Bc): TMA stores from the push staging
   CUtensorMap tmDX;           // dX1 rows [T*B][hp] fp32, box (64, Bc): Q0's dH_above prefetch (TSQ)
@@ -581,10 +582,19 @@ struct __align__(64) Bwd2Params {
 //   mat 0: dU1 = sum dA1_t^T h1_{t-1}   mat 1: dW1 = sum dA1_t^T h0_t
 //   mat 2: dU0 = sum dA0_t^T h0_{t-1}   mat 3: dW0 = sum dA0_t^T x_t
 // plus db1 / db0 (= sum dA_t, an MMA against a block of ones) on the dU tiles.
-// Items = (t, 64-wide batch chunk) in descending t; 2-stage TMA pipeline:
-// thread 0 acquires the dA_t flags and loads, thread 32 issues the MMAs.
+// Items = (t, 64-wide batch chunk) in descending t; a TMA ring of P.wstages stages (as
+// deep as the launch's shared memory -- sized for the Q roles -- allows: the W role is a
+// throughput role whose item loads are latency-bound; with 2 stages it trailed the Q0
+// chain by ~90 us at C2 B = 128): thread 0 acquires the dA_t flags and loads, thread 32
+// issues the MMAs.
 constexpr int WG_STAGE = 2 * 8192 + 4 * 8192;  // A: 2 m-atoms x 64 b; B: up to 4 n-atoms x 64 b
-size_t wgrad_smem() { return 1024 + 2 * (size_t)WG_STAGE + 2048 + 256; }
+constexpr int WG_MAX_STAGES = 4;
+constexpr size_t WG_FIXED = 1024 + 2048 + 256;  // align slack, ones block, barriers
+size_t wgrad_smem() { return WG_FIXED + 2 * (size_t)WG_STAGE; }
+int wgrad_stages(size_t smem) {
+  const int n = (int)((smem - WG_FIXED) / WG_STAGE);
+  return n < 2 ? 2 : n > WG_MAX_STAGES ? WG_MAX_STAGES : n;
+}
 
 __device__ __forceinline__ void bwd_wgrad_role(const Bwd2Params& P, int tile) {
   extern __shared__ uint8_t smem_raw[];
@@ -598,12 +608,13 @@ __device__ __forceinline__ void bwd_wgrad_role(const Bwd2Params& P, int tile) {
   const int N = mat == 3 ? 16 * ((P.Ip0 + 15) / 16) : hp;
   const int natom = (N + 63) / 64;
   const bool withb = mat == 0 || mat == 2;
-  uint8_t* sones = smem + 2 * WG_STAGE;        // [16 rows][128 B] fp16 ones, K-major B operand (N = 16)
+  const int NS = P.wstages;
+  uint8_t* sones = smem + NS * WG_STAGE;       // [16 rows][128 B] fp16 ones, K-major B operand (N = 16)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sones + 2048);
-  uint64_t* full = bars;                       // [2]
-  uint64_t* empty = bars + 2;                  // [2]
-  uint64_t* done = bars + 4;
-  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 5);
+  uint64_t* full = bars;                       // [NS]
+  uint64_t* empty = bars + WG_MAX_STAGES;      // [NS]
+  uint64_t* done = bars + 2 * WG_MAX_STAGES;
+  uint32_t* tslot = reinterpret_cast<uint32_t*>(bars + 2 * WG_MAX_STAGES + 1);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const unsigned* flags = layer == 1 ? P.q1done : P.q0done;
   const int G = gridDim.x;
@@ -611,7 +622,7 @@ __device__ __forceinline__ void bwd_wgrad_role(const Bwd2Params& P, int tile) {
   const int nitems = T * nbc;
   if (threadIdx.x == 0) {
     ptx::tma_prefetch(&P.tmdA[ai]);
-    for (int i = 0; i < 2; ++i) {
+    for (int i = 0; i < NS; ++i) {
       ptx::mbar_init(full + i, 1);
       ptx::mbar_init(empty + i, 1);
     }
@@ -631,13 +642,13 @@ __device__ __forceinline__ void bwd_wgrad_role(const Bwd2Params& P, int tile) {
     const CUtensorMap* tb = mat == 3 ? &P.tmX0 : mat == 1 ? &P.tmHs[1] : &P.tmHt[mat == 0 ? 0 : 1];
     for (int it = 0; it < nitems; ++it) {
       const int t = T - 1 - it / nbc, bc = it % nbc;
-      const int s = it & 1;
+      const int s = it % NS;
       if (bc == 0) {
         const unsigned target = (unsigned)(G * (T - t));
         for (int g = 0; g < P.nbg; ++g) spin_until(flags + g * 32, target);
         fence_proxy_async();
       }
-      ptx::mbar_wait(empty + s, ((it >> 1) & 1) ^ 1);
+      ptx::mbar_wait(empty + s, ((it / NS) & 1) ^ 1);
       uint8_t* sa = smem + s * WG_STAGE;
       uint8_t* sb = sa + 2 * 8192;
       ptx::mbar_arrive_expect_tx(full + s, 2 * 8192 + natom * 8192);
@@ -653,8 +664,8 @@ __device__ __forceinline__ void bwd_wgrad_role(const Bwd2Params& P, int tile) {
     const uint32_t idesc = ptx::idesc_f16_f32(128, natom * 64, 1, 1);  // whole 64-wide MN atoms
     const uint32_t idb = ptx::idesc_f16_f32(128, 16, 1, 0);
     for (int it = 0; it < nitems; ++it) {
-      const int s = it & 1;
-      ptx::mbar_wait(full + s, (it >> 1) & 1);
+      const int s = it % NS;
+      ptx::mbar_wait(full + s, (it / NS) & 1);
       ptx::tc_fence_after();
       const uint32_t sa = ptx::smem_u32(smem + s * WG_STAGE), sb = sa + 2 * 8192;
       const int bc = it % nbc;
@@ -2414,6 +2425,7 @@ cudaError_t launch_recur2_bwd(const Recur2BwdArgs& a, cudaStream_t s) {
     P.gb[1] = a.gb[1];
     P.Ip0 = a.Ip0;
     P.wtiles = 4 * ((4 * a.hp + 127) / 128);
+    P.wstages = wgrad_stages(std::max(bwd_cl_smem(a.hp, Bc), wgrad_smem()));
   }
   P.trace = a.trace;
   {
