@@ -636,18 +636,33 @@ __device__ __forceinline__ void bwd_wgrad_role(const Bwd2Params& P, int tile) {
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tbase = *tslot;               // [0, N): weight grad; [256, 272): bias grad
-  if (threadIdx.x == 0) {
-    // ---- producer
+  if (warp == 0) {
+    // ---- producer (lane 0 issues; the whole warp polls the batch groups' dA_t flags)
     // dU: h~_{t-1} (Hst with recurrent dropout, else Hs); dW1: the unmasked h0_t; dW0: x_t
     const CUtensorMap* tb = mat == 3 ? &P.tmX0 : mat == 1 ? &P.tmHs[1] : &P.tmHt[mat == 0 ? 0 : 1];
+    // minimum over the batch groups of the published counts seen so far: a step whose
+    // target it already covers needs no poll.  (Round 1 acquired the nbg flags one after
+    // the other for every step: nbg sequential L2 round trips per step made this role the
+    // tail of the launch.)
+    unsigned minpub = 0;
     for (int it = 0; it < nitems; ++it) {
       const int t = T - 1 - it / nbc, bc = it % nbc;
       const int s = it % NS;
       if (bc == 0) {
         const unsigned target = (unsigned)(G * (T - t));
-        for (int g = 0; g < P.nbg; ++g) spin_until(flags + g * 32, target);
+        if (minpub < target) {
+          const uint64_t t0 = ptx::globaltimer_ns();
+          for (;;) {
+            const unsigned v = lane < P.nbg ? acquire_ld(flags + lane * 32) : 0xFFFFFFFFu;
+            minpub = __reduce_min_sync(0xffffffffu, v);
+            if (minpub >= target) break;
+            if (ptx::globaltimer_ns() - t0 > 10000000000ull) __trap();
+          }
+        }
+        __syncwarp();  // the lanes' acquires happen-before lane 0's TMA reads (memory ordering of the warp barrier)
         fence_proxy_async();
       }
+      if (lane != 0) continue;
       ptx::mbar_wait(empty + s, ((it / NS) & 1) ^ 1);
       uint8_t* sa = smem + s * WG_STAGE;
       uint8_t* sb = sa + 2 * 8192;
