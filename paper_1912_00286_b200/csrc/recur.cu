@@ -1571,6 +1571,13 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int T = P.T, B = P.B, Bc = P.Bc, hp = P.hp;
   const int role = blockIdx.y / P.nbg, grp = blockIdx.y % P.nbg;
+  // phase trace: per-CTA entry / exit stamps and role (0 R0, 1 P, 2 R1) after the step stamps
+  unsigned long long* ctas = (P.trace && threadIdx.x == 0)
+                                 ? P.trace + (size_t)6 * T * 5 + 3 * (blockIdx.y * gridDim.x + blockIdx.x) : nullptr;
+  if (ctas) {
+    ctas[0] = ptx::globaltimer_ns();
+    ctas[2] = (unsigned long long)role;
+  }
   const int nkb = (hp + 63) / 64;             // == cluster size
   const int nk16 = (hp + 15) / 16;
   const int nwarps = blockDim.x >> 5;
@@ -2034,6 +2041,7 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
   ptx::cluster_wait();
   ptx::tc_fence_after();
   if (warp == 2) ptx::tmem_dealloc(tbase, tcols);
+  if (ctas) ctas[1] = ptx::globaltimer_ns();
 }
 
 

@@ -43,6 +43,24 @@ void print_trace(TraceKind kind, const unsigned long long* h, int T, int l) {
           fprintf(stderr, "[hdp trace] wavefront R0 epilogue: acc load %.0f  act+stage %.0f  cell+stores %.0f ns\n",
                   q[0] / n, q[1] / n, q[2] / n);
       }
+      {  // per-CTA entry / exit per role, relative to R0's first step
+        const unsigned long long* c = h + (size_t)6 * T * 5;
+        const char* rn[3] = {"R0", "P", "R1"};
+        const unsigned long long t00 = h[0];
+        for (int r = 0; r < 3; ++r) {
+          unsigned long long lo = ~0ull, hi = 0;
+          int n = 0;
+          for (int k = 0; k < 148; ++k) {
+            if (!c[3 * k] || c[3 * k + 2] != (unsigned long long)r) continue;
+            lo = c[3 * k] < lo ? c[3 * k] : lo;
+            hi = c[3 * k + 1] > hi ? c[3 * k + 1] : hi;
+            ++n;
+          }
+          if (n)
+            fprintf(stderr, "[hdp trace] fwd %s: %d CTAs, first entry %+.0f ns, last exit %+.0f ns (vs R0 step 0)\n",
+                    rn[r], n, (double)lo - (double)t00, (double)hi - (double)t00);
+        }
+      }
       break;
     }
     case TRACE_FWD_LAYER: {
