@@ -833,6 +833,15 @@ __device__ __forceinline__ void bwd_proj_role_ts(const Bwd2Params& P, int grp) {
       if (ptx::elect_one_sync()) ptx::mma_commit(barM);
       __syncwarp();
     }
+    // publish dX1_{t+1} inside the MMA wait (the store thread issues no MMAs): step t+1's
+    // store group is the latest, so a full wait completes it -- one step of hand-off lag to
+    // the layer-0 chain instead of two
+    if (threadIdx.x == st_thr && t < T - 1) {
+      ptx::bulk_wait_group0();
+      fence_proxy_async();
+      release_add(xf, 1u);
+      if (P.trace && rank == 0 && grp == 0) P.trace[(size_t)4 * T * 5 + (t + 1) * 5 + 1] = ptx::globaltimer_ns();
+    }
     {
       ptx::mbar_wait_relaxed(barM, mph);
     }
@@ -860,18 +869,12 @@ __device__ __forceinline__ void bwd_proj_role_ts(const Bwd2Params& P, int grp) {
     __syncthreads();  // MMA reads of the ring slot done (barM), staging complete
     if (xtr) xtr[t * 5 + 3] = ptx::globaltimer_ns();
     if (threadIdx.x == st_thr) {
-      if (t < T - 2) {  // all but step t+1's group complete -> publish step t+2
-        ptx::bulk_wait_group1();
-        fence_proxy_async();
-        release_add(xf, 1u);
-        if (P.trace && rank == 0 && grp == 0) P.trace[(size_t)4 * T * 5 + (t + 2) * 5 + 1] = ptx::globaltimer_ns();
-      }
       ptx::tma_store_2d(&P.tmDXo, so, j0, t * B + col0);
       ptx::bulk_commit_group();
-      if (t == 0) {
+      if (t == 0) {  // step 0 (steps T-1 .. 1 were published in the MMA waits of steps T-2 .. 0)
         ptx::bulk_wait_group0();
         fence_proxy_async();
-        release_add(xf, T >= 2 ? 2u : 1u);
+        release_add(xf, 1u);
       }
     }
     // ring slot (t-2) % 3 = (t+1) % 3 was read by step t+1's MMAs (complete): prefetch ahead
@@ -1268,6 +1271,14 @@ __global__ void __launch_bounds__(128, 1)
           fence_proxy_async();
           release_add(P.q0done + grp * 32, 1u);
         }
+        // Q1 publishes dA1_{t+1} (for X, on the layer-0 chain's path) in the same window:
+        // step t+1's store group is the latest one, so a full wait completes it -- one step
+        // of hand-off lag instead of two
+        if (qi == 0 && threadIdx.x == st_thr) {
+          ptx::bulk_wait_group0();
+          fence_proxy_async();
+          release_add(P.q1done + grp * 32, 1u);
+        }
       } else if (lane == 0) {
         ptx::mbar_wait(fullA + p, fphase[p]);  // every peer's dA_{t+1} slice landed in sA[p]
         ptx::tc_fence_after();
@@ -1396,20 +1407,15 @@ __global__ void __launch_bounds__(128, 1)
       if (threadIdx.x == 64 && publish) release_add((qi == 0 ? P.q1done : P.q0done) + grp * 32, 1u);
     } else if (threadIdx.x == st_thr) {
       unsigned* pubf = (qi == 0 ? P.q1done : P.q0done) + grp * 32;
-      if (qi == 0 && publish && t < T - 2) {  // all but step t+1's store group complete -> publish step t+2
-                                              // (Q0: at the top of step t-1, see above)
-        ptx::bulk_wait_group1();
-        fence_proxy_async();
-        release_add(pubf, 1u);
-      }
+      // (Q1 publishes step t+1 inside step t's MMA wait, Q0 step t+2 -- see above)
       for (int kb = 0; kb < 4; ++kb)
         if (j0 * 4 + kb * 64 < fourhp) ptx::tma_store_2d(&P.tmdAo[qi], stg + kb * Bc * 128, j0 * 4 + kb * 64, t * B + col0);
       ptx::bulk_commit_group();
       if (t == 0) {
         ptx::bulk_wait_group0();
-        if (publish) {  // steps min(1, T-1) .. 0
+        if (publish) {  // Q1: step 0; Q0: steps min(1, T-1) .. 0
           fence_proxy_async();
-          release_add(pubf, T >= 2 ? 2u : 1u);
+          release_add(pubf, qi == 0 ? 1u : (T >= 2 ? 2u : 1u));
         }
       }
     }
