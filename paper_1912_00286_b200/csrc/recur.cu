@@ -1548,6 +1548,24 @@ __device__ __forceinline__ void tmem_load_rows(uint32_t taddr_quadrant_col, cons
 }
 
 
+// Same columns from the SWIZZLE_128B K-major SMEM copy a TMA load made of the rows (64-wide
+// K-blocks of `kbstride` bytes, 128-B rows, 16-B chunk c of row r at ((c ^ (r & 7)) << 4));
+// row r_local of the block, K elements (zero beyond the tensor: TMA out-of-bounds fill).
+__device__ __forceinline__ void tmem_load_rows_sw(uint32_t taddr_quadrant_col, const uint8_t* sbase, int r_local,
+                                                  int K, int kbstride) {
+  for (int c0 = 0; c0 < (K + 31) / 32 * 16; c0 += 16) {
+    uint32_t v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) {
+      const int kk = 2 * (c0 + j), kb = kk >> 6, w = kk & 63;
+      v[j] = *reinterpret_cast<const uint32_t*>(sbase + kb * kbstride + r_local * 128 +
+                                                ((((w >> 3) ^ (r_local & 7))) << 4) + (w & 7) * 2);
+    }
+    ptx::tmem_st16(taddr_quadrant_col + c0, v);
+  }
+  ptx::tmem_wait_st();
+}
+
 // Forward roles' per-step MMAs for issuing warp W of 4, K-steps known at compile time:
 // warp-uniform, fully unrolled, one elected lane issues (k = W, W+4, ... < NKS; both
 // M=128 halves of the 256-row A slice; accumulator (half, W)).
@@ -1649,11 +1667,27 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
   ptx::tc_fence_after();
   const uint32_t tbase = *tslot;
   const uint32_t tA = tbase + 256, tW0 = tbase + 256 + 2 * KCP;
-  if (TSA && cg == 0) {
-    // A slice rows into TMEM: warp (quarter, hf) owns gate rows hf*128 + 32*quarter + lane
-    const uint32_t tq = (static_cast<uint32_t>(quarter * 32) << 16);
-    tmem_load_rows(tA + tq + hf * KCP, P.Ag[role], grow, fourhp, hp, hp);
-    if (fx) tmem_load_rows(tW0 + tq + hf * 16, P.W0g, grow, fourhp, P.Ip0, P.Ip0);  // 16 columns per half
+  if (TSA) {
+    // A slice (and the fused W0 slice) by TMA into the otherwise unused sU / sW0 regions,
+    // then SMEM -> TMEM: warp (quarter, hf) owns gate rows hf*128 + 32*quarter + lane.
+    // (Round 1 gathered the rows from global memory with strided 2-byte loads: ~20 us of
+    // every forward launch before its first step.)
+    if (threadIdx.x == 0) {
+      ptx::mbar_arrive_expect_tx(barU, 2 * nkb * 16384 + (fx ? 32768 : 0));
+      for (int h2 = 0; h2 < 2; ++h2)
+        for (int kb = 0; kb < nkb; ++kb)
+          ptx::tma_load_2d(sU + (h2 * nkb + kb) * 16384, &P.tmA[role], barU, kb * 64, row0 + h2 * 128);
+      if (fx)
+        for (int h2 = 0; h2 < 2; ++h2) ptx::tma_load_2d(sW0 + h2 * 16384, &P.tmW0, barU, 0, row0 + h2 * 128);
+    }
+    ptx::mbar_wait(barU, 0);
+    if (cg == 0) {
+      const uint32_t tq = (static_cast<uint32_t>(quarter * 32) << 16);
+      const int rl = quarter * 32 + lane;
+      tmem_load_rows_sw(tA + tq + hf * KCP, sU + hf * nkb * 16384, rl, hp, 16384);
+      if (fx) tmem_load_rows_sw(tW0 + tq + hf * 16, sW0 + hf * 16384, rl, P.Ip0, 16384);  // 16 columns per half
+    }
+    ptx::fence_async_smem();  // generic reads of sU / sW0 before the async-proxy writes that reuse them
   }
   ptx::tc_fence_before();
   __syncthreads();
