@@ -577,11 +577,16 @@ struct __align__(64) Bwd2Params {
   float drop_scale;
 };
 
-// Weight-gradient role: one CTA per (matrix, 128-gate-row tile) accumulates over all
-// (t, b) in TMEM as the recurrence roles publish dA_t (A8 of the paper's step):
+// Weight-gradient role: one CTA per (matrix, 128-gate-row tile[, column half]) accumulates
+// over all (t, b) in TMEM as the recurrence roles publish dA_t (A8 of the paper's step):
 //   mat 0: dU1 = sum dA1_t^T h1_{t-1}   mat 1: dW1 = sum dA1_t^T h0_t
 //   mat 2: dU0 = sum dA0_t^T h0_{t-1}   mat 3: dW0 = sum dA0_t^T x_t
-// plus db1 / db0 (= sum dA_t, an MMA against a block of ones) on the dU tiles.
+// plus db1 / db0 (= sum dA_t, an MMA against a block of ones) on the dU tiles.  For
+// h_p > 128 each dU tile is split into two column halves (two CTAs), so the heaviest tiles
+// (N = h_p) keep pace with the layer-0 chain instead of trailing it (the trace showed the
+// dU0 tiles finishing ~30 us after Q0 at C2).
+__host__ __device__ inline int wg_usplit(int hp) { return hp > 128 ? 2 : 1; }
+__host__ __device__ inline int wg_tiles(int hp) { return (2 + 2 * wg_usplit(hp)) * ((4 * hp + 127) / 128); }
 // Items = (t, 64-wide batch chunk) in descending t; a TMA ring of P.wstages stages (as
 // deep as the launch's shared memory -- sized for the Q roles -- allows: the W role is a
 // throughput role whose item loads are latency-bound; with 2 stages it trailed the Q0
@@ -601,13 +606,20 @@ __device__ __forceinline__ void bwd_wgrad_role(const Bwd2Params& P, int tile) {
   uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   const int T = P.T, B = P.B, hp = P.hp, fourhp = 4 * hp;
   const int ntile = (fourhp + 127) / 128;
-  if (tile >= 4 * ntile) return;  // padding CTA of the last cluster
-  const int mat = tile / ntile, m0 = (tile % ntile) * 128;
+  if (tile >= wg_tiles(hp)) return;  // padding CTA of the last cluster
+  // job = (matrix, column half): dU1 halves, dW1, dU0 halves, dW0
+  const int us = wg_usplit(hp);
+  const int job = tile / ntile, m0 = (tile % ntile) * 128;
+  const int mat = job < us ? 0 : job == us ? 1 : job < 2 * us + 1 ? 2 : 3;
+  const int uhalf = mat == 0 ? job : mat == 2 ? job - us - 1 : 0;
   const int layer = mat < 2 ? 1 : 0;           // whose dA
   const int ai = mat < 2 ? 0 : 1;              // tmdA / tmHs index: [0] layer 1, [1] layer 0
-  const int N = mat == 3 ? 16 * ((P.Ip0 + 15) / 16) : hp;
+  const int nfull = mat == 3 ? 16 * ((P.Ip0 + 15) / 16) : hp;
+  const int ucols = (mat == 0 || mat == 2) && us == 2 ? 128 : nfull;  // column-half width
+  const int n0 = uhalf * ucols;                                        // first output column
+  const int N = (mat == 0 || mat == 2) ? min(ucols, hp - n0) : nfull;
   const int natom = (N + 63) / 64;
-  const bool withb = mat == 0 || mat == 2;
+  const bool withb = (mat == 0 || mat == 2) && uhalf == 0;
   const int NS = P.wstages;
   uint8_t* sones = smem + NS * WG_STAGE;       // [16 rows][128 B] fp16 ones, K-major B operand (N = 16)
   uint64_t* bars = reinterpret_cast<uint64_t*>(sones + 2048);
@@ -672,7 +684,7 @@ __device__ __forceinline__ void bwd_wgrad_role(const Bwd2Params& P, int tile) {
       ptx::tma_load_2d(sa + 8192, &P.tmdA[ai], full + s, m0 + 64, brow);
       // B rows: h_{t-1} = Hs slot t (dU), h0_t = Hs0 slot t+1 (dW1), x_t (dW0)
       const int hrow = mat == 1 ? (t + 1) * B + bc * 64 : mat == 3 ? brow : t * B + bc * 64;
-      for (int a = 0; a < natom; ++a) ptx::tma_load_2d(sb + a * 8192, tb, full + s, a * 64, hrow);
+      for (int a = 0; a < natom; ++a) ptx::tma_load_2d(sb + a * 8192, tb, full + s, n0 + a * 64, hrow);
     }
   } else if (threadIdx.x == 32) {
     // ---- MMA issuer
@@ -710,7 +722,7 @@ __device__ __forceinline__ void bwd_wgrad_role(const Bwd2Params& P, int tile) {
       const int ld = mat == 3 ? P.Ip0 : hp;
 #pragma unroll
       for (int q = 0; q < 16; ++q)
-        if (c + q < ld) gout[(size_t)row * ld + c + q] = __float2half_rn(v[q]);
+        if (c + q < N && n0 + c + q < ld) gout[(size_t)row * ld + n0 + c + q] = __float2half_rn(v[q]);
     }
   }
   if (withb) {
@@ -2361,8 +2373,7 @@ struct W2BPlan {
 };
 int wgrad_rows(int hp) {
   const int G = (hp + 63) / 64;
-  const int tiles = 4 * ((4 * hp + 127) / 128);
-  return (tiles + G - 1) / G;
+  return (wg_tiles(hp) + G - 1) / G;
 }
 bool plan_w2b(int B, int hp, bool want_wgrad, W2BPlan* out) {
   static std::map<std::tuple<int, int, bool>, W2BPlan> cache;
@@ -2487,7 +2498,7 @@ cudaError_t launch_recur2_bwd(const Recur2BwdArgs& a, cudaStream_t s) {
     P.gb[0] = a.gb[0];
     P.gb[1] = a.gb[1];
     P.Ip0 = a.Ip0;
-    P.wtiles = 4 * ((4 * a.hp + 127) / 128);
+    P.wtiles = wg_tiles(a.hp);
     P.wstages = wgrad_stages(std::max(bwd_cl_smem(a.hp, Bc), wgrad_smem()));
   }
   P.trace = a.trace;
