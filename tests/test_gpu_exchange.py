@@ -37,6 +37,8 @@ CASES = [
     ("C1", 8, 2, None, "sgdm", 0.05),
     ("C2", 64, 2, 16, "sgdm", 0.0),    # 2-layer wavefront kernels + FC head
     ("C3", 16, 2, 12, "sgdm", 0.0),    # embedding bucket
+    ("C3", 32, 8, 8, "sgdm", 0.0),     # C3 at N = 8 workers (SURVEY §8(c) parity plan), 8 weight copies
+    ("C2", 64, 4, 12, "sgdm", 0.0),    # 4 workers of B = 16: the wavefront kernels' smallest batch group
 ]
 
 
