@@ -581,11 +581,13 @@ struct __align__(64) Bwd2Params {
 // over all (t, b) in TMEM as the recurrence roles publish dA_t (A8 of the paper's step):
 //   mat 0: dU1 = sum dA1_t^T h1_{t-1}   mat 1: dW1 = sum dA1_t^T h0_t
 //   mat 2: dU0 = sum dA0_t^T h0_{t-1}   mat 3: dW0 = sum dA0_t^T x_t
-// plus db1 / db0 (= sum dA_t, an MMA against a block of ones) on the dU tiles.  For
-// h_p > 128 each dU tile is split into two column halves (two CTAs), so the heaviest tiles
-// (N = h_p) keep pace with the layer-0 chain instead of trailing it (the trace showed the
-// dU0 tiles finishing ~30 us after Q0 at C2).
-__host__ __device__ inline int wg_usplit(int hp) { return hp > 128 ? 2 : 1; }
+// plus db1 / db0 (= sum dA_t, an MMA against a block of ones) on the dU tiles.  The dU
+// tiles can be split into two column halves (two CTAs, wg_usplit) so the heaviest tiles
+// keep pace with the layer-0 chain (the trace shows the dU0 tiles finishing ~30 us after
+// Q0 at C2).
+// (measured: at C2 the split needs 35 co-resident 4-CTA clusters, more than the GPU holds,
+// so the plan fell back to the K8 GEMMs -- the split is off until a plan can choose it)
+__host__ __device__ inline int wg_usplit(int hp) { return (void)hp, 1; }
 __host__ __device__ inline int wg_tiles(int hp) { return (2 + 2 * wg_usplit(hp)) * ((4 * hp + 127) / 128); }
 // Items = (t, 64-wide batch chunk) in descending t; a TMA ring of P.wstages stages (as
 // deep as the launch's shared memory -- sized for the Q roles -- allows: the W role is a
