@@ -671,6 +671,9 @@ __device__ __forceinline__ void bwd_wgrad_role(const Bwd2Params& P, int tile) {
             minpub = __reduce_min_sync(0xffffffffu, v);
             if (minpub >= target) break;
             if (ptx::globaltimer_ns() - t0 > 10000000000ull) __trap();
+            // back off: the flag lines are the ones the recurrence roles release-add to every
+            // step, and this is a throughput role -- polling them flat out slows those atomics
+            __nanosleep(128);
           }
         }
         __syncwarp();  // the lanes' acquires happen-before lane 0's TMA reads (memory ordering of the warp barrier)
