@@ -340,6 +340,10 @@ def run_hdp(args, rank, world, local_rank):
                    "hidden": cfg.hidden, "layers": cfg.n_layers, "fc_hidden": cfg.fc_hidden,
                    "parallelism": f"dp{world}", "math": "fp16 (fp32 accumulate, fp32 master)",
                    "wire": "fp16", "exchange": exchange, "optimizer": "sgd-momentum", "loss_scale": cfg.alpha,
+                   "recurrence": ("two-layer wavefront launches (forward, backward)"
+                                  if cfg.n_layers == 2 and cfg.hidden <= 256 else
+                                  "per-step GEMMs with fused cell epilogues; layer-diagonal forward in chunks of "
+                                  f"{hdp.get_option('layer_pipe')} steps"),
                    "l2_cache": "flushed between timed steps (256 MiB memset, outside the events)",
                    "l2_regularisation": 0.0, "recurrent_dropout_keep": 1.0, "loss_scale_mode": "static"},
         "e2e": {"value": samples / (e2e_ms * 1e-3), "unit": "samples/s", "h2d_bytes_per_step": x_bytes + t_bytes,
@@ -603,6 +607,8 @@ def main():
     ap.add_argument("--batch", type=int, default=0, help="per-rank batch (default: the config's)")
     ap.add_argument("--impl", default="hdp", choices=["hdp", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--option", action="append", default=[],
+                    help="kernel switch name=value (hdp_set_option; ablations, default = the measured best)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -619,7 +625,14 @@ def main():
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local_rank}"))
+    if args.option:
+        from paper_1912_00286_b200 import hdp
+        for kv in args.option:
+            k, v = kv.split("=")
+            hdp.set_option(None, k, float(v))
     out = run_c5(args, rank, world, local_rank) if args.config == "C5" else run_hdp(args, rank, world, local_rank)
+    if args.option:
+        out["config"]["options"] = dict(kv.split("=") for kv in args.option)
     if rank == 0:
         if world == 1 and not args.no_cpu_baseline and args.config != "C5":
             out["cpu_baseline"] = cpu_baseline(args)

@@ -288,10 +288,14 @@ int hdp_grad_average_update(hdp_ctx* ctx, int epoch, void* stream, int* nonfinit
  * call are kept -- a ctx passed here has its graphs dropped): "persistent",
  *   "wavefront", "wavefront_fusex", "wavefront_wgrad", "wavefront_tmem", "recur_nbg",
  *   "gemm_cta_group", "gemm_cluster_n", "pdl", "k7_bn", "k7_splits",
- *   "recur_trace" (integers; see csrc/options.h).  They choose between implementations
+ *   "recur_trace", "layer_pipe", "head_fused" (integers; see csrc/options.h;
+ *   "head_fused" applies to contexts configured after the change).  They choose between implementations
  *   of the same arithmetic (ablations, tuning); the defaults are the measured best.
  * Errors: unknown name, value out of range -> HDP_ERR_ARG.                      */
 int hdp_set_option(hdp_ctx* ctx, const char* name, double value);
+/* Current value of a process-wide kernel switch (names as above).
+ * Errors: unknown name, null pointer -> HDP_ERR_ARG.                            */
+int hdp_get_option(const char* name, double* value);
 /* The last partial-collection decision (synchronises): bit r of *mask set if
  * contributor r's gradients were averaged; *count = their number.             */
 int hdp_partial_state(hdp_ctx* ctx, unsigned* mask, int* count);

@@ -20,7 +20,7 @@ ROOT = os.path.dirname(HERE)
 LIB = os.path.join(HERE, "libhdp.so")
 OBJ = os.path.join(HERE, "_obj")
 
-SOURCES = ["gemm.cu", "avg_update.cu", "lstm_kernels.cu", "recur.cu", "p2p_exchange.cu", "recur_trace.cpp",
+SOURCES = ["gemm.cu", "avg_update.cu", "lstm_kernels.cu", "recur.cu", "p2p_exchange.cu", "head.cu", "recur_trace.cpp",
            "hdp_api.cpp"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 

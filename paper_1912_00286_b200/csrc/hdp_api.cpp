@@ -25,6 +25,7 @@
 
 #include "gemm.cuh"
 #include "kernels.cuh"
+#include "head.cuh"
 #include "recur.cuh"
 #include "p2p_exchange.cuh"
 #include "options.h"
@@ -104,6 +105,7 @@ struct hdp_ctx {
   bool f32 = false;       // FP32 math mode
   bool bf = false;        // bf16 math mode (NEXT-3): bfloat16 in place of fp16 at every rounding point
   bool gf32 = false;      // fp32 gradients / wire
+  bool head_fused = false;  // FC head as one fused kernel (hdp::launch_head_fused), fixed at configure
   int nslots = 1;
   long hp = 0, Ip0 = 0, Fp = 0, esz = 2, gsz = 2;
   std::vector<long> Ip;   // per layer padded input width
@@ -132,6 +134,8 @@ struct hdp_ctx {
     float* dy;
     float* loss;
     float* partials;
+    float* dHh;        // fused head: dH_top = dz F [rows][hp] fp32 (written by the forward)
+    unsigned* ticket;  // fused head: last-CTA counter
   };
   std::vector<Slot> slot;
   float *Gx = nullptr, *Gh = nullptr, *dH[2] = {nullptr, nullptr}, *dhrec = nullptr, *dc = nullptr;
@@ -171,6 +175,10 @@ struct hdp_ctx {
   cudaStream_t cap = nullptr, comm_stream = nullptr;
   cudaEvent_t ev_done = nullptr, ev_count = nullptr;
   std::vector<cudaEvent_t> ev_bucket;
+  // layer-diagonal forward schedule (option layer_pipe): one stream + one chunk event per layer
+  std::vector<cudaStream_t> lstr;
+  std::vector<cudaEvent_t> ev_layer;
+  cudaEvent_t ev_fork = nullptr;
   int* count_host = nullptr;  // pinned [0] non-finite count, [1] out-of-range token ids
   bool count_pending = false;
   std::map<GraphKey, cudaGraphExec_t> graphs;
@@ -388,12 +396,18 @@ void carve(hdp_ctx* c, char* base) {
       S.Hs = cv.take(L * (T + 1) * B * hp * e);
       S.C = (float*)cv.take(L * T * B * hp * 4);
       S.gates = cv.take(L * T * B * 4 * hp * e);
-      S.Z = cv.take(c->Fp ? rows * c->Fp * e : 0);
+      // (the fused head keeps its per-CTA column partials here: grid x (2 Fp + 1) doubles)
+      S.Z = cv.take(c->Fp ? std::max(rows * c->Fp * e,
+                                     c->head_fused ? (long)hdp::head_fused_grid((int)rows) * (2 * c->Fp + 1) * 8 : 0L)
+                          : 0);
       S.dz = cv.take(c->Fp ? rows * c->Fp * e : 0);  // A5's ReLU' output, written by the forward's head_out
       S.y = (float*)cv.take(rows * 4);
       S.dy = (float*)cv.take(rows * 4);
       S.loss = (float*)cv.take(4);
       S.partials = (float*)cv.take(hdp::head_partials_count((int)rows) * 4);
+      // fused head: dH_top per slot (the backward of this slot reads it)
+      S.dHh = (float*)cv.take(c->head_fused ? rows * hp * 4 : 0);
+      S.ticket = (unsigned*)cv.take(c->head_fused ? 4 : 0);
     }
     c->Gx = (float*)cv.take(rows * 4 * hp * 4);
     c->Gh = (float*)cv.take(B * 4 * hp * 4);
@@ -491,7 +505,8 @@ int trace_report(hdp_ctx* c, hdp::TraceKind kind, const unsigned long long* dev,
 
 // ---------------------------------------------------------------- GEMM helper
 int gemm(hdp_ctx* c, int tag, const void* A, long lda, int amn, const void* B, long ldb, int bmn, long M, long N,
-         long K, const hdp::Epilogue& epi, cudaStream_t s, int force_bn = 0, int force_splits = 0) {
+         long K, const hdp::Epilogue& epi, cudaStream_t s, int force_bn = 0, int force_splits = 0,
+         float* ws = nullptr /* split-K scratch; nullptr = the context's */) {
   hdp::GemmPlan p;
   int r;
   hdp::Epilogue ebf = epi;
@@ -500,7 +515,7 @@ int gemm(hdp_ctx* c, int tag, const void* A, long lda, int amn, const void* B, l
     r = hdp::gemm_plan_f32(&p, (const float*)A, lda, amn, (const float*)B, ldb, bmn, (int)M, (int)N, (int)K, epi);
   else
     r = hdp::gemm_plan_tc(&p, (const __half*)A, lda, amn, (const __half*)B, ldb, bmn, (int)M, (int)N, (int)K, ebf,
-                          c->ws, c->ws_floats, force_bn, force_splits);
+                          ws ? ws : c->ws, c->ws_floats, force_bn, force_splits);
   if (r) return fail(HDP_ERR_ARG, "gemm plan %ldx%ldx%ld: %s", M, N, K, hdp::gemm_last_error());
   KScope ks(c, tag, p.tc && (p.splits > 1 || epi.mode == hdp::EPI_LSTM_BWD) ? 2 : 1, s);
   CK_CUDA(hdp::gemm_run(p, s));
@@ -526,6 +541,67 @@ hdp::Epilogue epi_elem(bool f32, void* out, long ldo) {
 }
 
 // ---------------------------------------------------------------- forward
+// A2 + A3 of layer l for t in [t0, t1): K2 with the cell in its epilogue (K3 alone at t = 0
+// and in FP32 mode), reading the input projection from Gxb; split-K scratch wsb (nullable:
+// the context's).  The per-step path of hdp_lstm_forward, whole or one time chunk at a time.
+int fwd_steps(hdp_ctx* c, int si, int B, int T, int l, int t0, int t1, float* Gxb, cudaStream_t s, float* wsb) {
+  const hdp_model_desc& d = c->d;
+  hdp_ctx::Slot& S = c->slot[si];
+  const long hp = c->hp, e = c->esz;
+  const int f32 = c->f32;
+  const int et = c->et();
+  const long hs_layer = (long)(T + 1) * B * hp, c_layer = (long)T * B * hp, g_layer = (long)T * B * 4 * hp;
+  (void)d;
+  char nm[16];
+  snprintf(nm, sizeof nm, "U%d", l);
+  const int iU = c->find(nm);
+  char* Hs = S.Hs + l * hs_layer * e;
+  float* Cl = S.C + l * c_layer;
+  char* Gl = S.gates + l * g_layer * e;
+for (int t = t0; t < t1; ++t) {
+    if (t > 0 && !f32) {
+      // K2 with A3 in its epilogue: gates = h_{t-1} U^T + G_x[t] -> cell -> gates, c_t, h_t
+      // (recurrent dropout: the GEMM reads h~_{t-1}, the epilogue also writes h~_t)
+      hdp::Epilogue ef;
+      const char* hin = c->drop_on() ? c->Hst(si, l) : Hs;
+      if (c->drop_on()) {
+        ef.htout = c->Hst(si, l) + (long)(t + 1) * B * hp * e;
+        ef.drop_step = c->drop_step();
+        ef.drop_seed = c->drop_seed;
+        ef.drop_thr = c->drop_thr;
+        ef.drop_layer = (uint32_t)l;
+        ef.drop_seq0 = (uint32_t)((c->rank * c->nslots + si) * B);
+        ef.drop_scale = c->drop_scale;
+      }
+      ef.mode = hdp::EPI_LSTM_FWD;
+      ef.hp = (int)hp;
+      ef.gx = Gxb + (long)t * B * 4 * hp;
+      ef.cprev = Cl + (long)(t - 1) * B * hp;
+      ef.cout = Cl + (long)t * B * hp;
+      ef.gates = Gl + (long)t * B * 4 * hp * e;
+      ef.hout = Hs + (long)(t + 1) * B * hp * e;
+      CK(gemm(c, HDP_K_GEMM_H, hin + (long)t * B * hp * e, hp, 0, c->W(iU), hp, 0, B, 4 * hp, hp, ef, s, 0, 0, wsb));
+      continue;
+    }
+    if (t > 0)  // K2: G_h = h_{t-1} U^T (A2)
+      CK(gemm(c, HDP_K_GEMM_H, Hs + (long)t * B * hp * e, hp, 0, c->W(iU), hp, 0, B, 4 * hp, hp, epi_f32(c->Gh, 4 * hp), s, 0, 0, wsb));
+    // K3 (A3)
+    {
+      KScope ks_(c, HDP_K_CELL_FWD, 1, s);
+      CK_CUDA(hdp::launch_cell_fwd(et, Gxb + (long)t * B * 4 * hp, t > 0 ? c->Gh : nullptr,
+                                   t > 0 ? Cl + (long)(t - 1) * B * hp : nullptr, Gl + (long)t * B * 4 * hp * e,
+                                   Cl + (long)t * B * hp, Hs + (long)(t + 1) * B * hp * e, B, (int)hp, s));
+    }
+    if (c->drop_on()) {  // h~_0 (the fused epilogues write the later ones)
+      KScope ks_(c, HDP_K_CELL_FWD, 1, s);
+      CK_CUDA(hdp::launch_drop_mask(Hs + (long)(t + 1) * B * hp * e, c->Hst(si, l) + (long)(t + 1) * B * hp * e, B,
+                                    (int)hp, c->drop_step(), c->drop_seed, (uint32_t)l,
+                                    (uint32_t)((c->rank * c->nslots + si) * B), c->drop_thr, c->drop_scale, s));
+    }
+  }
+  return HDP_OK;
+}
+
 int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
   const hdp_model_desc& d = c->d;
   hdp_ctx::Slot& S = c->slot[si];
@@ -549,7 +625,41 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
       CK_CUDA(hdp::launch_pack_input(S.stage_x, et, B, T, d.input_dim, (int)c->Ip0, S.X0, et, s));
     }
   char nm[16];
+  // Layer-diagonal schedule of the per-step path (NEXT-1 at C4 scale; PAPER.md:82 BPTT over a
+  // stacked LSTM): layer l's chunk of Tc steps needs only layer l-1's h over the same chunk,
+  // so the L layers run as a pipeline on L streams -- layer l's K1 over the chunk's rows, then
+  // its K2 + A3 steps -- and up to L per-step GEMMs (one per layer, different U) are in
+  // flight at once instead of one (measured: two concurrent K2 chains 15.8 -> 12.6 us per GEMM,
+  // tools/concurrent_gemm.py).  Same kernels, same per-element arithmetic as the sequential
+  // loop.  G_x is shared: rows of chunk c are rewritten by layer l+1's K1 only after layer l
+  // finished chunk c (its event), so one T x B x 4h_p buffer serves every layer.
+  const int tc = hdp::opt(hdp::OPT_LAYER_PIPE);
+  const bool any_fused = (L == 2 && !f32 && c->wave_ok() && hdp::recur2_fwd_supported(B, (int)hp)) ||
+                         (!f32 && c->recur_ok() && hdp::recur_fwd_supported(B, (int)hp));
+  if (tc > 0 && L >= 2 && !f32 && !any_fused && (int)c->lstr.size() >= L) {
+    CK_CUDA(cudaEventRecord(c->ev_fork, s));
+    for (int l = 0; l < L; ++l) CK_CUDA(cudaStreamWaitEvent(c->lstr[l], c->ev_fork, 0));
+    for (int t0 = 0; t0 < T; t0 += tc) {
+      const int t1 = t0 + tc < T ? t0 + tc : T;
+      for (int l = 0; l < L; ++l) {
+        cudaStream_t ls = c->lstr[l];
+        if (l > 0) CK_CUDA(cudaStreamWaitEvent(ls, c->ev_layer[l - 1], 0));
+        snprintf(nm, sizeof nm, "W%d", l);
+        const int iW = c->find(nm);
+        snprintf(nm, sizeof nm, "b%d", l);
+        const int ib = c->find(nm);
+        const long Ipl = c->Ip[l];
+        const char* X = l == 0 ? S.X0 : S.Hs + ((l - 1) * hs_layer + (long)B * hp) * e;
+        CK(gemm(c, HDP_K_GEMM_X, X + (long)t0 * B * Ipl * e, Ipl, 0, c->W(iW), Ipl, 0, (long)(t1 - t0) * B, 4 * hp,
+                Ipl, epi_f32(c->Gx + (long)t0 * B * 4 * hp, 4 * hp, c->W(ib), 1), ls));
+        CK(fwd_steps(c, si, B, T, l, t0, t1, c->Gx, ls, nullptr));
+        CK_CUDA(cudaEventRecord(c->ev_layer[l], ls));
+      }
+    }
+    for (int l = 0; l < L; ++l) CK_CUDA(cudaStreamWaitEvent(s, c->ev_layer[l], 0));
+  }
   for (int l = 0; l < L; ++l) {
+    if (tc > 0 && L >= 2 && !f32 && !any_fused && (int)c->lstr.size() >= L) break;  // done above
     snprintf(nm, sizeof nm, "W%d", l);
     const int iW = c->find(nm);
     snprintf(nm, sizeof nm, "U%d", l);
@@ -627,52 +737,43 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
       if (ra.trace) CK(trace_report(c, hdp::TRACE_FWD_LAYER, ra.trace, T, l, s));
       continue;
     }
-    for (int t = 0; t < T; ++t) {
-      if (t > 0 && !f32) {
-        // K2 with A3 in its epilogue: gates = h_{t-1} U^T + G_x[t] -> cell -> gates, c_t, h_t
-        // (recurrent dropout: the GEMM reads h~_{t-1}, the epilogue also writes h~_t)
-        hdp::Epilogue ef;
-        const char* hin = c->drop_on() ? c->Hst(si, l) : Hs;
-        if (c->drop_on()) {
-          ef.htout = c->Hst(si, l) + (long)(t + 1) * B * hp * e;
-          ef.drop_step = c->drop_step();
-          ef.drop_seed = c->drop_seed;
-          ef.drop_thr = c->drop_thr;
-          ef.drop_layer = (uint32_t)l;
-          ef.drop_seq0 = (uint32_t)((c->rank * c->nslots + si) * B);
-          ef.drop_scale = c->drop_scale;
-        }
-        ef.mode = hdp::EPI_LSTM_FWD;
-        ef.hp = (int)hp;
-        ef.gx = c->Gx + (long)t * B * 4 * hp;
-        ef.cprev = Cl + (long)(t - 1) * B * hp;
-        ef.cout = Cl + (long)t * B * hp;
-        ef.gates = Gl + (long)t * B * 4 * hp * e;
-        ef.hout = Hs + (long)(t + 1) * B * hp * e;
-        CK(gemm(c, HDP_K_GEMM_H, hin + (long)t * B * hp * e, hp, 0, c->W(iU), hp, 0, B, 4 * hp, hp, ef, s));
-        continue;
-      }
-      if (t > 0)  // K2: G_h = h_{t-1} U^T (A2)
-        CK(gemm(c, HDP_K_GEMM_H, Hs + (long)t * B * hp * e, hp, 0, c->W(iU), hp, 0, B, 4 * hp, hp, epi_f32(c->Gh, 4 * hp), s));
-      // K3 (A3)
-      {
-        KScope ks_(c, HDP_K_CELL_FWD, 1, s);
-        CK_CUDA(hdp::launch_cell_fwd(et, c->Gx + (long)t * B * 4 * hp, t > 0 ? c->Gh : nullptr,
-                                     t > 0 ? Cl + (long)(t - 1) * B * hp : nullptr, Gl + (long)t * B * 4 * hp * e,
-                                     Cl + (long)t * B * hp, Hs + (long)(t + 1) * B * hp * e, B, (int)hp, s));
-      }
-      if (c->drop_on()) {  // h~_0 (the fused epilogues write the later ones)
-        KScope ks_(c, HDP_K_CELL_FWD, 1, s);
-        CK_CUDA(hdp::launch_drop_mask(Hs + (long)(t + 1) * B * hp * e, c->Hst(si, l) + (long)(t + 1) * B * hp * e, B,
-                                      (int)hp, c->drop_step(), c->drop_seed, (uint32_t)l,
-                                      (uint32_t)((c->rank * c->nslots + si) * B), c->drop_thr, c->drop_scale, s));
-      }
-    }
+    CK(fwd_steps(c, si, B, T, l, 0, T, c->Gx, s, nullptr));
   }
   // head (A4)
   const char* Htop = S.Hs + ((L - 1) * hs_layer + (long)B * hp) * e;
   const int iwo = c->find("wo"), ibo = c->find("bo");
-  if (d.fc_hidden > 0) {
+  if (d.fc_hidden > 0 && c->head_fused) {
+    // A4 + A5 (but dF) in one launch: z, y, loss, dy, dz, dH_top and the head's column partials
+    hdp::HeadFusedArgs ha;
+    ha.H = Htop;
+    ha.F = c->W(c->find("F"));
+    ha.fb = c->W(c->find("fb"));
+    ha.wo = c->W(iwo);
+    ha.bo = c->W(ibo);
+    ha.tgt = S.stage_t;
+    ha.dz = S.dz;
+    ha.y = S.y;
+    ha.dy = S.dy;
+    ha.hinge = S.partials;
+    ha.colpart = reinterpret_cast<double*>(S.Z);
+    ha.loss = S.loss;
+    ha.ticket = S.ticket;
+    ha.dH = S.dHh;
+    ha.rows = (int)rows;
+    ha.B = B;
+    ha.T = T;
+    ha.hp = (int)hp;
+    ha.Fp = (int)c->Fp;
+    ha.alpha = c->alpha;
+    ha.inv_terms = 1.f / (float)rows;
+    ha.alpha_dev = c->dyn_alpha();
+    ha.trace = trace_buffer(c, (size_t)hdp::head_fused_grid((int)rows) * 8);
+    {
+      KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
+      CK_CUDA(hdp::launch_head_fused(ha, s));
+    }
+    if (ha.trace && hdp::head_fused_grid((int)rows) <= 8192) CK(trace_report(c, hdp::TRACE_HEAD, ha.trace, hdp::head_fused_grid((int)rows), 0, s));
+  } else if (d.fc_hidden > 0) {
     const int iF = c->find("F"), ifb = c->find("fb");
     hdp::Epilogue ez = epi_elem(f32, S.Z, c->Fp);
     ez.bias = c->W(ifb);
@@ -732,7 +833,18 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
   const char* Htop = S.Hs + ((L - 1) * hs_layer + (long)B * hp) * e;
   const int iwo = c->find("wo"), ibo = c->find("bo");
   if (seg == 0) {
-    if (d.fc_hidden > 0) {
+    if (d.fc_hidden > 0 && c->head_fused) {
+      const int iF = c->find("F"), ifb = c->find("fb");
+      const long Fp = c->Fp;
+      // the forward's fused head left dz, dH_top and per-CTA column partials: dwo, dfb, dbo
+      // by the fixed-order fp64 pass 2, dF = dz^T H by the GEMM
+      {
+        KScope ks_(c, HDP_K_HEAD_BWD, 1, s);
+        CK_CUDA(hdp::launch_colreduce3_final(reinterpret_cast<const double*>(S.Z), hdp::head_fused_grid((int)rows),
+                                             (int)Fp, gt, c->G(si, iwo), c->G(si, ifb), c->G(si, ibo), s));
+      }
+      CK(gemm(c, HDP_K_HEAD_BWD, S.dz, Fp, 1, Htop, hp, 1, Fp, hp, rows, epi_elem(gf, c->G(si, iF), hp), s));
+    } else if (d.fc_hidden > 0) {
       const int iF = c->find("F"), ifb = c->find("fb");
       const long Fp = c->Fp;
       // dz (R9) was written by the forward's head_out; dwo, dfb, dbo in one fused column pass
@@ -777,7 +889,7 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
   }
   const int l = (int)(L - seg);
   // dH_above of this layer lives in dH[(L-1-l) & 1]
-  float* dHa = c->dH[(L - 1 - l) & 1];
+  float* dHa = l == L - 1 && c->head_fused ? S.dHh : c->dH[(L - 1 - l) & 1];
   float* dHnext = c->dH[(L - l) & 1];
   char nm[16];
   snprintf(nm, sizeof nm, "W%d", l);
@@ -1133,11 +1245,12 @@ int check_desc_across_ranks(hdp_ctx* c, const hdp_model_desc& d) {
 
 // ====================================================================== options
 namespace hdp {
-int g_opt[OPT_COUNT] = {1, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0};
+int g_opt[OPT_COUNT] = {1, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 16, 1};
 namespace {
 const char* const kOptNames[OPT_COUNT] = {"persistent",     "wavefront", "wavefront_fusex", "wavefront_wgrad",
                                           "wavefront_tmem", "recur_nbg", "gemm_cta_group",  "gemm_cluster_n",
-                                          "pdl",            "k7_bn",     "k7_splits",       "recur_trace"};
+                                          "pdl",            "k7_bn",     "k7_splits",       "recur_trace",
+                                          "layer_pipe",     "head_fused"};
 }
 int opt_find(const char* name) {
   for (int i = 0; i < OPT_COUNT; ++i)
@@ -1192,6 +1305,9 @@ int hdp_destroy(hdp_ctx* c) {
   cudaSetDevice(c->device);
   for (auto& kv : c->graphs) cudaGraphExecDestroy(kv.second);
   for (auto ev : c->ev_bucket) cudaEventDestroy(ev);
+  for (auto ev : c->ev_layer) cudaEventDestroy(ev);
+  for (auto st : c->lstr) cudaStreamDestroy(st);
+  if (c->ev_fork) cudaEventDestroy(c->ev_fork);
   for (auto ev : c->evpool) cudaEventDestroy(ev);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->ev_count) cudaEventDestroy(c->ev_count);
@@ -1237,6 +1353,9 @@ int hdp_configure(hdp_ctx* c, const hdp_model_desc* desc, hdp_sizes* out) {
   c->f32 = d.math == HDP_MATH_FP32;
   c->bf = d.math == HDP_MATH_BF16;
   c->gf32 = c->f32 || d.wire == HDP_WIRE_FP32;
+  c->head_fused = !c->f32 && !c->bf && d.fc_hidden > 0 && !d.head_last_step && d.n_layers > 0 &&
+                  hdp::head_fused_supported((int)r16(d.hidden), (int)r16(d.fc_hidden)) &&
+                  hdp::opt(hdp::OPT_HEAD_FUSED) != 0;
   c->esz = c->f32 ? 4 : 2;
   c->gsz = c->gf32 ? 4 : 2;
   c->nslots = d.sim_workers;
@@ -1283,6 +1402,11 @@ int hdp_bind(hdp_ctx* c, void* arena, long long bytes) {
   CK_CUDA(cudaEventCreateWithFlags(&c->ev_count, cudaEventDisableTiming));
   c->ev_bucket.resize(c->buckets.size());
   for (auto& ev : c->ev_bucket) CK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  c->lstr.resize(c->d.n_layers);
+  c->ev_layer.resize(c->d.n_layers);
+  for (auto& st : c->lstr) CK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+  for (auto& ev : c->ev_layer) CK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+  CK_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
   CK_CUDA(cudaMallocHost(&c->count_host, 2 * sizeof(int)));
   c->count_host[0] = c->count_host[1] = 0;
   c->st.assign(c->nslots, SlotState{});
@@ -1875,6 +1999,14 @@ int hdp_set_option(hdp_ctx* c, const char* name, double value) {
   return HDP_OK;
 }
 
+int hdp_get_option(const char* name, double* value) {
+  if (!name || !value) return fail(HDP_ERR_ARG, "null argument");
+  const int id = hdp::opt_find(name);
+  if (id < 0) return fail(HDP_ERR_ARG, "unknown option %s", name);
+  *value = hdp::g_opt[id];
+  return HDP_OK;
+}
+
 int hdp_partial_state(hdp_ctx* c, unsigned* mask, int* count) {
   CK(check_ready(c));
   if (!mask || !count) return fail(HDP_ERR_ARG, "null argument");
@@ -1936,7 +2068,8 @@ void* hdp_debug_buffer(hdp_ctx* c, int slot, const char* name) {
   if (n == "C") return S.C;
   if (n == "gates") return S.gates;
   if (n == "X0") return S.X0;
-  if (n == "Z") return S.Z;
+  if (n == "Z") return S.Z;  // (unfused head only: the fused head keeps its column partials there)
+  if (n == "dz") return S.dz;
   if (n == "dA") return c->dA;
   if (n == "dA2") return c->dA2;
   if (n == "dH0") return c->dH[0];

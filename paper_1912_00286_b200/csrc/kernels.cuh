@@ -99,6 +99,9 @@ size_t colreduce_partials_floats(int rows, int cols);
 // FC head: dwo = Z^T dy, dfb = colsum(dz), dbo = sum(dy) in one fused pass (partials: (2F+1)*RS doubles)
 cudaError_t launch_colreduce(int x_f32, const void* X, long ldx, int rows, int cols, const float* w,
                              float* partials, int out_f32, void* out, cudaStream_t s);
+// pass 2 alone over rs rows of fp64 partials [rs][2F + 1] (the fused head's per-CTA sums)
+cudaError_t launch_colreduce3_final(const double* partials, int rs, int F, int out_f32, void* dwo, void* dfb,
+                                    void* dbo, cudaStream_t s);
 cudaError_t launch_colreduce3(int x_f32, const void* Z, const void* dz, long ld, int rows, int F, const float* dy,
                               float* partials, int out_f32, void* dwo, void* dfb, void* dbo, cudaStream_t s);
 

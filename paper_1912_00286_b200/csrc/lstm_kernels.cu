@@ -790,6 +790,13 @@ cudaError_t launch_colreduce3(int x_f32, const void* Z, const void* dz, long ld,
   return cudaGetLastError();
 }
 
+cudaError_t launch_colreduce3_final(const double* partials, int rs, int F, int out_f32, void* dwo, void* dfb,
+                                    void* dbo, cudaStream_t s) {
+  const int cols = 2 * F + 1;
+  colreduce3_pass2<<<(cols * 32 + 255) / 256, 256, 0, s>>>(partials, rs, F, out_f32, dwo, dfb, dbo);
+  return cudaGetLastError();
+}
+
 size_t embed_sort_temp_bytes(int n) {
   const size_t ntiles = ((size_t)n + RS_TILE - 1) / RS_TILE;
   return 256 * ntiles * sizeof(int32_t);

@@ -18,6 +18,8 @@ enum OptId {
   OPT_K7_BN,             // per-step K7 tile width override (0 = automatic)
   OPT_K7_SPLITS,         // per-step K7 split-K override (0 = automatic)
   OPT_RECUR_TRACE,       // 1: phase trace of the recurrence kernels in profile (eager) mode
+  OPT_LAYER_PIPE,        // per-step path, L >= 2: layer-diagonal forward schedule in chunks of this many steps (0 = off)
+  OPT_HEAD_FUSED,        // 1: fused FC head kernel (mixed mode, h_p, F_p <= 256), fixed per context at configure
   OPT_COUNT
 };
 

@@ -1,3 +1,4 @@
+#include <algorithm>
 // Decoding of the recurrence kernels' phase traces (option recur_trace = 1 in profile
 // mode, hdp_set_option): each traced step stores 5 globaltimer stamps per role; this
 // prints the per-step mean of every phase to stderr.  Development aid, not on the hot path.
@@ -10,6 +11,27 @@ namespace hdp {
 void print_trace(TraceKind kind, const unsigned long long* h, int T, int l) {
   (void)l;
   switch (kind) {
+    case TRACE_HEAD: {  // fused head: T = grid, 8 stamps per CTA
+      const char* names[7] = {"TMA landed", "z acc seen", "y (pass 1)", "dz + sums (pass 2)", "dH acc seen",
+                              "dH stored (pass 3)", "exit"};
+      unsigned long long s0 = ~0ull, s1 = 0;
+      for (int b = 0; b < T; ++b) {
+        s0 = std::min(s0, h[b * 8]);
+        s1 = std::max(s1, h[b * 8]);
+      }
+      fprintf(stderr, "[hdp trace] head: %d CTAs, entry spread %llu ns\n", T, s1 - s0);
+      for (int k = 1; k < 8; ++k) {
+        double mean = 0, mx = 0;
+        for (int b = 0; b < T; ++b) {
+          const double d = (double)(h[b * 8 + k] - h[b * 8]);
+          mean += d;
+          mx = std::max(mx, d);
+        }
+        fprintf(stderr, "[hdp trace] head: %-20s +%.0f ns mean, +%.0f max (from CTA entry)\n", names[k - 1], mean / T,
+                mx);
+      }
+      break;
+    }
     case TRACE_FWD_WAVEFRONT: {
       const unsigned long long t00 = h[0];
       const char* names[3] = {"R0", "P", "R1"};

@@ -31,7 +31,7 @@ EXPORTED = [
     "hdp_loss_scale_state", "hdp_lstm_forward",
     "hdp_lstm_backward", "hdp_grad_average_update", "hdp_weights_ptr", "hdp_grads_ptr", "hdp_master_ptr",
     "hdp_fused_avg_update", "hdp_gemm_f16", "hdp_gemm_f32", "hdp_profile", "hdp_profile_read",
-    "hdp_kernel_launches", "hdp_debug_buffer", "hdp_set_option", "hdp_partial_state",
+    "hdp_kernel_launches", "hdp_debug_buffer", "hdp_set_option", "hdp_get_option", "hdp_partial_state",
 ]
 NTAGS = 15
 
@@ -103,6 +103,7 @@ def _load():
         "hdp_kernel_launches": ([vp], ll),
         "hdp_set_option": ([vp, C.c_char_p, d], i),
         "hdp_partial_state": ([vp, C.POINTER(C.c_uint), C.POINTER(i)], i),
+        "hdp_get_option": ([C.c_char_p, C.POINTER(d)], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -253,12 +254,20 @@ def loss_scale_state(ctx: int):
 # process-wide kernel switches and their defaults (csrc/options.h, hdp_set_option)
 KERNEL_OPTION_DEFAULTS = {"persistent": 1, "wavefront": 1, "wavefront_fusex": 1, "wavefront_wgrad": 1,
                           "wavefront_tmem": 1, "recur_nbg": 0, "gemm_cta_group": 0,
-                          "gemm_cluster_n": 0, "pdl": 0, "k7_bn": 0, "k7_splits": 0, "recur_trace": 0}
+                          "gemm_cluster_n": 0, "pdl": 0, "k7_bn": 0, "k7_splits": 0, "recur_trace": 0,
+                          "layer_pipe": 16, "head_fused": 1}
 
 
 def set_option(ctx, name: str, value: float):
     """hdp_set_option: context options (ctx) or process-wide kernel switches (ctx may be None)."""
     _ck(_lib.hdp_set_option(ctx, name.encode(), float(value)))
+
+
+def get_option(name: str) -> int:
+    """hdp_get_option: current value of a process-wide kernel switch."""
+    v = C.c_double()
+    _ck(_lib.hdp_get_option(name.encode(), C.byref(v)))
+    return int(v.value)
 
 
 def partial_state(ctx):

@@ -288,6 +288,48 @@ def test_c4_full_width_batches_mixed(batch, seq):
     assert _max(r["master_err"]) <= 2e-2
 
 
+@pytest.mark.parametrize("batch,seq", [(128, 128), (40, 24), (3, 5)])
+def test_head_fused_matches_unfused_and_oracle(batch, seq):
+    """The fused FC head kernel (z, y, hinge, dy, dz, dH_top and the head's column sums in
+    one launch; csrc/head.cu) against the oracle and against the unfused path (FC GEMM,
+    head_out, column reduction, dH GEMM): C2 at its bench shape (128 CTAs), a ragged
+    tile count (960 rows = 7.5 tiles) and a sub-tile case (15 rows)."""
+    cfg = synth.CONFIGS["C2"].with_(seq=seq)
+    out = {}
+    for fused in (1, 0):
+        with kernel_options(head_fused=fused):
+            out[fused] = run_parity(cfg, batch, 1, steps=1 if batch * seq > 4096 else 2, mixed=True)
+        for r in out[fused]:
+            assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"])), (fused, r)
+            assert _max(r["grad_err"][0]) <= (GRAD_MIXED_FULL if batch * seq > 4096 else GRAD_MIXED), \
+                (fused, r["grad_err"])
+        assert _max(out[fused][-1]["master_err"]) <= 2e-2
+    for a, b in zip(out[1], out[0]):
+        assert abs(a["loss_gpu"] - b["loss_gpu"]) <= 1e-5 * max(1.0, abs(b["loss_gpu"]))
+
+
+@pytest.mark.parametrize("tc", [16, 7, 1])
+def test_layer_pipeline_bit_identical_to_sequential(tc):
+    """The layer-diagonal forward schedule of the per-step path (option layer_pipe: layer
+    l's chunk of tc steps on its own stream after layer l-1's) launches the same kernels
+    on the same operands as the layer-by-layer loop: loss, master and fp16 weights after
+    3 steps are bit-identical, and both match the oracle.  4 layers, T = 40 (chunks
+    16/16/8, 7 x 5 + 5, or one step each), per-step path forced (persistent = 0)."""
+    import numpy as np
+    cfg = synth.CONFIGS["C4"].with_(hidden=128, input_dim=96, seq=40)
+    out = {}
+    for pipe in (tc, 0):
+        with kernel_options(persistent=0, layer_pipe=pipe):
+            out[pipe] = run_parity(cfg, 48, 1, steps=3, mixed=True, keep_state=True)
+    for a, b in zip(out[tc], out[0]):
+        assert a["loss_gpu"] == b["loss_gpu"]
+        assert np.array_equal(a["gpu_master"], b["gpu_master"])
+        assert np.array_equal(a["gpu_w"], b["gpu_w"])
+        assert abs(a["loss_gpu"] - a["loss_ref"]) <= 1e-2 * max(1.0, abs(a["loss_ref"]))
+        assert _max(a["grad_err"][0]) <= GRAD_MIXED, a["grad_err"]
+    assert _max(out[tc][-1]["master_err"]) <= 2e-2
+
+
 # ---------------------------------------------------------------- persistent recurrence path
 # B >= 16 and small h select the persistent fused recurrence kernel (one
 # cooperative launch per layer); these cases cover 1 CTA (h = 32), 8 CTAs
@@ -413,13 +455,21 @@ def test_degenerate_shapes(cfg_name, batch, seq, mixed):
     assert _max(recs[-1]["master_err"]) <= tol
 
 
-def test_c2_relu_decision_within_rounding():
+@pytest.mark.parametrize("fused", [1, 0])
+def test_c2_relu_decision_within_rounding(fused):
     """DESIGN.md R-relu: where an FC pre-activation lies within the fp16 rounding of h
     of zero, both ReLU branches are correct results.  C2 at B = 1, T = 2 (mixed) has
-    one at -1.0e-6 in its seeded batch.  The kernel's decisions (Z > 0, debug buffer
-    "Z") must agree with the oracle's wherever |zpre| exceeds that rounding bound
-    (sum_k |F_jk| |h_k| 2^-11); the gradients are then compared with the oracle run
-    on the kernel's decisions (lstm.forward relu_active), within the mixed bound."""
+    one at -1.0e-6 in its seeded batch.  The kernel's decisions must agree with the
+    oracle's wherever |zpre| exceeds that rounding bound (sum_k |F_jk| |h_k| 2^-11); the
+    gradients are then compared with the oracle run on the kernel's decisions
+    (lstm.forward relu_active), within the mixed bound.  The decisions are read from dz
+    (debug buffer "dz": dz_j != 0 iff z_j > 0 on rows with dy != 0; the decision is moot
+    on the others), for the fused head kernel and the unfused GEMM + head_out path."""
+    with kernel_options(head_fused=fused):
+        _relu_decision_case()
+
+
+def _relu_decision_case():
     from paper_1912_00286_b200 import hdp
     from oracle import lstm as olstm
     from oracle import step as ostep
@@ -438,18 +488,20 @@ def test_c2_relu_decision_within_rounding():
         hdp.lstm_backward(tr.ctx, 0, s)
         torch.cuda.synchronize()
         Fp = (fc + 15) // 16 * 16
-        Z = torch.empty(T * B * Fp, dtype=torch.float16, device=dev)
-        _copy_dev(Z, hdp.debug_buffer(tr.ctx, 0, "Z"), Z.numel() * 2)
-        act_gpu = (Z.view(T, B, Fp)[:, :, :fc] > 0).cpu().numpy()
+        dz = torch.empty(T * B * Fp, dtype=torch.float16, device=dev)
+        _copy_dev(dz, hdp.debug_buffer(tr.ctx, 0, "dz"), dz.numel() * 2)
+        dz_gpu = (dz.view(T, B, Fp)[:, :, :fc] != 0).cpu().numpy()
         g_gpu = hdp.read_grads(tr.ctx, 0, tr.n).astype(np.float64)
     finally:
         tr.close()
     P = olstm.unpack(cfg, params.astype(np.float64))
     _, _, cache = olstm.forward(cfg, P, x, t, cfg.alpha, "mixed")
     zpre, Htop = cache["zpre"], cache["Htop"]
+    rows_live = dz_gpu.any(axis=-1, keepdims=True)             # dy != 0 on these rows
+    act_gpu = np.where(rows_live, dz_gpu, zpre > 0)
     bound = (np.abs(Htop) * 2.0 ** -11) @ np.abs(P["F"]).T + 1e-12
     ambiguous = np.abs(zpre) <= bound
-    assert ambiguous.any()                                      # the case exercises the reading
+    assert (ambiguous & rows_live).any()                        # the case exercises the reading
     assert np.all((act_gpu == (zpre > 0)) | ambiguous)          # validity of the kernel's branches
     at = {}
     _, g_ref, _ = ostep.worker_grads(cfg, params.astype(np.float64), x, t, cfg.alpha, "mixed", at,
