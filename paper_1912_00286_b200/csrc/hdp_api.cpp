@@ -179,6 +179,10 @@ struct hdp_ctx {
   std::vector<cudaStream_t> lstr;
   std::vector<cudaEvent_t> ev_layer;
   cudaEvent_t ev_fork = nullptr;
+  // fused head: its backward segment (column sums + dF GEMM) runs on hstr next to the layers'
+  cudaStream_t hstr = nullptr;
+  cudaEvent_t ev_hfork = nullptr;
+  float* ws_head = nullptr;  // split-K scratch of the head's dF GEMM (concurrent with the layers' GEMMs)
   int* count_host = nullptr;  // pinned [0] non-finite count, [1] out-of-range token ids
   bool count_pending = false;
   std::map<GraphKey, cudaGraphExec_t> graphs;
@@ -434,6 +438,7 @@ void carve(hdp_ctx* c, char* base) {
     if (c->f32) ws = 0;
     c->ws_floats = ws;
     c->ws = (float*)cv.take(ws * 4);
+    c->ws_head = (float*)cv.take(c->head_fused ? gemm_need((int)c->Fp, (int)hp, (int)rows) * 4 : 0);
     if (d.vocab > 0) {
       c->keys_in = (int32_t*)cv.take(rows * 4);
       c->keys_out = (int32_t*)cv.take(rows * 4);
@@ -843,7 +848,8 @@ int enqueue_backward_seg(hdp_ctx* c, int si, int B, int T, int seg, cudaStream_t
         CK_CUDA(hdp::launch_colreduce3_final(reinterpret_cast<const double*>(S.Z), hdp::head_fused_grid((int)rows),
                                              (int)Fp, gt, c->G(si, iwo), c->G(si, ifb), c->G(si, ibo), s));
       }
-      CK(gemm(c, HDP_K_HEAD_BWD, S.dz, Fp, 1, Htop, hp, 1, Fp, hp, rows, epi_elem(gf, c->G(si, iF), hp), s));
+      CK(gemm(c, HDP_K_HEAD_BWD, S.dz, Fp, 1, Htop, hp, 1, Fp, hp, rows, epi_elem(gf, c->G(si, iF), hp), s, 0, 0,
+              c->ws_head));
     } else if (d.fc_hidden > 0) {
       const int iF = c->find("F"), ifb = c->find("fb");
       const long Fp = c->Fp;
@@ -1308,6 +1314,8 @@ int hdp_destroy(hdp_ctx* c) {
   for (auto ev : c->ev_layer) cudaEventDestroy(ev);
   for (auto st : c->lstr) cudaStreamDestroy(st);
   if (c->ev_fork) cudaEventDestroy(c->ev_fork);
+  if (c->ev_hfork) cudaEventDestroy(c->ev_hfork);
+  if (c->hstr) cudaStreamDestroy(c->hstr);
   for (auto ev : c->evpool) cudaEventDestroy(ev);
   if (c->ev_done) cudaEventDestroy(c->ev_done);
   if (c->ev_count) cudaEventDestroy(c->ev_count);
@@ -1407,6 +1415,8 @@ int hdp_bind(hdp_ctx* c, void* arena, long long bytes) {
   for (auto& st : c->lstr) CK_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
   for (auto& ev : c->ev_layer) CK_CUDA(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
   CK_CUDA(cudaEventCreateWithFlags(&c->ev_fork, cudaEventDisableTiming));
+  CK_CUDA(cudaStreamCreateWithFlags(&c->hstr, cudaStreamNonBlocking));
+  CK_CUDA(cudaEventCreateWithFlags(&c->ev_hfork, cudaEventDisableTiming));
   CK_CUDA(cudaMallocHost(&c->count_host, 2 * sizeof(int)));
   c->count_host[0] = c->count_host[1] = 0;
   c->st.assign(c->nslots, SlotState{});
@@ -1709,11 +1719,26 @@ int hdp_lstm_backward(hdp_ctx* c, int slot, void* stream) {
   if (c->poisoned) return fail(HDP_ERR_STATE, "context poisoned");
   cudaStream_t s = (cudaStream_t)stream;
   const int B = c->st[slot].B, T = c->st[slot].T;
+  // fused head: the forward already produced dH_top, so the head's own gradient work (column
+  // sums, dF GEMM) is off the layers' path -- it runs on a side stream, launched after the
+  // first layer segment so the recurrence launch is dispatched first and the GEMM fills the
+  // SMs it leaves idle
+  const bool head_side = c->head_fused && c->hstr && nsegs(c) > 1;
+  if (head_side) {
+    CK_CUDA(cudaEventRecord(c->ev_hfork, s));
+    CK_CUDA(cudaStreamWaitEvent(c->hstr, c->ev_hfork, 0));
+  }
   for (int seg = 0; seg < nsegs(c); ++seg) {
+    if (seg == 0 && head_side) continue;
     CK(run_graph(c, slot, B, T, seg, s));
     // bucket `seg` (head, then layers top-down) is complete: the exchange may start
     CK_CUDA(cudaEventRecord(c->ev_bucket[seg], s));
+    if (seg == 1 && head_side) {
+      CK(run_graph(c, slot, B, T, 0, c->hstr));
+      CK_CUDA(cudaEventRecord(c->ev_bucket[0], c->hstr));
+    }
   }
+  if (head_side) CK_CUDA(cudaStreamWaitEvent(s, c->ev_bucket[0], 0));  // the caller's stream sees it all
   if (c->d.vocab > 0) CK_CUDA(cudaEventRecord(c->ev_bucket[nsegs(c)], s));  // embedding (after layer 0)
   c->st[slot].bwd = true;
   return HDP_OK;
@@ -1880,10 +1905,18 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
         }
         CK_NCCL(ncclGroupEnd());
       }
+      // world 1: a group's buckets are contiguous in every buffer (one shard each, master
+      // offset = gradient offset), so the group is one K11 launch over their union
+      const bool merge = c->world == 1;
       for (size_t bi = b0; bi < b1; ++bi) {
         if (c->task0 && c->rank != 0) break;  // step 5 runs on task 0 only
         const Bucket& bk = c->buckets[bi];
         a.count = bk.shard;
+        if (merge) {
+          const Bucket& bl = c->buckets[b1 - 1];
+          a.count = bl.off + bl.len - bk.off;
+          bi = b1 - 1;
+        }
         a.W = c->master + bk.moff;
         a.S1 = c->s1 + bk.moff;
         a.S2 = c->s2 ? c->s2 + bk.moff : nullptr;
