@@ -678,6 +678,11 @@ __device__ __forceinline__ void bwd_wgrad_role(const Bwd2Params& P, int tile) {
         }
         __syncwarp();  // the lanes' acquires happen-before lane 0's TMA reads (memory ordering of the warp barrier)
         fence_proxy_async();
+        if (P.trace && t == 0 && lane == 0) {  // phase trace: the last step's dA seen (W slots after the CTA stamps)
+          unsigned long long* w = P.trace + (size_t)6 * T * 5 + 3 * 148 + 3 * (blockIdx.y * gridDim.x + blockIdx.x);
+          w[0] = ptx::globaltimer_ns();
+          w[2] = 1 + mat;
+        }
       }
       if (lane != 0) continue;
       ptx::mbar_wait(empty + s, ((it / NS) & 1) ^ 1);
@@ -717,17 +722,42 @@ __device__ __forceinline__ void bwd_wgrad_role(const Bwd2Params& P, int tile) {
   __syncwarp();
   ptx::mbar_wait(done, 0);
   ptx::tc_fence_after();
-  // ---- epilogue: TMEM lane = tile row; fp32 sums rounded once to fp16 (R13)
+  if (P.trace && threadIdx.x == 0)
+    P.trace[(size_t)6 * T * 5 + 3 * 148 + 3 * (blockIdx.y * gridDim.x + blockIdx.x) + 1] = ptx::globaltimer_ns();
+  // ---- epilogue: TMEM lane = tile row; fp32 sums rounded once to fp16 (R13), staged as a
+  // [128][N] fp16 tile in the (now idle) TMA ring and written as whole 16-B row chunks.
+  // (Round 2 stored 2-byte values lane-per-row: 32 scattered sectors per instruction, a
+  // 28 us tail of the launch after the layer-0 chain at C2.)
   const int row = m0 + warp * 32 + lane;
   __half* gout = P.gW[mat];
+  const int ld = mat == 3 ? P.Ip0 : hp;
+  const int lds = natom * 64 + 8;              // staging row stride (halves): conflict-free 16-B rows
+  __half* stile = reinterpret_cast<__half*>(smem);
   for (int c = 0; c < N; c += 16) {
     float v[16];
     ptx::tmem_ld16(tbase + (static_cast<uint32_t>(warp * 32) << 16) + c, v);
-    if (row < fourhp) {
-      const int ld = mat == 3 ? P.Ip0 : hp;
+    __align__(16) __half hv[16];
 #pragma unroll
-      for (int q = 0; q < 16; ++q)
-        if (c + q < N && n0 + c + q < ld) gout[(size_t)row * ld + n0 + c + q] = __float2half_rn(v[q]);
+    for (int q = 0; q < 16; ++q) hv[q] = __float2half_rn(v[q]);
+    uint4* dst = reinterpret_cast<uint4*>(stile + (size_t)(warp * 32 + lane) * lds + c);
+    dst[0] = reinterpret_cast<const uint4*>(hv)[0];
+    dst[1] = reinterpret_cast<const uint4*>(hv)[1];
+  }
+  __syncthreads();
+  {
+    const int ncol = min(N, ld - n0);            // valid output columns of this tile
+    const int nch = (ncol + 7) / 8;              // 8-half chunks per row
+    for (int i = threadIdx.x; i < 128 * nch; i += blockDim.x) {
+      const int r = i / nch, ch = i % nch;
+      const int grow = m0 + r, col = ch * 8;
+      if (grow >= fourhp) continue;
+      const __half* src = stile + (size_t)r * lds + col;
+      __half* o = gout + (size_t)grow * ld + n0 + col;
+      if (col + 8 <= ncol && (((size_t)grow * ld + n0 + col) & 7) == 0) {
+        *reinterpret_cast<uint4*>(o) = *reinterpret_cast<const uint4*>(src);
+      } else {
+        for (int q = 0; q < 8 && col + q < ncol; ++q) o[q] = src[q];
+      }
     }
   }
   if (withb) {

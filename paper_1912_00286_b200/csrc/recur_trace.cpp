@@ -165,6 +165,24 @@ void print_trace(TraceKind kind, const unsigned long long* h, int T, int l) {
                 names[role], ph[0] / n, ph[1] / n, ph[2] / n, ph[3] / n, step / n,
                 (double)(h[((size_t)role * T + T - 2) * 5] - t00), (double)(h[((size_t)role * T) * 5 + 4] - t00));
       }
+      {  // W role: last step's dA seen by the producer, MMAs done (per weight matrix)
+        const unsigned long long* w = h + (size_t)6 * T * 5 + 3 * 148;
+        const unsigned long long t00 = h[(size_t)(T - 1) * 5];
+        const char* mn[4] = {"dU1", "dW1", "dU0", "dW0"};
+        for (int mat = 0; mat < 4; ++mat) {
+          double seen = 0, done = 0;
+          int n = 0;
+          for (int k = 0; k < 148; ++k) {
+            if (!w[3 * k] || w[3 * k + 2] != (unsigned long long)(1 + mat)) continue;
+            seen = std::max(seen, (double)(w[3 * k] - t00));
+            done = std::max(done, (double)(w[3 * k + 1] - t00));
+            ++n;
+          }
+          if (n)
+            fprintf(stderr, "[hdp trace] bwd W %s: %d CTAs, last dA_0 seen +%.0f ns, MMAs done +%.0f ns (vs Q1 step T-1)\n",
+                    mn[mat], n, seen, done);
+        }
+      }
       {  // per-CTA entry / exit per role, relative to Q1's first step
         const unsigned long long* c = h + (size_t)6 * T * 5;
         const char* rn[4] = {"Q1", "X", "Q0", "W"};
