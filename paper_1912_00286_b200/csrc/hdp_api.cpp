@@ -490,18 +490,18 @@ struct KScope {
 // %globaltimer per phase; trace_report (recur_trace.cpp) prints the per-step means.
 unsigned long long* trace_buffer(hdp_ctx* c, size_t words) {
   if (!c->prof || !hdp::opt(hdp::OPT_RECUR_TRACE)) return nullptr;
-  if (!c->trace && cudaMalloc(&c->trace, ((size_t)6 * 8192 * 5 + 6 * 148) * sizeof(unsigned long long)) != cudaSuccess) {
+  if (!c->trace && cudaMalloc(&c->trace, ((size_t)6 * 8192 * 5 + 6 * 148 + 16) * sizeof(unsigned long long)) != cudaSuccess) {
     c->trace = nullptr;
     return nullptr;
   }
   (void)words;
-  cudaMemset(c->trace, 0, ((size_t)6 * 8192 * 5 + 6 * 148) * sizeof(unsigned long long));
+  cudaMemset(c->trace, 0, ((size_t)6 * 8192 * 5 + 6 * 148 + 16) * sizeof(unsigned long long));
   return c->trace;
 }
 int trace_report(hdp_ctx* c, hdp::TraceKind kind, const unsigned long long* dev, int T, int layer, cudaStream_t s) {
   (void)c;
   if (T > 8192) return HDP_OK;
-  std::vector<unsigned long long> h((size_t)6 * T * 5 + 6 * 148);  // + per-CTA entry / exit / role stamps, W-role stamps
+  std::vector<unsigned long long> h((size_t)6 * T * 5 + 6 * 148 + 16);  // + per-CTA entry / exit / role stamps, W-role stamps
   CK_CUDA(cudaStreamSynchronize(s));
   CK_CUDA(cudaMemcpy(h.data(), dev, h.size() * 8, cudaMemcpyDeviceToHost));
   hdp::print_trace(kind, h.data(), T, layer);

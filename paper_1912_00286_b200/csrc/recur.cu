@@ -825,14 +825,17 @@ __device__ __forceinline__ void bwd_proj_role_ts(const Bwd2Params& P, int grp) {
     const int i = lane & 15;
     const int u = warp * 16 + i;
     const uint32_t tq = tA + (static_cast<uint32_t>(warp * 32) << 16);
+    int off[8];  // swizzled offsets repeat every 8 rows (see the Q roles' copy)
+#pragma unroll
+    for (int r8 = 0; r8 < 8; ++r8) off[r8] = r8 * 128 + (((u >> 3) ^ r8) << 4) + (u & 7) * 2;
     for (int c0 = 0; c0 < 2 * hp; c0 += 16) {
+      const uint8_t* base = sW + (size_t)c0 * 256;
       uint32_t v[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const int kk = 2 * (c0 + j), kb = kk >> 6, kr = kk & 63;
-        const uint8_t* row = sW + kb * 8192 + kr * 128;
-        const uint32_t lo = __half_as_ushort(*reinterpret_cast<const __half*>(row + (((u >> 3) ^ (kr & 7)) << 4) + (u & 7) * 2));
-        const uint32_t hi = __half_as_ushort(*reinterpret_cast<const __half*>(row + 128 + (((u >> 3) ^ ((kr + 1) & 7)) << 4) + (u & 7) * 2));
+        const uint8_t* g8 = base + ((2 * j) & ~7) * 128;
+        const uint32_t lo = *reinterpret_cast<const uint16_t*>(g8 + off[(2 * j) & 7]);
+        const uint32_t hi = *reinterpret_cast<const uint16_t*>(g8 + off[(2 * j + 1) & 7]);
         v[j] = lane < 16 ? (lo | (hi << 16)) : 0u;
       }
       ptx::tmem_st16(tq + c0, v);
@@ -1148,10 +1151,15 @@ __global__ void __launch_bounds__(128, 1)
     for (int i = 0; i < RG; ++i) ptx::mbar_init(barP + i, 1);
     ptx::fence_mbar_init();
   }
+  // phase trace: prologue stamps of CTA 0 / group 0 (after the W-role slots)
+  unsigned long long* tpro = (P.trace && blockIdx.x == 0 && grp == 0 && threadIdx.x == 0)
+                                 ? P.trace + (size_t)6 * T * 5 + 6 * 148 + qi * 8 : nullptr;
+  if (tpro) tpro[0] = ptx::globaltimer_ns();
   if (warp == 2) ptx::tmem_alloc(tslot, tcols);
   ptx::tc_fence_before();
   __syncthreads();
   ptx::tc_fence_after();
+  if (tpro) tpro[1] = ptx::globaltimer_ns();
   const uint32_t tbase = *tslot;
   if (threadIdx.x == 0) {
     // arm both operand slots for their first use before any peer can deliver
@@ -1161,8 +1169,10 @@ __global__ void __launch_bounds__(128, 1)
     for (int kb = 0; kb < nkb; ++kb) ptx::tma_load_2d(sU + kb * 8192, &tmU, barU, j0, kb * 64);
     ptx::mbar_wait(barU, 0);
   }
+  if (tpro) tpro[2] = ptx::globaltimer_ns();
   ptx::cluster_arrive();  // all CTAs resident, barriers initialised and armed
   ptx::cluster_wait();
+  if (tpro) tpro[3] = ptx::globaltimer_ns();
   const uint32_t tA = tbase + 64;  // TSQ: A = U^T slice, columns [64, 64 + 2 h_p)
   if (TSQ) {
     // sU (MN-major SWIZZLE_128B: row k = 128 B of 64 units, 16-B chunk (unit/8) ^ (k%8)) -> TMEM:
@@ -1170,14 +1180,20 @@ __global__ void __launch_bounds__(128, 1)
     const int i = lane & 15;
     const int u = warp * 16 + i;
     const uint32_t tq = tA + (static_cast<uint32_t>(warp * 32) << 16);
+    // gate row kk of unit u sits at sU + kk * 128 + 16 * ((u / 8) ^ (kk % 8)) + 2 * (u % 8)
+    // (8 KB K blocks of 64 rows are contiguous): the swizzled offsets repeat every 8 rows,
+    // so they are computed once (the per-element address arithmetic made this copy 5 us)
+    int off[8];
+#pragma unroll
+    for (int r8 = 0; r8 < 8; ++r8) off[r8] = r8 * 128 + (((u >> 3) ^ r8) << 4) + (u & 7) * 2;
     for (int c0 = 0; c0 < 2 * hp; c0 += 16) {
+      const uint8_t* base = sU + (size_t)c0 * 256;  // gate row 2 c0
       uint32_t v[16];
 #pragma unroll
       for (int j = 0; j < 16; ++j) {
-        const int kk = 2 * (c0 + j), kb = kk >> 6, kr = kk & 63;
-        const uint8_t* row = sU + kb * 8192 + kr * 128;
-        const uint32_t lo = __half_as_ushort(*reinterpret_cast<const __half*>(row + (((u >> 3) ^ (kr & 7)) << 4) + (u & 7) * 2));
-        const uint32_t hi = __half_as_ushort(*reinterpret_cast<const __half*>(row + 128 + (((u >> 3) ^ ((kr + 1) & 7)) << 4) + (u & 7) * 2));
+        const uint8_t* g8 = base + ((2 * j) & ~7) * 128;
+        const uint32_t lo = *reinterpret_cast<const uint16_t*>(g8 + off[(2 * j) & 7]);
+        const uint32_t hi = *reinterpret_cast<const uint16_t*>(g8 + off[(2 * j + 1) & 7]);
         v[j] = lane < 16 ? (lo | (hi << 16)) : 0u;
       }
       ptx::tmem_st16(tq + c0, v);
@@ -1188,6 +1204,7 @@ __global__ void __launch_bounds__(128, 1)
     __syncthreads();
     ptx::tc_fence_after();
   }
+  if (tpro) tpro[4] = ptx::globaltimer_ns();
   const int st_thr = 96;  // TSQ: TMA stores + publication (warp 3, no MMA issue)
   // TSQ, Q0: dH_above = dX1 slices prefetched by TMA one step ahead into the (now free) sU
   // region, by a thread that issues no MMAs; the flag acquire leaves the step's chain

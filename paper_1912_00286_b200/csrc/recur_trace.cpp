@@ -183,6 +183,16 @@ void print_trace(TraceKind kind, const unsigned long long* h, int T, int l) {
                     mn[mat], n, seen, done);
         }
       }
+      {  // Q prologue (CTA 0 of group 0)
+        const unsigned long long* pr = h + (size_t)6 * T * 5 + 6 * 148;
+        const unsigned long long t00 = h[(size_t)(T - 1) * 5];
+        for (int q = 0; q < 2; ++q)
+          if (pr[q * 8])
+            fprintf(stderr, "[hdp trace] bwd %s prologue (vs Q1 step T-1): entry %+.0f, TMEM alloc %+.0f, U slice landed %+.0f, "
+                    "cluster sync %+.0f, U^T in TMEM %+.0f ns\n", q ? "Q0" : "Q1", (double)pr[q * 8] - (double)t00,
+                    (double)pr[q * 8 + 1] - (double)t00, (double)pr[q * 8 + 2] - (double)t00,
+                    (double)pr[q * 8 + 3] - (double)t00, (double)pr[q * 8 + 4] - (double)t00);
+      }
       {  // per-CTA entry / exit per role, relative to Q1's first step
         const unsigned long long* c = h + (size_t)6 * T * 5;
         const char* rn[4] = {"Q1", "X", "Q0", "W"};
