@@ -269,12 +269,23 @@ __device__ __forceinline__ void lstm_bwd_unit(const Epilogue& e, size_t idx, flo
 // a 128 x BN tile for the same flops.  Both CTAs' TMA loads complete on the leader's
 // full barrier; the leader's commits arrive on both CTAs' empty / accumulator barriers;
 // both epilogues arrive on the leader's drain barrier.
-template <int BN, int AMN, int BMN, int CN = 1, int CG = 1>
+//
+// CR = 8 (the fused cell backward, EPI_LSTM_BWD, 8 K-splits, one tile per CTA): the 8 splits
+// of an output tile form one cluster; after every split's accumulator is complete (cluster
+// barrier: all shared-memory rings idle) each CTA sends the 32-column slice d of its fp32
+// partial into CTA d's ring through DSMEM, and after a second cluster barrier CTA d sums the
+// 8 partials of its slice in split order -- the same fp32 operation order as
+// splitk_reduce_kernel, so bit-identical -- and runs the cell backward on them.  No partial
+// planes in global memory, no second launch.
+template <int BN, int AMN, int BMN, int CN = 1, int CG = 1, int CR = 1>
 __global__ void __launch_bounds__(320, 1)
     gemm_tc_kernel(const __grid_constant__ CUtensorMap tma, const __grid_constant__ CUtensorMap tmb, int M, int N,
                    int K, int kbps, int splits, Epilogue epi, float* ws) {
   static_assert(CN == 1 || AMN == 0, "A multicast needs K-major A");
   static_assert(CG == 1 || CN == 1, "CTA pairs: no multicast");
+  static_assert(CR == 1 || (CN == 1 && CG == 1 && BN == 256), "cluster split-K reduction: single CTAs, BN = 256");
+  static_assert(CR == 1 || CR * 128 * 36 * 4 <= TileCfg<BN, CG>::STAGES * TileCfg<BN, CG>::STAGE,
+                "the partials fit in the ring");
   using C = TileCfg<BN, CG>;
   constexpr int CL = CN * CG;  // cluster size
   extern __shared__ uint8_t smem_raw[];
@@ -293,8 +304,10 @@ __global__ void __launch_bounds__(320, 1)
   const int kb_total = (K + BK - 1) / BK;
   const int crank = CN > 1 ? (int)(blockIdx.x % CN) : 0;
   const int prank = CG > 1 ? (int)(blockIdx.x % CG) : 0;  // 0 = pair leader
-  const int tile0 = CL > 1 ? (int)(blockIdx.x / CL) : (int)blockIdx.x;
-  const int tstep = CL > 1 ? (int)(gridDim.x / CL) : (int)gridDim.x;
+  // CR > 1: cluster c's CTA z computes split z of output tile c (one tile per CTA)
+  const int tile0 = CR > 1 ? (int)(blockIdx.x % CR) * mt * ngr + (int)(blockIdx.x / CR)
+                           : CL > 1 ? (int)(blockIdx.x / CL) : (int)blockIdx.x;
+  const int tstep = CR > 1 ? ntiles : CL > 1 ? (int)(gridDim.x / CL) : (int)gridDim.x;
   auto decode = [&](int tile, int& m0, int& n0, int& z, int& kb0, int& nkb) {
     z = tile / (mt * ngr);
     const int r = tile % (mt * ngr);
@@ -383,6 +396,13 @@ __global__ void __launch_bounds__(320, 1)
         for (int i = 0; i < C::STAGES; ++i, ++it)  // landed here) before the cluster may exit
           ptx::mbar_wait(empty + it % C::STAGES, ((it / C::STAGES) & 1) ^ 1);
     }
+    if constexpr (CR > 1) {  // the epilogue's two cluster barriers (every thread of the cluster)
+      __syncwarp();
+      ptx::cluster_arrive();
+      ptx::cluster_wait();
+      ptx::cluster_arrive();
+      ptx::cluster_wait();
+    }
   } else if (warp == 1) {
     if (lane == 0 && prank == 0) {
       // ---------------- MMA issuer (the pair leader for CG = 2)
@@ -423,6 +443,53 @@ __global__ void __launch_bounds__(320, 1)
         if (CG > 1) ptx::mma_commit_cg2_mc(accf + b, pmask);  // both CTAs' accumulators complete
         else ptx::mma_commit(accf + b);     // accumulator b complete
       }
+    }
+    if constexpr (CR > 1) {
+      __syncwarp();
+      ptx::cluster_arrive();
+      ptx::cluster_wait();
+      ptx::cluster_arrive();
+      ptx::cluster_wait();
+    }
+  } else if (CR > 1) {
+    // ---------------- cluster split-K reduction + fused cell backward (one tile per CTA)
+    const int q = warp & 3;
+    const int ch = (warp - 2) >> 2;
+    int m0, n0, z, kb0, nkb;
+    decode(tile0, m0, n0, z, kb0, nkb);
+    ptx::mbar_wait(accf, 0);
+    ptx::tc_fence_after();
+    ptx::cluster_arrive();  // every split's MMAs are complete: all rings are idle
+    ptx::cluster_wait();
+    float* rbuf = reinterpret_cast<float*>(smem);  // [CR][128 rows][36] fp32 partial slices
+    const int row = q * 32 + lane;
+    const uint32_t tq = tbase + (static_cast<uint32_t>(q * 32) << 16);
+    const uint32_t my_slot = ptx::smem_u32(rbuf + ((size_t)z * 128 + row) * 36);
+#pragma unroll 1
+    for (int j = 0; j < BN / 64; ++j) {
+      const int c = ch * (BN / 2) + 32 * j;  // 32-column slice owned by CTA c / 32 of the cluster
+      float v[32];
+      ptx::tmem_ld16_nowait(tq + c, *reinterpret_cast<float(*)[16]>(v));
+      ptx::tmem_ld16_nowait(tq + c + 16, *reinterpret_cast<float(*)[16]>(v + 16));
+      ptx::tmem_wait_ld();
+      const uint32_t dst = ptx::mapa(my_slot, (uint32_t)(c >> 5));
+#pragma unroll
+      for (int k = 0; k < 8; ++k)
+        ptx::st_cluster_v4(dst + 16 * k, make_uint4(__float_as_uint(v[4 * k]), __float_as_uint(v[4 * k + 1]),
+                                                    __float_as_uint(v[4 * k + 2]), __float_as_uint(v[4 * k + 3])));
+    }
+    ptx::tc_fence_before();
+    ptx::cluster_arrive();  // release: every slice delivered
+    ptx::cluster_wait();
+    // my slice: columns n0 + 32 z + lane; warp e takes rows e, e + 8, ...; splits summed in order
+    const int n = n0 + 32 * z + lane;
+#pragma unroll 1
+    for (int rr = warp - 2; rr < BM; rr += 8) {
+      const int m = m0 + rr;
+      float s = rbuf[(size_t)rr * 36 + lane];
+#pragma unroll
+      for (int z2 = 1; z2 < CR; ++z2) s += rbuf[((size_t)z2 * 128 + rr) * 36 + lane];
+      if (m < M && n < N) lstm_bwd_unit(epi, (size_t)m * N + n, s);
     }
   } else {
     // ---------------- epilogue warps 2..9: TMEM lane quadrant q = warp % 4, column half ch
@@ -745,15 +812,15 @@ int num_sms() {
 // overlaps is short next to the predecessor's drain + flush
 bool use_pdl() { return opt(OPT_PDL) == 1; }
 
-template <int BN, int AMN, int BMN, int CN = 1, int CG = 1>
+template <int BN, int AMN, int BMN, int CN = 1, int CG = 1, int CR = 1>
 cudaError_t launch_tc(const GemmPlan& p, cudaStream_t s) {
   using C = TileCfg<BN, CG>;
-  constexpr int CL = CN * CG;
+  constexpr int CL = CN * CG * CR;
   const int groups = ((p.M + BM * CG - 1) / (BM * CG)) * ((((p.N + BN - 1) / BN) + CN - 1) / CN) * p.splits;
   Epilogue e = p.epi;
-  if (p.splits > 1 || e.mode == EPI_LSTM_BWD) e.mode = EPI_SPLITK;
+  if (CR == 1 && (p.splits > 1 || e.mode == EPI_LSTM_BWD)) e.mode = EPI_SPLITK;
   cudaLaunchConfig_t cfg = {};
-  cfg.gridDim = dim3(std::min(groups, num_sms() / CL) * CL);
+  cfg.gridDim = dim3(CR > 1 ? groups : std::min(groups, num_sms() / CL) * CL);
   cfg.blockDim = dim3(320);
   cfg.dynamicSmemBytes = C::SMEM;
   cfg.stream = s;
@@ -773,13 +840,13 @@ cudaError_t launch_tc(const GemmPlan& p, cudaStream_t s) {
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, AMN, BMN, CN, CG>, p.ta, p.tb, p.M, p.N, p.K, p.kbps, p.splits,
-                            e, p.ws);
+  return cudaLaunchKernelEx(&cfg, gemm_tc_kernel<BN, AMN, BMN, CN, CG, CR>, p.ta, p.tb, p.M, p.N, p.K, p.kbps,
+                            p.splits, e, p.ws);
 }
 
-template <int BN, int AMN, int BMN, int CN = 1, int CG = 1>
+template <int BN, int AMN, int BMN, int CN = 1, int CG = 1, int CR = 1>
 cudaError_t set_attr() {
-  return cudaFuncSetAttribute(gemm_tc_kernel<BN, AMN, BMN, CN, CG>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  return cudaFuncSetAttribute(gemm_tc_kernel<BN, AMN, BMN, CN, CG, CR>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                               TileCfg<BN, CG>::SMEM);
 }
 template <int BN>
@@ -803,6 +870,8 @@ cudaError_t set_attr_bn() {
 
 template <int BN>
 cudaError_t launch_tc_bn(const GemmPlan& p, cudaStream_t s) {
+  if constexpr (BN == 256)
+    if (p.cr == 8) return launch_tc<256, 0, 1, 1, 1, 8>(p, s);
   if (p.amn == 0 && p.cg == 2) return p.bmn ? launch_tc<BN, 0, 1, 1, 2>(p, s) : launch_tc<BN, 0, 0, 1, 2>(p, s);
   if (p.amn == 1 && p.cg == 2) return p.bmn ? launch_tc<BN, 1, 1, 1, 2>(p, s) : launch_tc<BN, 1, 0, 1, 2>(p, s);
   if (p.amn == 0 && p.cn == 2) return p.bmn ? launch_tc<BN, 0, 1, 2>(p, s) : launch_tc<BN, 0, 0, 2>(p, s);
@@ -830,6 +899,7 @@ cudaError_t gemm_init() {
   cudaError_t e;
   if ((e = set_attr_bn<64>()) != cudaSuccess) return e;
   if ((e = set_attr_bn<128>()) != cudaSuccess) return e;
+  if ((e = set_attr<256, 0, 1, 1, 1, 8>()) != cudaSuccess) return e;
   return set_attr_bn<256>();
 }
 
@@ -928,6 +998,16 @@ int gemm_plan_tc(GemmPlan* p, const __half* A, long lda, int a_mn, const __half*
     if (cg != 2 || cn != 1 || bn < 128) cg = 1;
   }
   p->cg = cg;
+  // the fused cell backward at 8 K-splits of 256-wide tiles (C4's K7): the splits of a tile
+  // reduce inside an 8-CTA cluster (option k7_cluster, off by default: B200 co-schedules at
+  // most 15 such clusters of one-CTA-per-SM CTAs, tools/micro/cluster_occ.cu, and C4's K7
+  // needs 16 -- the 16th runs as a second wave; C4 step 34.3 -> 59.0 ms with it on)
+  {
+    const int tiles = ((M + BM - 1) / BM) * ((N + bn - 1) / bn);
+    if (epi.mode == EPI_LSTM_BWD && bn == 256 && splits == 8 && a_mn == 0 && b_mn == 1 && cg == 1 && cn == 1 &&
+        tiles * splits <= num_sms() && opt(OPT_K7_CLUSTER))
+      p->cr = 8;
+  }
   int r;
   if (a_mn == 0)
     r = make_tmap(&p->ta, A, (uint64_t)K, (uint64_t)M, (uint64_t)lda, BM / cn);
@@ -978,7 +1058,7 @@ cudaError_t gemm_run(const GemmPlan& p, cudaStream_t s) {
     case 128: e = launch_tc_bn<128>(p, s); break;
     default: e = launch_tc_bn<256>(p, s); break;
   }
-  if (e != cudaSuccess || (p.splits <= 1 && p.epi.mode != EPI_LSTM_BWD)) return e;
+  if (e != cudaSuccess || (p.splits <= 1 && p.epi.mode != EPI_LSTM_BWD) || p.cr > 1) return e;
   const size_t total = (size_t)p.M * p.N;
   int blocks = (int)((total + 255) / 256);
   if (blocks > 148 * 8) blocks = 148 * 8;

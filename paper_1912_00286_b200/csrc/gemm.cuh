@@ -73,6 +73,7 @@ struct GemmPlan {
   int splits = 1, kbps = 0;
   int cn = 1;      // CTAs per cluster sharing (multicasting) the A tile
   int cg = 1;      // 2 = CTA pairs (cta_group::2) on 256-row tiles
+  int cr = 1;      // 8: the fused cell backward's split-K partials reduced inside an 8-CTA cluster (DSMEM)
   Epilogue epi;
   float* ws = nullptr;
 };

@@ -522,7 +522,7 @@ int gemm(hdp_ctx* c, int tag, const void* A, long lda, int amn, const void* B, l
     r = hdp::gemm_plan_tc(&p, (const __half*)A, lda, amn, (const __half*)B, ldb, bmn, (int)M, (int)N, (int)K, ebf,
                           ws ? ws : c->ws, c->ws_floats, force_bn, force_splits);
   if (r) return fail(HDP_ERR_ARG, "gemm plan %ldx%ldx%ld: %s", M, N, K, hdp::gemm_last_error());
-  KScope ks(c, tag, p.tc && (p.splits > 1 || epi.mode == hdp::EPI_LSTM_BWD) ? 2 : 1, s);
+  KScope ks(c, tag, p.tc && p.cr == 1 && (p.splits > 1 || epi.mode == hdp::EPI_LSTM_BWD) ? 2 : 1, s);
   CK_CUDA(hdp::gemm_run(p, s));
   return HDP_OK;
 }
@@ -1251,12 +1251,12 @@ int check_desc_across_ranks(hdp_ctx* c, const hdp_model_desc& d) {
 
 // ====================================================================== options
 namespace hdp {
-int g_opt[OPT_COUNT] = {1, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 16, 1};
+int g_opt[OPT_COUNT] = {1, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 16, 1, 0};
 namespace {
 const char* const kOptNames[OPT_COUNT] = {"persistent",     "wavefront", "wavefront_fusex", "wavefront_wgrad",
                                           "wavefront_tmem", "recur_nbg", "gemm_cta_group",  "gemm_cluster_n",
                                           "pdl",            "k7_bn",     "k7_splits",       "recur_trace",
-                                          "layer_pipe",     "head_fused"};
+                                          "layer_pipe",     "head_fused",      "k7_cluster"};
 }
 int opt_find(const char* name) {
   for (int i = 0; i < OPT_COUNT; ++i)

@@ -20,6 +20,8 @@ enum OptId {
   OPT_RECUR_TRACE,       // 1: phase trace of the recurrence kernels in profile (eager) mode
   OPT_LAYER_PIPE,        // per-step path, L >= 2: layer-diagonal forward schedule in chunks of this many steps (0 = off)
   OPT_HEAD_FUSED,        // 1: fused FC head kernel (mixed mode, h_p, F_p <= 256), fixed per context at configure
+  OPT_K7_CLUSTER,        // 1: K7's 8 split-K partials reduced in an 8-CTA cluster through DSMEM (no partial planes);
+                         // off: only 15 such clusters are co-resident on B200, C4 needs 16 (measured 34.3 -> 59.0 ms)
   OPT_COUNT
 };
 

@@ -308,6 +308,29 @@ def test_head_fused_matches_unfused_and_oracle(batch, seq):
         assert abs(a["loss_gpu"] - b["loss_gpu"]) <= 1e-5 * max(1.0, abs(b["loss_gpu"]))
 
 
+@pytest.mark.parametrize("batch,seq", [(256, 3), (136, 2)])
+def test_k7_cluster_reduction_bit_identical(batch, seq):
+    """K7 with the cell backward fused into its split-K reduction: the 8 partials of a tile
+    reduced inside an 8-CTA cluster through DSMEM (option k7_cluster, off by default) sum in
+    the same split order as the reduction kernel over the global partial planes, so loss,
+    master and weights after 2 steps are bit-identical; step 0 also matches the oracle
+    (multi-step oracle bounds at C4: test_c4_beta32_ten_steps_mixed).  C4 widths
+    (h = 2048, 256-wide tiles x 8 splits = 128 CTAs), full and ragged batch."""
+    import numpy as np
+    cfg = synth.CONFIGS["C4"].with_(seq=seq)
+    out = {}
+    for flag in (1, 0):
+        with kernel_options(k7_cluster=flag):
+            out[flag] = run_parity(cfg, batch, 1, steps=2, mixed=True, keep_state=True)
+    for a, b in zip(out[1], out[0]):
+        assert a["loss_gpu"] == b["loss_gpu"]
+        assert np.array_equal(a["gpu_master"], b["gpu_master"])
+        assert np.array_equal(a["gpu_w"], b["gpu_w"])
+    r = out[1][0]
+    assert abs(r["loss_gpu"] - r["loss_ref"]) <= 1e-2 * max(1.0, abs(r["loss_ref"]))
+    assert _max(r["grad_err"][0]) <= GRAD_MIXED, r["grad_err"]
+
+
 @pytest.mark.parametrize("tc", [16, 7, 1])
 def test_layer_pipeline_bit_identical_to_sequential(tc):
     """The layer-diagonal forward schedule of the per-step path (option layer_pipe: layer
