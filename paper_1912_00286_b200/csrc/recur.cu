@@ -1078,7 +1078,8 @@ __global__ void __launch_bounds__(128, 1)
   const int role = blockIdx.y / P.nbg, grp = blockIdx.y % P.nbg;
   cta_stamp(P, 0, role);  // 0 Q1, 1 X, 2 Q0, 3 W
   if (role == 1) {
-    if (NKQ != 0)
+    // (the TMEM-A projection needs 64 + 2 h_p <= 512 columns: h_p = 208 yes, 256 no)
+    if constexpr (NKQ != 0 && 64 + NKQ * 8 <= 512)
       bwd_proj_role_ts<NC, (NKQ != 0 ? NKQ : 52)>(P, grp);
     else
       bwd_proj_role<NC>(P, grp);
@@ -1130,6 +1131,9 @@ __global__ void __launch_bounds__(128, 1)
   // 1 accumulator each; dA_t written by TMA stores from the push staging; warps 2 / 3
   // push and store (async copies from an MMA-issuing thread delay its commits)
   constexpr bool TSQ = NKQ != 0;
+  // K-steps whose A (U^T slice) lives in TMEM: all of them while 64 + 8 NKQ <= 512 columns
+  // (h_p = 208); at h_p = 256 the last NKQ - NKT K-steps read A from the SMEM copy (MN-major)
+  constexpr int NKT = TSQ ? (64 + NKQ * 8 <= 512 ? NKQ : (512 - 64) / 8) : 0;
   constexpr int NACC = TSQ ? 2 : (Bc <= 32 ? 8 : 4);
   constexpr int AC = NACC * Bc;
   constexpr uint32_t tcols = TSQ ? 512u : (AC <= 32 ? 32u : AC <= 64 ? 64u : AC <= 128 ? 128u : 256u);
@@ -1186,7 +1190,7 @@ __global__ void __launch_bounds__(128, 1)
     int off[8];
 #pragma unroll
     for (int r8 = 0; r8 < 8; ++r8) off[r8] = r8 * 128 + (((u >> 3) ^ r8) << 4) + (u & 7) * 2;
-    for (int c0 = 0; c0 < 2 * hp; c0 += 16) {
+    for (int c0 = 0; c0 < 8 * NKT; c0 += 16) {     // (K-steps >= NKT stay in sU)
       const uint8_t* base = sU + (size_t)c0 * 256;  // gate row 2 c0
       uint32_t v[16];
 #pragma unroll
@@ -1320,8 +1324,13 @@ __global__ void __launch_bounds__(128, 1)
             const int kw = k + warp;  // this warp's K-steps: warp, warp + 2, ...
             const uint64_t bd = bd0 + (uint64_t)(((kw >> 2) * Bc * 128 + (kw & 3) * 32) >> 4);
             // (A from TMEM is K-major: the MN-major bit of the SMEM variant's idesc must be clear)
-            if (ptx::elect_one_sync())
-              ptx::mma_f16_ts(dacc, tA + kw * 8, bd, ptx::idesc_f16_f32(64, Bc, 0, 0), k > 0 ? 1u : 0u);
+            if (kw < NKT) {
+              if (ptx::elect_one_sync())
+                ptx::mma_f16_ts(dacc, tA + kw * 8, bd, ptx::idesc_f16_f32(64, Bc, 0, 0), k > 0 ? 1u : 0u);
+            } else {  // A from the SMEM copy of the slice: MN-major, 8 KB per 64-row K block
+              const uint64_t ad = ptx::smem_desc_sw128(ptx::smem_u32(sU) + (kw >> 2) * 8192 + (kw & 3) * 2048, 8192, 1024);
+              if (ptx::elect_one_sync()) ptx::mma_f16(dacc, ad, bd, ptx::idesc_f16_f32(64, Bc, 1, 0), k > 0 ? 1u : 0u);
+            }
           }
           if (ptx::elect_one_sync()) ptx::mma_commit(barM);
           __syncwarp();
@@ -2404,12 +2413,15 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
 
 namespace hdp {
 
-// U^T slice in TMEM needs 64 + 2 h_p <= 512 columns (h_p = 208 yes, 256 no): instantiated for
-// 4 h_p / 16 = 52 K-steps; everything else runs the SMEM-A variant (HDP_WAVEFRONT_TS=0 forces it)
+// U^T slice in TMEM: all of it needs 64 + 2 h_p <= 512 columns (h_p = 208); at h_p = 256
+// (4 h_p / 16 = 64 K-steps) 56 K-steps come from TMEM and 8 from the SMEM copy; everything
+// else runs the SMEM-A variant (option wavefront_tmem = 0 forces it)
 template <int NC>
 const void* recur2b_fn_nk(int hp) {
   if (opt(OPT_WAVEFRONT_TMEM) == 0) return (const void*)recur2_bwd_kernel<NC, 0>;
-  return 4 * hp / 16 == 52 ? (const void*)recur2_bwd_kernel<NC, 52> : (const void*)recur2_bwd_kernel<NC, 0>;
+  return 4 * hp / 16 == 52   ? (const void*)recur2_bwd_kernel<NC, 52>
+         : 4 * hp / 16 == 64 ? (const void*)recur2_bwd_kernel<NC, 64>
+                             : (const void*)recur2_bwd_kernel<NC, 0>;
 }
 const void* recur2b_fn(int Bc, int hp) {
   return Bc == 16 ? recur2b_fn_nk<1>(hp) : Bc == 32 ? recur2b_fn_nk<2>(hp) : Bc == 48 ? recur2b_fn_nk<3>(hp)
