@@ -443,9 +443,8 @@ __global__ void embed_keys_kernel(const int32_t* __restrict__ tok, int B, int Tn
 // (ceil(log2 vocab) / 8 passes; C3's vocab 20000 -> 2).  One pass:
 //   radix_hist_kernel    per tile of RS_TILE positions, the 256-bin digit histogram,
 //                        stored bin-major: hist[bin][tile];
-//   radix_scan_kernel    exclusive scan of hist (bin-major order = global output
-//                        offset of each (bin, tile) block);
-//   radix_scatter_kernel per tile: rank of each element among the elements of its
+//   radix_scatter_kernel per tile: its (bin, tile) output offsets from the bin-major
+//                        exclusive scan of hist (computed in-block), the rank of each element among the elements of its
 //                        tile with the same digit and a smaller position (in-warp:
 //                        __match_any_sync + popc of the lower lanes; across warps:
 //                        per-warp bin counts scanned in warp order), written to
@@ -465,48 +464,42 @@ __global__ void __launch_bounds__(RS_TILE) radix_hist_kernel(const int32_t* __re
   if (threadIdx.x < 256) hist[(long)threadIdx.x * ntiles + blockIdx.x] = h[threadIdx.x];
 }
 
-__global__ void __launch_bounds__(1024) radix_scan_kernel(int32_t* __restrict__ v, int m) {
-  __shared__ int wsum[32];
-  const int tid = threadIdx.x, per = (m + 1023) / 1024;
-  const int lo = min(m, tid * per), hi = min(m, lo + per);
-  int s = 0;
-  for (int i = lo; i < hi; ++i) s += v[i];
-  // exclusive block scan of the per-thread sums
-  const int lane = tid & 31, w = tid >> 5;
-  int x = s;
-#pragma unroll
-  for (int o = 1; o < 32; o <<= 1) {
-    const int y = __shfl_up_sync(0xffffffffu, x, o);
-    if (lane >= o) x += y;
-  }
-  if (lane == 31) wsum[w] = x;
-  __syncthreads();
-  if (w == 0) {
-    int z = wsum[lane];
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, z, o);
-      if (lane >= o) z += y;
-    }
-    wsum[lane] = z;
-  }
-  __syncthreads();
-  int run = x - s + (w > 0 ? wsum[w - 1] : 0);
-  for (int i = lo; i < hi; ++i) {
-    const int c = v[i];
-    v[i] = run;
-    run += c;
-  }
-}
-
+// The scatter computes its tiles' global offsets itself (no separate scan launch): for its
+// tile and every bin, offset = (elements of all smaller bins) + (elements of this bin in
+// earlier tiles) -- the bin-major exclusive scan evaluated at (bin, tile), exact integers.
 __global__ void __launch_bounds__(RS_TILE) radix_scatter_kernel(const int32_t* __restrict__ kin,
                                                                const int32_t* __restrict__ vin, int n, int shift,
-                                                               int ntiles, const int32_t* __restrict__ offs,
+                                                               int ntiles, const int32_t* __restrict__ hist,
                                                                int32_t* __restrict__ kout,
                                                                int32_t* __restrict__ vout) {
   __shared__ int wc[RS_TILE / 32][256];
+  __shared__ int offs[256];
+  __shared__ int wsum[8];
   const int tid = threadIdx.x, lane = tid & 31, w = tid >> 5;
   for (int i = tid; i < (RS_TILE / 32) * 256; i += RS_TILE) (&wc[0][0])[i] = 0;
+  if (tid < 256) {  // bin tid: total over all tiles, and over the tiles before mine
+    const int32_t* hb = hist + (long)tid * ntiles;
+    int tot = 0, before = 0;
+    for (int j = 0; j < ntiles; ++j) {
+      const int c = hb[j];
+      tot += c;
+      if (j < (int)blockIdx.x) before += c;
+    }
+    int x = tot;  // exclusive scan of the bin totals over the 256 bins (8 warps)
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, x, o);
+      if (lane >= o) x += y;
+    }
+    if (lane == 31) wsum[w] = x;
+    offs[tid] = x - tot + before;
+  }
+  __syncthreads();
+  if (tid < 256) {
+    int add = 0;
+    for (int j = 0; j < w; ++j) add += wsum[j];
+    offs[tid] += add;
+  }
   __syncthreads();
   const int p = blockIdx.x * RS_TILE + tid;
   const bool valid = p < n;
@@ -527,7 +520,7 @@ __global__ void __launch_bounds__(RS_TILE) radix_scatter_kernel(const int32_t* _
   }
   __syncthreads();
   if (valid) {
-    const int dst = offs[(long)d * ntiles + blockIdx.x] + wc[w][d] + rank;
+    const int dst = offs[d] + wc[w][d] + rank;
     kout[dst] = key;
     vout[dst] = vin[p];
   }
@@ -544,7 +537,7 @@ __global__ void __launch_bounds__(RS_TILE) radix_scatter_kernel(const int32_t* _
 //     [first, last) of sorted positions was recorded by embed_range_kernel.
 // No atomics; load-balanced for Zipf-frequent tokens.
 constexpr int EMB_CHUNK = 32;
-constexpr int EMB_BATCH = 8;
+constexpr int EMB_BATCH = 16;  // dX rows in flight per warp (was 8: the chunk pass was latency-bound)
 
 __global__ void embed_range_kernel(const int32_t* __restrict__ keys, int n, int32_t* __restrict__ first,
                                    int32_t* __restrict__ last) {
@@ -606,38 +599,60 @@ __global__ void embed_chunk_kernel(const int32_t* __restrict__ keys, const int32
   }
 }
 
-// one warp per (vocabulary row, 32-column slice); a Zipf-frequent token spans ~200 chunk
-// partials: 16 independent chains, combined in a fixed order (deterministic)
+// one warp per vocabulary row, lane = 4 consecutive columns (Ep <= 128; wider rows loop);
+// a Zipf-frequent token spans ~200 chunk partials: 16 independent chains per column,
+// combined in a fixed order (deterministic; the per-column arithmetic of round 2's
+// warp-per-32-column-slice version, whose 4x more warps made this pass latency-bound)
 __global__ void embed_segsum_kernel(const int32_t* __restrict__ first, const int32_t* __restrict__ last, int vocab,
                                     const float* __restrict__ part, int Ep, int out_f32, void* dE) {
   constexpr int CH = 16;
-  const long w = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  const long v = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  const int slices = (Ep + 31) >> 5;
-  const long v = w / slices;
-  const int k = (int)(w % slices) * 32 + lane;
-  if (v >= vocab || k >= Ep) return;
+  if (v >= vocab) return;
   const int lo = first[v], hi = last[v];  // [0, 0) for tokens that do not occur
-  float s = 0.f;
-  if (lo < hi) {
-    float a[CH];
+  for (int k0 = 4 * lane; k0 < Ep; k0 += 128) {
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+    if (lo < hi) {
+      float a[CH][4];
 #pragma unroll
-    for (int j = 0; j < CH; ++j) a[j] = 0.f;
-    long c = ((long)lo / EMB_CHUNK + 1) * EMB_CHUNK;
-    for (; c + (CH - 1) * EMB_CHUNK < hi; c += CH * EMB_CHUNK) {
+      for (int j = 0; j < CH; ++j)
 #pragma unroll
-      for (int j = 0; j < CH; ++j) a[j] += part[(c + j * EMB_CHUNK) * Ep + k];
+        for (int q = 0; q < 4; ++q) a[j][q] = 0.f;
+      long c = ((long)lo / EMB_CHUNK + 1) * EMB_CHUNK;
+      for (; c + (CH - 1) * EMB_CHUNK < hi; c += CH * EMB_CHUNK) {
+#pragma unroll
+        for (int j = 0; j < CH; ++j) {
+          const float4 p4 = *reinterpret_cast<const float4*>(part + (c + j * EMB_CHUNK) * Ep + k0);
+          a[j][0] += p4.x;
+          a[j][1] += p4.y;
+          a[j][2] += p4.z;
+          a[j][3] += p4.w;
+        }
+      }
+#pragma unroll
+      for (int j = 0; j < CH; ++j)
+        if (c + j * EMB_CHUNK < hi) {
+          const float4 p4 = *reinterpret_cast<const float4*>(part + (c + j * EMB_CHUNK) * Ep + k0);
+          a[j][0] += p4.x;
+          a[j][1] += p4.y;
+          a[j][2] += p4.z;
+          a[j][3] += p4.w;
+        }
+#pragma unroll
+      for (int m = CH / 2; m > 0; m >>= 1)
+#pragma unroll
+        for (int j = 0; j < m; ++j)
+#pragma unroll
+          for (int q = 0; q < 4; ++q) a[j][q] += a[j + m][q];
+      const float4 p0 = *reinterpret_cast<const float4*>(part + (long)lo * Ep + k0);
+      s[0] = p0.x + a[0][0];
+      s[1] = p0.y + a[0][1];
+      s[2] = p0.z + a[0][2];
+      s[3] = p0.w + a[0][3];
     }
 #pragma unroll
-    for (int j = 0; j < CH; ++j)
-      if (c + j * EMB_CHUNK < hi) a[j] += part[(c + j * EMB_CHUNK) * Ep + k];
-#pragma unroll
-    for (int m = CH / 2; m > 0; m >>= 1)
-#pragma unroll
-      for (int j = 0; j < m; ++j) a[j] += a[j + m];
-    s = part[(long)lo * Ep + k] + a[0];
+    for (int q = 0; q < 4; ++q) st_et(dE, v * Ep + k0 + q, s[q], out_f32);  // R12
   }
-  st_et(dE, v * Ep + k, s, out_f32);  // R12
 }
 
 // element-type dispatch of the launchers: et = ET_F16 (0), ET_F32 (1) or ET_BF16 (2)
@@ -818,7 +833,6 @@ cudaError_t launch_embed_backward(const int32_t* tok, int B, int T, int vocab, c
   int32_t *ka = keys_in, *va = vals_in, *kb = keys_out, *vb = vals_out;
   for (int shift = 0; shift < bits; shift += 8) {
     radix_hist_kernel<<<ntiles, RS_TILE, 0, s>>>(ka, n, shift, ntiles, hist);
-    radix_scan_kernel<<<1, 1024, 0, s>>>(hist, 256 * ntiles);
     radix_scatter_kernel<<<ntiles, RS_TILE, 0, s>>>(ka, va, n, shift, ntiles, hist, kb, vb);
     std::swap(ka, kb);
     std::swap(va, vb);
@@ -829,7 +843,7 @@ cudaError_t launch_embed_backward(const int32_t* tok, int B, int T, int vocab, c
   embed_range_kernel<<<(n + 255) / 256, 256, 0, s>>>(ka, n, range, range + vocab);
   const long cw = ((long)n + EMB_CHUNK - 1) / EMB_CHUNK * 32;
   embed_chunk_kernel<<<(int)((cw + 255) / 256), 256, 0, s>>>(ka, va, n, dX0, Ep, part);
-  const long threads = (long)vocab * ((Ep + 31) / 32) * 32;
+  const long threads = (long)vocab * 32;
   embed_segsum_kernel<<<(int)((threads + 255) / 256), 256, 0, s>>>(range, range + vocab, vocab, part, Ep, out_f32,
                                                                    dE);
   return cudaGetLastError();
