@@ -1966,14 +1966,17 @@ int hdp_grad_average_update(hdp_ctx* c, int epoch, void* stream, int* nonfinite_
     KScope ks_(c, HDP_K_UPDATE, 1, cs);
     CK_CUDA(hdp::launch_increment(c->drop_step(), cs));
   }
-  CK_CUDA(cudaMemcpyAsync(c->count_host, count_src, sizeof(int), cudaMemcpyDeviceToHost, cs));
-  if (c->d.vocab > 0) {  // out-of-range token ids counted by this step's forward passes
+  if (c->d.vocab > 0) {  // out-of-range token ids counted by this step's forward passes (the
+    // next forward counts into the same word: read and cleared before it may start)
     CK_CUDA(cudaMemcpyAsync(c->count_host + 1, c->status + 16, sizeof(int), cudaMemcpyDeviceToHost, cs));
     CK_CUDA(cudaMemsetAsync(c->status + 16, 0, sizeof(int), cs));
   }
-  CK_CUDA(cudaEventRecord(c->ev_count, cs));
   CK_CUDA(cudaEventRecord(c->ev_done, cs));
   CK_CUDA(cudaStreamWaitEvent(s, c->ev_done, 0));  // next forward sees the new weights
+  // the non-finite count's read-back stays off the caller's path (its source is written only
+  // by the update / exchange kernels, i.e. after the next call's reset on this stream)
+  CK_CUDA(cudaMemcpyAsync(c->count_host, count_src, sizeof(int), cudaMemcpyDeviceToHost, cs));
+  CK_CUDA(cudaEventRecord(c->ev_count, cs));
   for (auto& st : c->st) st.bwd = false;
   if (nonfinite_host) {
     CK_CUDA(cudaEventSynchronize(c->ev_count));
