@@ -617,7 +617,15 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
   const long hs_layer = (long)(T + 1) * B * hp;  // elements per layer in Hs (actual B, T)
   const long c_layer = (long)T * B * hp;
   const long g_layer = (long)T * B * 4 * hp;
-  for (int l = 0; l < L; ++l) CK_CUDA(cudaMemsetAsync(S.Hs + l * hs_layer * e, 0, B * hp * e, s));
+  // h_{-1} = 0 of every layer (row 0 of its Hs block): zeroed by the input-packing launch
+  // (row bytes B h_p e and the layer stride are multiples of 16 B: h_p is a multiple of 16)
+  hdp::ZeroRows zr;
+  zr.base = reinterpret_cast<uint4*>(S.Hs);
+  zr.stride = hs_layer * e / 16;
+  zr.nvec = (long)B * hp * e / 16;
+  zr.count = (int)L;
+  if (d.vocab > 0)
+    for (int l = 0; l < L; ++l) CK_CUDA(cudaMemsetAsync(S.Hs + l * hs_layer * e, 0, B * hp * e, s));
   if (d.vocab > 0)
     {
       KScope ks_(c, HDP_K_INPUT, 1, s);
@@ -627,7 +635,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
   else
     {
       KScope ks_(c, HDP_K_INPUT, 1, s);
-      CK_CUDA(hdp::launch_pack_input(S.stage_x, et, B, T, d.input_dim, (int)c->Ip0, S.X0, et, s));
+      CK_CUDA(hdp::launch_pack_input(S.stage_x, et, B, T, d.input_dim, (int)c->Ip0, S.X0, et, s, zr));
     }
   char nm[16];
   // Layer-diagonal schedule of the per-step path (NEXT-1 at C4 scale; PAPER.md:82 BPTT over a

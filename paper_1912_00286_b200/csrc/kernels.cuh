@@ -51,8 +51,13 @@ cudaError_t launch_loss_scale_update(int* st, float* alpha, int interval, float 
 
 // ---------------------------------------------------------------- input
 // x [B][T][I] (fp16 or fp32)  ->  X0 [T][B][Ip] (time-major, zero padded)
+struct ZeroRows {  // regions zeroed by the input-packing launch (16-B vectors)
+  uint4* base = nullptr;
+  long stride = 0, nvec = 0;
+  int count = 0;
+};
 cudaError_t launch_pack_input(const void* x, int x_f32, int B, int T, int I, int Ip, void* X0, int f32,
-                              cudaStream_t s);
+                              cudaStream_t s, ZeroRows z = ZeroRows());
 // tokens [B][T] -> X0[t][b][:] = E[tok[b][t]][:]  (K10 gather); a token outside
 // [0, vocab) reads row 0 and increments *bad
 cudaError_t launch_embed_gather(const int32_t* tok, int B, int T, const void* E, int Ep, void* X0, int f32,

@@ -75,8 +75,18 @@ __device__ __forceinline__ float4 ld4(const __nv_bfloat16* p) {
 }
 
 // ---------------------------------------------------------------- input
+// the forward's h_{-1} rows (one per layer, `count` regions of `nvec` 16-B vectors, `stride`
+// vectors apart) zeroed by the input-packing launch instead of one memset node per layer
+__device__ __forceinline__ void zero_rows(const ZeroRows& z) {
+  const long total = (long)z.count * z.nvec;
+  for (long i = blockIdx.x * (long)blockDim.x + threadIdx.x; i < total; i += (long)gridDim.x * blockDim.x)
+    z.base[(i / z.nvec) * z.stride + i % z.nvec] = make_uint4(0u, 0u, 0u, 0u);
+}
+
 template <typename XT, typename T>
-__global__ void pack_input_kernel(const XT* __restrict__ x, int B, int Tn, int I, int Ip, T* __restrict__ X0) {
+__global__ void pack_input_kernel(const XT* __restrict__ x, int B, int Tn, int I, int Ip, T* __restrict__ X0,
+                                  ZeroRows z) {
+  zero_rows(z);
   const long total = (long)Tn * B * Ip;
   for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
     const int k = (int)(idx % Ip);
@@ -101,7 +111,9 @@ __global__ void drop_mask_kernel(const __half* __restrict__ h, __half* __restric
 
 // same-type rows with I == Ip and 16-B aligned rows: one warp per (t, b) row, 16-B vectors
 // (a pure row permutation [B][T] -> [T][B]; C4 moves 134 MB per step through here)
-__global__ void pack_rows_kernel(const uint4* __restrict__ x, int B, int Tn, int vrow, uint4* __restrict__ X0) {
+__global__ void pack_rows_kernel(const uint4* __restrict__ x, int B, int Tn, int vrow, uint4* __restrict__ X0,
+                                 ZeroRows z) {
+  zero_rows(z);
   const long w = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
   if (w >= (long)Tn * B) return;
@@ -680,26 +692,26 @@ inline int grid_for(long n, int threads, int cap = 148 * 16) {
 
 // ============================================================== launchers
 cudaError_t launch_pack_input(const void* x, int x_f32, int B, int T, int I, int Ip, void* X0, int f32,
-                              cudaStream_t s) {
+                              cudaStream_t s, ZeroRows z) {
   const long n = (long)T * B * Ip;
   const int g = grid_for(n, 256);
   const int esz = f32 == ET_F32 ? 4 : 2;
   if (I == Ip && x_f32 == f32 && (I * esz) % 16 == 0 && !(reinterpret_cast<uintptr_t>(x) & 15) &&
       !(reinterpret_cast<uintptr_t>(X0) & 15)) {
     const long threads = (long)T * B * 32;
-    pack_rows_kernel<<<(int)((threads + 255) / 256), 256, 0, s>>>((const uint4*)x, B, T, I * esz / 16, (uint4*)X0);
+    pack_rows_kernel<<<(int)((threads + 255) / 256), 256, 0, s>>>((const uint4*)x, B, T, I * esz / 16, (uint4*)X0, z);
     return cudaGetLastError();
   }
   if (f32 == ET_BF16) {
     if (x_f32 != ET_BF16) return cudaErrorInvalidValue;
     pack_input_kernel<__nv_bfloat16, __nv_bfloat16><<<g, 256, 0, s>>>((const __nv_bfloat16*)x, B, T, I, Ip,
-                                                                      (__nv_bfloat16*)X0);
+                                                                      (__nv_bfloat16*)X0, z);
   } else if (f32) {
-    if (x_f32) pack_input_kernel<float, float><<<g, 256, 0, s>>>((const float*)x, B, T, I, Ip, (float*)X0);
-    else pack_input_kernel<__half, float><<<g, 256, 0, s>>>((const __half*)x, B, T, I, Ip, (float*)X0);
+    if (x_f32) pack_input_kernel<float, float><<<g, 256, 0, s>>>((const float*)x, B, T, I, Ip, (float*)X0, z);
+    else pack_input_kernel<__half, float><<<g, 256, 0, s>>>((const __half*)x, B, T, I, Ip, (float*)X0, z);
   } else {
-    if (x_f32) pack_input_kernel<float, __half><<<g, 256, 0, s>>>((const float*)x, B, T, I, Ip, (__half*)X0);
-    else pack_input_kernel<__half, __half><<<g, 256, 0, s>>>((const __half*)x, B, T, I, Ip, (__half*)X0);
+    if (x_f32) pack_input_kernel<float, __half><<<g, 256, 0, s>>>((const float*)x, B, T, I, Ip, (__half*)X0, z);
+    else pack_input_kernel<__half, __half><<<g, 256, 0, s>>>((const __half*)x, B, T, I, Ip, (__half*)X0, z);
   }
   return cudaGetLastError();
 }
