@@ -378,7 +378,7 @@ void carve(hdp_ctx* c, char* base) {
   c->w = cv.take(P * c->esz);
   c->master = (float*)cv.take(c->M_own * 4);
   c->s1 = (float*)cv.take(c->M_own * 4);
-  c->s2 = (float*)cv.take(d.optimizer == HDP_OPT_ADAM ? c->M_own * 4 : 0);
+  c->s2 = d.optimizer == HDP_OPT_ADAM ? (float*)cv.take(c->M_own * 4) : nullptr;  // Adam's v only
   c->grads = cv.take((size_t)c->nslots * P * c->gsz);
   // bucket bi received at its own offset (task 0: every rank's whole vector, [world][P] on rank 0)
   c->recv = cv.take(c->world > 1 ? (c->task0 ? (c->rank == 0 ? (size_t)c->world : 0) : 1) * c->P * c->gsz : 0);
