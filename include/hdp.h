@@ -288,7 +288,7 @@ int hdp_grad_average_update(hdp_ctx* ctx, int epoch, void* stream, int* nonfinit
  * call are kept -- a ctx passed here has its graphs dropped): "persistent",
  *   "wavefront", "wavefront_fusex", "wavefront_wgrad", "wavefront_tmem", "recur_nbg",
  *   "gemm_cta_group", "gemm_cluster_n", "pdl", "k7_bn", "k7_splits",
- *   "recur_trace", "layer_pipe", "head_fused" (integers; see csrc/options.h;
+ *   "recur_trace", "layer_pipe", "head_fused", "k7_cluster" (integers; see csrc/options.h;
  *   "head_fused" applies to contexts configured after the change).  They choose between implementations
  *   of the same arithmetic (ablations, tuning); the defaults are the measured best.
  * Errors: unknown name, value out of range -> HDP_ERR_ARG.                      */
@@ -323,6 +323,14 @@ int hdp_profile(hdp_ctx* ctx, int enable);
 /* Synchronises; accumulated milliseconds and event-pair counts per class
  * (arrays of HDP_K_NTAGS, nullable); reset != 0 clears the totals.        */
 int hdp_profile_read(hdp_ctx* ctx, double* ms, long long* launches, int reset);
+/* Synchronises; the event-pair records collected since the last hdp_profile_read
+ * as a timeline (the substitute for an nsys trace, which this image lacks): for
+ * record i < min(*n, cap) its class tags[i], stream lanes[i] (0 the caller's,
+ * 1 exchange / update, 2 the fused head's side stream, 3 + l the layer pipeline's
+ * stream of layer l) and start / end t0_ms[i] / t1_ms[i] relative to the first
+ * record's start.  *n = number of records.  Does not clear them.
+ * Errors: null n, cap > 0 with a null array -> HDP_ERR_ARG.               */
+int hdp_profile_timeline(hdp_ctx* ctx, int* tags, int* lanes, double* t0_ms, double* t1_ms, int cap, int* n);
 /* Number of this library's kernels enqueued so far (graph launches count
  * their captured kernels; NCCL's and cub's kernels are not counted).     */
 long long hdp_kernel_launches(const hdp_ctx* ctx);

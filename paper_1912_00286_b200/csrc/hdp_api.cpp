@@ -194,6 +194,7 @@ struct hdp_ctx {
     int tag;
     cudaEvent_t a, b;
     int nk;
+    int lane = 0;  // stream: 0 caller's, 1 exchange / update, 2 head side stream, 3 + l layer pipeline
   };
   std::vector<ProfRec> precs;
   std::vector<cudaEvent_t> evpool;
@@ -480,7 +481,13 @@ struct KScope {
     if (c->prof) {
       cudaEvent_t b = prof_event(c);
       cudaEventRecord(b, s);
-      c->precs.push_back({tag, a, b, nk});
+      int lane = 0;
+      if (s == c->comm_stream) lane = 1;
+      else if (s == c->hstr) lane = 2;
+      else
+        for (size_t l = 0; l < c->lstr.size(); ++l)
+          if (s == c->lstr[l]) lane = 3 + (int)l;
+      c->precs.push_back({tag, a, b, nk, lane});
     }
   }
 };
@@ -2092,6 +2099,26 @@ int hdp_profile_read(hdp_ctx* c, double* ms, long long* launches, int reset) {
       c->prof_ms[i] = 0;
       c->prof_n[i] = 0;
     }
+  }
+  return HDP_OK;
+}
+
+int hdp_profile_timeline(hdp_ctx* c, int* tags, int* lanes, double* t0_ms, double* t1_ms, int cap, int* n) {
+  CK(check_ready(c));
+  if (!n || cap < 0 || (cap > 0 && (!tags || !lanes || !t0_ms || !t1_ms))) return fail(HDP_ERR_ARG, "bad arguments");
+  CK_CUDA(cudaDeviceSynchronize());
+  *n = (int)c->precs.size();
+  if (c->precs.empty()) return HDP_OK;
+  const cudaEvent_t ref = c->precs[0].a;
+  for (int i = 0; i < *n && i < cap; ++i) {
+    const auto& r = c->precs[i];
+    float a = 0.f, b = 0.f;
+    CK_CUDA(cudaEventElapsedTime(&a, ref, r.a));
+    CK_CUDA(cudaEventElapsedTime(&b, ref, r.b));
+    tags[i] = r.tag;
+    lanes[i] = r.lane;
+    t0_ms[i] = a;
+    t1_ms[i] = b;
   }
   return HDP_OK;
 }

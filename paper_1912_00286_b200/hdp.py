@@ -31,7 +31,7 @@ EXPORTED = [
     "hdp_loss_scale_state", "hdp_lstm_forward",
     "hdp_lstm_backward", "hdp_grad_average_update", "hdp_weights_ptr", "hdp_grads_ptr", "hdp_master_ptr",
     "hdp_fused_avg_update", "hdp_gemm_f16", "hdp_gemm_f32", "hdp_profile", "hdp_profile_read",
-    "hdp_kernel_launches", "hdp_debug_buffer", "hdp_set_option", "hdp_get_option", "hdp_partial_state",
+    "hdp_kernel_launches", "hdp_debug_buffer", "hdp_set_option", "hdp_get_option", "hdp_partial_state", "hdp_profile_timeline",
 ]
 NTAGS = 15
 
@@ -104,6 +104,7 @@ def _load():
         "hdp_set_option": ([vp, C.c_char_p, d], i),
         "hdp_partial_state": ([vp, C.POINTER(C.c_uint), C.POINTER(i)], i),
         "hdp_get_option": ([C.c_char_p, C.POINTER(d)], i),
+        "hdp_profile_timeline": ([vp, C.POINTER(i), C.POINTER(i), C.POINTER(d), C.POINTER(d), i, C.POINTER(i)], i),
     }
     for name, (args, res) in sig.items():
         fn = getattr(lib, name)
@@ -268,6 +269,15 @@ def get_option(name: str) -> int:
     v = C.c_double()
     _ck(_lib.hdp_get_option(name.encode(), C.byref(v)))
     return int(v.value)
+
+
+def profile_timeline(ctx, cap=100000):
+    """hdp_profile_timeline: [(tag, lane, t0_ms, t1_ms)] of the profiled launches so far."""
+    tags, lanes = (C.c_int * cap)(), (C.c_int * cap)()
+    t0, t1 = (C.c_double * cap)(), (C.c_double * cap)()
+    n = C.c_int()
+    _ck(_lib.hdp_profile_timeline(ctx, tags, lanes, t0, t1, cap, C.byref(n)))
+    return [(tags[i], lanes[i], t0[i], t1[i]) for i in range(min(n.value, cap))]
 
 
 def partial_state(ctx):
