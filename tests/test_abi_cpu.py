@@ -61,6 +61,27 @@ def test_host_argument_errors(hdp):
                           None) == hdp.HDP_ERR_ARG
 
 
+def test_kernel_options_round_trip(hdp):
+    """hdp_set_option / hdp_get_option on the process-wide switches (no context, no GPU):
+    the Python defaults table matches the library's, values round-trip, bad names and
+    non-integers are rejected."""
+    L = hdp.lib()
+    for name, default in hdp.KERNEL_OPTION_DEFAULTS.items():
+        assert hdp.get_option(name) == default, name
+    hdp.set_option(None, "layer_pipe", 5)
+    try:
+        assert hdp.get_option("layer_pipe") == 5
+    finally:
+        hdp.set_option(None, "layer_pipe", hdp.KERNEL_OPTION_DEFAULTS["layer_pipe"])
+    v = ctypes.c_double()
+    assert L.hdp_get_option(b"no_such_option", ctypes.byref(v)) == hdp.HDP_ERR_ARG
+    assert L.hdp_get_option(b"layer_pipe", None) == hdp.HDP_ERR_ARG
+    assert L.hdp_set_option(None, b"no_such_option", ctypes.c_double(1.0)) == hdp.HDP_ERR_ARG
+    assert L.hdp_set_option(None, b"layer_pipe", ctypes.c_double(1.5)) == hdp.HDP_ERR_ARG
+    n = ctypes.c_int()
+    assert L.hdp_profile_timeline(None, None, None, None, None, 0, ctypes.byref(n)) < 0  # no context
+
+
 def test_no_cpu_fallback_in_product_path():
     # the product package never imports the oracle
     pkg = os.path.join(ROOT, "paper_1912_00286_b200")
