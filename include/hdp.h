@@ -22,9 +22,14 @@
  *    calls are asynchronous and stream-ordered on it.
  *  - Device memory is owned by the caller: hdp_configure reports the arena
  *    size, the caller allocates it (256-byte aligned) and hdp_bind()s it.
- *    The library owns only its NCCL communicator, two internal streams,
- *    events and captured CUDA graphs (freed by hdp_destroy), plus transient
- *    staging buffers inside hdp_load_params / hdp_gather_master.
+ *    The library owns (and hdp_destroy frees) its NCCL communicator, its
+ *    internal streams (capture, exchange, the fused head's side stream, one
+ *    per layer for the layer-diagonal forward), events and captured CUDA
+ *    graphs; at world > 1 with the NVLink exchange the IPC-shared gradient /
+ *    weight / flag windows it allocates (peers map them, so they cannot live
+ *    in the caller's arena); the phase-trace buffer when that debug option is
+ *    used; plus transient staging buffers inside hdp_load_params /
+ *    hdp_gather_master.
  *  - One context per process = one rank = one GPU.  A context is not
  *    thread-safe.  Every rank must make the same sequence of calls with the
  *    same B, T and epoch (NCCL's rule, and the paper's lock-step, :104).
