@@ -1134,7 +1134,13 @@ __global__ void __launch_bounds__(128, 1)
   // K-steps whose A (U^T slice) lives in TMEM: all of them while 64 + 8 NKQ <= 512 columns
   // (h_p = 208); at h_p = 256 the last NKQ - NKT K-steps read A from the SMEM copy (MN-major)
   constexpr int NKT = TSQ ? (64 + NKQ * 8 <= 512 ? NKQ : (512 - 64) / 8) : 0;
-  constexpr int NACC = TSQ ? 2 : (Bc <= 32 ? 8 : 4);
+  // TSQ accumulators: the 2 issuing warps alternate over QACC / 2 accumulators each
+  // (QACC * Bc <= 64 columns: tA at 64).  Measured at C2: 4 accumulators (13-MMA chains)
+  // leave the step's MMA phase at ~1.0 us like 2 (26-MMA chains) -- the chain length is
+  // not what separates it from the 0.38 us of tools/micro/mma_floor.cu -- so 2.
+  constexpr int QACC = 2;
+  constexpr int NACC = TSQ ? QACC : (Bc <= 32 ? 8 : 4);
+  static_assert(!TSQ || QACC * Bc <= 64, "TSQ accumulators must stay below the TMEM A slice");
   constexpr int AC = NACC * Bc;
   constexpr uint32_t tcols = TSQ ? 512u : (AC <= 32 ? 32u : AC <= 64 ? 64u : AC <= 128 ? 128u : 256u);
   constexpr int NISQ = TSQ ? 2 : 4;
@@ -1318,18 +1324,19 @@ __global__ void __launch_bounds__(128, 1)
           ptx::tc_fence_after();
           if (tr) trace[t * 5 + 1] = ptx::globaltimer_ns();
           const uint64_t bd0 = ptx::smem_desc_sw128(sA_addr + p * abuf, 0, 1024);
-          const uint32_t dacc = tbase + warp * Bc;
 #pragma unroll
           for (int k = 0; k < (TSQ ? NKQ : 1); k += 2) {
             const int kw = k + warp;  // this warp's K-steps: warp, warp + 2, ...
+            const int slot = (k >> 1) % (QACC / 2);  // this warp's accumulators round-robin
+            const uint32_t dacc = tbase + (warp + 2 * slot) * Bc;
+            const uint32_t acc = (k >> 1) >= QACC / 2 ? 1u : 0u;
             const uint64_t bd = bd0 + (uint64_t)(((kw >> 2) * Bc * 128 + (kw & 3) * 32) >> 4);
             // (A from TMEM is K-major: the MN-major bit of the SMEM variant's idesc must be clear)
             if (kw < NKT) {
-              if (ptx::elect_one_sync())
-                ptx::mma_f16_ts(dacc, tA + kw * 8, bd, ptx::idesc_f16_f32(64, Bc, 0, 0), k > 0 ? 1u : 0u);
+              if (ptx::elect_one_sync()) ptx::mma_f16_ts(dacc, tA + kw * 8, bd, ptx::idesc_f16_f32(64, Bc, 0, 0), acc);
             } else {  // A from the SMEM copy of the slice: MN-major, 8 KB per 64-row K block
               const uint64_t ad = ptx::smem_desc_sw128(ptx::smem_u32(sU) + (kw >> 2) * 8192 + (kw & 3) * 2048, 8192, 1024);
-              if (ptx::elect_one_sync()) ptx::mma_f16(dacc, ad, bd, ptx::idesc_f16_f32(64, Bc, 1, 0), k > 0 ? 1u : 0u);
+              if (ptx::elect_one_sync()) ptx::mma_f16(dacc, ad, bd, ptx::idesc_f16_f32(64, Bc, 1, 0), acc);
             }
           }
           if (ptx::elect_one_sync()) ptx::mma_commit(barM);
@@ -2418,10 +2425,15 @@ namespace hdp {
 // else runs the SMEM-A variant (option wavefront_tmem = 0 forces it)
 template <int NC>
 const void* recur2b_fn_nk(int hp) {
-  if (opt(OPT_WAVEFRONT_TMEM) == 0) return (const void*)recur2_bwd_kernel<NC, 0>;
-  return 4 * hp / 16 == 52   ? (const void*)recur2_bwd_kernel<NC, 52>
-         : 4 * hp / 16 == 64 ? (const void*)recur2_bwd_kernel<NC, 64>
-                             : (const void*)recur2_bwd_kernel<NC, 0>;
+  // (TMEM-A layout: the accumulators of Bc = 16 NC columns must fit below the slice at column 64)
+  if constexpr (NC > 2) {
+    return (void)hp, (const void*)recur2_bwd_kernel<NC, 0>;
+  } else {
+    if (opt(OPT_WAVEFRONT_TMEM) == 0) return (const void*)recur2_bwd_kernel<NC, 0>;
+    return 4 * hp / 16 == 52   ? (const void*)recur2_bwd_kernel<NC, 52>
+           : 4 * hp / 16 == 64 ? (const void*)recur2_bwd_kernel<NC, 64>
+                               : (const void*)recur2_bwd_kernel<NC, 0>;
+  }
 }
 const void* recur2b_fn(int Bc, int hp) {
   return Bc == 16 ? recur2b_fn_nk<1>(hp) : Bc == 32 ? recur2b_fn_nk<2>(hp) : Bc == 48 ? recur2b_fn_nk<3>(hp)
