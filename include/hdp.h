@@ -293,7 +293,7 @@ int hdp_grad_average_update(hdp_ctx* ctx, int epoch, void* stream, int* nonfinit
  * call are kept -- a ctx passed here has its graphs dropped): "persistent",
  *   "wavefront", "wavefront_fusex", "wavefront_wgrad", "wavefront_tmem", "recur_nbg",
  *   "gemm_cta_group", "gemm_cluster_n", "pdl", "k7_bn", "k7_splits",
- *   "recur_trace", "layer_pipe", "head_fused", "k7_cluster" (integers; see csrc/options.h;
+ *   "recur_trace", "layer_pipe", "head_fused", "k7_cluster", "fwd_pdl" (integers; see csrc/options.h;
  *   "head_fused" applies to contexts configured after the change).  They choose between implementations
  *   of the same arithmetic (ablations, tuning); the defaults are the measured best.
  * Errors: unknown name, value out of range -> HDP_ERR_ARG.                      */

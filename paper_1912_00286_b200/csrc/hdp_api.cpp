@@ -788,6 +788,7 @@ int enqueue_forward(hdp_ctx* c, int si, int B, int T, cudaStream_t s) {
     ha.inv_terms = 1.f / (float)rows;
     ha.alpha_dev = c->dyn_alpha();
     ha.trace = trace_buffer(c, (size_t)hdp::head_fused_grid((int)rows) * 8);
+    ha.pdl = hdp::opt(hdp::OPT_FWD_PDL) == 1;
     {
       KScope ks_(c, HDP_K_HEAD_FWD, 1, s);
       CK_CUDA(hdp::launch_head_fused(ha, s));
@@ -1266,12 +1267,13 @@ int check_desc_across_ranks(hdp_ctx* c, const hdp_model_desc& d) {
 
 // ====================================================================== options
 namespace hdp {
-int g_opt[OPT_COUNT] = {1, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 16, 1, 0};
+int g_opt[OPT_COUNT] = {1, 1, 1, 1, 1, 0, 0, 0, 0, 0, 0, 0, 16, 1, 0, 0};
 namespace {
 const char* const kOptNames[OPT_COUNT] = {"persistent",     "wavefront", "wavefront_fusex", "wavefront_wgrad",
                                           "wavefront_tmem", "recur_nbg", "gemm_cta_group",  "gemm_cluster_n",
                                           "pdl",            "k7_bn",     "k7_splits",       "recur_trace",
-                                          "layer_pipe",     "head_fused",      "k7_cluster"};
+                                          "layer_pipe",     "head_fused",      "k7_cluster",
+                                          "fwd_pdl"};
 }
 int opt_find(const char* name) {
   for (int i = 0; i < OPT_COUNT; ++i)

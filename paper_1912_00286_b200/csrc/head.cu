@@ -117,17 +117,16 @@ __global__ void __launch_bounds__(320, 1)
   const uint32_t tZ = tbase, tD = tbase + 256;
   unsigned long long* tr = a.trace ? a.trace + (size_t)blockIdx.x * 8 : nullptr;
   if (tr && threadIdx.x == 0) tr[0] = ptx::globaltimer_ns();
-  ptx::griddep_wait();
-  ptx::griddep_launch();
 
   if (warp == 0) {
     if (lane == 0) {
       // ---------------- TMA: H tile (K-major A) and all of F (K-major B of z = H F^T)
       ptx::mbar_arrive_expect_tx(bar_ld, nkH * (KB_BYTES + Fp * 128));
-      for (int kb = 0; kb < nkH; ++kb) {
-        ptx::tma_load_2d(sT + kb * KB_BYTES, &tmH, bar_ld, kb * 64, m0);
-        ptx::tma_load_2d(sF + kb * Fp * 128, &tmF, bar_ld, kb * 64, 0);
-      }
+      for (int kb = 0; kb < nkH; ++kb) ptx::tma_load_2d(sF + kb * Fp * 128, &tmF, bar_ld, kb * 64, 0);
+      // (PDL) only H is the previous kernel's output: F and the setup above overlap its tail;
+      // everything else this launch reads was written before the forward began
+      ptx::griddep_wait();
+      for (int kb = 0; kb < nkH; ++kb) ptx::tma_load_2d(sT + kb * KB_BYTES, &tmH, bar_ld, kb * 64, m0);
       // ---------------- z = H F^T: M = 128, N = Fp, K = hp
       ptx::mbar_wait(bar_ld, 0);
       ptx::tc_fence_after();
@@ -349,8 +348,17 @@ cudaError_t launch_head_fused(const HeadFusedArgs& a, cudaStream_t s) {
     if (e != cudaSuccess) return e;
     attr = true;
   }
-  head_fused_kernel<<<head_fused_grid(a.rows), 320, HeadSmem::BYTES, s>>>(mH, mF, mDz, a);
-  return cudaGetLastError();
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(head_fused_grid(a.rows));
+  cfg.blockDim = dim3(320);
+  cfg.dynamicSmemBytes = HeadSmem::BYTES;
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  at[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = at;
+  cfg.numAttrs = a.pdl ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, head_fused_kernel, mH, mF, mDz, a);
 }
 
 }  // namespace hdp

@@ -27,6 +27,7 @@ struct HeadFusedArgs {
   float alpha = 10.f, inv_terms = 1.f;
   const float* alpha_dev = nullptr;  // dynamic loss scaling: device alpha (nullable)
   unsigned long long* trace = nullptr;  // phase trace (option recur_trace): [grid][8] %globaltimer
+  int pdl = 0;  // launched as a programmatic dependent of the previous kernel (only H waits for it)
 };
 
 // Whether the fused kernel covers this shape (fp16 mixed mode only; hp, Fp <= 256).

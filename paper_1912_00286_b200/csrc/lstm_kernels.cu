@@ -86,6 +86,7 @@ __device__ __forceinline__ void zero_rows(const ZeroRows& z) {
 template <typename XT, typename T>
 __global__ void pack_input_kernel(const XT* __restrict__ x, int B, int Tn, int I, int Ip, T* __restrict__ X0,
                                   ZeroRows z) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");  // (PDL) the forward wavefront's prologue may start
   zero_rows(z);
   const long total = (long)Tn * B * Ip;
   for (long idx = blockIdx.x * (long)blockDim.x + threadIdx.x; idx < total; idx += (long)gridDim.x * blockDim.x) {
@@ -113,6 +114,7 @@ __global__ void drop_mask_kernel(const __half* __restrict__ h, __half* __restric
 // (a pure row permutation [B][T] -> [T][B]; C4 moves 134 MB per step through here)
 __global__ void pack_rows_kernel(const uint4* __restrict__ x, int B, int Tn, int vrow, uint4* __restrict__ X0,
                                  ZeroRows z) {
+  asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
   zero_rows(z);
   const long w = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;

@@ -22,6 +22,9 @@ enum OptId {
   OPT_HEAD_FUSED,        // 1: fused FC head kernel (mixed mode, h_p, F_p <= 256), fixed per context at configure
   OPT_K7_CLUSTER,        // 1: K7's 8 split-K partials reduced in an 8-CTA cluster through DSMEM (no partial planes);
                          // off: only 15 such clusters are co-resident on B200, C4 needs 16 (measured 34.3 -> 59.0 ms)
+  OPT_FWD_PDL,           // 1: programmatic dependent launch along the forward's input packing -> forward
+                         // wavefront -> fused head (each one's prologue overlaps its predecessor's tail);
+                         // off: measured neutral at C2 (0.802 vs 0.803 ms/step), parity-tested on
   OPT_COUNT
 };
 

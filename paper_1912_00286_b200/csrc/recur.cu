@@ -1533,7 +1533,7 @@ size_t bwd_cl_smem(int hp, int Bc) {
 }
 
 cudaError_t launch_cluster(const void* fn, dim3 grid, dim3 block, size_t smem, int cluster_x, cudaStream_t s,
-                           void** args) {
+                           void** args, bool pdl = false) {
   cudaError_t e = cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (e != cudaSuccess) return e;
   cudaLaunchConfig_t cfg = {};
@@ -1541,13 +1541,15 @@ cudaError_t launch_cluster(const void* fn, dim3 grid, dim3 block, size_t smem, i
   cfg.blockDim = block;
   cfg.dynamicSmemBytes = smem;
   cfg.stream = s;
-  cudaLaunchAttribute at[1];
+  cudaLaunchAttribute at[2];
   at[0].id = cudaLaunchAttributeClusterDimension;
   at[0].val.clusterDim.x = cluster_x;
   at[0].val.clusterDim.y = 1;
   at[0].val.clusterDim.z = 1;
+  at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;  // (the kernel griddep-waits before its inputs)
+  at[1].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = at;
-  cfg.numAttrs = 1;
+  cfg.numAttrs = pdl ? 2 : 1;
   return cudaLaunchKernelExC(&cfg, fn, args);
 }
 
@@ -1773,6 +1775,10 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
   __syncthreads();
   ptx::tc_fence_after();
   if (threadIdx.x == 0) {
+    // (PDL, option fwd_pdl) everything above reads weights only; the activations this
+    // launch reads (x_t, G_x) were written by the previous kernel: wait for it here -- the
+    // cluster barrier below orders every other thread's reads after this wait
+    ptx::griddep_wait();
     if (role != 1) {
       ptx::mbar_arrive_expect_tx(fullH, total_bytes);
       ptx::mbar_arrive_expect_tx(fullH + 1, total_bytes);
@@ -1793,6 +1799,7 @@ __global__ void __launch_bounds__(512, 1) recur2f_kernel(const __grid_constant__
   }
   ptx::cluster_arrive();
   ptx::cluster_wait();
+  ptx::griddep_launch();  // (PDL) every CTA resident: the next kernel (the head) may start its prologue
 
   const uint32_t idesc = ptx::idesc_f16_f32(128, Bc, 0, 0);
   const int nchunk = Bc / 16;
@@ -2412,7 +2419,7 @@ cudaError_t launch_recur2_fwd(const Recur2FwdArgs& a, cudaStream_t s) {
     return launch_cluster(recur2f_fn(pl.nci, a.hp, P.drop != 0), dim3(G, 3 * pl.nbg), dim3(256 * pl.cgN),
                           fwd_cl_smem(a.hp, pl.Bc, 8 * pl.cgN) + w2f_drop_bytes(pl.Bc) +
                               (pl.fuse ? w2f_fuse_bytes(pl.Bc) : 0),
-                          G, s, args);
+                          G, s, args, opt(OPT_FWD_PDL) == 1);
   }
 }
 

@@ -256,7 +256,7 @@ def loss_scale_state(ctx: int):
 KERNEL_OPTION_DEFAULTS = {"persistent": 1, "wavefront": 1, "wavefront_fusex": 1, "wavefront_wgrad": 1,
                           "wavefront_tmem": 1, "recur_nbg": 0, "gemm_cta_group": 0,
                           "gemm_cluster_n": 0, "pdl": 0, "k7_bn": 0, "k7_splits": 0, "recur_trace": 0,
-                          "layer_pipe": 16, "head_fused": 1, "k7_cluster": 0}
+                          "layer_pipe": 16, "head_fused": 1, "k7_cluster": 0, "fwd_pdl": 0}
 
 
 def set_option(ctx, name: str, value: float):

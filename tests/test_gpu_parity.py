@@ -288,6 +288,24 @@ def test_c4_full_width_batches_mixed(batch, seq):
     assert _max(r["master_err"]) <= 2e-2
 
 
+def test_forward_pdl_matches_oracle():
+    """Option fwd_pdl (programmatic dependent launch of the forward wavefront and the fused
+    head: their prologues start while the previous kernel drains, each waits on
+    griddepcontrol before its first activation read): same results as the plain launch
+    chain, bit for bit (the arithmetic is unchanged), and the oracle bound."""
+    import numpy as np
+    cfg = synth.CONFIGS["C2"].with_(seq=32)
+    out = {}
+    for flag in (1, 0):
+        with kernel_options(fwd_pdl=flag):
+            out[flag] = run_parity(cfg, 128, 1, steps=2, mixed=True, keep_state=True)
+    for a, b in zip(out[1], out[0]):
+        assert a["loss_gpu"] == b["loss_gpu"]
+        assert np.array_equal(a["gpu_master"], b["gpu_master"])
+        assert abs(a["loss_gpu"] - a["loss_ref"]) <= 1e-2 * max(1.0, abs(a["loss_ref"]))
+        assert _max(a["grad_err"][0]) <= GRAD_MIXED, a["grad_err"]
+
+
 @pytest.mark.parametrize("batch,seq", [(128, 128), (40, 24), (3, 5)])
 def test_head_fused_matches_unfused_and_oracle(batch, seq):
     """The fused FC head kernel (z, y, hinge, dy, dz, dH_top and the head's column sums in
