@@ -1,3 +1,4 @@
-timeout -s KILL 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29541 tools/overlap_timeline.py C4 > gpurun_out/r02an_c4.log 2>&1
-timeout -s KILL 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29542 tools/overlap_timeline.py C2 > gpurun_out/r02an_c2.log 2>&1
-timeout -s KILL 300 python tools/overlap_timeline.py C2 > gpurun_out/r02an_c2_n1.log 2>&1
+timeout -s KILL 2700 python -m pytest tests -q -m gpu -p no:cacheprovider > gpurun_out/r02fin3_tests.log 2>&1; echo exit=$? >> gpurun_out/r02fin3_tests.log
+timeout -s KILL 300 python -c "import __graft_entry__ as g; g.smoke()" > gpurun_out/r02fin3_smoke.log 2>&1; echo exit=$? >> gpurun_out/r02fin3_smoke.log
+timeout -s KILL 300 python bench.py > gpurun_out/r02fin3_c2_n1.json 2> gpurun_out/r02fin3_c2_n1.err
+timeout -s KILL 300 python -m torch.distributed.run --nnodes=1 --nproc-per-node 2 --master-addr 127.0.0.1 --master-port 29533 bench.py --gpus 2 > gpurun_out/r02fin3_c2_n2.json 2> gpurun_out/r02fin3_c2_n2.err
