@@ -613,60 +613,40 @@ __global__ void embed_chunk_kernel(const int32_t* __restrict__ keys, const int32
   }
 }
 
-// one warp per vocabulary row, lane = 4 consecutive columns (Ep <= 128; wider rows loop);
-// a Zipf-frequent token spans ~200 chunk partials: 16 independent chains per column,
-// combined in a fixed order (deterministic; the per-column arithmetic of round 2's
-// warp-per-32-column-slice version, whose 4x more warps made this pass latency-bound)
+// one warp per (vocabulary row, 32-column slice); a Zipf-frequent token spans ~200 chunk
+// partials: 16 independent chains, combined in a fixed order (deterministic).  (A warp per
+// row with 4 columns per lane measured slower: 32 -> 56 us cold-cache at C3, fewer
+// independent loads in flight.)
 __global__ void embed_segsum_kernel(const int32_t* __restrict__ first, const int32_t* __restrict__ last, int vocab,
                                     const float* __restrict__ part, int Ep, int out_f32, void* dE) {
   constexpr int CH = 16;
-  const long v = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
+  const long w = (blockIdx.x * (long)blockDim.x + threadIdx.x) >> 5;
   const int lane = threadIdx.x & 31;
-  if (v >= vocab) return;
+  const int slices = (Ep + 31) >> 5;
+  const long v = w / slices;
+  const int k = (int)(w % slices) * 32 + lane;
+  if (v >= vocab || k >= Ep) return;
   const int lo = first[v], hi = last[v];  // [0, 0) for tokens that do not occur
-  for (int k0 = 4 * lane; k0 < Ep; k0 += 128) {
-    float s[4] = {0.f, 0.f, 0.f, 0.f};
-    if (lo < hi) {
-      float a[CH][4];
+  float s = 0.f;
+  if (lo < hi) {
+    float a[CH];
 #pragma unroll
-      for (int j = 0; j < CH; ++j)
+    for (int j = 0; j < CH; ++j) a[j] = 0.f;
+    long c = ((long)lo / EMB_CHUNK + 1) * EMB_CHUNK;
+    for (; c + (CH - 1) * EMB_CHUNK < hi; c += CH * EMB_CHUNK) {
 #pragma unroll
-        for (int q = 0; q < 4; ++q) a[j][q] = 0.f;
-      long c = ((long)lo / EMB_CHUNK + 1) * EMB_CHUNK;
-      for (; c + (CH - 1) * EMB_CHUNK < hi; c += CH * EMB_CHUNK) {
-#pragma unroll
-        for (int j = 0; j < CH; ++j) {
-          const float4 p4 = *reinterpret_cast<const float4*>(part + (c + j * EMB_CHUNK) * Ep + k0);
-          a[j][0] += p4.x;
-          a[j][1] += p4.y;
-          a[j][2] += p4.z;
-          a[j][3] += p4.w;
-        }
-      }
-#pragma unroll
-      for (int j = 0; j < CH; ++j)
-        if (c + j * EMB_CHUNK < hi) {
-          const float4 p4 = *reinterpret_cast<const float4*>(part + (c + j * EMB_CHUNK) * Ep + k0);
-          a[j][0] += p4.x;
-          a[j][1] += p4.y;
-          a[j][2] += p4.z;
-          a[j][3] += p4.w;
-        }
-#pragma unroll
-      for (int m = CH / 2; m > 0; m >>= 1)
-#pragma unroll
-        for (int j = 0; j < m; ++j)
-#pragma unroll
-          for (int q = 0; q < 4; ++q) a[j][q] += a[j + m][q];
-      const float4 p0 = *reinterpret_cast<const float4*>(part + (long)lo * Ep + k0);
-      s[0] = p0.x + a[0][0];
-      s[1] = p0.y + a[0][1];
-      s[2] = p0.z + a[0][2];
-      s[3] = p0.w + a[0][3];
+      for (int j = 0; j < CH; ++j) a[j] += part[(c + j * EMB_CHUNK) * Ep + k];
     }
 #pragma unroll
-    for (int q = 0; q < 4; ++q) st_et(dE, v * Ep + k0 + q, s[q], out_f32);  // R12
+    for (int j = 0; j < CH; ++j)
+      if (c + j * EMB_CHUNK < hi) a[j] += part[(c + j * EMB_CHUNK) * Ep + k];
+#pragma unroll
+    for (int m = CH / 2; m > 0; m >>= 1)
+#pragma unroll
+      for (int j = 0; j < m; ++j) a[j] += a[j + m];
+    s = part[(long)lo * Ep + k] + a[0];
   }
+  st_et(dE, v * Ep + k, s, out_f32);  // R12
 }
 
 // element-type dispatch of the launchers: et = ET_F16 (0), ET_F32 (1) or ET_BF16 (2)
@@ -857,7 +837,7 @@ cudaError_t launch_embed_backward(const int32_t* tok, int B, int T, int vocab, c
   embed_range_kernel<<<(n + 255) / 256, 256, 0, s>>>(ka, n, range, range + vocab);
   const long cw = ((long)n + EMB_CHUNK - 1) / EMB_CHUNK * 32;
   embed_chunk_kernel<<<(int)((cw + 255) / 256), 256, 0, s>>>(ka, va, n, dX0, Ep, part);
-  const long threads = (long)vocab * 32;
+  const long threads = (long)vocab * ((Ep + 31) / 32) * 32;
   embed_segsum_kernel<<<(int)((threads + 255) / 256), 256, 0, s>>>(range, range + vocab, vocab, part, Ep, out_f32,
                                                                    dE);
   return cudaGetLastError();
