@@ -551,7 +551,7 @@ __global__ void __launch_bounds__(RS_TILE) radix_scatter_kernel(const int32_t* _
 //     [first, last) of sorted positions was recorded by embed_range_kernel.
 // No atomics; load-balanced for Zipf-frequent tokens.
 constexpr int EMB_CHUNK = 32;
-constexpr int EMB_BATCH = 16;  // dX rows in flight per warp (was 8: the chunk pass was latency-bound)
+constexpr int EMB_BATCH = 32;  // dX rows in flight per warp (the whole chunk; 8 left the chunk pass latency-bound)
 
 __global__ void embed_range_kernel(const int32_t* __restrict__ keys, int n, int32_t* __restrict__ first,
                                    int32_t* __restrict__ last) {
