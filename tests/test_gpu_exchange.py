@@ -110,6 +110,47 @@ def test_dynamic_loss_scale_both_exchanges(hdp, exchange):
 test_dynamic_loss_scale_both_exchanges.results = {}
 
 
+def test_dynamic_loss_scale_c2_fused_head(hdp):
+    """Dynamic loss scaling through the C2 path (two-layer wavefronts, the fused FC head
+    reading the device alpha for dy, its column sums and dH): the oracle's skip decisions
+    and alpha trajectory, and the master weights after the run."""
+    from oracle import optim as ooptim
+    from oracle import schedule as osched
+    from oracle import step as ostep
+    from parity import block_errors
+    cfg = synth.CONFIGS["C2"].with_(seq=12)
+    N, Bg = 2, 32
+    B = Bg // N
+    alpha0, interval, steps = 10.0 * 2.0 ** 14, 2, 6
+    params = synth.init_params(cfg)
+    desc = hdp.desc_from_config(cfg, B, hdp.MATH_MIXED16, sim_workers=N)
+    tr = hdp.Trainer(desc, params, lambda0=0.05, alpha=alpha0, gamma=cfg.gamma, n_half=1e9, momentum=cfg.momentum)
+    dev = torch.device("cuda:0")
+    master, state = params.astype(np.float64), {"H": np.zeros(tr.n)}
+    a_ref, good, skips_ref, skips_gpu = alpha0, 0, [], []
+    try:
+        hdp.set_dynamic_loss_scale(tr.ctx, interval)
+        for k in range(steps):
+            x, t = synth.model_batch(cfg, Bg, synth.DATA_SEED + k)
+            xs = [torch.from_numpy(np.ascontiguousarray(x[r * B:(r + 1) * B])).to(dev) for r in range(N)]
+            ts = [torch.from_numpy(np.ascontiguousarray(t[r * B:(r + 1) * B])).to(dev) for r in range(N)]
+            nf = tr.step(xs, ts, B, cfg.seq, epoch=0, stream=torch.cuda.current_stream(), sync=True)
+            skips_gpu.append(nf > 0)
+            lam = float(np.float32(osched.rate_for_epoch(0.05, N, 1e9, cfg.gamma, 0)))
+            ref = ostep.train_step(cfg, master, state, x, t, N, a_ref, lam, "mixed", skip_nonfinite=True)
+            a_ref, good, sk = ooptim.dynamic_loss_scale(a_ref, good, ref["nonfinite"], interval)
+            skips_ref.append(sk)
+            master, state = ref["master"], ref["state"]
+        a_gpu, nskip = hdp.loss_scale_state(tr.ctx)
+        got = hdp.gather_master(tr.ctx, tr.n)
+    finally:
+        tr.close()
+    assert skips_gpu == skips_ref, (skips_gpu, skips_ref)
+    assert any(skips_ref)
+    assert nskip == sum(skips_ref) and a_gpu == np.float32(a_ref)
+    assert max(block_errors(cfg, got.astype(np.float64), master).values()) <= 2e-2
+
+
 def test_dynamic_loss_scale_exchanges_agree(hdp):
     r = test_dynamic_loss_scale_both_exchanges.results
     if len(r) < 2:
