@@ -306,12 +306,13 @@ def test_forward_pdl_matches_oracle():
         assert _max(a["grad_err"][0]) <= GRAD_MIXED, a["grad_err"]
 
 
-@pytest.mark.parametrize("batch,seq", [(128, 128), (40, 24), (3, 5)])
+@pytest.mark.parametrize("batch,seq", [(128, 128), (256, 96), (40, 24), (3, 5)])
 def test_head_fused_matches_unfused_and_oracle(batch, seq):
     """The fused FC head kernel (z, y, hinge, dy, dz, dH_top and the head's column sums in
     one launch; csrc/head.cu) against the oracle and against the unfused path (FC GEMM,
-    head_out, column reduction, dH GEMM): C2 at its bench shape (128 CTAs), a ragged
-    tile count (960 rows = 7.5 tiles) and a sub-tile case (15 rows)."""
+    head_out, column reduction, dH GEMM): C2 at its bench shape (128 CTAs), a grid larger
+    than one wave (24576 rows = 192 CTAs on 148 SMs: the last-CTA loss reduction across
+    waves), a ragged tile count (960 rows = 7.5 tiles) and a sub-tile case (15 rows)."""
     cfg = synth.CONFIGS["C2"].with_(seq=seq)
     out = {}
     for fused in (1, 0):
