@@ -1,2 +1,2 @@
-timeout 900 python -m pytest tests/test_gpu_parity.py -q -x -k "k7_cluster" > gpurun_out/r02ba_tests.log 2>&1; echo exit=$? >> gpurun_out/r02ba_tests.log
-for o in 1 0; do timeout 300 python bench.py --config C4 --steps 5 --warmup 3 --no-cpu-baseline --option k7_cluster=$o > gpurun_out/r02ba_c4_k$o.json 2> gpurun_out/r02ba_c4_k$o.err; done
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_kernels.py -q -x -k "c4_full or k7_cluster or gemm" > gpurun_out/r02bb_tests.log 2>&1; echo exit=$? >> gpurun_out/r02bb_tests.log
+timeout 300 python bench.py > gpurun_out/r02bb_c2.json 2> gpurun_out/r02bb_c2.err
